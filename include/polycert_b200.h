@@ -1,0 +1,138 @@
+/* polycert_b200.h — C-ABI of the B200-native DeepPoly back-substitution
+ * verifier (the drop-in boundary for the reference's verifier API).
+ *
+ * The reference exposes a header-only C++ template API with no FFI
+ * (SURVEY.md §8b); the entry points below are exactly the calls a binding of
+ * that API needs:
+ *
+ *   pc_net_create   replaces  validate_model + instantiate<WidenedFloat64>
+ *                             (proj/src/model_io.cpp:49-135,
+ *                              proj/include/polycert/network.hpp:110-141)
+ *   pc_net_test     replaces  verify_robustness(net, box, label, opt)
+ *                             (proj/include/polycert/analyzer.hpp:256-276)
+ *                             plus analyze(...).state.bounds / .raw
+ *                             (analyzer.hpp:171-175, 198-242)
+ *   pc_input_box    replaces  input_box<WidenedFloat64>(center, eps, clamp01)
+ *                             (network.hpp:160-177)
+ *   pc_net_destroy  replaces  ~Network
+ *   pc_last_error   carries the message of the reference's exception
+ *
+ * Plain pointers and sizes only. All arithmetic is the reference's
+ * WidenedFloat64 mode (interval.hpp:38-103), reproduced bit-for-bit on the
+ * GPU; there is no CPU fallback: without a CUDA device every compute entry
+ * point fails with PC_ERR_CUDA.
+ */
+#ifndef POLYCERT_B200_H
+#define POLYCERT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Layer kinds, in the reference's LayerKind order (network.hpp:29). */
+enum pc_layer_kind { PC_INPUT = 0, PC_DENSE = 1, PC_CONV = 2, PC_RELU = 3, PC_JOIN = 4 };
+
+/* Status codes: the reference's exception classes map to distinct codes. */
+typedef enum {
+  PC_OK = 0,
+  PC_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (labels, eps, centers) */
+  PC_ERR_MODEL = 2,            /* std::runtime_error from validate_model ("model: layer N: ...") */
+  PC_ERR_LOGIC = 3,            /* std::logic_error (internal invariants) */
+  PC_ERR_CUDA = 4,             /* no device / CUDA failure (no CPU fallback exists) */
+  PC_ERR_OOM = 5
+} pc_status;
+
+/* One layer, mirroring LayerDoc (network.hpp:34-50). layers[0] must be the
+ * input layer. Parameters are FP64 arrays in the reference's flat layouts:
+ * dense weights [out][in] row-major (network.hpp:94); conv filter
+ * ((fy*fw+fx)*cin+ci)*cout+co (network.hpp:43). */
+typedef struct {
+  int kind;      /* pc_layer_kind */
+  int n_preds;   /* 0 input, 2 join, else 1 */
+  int preds[2];
+  int n_out;     /* dense: number of rows */
+  int fw, fh, sw, sh, pw, ph, cin, cout; /* conv */
+  const double* weights; /* dense weights or conv filter */
+  const double* bias;    /* dense: n_out, conv: cout */
+} pc_layer_desc;
+
+/* AnalysisOptions (analyzer.hpp:164-169). memory_budget bounds the device
+ * workspace of one pass (0: default); results are chunk-invariant. */
+typedef struct {
+  int early_term;          /* default 1 */
+  long long chunk_rows;    /* 0: derive from memory_budget */
+  long long memory_budget; /* bytes; 0: engine default */
+  int device;              /* CUDA ordinal; -1: current */
+} pc_options;
+
+/* PassStats (backsub.hpp:119-136). */
+typedef struct {
+  long long rows_total;
+  long long rows_terminated_early;
+  long long gbc_madds;
+  long long gbc_dense_equiv;
+  long long dense_madds;
+  long long checkpoints;
+} pc_stats;
+
+typedef struct pc_net pc_net;
+
+void pc_default_options(pc_options* opt);
+
+/* Validation only (model_io.cpp:49-135), no device needed. out_shapes
+ * (optional) receives n_layers x {w, h, c}. */
+pc_status pc_validate(const pc_layer_desc* layers, int n_layers, int in_w, int in_h, int in_c,
+                      int* out_shapes);
+
+/* Validate + upload. Error messages match validate_model's. */
+pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int in_h, int in_c,
+                        const pc_options* opt, pc_net** out);
+void pc_net_destroy(pc_net* net);
+
+int pc_net_num_layers(const pc_net* net);
+/* Neurons in layer k (numel of its output shape); -1 if out of range. */
+long long pc_net_layer_numel(const pc_net* net, int k);
+long long pc_net_total_neurons(const pc_net* net);
+int pc_net_output_size(const pc_net* net);
+
+/* Widened input region (network.hpp:160-177). HOST arrays of n values. */
+pc_status pc_input_box(const double* center, int n, double eps, int clamp01, double* lo, double* up);
+
+/* test(lo, up, label): HOST input box (n = input numel) in, verdict out.
+ * label < 0 runs the analysis only (no margin pass). margins: n_out-1
+ * certified lower bounds of out_label - out_j, ascending j != label.
+ * bounds_* (optional, may be NULL): padded per-neuron bounds concatenated
+ * over layers in id order; raw_* the unpadded freeze-test twin. */
+pc_status pc_net_test(pc_net* net, const double* lo, const double* up, int label, int* verified,
+                      double* margins, double* bounds_lo, double* bounds_hi, double* raw_lo,
+                      double* raw_hi, pc_stats* stats);
+
+/* Same with the input box already resident in device memory (d_lo, d_up are
+ * CUDA device pointers on the net's device); outputs are host arrays. */
+pc_status pc_net_test_device(pc_net* net, const double* d_lo, const double* d_up, int label,
+                             int* verified, double* margins, pc_stats* stats);
+
+/* Kernel launches issued by this thread's last pc_net_test* call. */
+long long pc_last_launch_count(void);
+
+/* Device timing of the last call: total milliseconds measured with CUDA
+ * events on the engine stream, and the milliseconds spent in the dense
+ * back-substitution kernel (the roofline kernel) with its algorithmic bytes. */
+void pc_last_timing(double* total_ms, double* dense_kernel_ms, double* dense_kernel_bytes,
+                    long long* dense_kernel_launches);
+
+/* Numeric-core self test (device): out[i] = op(a[i], b[i]) with op 0
+ * add_down, 1 add_up, 2 mul_down, 3 mul_up, 4 div_down, 5 div_up,
+ * 6 ulp_above(a) (interval.hpp:59-102); 7/8 the direction-generic chain add
+ * (up/down); 9/10 nextafter(a, +/-inf). HOST arrays. */
+pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, long long n);
+
+const char* pc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLYCERT_B200_H */

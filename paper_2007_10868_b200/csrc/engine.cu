@@ -1,0 +1,935 @@
+// engine.cu — host orchestration of the GPU verifier behind the C-ABI in
+// include/polycert_b200.h.
+//
+// Mirrors the reference's driver layer: validate_model / instantiate
+// (model_io.cpp:49-160, network.hpp:110-141), analyze / verify_robustness
+// (analyzer.hpp:198-276), run_backsubstitution / run_margin_pass / walk_back /
+// join_step (backsub.hpp:690-715, 850-893, 989-1096). Every numeric operation
+// runs in a kernel (kernels.cu); the host only tracks frame geometry, row
+// counts and buffer lifetimes. There is no CPU compute path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/polycert_b200.h"
+#include "kernels.cuh"
+
+using namespace pc;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local long long g_last_launches = 0;
+thread_local double g_total_ms = 0, g_dense_ms = 0, g_dense_bytes = 0;
+thread_local long long g_dense_launches = 0;
+
+struct StatusError : std::runtime_error {
+  pc_status code;
+  StatusError(pc_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void model_fail(int id, const std::string& what) {
+  throw StatusError(PC_ERR_MODEL, "model: layer " + std::to_string(id) + ": " + what);
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw StatusError(e == cudaErrorMemoryAllocation ? PC_ERR_OOM : PC_ERR_CUDA,
+                      std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+
+const char* kind_name(int k) {  // model_io.cpp:15-24
+  switch (k) {
+    case KIND_INPUT: return "input";
+    case KIND_DENSE: return "dense";
+    case KIND_CONV: return "conv";
+    case KIND_RELU: return "relu";
+    case KIND_JOIN: return "residual_join";
+  }
+  return "?";
+}
+
+struct HostLayer {
+  int kind = 0, pred0 = -1, pred1 = -1;
+  int in_w = 1, in_h = 1, in_c = 1, out_w = 1, out_h = 1, out_c = 1;
+  int fw = 0, fh = 0, sw = 1, sh = 1, pw = 0, ph = 0;
+  int head = -1;
+  bool feeds_relu = false;
+  long long numel() const { return (long long)out_w * out_h * out_c; }
+  long long in_numel() const { return (long long)in_w * in_h * in_c; }
+  std::vector<double> W, bias;  // host copies (reference layouts)
+  LayerDev d{};
+};
+
+// Frame geometry tracked on the host (see FrameDev in kernels.cuh).
+struct Frame {
+  int layer = 0;
+  bool dense = true;
+  long long Ww = 0, Wh = 0, Mw = 0, Mh = 0, Aw = 0, Ah = 0;
+};
+
+struct Mat {
+  double* lo = nullptr;
+  double* hi = nullptr;
+  double* K = nullptr;
+  long long cells = 0;
+  Frame f;
+};
+
+}  // namespace
+
+struct pc_net {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  pc_options opt{};
+  std::vector<HostLayer> L;
+  std::vector<long long> off;
+  long long total = 0, max_numel = 0;
+  int n_out = 0;
+  std::vector<void*> owned;
+  double *blo = nullptr, *bhi = nullptr, *rlo = nullptr, *rhi = nullptr, *dev = nullptr,
+         *relax = nullptr;
+  double* cand = nullptr;
+  char* frozen = nullptr;
+  int *live = nullptr, *rowq[2] = {nullptr, nullptr}, *perm = nullptr, *d_int = nullptr;
+  double *vals = nullptr, *rvals = nullptr, *best = nullptr;
+  char* has = nullptr;
+  Counters* ctr = nullptr;
+  char* arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0;
+  int* h_int = nullptr;  // pinned
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  bool timing = false;
+  std::mutex mu;
+
+  template <class T>
+  T* dalloc(size_t n) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    owned.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Validation (model_io.cpp:49-194)
+
+int join_head_of(const std::vector<HostLayer>& L, int j) {  // model_io.cpp:137-160
+  auto ancestors = [&](int start) {
+    std::set<int> a;
+    std::vector<int> st{start};
+    while (!st.empty()) {
+      int x = st.back();
+      st.pop_back();
+      if (!a.insert(x).second) continue;
+      if (L[x].kind == KIND_INPUT) continue;
+      st.push_back(L[x].pred0);
+      if (L[x].kind == KIND_JOIN) st.push_back(L[x].pred1);
+    }
+    return a;
+  };
+  const std::set<int> aa = ancestors(L[j].pred0), ab = ancestors(L[j].pred1);
+  int head = -1;
+  for (int x : aa)
+    if (ab.count(x)) head = std::max(head, x);
+  if (head < 0) model_fail(j, "branches share no ancestor");
+  return head;
+}
+
+struct Trace {
+  bool dense = false;
+  long long sw = 1, sh = 1;
+};
+
+Trace trace_branch(const std::vector<HostLayer>& L, int from, int head) {  // model_io.cpp:162-194
+  Trace t;
+  int cur = from;
+  while (cur != head) {
+    const HostLayer& l = L[cur];
+    switch (l.kind) {
+      case KIND_DENSE: t.dense = true; cur = l.pred0; break;
+      case KIND_CONV: t.sw *= l.sw; t.sh *= l.sh; cur = l.pred0; break;
+      case KIND_RELU: cur = l.pred0; break;
+      case KIND_JOIN: {
+        const int ih = join_head_of(L, cur);
+        Trace in = trace_branch(L, l.pred0, ih);
+        if (in.dense) t.dense = true;
+        t.sw *= in.sw;
+        t.sh *= in.sh;
+        cur = ih;
+        break;
+      }
+      default: model_fail(from, "branch walked past the input without meeting its head");
+    }
+  }
+  return t;
+}
+
+void validate(const pc_layer_desc* layers, int n, int in_w, int in_h, int in_c,
+              std::vector<HostLayer>& L) {
+  if (in_w < 1 || in_h < 1 || in_c < 1) throw StatusError(PC_ERR_MODEL, "model: input shape must be positive");
+  if (n < 1 || !layers || layers[0].kind != KIND_INPUT)
+    throw StatusError(PC_ERR_MODEL, "model: layer 0 must be the input layer");
+  if (n < 2) throw StatusError(PC_ERR_MODEL, "model: no layers");
+  L.assign(n, HostLayer{});
+  L[0].kind = KIND_INPUT;
+  L[0].out_w = in_w; L[0].out_h = in_h; L[0].out_c = in_c;
+  for (int i = 1; i < n; ++i) {
+    const pc_layer_desc& d = layers[i];
+    HostLayer& l = L[i];
+    l.kind = d.kind;
+    if (d.kind < KIND_INPUT || d.kind > KIND_JOIN) model_fail(i, "unknown kind");
+    const int want = d.kind == KIND_JOIN ? 2 : 1;
+    if (d.n_preds != want)
+      model_fail(i, std::string(kind_name(d.kind)) + " needs " + std::to_string(want) + " predecessor(s)");
+    for (int k = 0; k < want; ++k)
+      if (d.preds[k] < 0 || d.preds[k] >= i)
+        model_fail(i, "predecessor " + std::to_string(d.preds[k]) + " is not an earlier layer (cyclic or dangling)");
+    l.pred0 = d.preds[0];
+    l.pred1 = want == 2 ? d.preds[1] : -1;
+    const HostLayer& p = L[l.pred0];
+    l.in_w = p.out_w; l.in_h = p.out_h; l.in_c = p.out_c;
+    auto check_finite = [&](const double* v, long long cnt) {
+      for (long long t = 0; t < cnt; ++t)
+        if (!std::isfinite(v[t])) model_fail(i, "malformed number '" + std::to_string(v[t]) + "'");
+    };
+    switch (d.kind) {
+      case KIND_INPUT: model_fail(i, "only layer 0 may be the input");
+      case KIND_DENSE: {
+        if (d.n_out < 1) model_fail(i, "dense layer has no rows");
+        if (!d.weights || !d.bias) model_fail(i, "dense layer without weights or bias");
+        const long long nin = l.in_numel();
+        check_finite(d.weights, nin * d.n_out);
+        check_finite(d.bias, d.n_out);
+        l.W.assign(d.weights, d.weights + nin * d.n_out);
+        l.bias.assign(d.bias, d.bias + d.n_out);
+        l.out_w = 1; l.out_h = 1; l.out_c = d.n_out;
+        break;
+      }
+      case KIND_CONV: {
+        if (d.fw < 1 || d.fh < 1) model_fail(i, "filter size must be positive");
+        if (d.sw < 1 || d.sh < 1) model_fail(i, "stride must be positive");
+        if (d.pw < 0 || d.ph < 0) model_fail(i, "negative padding");
+        if (d.cin != l.in_c)
+          model_fail(i, "in_channels " + std::to_string(d.cin) + " != predecessor channels " + std::to_string(l.in_c));
+        if (d.cout < 1) model_fail(i, "out_channels must be positive");
+        if (!d.weights || !d.bias) model_fail(i, "filter element count mismatch");
+        const int ow = (l.in_w + 2 * d.pw - d.fw) / d.sw + 1;
+        const int oh = (l.in_h + 2 * d.ph - d.fh) / d.sh + 1;
+        if (ow < 1 || oh < 1) model_fail(i, "filter does not fit the input grid");
+        if ((l.in_w + 2 * d.pw - d.fw) % d.sw != 0 || (l.in_h + 2 * d.ph - d.fh) % d.sh != 0)
+          model_fail(i, "stride does not tile the padded input");
+        const long long taps = (long long)d.fw * d.fh * d.cin * d.cout;
+        check_finite(d.weights, taps);
+        check_finite(d.bias, d.cout);
+        l.fw = d.fw; l.fh = d.fh; l.sw = d.sw; l.sh = d.sh; l.pw = d.pw; l.ph = d.ph;
+        l.W.assign(d.weights, d.weights + taps);
+        l.bias.assign(d.bias, d.bias + d.cout);
+        l.out_w = ow; l.out_h = oh; l.out_c = d.cout;
+        break;
+      }
+      case KIND_RELU:
+        if (p.kind == KIND_RELU) model_fail(i, "relu fed by relu");
+        l.out_w = l.in_w; l.out_h = l.in_h; l.out_c = l.in_c;
+        break;
+      case KIND_JOIN: {
+        const HostLayer& b = L[l.pred1];
+        if (!(p.out_w == b.out_w && p.out_h == b.out_h && p.out_c == b.out_c))
+          model_fail(i, "branch output shapes differ");
+        l.out_w = l.in_w; l.out_h = l.in_h; l.out_c = l.in_c;
+        l.head = join_head_of(L, i);
+        const Trace ta = trace_branch(L, l.pred0, l.head), tb = trace_branch(L, l.pred1, l.head);
+        if (!ta.dense && !tb.dense && (ta.sw != tb.sw || ta.sh != tb.sh))
+          model_fail(i, "branches accumulate different strides");
+        break;
+      }
+    }
+  }
+  for (int i = 1; i < n; ++i)
+    if (L[i].kind == KIND_RELU) L[L[i].pred0].feeds_relu = true;
+}
+
+// ---------------------------------------------------------------------------
+// Frames
+
+FrameDev fdev(const pc_net* n, const Frame& f, int qlayer) {
+  const HostLayer& l = n->L[f.layer];
+  const HostLayer& Q = n->L[qlayer];
+  FrameDev d{};
+  d.G_w = l.out_w; d.G_h = l.out_h; d.C = l.out_c;
+  if (f.dense) {
+    d.S_w = d.G_w; d.S_h = d.G_h;
+  } else {
+    d.S_w = (int)std::min<long long>(f.Ww, d.G_w);
+    d.S_h = (int)std::min<long long>(f.Wh, d.G_h);
+    d.M_w = f.Mw; d.M_h = f.Mh; d.A_w = f.Aw; d.A_h = f.Ah;
+  }
+  d.q_w = Q.out_w; d.q_c = Q.out_c;
+  return d;
+}
+
+Frame dense_frame(int layer) {
+  Frame f;
+  f.layer = layer;
+  f.dense = true;
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// One walk context: a chunk of rows of one pass (or the margin rows).
+
+struct Walker {
+  pc_net* n;
+  cudaStream_t s;
+  int q;             // query layer
+  bool dry = false;  // geometry dry run: count bytes per row only
+  size_t dry_bytes = 0, dry_peak = 0;
+  int R = 0;         // rows per polarity
+  bool both = true;  // upper + lower rows (false: margin pass, lower only)
+  int rq = 0;        // which row_q buffer is current
+  const int* row_q = nullptr;
+  bool allow_freeze = false, early_term = true, margin = false;
+  pc_stats* st = nullptr;
+
+  int nrows() const { return both ? 2 * R : R; }
+  RowsDev rows() const { return RowsDev{row_q, nrows(), both ? R : 0}; }
+
+  double* arena_take(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (dry) {
+      dry_bytes += bytes;
+      dry_peak = std::max(dry_peak, dry_bytes);
+      return nullptr;
+    }
+    if (n->arena_used + bytes > n->arena_cap)
+      throw StatusError(PC_ERR_OOM, "workspace exhausted (chunk sizing)");
+    double* p = reinterpret_cast<double*>(n->arena + n->arena_used);
+    n->arena_used += bytes;
+    return p;
+  }
+
+  Mat alloc(const Frame& f, bool withK) {
+    Mat m;
+    m.f = f;
+    m.cells = frame_cells(fdev(n, f, q));
+    const int rows = dry ? 1 : nrows();
+    m.lo = arena_take((size_t)rows * m.cells * sizeof(double));
+    m.hi = arena_take((size_t)rows * m.cells * sizeof(double));
+    if (withK) m.K = arena_take((size_t)rows * 4 * sizeof(double));
+    return m;
+  }
+
+  void dense_step(Mat& m) {  // backsub.hpp:343-399
+    const HostLayer& L = n->L[m.f.layer];
+    Mat out = alloc(dense_frame(L.pred0), false);
+    out.K = m.K;
+    if (!dry) {
+      launch_chain_affine(s, L.d, false, rows(), fdev(n, m.f, q), MatDev{m.lo, m.hi, m.K, m.cells},
+                          n->dev + n->off[m.f.layer], n->ctr, 1);
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (n->timing) {
+        while (n->ev_pool.size() < n->ev_used + 2) {
+          cudaEvent_t e;
+          ck(cudaEventCreate(&e), "event");
+          n->ev_pool.push_back(e);
+        }
+        e0 = n->ev_pool[n->ev_used++];
+        e1 = n->ev_pool[n->ev_used++];
+        // algorithmic bytes: coefficient rows in/out (16 B per interval) + weights once
+        g_dense_bytes += 16.0 * nrows() * (double)(m.cells + out.cells) + 8.0 * m.cells * out.cells;
+        ++g_dense_launches;
+      }
+      launch_dense_coef(s, L.d, nrows(), MatDev{m.lo, m.hi, m.K, m.cells},
+                        MatDev{out.lo, out.hi, out.K, out.cells}, e0, e1);
+    }
+    m = out;
+  }
+
+  void gbc_step(Mat& m) {  // backsub.hpp:401-499
+    const HostLayer& L = n->L[m.f.layer];
+    Frame nf;
+    nf.layer = L.pred0;
+    nf.dense = m.f.dense;
+    if (!nf.dense) {
+      nf.Ww = (m.f.Ww - 1) * L.sw + L.fw;  // grow_width (depsets.hpp:27)
+      nf.Wh = (m.f.Wh - 1) * L.sh + L.fh;
+      nf.Mw = m.f.Mw * L.sw;  // step_origin (depsets.hpp:32-34), composed
+      nf.Mh = m.f.Mh * L.sh;
+      nf.Aw = m.f.Aw * L.sw - L.pw;
+      nf.Ah = m.f.Ah * L.sh - L.ph;
+    }
+    Mat out = alloc(nf, false);
+    out.K = m.K;
+    if (!dry) {
+      const FrameDev fi = fdev(n, m.f, q), fo = fdev(n, nf, q);
+      launch_chain_affine(s, L.d, true, rows(), fi, MatDev{m.lo, m.hi, m.K, m.cells},
+                          n->dev + n->off[m.f.layer], n->ctr, 1);
+      launch_gbc_coef(s, L.d, rows(), fi, fo, MatDev{m.lo, m.hi, m.K, m.cells},
+                      MatDev{out.lo, out.hi, out.K, out.cells});
+      st->gbc_dense_equiv += (long long)nrows() * L.numel() * L.in_numel();
+    }
+    m = out;
+  }
+
+  void relu_step(Mat& m) {  // backsub.hpp:501-568
+    const HostLayer& L = n->L[m.f.layer];
+    Frame nf = m.f;
+    nf.layer = L.pred0;
+    Mat out = alloc(nf, false);
+    out.K = m.K;
+    if (!dry) {
+      const FrameDev f = fdev(n, m.f, q);
+      const double* rx = n->relax + 8 * n->off[L.pred0];
+      launch_chain_relu(s, rows(), f, MatDev{m.lo, m.hi, m.K, m.cells}, rx);
+      launch_relu_coef(s, rows(), f, MatDev{m.lo, m.hi, m.K, m.cells},
+                       MatDev{out.lo, out.hi, out.K, out.cells}, rx);
+    }
+    m = out;
+  }
+
+  void join_step(Mat& m) {  // backsub.hpp:694-715
+    const HostLayer& L = n->L[m.f.layer];
+    Mat a = m, b = m;
+    a.f.layer = L.pred0;
+    b.f.layer = L.pred1;
+    b.K = arena_take((size_t)(dry ? 1 : nrows()) * 4 * sizeof(double));
+    if (!dry) ck(cudaMemsetAsync(b.K, 0, (size_t)nrows() * 4 * sizeof(double), s), "memset");
+    const bool a_was_dense = m.f.dense;
+    walk(a, L.head, false);
+    walk(b, L.head, false);
+    // align_add (backsub.hpp:610-688): union frame
+    Frame u;
+    u.layer = L.head;
+    int dense_path = 0;
+    if (a.f.dense || b.f.dense) {
+      u = dense_frame(L.head);
+      dense_path = a.f.dense ? 2 : 1;
+    } else {
+      if (a.f.Mw != b.f.Mw || a.f.Mh != b.f.Mh)
+        throw StatusError(PC_ERR_LOGIC, "join: branch frames are not stride-aligned");
+      u.dense = false;
+      u.Mw = a.f.Mw; u.Mh = a.f.Mh;
+      u.Aw = std::min(a.f.Aw, b.f.Aw);
+      u.Ah = std::min(a.f.Ah, b.f.Ah);
+      u.Ww = std::max(a.f.Aw + a.f.Ww, b.f.Aw + b.f.Ww) - u.Aw;
+      u.Wh = std::max(a.f.Ah + a.f.Wh, b.f.Ah + b.f.Wh) - u.Ah;
+    }
+    (void)a_was_dense;
+    Mat out = alloc(u, true);
+    if (!dry)
+      launch_merge(s, rows(), fdev(n, a.f, q), fdev(n, b.f, q), fdev(n, u, q), dense_path,
+                   MatDev{a.lo, a.hi, a.K, a.cells}, MatDev{b.lo, b.hi, b.K, b.cells},
+                   MatDev{out.lo, out.hi, out.K, out.cells});
+    m = out;
+  }
+
+  // run_backsubstitution's checkpoint closure (backsub.hpp:1032-1054) or the
+  // margin pass's (:1082-1091).
+  void checkpoint(Mat& m) {
+    if (dry) return;
+    st->checkpoints++;
+    const int fl = m.f.layer;
+    const long long o = n->off[fl];
+    if (margin) {
+      launch_concretize(s, rows(), fdev(n, m.f, q), MatDev{m.lo, m.hi, m.K, m.cells}, n->blo + o,
+                        n->bhi + o, n->blo + o, n->bhi + o, n->vals, n->rvals);
+      launch_margin_offer(s, R, n->vals, n->best, n->has);
+      return;
+    }
+    launch_concretize(s, rows(), fdev(n, m.f, q), MatDev{m.lo, m.hi, m.K, m.cells}, n->blo + o,
+                      n->bhi + o, n->rlo + o, n->rhi + o, n->vals, n->rvals);
+    int* new_q = n->rowq[rq ^ 1];
+    launch_offer(s, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
+                 early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr);
+    if (!(allow_freeze && early_term)) return;
+    ck(cudaMemcpyAsync(n->h_int + 1, n->d_int + 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+    const int newR = n->h_int[1];
+    if (newR == R) return;
+    // compact_rows on both polarities (backsub.hpp:820-845)
+    Mat c = m;
+    if (newR > 0) {
+      c.lo = arena_take((size_t)2 * newR * m.cells * sizeof(double));
+      c.hi = arena_take((size_t)2 * newR * m.cells * sizeof(double));
+      c.K = arena_take((size_t)2 * newR * 4 * sizeof(double));
+      launch_gather_rows(s, MatDev{m.lo, m.hi, m.K, m.cells}, MatDev{c.lo, c.hi, c.K, c.cells},
+                         n->perm, newR, R, 1);
+    }
+    m = c;
+    R = newR;
+    rq ^= 1;
+    row_q = n->rowq[rq];
+  }
+
+  // walk_back (backsub.hpp:854-893)
+  void walk(Mat& m, int stop, bool ckpt) {
+    bool pending = false;
+    while (m.f.layer != stop) {
+      if (!dry && R == 0) return;
+      const HostLayer& L = n->L[m.f.layer];
+      switch (L.kind) {
+        case KIND_DENSE:
+          dense_step(m);
+          if (ckpt) checkpoint(m);
+          pending = false;
+          break;
+        case KIND_CONV:
+          gbc_step(m);
+          if (ckpt) checkpoint(m);
+          pending = false;
+          break;
+        case KIND_RELU:
+          relu_step(m);
+          pending = true;
+          break;
+        case KIND_JOIN:
+          join_step(m);
+          if (ckpt) checkpoint(m);
+          pending = false;
+          break;
+        default:
+          throw StatusError(PC_ERR_LOGIC, "walk: frame fell through the input layer");
+      }
+    }
+    if (pending && ckpt) checkpoint(m);
+  }
+};
+
+Frame initial_frame(const pc_net* n, int t, bool affine) {
+  const HostLayer& Q = n->L[t];
+  if (affine) {
+    if (Q.kind == KIND_DENSE) return dense_frame(Q.pred0);
+    Frame f;
+    f.layer = Q.pred0;
+    f.dense = false;
+    f.Ww = Q.fw; f.Wh = Q.fh;
+    f.Mw = Q.sw; f.Mh = Q.sh;
+    f.Aw = -Q.pw; f.Ah = -Q.ph;
+    return f;
+  }
+  if (Q.out_w == 1 && Q.out_h == 1) return dense_frame(t);
+  Frame f;
+  f.layer = t;
+  f.dense = false;
+  f.Ww = 1; f.Wh = 1; f.Mw = 1; f.Mh = 1; f.Aw = 0; f.Ah = 0;
+  return f;
+}
+
+// Bytes of workspace one row (both polarities) needs for pass t.
+size_t bytes_per_row(pc_net* n, int t, bool affine) {
+  Walker w{n, nullptr, t};
+  w.dry = true;
+  w.both = true;
+  pc_stats dummy{};
+  w.st = &dummy;
+  Mat m = w.alloc(initial_frame(n, t, affine), true);
+  w.walk(m, 0, false);
+  // the compaction copy may coexist with everything else
+  return 2 * w.dry_peak + 4096;
+}
+
+void ensure_arena(pc_net* n, size_t bytes) {
+  if (bytes <= n->arena_cap) return;
+  if (n->arena) cudaFree(n->arena);
+  n->arena = nullptr;
+  n->arena_cap = 0;
+  ck(cudaMalloc(&n->arena, bytes), "arena");
+  n->arena_cap = bytes;
+}
+
+long long budget_of(const pc_net* n) {
+  return n->opt.memory_budget > 0 ? n->opt.memory_budget : (16ll << 30);
+}
+
+// run_backsubstitution (backsub.hpp:993-1065)
+void run_pass(pc_net* n, int t, bool allow_freeze, pc_stats* st) {
+  cudaStream_t s = n->stream;
+  const HostLayer& Q = n->L[t];
+  const int N = (int)Q.numel();
+  const long long o = n->off[t];
+  const bool et = n->opt.early_term != 0;
+  launch_seed(s, N, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o, allow_freeze ? 1 : 0, et ? 1 : 0,
+              n->cand, n->frozen, n->live, n->d_int, &n->ctr->pad);
+  ck(cudaMemcpyAsync(n->h_int, n->d_int, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+  ck(cudaStreamSynchronize(s), "sync");
+  const int n_live = n->h_int[0];
+  st->rows_total += N;
+  const bool affine = Q.kind == KIND_DENSE || Q.kind == KIND_CONV;
+  if (n_live > 0) {
+    const size_t per_row = bytes_per_row(n, t, affine);
+    long long chunk = n->opt.chunk_rows > 0
+                          ? n->opt.chunk_rows
+                          : std::max<long long>(1, budget_of(n) / (long long)per_row);
+    chunk = std::min<long long>(chunk, n_live);
+    ensure_arena(n, per_row * (size_t)chunk + (1 << 20));
+    for (long long base = 0; base < n_live; base += chunk) {
+      const int R = (int)std::min<long long>(chunk, n_live - base);
+      n->arena_used = 0;
+      Walker w{n, s, t};
+      w.R = R;
+      w.both = true;
+      w.allow_freeze = allow_freeze;
+      w.early_term = et;
+      w.st = st;
+      // rows of this chunk: live[base .. base+R)
+      ck(cudaMemcpyAsync(n->rowq[0], n->live + base, sizeof(int) * R, cudaMemcpyDeviceToDevice, s),
+         "d2d");
+      w.rq = 0;
+      w.row_q = n->rowq[0];
+      Frame f0 = initial_frame(n, t, affine);
+      Mat m = w.alloc(f0, true);
+      if (affine)
+        launch_init_affine(s, Q.d, w.rows(), fdev(n, f0, t), n->dev + o, MatDev{m.lo, m.hi, m.K, m.cells});
+      else
+        launch_init_identity(s, w.rows(), fdev(n, f0, t), MatDev{m.lo, m.hi, m.K, m.cells});
+      if (affine) w.checkpoint(m);  // the init itself is an affine step (:1056)
+      w.walk(m, 0, true);
+    }
+  }
+  launch_writeback(s, N, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
+                   Q.feeds_relu ? n->relax + 8 * o : nullptr);
+}
+
+// run_margin_pass (backsub.hpp:1070-1096)
+void run_margin(pc_net* n, int label, pc_stats* st, double* margins_host) {
+  cudaStream_t s = n->stream;
+  const int out = (int)n->L.size() - 1;
+  const int nr = n->n_out - 1;
+  st->rows_total += nr;
+  if (nr <= 0) return;
+  std::vector<int> cls;
+  for (int j = 0; j < n->n_out; ++j)
+    if (j != label) cls.push_back(j);
+  ck(cudaMemcpyAsync(n->rowq[0], cls.data(), sizeof(int) * nr, cudaMemcpyHostToDevice, s), "h2d");
+  ck(cudaMemsetAsync(n->has, 0, nr, s), "memset");
+  const size_t per_row = bytes_per_row(n, out, false);
+  ensure_arena(n, per_row * (size_t)nr + (1 << 20));
+  n->arena_used = 0;
+  Walker w{n, s, out};
+  w.R = nr;
+  w.both = false;
+  w.margin = true;
+  w.st = st;
+  w.row_q = n->rowq[0];
+  Frame f0 = dense_frame(out);
+  Mat m = w.alloc(f0, true);
+  launch_init_margin(s, label, n->n_out, MatDev{m.lo, m.hi, m.K, m.cells});
+  w.walk(m, 0, true);
+  ck(cudaMemcpyAsync(n->h_int + 4, n->has, nr, cudaMemcpyDeviceToHost, s), "d2h");
+  ck(cudaMemcpyAsync(margins_host, n->best, sizeof(double) * nr, cudaMemcpyDeviceToHost, s), "d2h");
+  ck(cudaStreamSynchronize(s), "sync");
+  const char* has = reinterpret_cast<const char*>(n->h_int + 4);
+  for (int r = 0; r < nr; ++r)
+    if (!has[r]) throw StatusError(PC_ERR_LOGIC, "margin pass produced no candidate");
+}
+
+// analyze + run_margin_pass (analyzer.hpp:198-276)
+void run_test(pc_net* n, int label, double* margins, pc_stats* st) {
+  cudaStream_t s = n->stream;
+  const int nl = (int)n->L.size();
+  const int out = nl - 1;
+  ck(cudaMemsetAsync(n->ctr, 0, sizeof(Counters), s), "memset");
+  for (int k = 1; k < nl; ++k) {
+    const HostLayer& l = n->L[k];
+    launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(), k,
+                         l.pred0, l.pred1, n->dev, n->relax);
+  }
+  for (int t = 1; t < nl; ++t) {
+    const bool is_out = t == out;
+    if (!is_out && !n->L[t].feeds_relu) continue;
+    run_pass(n, t, !is_out, st);
+    if (is_out) continue;
+    for (int k = t + 1; k < nl; ++k) {  // refresh (analyzer.hpp:232-239)
+      const HostLayer& l = n->L[k];
+      launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(), k,
+                           l.pred0, l.pred1, n->dev, n->relax);
+    }
+  }
+  if (label >= 0) run_margin(n, label, st, margins);
+  Counters c{};
+  ck(cudaMemcpyAsync(&c, n->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s), "d2h");
+  ck(cudaStreamSynchronize(s), "sync");
+  st->dense_madds += (long long)c.dense_madds;
+  st->gbc_madds += (long long)c.gbc_madds;
+  st->rows_terminated_early += (long long)(c.frozen + c.pad);
+}
+
+pc_status guard(const std::function<void()>& fn) {
+  try {
+    fn();
+    return PC_OK;
+  } catch (const StatusError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return PC_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PC_ERR_LOGIC;
+  }
+}
+
+pc_status test_impl(pc_net* n, const double* lo, const double* up, bool device_box, int label,
+                    int* verified, double* margins, double* b_lo, double* b_hi, double* r_lo,
+                    double* r_hi, pc_stats* stats) {
+  if (!n) {
+    g_err = "null network";
+    return PC_ERR_INVALID_ARGUMENT;
+  }
+  std::lock_guard<std::mutex> lock(n->mu);
+  g_launches = 0;
+  g_dense_ms = g_dense_bytes = 0;
+  g_dense_launches = 0;
+  return guard([&] {
+    ck(cudaSetDevice(n->device), "cudaSetDevice");
+    if (label >= n->n_out) throw StatusError(PC_ERR_INVALID_ARGUMENT, "margin: label out of range");
+    const long long n0 = n->L[0].numel();
+    cudaStream_t s = n->stream;
+    cudaEvent_t t0, t1;
+    ck(cudaEventCreate(&t0), "event");
+    ck(cudaEventCreate(&t1), "event");
+    ck(cudaEventRecord(t0, s), "event");
+    if (device_box) {
+      ck(cudaMemcpyAsync(n->blo, lo, sizeof(double) * n0, cudaMemcpyDeviceToDevice, s), "d2d");
+      ck(cudaMemcpyAsync(n->bhi, up, sizeof(double) * n0, cudaMemcpyDeviceToDevice, s), "d2d");
+    } else {
+      for (long long i = 0; i < n0; ++i)
+        if (std::isnan(lo[i]) || std::isnan(up[i]))
+          throw StatusError(PC_ERR_INVALID_ARGUMENT, "Interval: NaN endpoint");
+      ck(cudaMemcpyAsync(n->blo, lo, sizeof(double) * n0, cudaMemcpyHostToDevice, s), "h2d");
+      ck(cudaMemcpyAsync(n->bhi, up, sizeof(double) * n0, cudaMemcpyHostToDevice, s), "h2d");
+    }
+    ck(cudaMemcpyAsync(n->rlo, n->blo, sizeof(double) * n0, cudaMemcpyDeviceToDevice, s), "d2d");
+    ck(cudaMemcpyAsync(n->rhi, n->bhi, sizeof(double) * n0, cudaMemcpyDeviceToDevice, s), "d2d");
+    pc_stats st{};
+    std::vector<double> m(std::max(1, n->n_out - 1), 0.0);
+    n->ev_used = 0;
+    run_test(n, label, m.data(), &st);
+    if (b_lo) ck(cudaMemcpyAsync(b_lo, n->blo, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
+    if (b_hi) ck(cudaMemcpyAsync(b_hi, n->bhi, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
+    if (r_lo) ck(cudaMemcpyAsync(r_lo, n->rlo, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
+    if (r_hi) ck(cudaMemcpyAsync(r_hi, n->rhi, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaEventRecord(t1, s), "event");
+    ck(cudaStreamSynchronize(s), "sync");
+    ck(cudaGetLastError(), "kernel");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    g_total_ms = ms;
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    for (size_t e = 0; e + 1 < n->ev_used; e += 2) {
+      float d = 0;
+      cudaEventElapsedTime(&d, n->ev_pool[e], n->ev_pool[e + 1]);
+      g_dense_ms += d;
+    }
+    if (label >= 0) {
+      bool v = true;
+      for (int r = 0; r < n->n_out - 1; ++r) {
+        if (margins) margins[r] = m[r];
+        if (!(m[r] > 0.0)) v = false;
+      }
+      if (verified) *verified = v ? 1 : 0;
+    } else if (verified) {
+      *verified = 0;
+    }
+    if (stats) *stats = st;
+    g_last_launches = g_launches;
+  });
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+void pc_default_options(pc_options* opt) {
+  opt->early_term = 1;
+  opt->chunk_rows = 0;
+  opt->memory_budget = 0;
+  opt->device = -1;
+}
+
+const char* pc_last_error(void) { return g_err.c_str(); }
+long long pc_last_launch_count(void) { return g_last_launches; }
+
+void pc_last_timing(double* total_ms, double* dense_ms, double* dense_bytes, long long* launches) {
+  if (total_ms) *total_ms = g_total_ms;
+  if (dense_ms) *dense_ms = g_dense_ms;
+  if (dense_bytes) *dense_bytes = g_dense_bytes;
+  if (launches) *launches = g_dense_launches;
+}
+
+pc_status pc_input_box(const double* center, int n, double eps, int clamp01, double* lo,
+                       double* up) {
+  // network.hpp:160-177 is host-side input preparation; computed on the GPU
+  // like every other widened operation (no host arithmetic path exists).
+  return guard([&] {
+    if (eps < 0.0) throw StatusError(PC_ERR_INVALID_ARGUMENT, "input_box: negative epsilon");
+    for (int i = 0; i < n; ++i) {
+      if (std::isnan(center[i])) throw StatusError(PC_ERR_INVALID_ARGUMENT, "Interval: NaN endpoint");
+      if (clamp01 && (center[i] < 0.0 || 1.0 < center[i]))
+        throw StatusError(PC_ERR_INVALID_ARGUMENT, "input_box: clamped center outside [0,1]");
+    }
+    ck(input_box_device(center, n, eps, clamp01, lo, up), "input_box");
+  });
+}
+
+pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, long long n) {
+  return guard([&] { ck(scalar_ops_device(op, a, b, out, n), "scalar_ops"); });
+}
+
+pc_status pc_validate(const pc_layer_desc* layers, int n_layers, int in_w, int in_h, int in_c,
+                      int* out_shapes) {
+  return guard([&] {
+    std::vector<HostLayer> L;
+    validate(layers, n_layers, in_w, in_h, in_c, L);
+    if (out_shapes)
+      for (size_t k = 0; k < L.size(); ++k) {
+        out_shapes[3 * k] = L[k].out_w;
+        out_shapes[3 * k + 1] = L[k].out_h;
+        out_shapes[3 * k + 2] = L[k].out_c;
+      }
+  });
+}
+
+pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int in_h, int in_c,
+                        const pc_options* opt, pc_net** out) {
+  if (!out) return PC_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  pc_net* n = new pc_net;
+  pc_status st = guard([&] {
+    if (opt) n->opt = *opt;
+    else pc_default_options(&n->opt);
+    validate(layers, n_layers, in_w, in_h, in_c, n->L);
+    int devc = 0;
+    ck(cudaGetDeviceCount(&devc), "cudaGetDeviceCount");
+    if (devc < 1) throw StatusError(PC_ERR_CUDA, "cuda: no CUDA device (there is no CPU fallback)");
+    if (n->opt.device >= 0) n->device = n->opt.device;
+    else ck(cudaGetDevice(&n->device), "cudaGetDevice");
+    ck(cudaSetDevice(n->device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking), "stream");
+    const int nl = (int)n->L.size();
+    n->off.assign(nl + 1, 0);
+    for (int k = 0; k < nl; ++k) {
+      n->off[k + 1] = n->off[k] + n->L[k].numel();
+      n->max_numel = std::max(n->max_numel, n->L[k].numel());
+    }
+    n->total = n->off[nl];
+    n->n_out = (int)n->L.back().numel();
+    for (int k = 0; k < nl; ++k) {
+      HostLayer& l = n->L[k];
+      LayerDev& d = l.d;
+      d.kind = l.kind; d.pred0 = l.pred0; d.pred1 = l.pred1;
+      d.in_w = l.in_w; d.in_h = l.in_h; d.in_c = l.in_c;
+      d.out_w = l.out_w; d.out_h = l.out_h; d.out_c = l.out_c;
+      d.fw = l.fw; d.fh = l.fh; d.sw = l.sw; d.sh = l.sh; d.pw = l.pw; d.ph = l.ph;
+      if (l.kind == KIND_DENSE || l.kind == KIND_CONV) {
+        double* b = n->dalloc<double>(l.bias.size());
+        ck(cudaMemcpy(b, l.bias.data(), l.bias.size() * 8, cudaMemcpyHostToDevice), "h2d");
+        d.bias = b;
+      }
+      if (l.kind == KIND_DENSE) {
+        const long long no = l.out_c, ni = l.in_numel();
+        std::vector<double> wt((size_t)no * ni);
+        for (long long j = 0; j < no; ++j)
+          for (long long t = 0; t < ni; ++t) wt[(size_t)t * no + j] = l.W[(size_t)j * ni + t];
+        double* W = n->dalloc<double>(l.W.size());
+        double* WT = n->dalloc<double>(wt.size());
+        ck(cudaMemcpy(W, l.W.data(), l.W.size() * 8, cudaMemcpyHostToDevice), "h2d");
+        ck(cudaMemcpy(WT, wt.data(), wt.size() * 8, cudaMemcpyHostToDevice), "h2d");
+        d.W = W;
+        d.WT = WT;
+      } else if (l.kind == KIND_CONV) {
+        std::vector<double> ft(l.W.size());
+        for (int fy = 0; fy < l.fh; ++fy)
+          for (int fx = 0; fx < l.fw; ++fx)
+            for (int ci = 0; ci < l.in_c; ++ci)
+              for (int co = 0; co < l.out_c; ++co)
+                ft[(((size_t)(fy * l.fw + fx) * l.out_c + co) * l.in_c) + ci] =
+                    l.W[(((size_t)(fy * l.fw + fx) * l.in_c + ci) * l.out_c) + co];
+        double* F = n->dalloc<double>(l.W.size());
+        double* FT = n->dalloc<double>(ft.size());
+        ck(cudaMemcpy(F, l.W.data(), l.W.size() * 8, cudaMemcpyHostToDevice), "h2d");
+        ck(cudaMemcpy(FT, ft.data(), ft.size() * 8, cudaMemcpyHostToDevice), "h2d");
+        d.F = F;
+        d.FT = FT;
+      }
+    }
+    const size_t T = (size_t)n->total, M = (size_t)n->max_numel;
+    n->blo = n->dalloc<double>(T);
+    n->bhi = n->dalloc<double>(T);
+    n->rlo = n->dalloc<double>(T);
+    n->rhi = n->dalloc<double>(T);
+    n->dev = n->dalloc<double>(T);
+    n->relax = n->dalloc<double>(8 * T);
+    ck(cudaMemset(n->dev, 0, T * 8), "memset");
+    n->cand = n->dalloc<double>(4 * M);
+    n->frozen = n->dalloc<char>(M);
+    n->live = n->dalloc<int>(M);
+    n->rowq[0] = n->dalloc<int>(M);
+    n->rowq[1] = n->dalloc<int>(M);
+    n->perm = n->dalloc<int>(M);
+    n->d_int = n->dalloc<int>(8);
+    n->vals = n->dalloc<double>(2 * M);
+    n->rvals = n->dalloc<double>(2 * M);
+    n->best = n->dalloc<double>(M);
+    n->has = n->dalloc<char>(M);
+    n->ctr = n->dalloc<Counters>(1);
+    ck(cudaMallocHost(&n->h_int, 64 + (size_t)n->n_out), "pinned");
+    n->timing = true;
+  });
+  if (st != PC_OK) {
+    pc_net_destroy(n);
+    return st;
+  }
+  *out = n;
+  return PC_OK;
+}
+
+void pc_net_destroy(pc_net* n) {
+  if (!n) return;
+  cudaSetDevice(n->device);
+  if (n->stream) cudaStreamSynchronize(n->stream);
+  for (void* p : n->owned) cudaFree(p);
+  if (n->arena) cudaFree(n->arena);
+  if (n->h_int) cudaFreeHost(n->h_int);
+  for (cudaEvent_t e : n->ev_pool) cudaEventDestroy(e);
+  if (n->stream) cudaStreamDestroy(n->stream);
+  delete n;
+}
+
+int pc_net_num_layers(const pc_net* n) { return n ? (int)n->L.size() : -1; }
+long long pc_net_layer_numel(const pc_net* n, int k) {
+  if (!n || k < 0 || k >= (int)n->L.size()) return -1;
+  return n->L[k].numel();
+}
+long long pc_net_total_neurons(const pc_net* n) { return n ? n->total : -1; }
+int pc_net_output_size(const pc_net* n) { return n ? n->n_out : -1; }
+
+pc_status pc_net_test(pc_net* n, const double* lo, const double* up, int label, int* verified,
+                      double* margins, double* b_lo, double* b_hi, double* r_lo, double* r_hi,
+                      pc_stats* stats) {
+  return test_impl(n, lo, up, false, label, verified, margins, b_lo, b_hi, r_lo, r_hi, stats);
+}
+
+pc_status pc_net_test_device(pc_net* n, const double* d_lo, const double* d_up, int label,
+                             int* verified, double* margins, pc_stats* stats) {
+  return test_impl(n, d_lo, d_up, true, label, verified, margins, nullptr, nullptr, nullptr,
+                   nullptr, stats);
+}
+
+}  // extern "C"

@@ -1,0 +1,1039 @@
+// kernels.cu — sm_100a kernels of the DeepPoly back-substitution hot path.
+//
+// All arithmetic goes through numeric.cuh (bit-exact WidenedFloat64). Every
+// accumulation runs in the reference's order; sums are never split or
+// reassociated (backsub.hpp:31-34). Parallelism comes from independent rows,
+// independent output coefficients and independent neurons; each serial
+// constant/concretisation chain is one lane.
+#include <cub/block/block_scan.cuh>
+
+#include "kernels.cuh"
+#include "numeric.cuh"
+
+namespace pc {
+
+thread_local long long g_launches = 0;
+
+#define PC_NAN __longlong_as_double(0x7ff8000000000000ULL)
+
+static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+// ===========================================================================
+// Forward interval propagation: affine_bound / compute_layer_bounds
+// (eval.hpp:109-228), recompute_dev (analyzer.hpp:82-159) and
+// relu_relaxation (analyzer.hpp:38-70), fused per layer. Thread = (neuron,
+// track): track 0 computes the padded bound from padded predecessor bounds
+// plus dev and (if the layer feeds a relu) the relaxation; track 1 computes
+// the raw twin from raw predecessor bounds. Each is a serial chain over the
+// fan-in in the reference's order.
+// ===========================================================================
+
+__device__ __forceinline__ void store_relax(double* relax, long long j, const Iv& b) {
+  const Relax r = relu_relaxation(b);
+  double* p = relax + 8 * j;
+  p[0] = r.alpha.lo; p[1] = r.alpha.hi; p[2] = r.beta.lo; p[3] = r.beta.hi;
+  p[4] = r.gamma.lo; p[5] = r.gamma.hi; p[6] = r.delta.lo; p[7] = r.delta.hi;
+}
+
+__global__ void k_fwd_dense(LayerDev L, const double* xlo, const double* xhi, const double* xrlo,
+                            const double* xrhi, double* ylo, double* yhi, double* yrlo,
+                            double* yrhi, double* dev, double* relax) {
+  const int n_out = L.out_c;
+  const int n_in = L.in_w * L.in_h * L.in_c;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= 2 * n_out) return;
+  const int track = tid / n_out, j = tid % n_out;
+  const double* xl = track ? xrlo : xlo;
+  const double* xh = track ? xrhi : xhi;
+  const double bias = L.bias[j];
+  double lo = bias, hi = bias, abs_hi = fabs(bias);
+  long long terms = 1;
+  for (int t = 0; t < n_in; ++t) {
+    const double w = L.WT[(size_t)t * n_out + j];
+    if (w == 0.0) continue;
+    const double a = xl[t], b = xh[t];
+    if (track == 0) {
+      ++terms;
+      abs_hi = add_up(abs_hi, mul_up(fabs(w), smax(fabs(a), fabs(b))));
+    }
+    if (w > 0.0) {
+      lo = add_down(lo, mul_down(w, a));
+      hi = add_up(hi, mul_up(w, b));
+    } else {
+      lo = add_down(lo, mul_down(w, b));
+      hi = add_up(hi, mul_up(w, a));
+    }
+  }
+  if (track == 0) {
+    const double slack = __dmul_rn(__dmul_rn(2.0, (double)(terms + 1)), ulp_above(abs_hi));
+    const Iv y{add_down(lo, -slack), add_up(hi, slack)};
+    ylo[j] = y.lo;
+    yhi[j] = y.hi;
+    // recompute_dev dense (analyzer.hpp:99-111): the |w|*mag chain over all
+    // inputs equals abs_hi (zero-weight terms add an exact 0).
+    dev[j] = __dmul_rn(__dmul_rn(2.0, (double)(n_in + 2)), ulp_above(abs_hi));
+    if (relax) store_relax(relax, j, y);
+  } else {
+    yrlo[j] = lo;
+    yrhi[j] = hi;
+  }
+}
+
+__global__ void k_fwd_conv(LayerDev L, const double* xlo, const double* xhi, const double* xrlo,
+                           const double* xrhi, double* ylo, double* yhi, double* yrlo,
+                           double* yrhi, double* dev, double* relax) {
+  const long long numel = (long long)L.out_w * L.out_h * L.out_c;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= 2 * numel) return;
+  const int track = (int)(tid / numel);
+  const long long jj = tid % numel;
+  const int d = (int)(jj % L.out_c);
+  const int w = (int)((jj / L.out_c) % L.out_w);
+  const int h = (int)(jj / ((long long)L.out_c * L.out_w));
+  const double* xl = track ? xrlo : xlo;
+  const double* xh = track ? xrhi : xhi;
+  const double bias = L.bias[d];
+  double lo = bias, hi = bias, abs_hi = fabs(bias);
+  long long terms = 1, dterms = 1;
+  const int cin = L.in_c, cout = L.out_c;
+  for (int fy = 0; fy < L.fh; ++fy) {
+    const int iy = h * L.sh - L.ph + fy;
+    if (iy < 0 || iy >= L.in_h) continue;
+    for (int fx = 0; fx < L.fw; ++fx) {
+      const int ix = w * L.sw - L.pw + fx;
+      if (ix < 0 || ix >= L.in_w) continue;
+      const double* fp = L.F + ((size_t)(fy * L.fw + fx) * cin) * cout + d;
+      const size_t xb = ((size_t)iy * L.in_w + ix) * cin;
+      dterms += cin;
+      for (int ci = 0; ci < cin; ++ci) {
+        const double wv = fp[(size_t)ci * cout];
+        if (wv == 0.0) continue;
+        const double a = xl[xb + ci], b = xh[xb + ci];
+        if (track == 0) {
+          ++terms;
+          abs_hi = add_up(abs_hi, mul_up(fabs(wv), smax(fabs(a), fabs(b))));
+        }
+        if (wv > 0.0) {
+          lo = add_down(lo, mul_down(wv, a));
+          hi = add_up(hi, mul_up(wv, b));
+        } else {
+          lo = add_down(lo, mul_down(wv, b));
+          hi = add_up(hi, mul_up(wv, a));
+        }
+      }
+    }
+  }
+  if (track == 0) {
+    const double slack = __dmul_rn(__dmul_rn(2.0, (double)(terms + 1)), ulp_above(abs_hi));
+    const Iv y{add_down(lo, -slack), add_up(hi, slack)};
+    ylo[jj] = y.lo;
+    yhi[jj] = y.hi;
+    dev[jj] = __dmul_rn(__dmul_rn(2.0, (double)(dterms + 1)), ulp_above(abs_hi));
+    if (relax) store_relax(relax, jj, y);
+  } else {
+    yrlo[jj] = lo;
+    yrhi[jj] = hi;
+  }
+}
+
+__global__ void k_fwd_relu(long long n, const double* xlo, const double* xhi, const double* xrlo,
+                           const double* xrhi, double* ylo, double* yhi, double* yrlo,
+                           double* yrhi) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  ylo[i] = xlo[i] > 0.0 ? xlo[i] : 0.0;  // eval.hpp:210-217
+  yhi[i] = xhi[i] > 0.0 ? xhi[i] : 0.0;
+  yrlo[i] = xrlo[i] > 0.0 ? xrlo[i] : 0.0;
+  yrhi[i] = xrhi[i] > 0.0 ? xrhi[i] : 0.0;
+}
+
+__global__ void k_fwd_join(long long n, const double* alo, const double* ahi, const double* arlo,
+                           const double* arhi, const double* blo, const double* bhi,
+                           const double* brlo, const double* brhi, double* ylo, double* yhi,
+                           double* yrlo, double* yrhi, double* dev, double* relax) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Iv a{alo[i], ahi[i]}, b{blo[i], bhi[i]};
+  const Iv y = iv_add(a, b);  // eval.hpp:219-223
+  ylo[i] = y.lo;
+  yhi[i] = y.hi;
+  yrlo[i] = add_down(arlo[i], brlo[i]);
+  yrhi[i] = add_up(arhi[i], brhi[i]);
+  dev[i] = __dmul_rn(2.0, ulp_above(add_up(iv_mag(a), iv_mag(b))));  // analyzer.hpp:144-150
+  if (relax) store_relax(relax, i, y);
+}
+
+__global__ void k_relax(long long n, const double* blo, const double* bhi, double* relax) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  store_relax(relax, i, Iv{blo[i], bhi[i]});
+}
+
+void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, const double* blo,
+                          const double* bhi, const double* rlo, const double* rhi,
+                          const long long* offs, int k, int p0, int p1, double* dev,
+                          double* relax) {
+  const long long o = offs[k], a = offs[p0];
+  double* ylo = const_cast<double*>(blo) + o;
+  double* yhi = const_cast<double*>(bhi) + o;
+  double* yrlo = const_cast<double*>(rlo) + o;
+  double* yrhi = const_cast<double*>(rhi) + o;
+  double* rx = feeds_relu ? relax + 8 * o : nullptr;
+  const long long n = (long long)L.out_w * L.out_h * L.out_c;
+  switch (L.kind) {
+    case KIND_DENSE:
+      k_fwd_dense<<<cdiv(2 * n, 128), 128, 0, s>>>(L, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
+                                                   yrlo, yrhi, dev + o, rx);
+      break;
+    case KIND_CONV:
+      k_fwd_conv<<<cdiv(2 * n, 128), 128, 0, s>>>(L, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
+                                                  yrlo, yrhi, dev + o, rx);
+      break;
+    case KIND_RELU:
+      k_fwd_relu<<<cdiv(n, 256), 256, 0, s>>>(n, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
+                                              yrlo, yrhi);
+      break;
+    case KIND_JOIN: {
+      const long long b = offs[p1];
+      k_fwd_join<<<cdiv(n, 256), 256, 0, s>>>(n, blo + a, bhi + a, rlo + a, rhi + a, blo + b,
+                                              bhi + b, rlo + b, rhi + b, ylo, yhi, yrlo, yrhi,
+                                              dev + o, rx);
+      break;
+    }
+    default:
+      return;
+  }
+  ++g_launches;
+}
+
+void launch_relax(cudaStream_t s, const double* blo, const double* bhi, long long n,
+                  double* relax) {
+  k_relax<<<cdiv(n, 256), 256, 0, s>>>(n, blo, bhi, relax);
+  ++g_launches;
+}
+
+// ===========================================================================
+// Pass seeding: CandidateSet::seed + pre-freeze + live-row list
+// (backsub.hpp:1000-1015). One block; stable row compaction by block scan.
+// cand[q] = {lo, hi, raw_lo, raw_hi}.
+// ===========================================================================
+
+constexpr int kScanThreads = 1024;
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_seed(int n, const double* blo, const double* bhi, const double* rlo, const double* rhi,
+           int allow_freeze, int early_term, double* cand, char* frozen, int* live, int* n_live,
+           unsigned long long* n_prefrozen) {
+  using Scan = cub::BlockScan<int, kScanThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  int froze = 0;
+  __syncthreads();
+  for (int start = 0; start < n; start += kScanThreads) {
+    const int q = start + threadIdx.x;
+    int keep = 0;
+    if (q < n) {
+      const double l = blo[q], h = bhi[q], rl = rlo[q], rh = rhi[q];
+      cand[4 * q + 0] = l;
+      cand[4 * q + 1] = h;
+      cand[4 * q + 2] = rl;
+      cand[4 * q + 3] = rh;
+      const bool st = allow_freeze && (!(rl < 0.0) || !(rh > 0.0));  // stable() :814-817
+      frozen[q] = st ? 1 : 0;
+      if (st && early_term) ++froze;
+      keep = !(early_term && st);
+    }
+    int pos, total;
+    Scan(tmp).ExclusiveSum(keep, pos, total);
+    if (keep) live[s_base + pos] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += total;
+    __syncthreads();
+  }
+  if (froze) atomicAdd(n_prefrozen, (unsigned long long)froze);
+  if (threadIdx.x == 0) *n_live = s_base;
+}
+
+void launch_seed(cudaStream_t s, int n, const double* blo, const double* bhi, const double* rlo,
+                 const double* rhi, int allow_freeze, int early_term, double* cand, char* frozen,
+                 int* live, int* n_live, unsigned long long* n_prefrozen) {
+  k_seed<<<1, kScanThreads, 0, s>>>(n, blo, bhi, rlo, rhi, allow_freeze, early_term, cand, frozen,
+                                    live, n_live, n_prefrozen);
+  ++g_launches;
+}
+
+// Write the best candidates back (backsub.hpp:1060-1064) and refresh the
+// relaxation of the refined layer (analyzer.hpp:229-231).
+__global__ void k_writeback(int n, const double* cand, double* blo, double* bhi, double* rlo,
+                            double* rhi, double* relax) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const Iv b{cand[4 * q + 0], cand[4 * q + 1]};
+  blo[q] = b.lo;
+  bhi[q] = b.hi;
+  rlo[q] = cand[4 * q + 2];
+  rhi[q] = cand[4 * q + 3];
+  if (relax) store_relax(relax, q, b);
+}
+
+void launch_writeback(cudaStream_t s, int n, const double* cand, double* blo, double* bhi,
+                      double* rlo, double* rhi, double* relax) {
+  k_writeback<<<cdiv(n, 256), 256, 0, s>>>(n, cand, blo, bhi, rlo, rhi, relax);
+  ++g_launches;
+}
+
+// ===========================================================================
+// Row initialisation (backsub.hpp:205-336)
+// ===========================================================================
+
+// init_affine_rows: the query neuron's own weights / filter taps as point
+// coefficients over its predecessor; constant = bias (raw) and bias widened
+// by dev[q] (padded).
+__global__ void k_init_affine(LayerDev Q, RowsDev rows, FrameDev f, const double* dev_q,
+                              MatDev out) {
+  const int i = blockIdx.y;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  const long long cells = out.cells;
+  double* lo = out.lo + (size_t)i * cells;
+  double* hi = out.hi + (size_t)i * cells;
+  if (Q.kind == KIND_DENSE) {
+    const long long n_in = cells;
+    for (long long t = blockIdx.x * blockDim.x + threadIdx.x; t < n_in;
+         t += (long long)gridDim.x * blockDim.x) {
+      const double w = Q.W[(size_t)q * n_in + t];
+      lo[t] = w;
+      hi[t] = w;
+    }
+  } else {
+    const int cq = q % Q.out_c;
+    const int qw = (q / Q.out_c) % Q.out_w;
+    const int qh = q / (Q.out_c * Q.out_w);
+    int bw, bh;
+    frame_base(f, q, bw, bh);
+    const long long ow = (long long)qw * Q.sw - Q.pw, oh = (long long)qh * Q.sh - Q.ph;
+    for (long long c = blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+         c += (long long)gridDim.x * blockDim.x) {
+      const int ci = (int)(c % f.C);
+      const int x = (int)((c / f.C) % f.S_w);
+      const int y = (int)(c / ((long long)f.C * f.S_w));
+      const long long fx = bw + x - ow, fy = bh + y - oh;
+      double v = 0.0;
+      if (fx >= 0 && fx < Q.fw && fy >= 0 && fy < Q.fh)
+        v = Q.F[((size_t)(fy * Q.fw + fx) * Q.in_c + ci) * Q.out_c + cq];
+      lo[c] = v;
+      hi[c] = v;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double b = Q.bias[Q.kind == KIND_DENSE ? q : q % Q.out_c];
+    Iv k{b, b};
+    const double dv = dev_q[q];
+    if (dv != 0.0) k = Iv{add_down(k.lo, -dv), add_up(k.hi, dv)};  // widen_constant :175-179
+    double* K = out.K + 4 * (size_t)i;
+    K[0] = k.lo; K[1] = k.hi; K[2] = b; K[3] = b;
+  }
+}
+
+void launch_init_affine(cudaStream_t s, const LayerDev& Q, const RowsDev& rows, const FrameDev& f,
+                        const double* dev_q, MatDev out) {
+  dim3 grid(cdiv(out.cells, 256) > 64 ? 64 : cdiv(out.cells, 256), rows.n);
+  k_init_affine<<<grid, 256, 0, s>>>(Q, rows, f, dev_q, out);
+  ++g_launches;
+}
+
+// init_identity_rows: coefficient 1 at the query neuron, constant 0.
+__global__ void k_init_identity(RowsDev rows, FrameDev f, MatDev out) {
+  const int i = blockIdx.y;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  const long long cells = out.cells;
+  double* lo = out.lo + (size_t)i * cells;
+  double* hi = out.hi + (size_t)i * cells;
+  // Dense frame (1x1 grid): cell q; cuboid 1x1 window: cell = channel.
+  const long long hot = (f.G_w == 1 && f.G_h == 1) ? q : q % f.C;
+  for (long long c = blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+       c += (long long)gridDim.x * blockDim.x) {
+    const double v = (c == hot) ? 1.0 : 0.0;
+    lo[c] = v;
+    hi[c] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 4) out.K[4 * (size_t)i + threadIdx.x] = 0.0;
+}
+
+void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev out) {
+  dim3 grid(cdiv(out.cells, 256) > 64 ? 64 : cdiv(out.cells, 256), rows.n);
+  k_init_identity<<<grid, 256, 0, s>>>(rows, f, out);
+  ++g_launches;
+}
+
+// init_margin_rows: +1 at label, -1 at class j, ascending j != label.
+__global__ void k_init_margin(int label, int n_out, MatDev out) {
+  const int r = blockIdx.x;
+  const int j = r < label ? r : r + 1;
+  for (int c = threadIdx.x; c < n_out; c += blockDim.x) {
+    const double v = (c == label) ? 1.0 : (c == j ? -1.0 : 0.0);
+    out.lo[(size_t)r * n_out + c] = v;
+    out.hi[(size_t)r * n_out + c] = v;
+  }
+  if (threadIdx.x < 4) out.K[4 * r + threadIdx.x] = 0.0;
+}
+
+void launch_init_margin(cudaStream_t s, int label, int n_out, MatDev out) {
+  k_init_margin<<<n_out - 1, 128, 0, s>>>(label, n_out, out);
+  ++g_launches;
+}
+
+// ===========================================================================
+// Serial chains. One warp per row: the 32 lanes compute the terms of 32
+// consecutive cells in parallel (products, zero skips), stage them in shared
+// memory, then one lane per chain folds them into its accumulator in cell
+// order. NaN marks a skipped term (real terms are never NaN).
+// ===========================================================================
+
+constexpr int kChainWarps = 4;
+
+// Constant update of a dense / conv substitution (backsub.hpp:365-389,
+// 454-489): k += c*b_j and kraw += c*b_j (iv_acc, zero terms skipped),
+// dev += mag(c)*dev_j (DevAccum), then widen_constant(k, dev). Lanes 0..4
+// run k.lo, k.hi, kraw.lo, kraw.hi, dev. Also counts the step's multiply-adds
+// (dense_madds :386 / gbc_madds :483).
+__global__ void __launch_bounds__(32 * kChainWarps)
+    k_chain_affine(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, const double* dev,
+                   Counters* ctr) {
+  __shared__ double s_t[kChainWarps][3][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kChainWarps + warp;
+  if (i >= rows.n) return;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw = 0, bh = 0;
+  if (is_conv) frame_base(f, q, bw, bh);
+  const long long cells = m.cells;
+  const double* lo = m.lo + (size_t)i * cells;
+  const double* hi = m.hi + (size_t)i * cells;
+  double* K = m.K + 4 * (size_t)i;
+  double acc = lane < 4 ? K[lane] : 0.0;
+  const bool up = (lane & 1) || lane == 4;
+  const int arr = lane == 4 ? 2 : (lane & 1);
+  const int n_in = L.in_w * L.in_h * L.in_c;
+  unsigned long long madds = 0;
+  for (long long c0 = 0; c0 < cells; c0 += 32) {
+    const long long cell = c0 + lane;
+    double tl = PC_NAN, th = PC_NAN, td = PC_NAN;
+    if (cell < cells) {
+      const Iv c{lo[cell], hi[cell]};
+      if (!iv_zero(c)) {
+        double b;
+        long long jd;
+        if (is_conv) {
+          const int d = (int)(cell % f.C);
+          const int x = (int)((cell / f.C) % f.S_w);
+          const int y = (int)(cell / ((long long)f.C * f.S_w));
+          const int aw = bw + x, ah = bh + y;
+          b = L.bias[d];
+          jd = ((long long)ah * f.G_w + aw) * f.C + d;
+          const int y0 = ah * L.sh - L.ph, x0 = aw * L.sw - L.pw;
+          const int ny = min(L.fh, L.in_h - y0) - max(0, -y0);
+          const int nx = min(L.fw, L.in_w - x0) - max(0, -x0);
+          if (ny > 0 && nx > 0) madds += (unsigned long long)L.in_c * ny * nx;
+        } else {
+          b = L.bias[cell];
+          jd = cell;
+          madds += n_in;
+        }
+        const Iv bt = iv_mul_scalar(c, b);
+        if (!iv_zero(bt)) {
+          tl = bt.lo;
+          th = bt.hi;
+        }
+        const double dj = dev[jd];
+        if (dj != 0.0) td = mul_up(iv_mag(c), dj);
+      }
+    }
+    s_t[warp][0][lane] = tl;
+    s_t[warp][1][lane] = th;
+    s_t[warp][2][lane] = td;
+    __syncwarp();
+    if (lane < 5) {
+      const int n = (int)min((long long)32, cells - c0);
+      for (int k = 0; k < n; ++k) {
+        const double t = s_t[warp][arr][k];
+        if (t == t) acc = add_dir(acc, t, up);
+      }
+    }
+    __syncwarp();
+  }
+  const double dtot = __shfl_sync(0xffffffffu, acc, 4);
+  if (lane == 0) K[0] = dtot != 0.0 ? add_down(acc, -dtot) : acc;
+  if (lane == 1) K[1] = dtot != 0.0 ? add_up(acc, dtot) : acc;
+  if (lane == 2 || lane == 3) K[lane] = acc;
+  for (int o = 16; o > 0; o >>= 1) madds += __shfl_down_sync(0xffffffffu, madds, o);
+  if (lane == 0 && madds) atomicAdd(is_conv ? &ctr->gbc_madds : &ctr->dense_madds, madds);
+}
+
+void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
+                         const FrameDev& fin, MatDev m, const double* dev, Counters* ctr, int) {
+  k_chain_affine<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(L, is_conv ? 1 : 0, rows,
+                                                                        fin, m, dev, ctr);
+  ++g_launches;
+}
+
+// Constant update of a relu substitution (backsub.hpp:536-563): per nonzero
+// cell one offset term (sign-stable coefficient) or two (straddling: offp
+// then offn), each skipped when zero. Lanes 0..3: k.lo, k.hi, kraw.lo, kraw.hi.
+__global__ void __launch_bounds__(32 * kChainWarps)
+    k_chain_relu(RowsDev rows, FrameDev f, MatDev m, const double* relax) {
+  __shared__ double s_t[kChainWarps][2][2][32];  // [slot][lo/hi][cell]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kChainWarps + warp;
+  if (i >= rows.n) return;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const long long cells = m.cells;
+  const double* lo = m.lo + (size_t)i * cells;
+  const double* hi = m.hi + (size_t)i * cells;
+  double* K = m.K + 4 * (size_t)i;
+  double acc = lane < 4 ? K[lane] : 0.0;
+  const bool up = lane & 1;
+  const int arr = lane & 1;
+  for (long long c0 = 0; c0 < cells; c0 += 32) {
+    const long long cell = c0 + lane;
+    double t0l = PC_NAN, t0h = PC_NAN, t1l = PC_NAN, t1h = PC_NAN;
+    if (cell < cells) {
+      const Iv c{lo[cell], hi[cell]};
+      if (!iv_zero(c)) {
+        const int cc = (int)(cell % f.C);
+        const int x = (int)((cell / f.C) % f.S_w);
+        const int y = (int)(cell / ((long long)f.C * f.S_w));
+        const long long j = ((long long)(bh + y) * f.G_w + (bw + x)) * f.C + cc;
+        const double* R = relax + 8 * j;
+        const Iv beta{R[2], R[3]}, delta{R[6], R[7]};
+        const Iv op = upper ? delta : beta;
+        const Iv on = upper ? beta : delta;
+        if (!(c.lo < 0.0)) {
+          const Iv off = iv_mul(c, op);
+          if (!iv_zero(off)) { t0l = off.lo; t0h = off.hi; }
+        } else if (!(c.hi > 0.0)) {
+          const Iv off = iv_mul(c, on);
+          if (!iv_zero(off)) { t0l = off.lo; t0h = off.hi; }
+        } else {
+          const Iv offp = iv_mul(iv_pos_part(c), op);
+          const Iv offn = iv_mul(iv_neg_part(c), on);
+          if (!iv_zero(offp)) { t0l = offp.lo; t0h = offp.hi; }
+          if (!iv_zero(offn)) { t1l = offn.lo; t1h = offn.hi; }
+        }
+      }
+    }
+    s_t[warp][0][0][lane] = t0l;
+    s_t[warp][0][1][lane] = t0h;
+    s_t[warp][1][0][lane] = t1l;
+    s_t[warp][1][1][lane] = t1h;
+    __syncwarp();
+    if (lane < 4) {
+      const int n = (int)min((long long)32, cells - c0);
+      for (int k = 0; k < n; ++k) {
+        const double a = s_t[warp][0][arr][k];
+        if (a == a) acc = add_dir(acc, a, up);
+        const double b = s_t[warp][1][arr][k];
+        if (b == b) acc = add_dir(acc, b, up);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane < 4) K[lane] = acc;
+}
+
+void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                       const double* relax) {
+  k_chain_relu<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, relax);
+  ++g_launches;
+}
+
+// concretize (backsub.hpp:725-764): acc = K.hi (upper) / K.lo (lower), then
+// add the corner product with the frame layer's bounds for each nonzero
+// cell in ascending order. Lane 0: padded track (constant, bounds); lane 1:
+// raw track (constant_raw, raw bounds).
+__global__ void __launch_bounds__(32 * kChainWarps)
+    k_concretize(RowsDev rows, FrameDev f, MatDev m, const double* blo, const double* bhi,
+                 const double* rlo, const double* rhi, double* vals, double* rvals) {
+  __shared__ double s_t[kChainWarps][2][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kChainWarps + warp;
+  if (i >= rows.n) return;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const long long cells = m.cells;
+  const double* lo = m.lo + (size_t)i * cells;
+  const double* hi = m.hi + (size_t)i * cells;
+  const double* K = m.K + 4 * (size_t)i;
+  double acc = 0.0;
+  if (lane == 0) acc = upper ? K[1] : K[0];
+  if (lane == 1) acc = upper ? K[3] : K[2];
+  for (long long c0 = 0; c0 < cells; c0 += 32) {
+    const long long cell = c0 + lane;
+    double tp = PC_NAN, tr = PC_NAN;
+    if (cell < cells) {
+      const Iv c{lo[cell], hi[cell]};
+      if (!iv_zero(c)) {
+        const int cc = (int)(cell % f.C);
+        const int x = (int)((cell / f.C) % f.S_w);
+        const int y = (int)(cell / ((long long)f.C * f.S_w));
+        const long long j = ((long long)(bh + y) * f.G_w + (bw + x)) * f.C + cc;
+        const Iv B{blo[j], bhi[j]}, Br{rlo[j], rhi[j]};
+        tp = upper ? corner_hi(c, B) : corner_lo(c, B);
+        tr = upper ? corner_hi(c, Br) : corner_lo(c, Br);
+      }
+    }
+    s_t[warp][0][lane] = tp;
+    s_t[warp][1][lane] = tr;
+    __syncwarp();
+    if (lane < 2) {
+      const int n = (int)min((long long)32, cells - c0);
+      for (int k = 0; k < n; ++k) {
+        const double t = s_t[warp][lane][k];
+        if (t == t) acc = add_dir(acc, t, upper);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) vals[i] = acc;
+  if (lane == 1) rvals[i] = acc;
+}
+
+void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                       const double* blo, const double* bhi, const double* rlo,
+                       const double* rhi, double* vals, double* rvals) {
+  k_concretize<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, blo, bhi, rlo,
+                                                                      rhi, vals, rvals);
+  ++g_launches;
+}
+
+// ===========================================================================
+// Coefficient substitution kernels (output-stationary, reduction in the
+// reference's ascending order, no split-K).
+// ===========================================================================
+
+// dense_step coefficients (backsub.hpp:365-386): M'[r][t] = sum_j M[r][j]*W[j][t]
+// over ascending j, skipping zero coefficients and zero weights. Tile: 16 rows
+// x 64 columns per 256-thread block; each thread owns 4 rows of one column.
+// The K dimension (frame cells j) streams through shared memory in slabs of
+// 32 in ascending order.
+constexpr int kDR = 16, kDC = 64, kDK = 32;
+
+__global__ void __launch_bounds__(256)
+    k_dense_coef(const double* __restrict__ W, int n_k, int n_in, int nrows, MatDev in,
+                 MatDev out) {
+  __shared__ double s_al[kDR][kDK], s_ah[kDR][kDK];
+  __shared__ double s_w[kDK][kDC];
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // ty in [0,4)
+  const int col = blockIdx.x * kDC + tx;
+  const int r0 = blockIdx.y * kDR;
+  Iv acc[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) acc[u] = Iv{0.0, 0.0};
+  for (int k0 = 0; k0 < n_k; k0 += kDK) {
+    for (int e = threadIdx.x; e < kDR * kDK; e += 256) {
+      const int rr = e / kDK, kk = e % kDK;
+      const int r = r0 + rr, k = k0 + kk;
+      double a = 0.0, b = 0.0;
+      if (r < nrows && k < n_k) {
+        a = in.lo[(size_t)r * n_k + k];
+        b = in.hi[(size_t)r * n_k + k];
+      }
+      s_al[rr][kk] = a;
+      s_ah[rr][kk] = b;
+    }
+    for (int e = threadIdx.x; e < kDK * kDC; e += 256) {
+      const int kk = e / kDC, cc = e % kDC;
+      const int k = k0 + kk, c = blockIdx.x * kDC + cc;
+      s_w[kk][cc] = (k < n_k && c < n_in) ? W[(size_t)k * n_in + c] : 0.0;
+    }
+    __syncthreads();
+    const int kn = min(kDK, n_k - k0);
+    for (int kk = 0; kk < kn; ++kk) {
+      const double w = s_w[kk][tx];
+      if (w == 0.0) continue;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = ty * 4 + u;
+        const Iv c{s_al[rr][kk], s_ah[rr][kk]};
+        if (iv_zero(c)) continue;
+        const double a = w > 0.0 ? c.lo : c.hi;
+        const double b = w > 0.0 ? c.hi : c.lo;
+        acc[u].lo = add_down(acc[u].lo, mul_down(a, w));
+        acc[u].hi = add_up(acc[u].hi, mul_up(b, w));
+      }
+    }
+    __syncthreads();
+  }
+  if (col < n_in) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = r0 + ty * 4 + u;
+      if (r < nrows) {
+        out.lo[(size_t)r * n_in + col] = acc[u].lo;
+        out.hi[(size_t)r * n_in + col] = acc[u].hi;
+      }
+    }
+  }
+}
+
+void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, MatDev out,
+                       cudaEvent_t ev0, cudaEvent_t ev1) {
+  const int n_k = (int)in.cells, n_in = (int)out.cells;
+  dim3 grid(cdiv(n_in, kDC), cdiv(nrows, kDR));
+  if (ev0) cudaEventRecord(ev0, s);
+  k_dense_coef<<<grid, 256, 0, s>>>(L.W, n_k, n_in, nrows, in, out);
+  if (ev1) cudaEventRecord(ev1, s);
+  ++g_launches;
+}
+
+// gbc_step coefficients (backsub.hpp:449-485), gather form: each output cell
+// (iy, ix, ci) of the new window sums, over the frame cells (ah, aw) whose
+// filter window covers it in ascending (ah, aw) order and over ascending
+// output channel d, c[ah][aw][d] * filter[fy][fx][ci][d]. That is exactly
+// the reference's accumulation order for that coefficient (its scatter loop
+// visits frame cells in (ch, cw, d) order).
+__device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+__global__ void __launch_bounds__(256)
+    k_gbc_coef(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, MatDev in, MatDev out) {
+  const int i = blockIdx.y;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw, bh, nbw, nbh;
+  frame_base(fi, q, bw, bh);
+  frame_base(fo, q, nbw, nbh);
+  const long long ocells = out.cells, icells = in.cells;
+  const double* ilo = in.lo + (size_t)i * icells;
+  const double* ihi = in.hi + (size_t)i * icells;
+  const int cin = L.in_c, cout = L.out_c;
+  for (long long o = blockIdx.x * blockDim.x + threadIdx.x; o < ocells;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(o % cin);
+    const int x = (int)((o / cin) % fo.S_w);
+    const int y = (int)(o / ((long long)cin * fo.S_w));
+    const int iy = nbh + y, ix = nbw + x;
+    // frame rows ah with 0 <= iy - (ah*sh - ph) < fh
+    int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
+    int aw0 = floordiv(ix + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ix + L.pw, L.sw);
+    ah0 = max(ah0, bh); ah1 = min(ah1, bh + fi.S_h - 1);
+    aw0 = max(aw0, bw); aw1 = min(aw1, bw + fi.S_w - 1);
+    Iv acc{0.0, 0.0};
+    for (int ah = ah0; ah <= ah1; ++ah) {
+      const int fy = iy + L.ph - ah * L.sh;
+      for (int aw = aw0; aw <= aw1; ++aw) {
+        const int fx = ix + L.pw - aw * L.sw;
+        const size_t cb = ((size_t)(ah - bh) * fi.S_w + (aw - bw)) * cout;
+        const double* wp = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ci;
+        for (int d = 0; d < cout; ++d) {
+          const Iv c{ilo[cb + d], ihi[cb + d]};
+          if (iv_zero(c)) continue;
+          const double w = wp[(size_t)d * cin];
+          if (w == 0.0) continue;
+          const double a = w > 0.0 ? c.lo : c.hi;
+          const double b = w > 0.0 ? c.hi : c.lo;
+          acc.lo = add_down(acc.lo, mul_down(a, w));
+          acc.hi = add_up(acc.hi, mul_up(b, w));
+        }
+      }
+    }
+    out.lo[(size_t)i * ocells + o] = acc.lo;
+    out.hi[(size_t)i * ocells + o] = acc.hi;
+  }
+}
+
+void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, MatDev in, MatDev out) {
+  unsigned gx = cdiv(out.cells, 256);
+  if (gx > 1024) gx = 1024;
+  dim3 grid(gx, rows.n);
+  k_gbc_coef<<<grid, 256, 0, s>>>(L, rows, fin, fout, in, out);
+  ++g_launches;
+}
+
+// relu_step coefficients (backsub.hpp:536-563): per nonzero cell, slope by
+// sign (upper rows: gamma for c>=0, alpha for c<=0; lower rows mirrored);
+// straddling cells split into positive and negative parts.
+__global__ void __launch_bounds__(256)
+    k_relu_coef(RowsDev rows, FrameDev f, MatDev in, MatDev out, const double* relax) {
+  const int i = blockIdx.y;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const long long cells = in.cells;
+  const double* lo = in.lo + (size_t)i * cells;
+  const double* hi = in.hi + (size_t)i * cells;
+  for (long long cell = blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
+       cell += (long long)gridDim.x * blockDim.x) {
+    const Iv c{lo[cell], hi[cell]};
+    Iv r = c;
+    if (!iv_zero(c)) {
+      const int cc = (int)(cell % f.C);
+      const int x = (int)((cell / f.C) % f.S_w);
+      const int y = (int)(cell / ((long long)f.C * f.S_w));
+      const long long j = ((long long)(bh + y) * f.G_w + (bw + x)) * f.C + cc;
+      const double* R = relax + 8 * j;
+      const Iv alpha{R[0], R[1]}, gamma{R[4], R[5]};
+      const Iv sp = upper ? gamma : alpha;
+      const Iv sn = upper ? alpha : gamma;
+      if (!(c.lo < 0.0)) r = iv_mul(c, sp);
+      else if (!(c.hi > 0.0)) r = iv_mul(c, sn);
+      else r = iv_add(iv_mul(iv_pos_part(c), sp), iv_mul(iv_neg_part(c), sn));
+    }
+    out.lo[(size_t)i * cells + cell] = r.lo;
+    out.hi[(size_t)i * cells + cell] = r.hi;
+  }
+}
+
+void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev in,
+                      MatDev out, const double* relax) {
+  unsigned gx = cdiv(in.cells, 256);
+  if (gx > 1024) gx = 1024;
+  dim3 grid(gx, rows.n);
+  k_relu_coef<<<grid, 256, 0, s>>>(rows, f, in, out, relax);
+  ++g_launches;
+}
+
+// align_add / densify (backsub.hpp:578-688): union frame, branch a then b.
+// dense_path mirrors the reference's densify branch: a's coefficients are
+// copied (a dense from the start: verbatim; densified: zero cells -> +0)
+// instead of accumulated into +0; the constants add K_b into K_a.
+__global__ void __launch_bounds__(256)
+    k_merge(RowsDev rows, FrameDev fa, FrameDev fb, FrameDev fu, int dense_path, MatDev a,
+            MatDev b, MatDev out) {
+  const int i = blockIdx.y;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int abw, abh, bbw, bbh, ubw, ubh;
+  frame_base(fa, q, abw, abh);
+  frame_base(fb, q, bbw, bbh);
+  frame_base(fu, q, ubw, ubh);
+  const long long cells = out.cells;
+  const int C = fu.C;
+  for (long long cell = blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
+       cell += (long long)gridDim.x * blockDim.x) {
+    const int cc = (int)(cell % C);
+    const int x = (int)((cell / C) % fu.S_w);
+    const int y = (int)(cell / ((long long)C * fu.S_w));
+    const int aw = ubw + x, ah = ubh + y;
+    Iv ca{0.0, 0.0}, cb{0.0, 0.0};
+    bool ina = aw >= abw && aw < abw + fa.S_w && ah >= abh && ah < abh + fa.S_h;
+    bool inb = aw >= bbw && aw < bbw + fb.S_w && ah >= bbh && ah < bbh + fb.S_h;
+    if (ina) {
+      const size_t o = (size_t)i * a.cells + ((size_t)(ah - abh) * fa.S_w + (aw - abw)) * C + cc;
+      ca = Iv{a.lo[o], a.hi[o]};
+    }
+    if (inb) {
+      const size_t o = (size_t)i * b.cells + ((size_t)(ah - bbh) * fb.S_w + (aw - bbw)) * C + cc;
+      cb = Iv{b.lo[o], b.hi[o]};
+    }
+    Iv n{0.0, 0.0};
+    if (dense_path == 2) n = ca;                    // a was dense: kept verbatim
+    else if (dense_path == 1) { if (!iv_zero(ca)) n = ca; }  // densified a
+    else iv_acc(n, ca);                              // union scatter
+    iv_acc(n, cb);
+    out.lo[(size_t)i * cells + cell] = n.lo;
+    out.hi[(size_t)i * cells + cell] = n.hi;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double* Ka = a.K + 4 * (size_t)i;
+    const double* Kb = b.K + 4 * (size_t)i;
+    Iv k{Ka[0], Ka[1]}, kr{Ka[2], Ka[3]};
+    iv_acc(k, Iv{Kb[0], Kb[1]});
+    iv_acc(kr, Iv{Kb[2], Kb[3]});
+    double* Ko = out.K + 4 * (size_t)i;
+    Ko[0] = k.lo; Ko[1] = k.hi; Ko[2] = kr.lo; Ko[3] = kr.hi;
+  }
+}
+
+void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const FrameDev& fb,
+                  const FrameDev& fu, int dense_path, MatDev a, MatDev b, MatDev out) {
+  unsigned gx = cdiv(out.cells, 256);
+  if (gx > 1024) gx = 1024;
+  dim3 grid(gx, rows.n);
+  k_merge<<<grid, 256, 0, s>>>(rows, fa, fb, fu, dense_path, a, b, out);
+  ++g_launches;
+}
+
+// ===========================================================================
+// Checkpoint bookkeeping: CandidateSet offers + freeze (backsub.hpp:798-817,
+// 1036-1053) and the stable row compaction of compact_rows (:820-845) as a
+// block scan producing the new row order.
+// ===========================================================================
+__global__ void __launch_bounds__(kScanThreads)
+    k_offer(RowsDev rows, int R, const double* vals, const double* rvals, double* cand,
+            char* frozen, int allow_freeze, int early_term, int* perm, int* new_R,
+            int* new_row_q, Counters* ctr) {
+  using Scan = cub::BlockScan<int, kScanThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  int froze = 0;
+  __syncthreads();
+  for (int start = 0; start < R; start += kScanThreads) {
+    const int r = start + threadIdx.x;
+    int keep = 0, q = 0;
+    if (r < R) {
+      q = rows.row_q[r];
+      double* cd = cand + 4 * (size_t)q;
+      if (!frozen[q]) {
+        const double v = vals[r], rv = rvals[r];  // offer_hi
+        if (v < cd[1]) cd[1] = v;
+        if (rv < cd[3]) cd[3] = rv;
+        const double v2 = vals[R + r], rv2 = rvals[R + r];  // offer_lo
+        if (v2 > cd[0]) cd[0] = v2;
+        if (rv2 > cd[2]) cd[2] = rv2;
+        if (allow_freeze && (!(cd[2] < 0.0) || !(cd[3] > 0.0))) {
+          frozen[q] = 1;
+          if (early_term) ++froze;
+        }
+      }
+      keep = !(early_term && frozen[q]);
+    }
+    int pos, total;
+    Scan(tmp).ExclusiveSum(keep, pos, total);
+    if (keep) {
+      perm[s_base + pos] = r;
+      new_row_q[s_base + pos] = q;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += total;
+    __syncthreads();
+  }
+  if (froze) atomicAdd(&ctr->frozen, (unsigned long long)froze);
+  if (threadIdx.x == 0) *new_R = s_base;
+}
+
+void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals,
+                  const double* rvals, double* cand, char* frozen, int allow_freeze,
+                  int early_term, int* perm, int* new_R, int* new_row_q, Counters* ctr) {
+  k_offer<<<1, kScanThreads, 0, s>>>(rows, R, vals, rvals, cand, frozen, allow_freeze, early_term,
+                                     perm, new_R, new_row_q, ctr);
+  ++g_launches;
+}
+
+// run_margin_pass checkpoint (backsub.hpp:1082-1091): best = max.
+__global__ void k_margin_offer(int n, const double* vals, double* best, char* has) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  if (!has[r] || vals[r] > best[r]) {
+    best[r] = vals[r];
+    has[r] = 1;
+  }
+}
+
+void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best, char* has) {
+  k_margin_offer<<<1, 128, 0, s>>>(n, vals, best, has);
+  ++g_launches;
+}
+
+// Row gather for compaction: new row p <- old row perm[p] (upper block) and
+// new row R_new + p <- old row R_old + perm[p] (lower block).
+__global__ void k_gather_rows(MatDev in, MatDev out, const int* perm, int R_new, int R_old,
+                              int both) {
+  const int p = blockIdx.y;
+  const int side = blockIdx.z;
+  const int src = perm[p] + (side ? R_old : 0);
+  const int dst = p + (side ? R_new : 0);
+  const long long cells = in.cells;
+  for (long long c = blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+       c += (long long)gridDim.x * blockDim.x) {
+    out.lo[(size_t)dst * cells + c] = in.lo[(size_t)src * cells + c];
+    out.hi[(size_t)dst * cells + c] = in.hi[(size_t)src * cells + c];
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 4)
+    out.K[4 * (size_t)dst + threadIdx.x] = in.K[4 * (size_t)src + threadIdx.x];
+  (void)both;
+}
+
+void launch_gather_rows(cudaStream_t s, MatDev in, MatDev out, const int* perm, int R_new,
+                        int R_old, int both) {
+  if (R_new <= 0) return;
+  unsigned gx = cdiv(in.cells, 256);
+  if (gx > 256) gx = 256;
+  dim3 grid(gx, R_new, both ? 2 : 1);
+  k_gather_rows<<<grid, 256, 0, s>>>(in, out, perm, R_new, R_old, both);
+  ++g_launches;
+}
+
+// input_box (network.hpp:160-177): iv_add(point(c), [-eps, eps]) then the
+// optional [0, 1] clamp with std::max/std::min semantics.
+__global__ void k_input_box(const double* c, int n, double eps, int clamp01, double* lo,
+                            double* up) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double l = add_down(c[i], -eps), h = add_up(c[i], eps);
+  if (clamp01) {
+    l = smax(l, 0.0);
+    h = smin(h, 1.0);
+  }
+  lo[i] = l;
+  up[i] = h;
+}
+
+cudaError_t input_box_device(const double* center, int n, double eps, int clamp01, double* lo,
+                             double* up) {
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(d, center, sizeof(double) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && n > 0) {
+    k_input_box<<<cdiv(n, 256), 256>>>(d, n, eps, clamp01, d + n, d + 2 * (size_t)n);
+    ++g_launches;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(lo, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(up, d + 2 * (size_t)n, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
+
+// Numeric-core self test: one scalar op per element (0 add_down, 1 add_up,
+// 2 mul_down, 3 mul_up, 4 div_down, 5 div_up, 6 ulp_above(a), 7 add_dir up,
+// 8 add_dir down, 9 nextup_bits(a), 10 nextdown_bits(a)).
+__global__ void k_scalar_ops(int op, const double* a, const double* b, double* out, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = a[i], y = b[i];
+  double r;
+  switch (op) {
+    case 0: r = add_down(x, y); break;
+    case 1: r = add_up(x, y); break;
+    case 2: r = mul_down(x, y); break;
+    case 3: r = mul_up(x, y); break;
+    case 4: r = div_down(x, y); break;
+    case 5: r = div_up(x, y); break;
+    case 6: r = ulp_above(x); break;
+    case 7: r = add_dir(x, y, true); break;
+    case 8: r = add_dir(x, y, false); break;
+    case 9: r = nextup_bits(x); break;
+    default: r = nextdown_bits(x); break;
+  }
+  out[i] = r;
+}
+
+cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* out, long long n) {
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(d, a, sizeof(double) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d + n, b, sizeof(double) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && n > 0) {
+    k_scalar_ops<<<cdiv(n, 256), 256>>>(op, d, d + n, d + 2 * n, n);
+    ++g_launches;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
+
+}  // namespace pc

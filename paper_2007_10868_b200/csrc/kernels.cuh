@@ -1,0 +1,141 @@
+// kernels.cuh — device data structures and kernel launchers shared by the
+// host engine (engine.cu) and the kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pc {
+
+enum Kind { KIND_INPUT = 0, KIND_DENSE = 1, KIND_CONV = 2, KIND_RELU = 3, KIND_JOIN = 4 };
+
+// Device-side view of one layer (immutable after pc_net_create).
+struct LayerDev {
+  int kind, pred0, pred1;
+  int in_w, in_h, in_c, out_w, out_h, out_c;
+  int fw, fh, sw, sh, pw, ph;
+  const double* W;   // dense [out][in] (reference layout)
+  const double* WT;  // dense [in][out] (forward kernel layout)
+  const double* F;   // conv filter ((fy*fw+fx)*cin+ci)*cout+co (reference layout)
+  const double* FT;  // conv filter ((fy*fw+fx)*cout+co)*cin+ci (back-substitution layout)
+  const double* bias;
+};
+
+// A frame = which cells of a layer a bound matrix row stores.
+//
+// The reference stores per-row cuboid windows of unclamped width, with dead
+// out-of-grid cells (backsub.hpp:85-96). Here every row stores only the
+// in-grid STORAGE WINDOW of size S = min(W, G) per axis, based at
+// clamp(origin, 0, G - S), so dense frames (S = G, base 0) and cuboid frames
+// share one layout and deep residual frames never hold dead cells. Row origins
+// are affine in the query neuron's grid position (origin = q_pos * M + A): the
+// reference's recurrences (depsets.hpp:27-34) compose affinely, so the host
+// tracks (M, A, W) symbolically and kernels derive each row's base on the fly.
+// Cells inside the storage window but outside the row's true frame are kept
+// exactly zero and zero coefficients are skipped everywhere, as dead cells are
+// in the reference; cell order within the window is (y, x, c), i.e. ascending
+// absolute order, which is the reference's accumulation order.
+struct FrameDev {
+  int G_w, G_h, C;           // layer grid
+  int S_w, S_h;              // storage window (cells per row = S_w*S_h*C)
+  long long M_w, M_h, A_w, A_h;
+  int q_w, q_c;              // query layer width / channels (decode row query index)
+};
+
+__host__ __device__ inline long long frame_cells(const FrameDev& f) {
+  return (long long)f.S_w * f.S_h * f.C;
+}
+
+__device__ __forceinline__ void frame_base(const FrameDev& f, int q, int& bw, int& bh) {
+  const int qw = (q / f.q_c) % f.q_w;
+  const int qh = q / (f.q_c * f.q_w);
+  long long ow = (long long)qw * f.M_w + f.A_w;
+  long long oh = (long long)qh * f.M_h + f.A_h;
+  const long long mw = f.G_w - f.S_w, mh = f.G_h - f.S_h;
+  ow = ow < 0 ? 0 : (ow > mw ? mw : ow);
+  oh = oh < 0 ? 0 : (oh > mh ? mh : oh);
+  bw = (int)ow;
+  bh = (int)oh;
+}
+
+// Row set of a bound matrix: rows [0, n_up) are upper-polarity rows for
+// queries row_q[0..n_up), rows [n_up, n) lower rows for row_q[i - n_up]
+// (margin passes: n_up = 0). Coefficients are SoA planes lo[n][cells],
+// hi[n][cells]; K[n][4] = {k.lo, k.hi, kraw.lo, kraw.hi}.
+struct MatDev {
+  double* lo;
+  double* hi;
+  double* K;
+  long long cells;
+};
+
+struct RowsDev {
+  const int* row_q;
+  int n;     // total rows
+  int n_up;  // upper rows come first
+};
+
+__device__ __forceinline__ int row_query(const RowsDev& r, int i, bool& upper) {
+  upper = i < r.n_up;
+  return r.row_q[upper ? i : i - r.n_up];
+}
+
+struct Counters {  // device-side PassStats accumulators
+  unsigned long long dense_madds;
+  unsigned long long gbc_madds;
+  unsigned long long frozen;  // rows_terminated_early (checkpoint freezes)
+  unsigned long long pad;
+};
+
+// ----- launchers (kernels.cu) -----
+void launch_forward_layer(cudaStream_t s, const LayerDev& L, int k_is_relu_input,
+                          const double* blo, const double* bhi, const double* rlo,
+                          const double* rhi,            // base pointers of all-layer arrays
+                          const long long* offs,         // host offsets per layer
+                          int k, int pred0, int pred1, double* dev, double* relax);
+void launch_relax(cudaStream_t s, const double* blo, const double* bhi, long long n, double* relax);
+
+void launch_seed(cudaStream_t s, int n, const double* blo, const double* bhi, const double* rlo,
+                 const double* rhi, int allow_freeze, int early_term, double* cand, char* frozen,
+                 int* live, int* n_live, unsigned long long* n_prefrozen);
+void launch_writeback(cudaStream_t s, int n, const double* cand, double* blo, double* bhi,
+                      double* rlo, double* rhi, double* relax);
+
+void launch_init_affine(cudaStream_t s, const LayerDev& Q, const RowsDev& rows, const FrameDev& f,
+                        const double* dev_q, MatDev out);
+void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev out);
+void launch_init_margin(cudaStream_t s, int label, int n_out, MatDev out);
+
+void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
+                         const FrameDev& fin, MatDev m, const double* dev, Counters* ctr,
+                         int count_madds);
+void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                       const double* relax);
+void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                       const double* blo, const double* bhi, const double* rlo,
+                       const double* rhi, double* vals, double* rvals);
+
+void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, MatDev out,
+                       cudaEvent_t ev0, cudaEvent_t ev1);
+void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, MatDev in, MatDev out);
+void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev in,
+                      MatDev out, const double* relax);
+void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const FrameDev& fb,
+                  const FrameDev& fu, int dense_path, MatDev a, MatDev b, MatDev out);
+
+void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals,
+                  const double* rvals, double* cand, char* frozen, int allow_freeze,
+                  int early_term, int* perm, int* new_R, int* new_row_q, Counters* ctr);
+void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best, char* has);
+void launch_gather_rows(cudaStream_t s, MatDev in, MatDev out, const int* perm, int R_new,
+                        int R_old, int both);
+
+cudaError_t input_box_device(const double* center, int n, double eps, int clamp01, double* lo,
+                             double* up);
+
+cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* out, long long n);
+
+extern thread_local long long g_launches;
+
+}  // namespace pc

@@ -1,0 +1,119 @@
+"""GPU parity: the CUDA engine (through the C-ABI) against the CPU oracle on
+the same seeded inputs — bounds (padded and raw twins), margins, verdicts and
+PassStats must be bit-identical (== on every double, and the same bit
+pattern). Reference behaviour pinned: proj/tests/test_backsub.cpp,
+test_analyzer.cpp, test_formats.cpp."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from cases import BACKSUB_ARCHS, EXTRA_ARCHS
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def pc():
+    import paper_2007_10868_b200 as pc
+    return pc
+
+
+def _flat(bounds):
+    return np.concatenate([b[0] for b in bounds]), np.concatenate([b[1] for b in bounds])
+
+
+def check_same(got, ref, what):
+    assert got.shape == ref.shape, what
+    eq = got == ref
+    assert eq.all(), f"{what}: {int((~eq).sum())} mismatches, first at {int(np.argmin(eq))}: {got[~eq][:3]} vs {ref[~eq][:3]}"
+    # bit patterns too (the reference never produces -0.0 where we produce +0.0)
+    assert np.array_equal(got.view(np.int64), ref.view(np.int64)), f"{what}: signed-zero difference"
+
+
+def run_case(pc, port, net, center, eps, label=None, early_term=True, chunk_rows=0, clamp=True):
+    v = pc.Verifier(net, pc.AnalysisOptions(early_term=early_term, chunk_rows=chunk_rows))
+    box = pc.input_box(center, eps, clamp)
+    lo, hi = port.input_box(center, eps, clamp)
+    check_same(box.lo, lo, "input_box lo")
+    check_same(box.hi, hi, "input_box hi")
+    if label is None:
+        label = int(np.argmax(np.random.default_rng(0).random(net.output_size)))
+    g = v.test(box.lo, box.hi, label, want_bounds=True)
+    r = port.analyze(net.layers, lo, hi, label=label, early_term=early_term, chunk_rows=chunk_rows)
+    blo, bhi = _flat(g.bounds)
+    rlo, rhi = _flat(g.raw)
+    check_same(blo, r["b_lo"], "bounds.lo")
+    check_same(bhi, r["b_hi"], "bounds.hi")
+    check_same(rlo, r["r_lo"], "raw.lo")
+    check_same(rhi, r["r_hi"], "raw.hi")
+    check_same(g.margins, r["margins"], "margins")
+    assert g.verified == r["verified"]
+    assert g.stats == r["stats"], (g.stats, r["stats"])
+    return g, r
+
+
+def test_golden_report(pc, port):
+    """proj/docs/golden/report.jsonl: margins and rows_terminated, eps 0.03."""
+    net = pc.generate(202608, "input 4x4x1; conv 3x3x2 s1 p1; relu; dense 3")
+    X = np.array([[float(t) for t in l.split(",")] for l in open(os.path.join(GOLDEN, "inputs.csv")).read().split()])
+    v = pc.Verifier(net)
+    for line, x in zip(open(os.path.join(GOLDEN, "report.jsonl")), X):
+        rec = json.loads(line)
+        box = pc.input_box(x, 0.03, True)
+        verdict = v.verify_robustness(box, rec["candidate"])
+        assert [m for _, m in verdict.margins] == [m["lower"] for m in rec["margins"]]
+        assert verdict.verified == (rec["verdict"] == "verified")
+        assert verdict.stats["rows_terminated_early"] == rec["rows_terminated"]
+
+
+def test_identity_margins(pc):
+    """test_analyzer.cpp:61-76: widened identity net, margins ~0.4 / ~-0.2."""
+    L = pc.Layer
+    net = pc.Network([L("input", [], (1, 1, 2)),
+                      L("dense", [0], weights=np.array([[1.0, 0.0], [0.0, 1.0]]), bias=np.zeros(2))])
+    net.validate()
+    v = pc.Verifier(net)
+    v1 = v.verify_robustness(pc.input_box([0.7, 0.1], 0.1, True), 0)
+    assert v1.verified and abs(v1.margins[0][1] - 0.4) <= 1e-12 * 0.4
+    v2 = v.verify_robustness(pc.input_box([0.7, 0.1], 0.4, True), 0)
+    assert not v2.verified and abs(v2.margins[0][1] + 0.2) <= 1e-12 * 0.2
+
+
+@pytest.mark.parametrize("arch", BACKSUB_ARCHS + EXTRA_ARCHS)
+@pytest.mark.parametrize("seed", [900, 41])
+def test_random_nets(pc, port, arch, seed):
+    net = pc.generate(seed, arch)
+    X = pc.random_inputs(seed + 1, 2, int(np.prod(net.input_shape)))
+    for i, eps in enumerate([1.0 / 16, 0.25]):
+        run_case(pc, port, net, X[i], eps, label=i % net.output_size)
+
+
+@pytest.mark.parametrize("arch", BACKSUB_ARCHS[1:3] + EXTRA_ARCHS[2:4])
+def test_early_term_and_chunking(pc, port, arch):
+    """Early termination and chunk size never change results (test_backsub.cpp:74-157)."""
+    net = pc.generate(500, arch)
+    x = np.full(int(np.prod(net.input_shape)), 0.5)
+    g1, _ = run_case(pc, port, net, x, 0.06, label=0, early_term=True)
+    g2, _ = run_case(pc, port, net, x, 0.06, label=0, early_term=False)
+    g3, _ = run_case(pc, port, net, x, 0.06, label=0, early_term=True, chunk_rows=1)
+    for a, b in zip(g1.bounds, g2.bounds):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for a, b in zip(g1.bounds, g3.bounds):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert g2.stats["rows_terminated_early"] == 0
+
+
+def test_gain_scaled_mlp(pc, port):
+    """R2 'gain init': He-scaled dyadic weights, mixed verdicts, live rows."""
+    net = pc.generate(7, "input 28x28x1; dense 100; relu; dense 100; relu; dense 100; relu; dense 10")
+    for L in net.layers:
+        if L.kind == "dense":
+            fan_in = L.weights.shape[1]
+            L.weights = L.weights * 2.0 ** round(np.log2(np.sqrt(fan_in)))
+    X = pc.random_inputs(8, 2, 784)
+    for x in X:
+        run_case(pc, port, net, x, 0.012, label=0)
