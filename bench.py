@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark: ms/image to verify one image (BASELINE.json metric), GPU engine
+vs the reference's own CPU verifier.
+
+A "step" verifies one image: analyze + margin pass (verify_robustness,
+analyzer.hpp:256-276) on a generator-built network (random-init dyadic
+weights of the named architecture, gen.cpp) and generator inputs. Default
+workload: configs[1] = MNIST 9x500, eps 0.026, early termination on.
+
+  value  device-resident inputs (pc_net_test_device), per-step CUDA events on
+         the engine stream, L2 flushed between steps (outside the events)
+  e2e    the C-ABI call with HOST buffers (pc_net_test): box H2D + margins D2H
+         inside the timed region
+  cpu_baseline / --impl reference: the unmodified reference (oracle/_ref,
+         compiled from /root/reference) on the host's cores; falls back to the
+         plain-C restatement (oracle/, "port") if the reference lib is absent.
+
+Multi-GPU (torchrun): replicas — rank r verifies images r, r+N, ...; no
+collective on the data path; time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms/image to verify (1/2/4/8 B200) + certified count == CPU ref; HBM GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mnist_9x500")
+    ap.add_argument("--no-early-term", action="store_true")
+    ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(name):
+    from paper_2007_10868_b200.configs import CONFIGS, INPUT_SEED, MODEL_SEED
+    arch, eps = CONFIGS[name]
+    return arch, eps, MODEL_SEED, INPUT_SEED
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([t.strip() for t in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        busy = [float(s[6]) for s in self.samples if len(s) > 6 and s[6].replace(".", "").isdigit()]
+        loaded = [v for v, b in zip(sm, busy) if b > 0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+_REF_CACHE = {}
+
+
+def cpu_reference(arch, eps_s, mseed, iseed, n_images, threads, early_term):
+    """The reference's CPU verifier on `threads` host cores (oracle/_ref), else
+    the plain-C restatement. Returns (ms_per_image, kind, verdicts, seconds)."""
+    from oracle.pyoracle import Ref
+    if Ref.available():
+        key = (arch, mseed)
+        if key not in _REF_CACHE:
+            ref = Ref()
+            h = ref.generate(mseed, arch)
+            _REF_CACHE[key] = (ref, h, int(np.prod(ref.layers(h)[0].out_shape)))
+        ref, h, dim = _REF_CACHE[key]
+        X = ref.random_inputs(iseed, n_images, dim)
+        eps = ref.double_from_decimal(eps_s)
+        verdicts, wall, per = ref.verify_batch(h, X, eps, True, threads, early_term)
+        return 1000.0 * wall / n_images, "reference", verdicts, wall, per
+    # plain-C restatement, one image at a time per thread
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.pyoracle import Port
+    import paper_2007_10868_b200 as pc
+    port = Port()
+    net = pc.generate(mseed, arch)
+    X = pc.random_inputs(iseed, n_images, int(np.prod(net.input_shape)))
+    eps = float(eps_s)
+    v = pc.Verifier(net)
+    labels = [v.candidate(x) for x in X]
+
+    def one(i):
+        lo, hi = port.input_box(X[i], eps)
+        t0 = time.perf_counter()
+        r = port.analyze(net.layers, lo, hi, label=max(labels[i], 0), early_term=early_term)
+        return (1 if r["verified"] else 0), time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        res = list(ex.map(one, range(n_images)))
+    wall = time.perf_counter() - t0
+    return 1000.0 * wall / n_images, "port", np.array([r[0] for r in res]), wall, [r[1] for r in res]
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    arch, eps_s, mseed, iseed = workload(args.config)
+    threads = os.cpu_count() or 1
+    et = not args.no_early_term
+    # one image per host thread per step (the CLI's worker-pool mode)
+    per_step = threads
+    steps, warm = args.steps, args.warmup
+    t_all = 0.0
+    n_timed = 0
+    verified = 0
+    for s in range(warm + steps):
+        ms, kind, verdicts, wall, _ = cpu_reference(arch, eps_s, mseed, iseed + 1000 * s, per_step,
+                                                    threads, et)
+        if s >= warm:
+            t_all += wall
+            n_timed += per_step
+            verified += int((np.asarray(verdicts) == 1).sum())
+    val = 1000.0 * t_all / max(n_timed, 1)
+    line = {"metric": METRIC, "value": val, "unit": "ms/image", "n_gpus": 0, "steps": steps,
+            "warmup": warm, "ms_per_step": 1000.0 * t_all / max(steps, 1), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": args.config, "arch": arch, "eps": eps_s, "model_seed": mseed,
+                       "early_term": et, "images_per_step": per_step},
+            "cpu_baseline": {"value": val, "unit": "ms/image", "cores": threads, "kind": kind,
+                             "sample": f"{n_timed} images ({per_step} per step, one image per host "
+                                       f"thread, reference CLI worker-pool mode), {verified} verified"},
+            "e2e": {"value": val, "unit": "ms/image", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2007_10868_b200 as pc
+
+    arch, eps_s, mseed, iseed = workload(args.config)
+    eps = float(eps_s)  # correctly rounded, == strtod (decimal.cpp:63-76)
+    et = not args.no_early_term
+    net = pc.generate(mseed, arch)
+    v = pc.Verifier(net, pc.AnalysisOptions(early_term=et, device=local))
+    n_in = int(np.prod(net.input_shape))
+    steps, warm = args.steps, args.warmup
+    total_imgs = (steps + warm) * world
+    X = pc.random_inputs(iseed, total_imgs, n_in)
+    mine = [i for i in range(total_imgs) if i % world == rank]
+    boxes = [pc.input_box(X[i], eps, True) for i in mine]
+    labels = [v.candidate(X[i]) for i in mine]
+    labels = [l if l >= 0 else 0 for l in labels]
+    dev = torch.device("cuda", local)
+    d_lo = [torch.from_numpy(b.lo).to(dev) for b in boxes]
+    d_hi = [torch.from_numpy(b.hi).to(dev) for b in boxes]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.ExternalStream(v.stream_handle, device=dev)
+    torch.cuda.synchronize()
+
+    def timed_loop(fn):
+        evs = []
+        launches = 0
+        dense_ms = dense_bytes = 0.0
+        dense_n = 0
+        for s in range(warm + steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(s & 0xFF)  # evict L2 between steps (outside the events)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            fn(s)
+            e1.record(stream)
+            if s >= warm:
+                evs.append((e0, e1))
+                t = v.last_timing()
+                launches += t["launches"]
+                dense_ms += t["dense_ms"]
+                dense_bytes += t["dense_bytes"]
+                dense_n += t["dense_launches"]
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        return ms, launches, dense_ms, dense_bytes, dense_n
+
+    verdicts = {}
+
+    def dev_step(s):
+        ok, m, st = v.test_device(d_lo[s].data_ptr(), d_hi[s].data_ptr(), labels[s])
+        verdicts[s] = ok
+
+    def e2e_step(s):
+        r = v.test(boxes[s].lo, boxes[s].hi, labels[s])
+        verdicts[s] = r.verified
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        dev_ms, launches, dense_ms, dense_bytes, dense_n = timed_loop(dev_step)
+    dev_verified = sum(1 for s in range(warm, warm + steps) if verdicts.get(s))
+    e2e_ms, _, _, _, _ = timed_loop(e2e_step)
+    if world > 1:
+        t = torch.tensor([dev_ms, e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms, e2e_ms = float(t[0]), float(t[1])
+        c = torch.tensor([dev_verified], device=dev)
+        torch.distributed.all_reduce(c)
+        dev_verified = int(c[0])
+    imgs = steps * world
+    value = dev_ms / imgs
+    e2e_val = e2e_ms / imgs
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = (dense_bytes / (dense_ms / 1000.0) / 1e9) if dense_ms > 0 else 0.0
+    line = {
+        "metric": METRIC, "value": value, "unit": "ms/image", "n_gpus": world, "steps": steps,
+        "warmup": warm, "ms_per_step": dev_ms / steps, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "arch": arch, "eps": eps_s, "model_seed": mseed,
+                   "input_seed": iseed, "early_term": et,
+                   "parallelism": f"replicas x{world} (image sharding)",
+                   "l2": "flushed between steps (256 MB write, outside the timed events)",
+                   "verified": f"{dev_verified}/{imgs}"},
+        "e2e": {"value": e2e_val, "unit": "ms/image", "h2d_bytes_per_step": 2 * 8 * n_in,
+                "d2h_bytes_per_step": 8 * (net.output_size - 1) + 4},
+        "gpu_launches": int(launches),
+        "roofline": {"kernel": "k_dense_coef (dense back-substitution)", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                     "launches": dense_n, "kernel_ms": dense_ms,
+                     "algorithmic_bytes": dense_bytes,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            ms1, kind, _, _, _ = cpu_reference(arch, eps_s, mseed, iseed, 1, 1, et)
+            n = max(1, min(4 * threads, int(args.cpu_sample_seconds * 1000.0 * threads / max(ms1, 1e-3))))
+            ms, kind, vd, wall, per = cpu_reference(arch, eps_s, mseed, iseed, n, threads, et)
+            line["cpu_baseline"] = {
+                "value": ms, "unit": "ms/image", "cores": threads, "kind": kind,
+                "sample": f"{n} images of {args.config} ({wall:.1f} s wall; one image per thread; "
+                          f"single-image latency {1000 * float(np.mean(per)):.1f} ms)"}
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -115,6 +115,15 @@ pc_status pc_net_test(pc_net* net, const double* lo, const double* up, int label
 pc_status pc_net_test_device(pc_net* net, const double* d_lo, const double* d_up, int label,
                              int* verified, double* margins, pc_stats* stats);
 
+/* Candidate label: unique argmax of the concrete forward pass at `center`
+ * (forward_eval, eval.hpp:39-102; unique_argmax, tools/main.cpp:86-100), -1
+ * on a tie. logits (optional) receives the n_out outputs. HOST arrays. */
+pc_status pc_net_candidate(pc_net* net, const double* center, int* label, double* logits);
+
+/* The CUDA stream (cudaStream_t) every kernel of this net is launched on,
+ * for callers that time or order work around pc_net_test* with CUDA events. */
+void* pc_net_stream(const pc_net* net);
+
 /* Kernel launches issued by this thread's last pc_net_test* call. */
 long long pc_last_launch_count(void);
 

@@ -912,6 +912,41 @@ void pc_net_destroy(pc_net* n) {
   delete n;
 }
 
+pc_status pc_net_candidate(pc_net* n, const double* center, int* label, double* logits) {
+  if (!n || !label) return PC_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lock(n->mu);
+  return guard([&] {
+    ck(cudaSetDevice(n->device), "cudaSetDevice");
+    cudaStream_t s = n->stream;
+    // concrete activations reuse the raw-bound buffers as scratch
+    ck(cudaMemcpyAsync(n->rlo, center, sizeof(double) * n->L[0].numel(), cudaMemcpyHostToDevice, s), "h2d");
+    for (size_t k = 1; k < n->L.size(); ++k) {
+      const HostLayer& l = n->L[k];
+      launch_eval_layer(s, l.d, n->rlo + n->off[l.pred0], l.pred1 >= 0 ? n->rlo + n->off[l.pred1] : nullptr,
+                        n->rlo + n->off[k]);
+    }
+    std::vector<double> y(n->n_out);
+    ck(cudaMemcpyAsync(y.data(), n->rlo + n->off[n->L.size() - 1], sizeof(double) * n->n_out,
+                       cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+    ck(cudaGetLastError(), "kernel");
+    if (logits) std::copy(y.begin(), y.end(), logits);
+    int best = 0;  // unique_argmax (tools/main.cpp:86-100)
+    bool tie = false;
+    for (int j = 1; j < n->n_out; ++j) {
+      if (y[j] > y[best]) {
+        best = j;
+        tie = false;
+      } else if (y[j] == y[best]) {
+        tie = true;
+      }
+    }
+    *label = tie ? -1 : best;
+  });
+}
+
+void* pc_net_stream(const pc_net* n) { return n ? (void*)n->stream : nullptr; }
+
 int pc_net_num_layers(const pc_net* n) { return n ? (int)n->L.size() : -1; }
 long long pc_net_layer_numel(const pc_net* n, int k) {
   if (!n || k < 0 || k >= (int)n->L.size()) return -1;

@@ -996,6 +996,58 @@ cudaError_t input_box_device(const double* center, int n, double eps, int clamp0
   return e;
 }
 
+// ===========================================================================
+// Concrete forward evaluation (eval.hpp:39-102): round-to-nearest, bias first
+// then ascending inputs, separate multiply and add roundings (no FMA), all
+// weights including zeros. Used for the candidate label (tools/main.cpp:86-100).
+// ===========================================================================
+__global__ void k_eval_layer(LayerDev L, const double* x, const double* x2, double* y) {
+  const long long n = (long long)L.out_w * L.out_h * L.out_c;
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  switch (L.kind) {
+    case KIND_DENSE: {
+      const int n_in = L.in_w * L.in_h * L.in_c;
+      double acc = L.bias[j];
+      for (int t = 0; t < n_in; ++t) acc = __dadd_rn(acc, __dmul_rn(L.WT[(size_t)t * n + j], x[t]));
+      y[j] = acc;
+      break;
+    }
+    case KIND_CONV: {
+      const int d = (int)(j % L.out_c);
+      const int w = (int)((j / L.out_c) % L.out_w);
+      const int h = (int)(j / ((long long)L.out_c * L.out_w));
+      double acc = L.bias[d];
+      for (int fy = 0; fy < L.fh; ++fy) {
+        const int iy = h * L.sh - L.ph + fy;
+        if (iy < 0 || iy >= L.in_h) continue;
+        for (int fx = 0; fx < L.fw; ++fx) {
+          const int ix = w * L.sw - L.pw + fx;
+          if (ix < 0 || ix >= L.in_w) continue;
+          for (int ci = 0; ci < L.in_c; ++ci)
+            acc = __dadd_rn(acc, __dmul_rn(L.F[((size_t)(fy * L.fw + fx) * L.in_c + ci) * L.out_c + d],
+                                           x[((size_t)iy * L.in_w + ix) * L.in_c + ci]));
+        }
+      }
+      y[j] = acc;
+      break;
+    }
+    case KIND_RELU:
+      y[j] = x[j] > 0.0 ? x[j] : 0.0;
+      break;
+    case KIND_JOIN:
+      y[j] = __dadd_rn(x[j], x2[j]);
+      break;
+  }
+}
+
+void launch_eval_layer(cudaStream_t s, const LayerDev& L, const double* x, const double* x2,
+                       double* y) {
+  const long long n = (long long)L.out_w * L.out_h * L.out_c;
+  k_eval_layer<<<cdiv(n, 128), 128, 0, s>>>(L, x, x2, y);
+  ++g_launches;
+}
+
 // Numeric-core self test: one scalar op per element (0 add_down, 1 add_up,
 // 2 mul_down, 3 mul_up, 4 div_down, 5 div_up, 6 ulp_above(a), 7 add_dir up,
 // 8 add_dir down, 9 nextup_bits(a), 10 nextdown_bits(a)).

@@ -134,6 +134,9 @@ void launch_gather_rows(cudaStream_t s, MatDev in, MatDev out, const int* perm, 
 cudaError_t input_box_device(const double* center, int n, double eps, int clamp01, double* lo,
                              double* up);
 
+void launch_eval_layer(cudaStream_t s, const LayerDev& L, const double* x, const double* x2,
+                       double* y);
+
 cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* out, long long n);
 
 extern thread_local long long g_launches;

@@ -142,6 +142,29 @@ class Verifier:
         """analyze (analyzer.hpp:198-242): refined per-neuron bounds."""
         return self.test(box.lo, box.hi, -1, want_bounds=True)
 
+    def candidate(self, center) -> int:
+        """Unique argmax of the concrete forward pass (-1 on ties), on the GPU."""
+        c = np.ascontiguousarray(center, dtype=np.float64)
+        lab = ctypes.c_int(-1)
+        _lib.check(_lib.lib.pc_net_candidate(self._h, _ptr(c), ctypes.byref(lab), None))
+        return lab.value
+
+    @property
+    def stream_handle(self) -> int:
+        """cudaStream_t of the engine (for CUDA-event timing by callers)."""
+        return int(_lib.lib.pc_net_stream(self._h) or 0)
+
+    def test_device(self, d_lo: int, d_up: int, label: int):
+        """test(lo, up, label) with the box already in device memory (pointers)."""
+        nm = max(self.n_out - 1, 1)
+        margins = np.zeros(nm)
+        verified = ctypes.c_int(0)
+        st = _lib.PcStats()
+        _lib.check(_lib.lib.pc_net_test_device(self._h, ctypes.c_void_p(d_lo), ctypes.c_void_p(d_up),
+                                               int(label), ctypes.byref(verified), _ptr(margins),
+                                               ctypes.byref(st)))
+        return bool(verified.value), margins[: self.n_out - 1], st.as_dict()
+
     def last_timing(self):
         t, dm, db, dl = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
         _lib.lib.pc_last_timing(ctypes.byref(t), ctypes.byref(dm), ctypes.byref(db), ctypes.byref(dl))
