@@ -35,66 +35,131 @@ __device__ __forceinline__ void store_relax(double* relax, long long j, const Iv
   p[4] = r.gamma.lo; p[5] = r.gamma.hi; p[6] = r.delta.lo; p[7] = r.delta.hi;
 }
 
-__global__ void k_fwd_dense(LayerDev L, const double* xlo, const double* xhi, const double* xrlo,
-                            const double* xrhi, double* ylo, double* yhi, double* yrlo,
-                            double* yrhi, double* dev, double* relax) {
-  const int n_out = L.out_c;
-  const int n_in = L.in_w * L.in_h * L.in_c;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= 2 * n_out) return;
-  const int track = tid / n_out, j = tid % n_out;
-  const double* xl = track ? xrlo : xlo;
-  const double* xh = track ? xrhi : xhi;
-  const double bias = L.bias[j];
-  double lo = bias, hi = bias, abs_hi = fabs(bias);
-  long long terms = 1;
-  for (int t = 0; t < n_in; ++t) {
-    const double w = L.WT[(size_t)t * n_out + j];
-    if (w == 0.0) continue;
-    const double a = xl[t], b = xh[t];
-    if (track == 0) {
-      ++terms;
-      abs_hi = add_up(abs_hi, mul_up(fabs(w), smax(fabs(a), fabs(b))));
-    }
-    if (w > 0.0) {
-      lo = add_down(lo, mul_down(w, a));
-      hi = add_up(hi, mul_up(w, b));
-    } else {
-      lo = add_down(lo, mul_down(w, b));
-      hi = add_up(hi, mul_up(w, a));
-    }
-  }
-  if (track == 0) {
-    const double slack = __dmul_rn(__dmul_rn(2.0, (double)(terms + 1)), ulp_above(abs_hi));
-    const Iv y{add_down(lo, -slack), add_up(hi, slack)};
-    ylo[j] = y.lo;
-    yhi[j] = y.hi;
-    // recompute_dev dense (analyzer.hpp:99-111): the |w|*mag chain over all
-    // inputs equals abs_hi (zero-weight terms add an exact 0).
-    dev[j] = __dmul_rn(__dmul_rn(2.0, (double)(n_in + 2)), ulp_above(abs_hi));
-    if (relax) store_relax(relax, j, y);
+// One affine term of affine_bound (eval.hpp:133-148) for both tracks:
+// padded (lo, hi, abs_hi) from padded inputs and raw (rlo, rhi) from raw
+// inputs. Zero weights are skipped (selects, no branch, in the fast path).
+template <bool FAST>
+__device__ __forceinline__ void affine_term(double w, double a, double b, double ra, double rb,
+                                            double& lo, double& hi, double& ab, double& rlo,
+                                            double& rhi, long long& terms, bool& bad) {
+  const bool nz = w != 0.0, pos = w > 0.0;
+  const double x1 = pos ? a : b, x2 = pos ? b : a;
+  const double r1 = pos ? ra : rb, r2 = pos ? rb : ra;
+  if (FAST) {
+    const double pl = f_mul_dn(w, x1, bad), ph = f_mul_up(w, x2, bad);
+    const double pa = f_mul_up(fabs(w), smax(fabs(a), fabs(b)), bad);
+    const double ql = f_mul_dn(w, r1, bad), qh = f_mul_up(w, r2, bad);
+    const double n_lo = f_add_dn(lo, pl), n_hi = f_add_up(hi, ph), n_ab = f_add_up(ab, pa);
+    const double n_rlo = f_add_dn(rlo, ql), n_rhi = f_add_up(rhi, qh);
+    lo = nz ? n_lo : lo;
+    hi = nz ? n_hi : hi;
+    ab = nz ? n_ab : ab;
+    rlo = nz ? n_rlo : rlo;
+    rhi = nz ? n_rhi : rhi;
+    terms += nz;
   } else {
-    yrlo[j] = lo;
-    yrhi[j] = hi;
+    if (!nz) return;
+    ++terms;
+    ab = add_up(ab, mul_up(fabs(w), smax(fabs(a), fabs(b))));
+    lo = add_down(lo, mul_down(w, x1));
+    hi = add_up(hi, mul_up(w, x2));
+    rlo = add_down(rlo, mul_down(w, r1));
+    rhi = add_up(rhi, mul_up(w, r2));
   }
 }
 
-__global__ void k_fwd_conv(LayerDev L, const double* xlo, const double* xhi, const double* xrlo,
-                           const double* xrhi, double* ylo, double* yhi, double* yrlo,
-                           double* yrhi, double* dev, double* relax) {
-  const long long numel = (long long)L.out_w * L.out_h * L.out_c;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= 2 * numel) return;
-  const int track = (int)(tid / numel);
-  const long long jj = tid % numel;
-  const int d = (int)(jj % L.out_c);
-  const int w = (int)((jj / L.out_c) % L.out_w);
-  const int h = (int)(jj / ((long long)L.out_c * L.out_w));
-  const double* xl = track ? xrlo : xlo;
-  const double* xh = track ? xrhi : xhi;
+// Padded result, dev and relaxation of one affine neuron (eval.hpp:149-151,
+// analyzer.hpp:109/140, analyzer.hpp:38-70).
+__device__ __forceinline__ void affine_finish(long long j, double lo, double hi, double ab,
+                                              long long terms, long long dterms, double rlo,
+                                              double rhi, double* ylo, double* yhi,
+                                              double* yrlo, double* yrhi, double* dev,
+                                              double* relax) {
+  const double slack = __dmul_rn(__dmul_rn(2.0, (double)(terms + 1)), ulp_above(ab));
+  const Iv y{add_down(lo, -slack), add_up(hi, slack)};
+  ylo[j] = y.lo;
+  yhi[j] = y.hi;
+  yrlo[j] = rlo;
+  yrhi[j] = rhi;
+  // recompute_dev: the |w|*mag chain over all inputs equals abs_hi (zero
+  // weights add an exact 0); only the term count differs.
+  dev[j] = __dmul_rn(__dmul_rn(2.0, (double)(dterms + 1)), ulp_above(ab));
+  if (relax) store_relax(relax, j, y);
+}
+
+// Dense layer: one thread per output neuron, both tracks (5 independent
+// chains for ILP); inputs streamed through shared memory in ascending order.
+constexpr int kFwdTile = 512;
+
+template <bool FAST>
+__device__ __forceinline__ bool fwd_dense_chain(const LayerDev& L, int j, int n_out, int n_in,
+                                                const double* xlo, const double* xhi,
+                                                const double* xrlo, const double* xrhi,
+                                                double& lo, double& hi, double& ab, double& rlo,
+                                                double& rhi, long long& terms) {
+  const double bias = L.bias[j];
+  lo = hi = rlo = rhi = bias;
+  ab = fabs(bias);
+  terms = 1;
+  bool bad = false;
+  for (int t = 0; t < n_in; ++t)
+    affine_term<FAST>(L.WT[(size_t)t * n_out + j], xlo[t], xhi[t], xrlo[t], xrhi[t], lo, hi, ab,
+                      rlo, rhi, terms, bad);
+  return bad;
+}
+
+__global__ void __launch_bounds__(128)
+    k_fwd_dense(LayerDev L, const double* xlo, const double* xhi, const double* xrlo,
+                const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi,
+                double* dev, double* relax) {
+  __shared__ double s_x[4][kFwdTile];
+  const int n_out = L.out_c;
+  const int n_in = L.in_w * L.in_h * L.in_c;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool act = j < n_out;
+  const double bias = act ? L.bias[j] : 0.0;
+  double lo = bias, hi = bias, rlo = bias, rhi = bias, ab = fabs(bias);
+  long long terms = 1;
+  bool bad = false;
+  for (int t0 = 0; t0 < n_in; t0 += kFwdTile) {
+    const int tn = min(kFwdTile, n_in - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < tn; e += blockDim.x) {
+      s_x[0][e] = xlo[t0 + e];
+      s_x[1][e] = xhi[t0 + e];
+      s_x[2][e] = xrlo[t0 + e];
+      s_x[3][e] = xrhi[t0 + e];
+    }
+    __syncthreads();
+    if (act) {
+      const double* wp = L.WT + (size_t)t0 * n_out + j;
+#pragma unroll 4
+      for (int t = 0; t < tn; ++t)
+        affine_term<true>(wp[(size_t)t * n_out], s_x[0][t], s_x[1][t], s_x[2][t], s_x[3][t], lo,
+                          hi, ab, rlo, rhi, terms, bad);
+    }
+  }
+  if (!act) return;
+  if (bad)  // out-of-band operand somewhere: redo this neuron with the exact ops
+    fwd_dense_chain<false>(L, j, n_out, n_in, xlo, xhi, xrlo, xrhi, lo, hi, ab, rlo, rhi, terms);
+  affine_finish(j, lo, hi, ab, terms, (long long)n_in + 1, rlo, rhi, ylo, yhi, yrlo, yrhi, dev,
+                relax);
+}
+
+// Conv layer: one thread per output neuron (h, w, d), both tracks; taps in
+// the reference order (fy, fx, ci), out-of-grid taps skipped.
+template <bool FAST>
+__device__ __forceinline__ bool fwd_conv_chain(const LayerDev& L, int h, int w, int d,
+                                               const double* xl, const double* xh,
+                                               const double* xrl, const double* xrh, double& lo,
+                                               double& hi, double& ab, double& rlo, double& rhi,
+                                               long long& terms, long long& dterms) {
   const double bias = L.bias[d];
-  double lo = bias, hi = bias, abs_hi = fabs(bias);
-  long long terms = 1, dterms = 1;
+  lo = hi = rlo = rhi = bias;
+  ab = fabs(bias);
+  terms = 1;
+  dterms = 1;
+  bool bad = false;
   const int cin = L.in_c, cout = L.out_c;
   for (int fy = 0; fy < L.fh; ++fy) {
     const int iy = h * L.sh - L.ph + fy;
@@ -105,35 +170,30 @@ __global__ void k_fwd_conv(LayerDev L, const double* xlo, const double* xhi, con
       const double* fp = L.F + ((size_t)(fy * L.fw + fx) * cin) * cout + d;
       const size_t xb = ((size_t)iy * L.in_w + ix) * cin;
       dterms += cin;
-      for (int ci = 0; ci < cin; ++ci) {
-        const double wv = fp[(size_t)ci * cout];
-        if (wv == 0.0) continue;
-        const double a = xl[xb + ci], b = xh[xb + ci];
-        if (track == 0) {
-          ++terms;
-          abs_hi = add_up(abs_hi, mul_up(fabs(wv), smax(fabs(a), fabs(b))));
-        }
-        if (wv > 0.0) {
-          lo = add_down(lo, mul_down(wv, a));
-          hi = add_up(hi, mul_up(wv, b));
-        } else {
-          lo = add_down(lo, mul_down(wv, b));
-          hi = add_up(hi, mul_up(wv, a));
-        }
-      }
+#pragma unroll 4
+      for (int ci = 0; ci < cin; ++ci)
+        affine_term<FAST>(fp[(size_t)ci * cout], xl[xb + ci], xh[xb + ci], xrl[xb + ci],
+                          xrh[xb + ci], lo, hi, ab, rlo, rhi, terms, bad);
     }
   }
-  if (track == 0) {
-    const double slack = __dmul_rn(__dmul_rn(2.0, (double)(terms + 1)), ulp_above(abs_hi));
-    const Iv y{add_down(lo, -slack), add_up(hi, slack)};
-    ylo[jj] = y.lo;
-    yhi[jj] = y.hi;
-    dev[jj] = __dmul_rn(__dmul_rn(2.0, (double)(dterms + 1)), ulp_above(abs_hi));
-    if (relax) store_relax(relax, jj, y);
-  } else {
-    yrlo[jj] = lo;
-    yrhi[jj] = hi;
-  }
+  return bad;
+}
+
+__global__ void __launch_bounds__(128)
+    k_fwd_conv(LayerDev L, const double* xlo, const double* xhi, const double* xrlo,
+               const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi,
+               double* dev, double* relax) {
+  const long long numel = (long long)L.out_w * L.out_h * L.out_c;
+  const long long jj = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (jj >= numel) return;
+  const int d = (int)(jj % L.out_c);
+  const int w = (int)((jj / L.out_c) % L.out_w);
+  const int h = (int)(jj / ((long long)L.out_c * L.out_w));
+  double lo, hi, ab, rlo, rhi;
+  long long terms, dterms;
+  if (fwd_conv_chain<true>(L, h, w, d, xlo, xhi, xrlo, xrhi, lo, hi, ab, rlo, rhi, terms, dterms))
+    fwd_conv_chain<false>(L, h, w, d, xlo, xhi, xrlo, xrhi, lo, hi, ab, rlo, rhi, terms, dterms);
+  affine_finish(jj, lo, hi, ab, terms, dterms, rlo, rhi, ylo, yhi, yrlo, yrhi, dev, relax);
 }
 
 __global__ void k_fwd_relu(long long n, const double* xlo, const double* xhi, const double* xrlo,
@@ -182,11 +242,11 @@ void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, con
   const long long n = (long long)L.out_w * L.out_h * L.out_c;
   switch (L.kind) {
     case KIND_DENSE:
-      k_fwd_dense<<<cdiv(2 * n, 128), 128, 0, s>>>(L, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
+      k_fwd_dense<<<cdiv(n, 32), 32, 0, s>>>(L, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
                                                    yrlo, yrhi, dev + o, rx);
       break;
     case KIND_CONV:
-      k_fwd_conv<<<cdiv(2 * n, 128), 128, 0, s>>>(L, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
+      k_fwd_conv<<<cdiv(n, 64), 64, 0, s>>>(L, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
                                                   yrlo, yrhi, dev + o, rx);
       break;
     case KIND_RELU:
@@ -394,31 +454,31 @@ void launch_init_margin(cudaStream_t s, int label, int n_out, MatDev out) {
 
 constexpr int kChainWarps = 4;
 
+// Lane fold of one staged group of terms: acc (+)= t for non-NaN t.
+template <bool FAST>
+__device__ __forceinline__ double fold(double acc, double t, bool up) {
+  if (FAST) {
+    const double n = f_add_dir(acc, t, up);
+    return (t == t) ? n : acc;
+  }
+  return (t == t) ? add_dir(acc, t, up) : acc;
+}
+
 // Constant update of a dense / conv substitution (backsub.hpp:365-389,
 // 454-489): k += c*b_j and kraw += c*b_j (iv_acc, zero terms skipped),
 // dev += mag(c)*dev_j (DevAccum), then widen_constant(k, dev). Lanes 0..4
 // run k.lo, k.hi, kraw.lo, kraw.hi, dev. Also counts the step's multiply-adds
 // (dense_madds :386 / gbc_madds :483).
-__global__ void __launch_bounds__(32 * kChainWarps)
-    k_chain_affine(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, const double* dev,
-                   Counters* ctr) {
-  __shared__ double s_t[kChainWarps][3][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kChainWarps + warp;
-  if (i >= rows.n) return;
-  bool upper;
-  const int q = row_query(rows, i, upper);
-  int bw = 0, bh = 0;
-  if (is_conv) frame_base(f, q, bw, bh);
-  const long long cells = m.cells;
-  const double* lo = m.lo + (size_t)i * cells;
-  const double* hi = m.hi + (size_t)i * cells;
-  double* K = m.K + 4 * (size_t)i;
-  double acc = lane < 4 ? K[lane] : 0.0;
+template <bool FAST>
+__device__ __forceinline__ bool chain_affine_row(const LayerDev& L, int is_conv, const FrameDev& f,
+                                                 int bw, int bh, long long cells, const double* lo,
+                                                 const double* hi, const double* dev, double acc,
+                                                 double (*s_t)[32], int lane, double& out,
+                                                 unsigned long long& madds) {
   const bool up = (lane & 1) || lane == 4;
   const int arr = lane == 4 ? 2 : (lane & 1);
   const int n_in = L.in_w * L.in_h * L.in_c;
-  unsigned long long madds = 0;
+  bool bad = FAST && lane < 5 && start_bad(acc);
   for (long long c0 = 0; c0 < cells; c0 += 32) {
     const long long cell = c0 + lane;
     double tl = PC_NAN, th = PC_NAN, td = PC_NAN;
@@ -443,27 +503,64 @@ __global__ void __launch_bounds__(32 * kChainWarps)
           jd = cell;
           madds += n_in;
         }
-        const Iv bt = iv_mul_scalar(c, b);
-        if (!iv_zero(bt)) {
-          tl = bt.lo;
-          th = bt.hi;
-        }
         const double dj = dev[jd];
-        if (dj != 0.0) td = mul_up(iv_mag(c), dj);
+        if (FAST) {
+          const bool pos = b > 0.0;
+          const double p1 = f_mul_dn(pos ? c.lo : c.hi, b, bad);
+          const double p2 = f_mul_up(pos ? c.hi : c.lo, b, bad);
+          if (b != 0.0) {
+            tl = p1;
+            th = p2;
+          }
+          const double pd = f_mul_up(iv_mag(c), dj, bad);
+          if (dj != 0.0) td = pd;
+        } else {
+          const Iv bt = iv_mul_scalar(c, b);
+          if (!iv_zero(bt)) {
+            tl = bt.lo;
+            th = bt.hi;
+          }
+          if (dj != 0.0) td = mul_up(iv_mag(c), dj);
+        }
       }
     }
-    s_t[warp][0][lane] = tl;
-    s_t[warp][1][lane] = th;
-    s_t[warp][2][lane] = td;
+    s_t[0][lane] = tl;
+    s_t[1][lane] = th;
+    s_t[2][lane] = td;
     __syncwarp();
     if (lane < 5) {
       const int n = (int)min((long long)32, cells - c0);
-      for (int k = 0; k < n; ++k) {
-        const double t = s_t[warp][arr][k];
-        if (t == t) acc = add_dir(acc, t, up);
-      }
+      for (int k = 0; k < n; ++k) acc = fold<FAST>(acc, s_t[arr][k], up);
     }
     __syncwarp();
+  }
+  out = acc;
+  return __any_sync(0xffffffffu, bad);
+}
+
+__global__ void __launch_bounds__(32 * kChainWarps)
+    k_chain_affine(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, const double* dev,
+                   Counters* ctr) {
+  __shared__ double s_t[kChainWarps][3][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kChainWarps + warp;
+  if (i >= rows.n) return;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw = 0, bh = 0;
+  if (is_conv) frame_base(f, q, bw, bh);
+  const long long cells = m.cells;
+  const double* lo = m.lo + (size_t)i * cells;
+  const double* hi = m.hi + (size_t)i * cells;
+  double* K = m.K + 4 * (size_t)i;
+  const double acc0 = lane < 4 ? K[lane] : 0.0;
+  unsigned long long madds = 0;
+  double acc;
+  if (chain_affine_row<true>(L, is_conv, f, bw, bh, cells, lo, hi, dev, acc0, s_t[warp], lane, acc,
+                             madds)) {
+    madds = 0;
+    chain_affine_row<false>(L, is_conv, f, bw, bh, cells, lo, hi, dev, acc0, s_t[warp], lane, acc,
+                            madds);
   }
   const double dtot = __shfl_sync(0xffffffffu, acc, 4);
   if (lane == 0) K[0] = dtot != 0.0 ? add_down(acc, -dtot) : acc;
@@ -483,23 +580,14 @@ void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const 
 // Constant update of a relu substitution (backsub.hpp:536-563): per nonzero
 // cell one offset term (sign-stable coefficient) or two (straddling: offp
 // then offn), each skipped when zero. Lanes 0..3: k.lo, k.hi, kraw.lo, kraw.hi.
-__global__ void __launch_bounds__(32 * kChainWarps)
-    k_chain_relu(RowsDev rows, FrameDev f, MatDev m, const double* relax) {
-  __shared__ double s_t[kChainWarps][2][2][32];  // [slot][lo/hi][cell]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kChainWarps + warp;
-  if (i >= rows.n) return;
-  bool upper;
-  const int q = row_query(rows, i, upper);
-  int bw, bh;
-  frame_base(f, q, bw, bh);
-  const long long cells = m.cells;
-  const double* lo = m.lo + (size_t)i * cells;
-  const double* hi = m.hi + (size_t)i * cells;
-  double* K = m.K + 4 * (size_t)i;
-  double acc = lane < 4 ? K[lane] : 0.0;
+template <bool FAST>
+__device__ __forceinline__ bool chain_relu_row(const FrameDev& f, int bw, int bh, bool upper,
+                                               long long cells, const double* lo, const double* hi,
+                                               const double* relax, double acc,
+                                               double (*s_t)[2][32], int lane, double& out) {
   const bool up = lane & 1;
   const int arr = lane & 1;
+  bool bad = FAST && lane < 4 && start_bad(acc);
   for (long long c0 = 0; c0 < cells; c0 += 32) {
     const long long cell = c0 + lane;
     double t0l = PC_NAN, t0h = PC_NAN, t1l = PC_NAN, t1h = PC_NAN;
@@ -514,36 +602,53 @@ __global__ void __launch_bounds__(32 * kChainWarps)
         const Iv beta{R[2], R[3]}, delta{R[6], R[7]};
         const Iv op = upper ? delta : beta;
         const Iv on = upper ? beta : delta;
-        if (!(c.lo < 0.0)) {
-          const Iv off = iv_mul(c, op);
-          if (!iv_zero(off)) { t0l = off.lo; t0h = off.hi; }
-        } else if (!(c.hi > 0.0)) {
-          const Iv off = iv_mul(c, on);
-          if (!iv_zero(off)) { t0l = off.lo; t0h = off.hi; }
-        } else {
-          const Iv offp = iv_mul(iv_pos_part(c), op);
-          const Iv offn = iv_mul(iv_neg_part(c), on);
-          if (!iv_zero(offp)) { t0l = offp.lo; t0h = offp.hi; }
-          if (!iv_zero(offn)) { t1l = offn.lo; t1h = offn.hi; }
+        Iv o0, o1{0.0, 0.0};
+        if (!(c.lo < 0.0)) o0 = FAST ? f_iv_mul(c, op, bad) : iv_mul(c, op);
+        else if (!(c.hi > 0.0)) o0 = FAST ? f_iv_mul(c, on, bad) : iv_mul(c, on);
+        else {
+          o0 = FAST ? f_iv_mul(iv_pos_part(c), op, bad) : iv_mul(iv_pos_part(c), op);
+          o1 = FAST ? f_iv_mul(iv_neg_part(c), on, bad) : iv_mul(iv_neg_part(c), on);
         }
+        if (!iv_zero(o0)) { t0l = o0.lo; t0h = o0.hi; }
+        if (!iv_zero(o1)) { t1l = o1.lo; t1h = o1.hi; }
       }
     }
-    s_t[warp][0][0][lane] = t0l;
-    s_t[warp][0][1][lane] = t0h;
-    s_t[warp][1][0][lane] = t1l;
-    s_t[warp][1][1][lane] = t1h;
+    s_t[0][0][lane] = t0l;
+    s_t[0][1][lane] = t0h;
+    s_t[1][0][lane] = t1l;
+    s_t[1][1][lane] = t1h;
     __syncwarp();
     if (lane < 4) {
       const int n = (int)min((long long)32, cells - c0);
       for (int k = 0; k < n; ++k) {
-        const double a = s_t[warp][0][arr][k];
-        if (a == a) acc = add_dir(acc, a, up);
-        const double b = s_t[warp][1][arr][k];
-        if (b == b) acc = add_dir(acc, b, up);
+        acc = fold<FAST>(acc, s_t[0][arr][k], up);
+        acc = fold<FAST>(acc, s_t[1][arr][k], up);
       }
     }
     __syncwarp();
   }
+  out = acc;
+  return __any_sync(0xffffffffu, bad);
+}
+
+__global__ void __launch_bounds__(32 * kChainWarps)
+    k_chain_relu(RowsDev rows, FrameDev f, MatDev m, const double* relax) {
+  __shared__ double s_t[kChainWarps][2][2][32];  // [slot][lo/hi][cell]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kChainWarps + warp;
+  if (i >= rows.n) return;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const long long cells = m.cells;
+  const double* lo = m.lo + (size_t)i * cells;
+  const double* hi = m.hi + (size_t)i * cells;
+  double* K = m.K + 4 * (size_t)i;
+  const double acc0 = lane < 4 ? K[lane] : 0.0;
+  double acc;
+  if (chain_relu_row<true>(f, bw, bh, upper, cells, lo, hi, relax, acc0, s_t[warp], lane, acc))
+    chain_relu_row<false>(f, bw, bh, upper, cells, lo, hi, relax, acc0, s_t[warp], lane, acc);
   if (lane < 4) K[lane] = acc;
 }
 
@@ -557,6 +662,46 @@ void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, M
 // add the corner product with the frame layer's bounds for each nonzero
 // cell in ascending order. Lane 0: padded track (constant, bounds); lane 1:
 // raw track (constant_raw, raw bounds).
+template <bool FAST>
+__device__ __forceinline__ bool conc_row(const FrameDev& f, int bw, int bh, bool upper,
+                                         long long cells, const double* lo, const double* hi,
+                                         const double* blo, const double* bhi, const double* rlo,
+                                         const double* rhi, double acc, double (*s_t)[32],
+                                         int lane, double& out) {
+  bool bad = FAST && lane < 2 && start_bad(acc);
+  for (long long c0 = 0; c0 < cells; c0 += 32) {
+    const long long cell = c0 + lane;
+    double tp = PC_NAN, tr = PC_NAN;
+    if (cell < cells) {
+      const Iv c{lo[cell], hi[cell]};
+      if (!iv_zero(c)) {
+        const int cc = (int)(cell % f.C);
+        const int x = (int)((cell / f.C) % f.S_w);
+        const int y = (int)(cell / ((long long)f.C * f.S_w));
+        const long long j = ((long long)(bh + y) * f.G_w + (bw + x)) * f.C + cc;
+        const Iv B{blo[j], bhi[j]}, Br{rlo[j], rhi[j]};
+        if (FAST) {
+          tp = upper ? f_corner_hi(c, B, bad) : f_corner_lo(c, B, bad);
+          tr = upper ? f_corner_hi(c, Br, bad) : f_corner_lo(c, Br, bad);
+        } else {
+          tp = upper ? corner_hi(c, B) : corner_lo(c, B);
+          tr = upper ? corner_hi(c, Br) : corner_lo(c, Br);
+        }
+      }
+    }
+    s_t[0][lane] = tp;
+    s_t[1][lane] = tr;
+    __syncwarp();
+    if (lane < 2) {
+      const int n = (int)min((long long)32, cells - c0);
+      for (int k = 0; k < n; ++k) acc = fold<FAST>(acc, s_t[lane][k], upper);
+    }
+    __syncwarp();
+  }
+  out = acc;
+  return __any_sync(0xffffffffu, bad);
+}
+
 __global__ void __launch_bounds__(32 * kChainWarps)
     k_concretize(RowsDev rows, FrameDev f, MatDev m, const double* blo, const double* bhi,
                  const double* rlo, const double* rhi, double* vals, double* rvals) {
@@ -572,36 +717,12 @@ __global__ void __launch_bounds__(32 * kChainWarps)
   const double* lo = m.lo + (size_t)i * cells;
   const double* hi = m.hi + (size_t)i * cells;
   const double* K = m.K + 4 * (size_t)i;
-  double acc = 0.0;
-  if (lane == 0) acc = upper ? K[1] : K[0];
-  if (lane == 1) acc = upper ? K[3] : K[2];
-  for (long long c0 = 0; c0 < cells; c0 += 32) {
-    const long long cell = c0 + lane;
-    double tp = PC_NAN, tr = PC_NAN;
-    if (cell < cells) {
-      const Iv c{lo[cell], hi[cell]};
-      if (!iv_zero(c)) {
-        const int cc = (int)(cell % f.C);
-        const int x = (int)((cell / f.C) % f.S_w);
-        const int y = (int)(cell / ((long long)f.C * f.S_w));
-        const long long j = ((long long)(bh + y) * f.G_w + (bw + x)) * f.C + cc;
-        const Iv B{blo[j], bhi[j]}, Br{rlo[j], rhi[j]};
-        tp = upper ? corner_hi(c, B) : corner_lo(c, B);
-        tr = upper ? corner_hi(c, Br) : corner_lo(c, Br);
-      }
-    }
-    s_t[warp][0][lane] = tp;
-    s_t[warp][1][lane] = tr;
-    __syncwarp();
-    if (lane < 2) {
-      const int n = (int)min((long long)32, cells - c0);
-      for (int k = 0; k < n; ++k) {
-        const double t = s_t[warp][lane][k];
-        if (t == t) acc = add_dir(acc, t, upper);
-      }
-    }
-    __syncwarp();
-  }
+  double acc0 = 0.0;
+  if (lane == 0) acc0 = upper ? K[1] : K[0];
+  if (lane == 1) acc0 = upper ? K[3] : K[2];
+  double acc;
+  if (conc_row<true>(f, bw, bh, upper, cells, lo, hi, blo, bhi, rlo, rhi, acc0, s_t[warp], lane, acc))
+    conc_row<false>(f, bw, bh, upper, cells, lo, hi, blo, bhi, rlo, rhi, acc0, s_t[warp], lane, acc);
   if (lane == 0) vals[i] = acc;
   if (lane == 1) rvals[i] = acc;
 }
@@ -620,76 +741,100 @@ void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, M
 // ===========================================================================
 
 // dense_step coefficients (backsub.hpp:365-386): M'[r][t] = sum_j M[r][j]*W[j][t]
-// over ascending j, skipping zero coefficients and zero weights. Tile: 16 rows
-// x 64 columns per 256-thread block; each thread owns 4 rows of one column.
-// The K dimension (frame cells j) streams through shared memory in slabs of
-// 32 in ascending order.
-constexpr int kDR = 16, kDC = 64, kDK = 32;
+// over ascending j, skipping zero coefficients and zero weights.
+// Output-stationary: a block owns TM rows x 128 columns, each thread TM rows
+// of one column (TM independent interval chains for ILP); the frame cells j
+// (the reduction) stream through shared memory in ascending slabs. Fast
+// branch-free ops; any output whose operands leave the fast band is
+// recomputed with the exact ops.
+constexpr int kDC = 128, kDK = 32;
 
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void madd_fast(double w, double clo, double chi, double& lo, double& hi,
+                                          bool& bad) {
+  const bool skip = (w == 0.0) | ((clo == 0.0) & (chi == 0.0));
+  const bool pos = w > 0.0;
+  const double a = pos ? clo : chi, b = pos ? chi : clo;
+  const double pl = f_mul_dn(a, w, bad), ph = f_mul_up(b, w, bad);
+  const double nl = f_add_dn(lo, pl), nh = f_add_up(hi, ph);
+  lo = skip ? lo : nl;
+  hi = skip ? hi : nh;
+}
+
+__device__ __forceinline__ void madd_exact(double w, double clo, double chi, double& lo,
+                                           double& hi) {
+  if (w == 0.0 || (clo == 0.0 && chi == 0.0)) return;
+  const double a = w > 0.0 ? clo : chi, b = w > 0.0 ? chi : clo;
+  lo = add_down(lo, mul_down(a, w));
+  hi = add_up(hi, mul_up(b, w));
+}
+
+template <int TM>
+__global__ void __launch_bounds__(kDC)
     k_dense_coef(const double* __restrict__ W, int n_k, int n_in, int nrows, MatDev in,
                  MatDev out) {
-  __shared__ double s_al[kDR][kDK], s_ah[kDR][kDK];
+  __shared__ double s_al[TM][kDK], s_ah[TM][kDK];
   __shared__ double s_w[kDK][kDC];
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // ty in [0,4)
+  const int tx = threadIdx.x;
   const int col = blockIdx.x * kDC + tx;
-  const int r0 = blockIdx.y * kDR;
-  Iv acc[4];
+  const int r0 = blockIdx.y * TM;
+  double lo[TM], hi[TM];
+  bool bad[TM];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) acc[u] = Iv{0.0, 0.0};
+  for (int u = 0; u < TM; ++u) {
+    lo[u] = hi[u] = 0.0;
+    bad[u] = false;
+  }
   for (int k0 = 0; k0 < n_k; k0 += kDK) {
-    for (int e = threadIdx.x; e < kDR * kDK; e += 256) {
+    __syncthreads();
+    for (int e = tx; e < TM * kDK; e += kDC) {
       const int rr = e / kDK, kk = e % kDK;
       const int r = r0 + rr, k = k0 + kk;
-      double a = 0.0, b = 0.0;
-      if (r < nrows && k < n_k) {
-        a = in.lo[(size_t)r * n_k + k];
-        b = in.hi[(size_t)r * n_k + k];
-      }
-      s_al[rr][kk] = a;
-      s_ah[rr][kk] = b;
+      const bool ok = r < nrows && k < n_k;
+      s_al[rr][kk] = ok ? in.lo[(size_t)r * n_k + k] : 0.0;
+      s_ah[rr][kk] = ok ? in.hi[(size_t)r * n_k + k] : 0.0;
     }
-    for (int e = threadIdx.x; e < kDK * kDC; e += 256) {
-      const int kk = e / kDC, cc = e % kDC;
-      const int k = k0 + kk, c = blockIdx.x * kDC + cc;
-      s_w[kk][cc] = (k < n_k && c < n_in) ? W[(size_t)k * n_in + c] : 0.0;
+    for (int kk = 0; kk < kDK; ++kk) {
+      const int k = k0 + kk;
+      s_w[kk][tx] = (k < n_k && col < n_in) ? W[(size_t)k * n_in + col] : 0.0;
     }
     __syncthreads();
     const int kn = min(kDK, n_k - k0);
+#pragma unroll 2
     for (int kk = 0; kk < kn; ++kk) {
       const double w = s_w[kk][tx];
-      if (w == 0.0) continue;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int rr = ty * 4 + u;
-        const Iv c{s_al[rr][kk], s_ah[rr][kk]};
-        if (iv_zero(c)) continue;
-        const double a = w > 0.0 ? c.lo : c.hi;
-        const double b = w > 0.0 ? c.hi : c.lo;
-        acc[u].lo = add_down(acc[u].lo, mul_down(a, w));
-        acc[u].hi = add_up(acc[u].hi, mul_up(b, w));
-      }
+      for (int u = 0; u < TM; ++u) madd_fast(w, s_al[u][kk], s_ah[u][kk], lo[u], hi[u], bad[u]);
     }
-    __syncthreads();
   }
-  if (col < n_in) {
+  if (col >= n_in) return;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = r0 + ty * 4 + u;
-      if (r < nrows) {
-        out.lo[(size_t)r * n_in + col] = acc[u].lo;
-        out.hi[(size_t)r * n_in + col] = acc[u].hi;
-      }
+  for (int u = 0; u < TM; ++u) {
+    const int r = r0 + u;
+    if (r >= nrows) continue;
+    if (bad[u]) {
+      lo[u] = hi[u] = 0.0;
+      for (int k = 0; k < n_k; ++k)
+        madd_exact(W[(size_t)k * n_in + col], in.lo[(size_t)r * n_k + k], in.hi[(size_t)r * n_k + k],
+                   lo[u], hi[u]);
     }
+    out.lo[(size_t)r * n_in + col] = lo[u];
+    out.hi[(size_t)r * n_in + col] = hi[u];
   }
 }
 
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, MatDev out,
                        cudaEvent_t ev0, cudaEvent_t ev1) {
   const int n_k = (int)in.cells, n_in = (int)out.cells;
-  dim3 grid(cdiv(n_in, kDC), cdiv(nrows, kDR));
   if (ev0) cudaEventRecord(ev0, s);
-  k_dense_coef<<<grid, 256, 0, s>>>(L.W, n_k, n_in, nrows, in, out);
+  // Few rows: one row per thread maximises parallelism (the chain length n_k
+  // bounds latency); many rows: 4 rows per thread for weight reuse.
+  if (nrows <= 64) {
+    dim3 grid(cdiv(n_in, kDC), nrows);
+    k_dense_coef<1><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, nrows, in, out);
+  } else {
+    dim3 grid(cdiv(n_in, kDC), cdiv(nrows, 4));
+    k_dense_coef<4><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, nrows, in, out);
+  }
   if (ev1) cudaEventRecord(ev1, s);
   ++g_launches;
 }
@@ -702,6 +847,36 @@ void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, 
 // visits frame cells in (ch, cw, d) order).
 __device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
+template <bool FAST>
+__device__ __forceinline__ Iv gbc_gather(const LayerDev& L, const FrameDev& fi, int bw, int bh,
+                                         const double* ilo, const double* ihi, int iy, int ix,
+                                         int ci, bool& bad) {
+  const int cin = L.in_c, cout = L.out_c;
+  int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
+  int aw0 = floordiv(ix + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ix + L.pw, L.sw);
+  ah0 = max(ah0, bh);
+  ah1 = min(ah1, bh + fi.S_h - 1);
+  aw0 = max(aw0, bw);
+  aw1 = min(aw1, bw + fi.S_w - 1);
+  double lo = 0.0, hi = 0.0;
+  for (int ah = ah0; ah <= ah1; ++ah) {
+    const int fy = iy + L.ph - ah * L.sh;
+    for (int aw = aw0; aw <= aw1; ++aw) {
+      const int fx = ix + L.pw - aw * L.sw;
+      const size_t cb = ((size_t)(ah - bh) * fi.S_w + (aw - bw)) * cout;
+      const double* wp = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ci;
+      if (FAST) {
+#pragma unroll 4
+        for (int d = 0; d < cout; ++d)
+          madd_fast(wp[(size_t)d * cin], ilo[cb + d], ihi[cb + d], lo, hi, bad);
+      } else {
+        for (int d = 0; d < cout; ++d) madd_exact(wp[(size_t)d * cin], ilo[cb + d], ihi[cb + d], lo, hi);
+      }
+    }
+  }
+  return Iv{lo, hi};
+}
+
 __global__ void __launch_bounds__(256)
     k_gbc_coef(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, MatDev in, MatDev out) {
   const int i = blockIdx.y;
@@ -713,37 +888,16 @@ __global__ void __launch_bounds__(256)
   const long long ocells = out.cells, icells = in.cells;
   const double* ilo = in.lo + (size_t)i * icells;
   const double* ihi = in.hi + (size_t)i * icells;
-  const int cin = L.in_c, cout = L.out_c;
+  const int cin = L.in_c;
   for (long long o = blockIdx.x * blockDim.x + threadIdx.x; o < ocells;
        o += (long long)gridDim.x * blockDim.x) {
     const int ci = (int)(o % cin);
     const int x = (int)((o / cin) % fo.S_w);
     const int y = (int)(o / ((long long)cin * fo.S_w));
     const int iy = nbh + y, ix = nbw + x;
-    // frame rows ah with 0 <= iy - (ah*sh - ph) < fh
-    int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
-    int aw0 = floordiv(ix + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ix + L.pw, L.sw);
-    ah0 = max(ah0, bh); ah1 = min(ah1, bh + fi.S_h - 1);
-    aw0 = max(aw0, bw); aw1 = min(aw1, bw + fi.S_w - 1);
-    Iv acc{0.0, 0.0};
-    for (int ah = ah0; ah <= ah1; ++ah) {
-      const int fy = iy + L.ph - ah * L.sh;
-      for (int aw = aw0; aw <= aw1; ++aw) {
-        const int fx = ix + L.pw - aw * L.sw;
-        const size_t cb = ((size_t)(ah - bh) * fi.S_w + (aw - bw)) * cout;
-        const double* wp = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ci;
-        for (int d = 0; d < cout; ++d) {
-          const Iv c{ilo[cb + d], ihi[cb + d]};
-          if (iv_zero(c)) continue;
-          const double w = wp[(size_t)d * cin];
-          if (w == 0.0) continue;
-          const double a = w > 0.0 ? c.lo : c.hi;
-          const double b = w > 0.0 ? c.hi : c.lo;
-          acc.lo = add_down(acc.lo, mul_down(a, w));
-          acc.hi = add_up(acc.hi, mul_up(b, w));
-        }
-      }
-    }
+    bool bad = false;
+    Iv acc = gbc_gather<true>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+    if (bad) acc = gbc_gather<false>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
     out.lo[(size_t)i * ocells + o] = acc.lo;
     out.hi[(size_t)i * ocells + o] = acc.hi;
   }
@@ -761,6 +915,23 @@ void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
 // relu_step coefficients (backsub.hpp:536-563): per nonzero cell, slope by
 // sign (upper rows: gamma for c>=0, alpha for c<=0; lower rows mirrored);
 // straddling cells split into positive and negative parts.
+template <bool FAST>
+__device__ __forceinline__ Iv relu_map(const Iv& c, const Iv& sp, const Iv& sn, bool& bad) {
+  if (FAST) {
+    const bool pos = !(c.lo < 0.0), neg = !(c.hi > 0.0);
+    // sign-stable: iv_mul(c, slope); straddling: iv_add of the two parts
+    const Iv s1 = (neg && !pos) ? sn : sp;
+    const Iv a = pos || neg ? c : iv_pos_part(c);
+    const Iv m1 = f_iv_mul(a, s1, bad);
+    const Iv m2 = f_iv_mul(iv_neg_part(c), sn, bad);  // products are band-checked
+    const Iv sum{f_add_dn(m1.lo, m2.lo), f_add_up(m1.hi, m2.hi)};
+    return (pos || neg) ? m1 : sum;
+  }
+  if (!(c.lo < 0.0)) return iv_mul(c, sp);
+  if (!(c.hi > 0.0)) return iv_mul(c, sn);
+  return iv_add(iv_mul(iv_pos_part(c), sp), iv_mul(iv_neg_part(c), sn));
+}
+
 __global__ void __launch_bounds__(256)
     k_relu_coef(RowsDev rows, FrameDev f, MatDev in, MatDev out, const double* relax) {
   const int i = blockIdx.y;
@@ -784,9 +955,9 @@ __global__ void __launch_bounds__(256)
       const Iv alpha{R[0], R[1]}, gamma{R[4], R[5]};
       const Iv sp = upper ? gamma : alpha;
       const Iv sn = upper ? alpha : gamma;
-      if (!(c.lo < 0.0)) r = iv_mul(c, sp);
-      else if (!(c.hi > 0.0)) r = iv_mul(c, sn);
-      else r = iv_add(iv_mul(iv_pos_part(c), sp), iv_mul(iv_neg_part(c), sn));
+      bool bad = false;
+      r = relu_map<true>(c, sp, sn, bad);
+      if (bad) r = relu_map<false>(c, sp, sn, bad);
     }
     out.lo[(size_t)i * cells + cell] = r.lo;
     out.hi[(size_t)i * cells + cell] = r.hi;

@@ -230,4 +230,95 @@ __device__ __forceinline__ Relax relu_relaxation(const Iv& b) {
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Branch-free fast paths ("f_" ops) for hot loops.
+//
+// Valid (bit-identical to the exact ops above) while every product magnitude
+// lies in [2^-1020, 2^980) and every sum operand below 2^1020. In that band
+// nextafter(p, -inf) == RM(p - denorm_min) and nextafter(p, +inf) ==
+// RP(p + denorm_min) exactly, and TwoSum cannot overflow. Callers accumulate a
+// `bad` flag from f_mul_* and verify chain starting values; when it is set,
+// the affected output is recomputed with the exact ops (same order), so the
+// result is always the reference's. Sums are safe when the terms are checked
+// and chains start below 2^1000: partial sums then stay below 2^1020 for
+// any chain shorter than 2^39 terms.
+// ---------------------------------------------------------------------------
+constexpr double kSafeHi = 0x1p980;
+constexpr double kSafeLo = 0x1p-1020;
+constexpr double kStartHi = 0x1p1000;
+
+__device__ __forceinline__ double f_add_up(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  const double rd = __dadd_rd(a, b), ru = __dadd_ru(a, b);
+  const double st = __dadd_ru(s, kTiny);
+  return (rd == ru) ? s : st;
+}
+__device__ __forceinline__ double f_add_dn(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  const double rd = __dadd_rd(a, b), ru = __dadd_ru(a, b);
+  const double st = __dadd_rd(s, -kTiny);
+  return (rd == ru) ? s : st;
+}
+__device__ __forceinline__ double f_add_dir(double a, double b, bool up) {
+  const double s = __dadd_rn(a, b);
+  const double rd = __dadd_rd(a, b), ru = __dadd_ru(a, b);
+  const double st = up ? __dadd_ru(s, kTiny) : __dadd_rd(s, -kTiny);
+  return (rd == ru) ? s : st;
+}
+__device__ __forceinline__ bool out_of_band(double p) {
+  const double ap = fabs(p);
+  return !(ap < kSafeHi) | (ap < kSafeLo);
+}
+// Products where either factor may be zero (zero short-circuit, exact 0).
+__device__ __forceinline__ double f_mul_up(double a, double b, bool& bad) {
+  const double p = __dmul_rn(a, b);
+  const double r = __fma_rn(a, b, -p);
+  const bool z = (a == 0.0) | (b == 0.0);
+  bad |= !z & out_of_band(p);
+  const double v = ((r == 0.0) & (fabs(p) >= kFloor)) ? p : __dadd_ru(p, kTiny);
+  return z ? 0.0 : v;
+}
+__device__ __forceinline__ double f_mul_dn(double a, double b, bool& bad) {
+  const double p = __dmul_rn(a, b);
+  const double r = __fma_rn(a, b, -p);
+  const bool z = (a == 0.0) | (b == 0.0);
+  bad |= !z & out_of_band(p);
+  const double v = ((r == 0.0) & (fabs(p) >= kFloor)) ? p : __dadd_rd(p, -kTiny);
+  return z ? 0.0 : v;
+}
+// Products of two nonzero factors.
+__device__ __forceinline__ double f_mul_up_nz(double a, double b, bool& bad) {
+  const double p = __dmul_rn(a, b);
+  const double r = __fma_rn(a, b, -p);
+  bad |= out_of_band(p);
+  return ((r == 0.0) & (fabs(p) >= kFloor)) ? p : __dadd_ru(p, kTiny);
+}
+__device__ __forceinline__ double f_mul_dn_nz(double a, double b, bool& bad) {
+  const double p = __dmul_rn(a, b);
+  const double r = __fma_rn(a, b, -p);
+  bad |= out_of_band(p);
+  return ((r == 0.0) & (fabs(p) >= kFloor)) ? p : __dadd_rd(p, -kTiny);
+}
+__device__ __forceinline__ double f_corner_hi(const Iv& a, const Iv& b, bool& bad) {
+  double v = f_mul_up(a.lo, b.lo, bad);
+  v = smax(v, f_mul_up(a.lo, b.hi, bad));
+  v = smax(v, f_mul_up(a.hi, b.lo, bad));
+  v = smax(v, f_mul_up(a.hi, b.hi, bad));
+  return v;
+}
+__device__ __forceinline__ double f_corner_lo(const Iv& a, const Iv& b, bool& bad) {
+  double v = f_mul_dn(a.lo, b.lo, bad);
+  v = smin(v, f_mul_dn(a.lo, b.hi, bad));
+  v = smin(v, f_mul_dn(a.hi, b.lo, bad));
+  v = smin(v, f_mul_dn(a.hi, b.hi, bad));
+  return v;
+}
+// iv_mul with both intervals known nonzero... or either zero (returns [0,0]).
+__device__ __forceinline__ Iv f_iv_mul(const Iv& a, const Iv& b, bool& bad) {
+  const bool z = iv_zero(a) | iv_zero(b);
+  const Iv r{f_corner_lo(a, b, bad), f_corner_hi(a, b, bad)};
+  return z ? Iv{0.0, 0.0} : r;
+}
+__device__ __forceinline__ bool start_bad(double x) { return !(fabs(x) < kStartHi); }
+
 }  // namespace pc
