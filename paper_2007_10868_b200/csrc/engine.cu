@@ -91,8 +91,12 @@ struct pc_net {
   cudaStream_t stream = nullptr;
   pc_options opt{};
   std::vector<HostLayer> L;
-  std::vector<long long> off;
+  std::vector<long long> off, pofs;  // neuron / grid-position offsets per layer
   long long total = 0, max_numel = 0;
+  int* gen_n = nullptr;
+  int* gen_pos = nullptr;
+  int* gen_l = nullptr;
+  int gen = 0;
   int n_out = 0;
   std::vector<void*> owned;
   double *blo = nullptr, *bhi = nullptr, *rlo = nullptr, *rhi = nullptr, *dev = nullptr,
@@ -597,8 +601,10 @@ void run_pass(pc_net* n, int t, bool allow_freeze, pc_stats* st) {
       w.walk(m, 0, true);
     }
   }
-  launch_writeback(s, N, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
-                   Q.feeds_relu ? n->relax + 8 * o : nullptr);
+  ++n->gen;  // refresh round: the write-back marks what this pass changed
+  launch_writeback(s, N, Q.out_c, t, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
+                   Q.feeds_relu ? n->relax + 8 * o : nullptr, n->gen_n, n->gen_pos, n->gen_l,
+                   n->gen, o, n->pofs[t]);
 }
 
 // run_margin_pass (backsub.hpp:1070-1096)
@@ -640,10 +646,12 @@ void run_test(pc_net* n, int label, double* margins, pc_stats* st) {
   const int nl = (int)n->L.size();
   const int out = nl - 1;
   ck(cudaMemsetAsync(n->ctr, 0, sizeof(Counters), s), "memset");
-  for (int k = 1; k < nl; ++k) {
+  ++n->gen;
+  for (int k = 1; k < nl; ++k) {  // forward_interval, padded + raw (analyzer.hpp:203-215)
     const HostLayer& l = n->L[k];
-    launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(), k,
-                         l.pred0, l.pred1, n->dev, n->relax);
+    launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
+                         n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
+                         n->gen_pos, n->gen_l, n->gen, 1);
   }
   for (int t = 1; t < nl; ++t) {
     const bool is_out = t == out;
@@ -652,8 +660,9 @@ void run_test(pc_net* n, int label, double* margins, pc_stats* st) {
     if (is_out) continue;
     for (int k = t + 1; k < nl; ++k) {  // refresh (analyzer.hpp:232-239)
       const HostLayer& l = n->L[k];
-      launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(), k,
-                           l.pred0, l.pred1, n->dev, n->relax);
+      launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
+                           n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
+                           n->gen_pos, n->gen_l, n->gen, 0);
     }
   }
   if (label >= 0) run_margin(n, label, st, margins);
@@ -829,6 +838,8 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
       n->max_numel = std::max(n->max_numel, n->L[k].numel());
     }
     n->total = n->off[nl];
+    n->pofs.assign(nl + 1, 0);
+    for (int k = 0; k < nl; ++k) n->pofs[k + 1] = n->pofs[k] + (long long)n->L[k].out_w * n->L[k].out_h;
     n->n_out = (int)n->L.back().numel();
     for (int k = 0; k < nl; ++k) {
       HostLayer& l = n->L[k];
@@ -889,6 +900,12 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
     n->best = n->dalloc<double>(M);
     n->has = n->dalloc<char>(M);
     n->ctr = n->dalloc<Counters>(1);
+    n->gen_n = n->dalloc<int>(T);
+    n->gen_pos = n->dalloc<int>((size_t)n->pofs[nl]);
+    n->gen_l = n->dalloc<int>(nl);
+    ck(cudaMemset(n->gen_n, 0, T * sizeof(int)), "memset");
+    ck(cudaMemset(n->gen_pos, 0, (size_t)n->pofs[nl] * sizeof(int)), "memset");
+    ck(cudaMemset(n->gen_l, 0, nl * sizeof(int)), "memset");
     ck(cudaMallocHost(&n->h_int, 64 + (size_t)n->n_out), "pinned");
     n->timing = true;
   });

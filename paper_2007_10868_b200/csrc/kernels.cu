@@ -87,63 +87,162 @@ __device__ __forceinline__ void affine_finish(long long j, double lo, double hi,
   if (relax) store_relax(relax, j, y);
 }
 
-// Dense layer: one thread per output neuron, both tracks (5 independent
-// chains for ILP); inputs streamed through shared memory in ascending order.
-constexpr int kFwdTile = 512;
+// Dirty tracking for the refresh after each pass (analyzer.hpp:232-239). A
+// refresh is a pure function of predecessor bounds, so a neuron whose inputs
+// did not change in this round keeps bit-identical bounds, dev and
+// relaxation; it is skipped. gen_n / gen_pos / gen_l record the round in
+// which a neuron / grid position / layer last changed (changed = any of the
+// four bound bit patterns differs). force: recompute everything (initial
+// forward pass).
+struct Dirty {
+  int* gen_n;    // per neuron (all layers, layer offsets)
+  int* gen_pos;  // per grid position (all layers, position offsets)
+  int* gen_l;    // per layer
+  int g;
+  int force;
+};
 
-template <bool FAST>
-__device__ __forceinline__ bool fwd_dense_chain(const LayerDev& L, int j, int n_out, int n_in,
-                                                const double* xlo, const double* xhi,
-                                                const double* xrlo, const double* xrhi,
-                                                double& lo, double& hi, double& ab, double& rlo,
-                                                double& rhi, long long& terms) {
-  const double bias = L.bias[j];
-  lo = hi = rlo = rhi = bias;
-  ab = fabs(bias);
-  terms = 1;
-  bool bad = false;
-  for (int t = 0; t < n_in; ++t)
-    affine_term<FAST>(L.WT[(size_t)t * n_out + j], xlo[t], xhi[t], xrlo[t], xrhi[t], lo, hi, ab,
-                      rlo, rhi, terms, bad);
-  return bad;
+__device__ __forceinline__ bool bits_differ(double a, double b) {
+  return __double_as_longlong(a) != __double_as_longlong(b);
 }
 
-__global__ void __launch_bounds__(128)
-    k_fwd_dense(LayerDev L, const double* xlo, const double* xhi, const double* xrlo,
+__device__ __forceinline__ void mark_changed(const Dirty& dt, long long neuron, long long pos,
+                                             int layer) {
+  dt.gen_n[neuron] = dt.g;
+  if (pos >= 0) dt.gen_pos[pos] = dt.g;
+  dt.gen_l[layer] = dt.g;
+}
+
+// Store one refreshed neuron; mark it if any track changed.
+__device__ __forceinline__ void store_bounds(double* ylo, double* yhi, double* yrlo, double* yrhi,
+                                             long long j, const Iv& y, double rl, double rh,
+                                             const Dirty& dt, long long gofs, long long pos,
+                                             int layer) {
+  const bool ch = dt.force || bits_differ(ylo[j], y.lo) || bits_differ(yhi[j], y.hi) ||
+                  bits_differ(yrlo[j], rl) || bits_differ(yrhi[j], rh);
+  ylo[j] = y.lo;
+  yhi[j] = y.hi;
+  yrlo[j] = rl;
+  yrhi[j] = rh;
+  if (ch) mark_changed(dt, gofs + j, pos, layer);
+}
+
+// Dense layer. Block = 32 neurons x 2 tracks (warp 0: padded lo/hi/abs,
+// warp 1: raw lo/hi); weights and inputs staged through shared memory in
+// ascending input tiles.
+constexpr int kFDN = 32, kFDT = 64;
+
+template <bool FAST>
+__device__ __forceinline__ void pad_term(double w, double a, double b, double m, double& lo,
+                                         double& hi, double& ab, long long& terms, bool& bad) {
+  const bool nz = w != 0.0, pos = w > 0.0;
+  const double x1 = pos ? a : b, x2 = pos ? b : a;
+  if (FAST) {
+    const double pl = f_mul_dn(w, x1, bad), ph = f_mul_up(w, x2, bad);
+    const double pa = f_mul_up(fabs(w), m, bad);
+    const double n_lo = f_add_dn(lo, pl), n_hi = f_add_up(hi, ph), n_ab = f_add_up(ab, pa);
+    lo = nz ? n_lo : lo;
+    hi = nz ? n_hi : hi;
+    ab = nz ? n_ab : ab;
+    terms += nz;
+  } else {
+    if (!nz) return;
+    ++terms;
+    ab = add_up(ab, mul_up(fabs(w), m));
+    lo = add_down(lo, mul_down(w, x1));
+    hi = add_up(hi, mul_up(w, x2));
+  }
+}
+
+template <bool FAST>
+__device__ __forceinline__ void raw_term(double w, double a, double b, double& lo, double& hi,
+                                         bool& bad) {
+  const bool nz = w != 0.0, pos = w > 0.0;
+  const double x1 = pos ? a : b, x2 = pos ? b : a;
+  if (FAST) {
+    const double pl = f_mul_dn(w, x1, bad), ph = f_mul_up(w, x2, bad);
+    const double n_lo = f_add_dn(lo, pl), n_hi = f_add_up(hi, ph);
+    lo = nz ? n_lo : lo;
+    hi = nz ? n_hi : hi;
+  } else {
+    if (!nz) return;
+    lo = add_down(lo, mul_down(w, x1));
+    hi = add_up(hi, mul_up(w, x2));
+  }
+}
+
+__global__ void __launch_bounds__(2 * kFDN)
+    k_fwd_dense(LayerDev L, int layer, const double* xlo, const double* xhi, const double* xrlo,
                 const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi,
-                double* dev, double* relax) {
-  __shared__ double s_x[4][kFwdTile];
+                double* dev, double* relax, Dirty dt, long long gofs) {
+  if (!dt.force && dt.gen_l[L.pred0] != dt.g) return;  // no input changed this round
+  __shared__ double s_w[kFDT][kFDN];
+  __shared__ double s_x[5][kFDT];  // padded lo, hi, mag; raw lo, hi
   const int n_out = L.out_c;
   const int n_in = L.in_w * L.in_h * L.in_c;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, track = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * kFDN, j = j0 + lane;
   const bool act = j < n_out;
   const double bias = act ? L.bias[j] : 0.0;
-  double lo = bias, hi = bias, rlo = bias, rhi = bias, ab = fabs(bias);
+  double lo = bias, hi = bias, ab = fabs(bias);
   long long terms = 1;
   bool bad = false;
-  for (int t0 = 0; t0 < n_in; t0 += kFwdTile) {
-    const int tn = min(kFwdTile, n_in - t0);
+  for (int t0 = 0; t0 < n_in; t0 += kFDT) {
+    const int tn = min(kFDT, n_in - t0);
     __syncthreads();
-    for (int e = threadIdx.x; e < tn; e += blockDim.x) {
-      s_x[0][e] = xlo[t0 + e];
-      s_x[1][e] = xhi[t0 + e];
-      s_x[2][e] = xrlo[t0 + e];
-      s_x[3][e] = xrhi[t0 + e];
+    for (int e = threadIdx.x; e < kFDT * kFDN; e += 2 * kFDN) {
+      const int tt = e / kFDN, jj = e % kFDN;
+      s_w[tt][jj] = (tt < tn && j0 + jj < n_out) ? L.WT[(size_t)(t0 + tt) * n_out + j0 + jj] : 0.0;
+    }
+    for (int e = threadIdx.x; e < tn; e += 2 * kFDN) {
+      const double a = xlo[t0 + e], b = xhi[t0 + e];
+      s_x[0][e] = a;
+      s_x[1][e] = b;
+      s_x[2][e] = smax(fabs(a), fabs(b));
+      s_x[3][e] = xrlo[t0 + e];
+      s_x[4][e] = xrhi[t0 + e];
     }
     __syncthreads();
-    if (act) {
-      const double* wp = L.WT + (size_t)t0 * n_out + j;
+    if (track == 0) {
 #pragma unroll 4
       for (int t = 0; t < tn; ++t)
-        affine_term<true>(wp[(size_t)t * n_out], s_x[0][t], s_x[1][t], s_x[2][t], s_x[3][t], lo,
-                          hi, ab, rlo, rhi, terms, bad);
+        pad_term<true>(s_w[t][lane], s_x[0][t], s_x[1][t], s_x[2][t], lo, hi, ab, terms, bad);
+    } else {
+#pragma unroll 4
+      for (int t = 0; t < tn; ++t) raw_term<true>(s_w[t][lane], s_x[3][t], s_x[4][t], lo, hi, bad);
     }
   }
-  if (!act) return;
-  if (bad)  // out-of-band operand somewhere: redo this neuron with the exact ops
-    fwd_dense_chain<false>(L, j, n_out, n_in, xlo, xhi, xrlo, xrhi, lo, hi, ab, rlo, rhi, terms);
-  affine_finish(j, lo, hi, ab, terms, (long long)n_in + 1, rlo, rhi, ylo, yhi, yrlo, yrhi, dev,
-                relax);
+  if (act && bad) {  // out-of-band operand: redo this chain with the exact ops
+    lo = hi = bias;
+    ab = fabs(bias);
+    terms = 1;
+    for (int t = 0; t < n_in; ++t) {
+      const double w = L.WT[(size_t)t * n_out + j];
+      if (track == 0)
+        pad_term<false>(w, xlo[t], xhi[t], smax(fabs(xlo[t]), fabs(xhi[t])), lo, hi, ab, terms, bad);
+      else
+        raw_term<false>(w, xrlo[t], xrhi[t], lo, hi, bad);
+    }
+  }
+  // exchange: padded warp needs the raw result of its neuron and vice versa
+  __shared__ double s_raw[2][kFDN];
+  if (track == 1) {
+    s_raw[0][lane] = lo;
+    s_raw[1][lane] = hi;
+  }
+  __syncthreads();
+  if (track != 0 || !act) return;
+  const double slack = __dmul_rn(__dmul_rn(2.0, (double)(terms + 1)), ulp_above(ab));
+  const Iv y{add_down(lo, -slack), add_up(hi, slack)};
+  const bool ch = dt.force || bits_differ(ylo[j], y.lo) || bits_differ(yhi[j], y.hi) ||
+                  bits_differ(yrlo[j], s_raw[0][lane]) || bits_differ(yrhi[j], s_raw[1][lane]);
+  ylo[j] = y.lo;
+  yhi[j] = y.hi;
+  yrlo[j] = s_raw[0][lane];
+  yrhi[j] = s_raw[1][lane];
+  dev[j] = __dmul_rn(__dmul_rn(2.0, (double)(n_in + 2)), ulp_above(ab));  // analyzer.hpp:109
+  if (relax) store_relax(relax, j, y);
+  if (ch) mark_changed(dt, gofs + j, -1, layer);
 }
 
 // Conv layer: one thread per output neuron (h, w, d), both tracks; taps in
@@ -180,45 +279,70 @@ __device__ __forceinline__ bool fwd_conv_chain(const LayerDev& L, int h, int w, 
 }
 
 __global__ void __launch_bounds__(128)
-    k_fwd_conv(LayerDev L, const double* xlo, const double* xhi, const double* xrlo,
+    k_fwd_conv(LayerDev L, int layer, const double* xlo, const double* xhi, const double* xrlo,
                const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi,
-               double* dev, double* relax) {
+               double* dev, double* relax, Dirty dt, long long gofs, long long pofs_in,
+               long long pofs_out) {
+  if (!dt.force && dt.gen_l[L.pred0] != dt.g) return;
   const long long numel = (long long)L.out_w * L.out_h * L.out_c;
   const long long jj = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (jj >= numel) return;
   const int d = (int)(jj % L.out_c);
   const int w = (int)((jj / L.out_c) % L.out_w);
   const int h = (int)(jj / ((long long)L.out_c * L.out_w));
+  if (!dt.force) {  // any input position of the receptive field changed this round?
+    bool any = false;
+    for (int fy = 0; fy < L.fh && !any; ++fy) {
+      const int iy = h * L.sh - L.ph + fy;
+      if (iy < 0 || iy >= L.in_h) continue;
+      for (int fx = 0; fx < L.fw; ++fx) {
+        const int ix = w * L.sw - L.pw + fx;
+        if (ix < 0 || ix >= L.in_w) continue;
+        if (dt.gen_pos[pofs_in + (long long)iy * L.in_w + ix] == dt.g) {
+          any = true;
+          break;
+        }
+      }
+    }
+    if (!any) return;
+  }
   double lo, hi, ab, rlo, rhi;
   long long terms, dterms;
   if (fwd_conv_chain<true>(L, h, w, d, xlo, xhi, xrlo, xrhi, lo, hi, ab, rlo, rhi, terms, dterms))
     fwd_conv_chain<false>(L, h, w, d, xlo, xhi, xrlo, xrhi, lo, hi, ab, rlo, rhi, terms, dterms);
-  affine_finish(jj, lo, hi, ab, terms, dterms, rlo, rhi, ylo, yhi, yrlo, yrhi, dev, relax);
+  const double slack = __dmul_rn(__dmul_rn(2.0, (double)(terms + 1)), ulp_above(ab));
+  const Iv y{add_down(lo, -slack), add_up(hi, slack)};
+  store_bounds(ylo, yhi, yrlo, yrhi, jj, y, rlo, rhi, dt, gofs, pofs_out + (long long)h * L.out_w + w,
+               layer);
+  dev[jj] = __dmul_rn(__dmul_rn(2.0, (double)(dterms + 1)), ulp_above(ab));  // analyzer.hpp:140
+  if (relax) store_relax(relax, jj, y);
 }
 
-__global__ void k_fwd_relu(long long n, const double* xlo, const double* xhi, const double* xrlo,
-                           const double* xrhi, double* ylo, double* yhi, double* yrlo,
-                           double* yrhi) {
+__global__ void k_fwd_relu(long long n, int C, int layer, const double* xlo, const double* xhi,
+                           const double* xrlo, const double* xrhi, double* ylo, double* yhi,
+                           double* yrlo, double* yrhi, Dirty dt, long long gofs_in, long long gofs,
+                           long long pofs_out) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  ylo[i] = xlo[i] > 0.0 ? xlo[i] : 0.0;  // eval.hpp:210-217
-  yhi[i] = xhi[i] > 0.0 ? xhi[i] : 0.0;
-  yrlo[i] = xrlo[i] > 0.0 ? xrlo[i] : 0.0;
-  yrhi[i] = xrhi[i] > 0.0 ? xrhi[i] : 0.0;
+  if (!dt.force && dt.gen_n[gofs_in + i] != dt.g) return;
+  const Iv y{xlo[i] > 0.0 ? xlo[i] : 0.0, xhi[i] > 0.0 ? xhi[i] : 0.0};  // eval.hpp:210-217
+  store_bounds(ylo, yhi, yrlo, yrhi, i, y, xrlo[i] > 0.0 ? xrlo[i] : 0.0,
+               xrhi[i] > 0.0 ? xrhi[i] : 0.0, dt, gofs, pofs_out + i / C, layer);
 }
 
-__global__ void k_fwd_join(long long n, const double* alo, const double* ahi, const double* arlo,
-                           const double* arhi, const double* blo, const double* bhi,
-                           const double* brlo, const double* brhi, double* ylo, double* yhi,
-                           double* yrlo, double* yrhi, double* dev, double* relax) {
+__global__ void k_fwd_join(long long n, int C, int layer, const double* alo, const double* ahi,
+                           const double* arlo, const double* arhi, const double* blo,
+                           const double* bhi, const double* brlo, const double* brhi, double* ylo,
+                           double* yhi, double* yrlo, double* yrhi, double* dev, double* relax,
+                           Dirty dt, long long gofs_a, long long gofs_b, long long gofs,
+                           long long pofs_out) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (!dt.force && dt.gen_n[gofs_a + i] != dt.g && dt.gen_n[gofs_b + i] != dt.g) return;
   const Iv a{alo[i], ahi[i]}, b{blo[i], bhi[i]};
   const Iv y = iv_add(a, b);  // eval.hpp:219-223
-  ylo[i] = y.lo;
-  yhi[i] = y.hi;
-  yrlo[i] = add_down(arlo[i], brlo[i]);
-  yrhi[i] = add_up(arhi[i], brhi[i]);
+  store_bounds(ylo, yhi, yrlo, yrhi, i, y, add_down(arlo[i], brlo[i]), add_up(arhi[i], brhi[i]),
+               dt, gofs, pofs_out + i / C, layer);
   dev[i] = __dmul_rn(2.0, ulp_above(add_up(iv_mag(a), iv_mag(b))));  // analyzer.hpp:144-150
   if (relax) store_relax(relax, i, y);
 }
@@ -231,8 +355,9 @@ __global__ void k_relax(long long n, const double* blo, const double* bhi, doubl
 
 void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, const double* blo,
                           const double* bhi, const double* rlo, const double* rhi,
-                          const long long* offs, int k, int p0, int p1, double* dev,
-                          double* relax) {
+                          const long long* offs, const long long* pofs, int k, int p0, int p1,
+                          double* dev, double* relax, int* gen_n, int* gen_pos, int* gen_l, int g,
+                          int force) {
   const long long o = offs[k], a = offs[p0];
   double* ylo = const_cast<double*>(blo) + o;
   double* yhi = const_cast<double*>(bhi) + o;
@@ -240,24 +365,25 @@ void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, con
   double* yrhi = const_cast<double*>(rhi) + o;
   double* rx = feeds_relu ? relax + 8 * o : nullptr;
   const long long n = (long long)L.out_w * L.out_h * L.out_c;
+  const Dirty dt{gen_n, gen_pos, gen_l, g, force};
   switch (L.kind) {
     case KIND_DENSE:
-      k_fwd_dense<<<cdiv(n, 32), 32, 0, s>>>(L, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
-                                                   yrlo, yrhi, dev + o, rx);
+      k_fwd_dense<<<cdiv(n, kFDN), 2 * kFDN, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo,
+                                                     yhi, yrlo, yrhi, dev + o, rx, dt, o);
       break;
     case KIND_CONV:
-      k_fwd_conv<<<cdiv(n, 64), 64, 0, s>>>(L, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
-                                                  yrlo, yrhi, dev + o, rx);
+      k_fwd_conv<<<cdiv(n, 64), 64, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi, yrlo,
+                                            yrhi, dev + o, rx, dt, o, pofs[p0], pofs[k]);
       break;
     case KIND_RELU:
-      k_fwd_relu<<<cdiv(n, 256), 256, 0, s>>>(n, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
-                                              yrlo, yrhi);
+      k_fwd_relu<<<cdiv(n, 256), 256, 0, s>>>(n, L.out_c, k, blo + a, bhi + a, rlo + a, rhi + a,
+                                              ylo, yhi, yrlo, yrhi, dt, a, o, pofs[k]);
       break;
     case KIND_JOIN: {
       const long long b = offs[p1];
-      k_fwd_join<<<cdiv(n, 256), 256, 0, s>>>(n, blo + a, bhi + a, rlo + a, rhi + a, blo + b,
-                                              bhi + b, rlo + b, rhi + b, ylo, yhi, yrlo, yrhi,
-                                              dev + o, rx);
+      k_fwd_join<<<cdiv(n, 256), 256, 0, s>>>(n, L.out_c, k, blo + a, bhi + a, rlo + a, rhi + a,
+                                              blo + b, bhi + b, rlo + b, rhi + b, ylo, yhi, yrlo,
+                                              yrhi, dev + o, rx, dt, a, b, o, pofs[k]);
       break;
     }
     default:
@@ -324,22 +450,30 @@ void launch_seed(cudaStream_t s, int n, const double* blo, const double* bhi, co
 }
 
 // Write the best candidates back (backsub.hpp:1060-1064) and refresh the
-// relaxation of the refined layer (analyzer.hpp:229-231).
-__global__ void k_writeback(int n, const double* cand, double* blo, double* bhi, double* rlo,
-                            double* rhi, double* relax) {
+// relaxation of the refined layer (analyzer.hpp:229-231); mark changed
+// neurons for the refresh round g.
+__global__ void k_writeback(int n, int C, int layer, const double* cand, double* blo, double* bhi,
+                            double* rlo, double* rhi, double* relax, Dirty dt, long long gofs,
+                            long long pofs) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const Iv b{cand[4 * q + 0], cand[4 * q + 1]};
+  const bool ch = bits_differ(blo[q], b.lo) || bits_differ(bhi[q], b.hi) ||
+                  bits_differ(rlo[q], cand[4 * q + 2]) || bits_differ(rhi[q], cand[4 * q + 3]);
   blo[q] = b.lo;
   bhi[q] = b.hi;
   rlo[q] = cand[4 * q + 2];
   rhi[q] = cand[4 * q + 3];
   if (relax) store_relax(relax, q, b);
+  if (ch) mark_changed(dt, gofs + q, pofs + q / C, layer);
 }
 
-void launch_writeback(cudaStream_t s, int n, const double* cand, double* blo, double* bhi,
-                      double* rlo, double* rhi, double* relax) {
-  k_writeback<<<cdiv(n, 256), 256, 0, s>>>(n, cand, blo, bhi, rlo, rhi, relax);
+void launch_writeback(cudaStream_t s, int n, int C, int layer, const double* cand, double* blo,
+                      double* bhi, double* rlo, double* rhi, double* relax, int* gen_n,
+                      int* gen_pos, int* gen_l, int g, long long gofs, long long pofs) {
+  const Dirty dt{gen_n, gen_pos, gen_l, g, 0};
+  k_writeback<<<cdiv(n, 256), 256, 0, s>>>(n, C, layer, cand, blo, bhi, rlo, rhi, relax, dt, gofs,
+                                           pofs);
   ++g_launches;
 }
 

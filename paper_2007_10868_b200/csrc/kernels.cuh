@@ -88,18 +88,21 @@ struct Counters {  // device-side PassStats accumulators
 };
 
 // ----- launchers (kernels.cu) -----
-void launch_forward_layer(cudaStream_t s, const LayerDev& L, int k_is_relu_input,
-                          const double* blo, const double* bhi, const double* rlo,
-                          const double* rhi,            // base pointers of all-layer arrays
-                          const long long* offs,         // host offsets per layer
-                          int k, int pred0, int pred1, double* dev, double* relax);
+// Forward bounds of layer k (padded + raw + dev + relaxation), skipping
+// neurons whose inputs did not change in refresh round g (force: all).
+void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, const double* blo,
+                          const double* bhi, const double* rlo, const double* rhi,
+                          const long long* offs, const long long* pofs, int k, int pred0,
+                          int pred1, double* dev, double* relax, int* gen_n, int* gen_pos,
+                          int* gen_l, int g, int force);
 void launch_relax(cudaStream_t s, const double* blo, const double* bhi, long long n, double* relax);
 
 void launch_seed(cudaStream_t s, int n, const double* blo, const double* bhi, const double* rlo,
                  const double* rhi, int allow_freeze, int early_term, double* cand, char* frozen,
                  int* live, int* n_live, unsigned long long* n_prefrozen);
-void launch_writeback(cudaStream_t s, int n, const double* cand, double* blo, double* bhi,
-                      double* rlo, double* rhi, double* relax);
+void launch_writeback(cudaStream_t s, int n, int C, int layer, const double* cand, double* blo,
+                      double* bhi, double* rlo, double* rhi, double* relax, int* gen_n,
+                      int* gen_pos, int* gen_l, int g, long long gofs, long long pofs);
 
 void launch_init_affine(cudaStream_t s, const LayerDev& Q, const RowsDev& rows, const FrameDev& f,
                         const double* dev_q, MatDev out);
