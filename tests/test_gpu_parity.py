@@ -117,3 +117,18 @@ def test_gain_scaled_mlp(pc, port):
     X = pc.random_inputs(8, 2, 784)
     for x in X:
         run_case(pc, port, net, x, 0.012, label=0)
+
+
+@pytest.mark.parametrize("name,n_img", [("mnist_6x100", 3), ("mnist_9x500", 1), ("cifar_convbig", 1)])
+def test_baseline_configs(pc, port, name, n_img):
+    """BASELINE.json configs: generator weights seed 7, inputs seed 8,
+    label = candidate of the concrete forward pass; verdicts, margins, bounds, stats."""
+    from paper_2007_10868_b200.configs import CONFIGS, INPUT_SEED, MODEL_SEED
+    arch, eps_s = CONFIGS[name]
+    net = pc.generate(MODEL_SEED, arch)
+    X = pc.random_inputs(INPUT_SEED, n_img, int(np.prod(net.input_shape)))
+    v = pc.Verifier(net)
+    for x in X:
+        lab = v.candidate(x)
+        assert lab >= 0
+        run_case(pc, port, net, x, float(eps_s), label=lab)
