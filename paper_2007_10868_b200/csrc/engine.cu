@@ -82,7 +82,15 @@ struct Mat {
   double* K = nullptr;
   long long cells = 0;
   Frame f;
+  const int* src = nullptr;  // row map after a compaction (see MatDev::src)
+  int phys = 0;              // physical rows in the buffers
 };
+
+MatDev md(const Mat& m) {
+  MatDev d{m.lo, m.hi, m.K, m.cells};
+  d.src = m.src;
+  return d;
+}
 
 }  // namespace
 
@@ -298,7 +306,7 @@ struct Walker {
   cudaStream_t s;
   int q;             // query layer
   bool dry = false;  // geometry dry run: count bytes per row only
-  size_t dry_bytes = 0, dry_peak = 0;
+  size_t dry_bytes = 0, dry_peak = 0, dry_allocs = 0;
   int R = 0;         // rows per polarity
   bool both = true;  // upper + lower rows (false: margin pass, lower only)
   int rq = 0;        // which row_q buffer is current
@@ -314,6 +322,7 @@ struct Walker {
     if (dry) {
       dry_bytes += bytes;
       dry_peak = std::max(dry_peak, dry_bytes);
+      ++dry_allocs;
       return nullptr;
     }
     if (n->arena_used + bytes > n->arena_cap)
@@ -323,24 +332,36 @@ struct Walker {
     return p;
   }
 
+  int alloc_rows() const { return dry ? (both ? 2 : 1) : nrows(); }
+
   Mat alloc(const Frame& f, bool withK) {
     Mat m;
     m.f = f;
     m.cells = frame_cells(fdev(n, f, q));
-    const int rows = dry ? 1 : nrows();
-    m.lo = arena_take((size_t)rows * m.cells * sizeof(double));
-    m.hi = arena_take((size_t)rows * m.cells * sizeof(double));
-    if (withK) m.K = arena_take((size_t)rows * 4 * sizeof(double));
+    m.phys = alloc_rows();
+    m.lo = arena_take((size_t)m.phys * m.cells * sizeof(double));
+    m.hi = arena_take((size_t)m.phys * m.cells * sizeof(double));
+    if (withK) m.K = arena_take((size_t)m.phys * 4 * sizeof(double));
     return m;
+  }
+
+  // Constants of the next step's output: in place when m is compact,
+  // otherwise a fresh compact array (the chain reads m.K through m.src).
+  double* k_out(const Mat& m) {
+    if (dry) {
+      arena_take((size_t)alloc_rows() * 4 * sizeof(double));
+      return nullptr;
+    }
+    return m.src ? arena_take((size_t)nrows() * 4 * sizeof(double)) : m.K;
   }
 
   void dense_step(Mat& m) {  // backsub.hpp:343-399
     const HostLayer& L = n->L[m.f.layer];
     Mat out = alloc(dense_frame(L.pred0), false);
-    out.K = m.K;
+    out.K = k_out(m);
     if (!dry) {
-      launch_chain_affine(s, L.d, false, rows(), fdev(n, m.f, q), MatDev{m.lo, m.hi, m.K, m.cells},
-                          n->dev + n->off[m.f.layer], n->ctr, 1);
+      launch_chain_affine(s, L.d, false, rows(), fdev(n, m.f, q), md(m), out.K,
+                          n->dev + n->off[m.f.layer], n->ctr);
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (n->timing) {
         while (n->ev_pool.size() < n->ev_used + 2) {
@@ -354,8 +375,7 @@ struct Walker {
         g_dense_bytes += 16.0 * nrows() * (double)(m.cells + out.cells) + 8.0 * m.cells * out.cells;
         ++g_dense_launches;
       }
-      launch_dense_coef(s, L.d, nrows(), MatDev{m.lo, m.hi, m.K, m.cells},
-                        MatDev{out.lo, out.hi, out.K, out.cells}, e0, e1);
+      launch_dense_coef(s, L.d, nrows(), md(m), md(out), e0, e1);
     }
     m = out;
   }
@@ -374,13 +394,12 @@ struct Walker {
       nf.Ah = m.f.Ah * L.sh - L.ph;
     }
     Mat out = alloc(nf, false);
-    out.K = m.K;
+    out.K = k_out(m);
     if (!dry) {
       const FrameDev fi = fdev(n, m.f, q), fo = fdev(n, nf, q);
-      launch_chain_affine(s, L.d, true, rows(), fi, MatDev{m.lo, m.hi, m.K, m.cells},
-                          n->dev + n->off[m.f.layer], n->ctr, 1);
-      launch_gbc_coef(s, L.d, rows(), fi, fo, MatDev{m.lo, m.hi, m.K, m.cells},
-                      MatDev{out.lo, out.hi, out.K, out.cells});
+      launch_chain_affine(s, L.d, true, rows(), fi, md(m), out.K, n->dev + n->off[m.f.layer],
+                          n->ctr);
+      launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out));
       st->gbc_dense_equiv += (long long)nrows() * L.numel() * L.in_numel();
     }
     m = out;
@@ -391,25 +410,24 @@ struct Walker {
     Frame nf = m.f;
     nf.layer = L.pred0;
     Mat out = alloc(nf, false);
-    out.K = m.K;
+    out.K = k_out(m);
     if (!dry) {
       const FrameDev f = fdev(n, m.f, q);
       const double* rx = n->relax + 8 * n->off[L.pred0];
-      launch_chain_relu(s, rows(), f, MatDev{m.lo, m.hi, m.K, m.cells}, rx);
-      launch_relu_coef(s, rows(), f, MatDev{m.lo, m.hi, m.K, m.cells},
-                       MatDev{out.lo, out.hi, out.K, out.cells}, rx);
+      launch_chain_relu(s, rows(), f, md(m), out.K, rx);
+      launch_relu_coef(s, rows(), f, md(m), md(out), rx);
     }
     m = out;
   }
 
   void join_step(Mat& m) {  // backsub.hpp:694-715
     const HostLayer& L = n->L[m.f.layer];
-    Mat a = m, b = m;
+    Mat a = m, b = m;  // both branches read m's rows (steps never write their input)
     a.f.layer = L.pred0;
     b.f.layer = L.pred1;
-    b.K = arena_take((size_t)(dry ? 1 : nrows()) * 4 * sizeof(double));
-    if (!dry) ck(cudaMemsetAsync(b.K, 0, (size_t)nrows() * 4 * sizeof(double), s), "memset");
-    const bool a_was_dense = m.f.dense;
+    // branch b starts from zero constants, laid out like m's rows
+    b.K = arena_take((size_t)(dry ? alloc_rows() : m.phys) * 4 * sizeof(double));
+    if (!dry) ck(cudaMemsetAsync(b.K, 0, (size_t)m.phys * 4 * sizeof(double), s), "memset");
     walk(a, L.head, false);
     walk(b, L.head, false);
     // align_add (backsub.hpp:610-688): union frame
@@ -429,12 +447,10 @@ struct Walker {
       u.Ww = std::max(a.f.Aw + a.f.Ww, b.f.Aw + b.f.Ww) - u.Aw;
       u.Wh = std::max(a.f.Ah + a.f.Wh, b.f.Ah + b.f.Wh) - u.Ah;
     }
-    (void)a_was_dense;
     Mat out = alloc(u, true);
     if (!dry)
-      launch_merge(s, rows(), fdev(n, a.f, q), fdev(n, b.f, q), fdev(n, u, q), dense_path,
-                   MatDev{a.lo, a.hi, a.K, a.cells}, MatDev{b.lo, b.hi, b.K, b.cells},
-                   MatDev{out.lo, out.hi, out.K, out.cells});
+      launch_merge(s, rows(), fdev(n, a.f, q), fdev(n, b.f, q), fdev(n, u, q), dense_path, md(a),
+                   md(b), md(out));
     m = out;
   }
 
@@ -446,13 +462,13 @@ struct Walker {
     const int fl = m.f.layer;
     const long long o = n->off[fl];
     if (margin) {
-      launch_concretize(s, rows(), fdev(n, m.f, q), MatDev{m.lo, m.hi, m.K, m.cells}, n->blo + o,
-                        n->bhi + o, n->blo + o, n->bhi + o, n->vals, n->rvals);
+      launch_concretize(s, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->blo + o,
+                        n->bhi + o, n->vals, n->rvals);
       launch_margin_offer(s, R, n->vals, n->best, n->has);
       return;
     }
-    launch_concretize(s, rows(), fdev(n, m.f, q), MatDev{m.lo, m.hi, m.K, m.cells}, n->blo + o,
-                      n->bhi + o, n->rlo + o, n->rhi + o, n->vals, n->rvals);
+    launch_concretize(s, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
+                      n->rhi + o, n->vals, n->rvals);
     int* new_q = n->rowq[rq ^ 1];
     launch_offer(s, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
                  early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr);
@@ -461,16 +477,9 @@ struct Walker {
     ck(cudaStreamSynchronize(s), "sync");
     const int newR = n->h_int[1];
     if (newR == R) return;
-    // compact_rows on both polarities (backsub.hpp:820-845)
-    Mat c = m;
-    if (newR > 0) {
-      c.lo = arena_take((size_t)2 * newR * m.cells * sizeof(double));
-      c.hi = arena_take((size_t)2 * newR * m.cells * sizeof(double));
-      c.K = arena_take((size_t)2 * newR * 4 * sizeof(double));
-      launch_gather_rows(s, MatDev{m.lo, m.hi, m.K, m.cells}, MatDev{c.lo, c.hi, c.K, c.cells},
-                         n->perm, newR, R, 1);
-    }
-    m = c;
+    // compact_rows on both polarities (backsub.hpp:820-845): the surviving
+    // rows stay in place; the next step reads them through the row map.
+    m.src = n->perm;
     R = newR;
     rq ^= 1;
     row_q = n->rowq[rq];
@@ -530,17 +539,22 @@ Frame initial_frame(const pc_net* n, int t, bool affine) {
   return f;
 }
 
-// Bytes of workspace one row (both polarities) needs for pass t.
-size_t bytes_per_row(pc_net* n, int t, bool affine) {
+// Workspace of pass t: bytes per query row (both polarities; the arena is a
+// bump allocator reset per chunk, so this is the walk's total) and the number
+// of allocations (each may round up by < 256 B).
+struct WalkSize {
+  size_t per_row, allocs;
+};
+
+WalkSize walk_size(pc_net* n, int t, bool affine, bool both) {
   Walker w{n, nullptr, t};
   w.dry = true;
-  w.both = true;
+  w.both = both;
   pc_stats dummy{};
   w.st = &dummy;
   Mat m = w.alloc(initial_frame(n, t, affine), true);
   w.walk(m, 0, false);
-  // the compaction copy may coexist with everything else
-  return 2 * w.dry_peak + 4096;
+  return WalkSize{w.dry_peak, w.dry_allocs};
 }
 
 void ensure_arena(pc_net* n, size_t bytes) {
@@ -571,12 +585,12 @@ void run_pass(pc_net* n, int t, bool allow_freeze, pc_stats* st) {
   st->rows_total += N;
   const bool affine = Q.kind == KIND_DENSE || Q.kind == KIND_CONV;
   if (n_live > 0) {
-    const size_t per_row = bytes_per_row(n, t, affine);
+    const WalkSize ws = walk_size(n, t, affine, true);
     long long chunk = n->opt.chunk_rows > 0
                           ? n->opt.chunk_rows
-                          : std::max<long long>(1, budget_of(n) / (long long)per_row);
+                          : std::max<long long>(1, budget_of(n) / (long long)ws.per_row);
     chunk = std::min<long long>(chunk, n_live);
-    ensure_arena(n, per_row * (size_t)chunk + (1 << 20));
+    ensure_arena(n, ws.per_row * (size_t)chunk + 256 * ws.allocs + (1 << 20));
     for (long long base = 0; base < n_live; base += chunk) {
       const int R = (int)std::min<long long>(chunk, n_live - base);
       n->arena_used = 0;
@@ -619,8 +633,8 @@ void run_margin(pc_net* n, int label, pc_stats* st, double* margins_host) {
     if (j != label) cls.push_back(j);
   ck(cudaMemcpyAsync(n->rowq[0], cls.data(), sizeof(int) * nr, cudaMemcpyHostToDevice, s), "h2d");
   ck(cudaMemsetAsync(n->has, 0, nr, s), "memset");
-  const size_t per_row = bytes_per_row(n, out, false);
-  ensure_arena(n, per_row * (size_t)nr + (1 << 20));
+  const WalkSize ws = walk_size(n, out, false, false);
+  ensure_arena(n, ws.per_row * (size_t)nr + 256 * ws.allocs + (1 << 20));
   n->arena_used = 0;
   Walker w{n, s, out};
   w.R = nr;
@@ -893,7 +907,7 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
     n->live = n->dalloc<int>(M);
     n->rowq[0] = n->dalloc<int>(M);
     n->rowq[1] = n->dalloc<int>(M);
-    n->perm = n->dalloc<int>(M);
+    n->perm = n->dalloc<int>(2 * M);
     n->d_int = n->dalloc<int>(8);
     n->vals = n->dalloc<double>(2 * M);
     n->rvals = n->dalloc<double>(2 * M);

@@ -673,8 +673,8 @@ __device__ __forceinline__ bool chain_affine_row(const LayerDev& L, int is_conv,
 }
 
 __global__ void __launch_bounds__(32 * kChainWarps)
-    k_chain_affine(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, const double* dev,
-                   Counters* ctr) {
+    k_chain_affine(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, double* Kout,
+                   const double* dev, Counters* ctr) {
   __shared__ double s_t[kChainWarps][3][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kChainWarps + warp;
@@ -684,10 +684,11 @@ __global__ void __launch_bounds__(32 * kChainWarps)
   int bw = 0, bh = 0;
   if (is_conv) frame_base(f, q, bw, bh);
   const long long cells = m.cells;
-  const double* lo = m.lo + (size_t)i * cells;
-  const double* hi = m.hi + (size_t)i * cells;
-  double* K = m.K + 4 * (size_t)i;
-  const double acc0 = lane < 4 ? K[lane] : 0.0;
+  const size_t pr = phys_row(m, i);
+  const double* lo = m.lo + pr * cells;
+  const double* hi = m.hi + pr * cells;
+  const double acc0 = lane < 4 ? m.K[4 * pr + lane] : 0.0;
+  double* K = Kout + 4 * (size_t)i;
   unsigned long long madds = 0;
   double acc;
   if (chain_affine_row<true>(L, is_conv, f, bw, bh, cells, lo, hi, dev, acc0, s_t[warp], lane, acc,
@@ -705,9 +706,10 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 }
 
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
-                         const FrameDev& fin, MatDev m, const double* dev, Counters* ctr, int) {
+                         const FrameDev& fin, MatDev m, double* Kout, const double* dev,
+                         Counters* ctr) {
   k_chain_affine<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(L, is_conv ? 1 : 0, rows,
-                                                                        fin, m, dev, ctr);
+                                                                        fin, m, Kout, dev, ctr);
   ++g_launches;
 }
 
@@ -766,7 +768,7 @@ __device__ __forceinline__ bool chain_relu_row(const FrameDev& f, int bw, int bh
 }
 
 __global__ void __launch_bounds__(32 * kChainWarps)
-    k_chain_relu(RowsDev rows, FrameDev f, MatDev m, const double* relax) {
+    k_chain_relu(RowsDev rows, FrameDev f, MatDev m, double* Kout, const double* relax) {
   __shared__ double s_t[kChainWarps][2][2][32];  // [slot][lo/hi][cell]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kChainWarps + warp;
@@ -776,10 +778,11 @@ __global__ void __launch_bounds__(32 * kChainWarps)
   int bw, bh;
   frame_base(f, q, bw, bh);
   const long long cells = m.cells;
-  const double* lo = m.lo + (size_t)i * cells;
-  const double* hi = m.hi + (size_t)i * cells;
-  double* K = m.K + 4 * (size_t)i;
-  const double acc0 = lane < 4 ? K[lane] : 0.0;
+  const size_t pr = phys_row(m, i);
+  const double* lo = m.lo + pr * cells;
+  const double* hi = m.hi + pr * cells;
+  const double acc0 = lane < 4 ? m.K[4 * pr + lane] : 0.0;
+  double* K = Kout + 4 * (size_t)i;
   double acc;
   if (chain_relu_row<true>(f, bw, bh, upper, cells, lo, hi, relax, acc0, s_t[warp], lane, acc))
     chain_relu_row<false>(f, bw, bh, upper, cells, lo, hi, relax, acc0, s_t[warp], lane, acc);
@@ -787,8 +790,8 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 }
 
 void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
-                       const double* relax) {
-  k_chain_relu<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, relax);
+                       double* Kout, const double* relax) {
+  k_chain_relu<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, Kout, relax);
   ++g_launches;
 }
 
@@ -848,9 +851,10 @@ __global__ void __launch_bounds__(32 * kChainWarps)
   int bw, bh;
   frame_base(f, q, bw, bh);
   const long long cells = m.cells;
-  const double* lo = m.lo + (size_t)i * cells;
-  const double* hi = m.hi + (size_t)i * cells;
-  const double* K = m.K + 4 * (size_t)i;
+  const size_t pr = phys_row(m, i);
+  const double* lo = m.lo + pr * cells;
+  const double* hi = m.hi + pr * cells;
+  const double* K = m.K + 4 * pr;
   double acc0 = 0.0;
   if (lane == 0) acc0 = upper ? K[1] : K[0];
   if (lane == 1) acc0 = upper ? K[3] : K[2];
@@ -924,8 +928,8 @@ __global__ void __launch_bounds__(kDC)
       const int rr = e / kDK, kk = e % kDK;
       const int r = r0 + rr, k = k0 + kk;
       const bool ok = r < nrows && k < n_k;
-      s_al[rr][kk] = ok ? in.lo[(size_t)r * n_k + k] : 0.0;
-      s_ah[rr][kk] = ok ? in.hi[(size_t)r * n_k + k] : 0.0;
+      s_al[rr][kk] = ok ? in.lo[phys_row(in, r) * n_k + k] : 0.0;
+      s_ah[rr][kk] = ok ? in.hi[phys_row(in, r) * n_k + k] : 0.0;
     }
     for (int kk = 0; kk < kDK; ++kk) {
       const int k = k0 + kk;
@@ -948,8 +952,8 @@ __global__ void __launch_bounds__(kDC)
     if (bad[u]) {
       lo[u] = hi[u] = 0.0;
       for (int k = 0; k < n_k; ++k)
-        madd_exact(W[(size_t)k * n_in + col], in.lo[(size_t)r * n_k + k], in.hi[(size_t)r * n_k + k],
-                   lo[u], hi[u]);
+        madd_exact(W[(size_t)k * n_in + col], in.lo[phys_row(in, r) * n_k + k],
+                   in.hi[phys_row(in, r) * n_k + k], lo[u], hi[u]);
     }
     out.lo[(size_t)r * n_in + col] = lo[u];
     out.hi[(size_t)r * n_in + col] = hi[u];
@@ -1020,8 +1024,8 @@ __global__ void __launch_bounds__(256)
   frame_base(fi, q, bw, bh);
   frame_base(fo, q, nbw, nbh);
   const long long ocells = out.cells, icells = in.cells;
-  const double* ilo = in.lo + (size_t)i * icells;
-  const double* ihi = in.hi + (size_t)i * icells;
+  const double* ilo = in.lo + phys_row(in, i) * icells;
+  const double* ihi = in.hi + phys_row(in, i) * icells;
   const int cin = L.in_c;
   for (long long o = blockIdx.x * blockDim.x + threadIdx.x; o < ocells;
        o += (long long)gridDim.x * blockDim.x) {
@@ -1074,8 +1078,8 @@ __global__ void __launch_bounds__(256)
   int bw, bh;
   frame_base(f, q, bw, bh);
   const long long cells = in.cells;
-  const double* lo = in.lo + (size_t)i * cells;
-  const double* hi = in.hi + (size_t)i * cells;
+  const double* lo = in.lo + phys_row(in, i) * cells;
+  const double* hi = in.hi + phys_row(in, i) * cells;
   for (long long cell = blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
        cell += (long long)gridDim.x * blockDim.x) {
     const Iv c{lo[cell], hi[cell]};
@@ -1133,11 +1137,11 @@ __global__ void __launch_bounds__(256)
     bool ina = aw >= abw && aw < abw + fa.S_w && ah >= abh && ah < abh + fa.S_h;
     bool inb = aw >= bbw && aw < bbw + fb.S_w && ah >= bbh && ah < bbh + fb.S_h;
     if (ina) {
-      const size_t o = (size_t)i * a.cells + ((size_t)(ah - abh) * fa.S_w + (aw - abw)) * C + cc;
+      const size_t o = phys_row(a, i) * a.cells + ((size_t)(ah - abh) * fa.S_w + (aw - abw)) * C + cc;
       ca = Iv{a.lo[o], a.hi[o]};
     }
     if (inb) {
-      const size_t o = (size_t)i * b.cells + ((size_t)(ah - bbh) * fb.S_w + (aw - bbw)) * C + cc;
+      const size_t o = phys_row(b, i) * b.cells + ((size_t)(ah - bbh) * fb.S_w + (aw - bbw)) * C + cc;
       cb = Iv{b.lo[o], b.hi[o]};
     }
     Iv n{0.0, 0.0};
@@ -1149,8 +1153,8 @@ __global__ void __launch_bounds__(256)
     out.hi[(size_t)i * cells + cell] = n.hi;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double* Ka = a.K + 4 * (size_t)i;
-    const double* Kb = b.K + 4 * (size_t)i;
+    const double* Ka = a.K + 4 * phys_row(a, i);
+    const double* Kb = b.K + 4 * phys_row(b, i);
     Iv k{Ka[0], Ka[1]}, kr{Ka[2], Ka[3]};
     iv_acc(k, Iv{Kb[0], Kb[1]});
     iv_acc(kr, Iv{Kb[2], Kb[3]});
@@ -1175,7 +1179,7 @@ void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const
 // ===========================================================================
 __global__ void __launch_bounds__(kScanThreads)
     k_offer(RowsDev rows, int R, const double* vals, const double* rvals, double* cand,
-            char* frozen, int allow_freeze, int early_term, int* perm, int* new_R,
+            char* frozen, int allow_freeze, int early_term, int* map, int* new_R,
             int* new_row_q, Counters* ctr) {
   using Scan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
@@ -1206,7 +1210,7 @@ __global__ void __launch_bounds__(kScanThreads)
     int pos, total;
     Scan(tmp).ExclusiveSum(keep, pos, total);
     if (keep) {
-      perm[s_base + pos] = r;
+      map[s_base + pos] = r;
       new_row_q[s_base + pos] = q;
     }
     __syncthreads();
@@ -1214,14 +1218,16 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
   }
   if (froze) atomicAdd(&ctr->frozen, (unsigned long long)froze);
-  if (threadIdx.x == 0) *new_R = s_base;
+  const int nR = s_base;
+  for (int p = threadIdx.x; p < nR; p += blockDim.x) map[nR + p] = R + map[p];  // lower rows
+  if (threadIdx.x == 0) *new_R = nR;
 }
 
 void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals,
                   const double* rvals, double* cand, char* frozen, int allow_freeze,
-                  int early_term, int* perm, int* new_R, int* new_row_q, Counters* ctr) {
+                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr) {
   k_offer<<<1, kScanThreads, 0, s>>>(rows, R, vals, rvals, cand, frozen, allow_freeze, early_term,
-                                     perm, new_R, new_row_q, ctr);
+                                     map, new_R, new_row_q, ctr);
   ++g_launches;
 }
 
@@ -1238,67 +1244,6 @@ __global__ void k_margin_offer(int n, const double* vals, double* best, char* ha
 void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best, char* has) {
   k_margin_offer<<<1, 128, 0, s>>>(n, vals, best, has);
   ++g_launches;
-}
-
-// Row gather for compaction: new row p <- old row perm[p] (upper block) and
-// new row R_new + p <- old row R_old + perm[p] (lower block).
-__global__ void k_gather_rows(MatDev in, MatDev out, const int* perm, int R_new, int R_old,
-                              int both) {
-  const int p = blockIdx.y;
-  const int side = blockIdx.z;
-  const int src = perm[p] + (side ? R_old : 0);
-  const int dst = p + (side ? R_new : 0);
-  const long long cells = in.cells;
-  for (long long c = blockIdx.x * blockDim.x + threadIdx.x; c < cells;
-       c += (long long)gridDim.x * blockDim.x) {
-    out.lo[(size_t)dst * cells + c] = in.lo[(size_t)src * cells + c];
-    out.hi[(size_t)dst * cells + c] = in.hi[(size_t)src * cells + c];
-  }
-  if (blockIdx.x == 0 && threadIdx.x < 4)
-    out.K[4 * (size_t)dst + threadIdx.x] = in.K[4 * (size_t)src + threadIdx.x];
-  (void)both;
-}
-
-void launch_gather_rows(cudaStream_t s, MatDev in, MatDev out, const int* perm, int R_new,
-                        int R_old, int both) {
-  if (R_new <= 0) return;
-  unsigned gx = cdiv(in.cells, 256);
-  if (gx > 256) gx = 256;
-  dim3 grid(gx, R_new, both ? 2 : 1);
-  k_gather_rows<<<grid, 256, 0, s>>>(in, out, perm, R_new, R_old, both);
-  ++g_launches;
-}
-
-// input_box (network.hpp:160-177): iv_add(point(c), [-eps, eps]) then the
-// optional [0, 1] clamp with std::max/std::min semantics.
-__global__ void k_input_box(const double* c, int n, double eps, int clamp01, double* lo,
-                            double* up) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double l = add_down(c[i], -eps), h = add_up(c[i], eps);
-  if (clamp01) {
-    l = smax(l, 0.0);
-    h = smin(h, 1.0);
-  }
-  lo[i] = l;
-  up[i] = h;
-}
-
-cudaError_t input_box_device(const double* center, int n, double eps, int clamp01, double* lo,
-                             double* up) {
-  double* d = nullptr;
-  cudaError_t e = cudaMalloc(&d, sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
-  if (e != cudaSuccess) return e;
-  e = cudaMemcpy(d, center, sizeof(double) * n, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && n > 0) {
-    k_input_box<<<cdiv(n, 256), 256>>>(d, n, eps, clamp01, d + n, d + 2 * (size_t)n);
-    ++g_launches;
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) e = cudaMemcpy(lo, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess) e = cudaMemcpy(up, d + 2 * (size_t)n, sizeof(double) * n, cudaMemcpyDeviceToHost);
-  cudaFree(d);
-  return e;
 }
 
 // ===========================================================================

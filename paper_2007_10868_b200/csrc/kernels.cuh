@@ -62,12 +62,20 @@ __device__ __forceinline__ void frame_base(const FrameDev& f, int q, int& bw, in
 // queries row_q[0..n_up), rows [n_up, n) lower rows for row_q[i - n_up]
 // (margin passes: n_up = 0). Coefficients are SoA planes lo[n][cells],
 // hi[n][cells]; K[n][4] = {k.lo, k.hi, kraw.lo, kraw.hi}.
+// src (nullable): after an early-termination compaction the surviving rows
+// are not moved; logical row i lives at physical row src[i] until the next
+// step consumes the matrix and writes a compact output.
 struct MatDev {
   double* lo;
   double* hi;
   double* K;
   long long cells;
+  const int* src = nullptr;
 };
+
+__host__ __device__ __forceinline__ size_t phys_row(const MatDev& m, int i) {
+  return (size_t)(m.src ? m.src[i] : i);
+}
 
 struct RowsDev {
   const int* row_q;
@@ -109,11 +117,12 @@ void launch_init_affine(cudaStream_t s, const LayerDev& Q, const RowsDev& rows, 
 void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev out);
 void launch_init_margin(cudaStream_t s, int label, int n_out, MatDev out);
 
+// Chains read the constants of m (through m.src) and write compact ones to Kout.
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
-                         const FrameDev& fin, MatDev m, const double* dev, Counters* ctr,
-                         int count_madds);
+                         const FrameDev& fin, MatDev m, double* Kout, const double* dev,
+                         Counters* ctr);
 void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
-                       const double* relax);
+                       double* Kout, const double* relax);
 void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        const double* blo, const double* bhi, const double* rlo,
                        const double* rhi, double* vals, double* rvals);
@@ -127,12 +136,12 @@ void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, Ma
 void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const FrameDev& fb,
                   const FrameDev& fu, int dense_path, MatDev a, MatDev b, MatDev out);
 
+// Offers + freeze; writes the compaction map (2 * new_R entries: upper then
+// lower physical rows) and the compacted query list.
 void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals,
                   const double* rvals, double* cand, char* frozen, int allow_freeze,
-                  int early_term, int* perm, int* new_R, int* new_row_q, Counters* ctr);
+                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr);
 void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best, char* has);
-void launch_gather_rows(cudaStream_t s, MatDev in, MatDev out, const int* perm, int R_new,
-                        int R_old, int both);
 
 cudaError_t input_box_device(const double* center, int n, double eps, int clamp01, double* lo,
                              double* up);
