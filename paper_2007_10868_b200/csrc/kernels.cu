@@ -1246,6 +1246,38 @@ void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best
   ++g_launches;
 }
 
+// input_box (network.hpp:160-177): iv_add(point(c), [-eps, eps]) then the
+// optional [0, 1] clamp with std::max/std::min semantics.
+__global__ void k_input_box(const double* c, int n, double eps, int clamp01, double* lo,
+                            double* up) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double l = add_down(c[i], -eps), h = add_up(c[i], eps);
+  if (clamp01) {
+    l = smax(l, 0.0);
+    h = smin(h, 1.0);
+  }
+  lo[i] = l;
+  up[i] = h;
+}
+
+cudaError_t input_box_device(const double* center, int n, double eps, int clamp01, double* lo,
+                             double* up) {
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(d, center, sizeof(double) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && n > 0) {
+    k_input_box<<<cdiv(n, 256), 256>>>(d, n, eps, clamp01, d + n, d + 2 * (size_t)n);
+    ++g_launches;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(lo, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(up, d + 2 * (size_t)n, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
+
 // ===========================================================================
 // Concrete forward evaluation (eval.hpp:39-102): round-to-nearest, bias first
 // then ascending inputs, separate multiply and add roundings (no FMA), all

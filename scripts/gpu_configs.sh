@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k baseline_configs 2>&1 | tail -3
-for c in cifar_convbig cifar_resnet18 cifar_resnet34; do
-  timeout 600 python bench.py --config $c --steps 2 --warmup 1 --no-cpu-baseline 2>&1 | tail -2 | cut -c1-700
+timeout 300 python -m pytest tests/test_gpu_numeric.py tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
+for c in cifar_resnet18 cifar_resnet34; do
+  timeout 900 python bench.py --config $c --steps 2 --warmup 1 --no-cpu-baseline 2>&1 | tail -2 | cut -c1-900
 done
