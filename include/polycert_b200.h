@@ -133,6 +133,11 @@ long long pc_last_launch_count(void);
 void pc_last_timing(double* total_ms, double* dense_kernel_ms, double* dense_kernel_bytes,
                     long long* dense_kernel_launches);
 
+/* Per-kernel-class device time of this thread's last pc_net_test* call as a
+ * JSON object {class: [launches, ms]} (collected only when the environment
+ * variable PC_PROFILE=1 is set when the net is created). Returns the length. */
+int pc_last_profile(char* buf, int len);
+
 /* Numeric-core self test (device): out[i] = op(a[i], b[i]) with op 0
  * add_down, 1 add_up, 2 mul_down, 3 mul_up, 4 div_down, 5 div_up,
  * 6 ulp_above(a) (interval.hpp:59-102); 7/8 the direction-generic chain add

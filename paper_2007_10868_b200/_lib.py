@@ -66,6 +66,7 @@ def _load():
         "pc_last_launch_count": (ll, []),
         "pc_last_timing": (None, [vp, vp, vp, vp]),
         "pc_scalar_ops": (i, [i, vp, vp, vp, ll]),
+        "pc_last_profile": (i, [ctypes.c_char_p, i]),
         "pc_last_error": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():

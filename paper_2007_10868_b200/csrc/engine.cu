@@ -121,6 +121,10 @@ struct pc_net {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   bool timing = false;
+  bool profile = false;  // PC_PROFILE=1: per-kernel-class device time
+  std::vector<std::pair<int, size_t>> prof;  // (class, event index of the begin event)
+  std::vector<size_t> dense_ev;               // begin events of dense-coefficient launches
+  int prof_open = -1;
   std::mutex mu;
 
   template <class T>
@@ -133,6 +137,34 @@ struct pc_net {
 };
 
 namespace {
+
+enum ProfClass { PROF_FWD, PROF_SEED, PROF_INIT, PROF_CHAIN_AFFINE, PROF_DENSE, PROF_GBC,
+                 PROF_CHAIN_RELU, PROF_RELU, PROF_MERGE, PROF_CONC, PROF_OFFER, PROF_WRITEBACK,
+                 PROF_N };
+const char* kProfNames[PROF_N] = {"forward", "seed", "init", "chain_affine", "dense_coef",
+                                  "gbc_coef", "chain_relu", "relu_coef", "merge", "concretize",
+                                  "offer", "writeback"};
+thread_local double g_prof_ms[PROF_N];
+thread_local long long g_prof_n[PROF_N];
+
+cudaEvent_t take_event(pc_net* n) {
+  while (n->ev_pool.size() <= n->ev_used) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event");
+    n->ev_pool.push_back(e);
+  }
+  return n->ev_pool[n->ev_used++];
+}
+
+void prof_begin(pc_net* n, int cls) {
+  if (!n->profile) return;
+  n->prof.emplace_back(cls, n->ev_used);
+  ck(cudaEventRecord(take_event(n), n->stream), "event");
+}
+void prof_end(pc_net* n) {
+  if (!n->profile) return;
+  ck(cudaEventRecord(take_event(n), n->stream), "event");
+}
 
 // ---------------------------------------------------------------------------
 // Validation (model_io.cpp:49-194)
@@ -360,17 +392,15 @@ struct Walker {
     Mat out = alloc(dense_frame(L.pred0), false);
     out.K = k_out(m);
     if (!dry) {
+      prof_begin(n, PROF_CHAIN_AFFINE);
       launch_chain_affine(s, L.d, false, rows(), fdev(n, m.f, q), md(m), out.K,
                           n->dev + n->off[m.f.layer], n->ctr);
+      prof_end(n);
       cudaEvent_t e0 = nullptr, e1 = nullptr;
-      if (n->timing) {
-        while (n->ev_pool.size() < n->ev_used + 2) {
-          cudaEvent_t e;
-          ck(cudaEventCreate(&e), "event");
-          n->ev_pool.push_back(e);
-        }
-        e0 = n->ev_pool[n->ev_used++];
-        e1 = n->ev_pool[n->ev_used++];
+      if (n->timing) {  // the roofline kernel is always timed (bench.py reads it)
+        n->dense_ev.push_back(n->ev_used);
+        e0 = take_event(n);
+        e1 = take_event(n);
         // algorithmic bytes: coefficient rows in/out (16 B per interval) + weights once
         g_dense_bytes += 16.0 * nrows() * (double)(m.cells + out.cells) + 8.0 * m.cells * out.cells;
         ++g_dense_launches;
@@ -397,9 +427,13 @@ struct Walker {
     out.K = k_out(m);
     if (!dry) {
       const FrameDev fi = fdev(n, m.f, q), fo = fdev(n, nf, q);
+      prof_begin(n, PROF_CHAIN_AFFINE);
       launch_chain_affine(s, L.d, true, rows(), fi, md(m), out.K, n->dev + n->off[m.f.layer],
                           n->ctr);
+      prof_end(n);
+      prof_begin(n, PROF_GBC);
       launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out));
+      prof_end(n);
       st->gbc_dense_equiv += (long long)nrows() * L.numel() * L.in_numel();
     }
     m = out;
@@ -414,8 +448,12 @@ struct Walker {
     if (!dry) {
       const FrameDev f = fdev(n, m.f, q);
       const double* rx = n->relax + 8 * n->off[L.pred0];
+      prof_begin(n, PROF_CHAIN_RELU);
       launch_chain_relu(s, rows(), f, md(m), out.K, rx);
+      prof_end(n);
+      prof_begin(n, PROF_RELU);
       launch_relu_coef(s, rows(), f, md(m), md(out), rx);
+      prof_end(n);
     }
     m = out;
   }
@@ -448,9 +486,12 @@ struct Walker {
       u.Wh = std::max(a.f.Ah + a.f.Wh, b.f.Ah + b.f.Wh) - u.Ah;
     }
     Mat out = alloc(u, true);
-    if (!dry)
+    if (!dry) {
+      prof_begin(n, PROF_MERGE);
       launch_merge(s, rows(), fdev(n, a.f, q), fdev(n, b.f, q), fdev(n, u, q), dense_path, md(a),
                    md(b), md(out));
+      prof_end(n);
+    }
     m = out;
   }
 
@@ -462,16 +503,22 @@ struct Walker {
     const int fl = m.f.layer;
     const long long o = n->off[fl];
     if (margin) {
+      prof_begin(n, PROF_CONC);
       launch_concretize(s, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->blo + o,
                         n->bhi + o, n->vals, n->rvals);
+      prof_end(n);
       launch_margin_offer(s, R, n->vals, n->best, n->has);
       return;
     }
+    prof_begin(n, PROF_CONC);
     launch_concretize(s, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
                       n->rhi + o, n->vals, n->rvals);
+    prof_end(n);
     int* new_q = n->rowq[rq ^ 1];
+    prof_begin(n, PROF_OFFER);
     launch_offer(s, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
                  early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr);
+    prof_end(n);
     if (!(allow_freeze && early_term)) return;
     ck(cudaMemcpyAsync(n->h_int + 1, n->d_int + 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
     ck(cudaStreamSynchronize(s), "sync");
@@ -577,8 +624,10 @@ void run_pass(pc_net* n, int t, bool allow_freeze, pc_stats* st) {
   const int N = (int)Q.numel();
   const long long o = n->off[t];
   const bool et = n->opt.early_term != 0;
+  prof_begin(n, PROF_SEED);
   launch_seed(s, N, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o, allow_freeze ? 1 : 0, et ? 1 : 0,
               n->cand, n->frozen, n->live, n->d_int, &n->ctr->pad);
+  prof_end(n);
   ck(cudaMemcpyAsync(n->h_int, n->d_int, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
   ck(cudaStreamSynchronize(s), "sync");
   const int n_live = n->h_int[0];
@@ -616,9 +665,11 @@ void run_pass(pc_net* n, int t, bool allow_freeze, pc_stats* st) {
     }
   }
   ++n->gen;  // refresh round: the write-back marks what this pass changed
+  prof_begin(n, PROF_WRITEBACK);
   launch_writeback(s, N, Q.out_c, t, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
                    Q.feeds_relu ? n->relax + 8 * o : nullptr, n->gen_n, n->gen_pos, n->gen_l,
                    n->gen, o, n->pofs[t]);
+  prof_end(n);
 }
 
 // run_margin_pass (backsub.hpp:1070-1096)
@@ -660,24 +711,34 @@ void run_test(pc_net* n, int label, double* margins, pc_stats* st) {
   const int nl = (int)n->L.size();
   const int out = nl - 1;
   ck(cudaMemsetAsync(n->ctr, 0, sizeof(Counters), s), "memset");
-  ++n->gen;
-  for (int k = 1; k < nl; ++k) {  // forward_interval, padded + raw (analyzer.hpp:203-215)
-    const HostLayer& l = n->L[k];
-    launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
-                         n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
-                         n->gen_pos, n->gen_l, n->gen, 1);
-  }
-  for (int t = 1; t < nl; ++t) {
-    const bool is_out = t == out;
-    if (!is_out && !n->L[t].feeds_relu) continue;
-    run_pass(n, t, !is_out, st);
-    if (is_out) continue;
-    for (int k = t + 1; k < nl; ++k) {  // refresh (analyzer.hpp:232-239)
+  // Targets: layers feeding a relu, ascending, then the output (analyzer.hpp:220-223).
+  std::vector<int> targets;
+  for (int k = 1; k < out; ++k)
+    if (n->L[k].feeds_relu) targets.push_back(k);
+  targets.push_back(out);
+  // Lazy refresh. The reference recomputes every layer k > t after pass t
+  // (analyzer.hpp:232-239), but pass t' reads only layers <= t' (its seed,
+  // relaxations, dev and frame bounds), and every layer beyond the next target
+  // is recomputed again after that target's pass from the same final
+  // predecessor values. So computing layer k once, right after the last pass
+  // before it (and the forward pass for k <= first target), yields the
+  // reference's state bit-for-bit with each layer evaluated once per image.
+  auto forward = [&](int k0, int k1) {  // layers (k0, k1]
+    for (int k = k0 + 1; k <= k1; ++k) {
       const HostLayer& l = n->L[k];
+      prof_begin(n, PROF_FWD);
       launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
                            n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
-                           n->gen_pos, n->gen_l, n->gen, 0);
+                           n->gen_pos, n->gen_l, n->gen, 1);
+      prof_end(n);
     }
+  };
+  forward(0, targets[0]);
+  for (size_t i = 0; i < targets.size(); ++i) {
+    const int t = targets[i];
+    const bool is_out = t == out;
+    run_pass(n, t, !is_out, st);
+    if (!is_out) forward(t, targets[i + 1]);
   }
   if (label >= 0) run_margin(n, label, st, margins);
   Counters c{};
@@ -739,6 +800,8 @@ pc_status test_impl(pc_net* n, const double* lo, const double* up, bool device_b
     pc_stats st{};
     std::vector<double> m(std::max(1, n->n_out - 1), 0.0);
     n->ev_used = 0;
+    n->prof.clear();
+    n->dense_ev.clear();
     run_test(n, label, m.data(), &st);
     if (b_lo) ck(cudaMemcpyAsync(b_lo, n->blo, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
     if (b_hi) ck(cudaMemcpyAsync(b_hi, n->bhi, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
@@ -752,10 +815,20 @@ pc_status test_impl(pc_net* n, const double* lo, const double* up, bool device_b
     g_total_ms = ms;
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
-    for (size_t e = 0; e + 1 < n->ev_used; e += 2) {
+    for (size_t e : n->dense_ev) {
       float d = 0;
       cudaEventElapsedTime(&d, n->ev_pool[e], n->ev_pool[e + 1]);
       g_dense_ms += d;
+    }
+    for (int c = 0; c < PROF_N; ++c) {
+      g_prof_ms[c] = 0;
+      g_prof_n[c] = 0;
+    }
+    for (const auto& pe : n->prof) {
+      float d = 0;
+      cudaEventElapsedTime(&d, n->ev_pool[pe.second], n->ev_pool[pe.second + 1]);
+      g_prof_ms[pe.first] += d;
+      g_prof_n[pe.first] += 1;
     }
     if (label >= 0) {
       bool v = true;
@@ -922,6 +995,8 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
     ck(cudaMemset(n->gen_l, 0, nl * sizeof(int)), "memset");
     ck(cudaMallocHost(&n->h_int, 64 + (size_t)n->n_out), "pinned");
     n->timing = true;
+    const char* pe = getenv("PC_PROFILE");
+    n->profile = pe && pe[0] == '1';
   });
   if (st != PC_OK) {
     pc_net_destroy(n);
@@ -974,6 +1049,21 @@ pc_status pc_net_candidate(pc_net* n, const double* center, int* label, double* 
     }
     *label = tie ? -1 : best;
   });
+}
+
+int pc_last_profile(char* buf, int len) {
+  std::string j = "{";
+  for (int c = 0; c < PROF_N; ++c) {
+    if (c) j += ", ";
+    j += "\"" + std::string(kProfNames[c]) + "\": [" + std::to_string(g_prof_n[c]) + ", " +
+         std::to_string(g_prof_ms[c]) + "]";
+  }
+  j += "}";
+  if (buf && len > 0) {
+    std::strncpy(buf, j.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)j.size();
 }
 
 void* pc_net_stream(const pc_net* n) { return n ? (void*)n->stream : nullptr; }

@@ -165,6 +165,14 @@ class Verifier:
                                                ctypes.byref(st)))
         return bool(verified.value), margins[: self.n_out - 1], st.as_dict()
 
+    @staticmethod
+    def last_profile() -> dict:
+        """Per-kernel-class {class: [launches, ms]} of the last call (PC_PROFILE=1)."""
+        import json
+        buf = ctypes.create_string_buffer(4096)
+        _lib.lib.pc_last_profile(buf, 4096)
+        return json.loads(buf.value.decode())
+
     def last_timing(self):
         t, dm, db, dl = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
         _lib.lib.pc_last_timing(ctypes.byref(t), ctypes.byref(dm), ctypes.byref(db), ctypes.byref(dl))
