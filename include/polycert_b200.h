@@ -124,6 +124,18 @@ pc_status pc_net_candidate(pc_net* net, const double* center, int* label, double
  * for callers that time or order work around pc_net_test* with CUDA events. */
 void* pc_net_stream(const pc_net* net);
 
+/* Throughput entry: verify n_images boxes concurrently, `concurrency` host
+ * worker threads each driving its own stream and per-call state on the net's
+ * device (images are independent; results equal pc_net_test's).
+ * lo/up: n_images x input-numel, HOST arrays (device arrays if
+ * device_inputs != 0). labels[i] < 0: analysis only. verified[n_images],
+ * margins[n_images x (n_out-1)], stats[n_images] are optional outputs.
+ * device_ms (optional): device time of the whole batch, CUDA events on a
+ * master stream every worker stream waits on / is awaited by. */
+pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const double* up,
+                            int device_inputs, const int* labels, int concurrency, int* verified,
+                            double* margins, pc_stats* stats, double* device_ms);
+
 /* Kernel launches issued by this thread's last pc_net_test* call. */
 long long pc_last_launch_count(void);
 

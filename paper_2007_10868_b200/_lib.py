@@ -61,6 +61,7 @@ def _load():
         "pc_input_box": (i, [vp, i, d, i, vp, vp]),
         "pc_net_test": (i, [vp, vp, vp, i, vp, vp, vp, vp, vp, vp, vp]),
         "pc_net_test_device": (i, [vp, vp, vp, i, vp, vp, vp]),
+        "pc_net_test_batch": (i, [vp, i, vp, vp, i, vp, i, vp, vp, vp, vp]),
         "pc_net_stream": (vp, [vp]),
         "pc_net_candidate": (i, [vp, vp, vp, vp]),
         "pc_last_launch_count": (ll, []),

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -94,19 +96,52 @@ MatDev md(const Mat& m) {
 
 }  // namespace
 
+struct Ctx;
+
 struct pc_net {
   int device = 0;
-  cudaStream_t stream = nullptr;
   pc_options opt{};
   std::vector<HostLayer> L;
   std::vector<long long> off, pofs;  // neuron / grid-position offsets per layer
   long long total = 0, max_numel = 0;
+  int n_out = 0;
+  bool timing = true;
+  bool profile = false;  // PC_PROFILE=1: per-kernel-class device time
+  std::vector<void*> owned;  // device weights
+  std::mutex pool_mu;
+  std::vector<Ctx*> pool;    // idle per-call contexts
+  std::vector<Ctx*> all;
+  Ctx* primary = nullptr;
+
+  template <class T>
+  T* dalloc(size_t n) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+    owned.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+// Per-call state: one verification in flight on its own stream. Concurrent
+// pc_net_test* calls (or pc_net_test_batch workers) each hold one context,
+// so images are verified concurrently on the same device and weights.
+struct Ctx {
+  pc_net* net;
+  const std::vector<HostLayer>& L;
+  const std::vector<long long>& off;
+  const std::vector<long long>& pofs;
+  const long long total, max_numel;
+  const int n_out;
+  const pc_options opt;
+  const int device;
+  const bool timing, profile;
+  long long budget = 0;  // workspace bytes for one pass (0: derive)
+  cudaStream_t stream = nullptr;
+  std::vector<void*> owned;
   int* gen_n = nullptr;
   int* gen_pos = nullptr;
   int* gen_l = nullptr;
   int gen = 0;
-  int n_out = 0;
-  std::vector<void*> owned;
   double *blo = nullptr, *bhi = nullptr, *rlo = nullptr, *rhi = nullptr, *dev = nullptr,
          *relax = nullptr;
   double* cand = nullptr;
@@ -120,12 +155,12 @@ struct pc_net {
   int* h_int = nullptr;  // pinned
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  bool timing = false;
-  bool profile = false;  // PC_PROFILE=1: per-kernel-class device time
   std::vector<std::pair<int, size_t>> prof;  // (class, event index of the begin event)
   std::vector<size_t> dense_ev;               // begin events of dense-coefficient launches
-  int prof_open = -1;
-  std::mutex mu;
+
+  explicit Ctx(pc_net* n)
+      : net(n), L(n->L), off(n->off), pofs(n->pofs), total(n->total), max_numel(n->max_numel),
+        n_out(n->n_out), opt(n->opt), device(n->device), timing(n->timing), profile(n->profile) {}
 
   template <class T>
   T* dalloc(size_t n) {
@@ -134,7 +169,85 @@ struct pc_net {
     owned.push_back(p);
     return static_cast<T*>(p);
   }
+
+  void init() {
+    ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    const int nl = (int)L.size();
+    const size_t T = (size_t)total, M = (size_t)max_numel;
+    blo = dalloc<double>(T);
+    bhi = dalloc<double>(T);
+    rlo = dalloc<double>(T);
+    rhi = dalloc<double>(T);
+    dev = dalloc<double>(T);
+    relax = dalloc<double>(8 * T);
+    ck(cudaMemset(dev, 0, T * 8), "memset");
+    cand = dalloc<double>(4 * M);
+    frozen = dalloc<char>(M);
+    live = dalloc<int>(M);
+    rowq[0] = dalloc<int>(M);
+    rowq[1] = dalloc<int>(M);
+    perm = dalloc<int>(2 * M);
+    d_int = dalloc<int>(8);
+    vals = dalloc<double>(2 * M);
+    rvals = dalloc<double>(2 * M);
+    best = dalloc<double>(M);
+    has = dalloc<char>(M);
+    ctr = dalloc<Counters>(1);
+    gen_n = dalloc<int>(T);
+    gen_pos = dalloc<int>((size_t)pofs[nl]);
+    gen_l = dalloc<int>(nl);
+    ck(cudaMemset(gen_n, 0, T * sizeof(int)), "memset");
+    ck(cudaMemset(gen_pos, 0, (size_t)pofs[nl] * sizeof(int)), "memset");
+    ck(cudaMemset(gen_l, 0, nl * sizeof(int)), "memset");
+    ck(cudaMallocHost(&h_int, 64 + (size_t)n_out), "pinned");
+  }
+
+  ~Ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : owned) cudaFree(p);
+    if (arena) cudaFree(arena);
+    if (h_int) cudaFreeHost(h_int);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
 };
+
+namespace {
+
+Ctx* acquire(pc_net* n) {
+  {
+    std::lock_guard<std::mutex> lk(n->pool_mu);
+    if (!n->pool.empty()) {
+      Ctx* c = n->pool.back();
+      n->pool.pop_back();
+      return c;
+    }
+  }
+  Ctx* c = new Ctx(n);
+  try {
+    c->init();
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  std::lock_guard<std::mutex> lk(n->pool_mu);
+  n->all.push_back(c);
+  return c;
+}
+
+void release(pc_net* n, Ctx* c) {
+  std::lock_guard<std::mutex> lk(n->pool_mu);
+  n->pool.push_back(c);
+}
+
+struct CtxLease {
+  pc_net* n;
+  Ctx* c;
+  explicit CtxLease(pc_net* net) : n(net), c(acquire(net)) {}
+  ~CtxLease() { release(n, c); }
+};
+
+}  // namespace
 
 namespace {
 
@@ -147,7 +260,7 @@ const char* kProfNames[PROF_N] = {"forward", "seed", "init", "chain_affine", "de
 thread_local double g_prof_ms[PROF_N];
 thread_local long long g_prof_n[PROF_N];
 
-cudaEvent_t take_event(pc_net* n) {
+cudaEvent_t take_event(Ctx* n) {
   while (n->ev_pool.size() <= n->ev_used) {
     cudaEvent_t e;
     ck(cudaEventCreate(&e), "event");
@@ -156,12 +269,12 @@ cudaEvent_t take_event(pc_net* n) {
   return n->ev_pool[n->ev_used++];
 }
 
-void prof_begin(pc_net* n, int cls) {
+void prof_begin(Ctx* n, int cls) {
   if (!n->profile) return;
   n->prof.emplace_back(cls, n->ev_used);
   ck(cudaEventRecord(take_event(n), n->stream), "event");
 }
-void prof_end(pc_net* n) {
+void prof_end(Ctx* n) {
   if (!n->profile) return;
   ck(cudaEventRecord(take_event(n), n->stream), "event");
 }
@@ -307,7 +420,7 @@ void validate(const pc_layer_desc* layers, int n, int in_w, int in_h, int in_c,
 // ---------------------------------------------------------------------------
 // Frames
 
-FrameDev fdev(const pc_net* n, const Frame& f, int qlayer) {
+FrameDev fdev(const Ctx* n, const Frame& f, int qlayer) {
   const HostLayer& l = n->L[f.layer];
   const HostLayer& Q = n->L[qlayer];
   FrameDev d{};
@@ -334,7 +447,7 @@ Frame dense_frame(int layer) {
 // One walk context: a chunk of rows of one pass (or the margin rows).
 
 struct Walker {
-  pc_net* n;
+  Ctx* n;
   cudaStream_t s;
   int q;             // query layer
   bool dry = false;  // geometry dry run: count bytes per row only
@@ -566,7 +679,7 @@ struct Walker {
   }
 };
 
-Frame initial_frame(const pc_net* n, int t, bool affine) {
+Frame initial_frame(const Ctx* n, int t, bool affine) {
   const HostLayer& Q = n->L[t];
   if (affine) {
     if (Q.kind == KIND_DENSE) return dense_frame(Q.pred0);
@@ -593,7 +706,7 @@ struct WalkSize {
   size_t per_row, allocs;
 };
 
-WalkSize walk_size(pc_net* n, int t, bool affine, bool both) {
+WalkSize walk_size(Ctx* n, int t, bool affine, bool both) {
   Walker w{n, nullptr, t};
   w.dry = true;
   w.both = both;
@@ -604,7 +717,7 @@ WalkSize walk_size(pc_net* n, int t, bool affine, bool both) {
   return WalkSize{w.dry_peak, w.dry_allocs};
 }
 
-void ensure_arena(pc_net* n, size_t bytes) {
+void ensure_arena(Ctx* n, size_t bytes) {
   if (bytes <= n->arena_cap) return;
   if (n->arena) cudaFree(n->arena);
   n->arena = nullptr;
@@ -613,12 +726,13 @@ void ensure_arena(pc_net* n, size_t bytes) {
   n->arena_cap = bytes;
 }
 
-long long budget_of(const pc_net* n) {
-  return n->opt.memory_budget > 0 ? n->opt.memory_budget : (16ll << 30);
+long long budget_of(const Ctx* n) {
+  if (n->opt.memory_budget > 0) return n->opt.memory_budget;
+  return n->budget > 0 ? n->budget : (16ll << 30);
 }
 
 // run_backsubstitution (backsub.hpp:993-1065)
-void run_pass(pc_net* n, int t, bool allow_freeze, pc_stats* st) {
+void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   cudaStream_t s = n->stream;
   const HostLayer& Q = n->L[t];
   const int N = (int)Q.numel();
@@ -673,7 +787,7 @@ void run_pass(pc_net* n, int t, bool allow_freeze, pc_stats* st) {
 }
 
 // run_margin_pass (backsub.hpp:1070-1096)
-void run_margin(pc_net* n, int label, pc_stats* st, double* margins_host) {
+void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
   cudaStream_t s = n->stream;
   const int out = (int)n->L.size() - 1;
   const int nr = n->n_out - 1;
@@ -706,7 +820,7 @@ void run_margin(pc_net* n, int label, pc_stats* st, double* margins_host) {
 }
 
 // analyze + run_margin_pass (analyzer.hpp:198-276)
-void run_test(pc_net* n, int label, double* margins, pc_stats* st) {
+void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
   cudaStream_t s = n->stream;
   const int nl = (int)n->L.size();
   const int out = nl - 1;
@@ -765,19 +879,10 @@ pc_status guard(const std::function<void()>& fn) {
   }
 }
 
-pc_status test_impl(pc_net* n, const double* lo, const double* up, bool device_box, int label,
-                    int* verified, double* margins, double* b_lo, double* b_hi, double* r_lo,
-                    double* r_hi, pc_stats* stats) {
-  if (!n) {
-    g_err = "null network";
-    return PC_ERR_INVALID_ARGUMENT;
-  }
-  std::lock_guard<std::mutex> lock(n->mu);
-  g_launches = 0;
-  g_dense_ms = g_dense_bytes = 0;
-  g_dense_launches = 0;
-  return guard([&] {
-    ck(cudaSetDevice(n->device), "cudaSetDevice");
+// One verification on context n (analyze + margin pass; verify_robustness).
+void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int label, int* verified,
+             double* margins, double* b_lo, double* b_hi, double* r_lo, double* r_hi,
+             pc_stats* stats) {
     if (label >= n->n_out) throw StatusError(PC_ERR_INVALID_ARGUMENT, "margin: label out of range");
     const long long n0 = n->L[0].numel();
     cudaStream_t s = n->stream;
@@ -842,6 +947,22 @@ pc_status test_impl(pc_net* n, const double* lo, const double* up, bool device_b
     }
     if (stats) *stats = st;
     g_last_launches = g_launches;
+}
+
+pc_status test_impl(pc_net* net, const double* lo, const double* up, bool device_box, int label,
+                    int* verified, double* margins, double* b_lo, double* b_hi, double* r_lo,
+                    double* r_hi, pc_stats* stats) {
+  if (!net) {
+    g_err = "null network";
+    return PC_ERR_INVALID_ARGUMENT;
+  }
+  g_launches = 0;
+  g_dense_ms = g_dense_bytes = 0;
+  g_dense_launches = 0;
+  return guard([&] {
+    ck(cudaSetDevice(net->device), "cudaSetDevice");
+    CtxLease lease(net);
+    run_one(lease.c, lo, up, device_box, label, verified, margins, b_lo, b_hi, r_lo, r_hi, stats);
   });
 }
 
@@ -917,7 +1038,6 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
     if (n->opt.device >= 0) n->device = n->opt.device;
     else ck(cudaGetDevice(&n->device), "cudaGetDevice");
     ck(cudaSetDevice(n->device), "cudaSetDevice");
-    ck(cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking), "stream");
     const int nl = (int)n->L.size();
     n->off.assign(nl + 1, 0);
     for (int k = 0; k < nl; ++k) {
@@ -967,36 +1087,11 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
         d.FT = FT;
       }
     }
-    const size_t T = (size_t)n->total, M = (size_t)n->max_numel;
-    n->blo = n->dalloc<double>(T);
-    n->bhi = n->dalloc<double>(T);
-    n->rlo = n->dalloc<double>(T);
-    n->rhi = n->dalloc<double>(T);
-    n->dev = n->dalloc<double>(T);
-    n->relax = n->dalloc<double>(8 * T);
-    ck(cudaMemset(n->dev, 0, T * 8), "memset");
-    n->cand = n->dalloc<double>(4 * M);
-    n->frozen = n->dalloc<char>(M);
-    n->live = n->dalloc<int>(M);
-    n->rowq[0] = n->dalloc<int>(M);
-    n->rowq[1] = n->dalloc<int>(M);
-    n->perm = n->dalloc<int>(2 * M);
-    n->d_int = n->dalloc<int>(8);
-    n->vals = n->dalloc<double>(2 * M);
-    n->rvals = n->dalloc<double>(2 * M);
-    n->best = n->dalloc<double>(M);
-    n->has = n->dalloc<char>(M);
-    n->ctr = n->dalloc<Counters>(1);
-    n->gen_n = n->dalloc<int>(T);
-    n->gen_pos = n->dalloc<int>((size_t)n->pofs[nl]);
-    n->gen_l = n->dalloc<int>(nl);
-    ck(cudaMemset(n->gen_n, 0, T * sizeof(int)), "memset");
-    ck(cudaMemset(n->gen_pos, 0, (size_t)n->pofs[nl] * sizeof(int)), "memset");
-    ck(cudaMemset(n->gen_l, 0, nl * sizeof(int)), "memset");
-    ck(cudaMallocHost(&n->h_int, 64 + (size_t)n->n_out), "pinned");
     n->timing = true;
     const char* pe = getenv("PC_PROFILE");
     n->profile = pe && pe[0] == '1';
+    n->primary = acquire(n);  // the first per-call context (stream + state buffers)
+    release(n, n->primary);
   });
   if (st != PC_OK) {
     pc_net_destroy(n);
@@ -1009,20 +1104,17 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
 void pc_net_destroy(pc_net* n) {
   if (!n) return;
   cudaSetDevice(n->device);
-  if (n->stream) cudaStreamSynchronize(n->stream);
+  for (Ctx* c : n->all) delete c;
   for (void* p : n->owned) cudaFree(p);
-  if (n->arena) cudaFree(n->arena);
-  if (n->h_int) cudaFreeHost(n->h_int);
-  for (cudaEvent_t e : n->ev_pool) cudaEventDestroy(e);
-  if (n->stream) cudaStreamDestroy(n->stream);
   delete n;
 }
 
-pc_status pc_net_candidate(pc_net* n, const double* center, int* label, double* logits) {
-  if (!n || !label) return PC_ERR_INVALID_ARGUMENT;
-  std::lock_guard<std::mutex> lock(n->mu);
+pc_status pc_net_candidate(pc_net* net, const double* center, int* label, double* logits) {
+  if (!net || !label) return PC_ERR_INVALID_ARGUMENT;
   return guard([&] {
-    ck(cudaSetDevice(n->device), "cudaSetDevice");
+    ck(cudaSetDevice(net->device), "cudaSetDevice");
+    CtxLease lease(net);
+    Ctx* n = lease.c;
     cudaStream_t s = n->stream;
     // concrete activations reuse the raw-bound buffers as scratch
     ck(cudaMemcpyAsync(n->rlo, center, sizeof(double) * n->L[0].numel(), cudaMemcpyHostToDevice, s), "h2d");
@@ -1066,7 +1158,9 @@ int pc_last_profile(char* buf, int len) {
   return (int)j.size();
 }
 
-void* pc_net_stream(const pc_net* n) { return n ? (void*)n->stream : nullptr; }
+void* pc_net_stream(const pc_net* n) {
+  return n && n->primary ? (void*)n->primary->stream : nullptr;
+}
 
 int pc_net_num_layers(const pc_net* n) { return n ? (int)n->L.size() : -1; }
 long long pc_net_layer_numel(const pc_net* n, int k) {
@@ -1080,6 +1174,90 @@ pc_status pc_net_test(pc_net* n, const double* lo, const double* up, int label, 
                       double* margins, double* b_lo, double* b_hi, double* r_lo, double* r_hi,
                       pc_stats* stats) {
   return test_impl(n, lo, up, false, label, verified, margins, b_lo, b_hi, r_lo, r_hi, stats);
+}
+
+pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const double* up,
+                            int device_inputs, const int* labels, int concurrency, int* verified,
+                            double* margins, pc_stats* stats, double* device_ms) {
+  if (!net || n_images < 0 || !lo || !up || !labels) {
+    g_err = "invalid batch arguments";
+    return PC_ERR_INVALID_ARGUMENT;
+  }
+  return guard([&] {
+    ck(cudaSetDevice(net->device), "cudaSetDevice");
+    const int conc = std::max(1, std::min(concurrency > 0 ? concurrency : 8, std::max(n_images, 1)));
+    const long long n0 = net->L[0].numel();
+    const int nm = std::max(1, net->n_out - 1);
+    size_t free_b = 0, total_b = 0;
+    ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const long long budget = std::min<long long>(16ll << 30, (long long)(free_b * 0.6) / conc);
+    cudaStream_t master;
+    cudaEvent_t start, end;
+    ck(cudaStreamCreateWithFlags(&master, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreate(&start), "event");
+    ck(cudaEventCreate(&end), "event");
+    std::vector<Ctx*> ctxs(conc);
+    for (int w = 0; w < conc; ++w) {
+      ctxs[w] = acquire(net);
+      ctxs[w]->budget = budget;
+    }
+    ck(cudaEventRecord(start, master), "event");
+    for (Ctx* c : ctxs) ck(cudaStreamWaitEvent(c->stream, start, 0), "wait");
+    std::atomic<int> next{0};
+    std::atomic<long long> launches{0};
+    std::mutex err_mu;
+    std::string err;
+    pc_status err_code = PC_OK;
+    auto work = [&](int w) {
+      cudaSetDevice(net->device);
+      g_launches = 0;
+      for (;;) {
+        const int i = next.fetch_add(1);
+        if (i >= n_images) break;
+        const double* li = lo + (size_t)i * n0;
+        const double* ui = up + (size_t)i * n0;
+        const pc_status st = guard([&] {
+          run_one(ctxs[w], li, ui, device_inputs != 0, labels[i], verified ? verified + i : nullptr,
+                  margins ? margins + (size_t)i * nm : nullptr, nullptr, nullptr, nullptr, nullptr,
+                  stats ? stats + i : nullptr);
+        });
+        if (st != PC_OK) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (err_code == PC_OK) {
+            err_code = st;
+            err = g_err;
+          }
+        }
+      }
+      launches += g_launches;
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < conc; ++w) pool.emplace_back(work, w);
+    work(0);
+    for (auto& t : pool) t.join();
+    cudaEvent_t* done = new cudaEvent_t[conc];
+    for (int w = 0; w < conc; ++w) {
+      ck(cudaEventCreate(&done[w]), "event");
+      ck(cudaEventRecord(done[w], ctxs[w]->stream), "event");
+      ck(cudaStreamWaitEvent(master, done[w], 0), "wait");
+    }
+    ck(cudaEventRecord(end, master), "event");
+    ck(cudaStreamSynchronize(master), "sync");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, start, end);
+    if (device_ms) *device_ms = ms;
+    for (int w = 0; w < conc; ++w) {
+      cudaEventDestroy(done[w]);
+      ctxs[w]->budget = 0;
+      release(net, ctxs[w]);
+    }
+    delete[] done;
+    cudaEventDestroy(start);
+    cudaEventDestroy(end);
+    cudaStreamDestroy(master);
+    g_last_launches = launches.load();
+    if (err_code != PC_OK) throw StatusError(err_code, err);
+  });
 }
 
 pc_status pc_net_test_device(pc_net* n, const double* d_lo, const double* d_up, int label,

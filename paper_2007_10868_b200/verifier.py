@@ -142,6 +142,28 @@ class Verifier:
         """analyze (analyzer.hpp:198-242): refined per-neuron bounds."""
         return self.test(box.lo, box.hi, -1, want_bounds=True)
 
+    def test_batch(self, lo, up, labels, concurrency: int = 8, device_inputs: bool = False):
+        """Verify many boxes concurrently (one stream per worker). lo/up: (n, input numel)
+        host arrays, or device pointers (ints) when device_inputs. Returns
+        (verified[n], margins[n, n_out-1], stats list, device_ms)."""
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        n = len(labels)
+        nm = max(self.n_out - 1, 1)
+        verified = np.zeros(n, dtype=np.int32)
+        margins = np.zeros((n, nm))
+        stats = (_lib.PcStats * max(n, 1))()
+        ms = ctypes.c_double(0)
+        if device_inputs:
+            plo, pup = ctypes.c_void_p(lo), ctypes.c_void_p(up)
+        else:
+            lo = np.ascontiguousarray(lo, dtype=np.float64)
+            up = np.ascontiguousarray(up, dtype=np.float64)
+            plo, pup = _ptr(lo), _ptr(up)
+        _lib.check(_lib.lib.pc_net_test_batch(self._h, n, plo, pup, int(bool(device_inputs)),
+                                              _ptr(labels), int(concurrency), _ptr(verified),
+                                              _ptr(margins), stats, ctypes.byref(ms)))
+        return verified.astype(bool), margins[:, : self.n_out - 1], [s.as_dict() for s in stats[:n]], ms.value
+
     def candidate(self, center) -> int:
         """Unique argmax of the concrete forward pass (-1 on ties), on the GPU."""
         c = np.ascontiguousarray(center, dtype=np.float64)

@@ -132,3 +132,20 @@ def test_baseline_configs(pc, port, name, n_img):
         lab = v.candidate(x)
         assert lab >= 0
         run_case(pc, port, net, x, float(eps_s), label=lab)
+
+
+def test_batch_matches_sequential(pc):
+    """pc_net_test_batch (concurrent contexts/streams) == one-at-a-time pc_net_test."""
+    net = pc.generate(11, EXTRA_ARCHS[3])
+    v = pc.Verifier(net)
+    X = pc.random_inputs(12, 12, int(np.prod(net.input_shape)))
+    boxes = [pc.input_box(x, 0.05) for x in X]
+    labels = np.array([max(v.candidate(x), 0) for x in X], dtype=np.int32)
+    lo = np.stack([b.lo for b in boxes])
+    hi = np.stack([b.hi for b in boxes])
+    ver, mar, st, ms = v.test_batch(lo, hi, labels, concurrency=5)
+    assert ms > 0
+    for i in range(len(X)):
+        r = v.test(lo[i], hi[i], int(labels[i]))
+        assert np.array_equal(r.margins.view(np.int64), mar[i].view(np.int64))
+        assert bool(ver[i]) == r.verified and st[i] == r.stats
