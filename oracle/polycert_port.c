@@ -9,7 +9,7 @@
  * (proj/docs/golden/report.jsonl, committed as tests/golden/).
  *
  * Every function follows one reference function; file:line citations are to
- * /root/reference/proj/include/polycert/*.hpp unless noted. Loop orders, zero
+ * /root/reference/proj/include/polycert/ headers unless noted. Loop orders, zero
  * skips and the outward-step rounding rule are restated exactly, so results
  * are bit-identical to the reference (compile with -ffp-contract=off).
  */
