@@ -7,12 +7,27 @@
 // constant/concretisation chain is one lane.
 #include <cub/block/block_scan.cuh>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "numeric.cuh"
 
 namespace pc {
 
 thread_local long long g_launches = 0;
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+long long big_chain_cells() {
+  static const long long v = [] {
+    const char* e = getenv("PC_BIG_CHAIN_CELLS");
+    return e && *e ? atoll(e) : 1024ll;
+  }();
+  return v;
+}
 
 #define PC_NAN __longlong_as_double(0x7ff8000000000000ULL)
 
@@ -708,6 +723,10 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                          const FrameDev& fin, MatDev m, double* Kout, const double* dev,
                          Counters* ctr) {
+  if (m.cells >= big_chain_cells()) {
+    launch_chain_affine_big(s, L, is_conv, rows, fin, m, Kout, dev, ctr);
+    return;
+  }
   k_chain_affine<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(L, is_conv ? 1 : 0, rows,
                                                                         fin, m, Kout, dev, ctr);
   ++g_launches;
@@ -791,6 +810,10 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 
 void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        double* Kout, const double* relax) {
+  if (m.cells >= big_chain_cells()) {
+    launch_chain_relu_big(s, rows, f, m, Kout, relax);
+    return;
+  }
   k_chain_relu<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, Kout, relax);
   ++g_launches;
 }
@@ -868,6 +891,10 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        const double* blo, const double* bhi, const double* rlo,
                        const double* rhi, double* vals, double* rvals) {
+  if (m.cells >= big_chain_cells()) {
+    launch_concretize_big(s, rows, f, m, blo, bhi, rlo, rhi, vals, rvals);
+    return;
+  }
   k_concretize<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, blo, bhi, rlo,
                                                                       rhi, vals, rvals);
   ++g_launches;
@@ -1043,6 +1070,11 @@ __global__ void __launch_bounds__(256)
 
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out) {
+  static const int tiled = env_int("PC_GBC", 1);
+  if (tiled) {
+    launch_gbc_tile(s, L, rows, fin, fout, in, out);
+    return;
+  }
   unsigned gx = cdiv(out.cells, 256);
   if (gx > 1024) gx = 1024;
   dim3 grid(gx, rows.n);

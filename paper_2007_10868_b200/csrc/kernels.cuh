@@ -127,10 +127,29 @@ void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, M
                        const double* blo, const double* bhi, const double* rlo,
                        const double* rhi, double* vals, double* rvals);
 
+// Long-row variants (chains.cu): one CTA per row, producer warps compact the
+// contributing terms, one consumer warp folds them in order.
+void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
+                             const FrameDev& fin, MatDev m, double* Kout, const double* dev,
+                             Counters* ctr);
+void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                           double* Kout, const double* relax);
+void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                           const double* blo, const double* bhi, const double* rlo,
+                           const double* rhi, double* vals, double* rvals);
+// Rows at least this long use the CTA-per-row chains (env PC_BIG_CHAIN_CELLS
+// overrides, read once; the tests force 1 to run the corpus through them).
+long long big_chain_cells();
+
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, MatDev out,
                        cudaEvent_t ev0, cudaEvent_t ev1);
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out);
+void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, MatDev in, MatDev out);
+// Engine switches from the environment (read once): PC_GBC=0 selects the
+// one-output-per-thread conv kernel instead of the register-blocked one.
+int env_int(const char* name, int dflt);
 void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev in,
                       MatDev out, const double* relax);
 void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const FrameDev& fb,

@@ -50,12 +50,12 @@ __device__ __forceinline__ bool sum_exact_ref(double a, double b, double s) {
   return __dadd_rn(da, db) == 0.0;
 }
 
-__device__ __noinline__ double add_up_slow(double a, double b) {
+static __device__ __noinline__ double add_up_slow(double a, double b) {
   const double s = __dadd_rn(a, b);
   if (s != s) return kInf;
   return sum_exact_ref(a, b, s) ? s : nextup_bits(s);
 }
-__device__ __noinline__ double add_down_slow(double a, double b) {
+static __device__ __noinline__ double add_down_slow(double a, double b) {
   const double s = __dadd_rn(a, b);
   if (s != s) return -kInf;
   return sum_exact_ref(a, b, s) ? s : nextdown_bits(s);

@@ -85,13 +85,14 @@ int main() {
     }
     CHECK(threw);
   }
-  {  // margins match explicit output differences: dyadic, so widened == exact
+  {  // margins match explicit output differences: exact 1/8 and 3/16 (rational mode);
+     // widened mode certifies slightly less (inference-deviation allowances)
     Network net = instantiate(dense_net(Shape{1, 1, 2}, {{{{1, 0}, {0, 1}, {0.5, 0.5}}, {0, 0.25, 0}}}), opt);
     const Verdict v = verify_robustness(net, input_box({0.5, 0.5}, 1.0 / 16, true), 1, opt);
     CHECK(v.margins.size() == 2);
     CHECK(v.margins[0].first == 0 && v.margins[1].first == 2);
-    CHECK(v.margins[0].second == 1.0 / 8);
-    CHECK(v.margins[1].second == 3.0 / 16);
+    CHECK(v.margins[0].second <= 1.0 / 8 && 1.0 / 8 - v.margins[0].second < 1e-12);
+    CHECK(v.margins[1].second <= 3.0 / 16 && 3.0 / 16 - v.margins[1].second < 1e-12);
     CHECK(v.verified);
   }
   {  // relu-free networks get the exact affine image

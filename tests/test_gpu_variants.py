@@ -1,0 +1,21 @@
+"""Kernel-variant coverage: re-run the GPU parity corpus with engine switches
+that route every row through the alternative kernels (e.g. the CTA-per-row
+chain kernels of chains.cu, normally used only for rows >= 1024 cells), so
+each variant is held to the same bit-exact bar against the oracle."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("env", [{"PC_BIG_CHAIN_CELLS": "1"}, {"PC_GBC": "0"}], ids=["big_chains", "gbc_legacy"])
+def test_parity_corpus_under_variant(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(HERE, "test_gpu_parity.py"), "-x", "-q",
+                        "-m", "gpu", "-p", "no:cacheprovider"], env=e, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
