@@ -136,6 +136,22 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
                             int device_inputs, const int* labels, int concurrency, int* verified,
                             double* margins, pc_stats* stats, double* device_ms);
 
+/* Row sharding across ranks (one process per GPU). With
+ * world > 1 every rank runs every pass's seed and refresh (identical,
+ * deterministic), back-substitutes only its contiguous slice of the pass's
+ * live rows (and of the margin rows), and the refined candidate bounds
+ * (32 B per row; 8 B per margin row) are all-gathered before the write-back —
+ * the path's one exchange step. Results are bit-identical to world = 1.
+ * `allgather` must gather `bytes` from every rank's device buffer d_send into
+ * d_recv (rank-major, world * bytes), ordered on `stream` (a cudaStream_t),
+ * e.g. ncclAllGather(d_send, d_recv, bytes, ncclUint8, comm, stream); it
+ * returns 0 on success. Every rank must call pc_net_test on the same box and
+ * label. pc_net_test_batch refuses a sharded net. world = 1 disables. */
+typedef int (*pc_allgather_fn)(void* user, const void* d_send, void* d_recv, size_t bytes,
+                               void* stream);
+pc_status pc_net_set_sharding(pc_net* net, int rank, int world, pc_allgather_fn allgather,
+                              void* user);
+
 /* Kernel launches issued by this thread's last pc_net_test* call. */
 long long pc_last_launch_count(void);
 

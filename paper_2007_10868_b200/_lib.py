@@ -42,6 +42,11 @@ class PcStats(ctypes.Structure):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
 
 
+# int (*pc_allgather_fn)(void* user, const void* d_send, void* d_recv, size_t bytes, void* stream)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_size_t, ctypes.c_void_p)
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -69,6 +74,7 @@ def _load():
         "pc_scalar_ops": (i, [i, vp, vp, vp, ll]),
         "pc_last_profile": (i, [ctypes.c_char_p, i]),
         "pc_last_error": (ctypes.c_char_p, []),
+        "pc_net_set_sharding": (i, [vp, i, i, ALLGATHER_FN, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

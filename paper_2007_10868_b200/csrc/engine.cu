@@ -86,11 +86,13 @@ struct Mat {
   Frame f;
   const int* src = nullptr;  // row map after a compaction (see MatDev::src)
   int phys = 0;              // physical rows in the buffers
+  unsigned* stat = nullptr;  // magnitude statistics (MatDev::stat)
 };
 
 MatDev md(const Mat& m) {
   MatDev d{m.lo, m.hi, m.K, m.cells};
   d.src = m.src;
+  d.stat = m.stat;
   return d;
 }
 
@@ -112,6 +114,10 @@ struct pc_net {
   std::vector<Ctx*> pool;    // idle per-call contexts
   std::vector<Ctx*> all;
   Ctx* primary = nullptr;
+  // row sharding (pc_net_set_sharding)
+  int shard_rank = 0, shard_world = 1;
+  pc_allgather_fn allgather = nullptr;
+  void* allgather_user = nullptr;
 
   template <class T>
   T* dalloc(size_t n) {
@@ -152,6 +158,10 @@ struct Ctx {
   Counters* ctr = nullptr;
   char* arena = nullptr;
   size_t arena_cap = 0, arena_used = 0;
+  unsigned* stats = nullptr;  // MagStat pool: 2 words per bound matrix of a walk
+  size_t stats_cap = 0, stats_used = 0;
+  double *sh_send = nullptr, *sh_recv = nullptr;  // sharding exchange buffers
+  size_t sh_cap = 0;                              // doubles per rank
   int* h_int = nullptr;  // pinned
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -206,6 +216,9 @@ struct Ctx {
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : owned) cudaFree(p);
     if (arena) cudaFree(arena);
+    if (stats) cudaFree(stats);
+    if (sh_send) cudaFree(sh_send);
+    if (sh_recv) cudaFree(sh_recv);
     if (h_int) cudaFreeHost(h_int);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -259,6 +272,7 @@ const char* kProfNames[PROF_N] = {"forward", "seed", "init", "chain_affine", "de
                                   "offer", "writeback"};
 thread_local double g_prof_ms[PROF_N];
 thread_local long long g_prof_n[PROF_N];
+thread_local double g_gap_ms[PROF_N];  // device idle (or unprofiled work) before each class
 
 cudaEvent_t take_event(Ctx* n) {
   while (n->ev_pool.size() <= n->ev_used) {
@@ -479,11 +493,24 @@ struct Walker {
 
   int alloc_rows() const { return dry ? (both ? 2 : 1) : nrows(); }
 
+  size_t dry_stats = 0;
+  unsigned* stat_take() {
+    if (dry) {
+      ++dry_stats;
+      return nullptr;
+    }
+    if (n->stats_used + 2 > n->stats_cap) return nullptr;  // consumers then use the exact ops
+    unsigned* p = n->stats + n->stats_used;
+    n->stats_used += 2;
+    return p;
+  }
+
   Mat alloc(const Frame& f, bool withK) {
     Mat m;
     m.f = f;
     m.cells = frame_cells(fdev(n, f, q));
     m.phys = alloc_rows();
+    m.stat = stat_take();
     m.lo = arena_take((size_t)m.phys * m.cells * sizeof(double));
     m.hi = arena_take((size_t)m.phys * m.cells * sizeof(double));
     if (withK) m.K = arena_take((size_t)m.phys * 4 * sizeof(double));
@@ -703,7 +730,7 @@ Frame initial_frame(const Ctx* n, int t, bool affine) {
 // bump allocator reset per chunk, so this is the walk's total) and the number
 // of allocations (each may round up by < 256 B).
 struct WalkSize {
-  size_t per_row, allocs;
+  size_t per_row, allocs, stats;
 };
 
 WalkSize walk_size(Ctx* n, int t, bool affine, bool both) {
@@ -714,7 +741,21 @@ WalkSize walk_size(Ctx* n, int t, bool affine, bool both) {
   w.st = &dummy;
   Mat m = w.alloc(initial_frame(n, t, affine), true);
   w.walk(m, 0, false);
-  return WalkSize{w.dry_peak, w.dry_allocs};
+  return WalkSize{w.dry_peak, w.dry_allocs, w.dry_stats};
+}
+
+// A fresh statistics pool for one walk: `count` matrices, all slots reset.
+void reset_stats(Ctx* n, size_t count) {
+  const size_t words = 2 * std::max<size_t>(count, 1);
+  if (words > n->stats_cap) {
+    if (n->stats) cudaFree(n->stats);
+    n->stats = nullptr;
+    n->stats_cap = 0;
+    ck(cudaMalloc(&n->stats, words * sizeof(unsigned)), "stats");
+    n->stats_cap = words;
+  }
+  ck(cudaMemsetAsync(n->stats, 0xFF, words * sizeof(unsigned), n->stream), "memset");
+  n->stats_used = 0;
 }
 
 void ensure_arena(Ctx* n, size_t bytes) {
@@ -729,6 +770,40 @@ void ensure_arena(Ctx* n, size_t bytes) {
 long long budget_of(const Ctx* n) {
   if (n->opt.memory_budget > 0) return n->opt.memory_budget;
   return n->budget > 0 ? n->budget : (16ll << 30);
+}
+
+// ---------------------------------------------------------------------------
+// Row sharding (pc_net_set_sharding): slices and the all-gather exchange.
+
+inline long long slice_begin(long long n, int r, int w) { return n * r / w; }
+
+void ensure_shard_buffers(Ctx* n, size_t per_rank_doubles) {
+  if (per_rank_doubles <= n->sh_cap) return;
+  if (n->sh_send) cudaFree(n->sh_send);
+  if (n->sh_recv) cudaFree(n->sh_recv);
+  n->sh_send = n->sh_recv = nullptr;
+  n->sh_cap = 0;
+  ck(cudaMalloc(&n->sh_send, per_rank_doubles * sizeof(double)), "shard buffers");
+  ck(cudaMalloc(&n->sh_recv, per_rank_doubles * sizeof(double) * n->net->shard_world), "shard buffers");
+  n->sh_cap = per_rank_doubles;
+}
+
+void exchange(Ctx* n, size_t bytes) {
+  const pc_net* net = n->net;
+  if (net->allgather(net->allgather_user, n->sh_send, n->sh_recv, bytes, (void*)n->stream) != 0)
+    throw StatusError(PC_ERR_CUDA, "sharding: allgather callback failed");
+}
+
+// Gather every rank's slice of `width` doubles per row of dst (row = live[g]
+// or g) so all ranks hold the full array.
+void allgather_rows(Ctx* n, const int* live, int n_rows, int width, double* dst) {
+  const int W = n->net->shard_world, r = n->net->shard_rank;
+  const int per = (n_rows + W - 1) / W;
+  ensure_shard_buffers(n, (size_t)per * width);
+  const int b = (int)slice_begin(n_rows, r, W), e = (int)slice_begin(n_rows, r + 1, W);
+  launch_shard_pack(n->stream, live, b, e - b, width, dst, n->sh_send);
+  exchange(n, (size_t)per * width * sizeof(double));
+  launch_shard_unpack(n->stream, live, n_rows, W, per, width, n->sh_recv, dst);
 }
 
 // run_backsubstitution (backsub.hpp:993-1065)
@@ -747,16 +822,21 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   const int n_live = n->h_int[0];
   st->rows_total += N;
   const bool affine = Q.kind == KIND_DENSE || Q.kind == KIND_CONV;
-  if (n_live > 0) {
+  // this rank's slice of the live rows (all of them unsharded)
+  const int W = n->net->shard_world;
+  const long long lb = slice_begin(n_live, n->net->shard_rank, W);
+  const long long le = slice_begin(n_live, n->net->shard_rank + 1, W);
+  if (le > lb) {
     const WalkSize ws = walk_size(n, t, affine, true);
     long long chunk = n->opt.chunk_rows > 0
                           ? n->opt.chunk_rows
                           : std::max<long long>(1, budget_of(n) / (long long)ws.per_row);
-    chunk = std::min<long long>(chunk, n_live);
+    chunk = std::min<long long>(chunk, le - lb);
     ensure_arena(n, ws.per_row * (size_t)chunk + 256 * ws.allocs + (1 << 20));
-    for (long long base = 0; base < n_live; base += chunk) {
-      const int R = (int)std::min<long long>(chunk, n_live - base);
+    for (long long base = lb; base < le; base += chunk) {
+      const int R = (int)std::min<long long>(chunk, le - base);
       n->arena_used = 0;
+      reset_stats(n, ws.stats);
       Walker w{n, s, t};
       w.R = R;
       w.both = true;
@@ -771,13 +851,14 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
       Frame f0 = initial_frame(n, t, affine);
       Mat m = w.alloc(f0, true);
       if (affine)
-        launch_init_affine(s, Q.d, w.rows(), fdev(n, f0, t), n->dev + o, MatDev{m.lo, m.hi, m.K, m.cells});
+        launch_init_affine(s, Q.d, w.rows(), fdev(n, f0, t), n->dev + o, md(m));
       else
-        launch_init_identity(s, w.rows(), fdev(n, f0, t), MatDev{m.lo, m.hi, m.K, m.cells});
+        launch_init_identity(s, w.rows(), fdev(n, f0, t), md(m));
       if (affine) w.checkpoint(m);  // the init itself is an affine step (:1056)
       w.walk(m, 0, true);
     }
   }
+  if (W > 1 && n_live > 0) allgather_rows(n, n->live, n_live, 4, n->cand);
   ++n->gen;  // refresh round: the write-back marks what this pass changed
   prof_begin(n, PROF_WRITEBACK);
   launch_writeback(s, N, Q.out_c, t, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
@@ -796,26 +877,43 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
   std::vector<int> cls;
   for (int j = 0; j < n->n_out; ++j)
     if (j != label) cls.push_back(j);
-  ck(cudaMemcpyAsync(n->rowq[0], cls.data(), sizeof(int) * nr, cudaMemcpyHostToDevice, s), "h2d");
-  ck(cudaMemsetAsync(n->has, 0, nr, s), "memset");
-  const WalkSize ws = walk_size(n, out, false, false);
-  ensure_arena(n, ws.per_row * (size_t)nr + 256 * ws.allocs + (1 << 20));
-  n->arena_used = 0;
-  Walker w{n, s, out};
-  w.R = nr;
-  w.both = false;
-  w.margin = true;
-  w.st = st;
-  w.row_q = n->rowq[0];
-  Frame f0 = dense_frame(out);
-  Mat m = w.alloc(f0, true);
-  launch_init_margin(s, label, n->n_out, MatDev{m.lo, m.hi, m.K, m.cells});
-  w.walk(m, 0, true);
-  ck(cudaMemcpyAsync(n->h_int + 4, n->has, nr, cudaMemcpyDeviceToHost, s), "d2h");
-  ck(cudaMemcpyAsync(margins_host, n->best, sizeof(double) * nr, cudaMemcpyDeviceToHost, s), "d2h");
+  // this rank's slice of the margin rows (all of them unsharded)
+  const int W = n->net->shard_world;
+  const int mb = (int)slice_begin(nr, n->net->shard_rank, W);
+  const int me = (int)slice_begin(nr, n->net->shard_rank + 1, W);
+  const int R = me - mb;
+  if (R > 0) {
+    ck(cudaMemcpyAsync(n->rowq[0], cls.data() + mb, sizeof(int) * R, cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemsetAsync(n->has, 0, R, s), "memset");
+    const WalkSize ws = walk_size(n, out, false, false);
+    ensure_arena(n, ws.per_row * (size_t)R + 256 * ws.allocs + (1 << 20));
+    n->arena_used = 0;
+    reset_stats(n, ws.stats);
+    Walker w{n, s, out};
+    w.R = R;
+    w.both = false;
+    w.margin = true;
+    w.st = st;
+    w.row_q = n->rowq[0];
+    Frame f0 = dense_frame(out);
+    Mat m = w.alloc(f0, true);
+    launch_init_margin(s, label, n->n_out, mb, R, md(m));
+    w.walk(m, 0, true);
+    ck(cudaMemcpyAsync(n->h_int + 4, n->has, R, cudaMemcpyDeviceToHost, s), "d2h");
+  }
+  double* best = n->best;
+  if (W > 1) {  // every rank's best values, in class order (8 B per margin row)
+    const int per = (nr + W - 1) / W;
+    ensure_shard_buffers(n, (size_t)per);
+    ck(cudaMemcpyAsync(n->sh_send, n->best, sizeof(double) * R, cudaMemcpyDeviceToDevice, s), "d2d");
+    exchange(n, (size_t)per * sizeof(double));
+    launch_shard_unpack(s, nullptr, nr, W, per, 1, n->sh_recv, n->vals);
+    best = n->vals;
+  }
+  ck(cudaMemcpyAsync(margins_host, best, sizeof(double) * nr, cudaMemcpyDeviceToHost, s), "d2h");
   ck(cudaStreamSynchronize(s), "sync");
   const char* has = reinterpret_cast<const char*>(n->h_int + 4);
-  for (int r = 0; r < nr; ++r)
+  for (int r = 0; r < R; ++r)
     if (!has[r]) throw StatusError(PC_ERR_LOGIC, "margin pass produced no candidate");
 }
 
@@ -858,6 +956,28 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
   Counters c{};
   ck(cudaMemcpyAsync(&c, n->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s), "d2h");
   ck(cudaStreamSynchronize(s), "sync");
+  const int W = n->net->shard_world;
+  if (W > 1) {
+    // per-rank work counters (walk freezes, madds, checkpoints, dense-equivalent
+    // GBC work) add up; pre-freezes and rows_total are identical on every rank
+    unsigned long long h[8] = {c.dense_madds, c.gbc_madds, c.frozen, 0,
+                               (unsigned long long)st->checkpoints,
+                               (unsigned long long)st->gbc_dense_equiv, 0, 0};
+    ensure_shard_buffers(n, 8);
+    ck(cudaMemcpyAsync(n->sh_send, h, sizeof(h), cudaMemcpyHostToDevice, s), "h2d");
+    exchange(n, sizeof(h));
+    std::vector<unsigned long long> all((size_t)8 * W);
+    ck(cudaMemcpyAsync(all.data(), n->sh_recv, all.size() * 8, cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+    unsigned long long sum[8] = {0};
+    for (int r = 0; r < W; ++r)
+      for (int k = 0; k < 8; ++k) sum[k] += all[(size_t)8 * r + k];
+    c.dense_madds = sum[0];
+    c.gbc_madds = sum[1];
+    c.frozen = sum[2];
+    st->checkpoints = (long long)sum[4];
+    st->gbc_dense_equiv = (long long)sum[5];
+  }
   st->dense_madds += (long long)c.dense_madds;
   st->gbc_madds += (long long)c.gbc_madds;
   st->rows_terminated_early += (long long)(c.frozen + c.pad);
@@ -928,12 +1048,19 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     for (int c = 0; c < PROF_N; ++c) {
       g_prof_ms[c] = 0;
       g_prof_n[c] = 0;
+      g_gap_ms[c] = 0;
     }
-    for (const auto& pe : n->prof) {
+    for (size_t k = 0; k < n->prof.size(); ++k) {
+      const auto& pe = n->prof[k];
       float d = 0;
       cudaEventElapsedTime(&d, n->ev_pool[pe.second], n->ev_pool[pe.second + 1]);
       g_prof_ms[pe.first] += d;
       g_prof_n[pe.first] += 1;
+      if (k) {
+        float gap = 0;
+        cudaEventElapsedTime(&gap, n->ev_pool[n->prof[k - 1].second + 1], n->ev_pool[pe.second]);
+        g_gap_ms[pe.first] += gap;
+      }
     }
     if (label >= 0) {
       bool v = true;
@@ -1055,7 +1182,16 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
       d.in_w = l.in_w; d.in_h = l.in_h; d.in_c = l.in_c;
       d.out_w = l.out_w; d.out_h = l.out_h; d.out_c = l.out_c;
       d.fw = l.fw; d.fh = l.fh; d.sw = l.sw; d.sh = l.sh; d.pw = l.pw; d.ph = l.ph;
+      d.wmin = d.wmax = 1.0;
       if (l.kind == KIND_DENSE || l.kind == KIND_CONV) {
+        bool any = false;
+        for (double w : l.W)
+          if (w != 0.0) {
+            const double a = std::fabs(w);
+            if (!any || a < d.wmin) d.wmin = a;
+            if (!any || a > d.wmax) d.wmax = a;
+            any = true;
+          }
         double* b = n->dalloc<double>(l.bias.size());
         ck(cudaMemcpy(b, l.bias.data(), l.bias.size() * 8, cudaMemcpyHostToDevice), "h2d");
         d.bias = b;
@@ -1148,7 +1284,8 @@ int pc_last_profile(char* buf, int len) {
   for (int c = 0; c < PROF_N; ++c) {
     if (c) j += ", ";
     j += "\"" + std::string(kProfNames[c]) + "\": [" + std::to_string(g_prof_n[c]) + ", " +
-         std::to_string(g_prof_ms[c]) + "]";
+         std::to_string(g_prof_ms[c]) + "], \"gap:" + kProfNames[c] + "\": [0, " +
+         std::to_string(g_gap_ms[c]) + "]";
   }
   j += "}";
   if (buf && len > 0) {
@@ -1181,6 +1318,10 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
                             double* margins, pc_stats* stats, double* device_ms) {
   if (!net || n_images < 0 || !lo || !up || !labels) {
     g_err = "invalid batch arguments";
+    return PC_ERR_INVALID_ARGUMENT;
+  }
+  if (net->shard_world > 1) {
+    g_err = "sharding: pc_net_test_batch runs images concurrently; use pc_net_test on a sharded net";
     return PC_ERR_INVALID_ARGUMENT;
   }
   return guard([&] {
@@ -1258,6 +1399,19 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
     g_last_launches = launches.load();
     if (err_code != PC_OK) throw StatusError(err_code, err);
   });
+}
+
+pc_status pc_net_set_sharding(pc_net* net, int rank, int world, pc_allgather_fn allgather,
+                              void* user) {
+  if (!net || world < 1 || rank < 0 || rank >= world || (world > 1 && !allgather)) {
+    g_err = "sharding: need 0 <= rank < world and an allgather callback";
+    return PC_ERR_INVALID_ARGUMENT;
+  }
+  net->shard_rank = world > 1 ? rank : 0;
+  net->shard_world = world;
+  net->allgather = world > 1 ? allgather : nullptr;
+  net->allgather_user = world > 1 ? user : nullptr;
+  return PC_OK;
 }
 
 pc_status pc_net_test_device(pc_net* n, const double* d_lo, const double* d_up, int label,

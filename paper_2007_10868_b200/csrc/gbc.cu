@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256)
   const double* ihi = in.hi + phys_row(in, i) * in.cells;
   double* olo = out.lo + (size_t)i * out.cells;
   double* ohi = out.hi + (size_t)i * out.cells;
+  MagAcc mag;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.tasks;
        t += (long long)gridDim.x * blockDim.x) {
     const int cg = (int)(t % g.nq);
@@ -182,7 +183,16 @@ __global__ void __launch_bounds__(256)
       gbc_task_exact(g, FT, ilo, ihi, bw, bh, iy, ix0, npos, ci0, olo, ohi, y, fo.S_w, first);
     else
       gbc_store(g, olo, ohi, y, fo.S_w, first, npos, ci0, lo, hi);
+    // statistics of this task's outputs (read back: the exact path stores directly)
+    for (int k = 0; k < npos; ++k) {
+      const size_t o = ((size_t)y * fo.S_w + first + (size_t)k * g.sw) * g.cin + ci0;
+      for (int j = 0; j < kGQ && ci0 + j < g.cin; ++j) {
+        mag.add(olo[o + j]);
+        mag.add(ohi[o + j]);
+      }
+    }
   }
+  mag.flush(out.stat);
 }
 
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,

@@ -507,6 +507,7 @@ __global__ void k_init_affine(LayerDev Q, RowsDev rows, FrameDev f, const double
   const long long cells = out.cells;
   double* lo = out.lo + (size_t)i * cells;
   double* hi = out.hi + (size_t)i * cells;
+  MagAcc mag;
   if (Q.kind == KIND_DENSE) {
     const long long n_in = cells;
     for (long long t = blockIdx.x * blockDim.x + threadIdx.x; t < n_in;
@@ -514,6 +515,7 @@ __global__ void k_init_affine(LayerDev Q, RowsDev rows, FrameDev f, const double
       const double w = Q.W[(size_t)q * n_in + t];
       lo[t] = w;
       hi[t] = w;
+      mag.add(w);
     }
   } else {
     const int cq = q % Q.out_c;
@@ -533,8 +535,10 @@ __global__ void k_init_affine(LayerDev Q, RowsDev rows, FrameDev f, const double
         v = Q.F[((size_t)(fy * Q.fw + fx) * Q.in_c + ci) * Q.out_c + cq];
       lo[c] = v;
       hi[c] = v;
+      mag.add(v);
     }
   }
+  mag.flush(out.stat);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const double b = Q.bias[Q.kind == KIND_DENSE ? q : q % Q.out_c];
     Iv k{b, b};
@@ -562,12 +566,15 @@ __global__ void k_init_identity(RowsDev rows, FrameDev f, MatDev out) {
   double* hi = out.hi + (size_t)i * cells;
   // Dense frame (1x1 grid): cell q; cuboid 1x1 window: cell = channel.
   const long long hot = (f.G_w == 1 && f.G_h == 1) ? q : q % f.C;
+  MagAcc mag;
   for (long long c = blockIdx.x * blockDim.x + threadIdx.x; c < cells;
        c += (long long)gridDim.x * blockDim.x) {
     const double v = (c == hot) ? 1.0 : 0.0;
     lo[c] = v;
     hi[c] = v;
+    mag.add(v);
   }
+  mag.flush(out.stat);
   if (blockIdx.x == 0 && threadIdx.x < 4) out.K[4 * (size_t)i + threadIdx.x] = 0.0;
 }
 
@@ -577,20 +584,26 @@ void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f
   ++g_launches;
 }
 
-// init_margin_rows: +1 at label, -1 at class j, ascending j != label.
-__global__ void k_init_margin(int label, int n_out, MatDev out) {
+// init_margin_rows: +1 at label, -1 at class j, ascending j != label. Rows
+// [first, first + gridDim.x) of the margin rows (a rank's slice when sharded).
+__global__ void k_init_margin(int label, int n_out, int first, MatDev out) {
   const int r = blockIdx.x;
-  const int j = r < label ? r : r + 1;
+  const int g = first + r;
+  const int j = g < label ? g : g + 1;
+  MagAcc mag;
   for (int c = threadIdx.x; c < n_out; c += blockDim.x) {
     const double v = (c == label) ? 1.0 : (c == j ? -1.0 : 0.0);
     out.lo[(size_t)r * n_out + c] = v;
     out.hi[(size_t)r * n_out + c] = v;
+    mag.add(v);
   }
+  mag.flush(out.stat);
   if (threadIdx.x < 4) out.K[4 * r + threadIdx.x] = 0.0;
 }
 
-void launch_init_margin(cudaStream_t s, int label, int n_out, MatDev out) {
-  k_init_margin<<<n_out - 1, 128, 0, s>>>(label, n_out, out);
+void launch_init_margin(cudaStream_t s, int label, int n_out, int first, int count, MatDev out) {
+  if (count <= 0) return;
+  k_init_margin<<<count, 128, 0, s>>>(label, n_out, first, out);
   ++g_launches;
 }
 
@@ -673,12 +686,18 @@ __device__ __forceinline__ bool chain_affine_row(const LayerDev& L, int is_conv,
         }
       }
     }
-    s_t[0][lane] = tl;
-    s_t[1][lane] = th;
-    s_t[2][lane] = td;
+    // compact the contributing cells (ascending) so the fold skips the rest
+    const bool v = (tl == tl) | (th == th) | (td == td);
+    const unsigned mask = __ballot_sync(0xffffffffu, v);
+    if (v) {
+      const int p = __popc(mask & ((1u << lane) - 1u));
+      s_t[0][p] = tl;
+      s_t[1][p] = th;
+      s_t[2][p] = td;
+    }
     __syncwarp();
     if (lane < 5) {
-      const int n = (int)min((long long)32, cells - c0);
+      const int n = __popc(mask);
       for (int k = 0; k < n; ++k) acc = fold<FAST>(acc, s_t[arr][k], up);
     }
     __syncwarp();
@@ -768,13 +787,18 @@ __device__ __forceinline__ bool chain_relu_row(const FrameDev& f, int bw, int bh
         if (!iv_zero(o1)) { t1l = o1.lo; t1h = o1.hi; }
       }
     }
-    s_t[0][0][lane] = t0l;
-    s_t[0][1][lane] = t0h;
-    s_t[1][0][lane] = t1l;
-    s_t[1][1][lane] = t1h;
+    const bool v = (t0l == t0l) | (t0h == t0h) | (t1l == t1l) | (t1h == t1h);
+    const unsigned mask = __ballot_sync(0xffffffffu, v);
+    if (v) {
+      const int p = __popc(mask & ((1u << lane) - 1u));
+      s_t[0][0][p] = t0l;
+      s_t[0][1][p] = t0h;
+      s_t[1][0][p] = t1l;
+      s_t[1][1][p] = t1h;
+    }
     __syncwarp();
     if (lane < 4) {
-      const int n = (int)min((long long)32, cells - c0);
+      const int n = __popc(mask);
       for (int k = 0; k < n; ++k) {
         acc = fold<FAST>(acc, s_t[0][arr][k], up);
         acc = fold<FAST>(acc, s_t[1][arr][k], up);
@@ -823,7 +847,7 @@ void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, M
 // cell in ascending order. Lane 0: padded track (constant, bounds); lane 1:
 // raw track (constant_raw, raw bounds).
 template <bool FAST>
-__device__ __forceinline__ bool conc_row(const FrameDev& f, int bw, int bh, bool upper,
+__device__ __forceinline__ bool conc_row(const FrameDev& f, int bw, int bh, bool upper, bool skip0,
                                          long long cells, const double* lo, const double* hi,
                                          const double* blo, const double* bhi, const double* rlo,
                                          const double* rhi, double acc, double (*s_t)[32],
@@ -847,13 +871,21 @@ __device__ __forceinline__ bool conc_row(const FrameDev& f, int bw, int bh, bool
           tp = upper ? corner_hi(c, B) : corner_lo(c, B);
           tr = upper ? corner_hi(c, Br) : corner_lo(c, Br);
         }
+        // a +0 term leaves a non-(-0) accumulator unchanged: skip it
+        if (skip0 && __double_as_longlong(tp) == 0) tp = PC_NAN;
+        if (skip0 && __double_as_longlong(tr) == 0) tr = PC_NAN;
       }
     }
-    s_t[0][lane] = tp;
-    s_t[1][lane] = tr;
+    const bool v = (tp == tp) | (tr == tr);
+    const unsigned mask = __ballot_sync(0xffffffffu, v);
+    if (v) {
+      const int p = __popc(mask & ((1u << lane) - 1u));
+      s_t[0][p] = tp;
+      s_t[1][p] = tr;
+    }
     __syncwarp();
     if (lane < 2) {
-      const int n = (int)min((long long)32, cells - c0);
+      const int n = __popc(mask);
       for (int k = 0; k < n; ++k) acc = fold<FAST>(acc, s_t[lane][k], upper);
     }
     __syncwarp();
@@ -882,8 +914,11 @@ __global__ void __launch_bounds__(32 * kChainWarps)
   if (lane == 0) acc0 = upper ? K[1] : K[0];
   if (lane == 1) acc0 = upper ? K[3] : K[2];
   double acc;
-  if (conc_row<true>(f, bw, bh, upper, cells, lo, hi, blo, bhi, rlo, rhi, acc0, s_t[warp], lane, acc))
-    conc_row<false>(f, bw, bh, upper, cells, lo, hi, blo, bhi, rlo, rhi, acc0, s_t[warp], lane, acc);
+  const double a0 = upper ? K[1] : K[0], a1 = upper ? K[3] : K[2];
+  const long long nz = (long long)0x8000000000000000ULL;
+  const bool skip0 = __double_as_longlong(a0) != nz && __double_as_longlong(a1) != nz;
+  if (conc_row<true>(f, bw, bh, upper, skip0, cells, lo, hi, blo, bhi, rlo, rhi, acc0, s_t[warp], lane, acc))
+    conc_row<false>(f, bw, bh, upper, skip0, cells, lo, hi, blo, bhi, rlo, rhi, acc0, s_t[warp], lane, acc);
   if (lane == 0) vals[i] = acc;
   if (lane == 1) rvals[i] = acc;
 }
@@ -933,15 +968,31 @@ __device__ __forceinline__ void madd_exact(double w, double clo, double chi, dou
   hi = add_up(hi, mul_up(b, w));
 }
 
+template <int TM, bool BAND>
+__device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const double (*s_ah)[kDK],
+                                           const double (*s_w)[kDC], int kn, int tx, double* lo,
+                                           double* hi, bool* bad) {
+#pragma unroll 2
+  for (int kk = 0; kk < kn; ++kk) {
+    const double w = s_w[kk][tx];
+#pragma unroll
+    for (int u = 0; u < TM; ++u) {
+      if (BAND) madd_band(w, s_al[u][kk], s_ah[u][kk], lo[u], hi[u]);
+      else madd_fast(w, s_al[u][kk], s_ah[u][kk], lo[u], hi[u], bad[u]);
+    }
+  }
+}
+
 template <int TM>
 __global__ void __launch_bounds__(kDC)
     k_dense_coef(const double* __restrict__ W, int n_k, int n_in, int nrows, MatDev in,
-                 MatDev out) {
+                 MatDev out, double wmin, double wmax) {
   __shared__ double s_al[TM][kDK], s_ah[TM][kDK];
   __shared__ double s_w[kDK][kDC];
   const int tx = threadIdx.x;
   const int col = blockIdx.x * kDC + tx;
   const int r0 = blockIdx.y * TM;
+  const bool band = products_in_band(in.stat, wmin, wmax);
   double lo[TM], hi[TM];
   bool bad[TM];
 #pragma unroll
@@ -964,14 +1015,11 @@ __global__ void __launch_bounds__(kDC)
     }
     __syncthreads();
     const int kn = min(kDK, n_k - k0);
-#pragma unroll 2
-    for (int kk = 0; kk < kn; ++kk) {
-      const double w = s_w[kk][tx];
-#pragma unroll
-      for (int u = 0; u < TM; ++u) madd_fast(w, s_al[u][kk], s_ah[u][kk], lo[u], hi[u], bad[u]);
-    }
+    if (band) dense_slab<TM, true>(s_al, s_ah, s_w, kn, tx, lo, hi, bad);
+    else dense_slab<TM, false>(s_al, s_ah, s_w, kn, tx, lo, hi, bad);
   }
   if (col >= n_in) return;
+  MagAcc mag;
 #pragma unroll
   for (int u = 0; u < TM; ++u) {
     const int r = r0 + u;
@@ -984,7 +1032,10 @@ __global__ void __launch_bounds__(kDC)
     }
     out.lo[(size_t)r * n_in + col] = lo[u];
     out.hi[(size_t)r * n_in + col] = hi[u];
+    mag.add(lo[u]);
+    mag.add(hi[u]);
   }
+  mag.flush(out.stat);
 }
 
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, MatDev out,
@@ -995,10 +1046,10 @@ void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, 
   // bounds latency); many rows: 4 rows per thread for weight reuse.
   if (nrows <= 64) {
     dim3 grid(cdiv(n_in, kDC), nrows);
-    k_dense_coef<1><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, nrows, in, out);
+    k_dense_coef<1><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, nrows, in, out, L.wmin, L.wmax);
   } else {
     dim3 grid(cdiv(n_in, kDC), cdiv(nrows, 4));
-    k_dense_coef<4><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, nrows, in, out);
+    k_dense_coef<4><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, nrows, in, out, L.wmin, L.wmax);
   }
   if (ev1) cudaEventRecord(ev1, s);
   ++g_launches;
@@ -1012,7 +1063,10 @@ void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, 
 // visits frame cells in (ch, cw, d) order).
 __device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-template <bool FAST>
+// MODE 2: band multiply-add (products proven in band for the launch);
+// 1: fast ops with per-product band checks (bad -> recompute with 0);
+// 0: the exact ops.
+template <int MODE>
 __device__ __forceinline__ Iv gbc_gather(const LayerDev& L, const FrameDev& fi, int bw, int bh,
                                          const double* ilo, const double* ihi, int iy, int ix,
                                          int ci, bool& bad) {
@@ -1030,10 +1084,17 @@ __device__ __forceinline__ Iv gbc_gather(const LayerDev& L, const FrameDev& fi, 
       const int fx = ix + L.pw - aw * L.sw;
       const size_t cb = ((size_t)(ah - bh) * fi.S_w + (aw - bw)) * cout;
       const double* wp = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ci;
-      if (FAST) {
+      if (MODE > 0) {
+        // A zero coefficient adds the zero interval (skipped by the reference's
+        // iv_acc). Lanes of a warp share (iy, ix) when cin >= 32, so this
+        // branch is warp-uniform and skips the work.
 #pragma unroll 4
-        for (int d = 0; d < cout; ++d)
-          madd_fast(wp[(size_t)d * cin], ilo[cb + d], ihi[cb + d], lo, hi, bad);
+        for (int d = 0; d < cout; ++d) {
+          const double cl = ilo[cb + d], ch = ihi[cb + d];
+          if (cl == 0.0 && ch == 0.0) continue;
+          if (MODE == 2) madd_band(wp[(size_t)d * cin], cl, ch, lo, hi);
+          else madd_fast(wp[(size_t)d * cin], cl, ch, lo, hi, bad);
+        }
       } else {
         for (int d = 0; d < cout; ++d) madd_exact(wp[(size_t)d * cin], ilo[cb + d], ihi[cb + d], lo, hi);
       }
@@ -1054,6 +1115,8 @@ __global__ void __launch_bounds__(256)
   const double* ilo = in.lo + phys_row(in, i) * icells;
   const double* ihi = in.hi + phys_row(in, i) * icells;
   const int cin = L.in_c;
+  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  MagAcc mag;
   for (long long o = blockIdx.x * blockDim.x + threadIdx.x; o < ocells;
        o += (long long)gridDim.x * blockDim.x) {
     const int ci = (int)(o % cin);
@@ -1061,16 +1124,24 @@ __global__ void __launch_bounds__(256)
     const int y = (int)(o / ((long long)cin * fo.S_w));
     const int iy = nbh + y, ix = nbw + x;
     bool bad = false;
-    Iv acc = gbc_gather<true>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
-    if (bad) acc = gbc_gather<false>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+    Iv acc;
+    if (band) {
+      acc = gbc_gather<2>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+    } else {
+      acc = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+      if (bad) acc = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+    }
     out.lo[(size_t)i * ocells + o] = acc.lo;
     out.hi[(size_t)i * ocells + o] = acc.hi;
+    mag.add(acc.lo);
+    mag.add(acc.hi);
   }
+  mag.flush(out.stat);
 }
 
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out) {
-  static const int tiled = env_int("PC_GBC", 1);
+  static const int tiled = env_int("PC_GBC", 0);
   if (tiled) {
     launch_gbc_tile(s, L, rows, fin, fout, in, out);
     return;
@@ -1112,6 +1183,7 @@ __global__ void __launch_bounds__(256)
   const long long cells = in.cells;
   const double* lo = in.lo + phys_row(in, i) * cells;
   const double* hi = in.hi + phys_row(in, i) * cells;
+  MagAcc mag;
   for (long long cell = blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
        cell += (long long)gridDim.x * blockDim.x) {
     const Iv c{lo[cell], hi[cell]};
@@ -1131,7 +1203,10 @@ __global__ void __launch_bounds__(256)
     }
     out.lo[(size_t)i * cells + cell] = r.lo;
     out.hi[(size_t)i * cells + cell] = r.hi;
+    mag.add(r.lo);
+    mag.add(r.hi);
   }
+  mag.flush(out.stat);
 }
 
 void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev in,
@@ -1159,6 +1234,7 @@ __global__ void __launch_bounds__(256)
   frame_base(fu, q, ubw, ubh);
   const long long cells = out.cells;
   const int C = fu.C;
+  MagAcc mag;
   for (long long cell = blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
        cell += (long long)gridDim.x * blockDim.x) {
     const int cc = (int)(cell % C);
@@ -1183,7 +1259,10 @@ __global__ void __launch_bounds__(256)
     iv_acc(n, cb);
     out.lo[(size_t)i * cells + cell] = n.lo;
     out.hi[(size_t)i * cells + cell] = n.hi;
+    mag.add(n.lo);
+    mag.add(n.hi);
   }
+  mag.flush(out.stat);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const double* Ka = a.K + 4 * phys_row(a, i);
     const double* Kb = b.K + 4 * phys_row(b, i);
@@ -1260,6 +1339,44 @@ void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals
                   int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr) {
   k_offer<<<1, kScanThreads, 0, s>>>(rows, R, vals, rvals, cand, frozen, allow_freeze, early_term,
                                      map, new_R, new_row_q, ctr);
+  ++g_launches;
+}
+
+// Row sharding (engine.cu run_pass / run_margin). width doubles per row;
+// live == nullptr: rows are identity-indexed.
+__global__ void k_shard_pack(const int* live, int b, int cnt, int width, const double* src,
+                             double* send) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cnt * width) return;
+  const int k = e / width, c = e % width;
+  const int row = live ? live[b + k] : b + k;
+  send[e] = src[(size_t)row * width + c];
+}
+
+__global__ void k_shard_unpack(const int* live, int n_live, int world, int per, int width,
+                               const double* recv, double* dst) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)world * per * width) return;
+  const int c = (int)(e % width);
+  const long long rk = e / width;
+  const int r = (int)(rk / per), k = (int)(rk % per);
+  const int b = (int)((long long)n_live * r / world), nb = (int)((long long)n_live * (r + 1) / world);
+  if (k >= nb - b) return;
+  const int row = live ? live[b + k] : b + k;
+  dst[(size_t)row * width + c] = recv[e];
+}
+
+void launch_shard_pack(cudaStream_t s, const int* live, int b, int cnt, int width,
+                       const double* src, double* send) {
+  if (cnt <= 0) return;
+  k_shard_pack<<<cdiv((long long)cnt * width, 256), 256, 0, s>>>(live, b, cnt, width, src, send);
+  ++g_launches;
+}
+
+void launch_shard_unpack(cudaStream_t s, const int* live, int n_live, int world, int per,
+                         int width, const double* recv, double* dst) {
+  k_shard_unpack<<<cdiv((long long)world * per * width, 256), 256, 0, s>>>(live, n_live, world, per,
+                                                                          width, recv, dst);
   ++g_launches;
 }
 

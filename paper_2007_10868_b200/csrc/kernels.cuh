@@ -19,6 +19,7 @@ struct LayerDev {
   const double* F;   // conv filter ((fy*fw+fx)*cin+ci)*cout+co (reference layout)
   const double* FT;  // conv filter ((fy*fw+fx)*cout+co)*cin+ci (back-substitution layout)
   const double* bias;
+  double wmin, wmax;  // smallest / largest nonzero |weight| (1, 1 if none)
 };
 
 // A frame = which cells of a layer a bound matrix row stores.
@@ -71,7 +72,71 @@ struct MatDev {
   double* K;
   long long cells;
   const int* src = nullptr;
+  // Magnitude statistics of the nonzero coefficients (see MagStat below);
+  // written by the kernel that produces the matrix, read by its consumer.
+  unsigned* stat = nullptr;
 };
+
+// ---------------------------------------------------------------------------
+// Magnitude statistics. key(x) = high 32 bits of |x| (exponent and top 20
+// mantissa bits), so keys order like magnitudes. stat[0] = min key over the
+// nonzero entries, stat[1] = ~(max key); both are reduced with atomicMin from
+// an initial 0xFFFFFFFF. A consumer proves from them (and the layer's weight
+// range) that every nonzero product |c*w| lies in [2^-499, 2^999]; then the
+// reference's exactness tests reduce to residual == 0 / RD == RU and the lean
+// "band" multiply-add below is bit-identical to the exact ops.
+struct MagAcc {
+  unsigned kmin = 0xFFFFFFFFu, kmaxinv = 0xFFFFFFFFu;
+  __device__ __forceinline__ void add(double x) {
+    const unsigned hi = (unsigned)__double2hiint(x) & 0x7FFFFFFFu;
+    if (hi | (unsigned)__double2loint(x)) {
+      kmin = min(kmin, hi);
+      kmaxinv = min(kmaxinv, ~hi);
+    }
+  }
+  // Warp-reduce over the lanes that reach this call, one atomic per warp.
+  __device__ __forceinline__ void flush(unsigned* stat) {
+    if (!stat) return;
+    const unsigned mask = __activemask();
+    const unsigned a = __reduce_min_sync(mask, kmin), b = __reduce_min_sync(mask, kmaxinv);
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1) && (a != 0xFFFFFFFFu || b != 0xFFFFFFFFu)) {
+      atomicMin(stat, a);
+      atomicMin(stat + 1, b);
+    }
+  }
+};
+
+__device__ __forceinline__ bool products_in_band(const unsigned* stat, double wmin, double wmax) {
+  if (!stat) return false;
+  const unsigned kmin = stat[0], kmax = ~stat[1];
+  if (kmin == 0xFFFFFFFFu) return true;  // no nonzero coefficient: every product is 0
+  const double cmin = __hiloint2double((int)kmin, 0);           // <= min |c|
+  const double cmax = __hiloint2double((int)kmax, (int)0xFFFFFFFFu);  // >= max |c|
+  return __dmul_rn(cmin, wmin) >= 0x1p-499 && __dmul_rn(cmax, wmax) <= 0x1p999;
+}
+
+// interval += c * w (backsub.hpp:385 / :481-482) for in-band operands (see
+// products_in_band), accumulators starting at +0 and fewer than 2^20 terms:
+// bit-identical to add_down(lo, mul_down(.)) / add_up(hi, mul_up(.)) with the
+// reference's zero skips (a zero factor adds an exact +-0, a no-op because the
+// accumulators are never -0). Exactness tests are the residual (integer test
+// on its bits) and RD == RU; outward steps are predicated.
+__device__ __forceinline__ bool bits_zero(double x) {
+  return (((unsigned)__double2hiint(x) << 1) | (unsigned)__double2loint(x)) == 0u;
+}
+__device__ __forceinline__ void madd_band(double w, double cl, double ch, double& lo, double& hi) {
+  const bool neg = __double2hiint(w) < 0;
+  const double a = neg ? ch : cl, b = neg ? cl : ch;
+  double pl = __dmul_rn(a, w), ph = __dmul_rn(b, w);
+  const double rl = __fma_rn(a, w, -pl), rh = __fma_rn(b, w, -ph);
+  if (!bits_zero(rl)) pl = __dadd_rd(pl, -4.9406564584124654e-324);
+  if (!bits_zero(rh)) ph = __dadd_ru(ph, 4.9406564584124654e-324);
+  double sl = __dadd_rn(lo, pl), sh = __dadd_rn(hi, ph);
+  if (__dadd_rd(lo, pl) != __dadd_ru(lo, pl)) sl = __dadd_rd(sl, -4.9406564584124654e-324);
+  if (__dadd_rd(hi, ph) != __dadd_ru(hi, ph)) sh = __dadd_ru(sh, 4.9406564584124654e-324);
+  lo = sl;
+  hi = sh;
+}
 
 __host__ __device__ __forceinline__ size_t phys_row(const MatDev& m, int i) {
   return (size_t)(m.src ? m.src[i] : i);
@@ -115,7 +180,7 @@ void launch_writeback(cudaStream_t s, int n, int C, int layer, const double* can
 void launch_init_affine(cudaStream_t s, const LayerDev& Q, const RowsDev& rows, const FrameDev& f,
                         const double* dev_q, MatDev out);
 void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev out);
-void launch_init_margin(cudaStream_t s, int label, int n_out, MatDev out);
+void launch_init_margin(cudaStream_t s, int label, int n_out, int first, int count, MatDev out);
 
 // Chains read the constants of m (through m.src) and write compact ones to Kout.
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
@@ -148,7 +213,7 @@ void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out);
 // Engine switches from the environment (read once): PC_GBC=0 selects the
-// one-output-per-thread conv kernel instead of the register-blocked one.
+// one-output-per-thread conv kernel (default), PC_GBC=1 the register-blocked one.
 int env_int(const char* name, int dflt);
 void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev in,
                       MatDev out, const double* relax);
@@ -161,6 +226,13 @@ void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals
                   const double* rvals, double* cand, char* frozen, int allow_freeze,
                   int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr);
 void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best, char* has);
+
+// Row sharding: pack this rank's slice of candidates (4 doubles per row, in
+// live order) / scatter every rank's slice back into cand.
+void launch_shard_pack(cudaStream_t s, const int* live, int b, int cnt, int width,
+                       const double* src, double* send);
+void launch_shard_unpack(cudaStream_t s, const int* live, int n_live, int world, int per,
+                         int width, const double* recv, double* dst);
 
 cudaError_t input_box_device(const double* center, int n, double eps, int clamp01, double* lo,
                              double* up);

@@ -187,6 +187,16 @@ class Verifier:
                                                ctypes.byref(st)))
         return bool(verified.value), margins[: self.n_out - 1], st.as_dict()
 
+    def enable_sharding(self, group=None):
+        """Row-shard every pass across the ranks of a torch.distributed group
+        (one process per GPU; results identical to unsharded). Returns (rank, world)."""
+        from . import sharding
+        return sharding.enable(self, group)
+
+    def disable_sharding(self):
+        from . import sharding
+        sharding.disable(self)
+
     @staticmethod
     def last_profile() -> dict:
         """Per-kernel-class {class: [launches, ms]} of the last call (PC_PROFILE=1)."""

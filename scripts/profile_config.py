@@ -28,9 +28,9 @@ for i, x in enumerate(X):
         continue  # warm-up
     t = v.last_timing()
     prof = v.last_profile()
-    tot = sum(ms for _, ms in prof.values())
+    tot = sum(ms for k, (_, ms) in prof.items() if not k.startswith("gap:"))
     print(json.dumps({"config": name, "image": i, "verified": verdict.verified, "wall_ms": round(wall, 2),
                       "device_ms": round(t["total_ms"], 2), "launches": t["launches"],
                       "stats": verdict.stats,
                       "classes": {k: [c, round(ms, 3), round(100 * ms / max(tot, 1e-9), 1)]
-                                  for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]) if c}}))
+                                  for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]) if c or ms > 0.05}}))
