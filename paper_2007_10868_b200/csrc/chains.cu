@@ -260,12 +260,16 @@ __device__ __forceinline__ double fold_row(G& g, const double* lo, const double*
 
 __global__ void __launch_bounds__(kCT)
     k_chain_affine_big(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, double* Kout,
-                       const double* dev, Counters* ctr) {
+                       const double* dev, Counters* ctr, const char* frozen) {
   extern __shared__ double buf[];
   __shared__ ChainShared sh;
   const int i = blockIdx.x;
   bool upper;
   const int q = row_query(rows, i, upper);
+  if (frozen && frozen[q]) return;
+  if (is_conv && threadIdx.x == 0)
+    atomicAdd(&ctr->gbc_dense_equiv, (unsigned long long)L.out_w * L.out_h * L.out_c *
+                                         ((unsigned long long)L.in_w * L.in_h * L.in_c));
   AffineGen g{L, is_conv, f, 0, 0, dev};
   if (is_conv) frame_base(f, q, g.bw, g.bh);
   const size_t pr = phys_row(m, i);
@@ -285,12 +289,14 @@ __global__ void __launch_bounds__(kCT)
 }
 
 __global__ void __launch_bounds__(kCT)
-    k_chain_relu_big(RowsDev rows, FrameDev f, MatDev m, double* Kout, const double* relax) {
+    k_chain_relu_big(RowsDev rows, FrameDev f, MatDev m, double* Kout, const double* relax,
+                     const char* frozen) {
   extern __shared__ double buf[];
   __shared__ ChainShared sh;
   const int i = blockIdx.x;
   bool upper;
   const int q = row_query(rows, i, upper);
+  if (frozen && frozen[q]) return;
   ReluGen g{f, 0, 0, upper, relax};
   frame_base(f, q, g.bw, g.bh);
   const size_t pr = phys_row(m, i);
@@ -301,12 +307,14 @@ __global__ void __launch_bounds__(kCT)
 
 __global__ void __launch_bounds__(kCT)
     k_concretize_big(RowsDev rows, FrameDev f, MatDev m, const double* blo, const double* bhi,
-                     const double* rlo, const double* rhi, double* vals, double* rvals) {
+                     const double* rlo, const double* rhi, double* vals, double* rvals,
+                     const char* frozen) {
   extern __shared__ double buf[];
   __shared__ ChainShared sh;
   const int i = blockIdx.x;
   bool upper;
   const int q = row_query(rows, i, upper);
+  if (frozen && frozen[q]) return;
   const size_t pr = phys_row(m, i);
   const double* K = m.K + 4 * pr;
   const double a0 = upper ? K[1] : K[0], a1 = upper ? K[3] : K[2];
@@ -339,26 +347,26 @@ static void set_attrs() {
 
 void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                              const FrameDev& fin, MatDev m, double* Kout, const double* dev,
-                             Counters* ctr) {
+                             Counters* ctr, const char* frozen) {
   set_attrs();
   k_chain_affine_big<<<rows.n, kCT, chain_smem<AffineGen>(), s>>>(L, is_conv ? 1 : 0, rows, fin, m,
-                                                                   Kout, dev, ctr);
+                                                                   Kout, dev, ctr, frozen);
   ++g_launches;
 }
 
 void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
-                           double* Kout, const double* relax) {
+                           double* Kout, const double* relax, const char* frozen) {
   set_attrs();
-  k_chain_relu_big<<<rows.n, kCT, chain_smem<ReluGen>(), s>>>(rows, f, m, Kout, relax);
+  k_chain_relu_big<<<rows.n, kCT, chain_smem<ReluGen>(), s>>>(rows, f, m, Kout, relax, frozen);
   ++g_launches;
 }
 
 void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            const double* blo, const double* bhi, const double* rlo,
-                           const double* rhi, double* vals, double* rvals) {
+                           const double* rhi, double* vals, double* rvals, const char* frozen) {
   set_attrs();
   k_concretize_big<<<rows.n, kCT, chain_smem<ConcGen>(), s>>>(rows, f, m, blo, bhi, rlo, rhi, vals,
-                                                               rvals);
+                                                               rvals, frozen);
   ++g_launches;
 }
 

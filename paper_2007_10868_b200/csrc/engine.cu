@@ -87,6 +87,7 @@ struct Mat {
   const int* src = nullptr;  // row map after a compaction (see MatDev::src)
   int phys = 0;              // physical rows in the buffers
   unsigned* stat = nullptr;  // magnitude statistics (MatDev::stat)
+  cudaEvent_t ready = nullptr;  // recorded on the coefficient stream after the coefficients
 };
 
 MatDev md(const Mat& m) {
@@ -142,7 +143,8 @@ struct Ctx {
   const int device;
   const bool timing, profile;
   long long budget = 0;  // workspace bytes for one pass (0: derive)
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // coefficient stream (and everything outside a walk)
+  cudaStream_t stream2 = nullptr;  // constants / concretisation / offers of a walk
   std::vector<void*> owned;
   int* gen_n = nullptr;
   int* gen_pos = nullptr;
@@ -163,6 +165,12 @@ struct Ctx {
   double *sh_send = nullptr, *sh_recv = nullptr;  // sharding exchange buffers
   size_t sh_cap = 0;                              // doubles per rank
   int* h_int = nullptr;  // pinned
+  // lazy compaction: per-checkpoint surviving-row counts (pinned) and events
+  static constexpr int kCkSlots = 64;
+  int* h_newR = nullptr;
+  cudaEvent_t ck_ev[kCkSlots] = {};
+  std::vector<cudaEvent_t> sync_pool;  // ordering events (no timing)
+  size_t sync_used = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<std::pair<int, size_t>> prof;  // (class, event index of the begin event)
@@ -182,6 +190,7 @@ struct Ctx {
 
   void init() {
     ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking), "stream");
     const int nl = (int)L.size();
     const size_t T = (size_t)total, M = (size_t)max_numel;
     blo = dalloc<double>(T);
@@ -210,18 +219,26 @@ struct Ctx {
     ck(cudaMemset(gen_pos, 0, (size_t)pofs[nl] * sizeof(int)), "memset");
     ck(cudaMemset(gen_l, 0, nl * sizeof(int)), "memset");
     ck(cudaMallocHost(&h_int, 64 + (size_t)n_out), "pinned");
+    ck(cudaMallocHost(&h_newR, sizeof(int) * kCkSlots), "pinned");
+    for (int k = 0; k < kCkSlots; ++k) ck(cudaEventCreateWithFlags(&ck_ev[k], cudaEventDisableTiming), "event");
   }
 
   ~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
+    if (stream2) cudaStreamSynchronize(stream2);
     for (void* p : owned) cudaFree(p);
     if (arena) cudaFree(arena);
     if (stats) cudaFree(stats);
     if (sh_send) cudaFree(sh_send);
     if (sh_recv) cudaFree(sh_recv);
     if (h_int) cudaFreeHost(h_int);
+    if (h_newR) cudaFreeHost(h_newR);
+    for (cudaEvent_t e : ck_ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : sync_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
+    if (stream2) cudaStreamDestroy(stream2);
   }
 };
 
@@ -283,14 +300,30 @@ cudaEvent_t take_event(Ctx* n) {
   return n->ev_pool[n->ev_used++];
 }
 
-void prof_begin(Ctx* n, int cls) {
+void prof_begin(Ctx* n, int cls, cudaStream_t st = nullptr) {
   if (!n->profile) return;
   n->prof.emplace_back(cls, n->ev_used);
-  ck(cudaEventRecord(take_event(n), n->stream), "event");
+  ck(cudaEventRecord(take_event(n), st ? st : n->stream), "event");
 }
-void prof_end(Ctx* n) {
+void prof_end(Ctx* n, cudaStream_t st = nullptr) {
   if (!n->profile) return;
-  ck(cudaEventRecord(take_event(n), n->stream), "event");
+  ck(cudaEventRecord(take_event(n), st ? st : n->stream), "event");
+}
+
+// Ordering between the coefficient stream and the constants stream.
+cudaEvent_t sync_event(Ctx* n) {
+  while (n->sync_pool.size() <= n->sync_used) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    n->sync_pool.push_back(e);
+  }
+  return n->sync_pool[n->sync_used++];
+}
+// `to` waits for everything enqueued on `from` so far.
+void stream_wait(Ctx* n, cudaStream_t to, cudaStream_t from) {
+  cudaEvent_t e = sync_event(n);
+  ck(cudaEventRecord(e, from), "event");
+  ck(cudaStreamWaitEvent(to, e, 0), "wait");
 }
 
 // ---------------------------------------------------------------------------
@@ -459,6 +492,20 @@ Frame dense_frame(int layer) {
 
 // ---------------------------------------------------------------------------
 // One walk context: a chunk of rows of one pass (or the margin rows).
+//
+// Two streams. The coefficient substitutions (dense / conv / relu / merge
+// coefficients) form the walk's backbone on `s`; nothing on it depends on
+// the row constants. The constant chains, concretisations and candidate
+// offers — serial-latency kernels — run on `s2`, each waiting only for the
+// coefficient matrix it reads (Mat::ready). So the chains of step k overlap
+// the coefficient work of steps k+1, k+2, ...
+//
+// Early-termination compaction is an optimisation that never changes results
+// (backsub.hpp:25-29): a frozen row's later offers are ignored. It is applied
+// lazily: each checkpoint's surviving-row count is copied to pinned memory
+// behind an event, and before each step the host polls (without blocking) the
+// checkpoints that have completed; only when they show enough frozen rows does
+// it drain `s2` and compact with the latest offer's row map.
 
 struct Walker {
   Ctx* n;
@@ -472,8 +519,15 @@ struct Walker {
   const int* row_q = nullptr;
   bool allow_freeze = false, early_term = true, margin = false;
   pc_stats* st = nullptr;
+  cudaStream_t s2 = nullptr;
+  // lazy compaction state: checkpoints launched since the last compaction
+  int ck_next = 0;             // next pinned slot
+  std::vector<int> ck_pending; // slots in launch order
+  int min_seen = 0;            // smallest completed surviving-row count seen
 
   int nrows() const { return both ? 2 * R : R; }
+  // rows frozen at an earlier checkpoint are skipped by the chain kernels
+  const char* fz() const { return (allow_freeze && early_term && !margin) ? n->frozen : nullptr; }
   RowsDev rows() const { return RowsDev{row_q, nrows(), both ? R : 0}; }
 
   double* arena_take(size_t bytes) {
@@ -527,15 +581,26 @@ struct Walker {
     return m.src ? arena_take((size_t)nrows() * 4 * sizeof(double)) : m.K;
   }
 
+  // m's coefficients are complete (recorded on s after their producer).
+  void mark(Mat& m) {
+    m.ready = sync_event(n);
+    ck(cudaEventRecord(m.ready, s), "event");
+  }
+  // s2 may read m's coefficients.
+  void need(const Mat& m) {
+    if (m.ready) ck(cudaStreamWaitEvent(s2, m.ready, 0), "wait");
+  }
+
   void dense_step(Mat& m) {  // backsub.hpp:343-399
     const HostLayer& L = n->L[m.f.layer];
     Mat out = alloc(dense_frame(L.pred0), false);
     out.K = k_out(m);
     if (!dry) {
-      prof_begin(n, PROF_CHAIN_AFFINE);
-      launch_chain_affine(s, L.d, false, rows(), fdev(n, m.f, q), md(m), out.K,
-                          n->dev + n->off[m.f.layer], n->ctr);
-      prof_end(n);
+      need(m);
+      prof_begin(n, PROF_CHAIN_AFFINE, s2);
+      launch_chain_affine(s2, L.d, false, rows(), fdev(n, m.f, q), md(m), out.K,
+                          n->dev + n->off[m.f.layer], n->ctr, fz());
+      prof_end(n, s2);
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (n->timing) {  // the roofline kernel is always timed (bench.py reads it)
         n->dense_ev.push_back(n->ev_used);
@@ -546,6 +611,7 @@ struct Walker {
         ++g_dense_launches;
       }
       launch_dense_coef(s, L.d, nrows(), md(m), md(out), e0, e1);
+      mark(out);
     }
     m = out;
   }
@@ -567,14 +633,15 @@ struct Walker {
     out.K = k_out(m);
     if (!dry) {
       const FrameDev fi = fdev(n, m.f, q), fo = fdev(n, nf, q);
-      prof_begin(n, PROF_CHAIN_AFFINE);
-      launch_chain_affine(s, L.d, true, rows(), fi, md(m), out.K, n->dev + n->off[m.f.layer],
-                          n->ctr);
-      prof_end(n);
+      need(m);
+      prof_begin(n, PROF_CHAIN_AFFINE, s2);
+      launch_chain_affine(s2, L.d, true, rows(), fi, md(m), out.K, n->dev + n->off[m.f.layer],
+                          n->ctr, fz());
+      prof_end(n, s2);
       prof_begin(n, PROF_GBC);
       launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out));
       prof_end(n);
-      st->gbc_dense_equiv += (long long)nrows() * L.numel() * L.in_numel();
+      mark(out);
     }
     m = out;
   }
@@ -588,12 +655,14 @@ struct Walker {
     if (!dry) {
       const FrameDev f = fdev(n, m.f, q);
       const double* rx = n->relax + 8 * n->off[L.pred0];
-      prof_begin(n, PROF_CHAIN_RELU);
-      launch_chain_relu(s, rows(), f, md(m), out.K, rx);
-      prof_end(n);
+      need(m);
+      prof_begin(n, PROF_CHAIN_RELU, s2);
+      launch_chain_relu(s2, rows(), f, md(m), out.K, rx, fz());
+      prof_end(n, s2);
       prof_begin(n, PROF_RELU);
       launch_relu_coef(s, rows(), f, md(m), md(out), rx);
       prof_end(n);
+      mark(out);
     }
     m = out;
   }
@@ -605,7 +674,7 @@ struct Walker {
     b.f.layer = L.pred1;
     // branch b starts from zero constants, laid out like m's rows
     b.K = arena_take((size_t)(dry ? alloc_rows() : m.phys) * 4 * sizeof(double));
-    if (!dry) ck(cudaMemsetAsync(b.K, 0, (size_t)m.phys * 4 * sizeof(double), s), "memset");
+    if (!dry) ck(cudaMemsetAsync(b.K, 0, (size_t)m.phys * 4 * sizeof(double), s2), "memset");
     walk(a, L.head, false);
     walk(b, L.head, false);
     // align_add (backsub.hpp:610-688): union frame
@@ -627,55 +696,100 @@ struct Walker {
     }
     Mat out = alloc(u, true);
     if (!dry) {
+      const FrameDev fa = fdev(n, a.f, q), fb = fdev(n, b.f, q), fu = fdev(n, u, q);
       prof_begin(n, PROF_MERGE);
-      launch_merge(s, rows(), fdev(n, a.f, q), fdev(n, b.f, q), fdev(n, u, q), dense_path, md(a),
-                   md(b), md(out));
+      launch_merge(s, rows(), fa, fb, fu, dense_path, md(a), md(b), md(out), 1);
       prof_end(n);
+      mark(out);
+      launch_merge(s2, rows(), fa, fb, fu, dense_path, md(a), md(b), md(out), 2);
     }
     m = out;
   }
 
   // run_backsubstitution's checkpoint closure (backsub.hpp:1032-1054) or the
-  // margin pass's (:1082-1091).
+  // margin pass's (:1082-1091). Runs on s2 after m's coefficients.
   void checkpoint(Mat& m) {
     if (dry) return;
-    st->checkpoints++;
+    if (margin) st->checkpoints++;  // pass checkpoints are counted on the device (k_offer)
     const int fl = m.f.layer;
     const long long o = n->off[fl];
+    need(m);
     if (margin) {
-      prof_begin(n, PROF_CONC);
-      launch_concretize(s, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->blo + o,
-                        n->bhi + o, n->vals, n->rvals);
-      prof_end(n);
-      launch_margin_offer(s, R, n->vals, n->best, n->has);
+      prof_begin(n, PROF_CONC, s2);
+      launch_concretize(s2, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->blo + o,
+                        n->bhi + o, n->vals, n->rvals, nullptr);
+      prof_end(n, s2);
+      launch_margin_offer(s2, R, n->vals, n->best, n->has);
       return;
     }
-    prof_begin(n, PROF_CONC);
-    launch_concretize(s, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
-                      n->rhi + o, n->vals, n->rvals);
-    prof_end(n);
+    prof_begin(n, PROF_CONC, s2);
+    launch_concretize(s2, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
+                      n->rhi + o, n->vals, n->rvals, fz());
+    prof_end(n, s2);
     int* new_q = n->rowq[rq ^ 1];
-    prof_begin(n, PROF_OFFER);
-    launch_offer(s, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
+    prof_begin(n, PROF_OFFER, s2);
+    launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
                  early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr);
-    prof_end(n);
+    prof_end(n, s2);
     if (!(allow_freeze && early_term)) return;
-    ck(cudaMemcpyAsync(n->h_int + 1, n->d_int + 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
-    ck(cudaStreamSynchronize(s), "sync");
-    const int newR = n->h_int[1];
-    if (newR == R) return;
-    // compact_rows on both polarities (backsub.hpp:820-845): the surviving
-    // rows stay in place; the next step reads them through the row map.
+    if ((int)ck_pending.size() == Ctx::kCkSlots) drain_pending();  // bounded lag
+    const int slot = ck_next;
+    ck_next = (ck_next + 1) % Ctx::kCkSlots;
+    ck(cudaMemcpyAsync(n->h_newR + slot, n->d_int + 1, sizeof(int), cudaMemcpyDeviceToHost, s2), "d2h");
+    ck(cudaEventRecord(n->ck_ev[slot], s2), "event");
+    ck_pending.push_back(slot);
+  }
+
+  // Fold the completed checkpoints into min_seen (in order; never blocks).
+  void poll_pending() {
+    size_t k = 0;
+    for (; k < ck_pending.size(); ++k) {
+      const cudaError_t e = cudaEventQuery(n->ck_ev[ck_pending[k]]);
+      if (e == cudaErrorNotReady) break;
+      ck(e, "event query");
+      min_seen = std::min(min_seen, n->h_newR[ck_pending[k]]);
+    }
+    ck_pending.erase(ck_pending.begin(), ck_pending.begin() + k);
+  }
+  void drain_pending() {
+    ck(cudaStreamSynchronize(s2), "sync");
+    poll_pending();
+  }
+
+  // compact_rows on both polarities (backsub.hpp:820-845) when enough rows
+  // froze: the surviving rows stay in place and the next step reads them
+  // through the latest offer's row map.
+  void maybe_compact(Mat& m) {
+    if (dry || !(allow_freeze && early_term)) return;
+    static const int lazy = env_int("PC_LAZY_COMPACT", 0);
+    if (lazy) {
+      // keep computing frozen rows while the constants stream lags; compact
+      // only once completed checkpoints show >= 1/8 of the rows frozen
+      poll_pending();
+      const int drop = R - min_seen;
+      if (drop <= 0 || (min_seen > 0 && 8 * drop < R)) return;
+    } else {
+      // eager (the reference's schedule): wait for the last checkpoint's
+      // offers; the constants chain of each step still overlaps that step's
+      // coefficient substitution
+      if (ck_pending.empty()) return;
+      drain_pending();
+      if (min_seen >= R) return;
+    }
+    drain_pending();  // every launched offer done: perm / rowq hold the latest map
+    const int newR = min_seen;
     m.src = n->perm;
     R = newR;
     rq ^= 1;
     row_q = n->rowq[rq];
+    min_seen = R;
   }
 
   // walk_back (backsub.hpp:854-893)
   void walk(Mat& m, int stop, bool ckpt) {
     bool pending = false;
     while (m.f.layer != stop) {
+      if (ckpt) maybe_compact(m);
       if (!dry && R == 0) return;
       const HostLayer& L = n->L[m.f.layer];
       switch (L.kind) {
@@ -838,7 +952,9 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
       n->arena_used = 0;
       reset_stats(n, ws.stats);
       Walker w{n, s, t};
+      w.s2 = n->stream2;
       w.R = R;
+      w.min_seen = R;
       w.both = true;
       w.allow_freeze = allow_freeze;
       w.early_term = et;
@@ -854,8 +970,10 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
         launch_init_affine(s, Q.d, w.rows(), fdev(n, f0, t), n->dev + o, md(m));
       else
         launch_init_identity(s, w.rows(), fdev(n, f0, t), md(m));
+      w.mark(m);
       if (affine) w.checkpoint(m);  // the init itself is an affine step (:1056)
       w.walk(m, 0, true);
+      stream_wait(n, s, n->stream2);  // the next chunk reuses the arena and row lists
     }
   }
   if (W > 1 && n_live > 0) allgather_rows(n, n->live, n_live, 4, n->cand);
@@ -890,7 +1008,9 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
     n->arena_used = 0;
     reset_stats(n, ws.stats);
     Walker w{n, s, out};
+    w.s2 = n->stream2;
     w.R = R;
+    w.min_seen = R;
     w.both = false;
     w.margin = true;
     w.st = st;
@@ -898,7 +1018,9 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
     Frame f0 = dense_frame(out);
     Mat m = w.alloc(f0, true);
     launch_init_margin(s, label, n->n_out, mb, R, md(m));
+    w.mark(m);
     w.walk(m, 0, true);
+    stream_wait(n, s, n->stream2);
     ck(cudaMemcpyAsync(n->h_int + 4, n->has, R, cudaMemcpyDeviceToHost, s), "d2h");
   }
   double* best = n->best;
@@ -961,8 +1083,8 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
     // per-rank work counters (walk freezes, madds, checkpoints, dense-equivalent
     // GBC work) add up; pre-freezes and rows_total are identical on every rank
     unsigned long long h[8] = {c.dense_madds, c.gbc_madds, c.frozen, 0,
-                               (unsigned long long)st->checkpoints,
-                               (unsigned long long)st->gbc_dense_equiv, 0, 0};
+                               (unsigned long long)st->checkpoints + c.checkpoints,
+                               c.gbc_dense_equiv, 0, 0};
     ensure_shard_buffers(n, 8);
     ck(cudaMemcpyAsync(n->sh_send, h, sizeof(h), cudaMemcpyHostToDevice, s), "h2d");
     exchange(n, sizeof(h));
@@ -976,8 +1098,11 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
     c.gbc_madds = sum[1];
     c.frozen = sum[2];
     st->checkpoints = (long long)sum[4];
-    st->gbc_dense_equiv = (long long)sum[5];
+    c.checkpoints = 0;
+    c.gbc_dense_equiv = sum[5];
   }
+  st->checkpoints += (long long)c.checkpoints;
+  st->gbc_dense_equiv += (long long)c.gbc_dense_equiv;
   st->dense_madds += (long long)c.dense_madds;
   st->gbc_madds += (long long)c.gbc_madds;
   st->rows_terminated_early += (long long)(c.frozen + c.pad);
@@ -1025,6 +1150,7 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     pc_stats st{};
     std::vector<double> m(std::max(1, n->n_out - 1), 0.0);
     n->ev_used = 0;
+    n->sync_used = 0;
     n->prof.clear();
     n->dense_ev.clear();
     run_test(n, label, m.data(), &st);

@@ -708,13 +708,17 @@ __device__ __forceinline__ bool chain_affine_row(const LayerDev& L, int is_conv,
 
 __global__ void __launch_bounds__(32 * kChainWarps)
     k_chain_affine(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, double* Kout,
-                   const double* dev, Counters* ctr) {
+                   const double* dev, Counters* ctr, const char* frozen) {
   __shared__ double s_t[kChainWarps][3][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kChainWarps + warp;
   if (i >= rows.n) return;
   bool upper;
   const int q = row_query(rows, i, upper);
+  if (frozen && frozen[q]) return;
+  if (is_conv && lane == 0)
+    atomicAdd(&ctr->gbc_dense_equiv, (unsigned long long)L.out_w * L.out_h * L.out_c *
+                                         ((unsigned long long)L.in_w * L.in_h * L.in_c));
   int bw = 0, bh = 0;
   if (is_conv) frame_base(f, q, bw, bh);
   const long long cells = m.cells;
@@ -741,13 +745,13 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                          const FrameDev& fin, MatDev m, double* Kout, const double* dev,
-                         Counters* ctr) {
+                         Counters* ctr, const char* frozen) {
   if (m.cells >= big_chain_cells()) {
-    launch_chain_affine_big(s, L, is_conv, rows, fin, m, Kout, dev, ctr);
+    launch_chain_affine_big(s, L, is_conv, rows, fin, m, Kout, dev, ctr, frozen);
     return;
   }
   k_chain_affine<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(L, is_conv ? 1 : 0, rows,
-                                                                        fin, m, Kout, dev, ctr);
+                                                                        fin, m, Kout, dev, ctr, frozen);
   ++g_launches;
 }
 
@@ -811,13 +815,15 @@ __device__ __forceinline__ bool chain_relu_row(const FrameDev& f, int bw, int bh
 }
 
 __global__ void __launch_bounds__(32 * kChainWarps)
-    k_chain_relu(RowsDev rows, FrameDev f, MatDev m, double* Kout, const double* relax) {
+    k_chain_relu(RowsDev rows, FrameDev f, MatDev m, double* Kout, const double* relax,
+                 const char* frozen) {
   __shared__ double s_t[kChainWarps][2][2][32];  // [slot][lo/hi][cell]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kChainWarps + warp;
   if (i >= rows.n) return;
   bool upper;
   const int q = row_query(rows, i, upper);
+  if (frozen && frozen[q]) return;
   int bw, bh;
   frame_base(f, q, bw, bh);
   const long long cells = m.cells;
@@ -833,12 +839,13 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 }
 
 void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
-                       double* Kout, const double* relax) {
+                       double* Kout, const double* relax, const char* frozen) {
   if (m.cells >= big_chain_cells()) {
-    launch_chain_relu_big(s, rows, f, m, Kout, relax);
+    launch_chain_relu_big(s, rows, f, m, Kout, relax, frozen);
     return;
   }
-  k_chain_relu<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, Kout, relax);
+  k_chain_relu<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, Kout, relax,
+                                                                      frozen);
   ++g_launches;
 }
 
@@ -896,13 +903,15 @@ __device__ __forceinline__ bool conc_row(const FrameDev& f, int bw, int bh, bool
 
 __global__ void __launch_bounds__(32 * kChainWarps)
     k_concretize(RowsDev rows, FrameDev f, MatDev m, const double* blo, const double* bhi,
-                 const double* rlo, const double* rhi, double* vals, double* rvals) {
+                 const double* rlo, const double* rhi, double* vals, double* rvals,
+                 const char* frozen) {
   __shared__ double s_t[kChainWarps][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kChainWarps + warp;
   if (i >= rows.n) return;
   bool upper;
   const int q = row_query(rows, i, upper);
+  if (frozen && frozen[q]) return;
   int bw, bh;
   frame_base(f, q, bw, bh);
   const long long cells = m.cells;
@@ -925,13 +934,13 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 
 void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        const double* blo, const double* bhi, const double* rlo,
-                       const double* rhi, double* vals, double* rvals) {
+                       const double* rhi, double* vals, double* rvals, const char* frozen) {
   if (m.cells >= big_chain_cells()) {
-    launch_concretize_big(s, rows, f, m, blo, bhi, rlo, rhi, vals, rvals);
+    launch_concretize_big(s, rows, f, m, blo, bhi, rlo, rhi, vals, rvals, frozen);
     return;
   }
   k_concretize<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, blo, bhi, rlo,
-                                                                      rhi, vals, rvals);
+                                                                      rhi, vals, rvals, frozen);
   ++g_launches;
 }
 
@@ -1087,9 +1096,26 @@ __device__ __forceinline__ Iv gbc_gather(const LayerDev& L, const FrameDev& fi, 
       if (MODE > 0) {
         // A zero coefficient adds the zero interval (skipped by the reference's
         // iv_acc). Lanes of a warp share (iy, ix) when cin >= 32, so this
-        // branch is warp-uniform and skips the work.
-#pragma unroll 4
-        for (int d = 0; d < cout; ++d) {
+        // branch is warp-uniform and skips the work. Operands are loaded in
+        // batches of kGB independent loads so their latency overlaps.
+        constexpr int kGB = 8;
+        int d = 0;
+        for (; d + kGB <= cout; d += kGB) {
+          double cl[kGB], ch[kGB], w[kGB];
+#pragma unroll
+          for (int k = 0; k < kGB; ++k) {
+            cl[k] = ilo[cb + d + k];
+            ch[k] = ihi[cb + d + k];
+            w[k] = wp[(size_t)(d + k) * cin];
+          }
+#pragma unroll
+          for (int k = 0; k < kGB; ++k) {
+            if (cl[k] == 0.0 && ch[k] == 0.0) continue;
+            if (MODE == 2) madd_band(w[k], cl[k], ch[k], lo, hi);
+            else madd_fast(w[k], cl[k], ch[k], lo, hi, bad);
+          }
+        }
+        for (; d < cout; ++d) {
           const double cl = ilo[cb + d], ch = ihi[cb + d];
           if (cl == 0.0 && ch == 0.0) continue;
           if (MODE == 2) madd_band(wp[(size_t)d * cin], cl, ch, lo, hi);
@@ -1224,7 +1250,7 @@ void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, Ma
 // instead of accumulated into +0; the constants add K_b into K_a.
 __global__ void __launch_bounds__(256)
     k_merge(RowsDev rows, FrameDev fa, FrameDev fb, FrameDev fu, int dense_path, MatDev a,
-            MatDev b, MatDev out) {
+            MatDev b, MatDev out, int part) {
   const int i = blockIdx.y;
   bool upper;
   const int q = row_query(rows, i, upper);
@@ -1235,7 +1261,7 @@ __global__ void __launch_bounds__(256)
   const long long cells = out.cells;
   const int C = fu.C;
   MagAcc mag;
-  for (long long cell = blockIdx.x * blockDim.x + threadIdx.x; cell < cells;
+  for (long long cell = blockIdx.x * blockDim.x + threadIdx.x; (part & 1) && cell < cells;
        cell += (long long)gridDim.x * blockDim.x) {
     const int cc = (int)(cell % C);
     const int x = (int)((cell / C) % fu.S_w);
@@ -1262,8 +1288,8 @@ __global__ void __launch_bounds__(256)
     mag.add(n.lo);
     mag.add(n.hi);
   }
-  mag.flush(out.stat);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (part & 1) mag.flush(out.stat);
+  if ((part & 2) && blockIdx.x == 0 && threadIdx.x == 0) {
     const double* Ka = a.K + 4 * phys_row(a, i);
     const double* Kb = b.K + 4 * phys_row(b, i);
     Iv k{Ka[0], Ka[1]}, kr{Ka[2], Ka[3]};
@@ -1275,11 +1301,11 @@ __global__ void __launch_bounds__(256)
 }
 
 void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const FrameDev& fb,
-                  const FrameDev& fu, int dense_path, MatDev a, MatDev b, MatDev out) {
-  unsigned gx = cdiv(out.cells, 256);
+                  const FrameDev& fu, int dense_path, MatDev a, MatDev b, MatDev out, int part) {
+  unsigned gx = (part & 1) ? cdiv(out.cells, 256) : 1;
   if (gx > 1024) gx = 1024;
   dim3 grid(gx, rows.n);
-  k_merge<<<grid, 256, 0, s>>>(rows, fa, fb, fu, dense_path, a, b, out);
+  k_merge<<<grid, (part & 1) ? 256 : 32, 0, s>>>(rows, fa, fb, fu, dense_path, a, b, out, part);
   ++g_launches;
 }
 
@@ -1295,7 +1321,11 @@ __global__ void __launch_bounds__(kScanThreads)
   using Scan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
-  if (threadIdx.x == 0) s_base = 0;
+  __shared__ int s_live;
+  if (threadIdx.x == 0) {
+    s_base = 0;
+    s_live = 0;
+  }
   int froze = 0;
   __syncthreads();
   for (int start = 0; start < R; start += kScanThreads) {
@@ -1305,6 +1335,7 @@ __global__ void __launch_bounds__(kScanThreads)
       q = rows.row_q[r];
       double* cd = cand + 4 * (size_t)q;
       if (!frozen[q]) {
+        s_live = 1;  // the reference still has this row: the checkpoint runs
         const double v = vals[r], rv = rvals[r];  // offer_hi
         if (v < cd[1]) cd[1] = v;
         if (rv < cd[3]) cd[3] = rv;
@@ -1329,6 +1360,7 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
   }
   if (froze) atomicAdd(&ctr->frozen, (unsigned long long)froze);
+  if (threadIdx.x == 0 && (s_live || !early_term)) atomicAdd(&ctr->checkpoints, 1ull);
   const int nR = s_base;
   for (int p = threadIdx.x; p < nR; p += blockDim.x) map[nR + p] = R + map[p];  // lower rows
   if (threadIdx.x == 0) *new_R = nR;

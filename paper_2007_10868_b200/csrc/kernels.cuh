@@ -158,6 +158,8 @@ struct Counters {  // device-side PassStats accumulators
   unsigned long long gbc_madds;
   unsigned long long frozen;  // rows_terminated_early (checkpoint freezes)
   unsigned long long pad;
+  unsigned long long gbc_dense_equiv;
+  unsigned long long checkpoints;  // non-margin checkpoints the reference would run
 };
 
 // ----- launchers (kernels.cu) -----
@@ -183,25 +185,28 @@ void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f
 void launch_init_margin(cudaStream_t s, int label, int n_out, int first, int count, MatDev out);
 
 // Chains read the constants of m (through m.src) and write compact ones to Kout.
+// frozen (nullable): rows whose query neuron froze at an earlier checkpoint
+// are skipped — the reference has compacted them away by then (early
+// termination, backsub.hpp:1040-1054); their results are never read.
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                          const FrameDev& fin, MatDev m, double* Kout, const double* dev,
-                         Counters* ctr);
+                         Counters* ctr, const char* frozen);
 void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
-                       double* Kout, const double* relax);
+                       double* Kout, const double* relax, const char* frozen);
 void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        const double* blo, const double* bhi, const double* rlo,
-                       const double* rhi, double* vals, double* rvals);
+                       const double* rhi, double* vals, double* rvals, const char* frozen);
 
 // Long-row variants (chains.cu): one CTA per row, producer warps compact the
 // contributing terms, one consumer warp folds them in order.
 void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                              const FrameDev& fin, MatDev m, double* Kout, const double* dev,
-                             Counters* ctr);
+                             Counters* ctr, const char* frozen);
 void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
-                           double* Kout, const double* relax);
+                           double* Kout, const double* relax, const char* frozen);
 void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            const double* blo, const double* bhi, const double* rlo,
-                           const double* rhi, double* vals, double* rvals);
+                           const double* rhi, double* vals, double* rvals, const char* frozen);
 // Rows at least this long use the CTA-per-row chains (env PC_BIG_CHAIN_CELLS
 // overrides, read once; the tests force 1 to run the corpus through them).
 long long big_chain_cells();
@@ -218,7 +223,8 @@ int env_int(const char* name, int dflt);
 void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev in,
                       MatDev out, const double* relax);
 void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const FrameDev& fb,
-                  const FrameDev& fu, int dense_path, MatDev a, MatDev b, MatDev out);
+                  const FrameDev& fu, int dense_path, MatDev a, MatDev b, MatDev out,
+                  int part);  // part: 1 coefficients, 2 constants, 3 both
 
 // Offers + freeze; writes the compaction map (2 * new_R entries: upper then
 // lower physical rows) and the compacted query list.

@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("env", [{"PC_BIG_CHAIN_CELLS": "1"}, {"PC_GBC": "1"}], ids=["big_chains", "gbc_tiled"])
+@pytest.mark.parametrize("env", [{"PC_BIG_CHAIN_CELLS": "1"}, {"PC_GBC": "1"}, {"PC_LAZY_COMPACT": "1"}],
+                         ids=["big_chains", "gbc_tiled", "lazy_compaction"])
 def test_parity_corpus_under_variant(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(HERE, "test_gpu_parity.py"), "-x", "-q",
