@@ -160,6 +160,9 @@ long long pc_last_launch_count(void);
  * back-substitution kernel (the roofline kernel) with its algorithmic bytes. */
 void pc_last_timing(double* total_ms, double* dense_kernel_ms, double* dense_kernel_bytes,
                     long long* dense_kernel_launches);
+/* Algorithmic interval multiply-adds of those dense-kernel launches (rows x
+ * frame cells x predecessor cells, summed). */
+double pc_last_dense_madds(void);
 
 /* Per-kernel-class device time of this thread's last pc_net_test* call as a
  * JSON object {class: [launches, ms]} (collected only when the environment

@@ -71,6 +71,7 @@ def _load():
         "pc_net_candidate": (i, [vp, vp, vp, vp]),
         "pc_last_launch_count": (ll, []),
         "pc_last_timing": (None, [vp, vp, vp, vp]),
+        "pc_last_dense_madds": (d, []),
         "pc_scalar_ops": (i, [i, vp, vp, vp, ll]),
         "pc_last_profile": (i, [ctypes.c_char_p, i]),
         "pc_last_error": (ctypes.c_char_p, []),
@@ -86,7 +87,7 @@ def _load():
 def header_symbols() -> list[str]:
     """Function names declared in include/polycert_b200.h."""
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:pc_status|void|int|long long|const char\*)\s+\**(pc_\w+)\(",
+    return sorted(set(re.findall(r"^\s*(?:pc_status|void|int|long long|double|const char)\s*\**\s*(pc_\w+)\(",
                                  txt, flags=re.M)))
 
 

@@ -30,7 +30,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local long long g_last_launches = 0;
-thread_local double g_total_ms = 0, g_dense_ms = 0, g_dense_bytes = 0;
+thread_local double g_total_ms = 0, g_dense_ms = 0, g_dense_bytes = 0, g_dense_madds = 0;
 thread_local long long g_dense_launches = 0;
 
 struct StatusError : std::runtime_error {
@@ -608,6 +608,7 @@ struct Walker {
         e1 = take_event(n);
         // algorithmic bytes: coefficient rows in/out (16 B per interval) + weights once
         g_dense_bytes += 16.0 * nrows() * (double)(m.cells + out.cells) + 8.0 * m.cells * out.cells;
+        g_dense_madds += (double)nrows() * m.cells * out.cells;
         ++g_dense_launches;
       }
       launch_dense_coef(s, L.d, nrows(), md(m), md(out), e0, e1);
@@ -1210,7 +1211,7 @@ pc_status test_impl(pc_net* net, const double* lo, const double* up, bool device
     return PC_ERR_INVALID_ARGUMENT;
   }
   g_launches = 0;
-  g_dense_ms = g_dense_bytes = 0;
+  g_dense_ms = g_dense_bytes = g_dense_madds = 0;
   g_dense_launches = 0;
   return guard([&] {
     ck(cudaSetDevice(net->device), "cudaSetDevice");
@@ -1234,6 +1235,7 @@ void pc_default_options(pc_options* opt) {
 }
 
 const char* pc_last_error(void) { return g_err.c_str(); }
+double pc_last_dense_madds(void) { return g_dense_madds; }
 long long pc_last_launch_count(void) { return g_last_launches; }
 
 void pc_last_timing(double* total_ms, double* dense_ms, double* dense_bytes, long long* launches) {

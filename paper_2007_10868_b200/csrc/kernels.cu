@@ -1027,6 +1027,10 @@ __global__ void __launch_bounds__(kDC)
     if (band) dense_slab<TM, true>(s_al, s_ah, s_w, kn, tx, lo, hi, bad);
     else dense_slab<TM, false>(s_al, s_ah, s_w, kn, tx, lo, hi, bad);
   }
+  if (band) {
+#pragma unroll
+    for (int u = 0; u < TM; ++u) lo[u] = canon0(lo[u]);
+  }
   if (col >= n_in) return;
   MagAcc mag;
 #pragma unroll
@@ -1153,6 +1157,7 @@ __global__ void __launch_bounds__(256)
     Iv acc;
     if (band) {
       acc = gbc_gather<2>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+      acc.lo = canon0(acc.lo);
     } else {
       acc = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
       if (bad) acc = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);

@@ -124,19 +124,29 @@ __device__ __forceinline__ bool products_in_band(const unsigned* stat, double wm
 __device__ __forceinline__ bool bits_zero(double x) {
   return (((unsigned)__double2hiint(x) << 1) | (unsigned)__double2loint(x)) == 0u;
 }
+// Outward steps without compares or selects (valid in the band):
+//  * product: with RN product p and exact residual r = a*w - p (FMA),
+//    0 < |r| <= ulp(p)/2 when inexact, so RD(p - |r|) = nextafter(p, -inf)
+//    and RU(p + |r|) = nextafter(p, +inf); r = 0 leaves p (the reference's
+//    "exact iff residual == 0", interval.hpp:71-83);
+//  * sum: with s = RN, d = RD, u = RU of a + b, t = u - d is 0 (exact) or one
+//    ulp, so RD(s - t/2) = nextafter(s, -inf) and RU(s + t/2) =
+//    nextafter(s, +inf) when inexact and s otherwise (interval.hpp:59-68).
+//    The lower form can turn an exact +0 into -0; value-equal, and the
+//    accumulators are canonicalised (+0) when stored.
 __device__ __forceinline__ void madd_band(double w, double cl, double ch, double& lo, double& hi) {
   const bool neg = __double2hiint(w) < 0;
   const double a = neg ? ch : cl, b = neg ? cl : ch;
-  double pl = __dmul_rn(a, w), ph = __dmul_rn(b, w);
-  const double rl = __fma_rn(a, w, -pl), rh = __fma_rn(b, w, -ph);
-  if (!bits_zero(rl)) pl = __dadd_rd(pl, -4.9406564584124654e-324);
-  if (!bits_zero(rh)) ph = __dadd_ru(ph, 4.9406564584124654e-324);
-  double sl = __dadd_rn(lo, pl), sh = __dadd_rn(hi, ph);
-  if (__dadd_rd(lo, pl) != __dadd_ru(lo, pl)) sl = __dadd_rd(sl, -4.9406564584124654e-324);
-  if (__dadd_rd(hi, ph) != __dadd_ru(hi, ph)) sh = __dadd_ru(sh, 4.9406564584124654e-324);
-  lo = sl;
-  hi = sh;
+  const double pl0 = __dmul_rn(a, w), ph0 = __dmul_rn(b, w);
+  const double pl = __dadd_rd(pl0, -fabs(__fma_rn(a, w, -pl0)));
+  const double ph = __dadd_ru(ph0, fabs(__fma_rn(b, w, -ph0)));
+  const double sl = __dadd_rn(lo, pl), dl = __dadd_rd(lo, pl), ul = __dadd_ru(lo, pl);
+  const double sh = __dadd_rn(hi, ph), dh = __dadd_rd(hi, ph), uh = __dadd_ru(hi, ph);
+  lo = __fma_rd(__dsub_rn(ul, dl), -0.5, sl);
+  hi = __fma_ru(__dsub_rn(uh, dh), 0.5, sh);
 }
+// -0 -> +0 (RN: -0 + +0 = +0), everything else unchanged.
+__device__ __forceinline__ double canon0(double x) { return __dadd_rn(x, 0.0); }
 
 __host__ __device__ __forceinline__ size_t phys_row(const MatDev& m, int i) {
   return (size_t)(m.src ? m.src[i] : i);

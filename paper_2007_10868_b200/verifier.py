@@ -209,4 +209,5 @@ class Verifier:
         t, dm, db, dl = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
         _lib.lib.pc_last_timing(ctypes.byref(t), ctypes.byref(dm), ctypes.byref(db), ctypes.byref(dl))
         return {"total_ms": t.value, "dense_ms": dm.value, "dense_bytes": db.value,
-                "dense_launches": dl.value, "launches": int(_lib.lib.pc_last_launch_count())}
+                "dense_launches": dl.value, "dense_madds": float(_lib.lib.pc_last_dense_madds()),
+                "launches": int(_lib.lib.pc_last_launch_count())}

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 400 python -m pytest tests/test_gpu_numeric.py tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
-for c in mnist_6x100 mnist_9x500 cifar_convbig; do
-  timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], 'value', round(d['value'],3), 'e2e', round(d['e2e']['value'],3), 'lat', d['latency_ms_per_image'], 'launches', d['gpu_launches'], d['config']['verified'], d['clocks'])"
-done
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+sleep 2
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; tail -c 2500 gpurun_out/bench_default.json; tail -3 gpurun_out/bench_default.err
+for c in cifar_convbig cifar_resnet18; do timeout 900 python bench.py --config $c --steps 3 --warmup 3 --batch 16 --no-cpu-baseline 2>&1 | tail -1 | cut -c1-700; done
