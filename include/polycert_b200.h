@@ -172,7 +172,9 @@ int pc_last_profile(char* buf, int len);
 /* Numeric-core self test (device): out[i] = op(a[i], b[i]) with op 0
  * add_down, 1 add_up, 2 mul_down, 3 mul_up, 4 div_down, 5 div_up,
  * 6 ulp_above(a) (interval.hpp:59-102); 7/8 the direction-generic chain add
- * (up/down); 9/10 nextafter(a, +/-inf). HOST arrays. */
+ * (up/down); 9/10 nextafter(a, +/-inf); 11/12 the compare-free band product
+ * (down/up) and 13/14 band sum (down/up) used by the conv/dense kernels when
+ * their operands are proven in band. HOST arrays. */
 pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, long long n);
 
 const char* pc_last_error(void);

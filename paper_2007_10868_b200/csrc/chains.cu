@@ -333,22 +333,23 @@ constexpr size_t chain_smem() {
   return (size_t)2 * G::NA * kTile * sizeof(double);
 }
 
-static bool g_attr_done = false;
 static void set_attrs() {
-  if (g_attr_done) return;
+  cudaFuncSetAttribute(k_chain_affine_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_chain_relu_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_concretize_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_chain_affine_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)chain_smem<AffineGen>());
   cudaFuncSetAttribute(k_chain_relu_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)chain_smem<ReluGen>());
   cudaFuncSetAttribute(k_concretize_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)chain_smem<ConcGen>());
-  g_attr_done = true;
 }
+
+void init_kernel_attrs_chains() { set_attrs(); }
 
 void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                              const FrameDev& fin, MatDev m, double* Kout, const double* dev,
                              Counters* ctr, const char* frozen) {
-  set_attrs();
   k_chain_affine_big<<<rows.n, kCT, chain_smem<AffineGen>(), s>>>(L, is_conv ? 1 : 0, rows, fin, m,
                                                                    Kout, dev, ctr, frozen);
   ++g_launches;
@@ -356,7 +357,6 @@ void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, co
 
 void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            double* Kout, const double* relax, const char* frozen) {
-  set_attrs();
   k_chain_relu_big<<<rows.n, kCT, chain_smem<ReluGen>(), s>>>(rows, f, m, Kout, relax, frozen);
   ++g_launches;
 }
@@ -364,7 +364,6 @@ void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& 
 void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            const double* blo, const double* bhi, const double* rlo,
                            const double* rhi, double* vals, double* rvals, const char* frozen) {
-  set_attrs();
   k_concretize_big<<<rows.n, kCT, chain_smem<ConcGen>(), s>>>(rows, f, m, blo, bhi, rlo, rhi, vals,
                                                                rvals, frozen);
   ++g_launches;

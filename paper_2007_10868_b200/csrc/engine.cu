@@ -1293,6 +1293,7 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
     if (n->opt.device >= 0) n->device = n->opt.device;
     else ck(cudaGetDevice(&n->device), "cudaGetDevice");
     ck(cudaSetDevice(n->device), "cudaSetDevice");
+    init_kernel_attrs(n->device);
     const int nl = (int)n->L.size();
     n->off.assign(nl + 1, 0);
     for (int k = 0; k < nl; ++k) {

@@ -195,6 +195,10 @@ __global__ void __launch_bounds__(256)
   mag.flush(out.stat);
 }
 
+void init_kernel_attrs_gbc() {
+  cudaFuncSetAttribute(k_gbc_tile, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out) {
   GbcGeom g;

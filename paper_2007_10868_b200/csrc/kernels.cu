@@ -8,6 +8,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <cstdlib>
+#include <mutex>
 
 #include "kernels.cuh"
 #include "numeric.cuh"
@@ -15,6 +16,18 @@
 namespace pc {
 
 thread_local long long g_launches = 0;
+
+void init_kernel_attrs(int device) {
+  static std::mutex mu;
+  static unsigned long long done = 0;  // one bit per device ordinal (< 64)
+  std::lock_guard<std::mutex> lk(mu);
+  const unsigned long long bit = 1ull << (device & 63);
+  if (done & bit) return;
+  init_kernel_attrs_kernels();
+  init_kernel_attrs_chains();
+  init_kernel_attrs_gbc();
+  done |= bit;
+}
 
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -1170,10 +1183,200 @@ __global__ void __launch_bounds__(256)
   mag.flush(out.stat);
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory tiled gbc_step coefficients (band path). A CTA owns 64 output
+// positions (flattened over the row's output window) x 64 input channels of
+// one row. The reduction runs tap by tap in the canonical order (fy, fx
+// descending = covering cells (ah, aw) ascending for every output) and, within
+// a tap, over d in chunks of 32 ascending: exactly each output's reference
+// order. Per stage, the 64 positions' covering coefficients c[ah][aw][d-chunk]
+// ({lo, hi} pairs, zero when the tap misses the position or the window) and
+// the tap's weights W[d-chunk][64 ci] are staged by cp.async into a double
+// buffer while the previous stage computes. Warp w owns positions 8w..8w+7,
+// lane l channels 2l, 2l+1: coefficient reads are warp-broadcasts, and a zero
+// coefficient (a no-op, as in the reference's iv_acc skip) is skipped
+// warp-uniformly. Operands outside the proven band fall back to the per-output
+// gather with the checked / exact ops.
+constexpr int kSC = 64, kSD = 32, kSW = 4;  // ci per CTA, d per stage, warps per CTA
+
+template <int PW>
+constexpr size_t gbc_smem_bytes() {  // double buffer of C [4*PW][kSD] {lo,hi} + W [kSD][kSC]
+  return 2 * (size_t)(kSW * PW * kSD * 2 + kSD * kSC) * sizeof(double);
+}
+
+struct GbcSmemGeom {
+  int n_pos, pos_tiles, ci_tiles;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// PW positions per warp (CTA: kSW warps = kSW*PW positions x kSC channels;
+// lane l owns channels 2l, 2l+1 of the CTA's 64).
+template <int PW>
+__global__ void __launch_bounds__(32 * kSW)
+    k_gbc_smem(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, MatDev in, MatDev out,
+               GbcSmemGeom g) {
+  extern __shared__ double sm[];
+  constexpr int kSP = kSW * PW;
+  constexpr int kCWords = kSP * kSD * 2, kWWords = kSD * kSC, kBuf = kCWords + kWWords;
+  const int i = blockIdx.y;
+  const int pt = blockIdx.x % g.pos_tiles, ct = blockIdx.x / g.pos_tiles;
+  const int p0 = pt * kSP, ci0 = ct * kSC;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw, bh, nbw, nbh;
+  frame_base(fi, q, bw, bh);
+  frame_base(fo, q, nbw, nbh);
+  const double* ilo = in.lo + phys_row(in, i) * in.cells;
+  const double* ihi = in.hi + phys_row(in, i) * in.cells;
+  const int cin = L.in_c, cout = L.out_c;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  double* olo = out.lo + (size_t)i * out.cells;
+  double* ohi = out.hi + (size_t)i * out.cells;
+  MagAcc mag;
+  if (!band) {  // checked fast ops, exact recompute on a flagged output
+    for (int e = tid; e < kSP * kSC; e += blockDim.x) {
+      const int p = p0 + e / kSC, ci = ci0 + e % kSC;
+      if (p >= g.n_pos || ci >= cin) continue;
+      const int iy = nbh + p / fo.S_w, ix = nbw + p % fo.S_w;
+      bool bad = false;
+      Iv acc = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+      if (bad) acc = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+      const size_t o = (size_t)p * cin + ci;
+      olo[o] = acc.lo;
+      ohi[o] = acc.hi;
+      mag.add(acc.lo);
+      mag.add(acc.hi);
+    }
+    mag.flush(out.stat);
+    return;
+  }
+  const int ntaps = L.fh * L.fw;
+  const int nchunks = (cout + kSD - 1) / kSD;
+  const int nstages = ntaps * nchunks;
+  auto stage = [&](int st, int b) {
+    const int tap = st / nchunks, d0 = (st % nchunks) * kSD;
+    const int fy = L.fh - 1 - tap / L.fw, fx = L.fw - 1 - tap % L.fw;
+    double* C = sm + (size_t)b * kBuf;
+    double* Wd = C + kCWords;
+    for (int e = tid; e < kSP * kSD; e += blockDim.x) {
+      const int pp = e / kSD, dd = e % kSD;
+      const int p = p0 + pp, d = d0 + dd;
+      bool ok = p < g.n_pos && d < cout;
+      size_t src = 0;
+      if (ok) {
+        const int iy = nbh + p / fo.S_w, ix = nbw + p % fo.S_w;
+        const int ny = iy + L.ph - fy, nx = ix + L.pw - fx;  // = ah * sh, aw * sw
+        ok = ny >= 0 && nx >= 0 && ny % L.sh == 0 && nx % L.sw == 0;
+        if (ok) {
+          const int ah = ny / L.sh - bh, aw = nx / L.sw - bw;
+          ok = ah >= 0 && ah < fi.S_h && aw >= 0 && aw < fi.S_w;
+          src = ((size_t)ah * fi.S_w + aw) * cout + d;
+        }
+      }
+      cp_async8(C + 2 * e, ilo + (ok ? src : 0), ok);
+      cp_async8(C + 2 * e + 1, ihi + (ok ? src : 0), ok);
+    }
+    const double* wt = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin;
+    for (int e = tid; e < kSD * kSC; e += blockDim.x) {
+      const int dd = e / kSC, cc = e % kSC;
+      const bool ok = d0 + dd < cout && ci0 + cc < cin;
+      cp_async8(Wd + e, wt + (ok ? (size_t)(d0 + dd) * cin + ci0 + cc : 0), ok);
+    }
+    cp_async_commit();
+  };
+  double lo[PW][2], hi[PW][2];
+#pragma unroll
+  for (int k = 0; k < PW; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) lo[k][j] = hi[k][j] = 0.0;
+  stage(0, 0);
+  for (int st = 0; st < nstages; ++st) {
+    cp_async_wait_all();
+    __syncthreads();  // stage st landed; stage st-1 consumed
+    if (st + 1 < nstages) stage(st + 1, (st + 1) & 1);
+    const double* C = sm + (size_t)(st & 1) * kBuf;
+    const double2* C2 = reinterpret_cast<const double2*>(C) + (size_t)(warp * PW) * kSD;
+    const double2* W2 = reinterpret_cast<const double2*>(C + kCWords) + lane;
+#pragma unroll 2
+    for (int dd = 0; dd < kSD; ++dd) {
+      const double2 w = W2[(size_t)dd * (kSC / 2)];
+#pragma unroll
+      for (int k = 0; k < PW; ++k) {
+        const double2 c = C2[(size_t)k * kSD + dd];
+        if (bits_zero(c.x) && bits_zero(c.y)) continue;
+        madd_band(w.x, c.x, c.y, lo[k][0], hi[k][0]);
+        madd_band(w.y, c.x, c.y, lo[k][1], hi[k][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < PW; ++k) {
+    const int p = p0 + warp * PW + k;
+    if (p >= g.n_pos) break;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int ci = ci0 + 2 * lane + j;
+      if (ci >= cin) continue;
+      const double l = canon0(lo[k][j]);
+      const size_t o = (size_t)p * cin + ci;
+      olo[o] = l;
+      ohi[o] = hi[k][j];
+      mag.add(l);
+      mag.add(hi[k][j]);
+    }
+  }
+  mag.flush(out.stat);
+}
+
+static bool gbc_smem_eligible(const LayerDev& L, const FrameDev& fout) {
+  static const int any = env_int("PC_GBC_SMEM_ANY", 0);  // tests: route every conv step here
+  return any || (L.in_c >= 32 && (long long)fout.S_w * fout.S_h >= 32);
+}
+
+void launch_gbc_smem(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, MatDev in, MatDev out) {
+  GbcSmemGeom g;
+  g.n_pos = fout.S_w * fout.S_h;
+  g.ci_tiles = (L.in_c + kSC - 1) / kSC;
+  // positions per warp: the most reuse that still gives >= 4 CTAs per SM
+  static const int forced = env_int("PC_GBC_PW", 0);
+  int pw = forced;
+  if (!pw) {
+    pw = 1;
+    for (int c : {8, 4, 2}) {
+      const long long ctas = (long long)((g.n_pos + kSW * c - 1) / (kSW * c)) * g.ci_tiles * rows.n;
+      if (ctas >= 4 * 148) { pw = c; break; }
+    }
+  }
+  g.pos_tiles = (g.n_pos + kSW * pw - 1) / (kSW * pw);
+  dim3 grid(g.pos_tiles * g.ci_tiles, rows.n);
+  switch (pw) {
+    case 8: k_gbc_smem<8><<<grid, 32 * kSW, gbc_smem_bytes<8>(), s>>>(L, rows, fin, fout, in, out, g); break;
+    case 4: k_gbc_smem<4><<<grid, 32 * kSW, gbc_smem_bytes<4>(), s>>>(L, rows, fin, fout, in, out, g); break;
+    case 2: k_gbc_smem<2><<<grid, 32 * kSW, gbc_smem_bytes<2>(), s>>>(L, rows, fin, fout, in, out, g); break;
+    default: k_gbc_smem<1><<<grid, 32 * kSW, gbc_smem_bytes<1>(), s>>>(L, rows, fin, fout, in, out, g); break;
+  }
+  ++g_launches;
+}
+
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out) {
-  static const int tiled = env_int("PC_GBC", 0);
-  if (tiled) {
+  // PC_GBC: 2 (default) shared-memory tiled kernel where eligible, 1 the
+  // register-blocked gather, 0 the one-output-per-thread gather
+  static const int variant = env_int("PC_GBC", 2);
+  if (variant == 2 && gbc_smem_eligible(L, fout)) {
+    launch_gbc_smem(s, L, rows, fin, fout, in, out);
+    return;
+  }
+  if (variant == 1) {
     launch_gbc_tile(s, L, rows, fin, fout, in, out);
     return;
   }
@@ -1432,6 +1635,28 @@ void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best
   ++g_launches;
 }
 
+// One shared-memory carveout for every kernel of a walk: the coefficient and
+// constants streams run concurrently, and an SM can only co-host CTAs of
+// kernels whose carveout it is configured for; mixed carveouts force SMs to
+// drain and reconfigure between them.
+template <class K>
+static void carve(K k) {
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+void init_kernel_attrs_kernels() {
+  carve(k_fwd_dense); carve(k_fwd_conv); carve(k_fwd_relu); carve(k_fwd_join); carve(k_relax);
+  carve(k_seed); carve(k_writeback); carve(k_init_affine); carve(k_init_identity);
+  carve(k_init_margin); carve(k_chain_affine); carve(k_chain_relu); carve(k_concretize);
+  carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef);
+  carve(k_relu_coef); carve(k_merge); carve(k_offer); carve(k_shard_pack); carve(k_shard_unpack);
+  carve(k_margin_offer);
+  carve(k_gbc_smem<1>); carve(k_gbc_smem<2>); carve(k_gbc_smem<4>); carve(k_gbc_smem<8>);
+  cudaFuncSetAttribute(k_gbc_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbc_smem_bytes<1>());
+  cudaFuncSetAttribute(k_gbc_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbc_smem_bytes<2>());
+  cudaFuncSetAttribute(k_gbc_smem<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbc_smem_bytes<4>());
+  cudaFuncSetAttribute(k_gbc_smem<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbc_smem_bytes<8>());
+}
+
 // input_box (network.hpp:160-177): iv_add(point(c), [-eps, eps]) then the
 // optional [0, 1] clamp with std::max/std::min semantics.
 __global__ void k_input_box(const double* c, int n, double eps, int clamp01, double* lo,
@@ -1535,7 +1760,12 @@ __global__ void k_scalar_ops(int op, const double* a, const double* b, double* o
     case 7: r = add_dir(x, y, true); break;
     case 8: r = add_dir(x, y, false); break;
     case 9: r = nextup_bits(x); break;
-    default: r = nextdown_bits(x); break;
+    case 10: r = nextdown_bits(x); break;
+    // band forms used by madd_band (valid for in-band operands only)
+    case 11: { const double p = __dmul_rn(x, y); r = __dadd_rd(p, -fabs(__fma_rn(x, y, -p))); break; }
+    case 12: { const double p = __dmul_rn(x, y); r = __dadd_ru(p, fabs(__fma_rn(x, y, -p))); break; }
+    case 13: r = canon0(__fma_rd(__dsub_rn(__dadd_ru(x, y), __dadd_rd(x, y)), -0.5, __dadd_rn(x, y))); break;
+    default: r = __fma_ru(__dsub_rn(__dadd_ru(x, y), __dadd_rd(x, y)), 0.5, __dadd_rn(x, y)); break;
   }
   out[i] = r;
 }

@@ -260,4 +260,11 @@ cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* 
 
 extern thread_local long long g_launches;
 
+// Per-kernel attributes (shared-memory carveout, dynamic smem limits), once per process.
+void init_kernel_attrs_kernels();
+void init_kernel_attrs_chains();
+void init_kernel_attrs_gbc();
+// Call with the device current (attributes are per device); idempotent.
+void init_kernel_attrs(int device);
+
 }  // namespace pc

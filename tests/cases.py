@@ -28,4 +28,6 @@ EXTRA_ARCHS = [
     "input 7x7x2; conv 1x1x3 s1 p0; relu; block(conv 3x3x3 s1 p1 | skip); relu; conv 3x3x2 s2 p1; relu; dense 2",
     # MLP of the MNIST family, small
     "input 4x4x1; dense 20; relu; dense 20; relu; dense 20; relu; dense 10",
+    # wide channels (>= 32: the shared-memory conv kernel), strided residual block
+    "input 8x8x3; conv 3x3x32 s1 p1; relu; block(conv 4x4x40 s2 p1; relu; conv 3x3x40 s1 p1 | conv 2x2x40 s2 p0); relu; conv 3x3x36 s1 p1; relu; dense 5",
 ]

@@ -73,3 +73,23 @@ def test_nextafter_bits():
     a = a[~np.isnan(a)]
     assert same_bits(gpu_ops(9, a, a), np.nextafter(a, np.inf))
     assert same_bits(gpu_ops(10, a, a), np.nextafter(a, -np.inf))
+
+
+def test_band_forms(port):
+    """madd_band's compare-free outward steps (kernels.cuh) equal the reference
+    ops for every in-band operand: products with |a*b| in [2^-499, 2^999] (or a
+    zero factor), sums of operands below 2^1000 (zero results compare by value:
+    the band forms may give -0 where the reference gives +0)."""
+    a, b = operands()
+    fin = np.isfinite(a) & np.isfinite(b)
+    a, b = a[fin], b[fin]
+    with np.errstate(all="ignore"):
+        p = np.abs(a * b)
+    pm = (a == 0) | (b == 0) | ((p >= 2.0 ** -499) & (p <= 2.0 ** 999))
+    sm = (np.abs(a) < 2.0 ** 1000) & (np.abs(b) < 2.0 ** 1000) & \
+         ((a == 0) | (np.abs(a) >= 2.0 ** -520)) & ((b == 0) | (np.abs(b) >= 2.0 ** -520))
+    for op, ref, m in ((11, 2, pm), (12, 3, pm), (13, 0, sm), (14, 1, sm)):
+        g, r = gpu_ops(op, a[m], b[m]), port.scalar_ops(ref, a[m], b[m])
+        assert np.array_equal(g, r), (op, np.flatnonzero(g != r)[:4])
+        nz = r != 0
+        assert same_bits(g[nz], r[nz]), op
