@@ -31,6 +31,10 @@ import time
 
 import numpy as np
 
+# Many concurrent per-image streams: give each its own hardware work queue
+# (the default of 8 aliases streams onto shared queues, serialising them).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -60,12 +60,19 @@ typedef struct {
 } pc_layer_desc;
 
 /* AnalysisOptions (analyzer.hpp:164-169). memory_budget bounds the device
- * workspace of one pass (0: default); results are chunk-invariant. */
+ * workspace of one pass (0: default); results are chunk-invariant.
+ * exec_mode: the host-driven schedule launches each step from the host and
+ * reads every checkpoint's surviving-row count (exact grids, chunking, early
+ * exit); the device-driven one keeps the live-row count on the device, so a
+ * whole verification is captured once as a CUDA graph and replayed per image
+ * (needs every pass in one chunk; launches are sized for all of a layer's
+ * neurons). auto = host-driven. Results identical. */
 typedef struct {
   int early_term;          /* default 1 */
   long long chunk_rows;    /* 0: derive from memory_budget */
   long long memory_budget; /* bytes; 0: engine default */
   int device;              /* CUDA ordinal; -1: current */
+  int exec_mode;           /* 0 auto, 1 host-driven schedule, 2 device-driven (CUDA graph) */
 } pc_options;
 
 /* PassStats (backsub.hpp:119-136). */

@@ -69,9 +69,10 @@ struct AnalysisOptions {  // analyzer.hpp:164-169
   long long memory_budget = 0;  // device workspace bytes per pass; 0: engine default
   int workers = 1;              // accepted for source compatibility; the GPU grid is the parallelism
   int device = -1;              // CUDA ordinal; -1: current
+  int exec_mode = 0;            // 0 auto, 1 host-driven schedule, 2 device-driven (CUDA graph)
   bool operator==(const AnalysisOptions& o) const {
     return early_term == o.early_term && chunk_rows == o.chunk_rows &&
-           memory_budget == o.memory_budget && device == o.device;
+           memory_budget == o.memory_budget && device == o.device && exec_mode == o.exec_mode;
   }
 };
 
@@ -158,6 +159,7 @@ class Network {
       o.chunk_rows = opt.chunk_rows;
       o.memory_budget = opt.memory_budget;
       o.device = opt.device;
+      o.exec_mode = opt.exec_mode;
       auto h = std::make_shared<detail::Handle>();
       h->opt = opt;
       detail::check(pc_net_create(d.data(), (int)d.size(), input_shape.w, input_shape.h,

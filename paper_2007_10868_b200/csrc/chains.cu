@@ -263,7 +263,8 @@ __global__ void __launch_bounds__(kCT)
                        const double* dev, Counters* ctr, const char* frozen) {
   extern __shared__ double buf[];
   __shared__ ChainShared sh;
-  const int i = blockIdx.x;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   if (frozen && frozen[q]) return;
@@ -293,7 +294,8 @@ __global__ void __launch_bounds__(kCT)
                      const char* frozen) {
   extern __shared__ double buf[];
   __shared__ ChainShared sh;
-  const int i = blockIdx.x;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   if (frozen && frozen[q]) return;
@@ -311,7 +313,8 @@ __global__ void __launch_bounds__(kCT)
                      const char* frozen) {
   extern __shared__ double buf[];
   __shared__ ChainShared sh;
-  const int i = blockIdx.x;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   if (frozen && frozen[q]) return;

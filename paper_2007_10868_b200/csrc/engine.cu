@@ -162,6 +162,19 @@ struct Ctx {
   size_t arena_cap = 0, arena_used = 0;
   unsigned* stats = nullptr;  // MagStat pool: 2 words per bound matrix of a walk
   size_t stats_cap = 0, stats_used = 0;
+  // device-driven walks (graph mode): label, per-checkpoint live-row counts,
+  // a second row-map buffer, and the captured whole-analysis graph
+  int* d_label = nullptr;
+  int* d_slots = nullptr;
+  static constexpr int kSlots = 8192;
+  int* perm2 = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int graph_label_mode = -1;       // label < 0 (analysis only) vs >= 0 when captured
+  bool graph_failed = false;
+  pc_stats graph_st{};             // host-side counts accumulated while capturing
+  std::vector<size_t> graph_dense_ev;
+  double graph_dense_bytes = 0, graph_dense_madds = 0;
+  long long graph_launches = 0, graph_dense_launches = 0;
   double *sh_send = nullptr, *sh_recv = nullptr;  // sharding exchange buffers
   size_t sh_cap = 0;                              // doubles per rank
   int* h_int = nullptr;  // pinned
@@ -220,6 +233,9 @@ struct Ctx {
     ck(cudaMemset(gen_l, 0, nl * sizeof(int)), "memset");
     ck(cudaMallocHost(&h_int, 64 + (size_t)n_out), "pinned");
     ck(cudaMallocHost(&h_newR, sizeof(int) * kCkSlots), "pinned");
+    d_label = dalloc<int>(1);
+    d_slots = dalloc<int>(kSlots);
+    perm2 = dalloc<int>(2 * M);
     for (int k = 0; k < kCkSlots; ++k) ck(cudaEventCreateWithFlags(&ck_ev[k], cudaEventDisableTiming), "event");
   }
 
@@ -229,6 +245,7 @@ struct Ctx {
     for (void* p : owned) cudaFree(p);
     if (arena) cudaFree(arena);
     if (stats) cudaFree(stats);
+    if (graph) cudaGraphExecDestroy(graph);
     if (sh_send) cudaFree(sh_send);
     if (sh_recv) cudaFree(sh_recv);
     if (h_int) cudaFreeHost(h_int);
@@ -520,6 +537,11 @@ struct Walker {
   bool allow_freeze = false, early_term = true, margin = false;
   pc_stats* st = nullptr;
   cudaStream_t s2 = nullptr;
+  // device-driven walk (graph mode): R is the launch bound; the live count is
+  // read by the kernels from dR, which each checkpoint's offers advance
+  bool devr = false;
+  const int* dR = nullptr;
+  int slot_next = 0, pq = 0;
   // lazy compaction state: checkpoints launched since the last compaction
   int ck_next = 0;             // next pinned slot
   std::vector<int> ck_pending; // slots in launch order
@@ -528,7 +550,11 @@ struct Walker {
   int nrows() const { return both ? 2 * R : R; }
   // rows frozen at an earlier checkpoint are skipped by the chain kernels
   const char* fz() const { return (allow_freeze && early_term && !margin) ? n->frozen : nullptr; }
-  RowsDev rows() const { return RowsDev{row_q, nrows(), both ? R : 0}; }
+  RowsDev rows() const {
+    RowsDev r{row_q, nrows(), both ? R : 0};
+    r.dR = devr ? dR : nullptr;
+    return r;
+  }
 
   double* arena_take(size_t bytes) {
     bytes = (bytes + 255) & ~size_t(255);
@@ -611,7 +637,7 @@ struct Walker {
         g_dense_madds += (double)nrows() * m.cells * out.cells;
         ++g_dense_launches;
       }
-      launch_dense_coef(s, L.d, nrows(), md(m), md(out), e0, e1);
+      launch_dense_coef(s, L.d, rows(), md(m), md(out), e0, e1);
       mark(out);
     }
     m = out;
@@ -728,6 +754,27 @@ struct Walker {
                       n->rhi + o, n->vals, n->rvals, fz());
     prof_end(n, s2);
     int* new_q = n->rowq[rq ^ 1];
+    if (devr) {
+      // device-driven: the offers' compaction (new live count, row map, query
+      // list) takes effect at once, without the host
+      if (slot_next >= Ctx::kSlots) throw StatusError(PC_ERR_LOGIC, "graph: out of checkpoint slots");
+      int* map = pq ? n->perm2 : n->perm;
+      int* nR = n->d_slots + slot_next++;
+      prof_begin(n, PROF_OFFER, s2);
+      launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
+                   early_term ? 1 : 0, map, nR, new_q, n->ctr);
+      prof_end(n, s2);
+      if (allow_freeze && early_term) {
+        m.src = map;
+        dR = nR;
+        rq ^= 1;
+        row_q = n->rowq[rq];
+        pq ^= 1;
+        // the coefficient stream's next kernels read the new rows, map and count
+        stream_wait(n, s, s2);
+      }
+      return;
+    }
     prof_begin(n, PROF_OFFER, s2);
     launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
                  early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr);
@@ -761,7 +808,7 @@ struct Walker {
   // froze: the surviving rows stay in place and the next step reads them
   // through the latest offer's row map.
   void maybe_compact(Mat& m) {
-    if (dry || !(allow_freeze && early_term)) return;
+    if (dry || devr || !(allow_freeze && early_term)) return;
     static const int lazy = env_int("PC_LAZY_COMPACT", 0);
     if (lazy) {
       // keep computing frozen rows while the constants stream lags; compact
@@ -922,6 +969,49 @@ void allgather_rows(Ctx* n, const int* live, int n_rows, int width, double* dst)
 }
 
 // run_backsubstitution (backsub.hpp:993-1065)
+// Device-driven pass (graph mode): one chunk sized for every neuron of the
+// layer; the live count and rows come from the seed on the device.
+void run_pass_graph(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
+  cudaStream_t s = n->stream;
+  const HostLayer& Q = n->L[t];
+  const int N = (int)Q.numel();
+  const long long o = n->off[t];
+  const bool et = n->opt.early_term != 0;
+  launch_seed(s, N, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o, allow_freeze ? 1 : 0, et ? 1 : 0,
+              n->cand, n->frozen, n->live, n->d_int, &n->ctr->pad);
+  st->rows_total += N;
+  const bool affine = Q.kind == KIND_DENSE || Q.kind == KIND_CONV;
+  const WalkSize ws = walk_size(n, t, affine, true);
+  n->arena_used = 0;
+  reset_stats(n, ws.stats);
+  Walker w{n, s, t};
+  w.s2 = n->stream2;
+  w.devr = true;
+  w.dR = n->d_int;  // the seed's live count
+  w.R = N;
+  w.min_seen = N;
+  w.both = true;
+  w.allow_freeze = allow_freeze;
+  w.early_term = et;
+  w.st = st;
+  w.rq = 0;
+  w.row_q = n->live;  // the seed's live list (stable order)
+  Frame f0 = initial_frame(n, t, affine);
+  Mat m = w.alloc(f0, true);
+  if (affine)
+    launch_init_affine(s, Q.d, w.rows(), fdev(n, f0, t), n->dev + o, md(m));
+  else
+    launch_init_identity(s, w.rows(), fdev(n, f0, t), md(m));
+  w.mark(m);
+  if (affine) w.checkpoint(m);
+  w.walk(m, 0, true);
+  stream_wait(n, s, n->stream2);
+  ++n->gen;
+  launch_writeback(s, N, Q.out_c, t, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
+                   Q.feeds_relu ? n->relax + 8 * o : nullptr, n->gen_n, n->gen_pos, n->gen_l,
+                   n->gen, o, n->pofs[t]);
+}
+
 void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   cudaStream_t s = n->stream;
   const HostLayer& Q = n->L[t];
@@ -986,6 +1076,34 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   prof_end(n);
 }
 
+// Device-driven margin pass (graph mode): label and class list on the device;
+// best / has are read back after the graph.
+void run_margin_graph(Ctx* n, pc_stats* st) {
+  cudaStream_t s = n->stream;
+  const int out = (int)n->L.size() - 1;
+  const int nr = n->n_out - 1;
+  st->rows_total += nr;
+  if (nr <= 0) return;
+  launch_margin_rows(s, n->d_label, n->n_out, n->rowq[0]);
+  ck(cudaMemsetAsync(n->has, 0, nr, s), "memset");
+  const WalkSize ws = walk_size(n, out, false, false);
+  n->arena_used = 0;
+  reset_stats(n, ws.stats);
+  Walker w{n, s, out};
+  w.s2 = n->stream2;
+  w.R = nr;
+  w.min_seen = nr;
+  w.both = false;
+  w.margin = true;
+  w.st = st;
+  w.row_q = n->rowq[0];
+  Mat m = w.alloc(dense_frame(out), true);
+  launch_init_margin(s, 0, n->d_label, n->n_out, 0, nr, md(m));
+  w.mark(m);
+  w.walk(m, 0, true);
+  stream_wait(n, s, n->stream2);
+}
+
 // run_margin_pass (backsub.hpp:1070-1096)
 void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
   cudaStream_t s = n->stream;
@@ -1018,7 +1136,7 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
     w.row_q = n->rowq[0];
     Frame f0 = dense_frame(out);
     Mat m = w.alloc(f0, true);
-    launch_init_margin(s, label, n->n_out, mb, R, md(m));
+    launch_init_margin(s, label, nullptr, n->n_out, mb, R, md(m));
     w.mark(m);
     w.walk(m, 0, true);
     stream_wait(n, s, n->stream2);
@@ -1040,11 +1158,156 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
     if (!has[r]) throw StatusError(PC_ERR_LOGIC, "margin pass produced no candidate");
 }
 
+// Targets: layers feeding a relu, ascending, then the output (analyzer.hpp:220-223).
+std::vector<int> pass_targets(const Ctx* n) {
+  const int out = (int)n->L.size() - 1;
+  std::vector<int> targets;
+  for (int k = 1; k < out; ++k)
+    if (n->L[k].feeds_relu) targets.push_back(k);
+  targets.push_back(out);
+  return targets;
+}
+
+// The device-driven schedule needs every pass in one chunk sized for all of
+// the layer's neurons (the live count is only known on the device).
+bool graph_eligible(Ctx* n, size_t* arena_bytes, size_t* stat_count) {
+  if (n->net->shard_world > 1 || n->profile || n->opt.exec_mode != 2 || n->graph_failed) return false;
+  if (n->opt.chunk_rows > 0) return false;  // an explicit chunking request keeps the host schedule
+  size_t arena = 0, stats = 0;
+  for (int t : pass_targets(n)) {
+    const HostLayer& Q = n->L[t];
+    const WalkSize ws = walk_size(n, t, Q.kind == KIND_DENSE || Q.kind == KIND_CONV, true);
+    const size_t need = ws.per_row * (size_t)Q.numel() + 256 * ws.allocs + (1 << 20);
+    if ((long long)need > budget_of(n)) return false;
+    if (2 * Q.numel() > 65535) return false;  // rows ride in gridDim.y
+    arena = std::max(arena, need);
+    stats = std::max(stats, ws.stats);
+  }
+  const int out = (int)n->L.size() - 1;
+  const WalkSize wm = walk_size(n, out, false, false);
+  arena = std::max(arena, wm.per_row * (size_t)std::max(1, n->n_out - 1) + 256 * wm.allocs + (1 << 20));
+  stats = std::max(stats, wm.stats);
+  *arena_bytes = arena;
+  *stat_count = stats;
+  // Opt-in: grids sized for every neuron of a layer cost more than the
+  // launches they save when few rows are live (measured).
+  return n->opt.exec_mode == 2;
+}
+
+void forward_layers(Ctx* n, int k0, int k1) {  // layers (k0, k1]
+  for (int k = k0 + 1; k <= k1; ++k) {
+    const HostLayer& l = n->L[k];
+    prof_begin(n, PROF_FWD);
+    launch_forward_layer(n->stream, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
+                         n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
+                         n->gen_pos, n->gen_l, n->gen, 1);
+    prof_end(n);
+  }
+}
+
+// Capture the whole analysis (+ margin pass when with_margin) as one CUDA
+// graph on this context: ~all launches of an image become one graph launch.
+void capture_graph(Ctx* n, bool with_margin, size_t arena, size_t stat_count) {
+  cudaStream_t s = n->stream;
+  ensure_arena(n, arena);
+  reset_stats(n, stat_count);  // size the pool outside the capture
+  ck(cudaStreamSynchronize(s), "sync");
+  while (n->sync_pool.size() < 8192) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    n->sync_pool.push_back(e);
+  }
+  while (n->ev_pool.size() < 4096) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event");
+    n->ev_pool.push_back(e);
+  }
+  n->sync_used = 0;
+  n->ev_used = 0;
+  n->dense_ev.clear();
+  const long long l0 = g_launches;
+  g_dense_bytes = g_dense_madds = 0;
+  g_dense_launches = 0;
+  pc_stats st{};
+  ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+  cudaGraph_t g = nullptr;
+  try {
+    stream_wait(n, n->stream2, s);  // fork the constants stream into the capture
+    ck(cudaMemsetAsync(n->ctr, 0, sizeof(Counters), s), "memset");
+    const std::vector<int> targets = pass_targets(n);
+    const int out = (int)n->L.size() - 1;
+    forward_layers(n, 0, targets[0]);
+    for (size_t i = 0; i < targets.size(); ++i) {
+      run_pass_graph(n, targets[i], targets[i] != out, &st);
+      if (targets[i] != out) forward_layers(n, targets[i], targets[i + 1]);
+    }
+    if (with_margin) run_margin_graph(n, &st);
+    ck(cudaStreamEndCapture(s, &g), "capture");
+  } catch (...) {
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  ck(e, "graph instantiate");
+  if (n->graph) cudaGraphExecDestroy(n->graph);
+  n->graph = exec;
+  n->graph_label_mode = with_margin ? 1 : 0;
+  n->graph_st = st;
+  n->graph_dense_ev = n->dense_ev;
+  n->graph_dense_bytes = g_dense_bytes;
+  n->graph_dense_madds = g_dense_madds;
+  n->graph_dense_launches = g_dense_launches;
+  n->graph_launches = g_launches - l0;
+}
+
 // analyze + run_margin_pass (analyzer.hpp:198-276)
 void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
   cudaStream_t s = n->stream;
   const int nl = (int)n->L.size();
   const int out = nl - 1;
+  size_t arena = 0, stat_count = 0;
+  if (graph_eligible(n, &arena, &stat_count)) {
+    const bool with_margin = label >= 0;
+    if (!n->graph || n->graph_label_mode != (with_margin ? 1 : 0)) {
+      try {
+        capture_graph(n, with_margin, arena, stat_count);
+      } catch (const StatusError&) {
+        cudaGetLastError();
+        n->graph_failed = true;  // fall back to the host-driven schedule
+      }
+    }
+    if (n->graph && n->graph_label_mode == (with_margin ? 1 : 0)) {
+      n->h_int[2] = label;
+      ck(cudaMemcpyAsync(n->d_label, n->h_int + 2, sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
+      ck(cudaGraphLaunch(n->graph, s), "graph launch");
+      g_launches += n->graph_launches;
+      n->dense_ev = n->graph_dense_ev;
+      g_dense_bytes = n->graph_dense_bytes;
+      g_dense_madds = n->graph_dense_madds;
+      g_dense_launches = n->graph_dense_launches;
+      *st = n->graph_st;
+      const int nr = n->n_out - 1;
+      if (with_margin && nr > 0) {
+        ck(cudaMemcpyAsync(margins, n->best, sizeof(double) * nr, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaMemcpyAsync(n->h_int + 4, n->has, nr, cudaMemcpyDeviceToHost, s), "d2h");
+      }
+      Counters c{};
+      ck(cudaMemcpyAsync(&c, n->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s), "d2h");
+      ck(cudaStreamSynchronize(s), "sync");
+      const char* has = reinterpret_cast<const char*>(n->h_int + 4);
+      for (int r = 0; with_margin && r < nr; ++r)
+        if (!has[r]) throw StatusError(PC_ERR_LOGIC, "margin pass produced no candidate");
+      st->checkpoints += (long long)c.checkpoints;
+      st->gbc_dense_equiv += (long long)c.gbc_dense_equiv;
+      st->dense_madds += (long long)c.dense_madds;
+      st->gbc_madds += (long long)c.gbc_madds;
+      st->rows_terminated_early += (long long)(c.frozen + c.pad);
+      return;
+    }
+  }
   ck(cudaMemsetAsync(n->ctr, 0, sizeof(Counters), s), "memset");
   // Targets: layers feeding a relu, ascending, then the output (analyzer.hpp:220-223).
   std::vector<int> targets;
@@ -1169,9 +1432,9 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     cudaEventDestroy(t1);
     for (size_t e : n->dense_ev) {
       float d = 0;
-      cudaEventElapsedTime(&d, n->ev_pool[e], n->ev_pool[e + 1]);
-      g_dense_ms += d;
+      if (cudaEventElapsedTime(&d, n->ev_pool[e], n->ev_pool[e + 1]) == cudaSuccess) g_dense_ms += d;
     }
+    cudaGetLastError();  // timing is best effort; never leave a sticky error behind
     for (int c = 0; c < PROF_N; ++c) {
       g_prof_ms[c] = 0;
       g_prof_n[c] = 0;
@@ -1232,6 +1495,7 @@ void pc_default_options(pc_options* opt) {
   opt->chunk_rows = 0;
   opt->memory_budget = 0;
   opt->device = -1;
+  opt->exec_mode = 0;
 }
 
 const char* pc_last_error(void) { return g_err.c_str(); }
@@ -1286,6 +1550,7 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
   pc_status st = guard([&] {
     if (opt) n->opt = *opt;
     else pc_default_options(&n->opt);
+    if (n->opt.exec_mode == 0) n->opt.exec_mode = env_int("PC_EXEC_MODE", 0);  // tests / experiments
     validate(layers, n_layers, in_w, in_h, in_c, n->L);
     int devc = 0;
     ck(cudaGetDeviceCount(&devc), "cudaGetDeviceCount");

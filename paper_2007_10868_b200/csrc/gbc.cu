@@ -141,7 +141,8 @@ __device__ __noinline__ void gbc_task_exact(const GbcGeom& g, const double* FT, 
 __global__ void __launch_bounds__(256)
     k_gbc_tile(GbcGeom g, const double* __restrict__ FT, RowsDev rows, FrameDev fi, FrameDev fo,
                MatDev in, MatDev out) {
-  const int i = blockIdx.y;
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   int bw, bh, nbw, nbh;

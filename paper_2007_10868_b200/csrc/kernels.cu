@@ -514,7 +514,8 @@ void launch_writeback(cudaStream_t s, int n, int C, int layer, const double* can
 // by dev[q] (padded).
 __global__ void k_init_affine(LayerDev Q, RowsDev rows, FrameDev f, const double* dev_q,
                               MatDev out) {
-  const int i = blockIdx.y;
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   const long long cells = out.cells;
@@ -571,7 +572,8 @@ void launch_init_affine(cudaStream_t s, const LayerDev& Q, const RowsDev& rows, 
 
 // init_identity_rows: coefficient 1 at the query neuron, constant 0.
 __global__ void k_init_identity(RowsDev rows, FrameDev f, MatDev out) {
-  const int i = blockIdx.y;
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   const long long cells = out.cells;
@@ -599,7 +601,9 @@ void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f
 
 // init_margin_rows: +1 at label, -1 at class j, ascending j != label. Rows
 // [first, first + gridDim.x) of the margin rows (a rank's slice when sharded).
-__global__ void k_init_margin(int label, int n_out, int first, MatDev out) {
+// d_label (device-driven walks): the label is read from device memory.
+__global__ void k_init_margin(int label, const int* d_label, int n_out, int first, MatDev out) {
+  if (d_label) label = *d_label;
   const int r = blockIdx.x;
   const int g = first + r;
   const int j = g < label ? g : g + 1;
@@ -614,9 +618,22 @@ __global__ void k_init_margin(int label, int n_out, int first, MatDev out) {
   if (threadIdx.x < 4) out.K[4 * r + threadIdx.x] = 0.0;
 }
 
-void launch_init_margin(cudaStream_t s, int label, int n_out, int first, int count, MatDev out) {
+// The margin pass's query list: classes j != label, ascending (device label).
+__global__ void k_margin_rows(const int* d_label, int n_out, int* row_q) {
+  const int label = *d_label;
+  for (int j = threadIdx.x; j < n_out; j += blockDim.x)
+    if (j != label) row_q[j < label ? j : j - 1] = j;
+}
+
+void launch_margin_rows(cudaStream_t s, const int* d_label, int n_out, int* row_q) {
+  k_margin_rows<<<1, 256, 0, s>>>(d_label, n_out, row_q);
+  ++g_launches;
+}
+
+void launch_init_margin(cudaStream_t s, int label, const int* d_label, int n_out, int first,
+                        int count, MatDev out) {
   if (count <= 0) return;
-  k_init_margin<<<count, 128, 0, s>>>(label, n_out, first, out);
+  k_init_margin<<<count, 128, 0, s>>>(label, d_label, n_out, first, out);
   ++g_launches;
 }
 
@@ -724,8 +741,8 @@ __global__ void __launch_bounds__(32 * kChainWarps)
                    const double* dev, Counters* ctr, const char* frozen) {
   __shared__ double s_t[kChainWarps][3][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kChainWarps + warp;
-  if (i >= rows.n) return;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * kChainWarps + warp, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   if (frozen && frozen[q]) return;
@@ -832,8 +849,8 @@ __global__ void __launch_bounds__(32 * kChainWarps)
                  const char* frozen) {
   __shared__ double s_t[kChainWarps][2][2][32];  // [slot][lo/hi][cell]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kChainWarps + warp;
-  if (i >= rows.n) return;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * kChainWarps + warp, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   if (frozen && frozen[q]) return;
@@ -920,8 +937,8 @@ __global__ void __launch_bounds__(32 * kChainWarps)
                  const char* frozen) {
   __shared__ double s_t[kChainWarps][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kChainWarps + warp;
-  if (i >= rows.n) return;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * kChainWarps + warp, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   if (frozen && frozen[q]) return;
@@ -1007,13 +1024,17 @@ __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const doub
 
 template <int TM>
 __global__ void __launch_bounds__(kDC)
-    k_dense_coef(const double* __restrict__ W, int n_k, int n_in, int nrows, MatDev in,
+    k_dense_coef(const double* __restrict__ W, int n_k, int n_in, RowsDev rows, MatDev in,
                  MatDev out, double wmin, double wmax) {
   __shared__ double s_al[TM][kDK], s_ah[TM][kDK];
   __shared__ double s_w[kDK][kDC];
   const int tx = threadIdx.x;
   const int col = blockIdx.x * kDC + tx;
   const int r0 = blockIdx.y * TM;
+  int i0;
+  rows_resolve(rows, 0, i0);  // live row count (physical rows 0..n-1 in order)
+  const int nrows = rows.n;
+  if (r0 >= nrows) return;
   const bool band = products_in_band(in.stat, wmin, wmax);
   double lo[TM], hi[TM];
   bool bad[TM];
@@ -1064,20 +1085,24 @@ __global__ void __launch_bounds__(kDC)
   mag.flush(out.stat);
 }
 
-void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, MatDev out,
-                       cudaEvent_t ev0, cudaEvent_t ev1) {
+void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
+                       MatDev out, cudaEvent_t ev0, cudaEvent_t ev1) {
+  const int nrows = rows.n;
   const int n_k = (int)in.cells, n_in = (int)out.cells;
-  if (ev0) cudaEventRecord(ev0, s);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (ev0 || ev1) cudaStreamIsCapturing(s, &cap);
+  const unsigned rf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0;
+  if (ev0) cudaEventRecordWithFlags(ev0, s, rf);  // external: timeable inside graphs
   // Few rows: one row per thread maximises parallelism (the chain length n_k
   // bounds latency); many rows: 4 rows per thread for weight reuse.
   if (nrows <= 64) {
     dim3 grid(cdiv(n_in, kDC), nrows);
-    k_dense_coef<1><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, nrows, in, out, L.wmin, L.wmax);
+    k_dense_coef<1><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax);
   } else {
     dim3 grid(cdiv(n_in, kDC), cdiv(nrows, 4));
-    k_dense_coef<4><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, nrows, in, out, L.wmin, L.wmax);
+    k_dense_coef<4><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax);
   }
-  if (ev1) cudaEventRecord(ev1, s);
+  if (ev1) cudaEventRecordWithFlags(ev1, s, rf);
   ++g_launches;
 }
 
@@ -1148,7 +1173,8 @@ __device__ __forceinline__ Iv gbc_gather(const LayerDev& L, const FrameDev& fi, 
 
 __global__ void __launch_bounds__(256)
     k_gbc_coef(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, MatDev in, MatDev out) {
-  const int i = blockIdx.y;
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   int bw, bh, nbw, nbh;
@@ -1225,7 +1251,8 @@ __global__ void __launch_bounds__(32 * kSW)
   extern __shared__ double sm[];
   constexpr int kSP = kSW * PW;
   constexpr int kCWords = kSP * kSD * 2, kWWords = kSD * kSC, kBuf = kCWords + kWWords;
-  const int i = blockIdx.y;
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
   const int pt = blockIdx.x % g.pos_tiles, ct = blockIdx.x / g.pos_tiles;
   const int p0 = pt * kSP, ci0 = ct * kSC;
   bool upper;
@@ -1409,7 +1436,8 @@ __device__ __forceinline__ Iv relu_map(const Iv& c, const Iv& sp, const Iv& sn, 
 
 __global__ void __launch_bounds__(256)
     k_relu_coef(RowsDev rows, FrameDev f, MatDev in, MatDev out, const double* relax) {
-  const int i = blockIdx.y;
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   int bw, bh;
@@ -1459,7 +1487,8 @@ void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, Ma
 __global__ void __launch_bounds__(256)
     k_merge(RowsDev rows, FrameDev fa, FrameDev fb, FrameDev fu, int dense_path, MatDev a,
             MatDev b, MatDev out, int part) {
-  const int i = blockIdx.y;
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
   const int q = row_query(rows, i, upper);
   int abw, abh, bbw, bbh, ubw, ubh;
@@ -1530,6 +1559,7 @@ __global__ void __launch_bounds__(kScanThreads)
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
   __shared__ int s_live;
+  if (rows.dR) R = *rows.dR;  // device-driven walk: the live rows of this checkpoint
   if (threadIdx.x == 0) {
     s_base = 0;
     s_live = 0;
@@ -1649,7 +1679,7 @@ void init_kernel_attrs_kernels() {
   carve(k_init_margin); carve(k_chain_affine); carve(k_chain_relu); carve(k_concretize);
   carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef);
   carve(k_relu_coef); carve(k_merge); carve(k_offer); carve(k_shard_pack); carve(k_shard_unpack);
-  carve(k_margin_offer);
+  carve(k_margin_offer); carve(k_margin_rows);
   carve(k_gbc_smem<1>); carve(k_gbc_smem<2>); carve(k_gbc_smem<4>); carve(k_gbc_smem<8>);
   cudaFuncSetAttribute(k_gbc_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbc_smem_bytes<1>());
   cudaFuncSetAttribute(k_gbc_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbc_smem_bytes<2>());

@@ -154,9 +154,38 @@ __host__ __device__ __forceinline__ size_t phys_row(const MatDev& m, int i) {
 
 struct RowsDev {
   const int* row_q;
-  int n;     // total rows
-  int n_up;  // upper rows come first
+  int n;     // total rows (launch bound when dR is set)
+  int n_up;  // upper rows come first (launch bound when dR is set)
+  // Device-driven walks (graph mode): the live rows per polarity are read from
+  // device memory (written by the pass seed and by each checkpoint's offers);
+  // launches are sized for the bound above and surplus blocks exit.
+  const int* dR = nullptr;
 };
+
+// Resolve the block-row index b of a launch into logical row i of the rows
+// actually live (upper rows [0, R), lower rows [R, 2R)); false: no such row.
+// Updates r.n / r.n_up to the live values.
+__device__ __forceinline__ bool rows_resolve(RowsDev& r, int b, int& i) {
+  if (!r.dR) {
+    i = b;
+    return b < r.n;
+  }
+  const int R = *r.dR;
+  if (r.n_up == 0) {  // one polarity (margin rows)
+    r.n = R;
+    i = b;
+    return b < R;
+  }
+  const int Rmax = r.n_up;
+  r.n = 2 * R;
+  r.n_up = R;
+  if (b < Rmax) {
+    i = b;
+    return b < R;
+  }
+  i = R + (b - Rmax);
+  return b - Rmax < R;
+}
 
 __device__ __forceinline__ int row_query(const RowsDev& r, int i, bool& upper) {
   upper = i < r.n_up;
@@ -192,7 +221,9 @@ void launch_writeback(cudaStream_t s, int n, int C, int layer, const double* can
 void launch_init_affine(cudaStream_t s, const LayerDev& Q, const RowsDev& rows, const FrameDev& f,
                         const double* dev_q, MatDev out);
 void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev out);
-void launch_init_margin(cudaStream_t s, int label, int n_out, int first, int count, MatDev out);
+void launch_init_margin(cudaStream_t s, int label, const int* d_label, int n_out, int first,
+                        int count, MatDev out);
+void launch_margin_rows(cudaStream_t s, const int* d_label, int n_out, int* row_q);
 
 // Chains read the constants of m (through m.src) and write compact ones to Kout.
 // frozen (nullable): rows whose query neuron froze at an earlier checkpoint
@@ -221,8 +252,8 @@ void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& 
 // overrides, read once; the tests force 1 to run the corpus through them).
 long long big_chain_cells();
 
-void launch_dense_coef(cudaStream_t s, const LayerDev& L, int nrows, MatDev in, MatDev out,
-                       cudaEvent_t ev0, cudaEvent_t ev1);
+void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
+                       MatDev out, cudaEvent_t ev0, cudaEvent_t ev1);
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out);
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,

@@ -26,6 +26,7 @@ class AnalysisOptions:  # analyzer.hpp:164-169
     chunk_rows: int = 0
     memory_budget: int = 0  # 0: engine default (16 GiB of device workspace)
     device: int = -1
+    exec_mode: int = 0  # 0 auto, 1 host-driven schedule, 2 device-driven (CUDA graph)
 
 
 @dataclass
@@ -78,6 +79,7 @@ class Verifier:
         o.chunk_rows = int(self.options.chunk_rows)
         o.memory_budget = int(self.options.memory_budget)
         o.device = int(self.options.device)
+        o.exec_mode = int(self.options.exec_mode)
         descs = net.descs()
         h = ctypes.c_void_p()
         w, hh, c = net.input_shape
