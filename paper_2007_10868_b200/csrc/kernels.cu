@@ -37,7 +37,7 @@ int env_int(const char* name, int dflt) {
 long long big_chain_cells() {
   static const long long v = [] {
     const char* e = getenv("PC_BIG_CHAIN_CELLS");
-    return e && *e ? atoll(e) : 1024ll;
+    return e && *e ? atoll(e) : 256ll;
   }();
   return v;
 }
@@ -986,7 +986,15 @@ void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, M
 // (the reduction) stream through shared memory in ascending slabs. Fast
 // branch-free ops; any output whose operands leave the fast band is
 // recomputed with the exact ops.
-constexpr int kDC = 128, kDK = 32;
+constexpr int kDC = 128, kDK = 16;  // columns per block, frame cells per slab
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 __device__ __forceinline__ void madd_fast(double w, double clo, double chi, double& lo, double& hi,
                                           bool& bad) {
@@ -1009,16 +1017,52 @@ __device__ __forceinline__ void madd_exact(double w, double clo, double chi, dou
 
 template <int TM, bool BAND>
 __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const double (*s_ah)[kDK],
-                                           const double (*s_w)[kDC], int kn, int tx, double* lo,
-                                           double* hi, bool* bad) {
-#pragma unroll 2
-  for (int kk = 0; kk < kn; ++kk) {
-    const double w = s_w[kk][tx];
+                                           const double* w, int kn, double* lo, double* hi,
+                                           bool* bad) {
+#pragma unroll
+  for (int kk = 0; kk < kDK; ++kk) {
+    if (kk >= kn) break;
 #pragma unroll
     for (int u = 0; u < TM; ++u) {
-      if (BAND) madd_band(w, s_al[u][kk], s_ah[u][kk], lo[u], hi[u]);
-      else madd_fast(w, s_al[u][kk], s_ah[u][kk], lo[u], hi[u], bad[u]);
+      if (BAND) {
+        // one row per thread: the chain is latency bound, take the short form
+        if (TM == 1) madd_band_lat(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u]);
+        else madd_band(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u]);
+      } else {
+        madd_fast(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u], bad[u]);
+      }
     }
+  }
+}
+
+// Row slabs (shared by every column of the block) stream through a
+// double buffer filled by cp.async one slab ahead; each thread's own weight
+// column is prefetched into registers one slab ahead.
+template <int TM>
+struct DenseSmem {
+  double al[2][TM][kDK], ah[2][TM][kDK];
+};
+
+template <int TM>
+__device__ __forceinline__ void dense_stage(DenseSmem<TM>& sm, int b, int k0, int n_k, int r0,
+                                            int nrows, const MatDev& in, int tx) {
+  for (int e = tx; e < TM * kDK; e += kDC) {
+    const int rr = e / kDK, kk = e % kDK;
+    const int r = r0 + rr, k = k0 + kk;
+    const bool ok = r < nrows && k < n_k;
+    const size_t o = ok ? phys_row(in, r) * (size_t)n_k + k : 0;
+    cp_async8(&sm.al[b][rr][kk], in.lo + o, ok);
+    cp_async8(&sm.ah[b][rr][kk], in.hi + o, ok);
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ void dense_wload(double* w, const double* __restrict__ W, int k0, int n_k,
+                                            int n_in, int col) {
+#pragma unroll
+  for (int kk = 0; kk < kDK; ++kk) {
+    const int k = k0 + kk;
+    w[kk] = (k < n_k && col < n_in) ? __ldg(W + (size_t)k * n_in + col) : 0.0;
   }
 }
 
@@ -1026,8 +1070,7 @@ template <int TM>
 __global__ void __launch_bounds__(kDC)
     k_dense_coef(const double* __restrict__ W, int n_k, int n_in, RowsDev rows, MatDev in,
                  MatDev out, double wmin, double wmax) {
-  __shared__ double s_al[TM][kDK], s_ah[TM][kDK];
-  __shared__ double s_w[kDK][kDC];
+  __shared__ DenseSmem<TM> sm;
   const int tx = threadIdx.x;
   const int col = blockIdx.x * kDC + tx;
   const int r0 = blockIdx.y * TM;
@@ -1043,23 +1086,22 @@ __global__ void __launch_bounds__(kDC)
     lo[u] = hi[u] = 0.0;
     bad[u] = false;
   }
-  for (int k0 = 0; k0 < n_k; k0 += kDK) {
-    __syncthreads();
-    for (int e = tx; e < TM * kDK; e += kDC) {
-      const int rr = e / kDK, kk = e % kDK;
-      const int r = r0 + rr, k = k0 + kk;
-      const bool ok = r < nrows && k < n_k;
-      s_al[rr][kk] = ok ? in.lo[phys_row(in, r) * n_k + k] : 0.0;
-      s_ah[rr][kk] = ok ? in.hi[phys_row(in, r) * n_k + k] : 0.0;
+  const int nslab = (n_k + kDK - 1) / kDK;
+  double w[kDK], wn[kDK];
+  dense_stage<TM>(sm, 0, 0, n_k, r0, nrows, in, tx);
+  dense_wload(w, W, 0, n_k, n_in, col);
+  for (int sl = 0; sl < nslab; ++sl) {
+    cp_async_wait_all();
+    __syncthreads();  // slab sl landed; slab sl-1 consumed
+    if (sl + 1 < nslab) {
+      dense_stage<TM>(sm, (sl + 1) & 1, (sl + 1) * kDK, n_k, r0, nrows, in, tx);
+      dense_wload(wn, W, (sl + 1) * kDK, n_k, n_in, col);
     }
-    for (int kk = 0; kk < kDK; ++kk) {
-      const int k = k0 + kk;
-      s_w[kk][tx] = (k < n_k && col < n_in) ? W[(size_t)k * n_in + col] : 0.0;
-    }
-    __syncthreads();
-    const int kn = min(kDK, n_k - k0);
-    if (band) dense_slab<TM, true>(s_al, s_ah, s_w, kn, tx, lo, hi, bad);
-    else dense_slab<TM, false>(s_al, s_ah, s_w, kn, tx, lo, hi, bad);
+    const int b = sl & 1, kn = min(kDK, n_k - sl * kDK);
+    if (band) dense_slab<TM, true>(sm.al[b], sm.ah[b], w, kn, lo, hi, bad);
+    else dense_slab<TM, false>(sm.al[b], sm.ah[b], w, kn, lo, hi, bad);
+#pragma unroll
+    for (int kk = 0; kk < kDK; ++kk) w[kk] = wn[kk];
   }
   if (band) {
 #pragma unroll
@@ -1234,13 +1276,6 @@ struct GbcSmemGeom {
   int n_pos, pos_tiles, ci_tiles;
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 8 : 0;  // src-size 0: zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 // PW positions per warp (CTA: kSW warps = kSW*PW positions x kSC channels;
 // lane l owns channels 2l, 2l+1 of the CTA's 64).

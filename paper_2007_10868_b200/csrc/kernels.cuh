@@ -145,6 +145,23 @@ __device__ __forceinline__ void madd_band(double w, double cl, double ch, double
   lo = __fma_rd(__dsub_rn(ul, dl), -0.5, sl);
   hi = __fma_ru(__dsub_rn(uh, dh), 0.5, sh);
 }
+// Same result as madd_band with a shorter dependency chain through the
+// accumulators (2 FP64 latencies + a select instead of 3): for latency-bound
+// chains with little independent work per thread.
+__device__ __forceinline__ void madd_band_lat(double w, double cl, double ch, double& lo,
+                                              double& hi) {
+  const bool neg = __double2hiint(w) < 0;
+  const double a = neg ? ch : cl, b = neg ? cl : ch;
+  const double pl0 = __dmul_rn(a, w), ph0 = __dmul_rn(b, w);
+  const double pl = __dadd_rd(pl0, -fabs(__fma_rn(a, w, -pl0)));
+  const double ph = __dadd_ru(ph0, fabs(__fma_rn(b, w, -ph0)));
+  const double sl = __dadd_rn(lo, pl), sh = __dadd_rn(hi, ph);
+  const bool xl = __dadd_rd(lo, pl) == __dadd_ru(lo, pl), xh = __dadd_rd(hi, ph) == __dadd_ru(hi, ph);
+  const double tl = __dadd_rd(sl, -4.9406564584124654e-324), th = __dadd_ru(sh, 4.9406564584124654e-324);
+  lo = xl ? sl : tl;
+  hi = xh ? sh : th;
+}
+
 // -0 -> +0 (RN: -0 + +0 = +0), everything else unchanged.
 __device__ __forceinline__ double canon0(double x) { return __dadd_rn(x, 0.0); }
 
