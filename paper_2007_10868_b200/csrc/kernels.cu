@@ -1019,6 +1019,32 @@ template <int TM, bool BAND>
 __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const double (*s_ah)[kDK],
                                            const double* w, int kn, double* lo, double* hi,
                                            bool* bad) {
+  if constexpr (BAND && TM == 1) {
+    // One row per thread: the add chain is the critical path. Form the slab's
+    // outward-rounded products first (independent of the accumulators), then
+    // run the two chains back to back.
+    double pl[kDK], ph[kDK];
+#pragma unroll
+    for (int kk = 0; kk < kDK; ++kk) {
+      const double wk = kk < kn ? w[kk] : 0.0;
+      const bool neg = __double2hiint(wk) < 0;
+      const double cl = s_al[0][kk], ch = s_ah[0][kk];
+      const double a = neg ? ch : cl, b = neg ? cl : ch;
+      const double p0 = __dmul_rn(a, wk), p1 = __dmul_rn(b, wk);
+      pl[kk] = __dadd_rd(p0, -fabs(__fma_rn(a, wk, -p0)));
+      ph[kk] = __dadd_ru(p1, fabs(__fma_rn(b, wk, -p1)));
+    }
+#pragma unroll
+    for (int kk = 0; kk < kDK; ++kk) {
+      const double sl = __dadd_rn(lo[0], pl[kk]), sh = __dadd_rn(hi[0], ph[kk]);
+      const bool xl = __dadd_rd(lo[0], pl[kk]) == __dadd_ru(lo[0], pl[kk]);
+      const bool xh = __dadd_rd(hi[0], ph[kk]) == __dadd_ru(hi[0], ph[kk]);
+      const double tl = __dadd_rd(sl, -4.9406564584124654e-324);
+      const double th = __dadd_ru(sh, 4.9406564584124654e-324);
+      lo[0] = xl ? sl : tl;  // a zero product (kk >= kn) adds an exact +-0: no-op
+      hi[0] = xh ? sh : th;
+    }
+  } else {
 #pragma unroll
   for (int kk = 0; kk < kDK; ++kk) {
     if (kk >= kn) break;
@@ -1032,6 +1058,7 @@ __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const doub
         madd_fast(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u], bad[u]);
       }
     }
+  }
   }
 }
 
