@@ -306,7 +306,8 @@ const char* kProfNames[PROF_N] = {"forward", "seed", "init", "chain_affine", "de
                                   "offer", "writeback"};
 thread_local double g_prof_ms[PROF_N];
 thread_local long long g_prof_n[PROF_N];
-thread_local double g_gap_ms[PROF_N];  // device idle (or unprofiled work) before each class
+thread_local double g_gap_ms[PROF_N];
+thread_local double g_gbc_window_madds = 0;  // PC_PROFILE: madds of the conv steps if no coefficient were zero  // device idle (or unprofiled work) before each class
 
 cudaEvent_t take_event(Ctx* n) {
   while (n->ev_pool.size() <= n->ev_used) {
@@ -666,8 +667,11 @@ struct Walker {
                           n->ctr, fz());
       prof_end(n, s2);
       prof_begin(n, PROF_GBC);
-      launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out));
+      launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out), n->d_int + 6);
       prof_end(n);
+      if (n->profile)  // dense-window work of this step (all coefficients nonzero)
+        g_gbc_window_madds += (double)nrows() * fo.S_w * fo.S_h * L.in_c * L.out_c *
+                              ((double)L.fh * L.fw / ((double)L.sh * L.sw));
       mark(out);
     }
     m = out;
@@ -1415,6 +1419,7 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     std::vector<double> m(std::max(1, n->n_out - 1), 0.0);
     n->ev_used = 0;
     n->sync_used = 0;
+    g_gbc_window_madds = 0;
     n->prof.clear();
     n->dense_ev.clear();
     run_test(n, label, m.data(), &st);
@@ -1681,7 +1686,7 @@ int pc_last_profile(char* buf, int len) {
          std::to_string(g_prof_ms[c]) + "], \"gap:" + kProfNames[c] + "\": [0, " +
          std::to_string(g_gap_ms[c]) + "]";
   }
-  j += "}";
+  j += ", \"gbc_window_madds\": [0, " + std::to_string(g_gbc_window_madds) + "]}";
   if (buf && len > 0) {
     std::strncpy(buf, j.c_str(), len - 1);
     buf[len - 1] = 0;

@@ -7,6 +7,7 @@
 // constant/concretisation chain is one lane.
 #include <cub/block/block_scan.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -1305,17 +1306,22 @@ struct GbcSmemGeom {
 
 
 // PW positions per warp (CTA: kSW warps = kSW*PW positions x kSC channels;
-// lane l owns channels 2l, 2l+1 of the CTA's 64).
+// lane l owns channels 2l, 2l+1 of the CTA's 64). Work items (row, position
+// tile, channel tile) are taken from an atomic queue by a grid sized to the
+// resident capacity, so rows whose coefficients are mostly zero (fast items)
+// do not leave SMs idle.
 template <int PW>
-__global__ void __launch_bounds__(32 * kSW)
-    k_gbc_smem(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, MatDev in, MatDev out,
-               GbcSmemGeom g) {
-  extern __shared__ double sm[];
+__device__ __forceinline__ void gbc_smem_item(const LayerDev& L, RowsDev rows, const FrameDev& fi,
+                                              const FrameDev& fo, const MatDev& in,
+                                              const MatDev& out, const GbcSmemGeom& g, int item,
+                                              double* sm, MagAcc& mag) {
   constexpr int kSP = kSW * PW;
   constexpr int kCWords = kSP * kSD * 2, kWWords = kSD * kSC, kBuf = kCWords + kWWords;
+  const int tiles = g.pos_tiles * g.ci_tiles;
   int i;
-  if (!rows_resolve(rows, blockIdx.y, i)) return;
-  const int pt = blockIdx.x % g.pos_tiles, ct = blockIdx.x / g.pos_tiles;
+  if (!rows_resolve(rows, item / tiles, i)) return;
+  const int t = item % tiles;
+  const int pt = t % g.pos_tiles, ct = t / g.pos_tiles;
   const int p0 = pt * kSP, ci0 = ct * kSC;
   bool upper;
   const int q = row_query(rows, i, upper);
@@ -1329,7 +1335,6 @@ __global__ void __launch_bounds__(32 * kSW)
   const bool band = products_in_band(in.stat, L.wmin, L.wmax);
   double* olo = out.lo + (size_t)i * out.cells;
   double* ohi = out.hi + (size_t)i * out.cells;
-  MagAcc mag;
   if (!band) {  // checked fast ops, exact recompute on a flagged output
     for (int e = tid; e < kSP * kSC; e += blockDim.x) {
       const int p = p0 + e / kSC, ci = ci0 + e % kSC;
@@ -1344,7 +1349,6 @@ __global__ void __launch_bounds__(32 * kSW)
       mag.add(acc.lo);
       mag.add(acc.hi);
     }
-    mag.flush(out.stat);
     return;
   }
   const int ntaps = L.fh * L.fw;
@@ -1422,6 +1426,23 @@ __global__ void __launch_bounds__(32 * kSW)
       mag.add(hi[k][j]);
     }
   }
+}
+
+template <int PW>
+__global__ void __launch_bounds__(32 * kSW)
+    k_gbc_smem(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, MatDev in, MatDev out,
+               GbcSmemGeom g, int* queue, int n_items) {
+  extern __shared__ double sm[];
+  __shared__ int s_item;
+  MagAcc mag;
+  for (;;) {
+    __syncthreads();  // the previous item is done with s_item and the buffers
+    if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= n_items) break;
+    gbc_smem_item<PW>(L, rows, fi, fo, in, out, g, item, sm, mag);
+  }
   mag.flush(out.stat);
 }
 
@@ -1431,38 +1452,59 @@ static bool gbc_smem_eligible(const LayerDev& L, const FrameDev& fout) {
 }
 
 void launch_gbc_smem(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
-                     const FrameDev& fout, MatDev in, MatDev out) {
+                     const FrameDev& fout, MatDev in, MatDev out, int* queue) {
   GbcSmemGeom g;
   g.n_pos = fout.S_w * fout.S_h;
   g.ci_tiles = (L.in_c + kSC - 1) / kSC;
-  // positions per warp: the most reuse that still gives >= 4 CTAs per SM
+  // positions per warp: the most reuse that still gives >= 4 items per SM
   static const int forced = env_int("PC_GBC_PW", 0);
   int pw = forced;
   if (!pw) {
     pw = 1;
     for (int c : {8, 4, 2}) {
-      const long long ctas = (long long)((g.n_pos + kSW * c - 1) / (kSW * c)) * g.ci_tiles * rows.n;
-      if (ctas >= 4 * 148) { pw = c; break; }
+      const long long items = (long long)((g.n_pos + kSW * c - 1) / (kSW * c)) * g.ci_tiles * rows.n;
+      if (items >= 4 * 148) { pw = c; break; }
     }
   }
   g.pos_tiles = (g.n_pos + kSW * pw - 1) / (kSW * pw);
-  dim3 grid(g.pos_tiles * g.ci_tiles, rows.n);
+  const long long items = (long long)g.pos_tiles * g.ci_tiles * rows.n;
+  // resident CTAs per SM for this variant (registers / shared memory), once
+  static int occ[9] = {0};
+  if (!occ[pw]) {
+    int b = 1;
+    switch (pw) {
+      case 8: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gbc_smem<8>, 32 * kSW, gbc_smem_bytes<8>()); break;
+      case 4: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gbc_smem<4>, 32 * kSW, gbc_smem_bytes<4>()); break;
+      case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gbc_smem<2>, 32 * kSW, gbc_smem_bytes<2>()); break;
+      default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gbc_smem<1>, 32 * kSW, gbc_smem_bytes<1>()); break;
+    }
+    occ[pw] = b > 0 ? b : 1;
+  }
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const unsigned grid = (unsigned)std::min<long long>(items, (long long)sms * occ[pw]);
+  cudaMemsetAsync(queue, 0, sizeof(int), s);
+  const int n_items = (int)items;
   switch (pw) {
-    case 8: k_gbc_smem<8><<<grid, 32 * kSW, gbc_smem_bytes<8>(), s>>>(L, rows, fin, fout, in, out, g); break;
-    case 4: k_gbc_smem<4><<<grid, 32 * kSW, gbc_smem_bytes<4>(), s>>>(L, rows, fin, fout, in, out, g); break;
-    case 2: k_gbc_smem<2><<<grid, 32 * kSW, gbc_smem_bytes<2>(), s>>>(L, rows, fin, fout, in, out, g); break;
-    default: k_gbc_smem<1><<<grid, 32 * kSW, gbc_smem_bytes<1>(), s>>>(L, rows, fin, fout, in, out, g); break;
+    case 8: k_gbc_smem<8><<<grid, 32 * kSW, gbc_smem_bytes<8>(), s>>>(L, rows, fin, fout, in, out, g, queue, n_items); break;
+    case 4: k_gbc_smem<4><<<grid, 32 * kSW, gbc_smem_bytes<4>(), s>>>(L, rows, fin, fout, in, out, g, queue, n_items); break;
+    case 2: k_gbc_smem<2><<<grid, 32 * kSW, gbc_smem_bytes<2>(), s>>>(L, rows, fin, fout, in, out, g, queue, n_items); break;
+    default: k_gbc_smem<1><<<grid, 32 * kSW, gbc_smem_bytes<1>(), s>>>(L, rows, fin, fout, in, out, g, queue, n_items); break;
   }
   ++g_launches;
 }
 
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
-                     const FrameDev& fout, MatDev in, MatDev out) {
+                     const FrameDev& fout, MatDev in, MatDev out, int* queue) {
   // PC_GBC: 2 (default) shared-memory tiled kernel where eligible, 1 the
   // register-blocked gather, 0 the one-output-per-thread gather
   static const int variant = env_int("PC_GBC", 2);
-  if (variant == 2 && gbc_smem_eligible(L, fout)) {
-    launch_gbc_smem(s, L, rows, fin, fout, in, out);
+  if (variant == 2 && gbc_smem_eligible(L, fout) && queue) {
+    launch_gbc_smem(s, L, rows, fin, fout, in, out, queue);
     return;
   }
   if (variant == 1) {

@@ -271,8 +271,9 @@ long long big_chain_cells();
 
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
                        MatDev out, cudaEvent_t ev0, cudaEvent_t ev1);
+// queue: a device int the work-queue variant resets and consumes (per stream).
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
-                     const FrameDev& fout, MatDev in, MatDev out);
+                     const FrameDev& fout, MatDev in, MatDev out, int* queue);
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out);
 // Engine switches from the environment (read once): PC_GBC=0 selects the
