@@ -659,6 +659,19 @@ struct Walker {
     }
     Mat out = alloc(nf, false);
     out.K = k_out(m);
+    // compacted nonzero input coefficients for the sparse conv kernel
+    const bool sparse = gbc_sparse_wanted(L.d);
+    SparseDev sp{};
+    if (sparse) {
+      const FrameDev fi0 = fdev(n, m.f, q);
+      sp.ncell = fi0.S_w * fi0.S_h;
+      sp.C = fi0.C;
+      const size_t rows_n = (size_t)alloc_rows(), slots = rows_n * (size_t)m.cells;
+      sp.cnt = reinterpret_cast<int*>(arena_take(rows_n * sp.ncell * sizeof(int)));
+      sp.idx = reinterpret_cast<unsigned short*>(arena_take(slots * sizeof(unsigned short)));
+      sp.lo = arena_take(slots * sizeof(double));
+      sp.hi = arena_take(slots * sizeof(double));
+    }
     if (!dry) {
       const FrameDev fi = fdev(n, m.f, q), fo = fdev(n, nf, q);
       need(m);
@@ -667,7 +680,12 @@ struct Walker {
                           n->ctr, fz());
       prof_end(n, s2);
       prof_begin(n, PROF_GBC);
-      launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out), n->d_int + 6);
+      if (sparse) {
+        launch_compact_cells(s, rows(), md(m), sp);
+        launch_gbc_sparse(s, L.d, rows(), fi, fo, sp, md(m), md(out));
+      } else {
+        launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out), n->d_int + 6);
+      }
       prof_end(n);
       if (n->profile)  // dense-window work of this step (all coefficients nonzero)
         g_gbc_window_madds += (double)nrows() * fo.S_w * fo.S_h * L.in_c * L.out_c *

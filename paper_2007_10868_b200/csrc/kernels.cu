@@ -1498,12 +1498,147 @@ void launch_gbc_smem(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
   ++g_launches;
 }
 
+// ---------------------------------------------------------------------------
+// Sparse conv back-substitution. About two thirds of a conv step's input
+// coefficients are zero on the ResNets (relu steps zero the stable-negative
+// neurons), and zero coefficients contribute nothing (the reference skips
+// them in iv_acc). k_compact_cells packs each frame cell's nonzero channels
+// (ascending, with their index) once; k_gbc_sparse then gathers only those,
+// in the reference's (ch, cw, d) order, without per-channel zero tests.
+
+__global__ void __launch_bounds__(256)
+    k_compact_cells(RowsDev rows, MatDev m, SparseDev sp) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = sp.C;
+  const double* lo = m.lo + phys_row(m, i) * m.cells;
+  const double* hi = m.hi + phys_row(m, i) * m.cells;
+  for (int cell = blockIdx.x * 8 + warp; cell < sp.ncell; cell += gridDim.x * 8) {
+    const size_t slot = ((size_t)i * sp.ncell + cell) * C;
+    int base = 0;
+    for (int c0 = 0; c0 < C; c0 += 32) {
+      const int c = c0 + lane;
+      double a = 0.0, b = 0.0;
+      if (c < C) {
+        a = lo[(size_t)cell * C + c];
+        b = hi[(size_t)cell * C + c];
+      }
+      const bool nz = c < C && !(bits_zero(a) && bits_zero(b));
+      const unsigned mask = __ballot_sync(0xffffffffu, nz);
+      if (nz) {
+        const int k = base + __popc(mask & ((1u << lane) - 1u));
+        sp.idx[slot + k] = (unsigned short)c;
+        sp.lo[slot + k] = a;
+        sp.hi[slot + k] = b;
+      }
+      base += __popc(mask);
+    }
+    if (lane == 0) sp.cnt[(size_t)i * sp.ncell + cell] = base;
+  }
+}
+
+void launch_compact_cells(cudaStream_t s, const RowsDev& rows, MatDev m, SparseDev sp) {
+  unsigned gx = cdiv(sp.ncell, 8);
+  if (gx > 512) gx = 512;
+  dim3 grid(gx, rows.n);
+  k_compact_cells<<<grid, 256, 0, s>>>(rows, m, sp);
+  ++g_launches;
+}
+
+__global__ void __launch_bounds__(256)
+    k_gbc_sparse(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
+                 MatDev out) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw, bh, nbw, nbh;
+  frame_base(fi, q, bw, bh);
+  frame_base(fo, q, nbw, nbh);
+  const long long ocells = out.cells;
+  const double* ilo = in.lo + phys_row(in, i) * in.cells;
+  const double* ihi = in.hi + phys_row(in, i) * in.cells;
+  const int cin = L.in_c, cout = L.out_c;
+  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  const int* cnt = sp.cnt + (size_t)i * sp.ncell;
+  const size_t rbase = (size_t)i * sp.ncell * sp.C;
+  MagAcc mag;
+  for (long long o = blockIdx.x * blockDim.x + threadIdx.x; o < ocells;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int ci = (int)(o % cin);
+    const int x = (int)((o / cin) % fo.S_w);
+    const int y = (int)(o / ((long long)cin * fo.S_w));
+    const int iy = nbh + y, ix = nbw + x;
+    Iv acc;
+    if (!band) {
+      bool bad = false;
+      acc = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+      if (bad) acc = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+    } else {
+      int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
+      int aw0 = floordiv(ix + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ix + L.pw, L.sw);
+      ah0 = max(ah0, bh);
+      ah1 = min(ah1, bh + fi.S_h - 1);
+      aw0 = max(aw0, bw);
+      aw1 = min(aw1, bw + fi.S_w - 1);
+      double lo = 0.0, hi = 0.0;
+      for (int ah = ah0; ah <= ah1; ++ah) {
+        const int fy = iy + L.ph - ah * L.sh;
+        for (int aw = aw0; aw <= aw1; ++aw) {
+          const int fx = ix + L.pw - aw * L.sw;
+          const int cell = (ah - bh) * fi.S_w + (aw - bw);
+          const int n = cnt[cell];
+          const size_t sb = rbase + (size_t)cell * sp.C;
+          const double* wp = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ci;
+          constexpr int kB = 8;
+          int e = 0;
+          for (; e + kB <= n; e += kB) {
+            double cl[kB], ch[kB], w[kB];
+#pragma unroll
+            for (int k = 0; k < kB; ++k) {
+              const int d = sp.idx[sb + e + k];
+              cl[k] = sp.lo[sb + e + k];
+              ch[k] = sp.hi[sb + e + k];
+              w[k] = wp[(size_t)d * cin];
+            }
+#pragma unroll
+            for (int k = 0; k < kB; ++k) madd_band(w[k], cl[k], ch[k], lo, hi);
+          }
+          for (; e < n; ++e)
+            madd_band(wp[(size_t)sp.idx[sb + e] * cin], sp.lo[sb + e], sp.hi[sb + e], lo, hi);
+        }
+      }
+      acc = Iv{canon0(lo), hi};
+    }
+    out.lo[(size_t)i * ocells + o] = acc.lo;
+    out.hi[(size_t)i * ocells + o] = acc.hi;
+    mag.add(acc.lo);
+    mag.add(acc.hi);
+  }
+  mag.flush(out.stat);
+}
+
+void launch_gbc_sparse(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                       const FrameDev& fout, SparseDev sp, MatDev in, MatDev out) {
+  unsigned gx = cdiv(out.cells, 256);
+  if (gx > 1024) gx = 1024;
+  dim3 grid(gx, rows.n);
+  k_gbc_sparse<<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out);
+  ++g_launches;
+}
+
+bool gbc_sparse_wanted(const LayerDev& L) {
+  static const int variant = env_int("PC_GBC", 3);
+  return variant == 3 && L.in_c >= 32 && L.out_c <= 65535;
+}
+
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out, int* queue) {
   // PC_GBC: 2 (default) shared-memory tiled kernel where eligible, 1 the
   // register-blocked gather, 0 the one-output-per-thread gather
-  static const int variant = env_int("PC_GBC", 2);
-  if (variant == 2 && gbc_smem_eligible(L, fout) && queue) {
+  static const int variant = env_int("PC_GBC", 3);
+  if (variant >= 2 && gbc_smem_eligible(L, fout) && queue) {
     launch_gbc_smem(s, L, rows, fin, fout, in, out, queue);
     return;
   }
@@ -1781,7 +1916,7 @@ void init_kernel_attrs_kernels() {
   carve(k_fwd_dense); carve(k_fwd_conv); carve(k_fwd_relu); carve(k_fwd_join); carve(k_relax);
   carve(k_seed); carve(k_writeback); carve(k_init_affine); carve(k_init_identity);
   carve(k_init_margin); carve(k_chain_affine); carve(k_chain_relu); carve(k_concretize);
-  carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef);
+  carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef); carve(k_gbc_sparse); carve(k_compact_cells);
   carve(k_relu_coef); carve(k_merge); carve(k_offer); carve(k_shard_pack); carve(k_shard_unpack);
   carve(k_margin_offer); carve(k_margin_rows);
   carve(k_gbc_smem<1>); carve(k_gbc_smem<2>); carve(k_gbc_smem<4>); carve(k_gbc_smem<8>);

@@ -271,13 +271,30 @@ long long big_chain_cells();
 
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
                        MatDev out, cudaEvent_t ev0, cudaEvent_t ev1);
+// Compacted nonzero coefficients of a conv step's input, per frame cell of
+// each (logical) row: cnt[row*ncell + cell] entries, channel idx and values
+// at ((row*ncell + cell)*C + k), ascending channel.
+struct SparseDev {
+  int* cnt;
+  unsigned short* idx;
+  double* lo;
+  double* hi;
+  int ncell, C;
+};
+void launch_compact_cells(cudaStream_t s, const RowsDev& rows, MatDev m, SparseDev sp);
+// Conv coefficients from the compacted input (band path; falls back to the
+// checked gather on `in` when the launch's operands are not proven in band).
+void launch_gbc_sparse(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                       const FrameDev& fout, SparseDev sp, MatDev in, MatDev out);
+bool gbc_sparse_wanted(const LayerDev& L);
 // queue: a device int the work-queue variant resets and consumes (per stream).
 void launch_gbc_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out, int* queue);
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, MatDev in, MatDev out);
-// Engine switches from the environment (read once): PC_GBC=0 selects the
-// one-output-per-thread conv kernel (default), PC_GBC=1 the register-blocked one.
+// Engine switches from the environment (read once): PC_GBC selects the conv
+// kernel: 3 (default) sparse gather where >= 32 channels, 2 shared-memory
+// tiled, 1 register-blocked gather, 0 one output per thread.
 int env_int(const char* name, int dflt);
 void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev in,
                       MatDev out, const double* relax);
