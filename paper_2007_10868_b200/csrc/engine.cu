@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <thread>
 #include <cmath>
@@ -942,13 +943,27 @@ void reset_stats(Ctx* n, size_t count) {
   n->stats_used = 0;
 }
 
+// Grow-only workspace. cudaFree / cudaMalloc synchronise the device and take
+// long for multi-GB buffers, so growth rounds up (1.25x, 64 MiB granules) and
+// is counted (PC_PROFILE reports it).
+thread_local double g_alloc_ms = 0;
+thread_local int g_allocs = 0;
 void ensure_arena(Ctx* n, size_t bytes) {
   if (bytes <= n->arena_cap) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  size_t want = std::max(bytes, n->arena_cap + n->arena_cap / 4);
+  want = (want + (64u << 20) - 1) & ~(size_t)((64u << 20) - 1);
   if (n->arena) cudaFree(n->arena);
   n->arena = nullptr;
   n->arena_cap = 0;
-  ck(cudaMalloc(&n->arena, bytes), "arena");
-  n->arena_cap = bytes;
+  if (cudaMalloc(&n->arena, want) != cudaSuccess) {  // headroom unavailable: exact size
+    cudaGetLastError();
+    want = bytes;
+    ck(cudaMalloc(&n->arena, want), "arena");
+  }
+  n->arena_cap = want;
+  g_alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  ++g_allocs;
 }
 
 long long budget_of(const Ctx* n) {
@@ -1438,6 +1453,8 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     n->ev_used = 0;
     n->sync_used = 0;
     g_gbc_window_madds = 0;
+    g_alloc_ms = 0;
+    g_allocs = 0;
     n->prof.clear();
     n->dense_ev.clear();
     run_test(n, label, m.data(), &st);
@@ -1704,7 +1721,8 @@ int pc_last_profile(char* buf, int len) {
          std::to_string(g_prof_ms[c]) + "], \"gap:" + kProfNames[c] + "\": [0, " +
          std::to_string(g_gap_ms[c]) + "]";
   }
-  j += ", \"gbc_window_madds\": [0, " + std::to_string(g_gbc_window_madds) + "]}";
+  j += ", \"gbc_window_madds\": [0, " + std::to_string(g_gbc_window_madds) + "]";
+  j += ", \"host_arena_alloc\": [" + std::to_string(g_allocs) + ", " + std::to_string(g_alloc_ms) + "]}";
   if (buf && len > 0) {
     std::strncpy(buf, j.c_str(), len - 1);
     buf[len - 1] = 0;

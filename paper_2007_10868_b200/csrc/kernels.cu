@@ -1037,6 +1037,9 @@ __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const doub
     }
 #pragma unroll
     for (int kk = 0; kk < kDK; ++kk) {
+      // a zero row coefficient adds the zero interval (skipped by the
+      // reference's iv_acc): block-uniform skip, shortens the chain
+      if (bits_zero(s_al[0][kk]) && bits_zero(s_ah[0][kk])) continue;
       const double sl = __dadd_rn(lo[0], pl[kk]), sh = __dadd_rn(hi[0], ph[kk]);
       const bool xl = __dadd_rd(lo[0], pl[kk]) == __dadd_ru(lo[0], pl[kk]);
       const bool xh = __dadd_rd(hi[0], ph[kk]) == __dadd_ru(hi[0], ph[kk]);
@@ -1052,6 +1055,7 @@ __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const doub
 #pragma unroll
     for (int u = 0; u < TM; ++u) {
       if (BAND) {
+        if (bits_zero(s_al[u][kk]) && bits_zero(s_ah[u][kk])) continue;  // block-uniform skip
         // one row per thread: the chain is latency bound, take the short form
         if (TM == 1) madd_band_lat(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u]);
         else madd_band(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u]);
