@@ -165,6 +165,11 @@ struct Ctx {
   size_t stats_cap = 0, stats_used = 0;
   // device-driven walks (graph mode): label, per-checkpoint live-row counts,
   // a second row-map buffer, and the captured whole-analysis graph
+  // compaction ring of the host-driven schedule (Walker::checkpoint)
+  static constexpr int kRing = 4;
+  int* ring_map[kRing] = {};
+  int* ring_q[kRing] = {};
+  int* d_ringR = nullptr;
   int* d_label = nullptr;
   int* d_slots = nullptr;
   static constexpr int kSlots = 8192;
@@ -234,6 +239,11 @@ struct Ctx {
     ck(cudaMemset(gen_l, 0, nl * sizeof(int)), "memset");
     ck(cudaMallocHost(&h_int, 64 + (size_t)n_out), "pinned");
     ck(cudaMallocHost(&h_newR, sizeof(int) * kCkSlots), "pinned");
+    for (int k = 0; k < kRing; ++k) {
+      ring_map[k] = dalloc<int>(2 * M);
+      ring_q[k] = dalloc<int>(M);
+    }
+    d_ringR = dalloc<int>(kRing);
     d_label = dalloc<int>(1);
     d_slots = dalloc<int>(kSlots);
     perm2 = dalloc<int>(2 * M);
@@ -546,8 +556,16 @@ struct Walker {
   int slot_next = 0, pq = 0;
   // lazy compaction state: checkpoints launched since the last compaction
   int ck_next = 0;             // next pinned slot
-  std::vector<int> ck_pending; // slots in launch order
-  int min_seen = 0;            // smallest completed surviving-row count seen
+  // Compaction ring: each checkpoint's offers write their row map, query list
+  // and surviving count into a ring slot; a completed checkpoint's compaction
+  // is applied to the current matrix while its rows are still in that
+  // checkpoint's order (generation).
+  struct Pending {
+    int ck, slot, gen;
+  };
+  std::vector<Pending> pend;
+  int gen = 0;
+  int cur_slot = -1;  // ring slot holding the current row list (-1: the chunk's own list)
 
   int nrows() const { return both ? 2 * R : R; }
   // rows frozen at an earlier checkpoint are skipped by the chain kernels
@@ -798,62 +816,99 @@ struct Walker {
       }
       return;
     }
+    if (!(allow_freeze && early_term)) {
+      prof_begin(n, PROF_OFFER, s2);
+      launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
+                   early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr);
+      prof_end(n, s2);
+      return;
+    }
+    int slot = free_slot();
+    if (slot < 0) {
+      resolve(m, 0);  // all slots referenced: settle the pending checkpoints
+      slot = free_slot();
+    }
     prof_begin(n, PROF_OFFER, s2);
-    launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
-                 early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr);
+    launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, 1, 1, n->ring_map[slot],
+                 n->d_ringR + slot, n->ring_q[slot], n->ctr);
     prof_end(n, s2);
-    if (!(allow_freeze && early_term)) return;
-    if ((int)ck_pending.size() == Ctx::kCkSlots) drain_pending();  // bounded lag
-    const int slot = ck_next;
+    const int ckx = ck_next;
     ck_next = (ck_next + 1) % Ctx::kCkSlots;
-    ck(cudaMemcpyAsync(n->h_newR + slot, n->d_int + 1, sizeof(int), cudaMemcpyDeviceToHost, s2), "d2h");
-    ck(cudaEventRecord(n->ck_ev[slot], s2), "event");
-    ck_pending.push_back(slot);
+    ck(cudaMemcpyAsync(n->h_newR + ckx, n->d_ringR + slot, sizeof(int), cudaMemcpyDeviceToHost, s2), "d2h");
+    ck(cudaEventRecord(n->ck_ev[ckx], s2), "event");
+    pend.push_back(Pending{ckx, slot, gen});
   }
 
-  // Fold the completed checkpoints into min_seen (in order; never blocks).
-  void poll_pending() {
-    size_t k = 0;
-    for (; k < ck_pending.size(); ++k) {
-      const cudaError_t e = cudaEventQuery(n->ck_ev[ck_pending[k]]);
-      if (e == cudaErrorNotReady) break;
-      ck(e, "event query");
-      min_seen = std::min(min_seen, n->h_newR[ck_pending[k]]);
+  int free_slot() const {
+    for (int k = 0; k < Ctx::kRing; ++k) {
+      if (k == cur_slot) continue;
+      bool used = false;
+      for (const Pending& p : pend) used |= p.slot == k;
+      if (!used) return k;
     }
-    ck_pending.erase(ck_pending.begin(), ck_pending.begin() + k);
+    return -1;
   }
-  void drain_pending() {
-    ck(cudaStreamSynchronize(s2), "sync");
-    poll_pending();
+
+  // Settle pending checkpoints until at most `keep` remain (blocking on their
+  // events); apply the compaction of a current-generation checkpoint that
+  // dropped rows. Later checkpoints of the old generation are then stale:
+  // their freezes stand (frozen[] / candidates), their row maps are dropped.
+  void resolve(Mat& m, int keep) {
+    while ((int)pend.size() > keep) {
+      const Pending p = pend.front();
+      pend.erase(pend.begin());
+      ck(cudaEventSynchronize(n->ck_ev[p.ck]), "sync");
+      apply(m, p);
+    }
   }
+  void apply(Mat& m, const Pending& p) {
+    if (p.gen != gen) return;
+    const int newR = n->h_newR[p.ck];
+    if (newR >= R) return;
+    m.src = n->ring_map[p.slot];
+    row_q = n->ring_q[p.slot];
+    R = newR;
+    cur_slot = p.slot;
+    ++gen;
+  }
+
 
   // compact_rows on both polarities (backsub.hpp:820-845) when enough rows
   // froze: the surviving rows stay in place and the next step reads them
   // through the latest offer's row map.
+  // compact_rows on both polarities (backsub.hpp:820-845): the surviving
+  // rows stay in place and the next step reads them through the row map.
+  // Schedules (results identical; only the wasted work on frozen rows and
+  // the waiting differ):
+  //   eager  - before each step, wait for the last checkpoint (the
+  //            reference's schedule);
+  //   lagged - for few rows (R <= PC_LAG_ROWS; off by default: measured on
+  //            ResNet-34, the extra conv step on rows that just froze costs
+  //            more than the overlap wins): keep the last checkpoint pending
+  //            and apply the one before, so a step's concretisation and
+  //            offers overlap the next step;
+  //   lazy   - (PC_LAZY_COMPACT=1) never block; apply the newest completed
+  //            checkpoint once it froze >= 1/8 of the rows.
   void maybe_compact(Mat& m) {
     if (dry || devr || !(allow_freeze && early_term)) return;
     static const int lazy = env_int("PC_LAZY_COMPACT", 0);
+    static const int lag_rows = env_int("PC_LAG_ROWS", 0);
     if (lazy) {
-      // keep computing frozen rows while the constants stream lags; compact
-      // only once completed checkpoints show >= 1/8 of the rows frozen
-      poll_pending();
-      const int drop = R - min_seen;
-      if (drop <= 0 || (min_seen > 0 && 8 * drop < R)) return;
-    } else {
-      // eager (the reference's schedule): wait for the last checkpoint's
-      // offers; the constants chain of each step still overlaps that step's
-      // coefficient substitution
-      if (ck_pending.empty()) return;
-      drain_pending();
-      if (min_seen >= R) return;
+      while (!pend.empty()) {
+        const cudaError_t e = cudaEventQuery(n->ck_ev[pend.front().ck]);
+        if (e == cudaErrorNotReady) break;
+        ck(e, "event query");
+        const Pending p = pend.front();
+        if (p.gen == gen && 8 * (R - n->h_newR[p.ck]) < R && n->h_newR[p.ck] > 0) {
+          pend.erase(pend.begin());  // not worth it yet; a later checkpoint supersedes it
+          continue;
+        }
+        pend.erase(pend.begin());
+        apply(m, p);
+      }
+      return;
     }
-    drain_pending();  // every launched offer done: perm / rowq hold the latest map
-    const int newR = min_seen;
-    m.src = n->perm;
-    R = newR;
-    rq ^= 1;
-    row_q = n->rowq[rq];
-    min_seen = R;
+    resolve(m, R <= lag_rows ? 1 : 0);
   }
 
   // walk_back (backsub.hpp:854-893)
@@ -1026,7 +1081,6 @@ void run_pass_graph(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   w.devr = true;
   w.dR = n->d_int;  // the seed's live count
   w.R = N;
-  w.min_seen = N;
   w.both = true;
   w.allow_freeze = allow_freeze;
   w.early_term = et;
@@ -1082,7 +1136,6 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
       Walker w{n, s, t};
       w.s2 = n->stream2;
       w.R = R;
-      w.min_seen = R;
       w.both = true;
       w.allow_freeze = allow_freeze;
       w.early_term = et;
@@ -1102,6 +1155,7 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
       if (affine) w.checkpoint(m);  // the init itself is an affine step (:1056)
       w.walk(m, 0, true);
       stream_wait(n, s, n->stream2);  // the next chunk reuses the arena and row lists
+      w.pend.clear();
     }
   }
   if (W > 1 && n_live > 0) allgather_rows(n, n->live, n_live, 4, n->cand);
@@ -1129,7 +1183,6 @@ void run_margin_graph(Ctx* n, pc_stats* st) {
   Walker w{n, s, out};
   w.s2 = n->stream2;
   w.R = nr;
-  w.min_seen = nr;
   w.both = false;
   w.margin = true;
   w.st = st;
@@ -1166,7 +1219,6 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
     Walker w{n, s, out};
     w.s2 = n->stream2;
     w.R = R;
-    w.min_seen = R;
     w.both = false;
     w.margin = true;
     w.st = st;
