@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <atomic>
 #include <thread>
@@ -170,6 +171,7 @@ struct Ctx {
   int* ring_map[kRing] = {};
   int* ring_q[kRing] = {};
   int* d_ringR = nullptr;
+  unsigned long long* d_ck = nullptr;  // the two pipelines' checkpoint tallies
   int* d_label = nullptr;
   int* d_slots = nullptr;
   static constexpr int kSlots = 8192;
@@ -181,6 +183,10 @@ struct Ctx {
   std::vector<size_t> graph_dense_ev;
   double graph_dense_bytes = 0, graph_dense_madds = 0;
   long long graph_launches = 0, graph_dense_launches = 0;
+  // second walk pipeline (run_pass): its own streams and walk resources, the
+  // analysis state aliased to this context's
+  Ctx* helper = nullptr;
+  bool is_helper = false;
   double *sh_send = nullptr, *sh_recv = nullptr;  // sharding exchange buffers
   size_t sh_cap = 0;                              // doubles per rank
   int* h_int = nullptr;  // pinned
@@ -244,6 +250,8 @@ struct Ctx {
       ring_q[k] = dalloc<int>(M);
     }
     d_ringR = dalloc<int>(kRing);
+    d_ck = dalloc<unsigned long long>(2);
+    ck(cudaMemset(d_ck, 0, 2 * sizeof(unsigned long long)), "memset");
     d_label = dalloc<int>(1);
     d_slots = dalloc<int>(kSlots);
     perm2 = dalloc<int>(2 * M);
@@ -251,6 +259,7 @@ struct Ctx {
   }
 
   ~Ctx() {
+    delete helper;
     if (stream) cudaStreamSynchronize(stream);
     if (stream2) cudaStreamSynchronize(stream2);
     for (void* p : owned) cudaFree(p);
@@ -318,7 +327,8 @@ const char* kProfNames[PROF_N] = {"forward", "seed", "init", "chain_affine", "de
 thread_local double g_prof_ms[PROF_N];
 thread_local long long g_prof_n[PROF_N];
 thread_local double g_gap_ms[PROF_N];
-thread_local double g_gbc_window_madds = 0;  // PC_PROFILE: madds of the conv steps if no coefficient were zero  // device idle (or unprofiled work) before each class
+thread_local double g_gbc_window_madds = 0;
+thread_local std::string g_pass_json = "[]";  // PC_PROFILE: [[target, live rows, ms], ...], -1 = margin  // PC_PROFILE: madds of the conv steps if no coefficient were zero  // device idle (or unprofiled work) before each class
 
 cudaEvent_t take_event(Ctx* n) {
   while (n->ev_pool.size() <= n->ev_used) {
@@ -566,6 +576,7 @@ struct Walker {
   std::vector<Pending> pend;
   int gen = 0;
   int cur_slot = -1;  // ring slot holding the current row list (-1: the chunk's own list)
+  unsigned long long* ck_count = nullptr;  // per-walker checkpoint tally (two pipelines)
 
   int nrows() const { return both ? 2 * R : R; }
   // rows frozen at an earlier checkpoint are skipped by the chain kernels
@@ -819,7 +830,7 @@ struct Walker {
     if (!(allow_freeze && early_term)) {
       prof_begin(n, PROF_OFFER, s2);
       launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
-                   early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr);
+                   early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr, ck_count);
       prof_end(n, s2);
       return;
     }
@@ -830,7 +841,7 @@ struct Walker {
     }
     prof_begin(n, PROF_OFFER, s2);
     launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, 1, 1, n->ring_map[slot],
-                 n->d_ringR + slot, n->ring_q[slot], n->ctr);
+                 n->d_ringR + slot, n->ring_q[slot], n->ctr, ck_count);
     prof_end(n, s2);
     const int ckx = ck_next;
     ck_next = (ck_next + 1) % Ctx::kCkSlots;
@@ -914,35 +925,46 @@ struct Walker {
   // walk_back (backsub.hpp:854-893)
   void walk(Mat& m, int stop, bool ckpt) {
     bool pending = false;
-    while (m.f.layer != stop) {
-      if (ckpt) maybe_compact(m);
-      if (!dry && R == 0) return;
-      const HostLayer& L = n->L[m.f.layer];
-      switch (L.kind) {
-        case KIND_DENSE:
-          dense_step(m);
-          if (ckpt) checkpoint(m);
-          pending = false;
-          break;
-        case KIND_CONV:
-          gbc_step(m);
-          if (ckpt) checkpoint(m);
-          pending = false;
-          break;
-        case KIND_RELU:
-          relu_step(m);
-          pending = true;
-          break;
-        case KIND_JOIN:
-          join_step(m);
-          if (ckpt) checkpoint(m);
-          pending = false;
-          break;
-        default:
-          throw StatusError(PC_ERR_LOGIC, "walk: frame fell through the input layer");
-      }
+    while (advance(m, stop, ckpt, pending)) {
     }
-    if (pending && ckpt) checkpoint(m);
+  }
+
+  // One iteration of walk_back: compaction, one step, its checkpoint; false
+  // once the walk is over (the final checkpoint after a relu included), so
+  // several walkers can be driven step by step in turn.
+  bool advance(Mat& m, int stop, bool ckpt, bool& pending) {
+    if (m.f.layer == stop) {
+      if (pending && ckpt) checkpoint(m);
+      pending = false;
+      return false;
+    }
+    if (ckpt) maybe_compact(m);
+    if (!dry && R == 0) return false;
+    const HostLayer& L = n->L[m.f.layer];
+    switch (L.kind) {
+      case KIND_DENSE:
+        dense_step(m);
+        if (ckpt) checkpoint(m);
+        pending = false;
+        break;
+      case KIND_CONV:
+        gbc_step(m);
+        if (ckpt) checkpoint(m);
+        pending = false;
+        break;
+      case KIND_RELU:
+        relu_step(m);
+        pending = true;
+        break;
+      case KIND_JOIN:
+        join_step(m);
+        if (ckpt) checkpoint(m);
+        pending = false;
+        break;
+      default:
+        throw StatusError(PC_ERR_LOGIC, "walk: frame fell through the input layer");
+    }
+    return true;
   }
 };
 
@@ -1061,6 +1083,63 @@ void allgather_rows(Ctx* n, const int* live, int n_rows, int width, double* dst)
 }
 
 // run_backsubstitution (backsub.hpp:993-1065)
+// The second walk pipeline of context n: a context of its own (streams,
+// arena, ring, concretisation buffers) whose analysis state (bounds,
+// relaxations, deviations, candidates, freeze flags, live list, counters) is
+// n's, so two halves of a pass's rows can be walked concurrently.
+Ctx* helper_of(Ctx* n) {
+  if (n->helper) return n->helper;
+  Ctx* h = new Ctx(n->net);
+  try {
+    h->init();
+  } catch (...) {
+    delete h;
+    throw;
+  }
+  h->is_helper = true;
+  h->blo = n->blo; h->bhi = n->bhi; h->rlo = n->rlo; h->rhi = n->rhi;
+  h->dev = n->dev; h->relax = n->relax; h->cand = n->cand; h->frozen = n->frozen;
+  h->live = n->live; h->ctr = n->ctr;
+  h->gen_n = n->gen_n; h->gen_pos = n->gen_pos; h->gen_l = n->gen_l;
+  h->budget = n->budget;
+  n->helper = h;
+  return h;
+}
+
+// One chunk walker: rows live[base .. base + R) of pass t on context c.
+struct ChunkWalk {
+  Walker w;
+  Mat m;
+  bool pending = false, running = true;
+};
+
+void start_chunk(Ctx* c, ChunkWalk& cw, int t, bool affine, long long base, int R,
+                 bool allow_freeze, bool et, pc_stats* st, const WalkSize& ws) {
+  const HostLayer& Q = c->L[t];
+  const long long o = c->off[t];
+  cudaStream_t s = c->stream;
+  c->arena_used = 0;
+  reset_stats(c, ws.stats);
+  Walker& w = cw.w;
+  w.s2 = c->stream2;
+  w.R = R;
+  w.both = true;
+  w.allow_freeze = allow_freeze;
+  w.early_term = et;
+  w.st = st;
+  ck(cudaMemcpyAsync(c->rowq[0], c->live + base, sizeof(int) * R, cudaMemcpyDeviceToDevice, s), "d2d");
+  w.rq = 0;
+  w.row_q = c->rowq[0];
+  Frame f0 = initial_frame(c, t, affine);
+  cw.m = w.alloc(f0, true);
+  if (affine)
+    launch_init_affine(s, Q.d, w.rows(), fdev(c, f0, t), c->dev + o, md(cw.m));
+  else
+    launch_init_identity(s, w.rows(), fdev(c, f0, t), md(cw.m));
+  w.mark(cw.m);
+  if (affine) w.checkpoint(cw.m);  // the init itself is an affine step (:1056)
+}
+
 // Device-driven pass (graph mode): one chunk sized for every neuron of the
 // layer; the live count and rows come from the seed on the device.
 void run_pass_graph(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
@@ -1128,34 +1207,42 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
                           ? n->opt.chunk_rows
                           : std::max<long long>(1, budget_of(n) / (long long)ws.per_row);
     chunk = std::min<long long>(chunk, le - lb);
-    ensure_arena(n, ws.per_row * (size_t)chunk + 256 * ws.allocs + (1 << 20));
+    // Two walk pipelines: the rows of a chunk are split between this context
+    // and its helper and the two walks are advanced step by step in turn, so
+    // one half's conv substitutions overlap the other half's serial constant
+    // / concretisation chains and checkpoint round trips (rows are
+    // independent, backsub.hpp:31-34; results identical).
+    static const int pipes = env_int("PC_PIPES", 2);
+    const bool two = pipes >= 2 && !n->is_helper && chunk >= 16;
+    Ctx* h = two ? helper_of(n) : nullptr;
+    const long long half = two ? (chunk + 1) / 2 : chunk;
+    ensure_arena(n, ws.per_row * (size_t)half + 256 * ws.allocs + (1 << 20));
+    if (h) ensure_arena(h, ws.per_row * (size_t)half + 256 * ws.allocs + (1 << 20));
     for (long long base = lb; base < le; base += chunk) {
       const int R = (int)std::min<long long>(chunk, le - base);
-      n->arena_used = 0;
-      reset_stats(n, ws.stats);
-      Walker w{n, s, t};
-      w.s2 = n->stream2;
-      w.R = R;
-      w.both = true;
-      w.allow_freeze = allow_freeze;
-      w.early_term = et;
-      w.st = st;
-      // rows of this chunk: live[base .. base+R)
-      ck(cudaMemcpyAsync(n->rowq[0], n->live + base, sizeof(int) * R, cudaMemcpyDeviceToDevice, s),
-         "d2d");
-      w.rq = 0;
-      w.row_q = n->rowq[0];
-      Frame f0 = initial_frame(n, t, affine);
-      Mat m = w.alloc(f0, true);
-      if (affine)
-        launch_init_affine(s, Q.d, w.rows(), fdev(n, f0, t), n->dev + o, md(m));
-      else
-        launch_init_identity(s, w.rows(), fdev(n, f0, t), md(m));
-      w.mark(m);
-      if (affine) w.checkpoint(m);  // the init itself is an affine step (:1056)
-      w.walk(m, 0, true);
+      if (h && R >= 16) {
+        const int RA = R / 2, RB = R - RA;
+        stream_wait(n, h->stream, s);  // the seed and live list are on s
+        ChunkWalk a{Walker{n, s, t}}, b{Walker{h, h->stream, t}};
+        a.w.ck_count = n->d_ck;
+        b.w.ck_count = n->d_ck + 1;
+        start_chunk(n, a, t, affine, base, RA, allow_freeze, et, st, ws);
+        start_chunk(h, b, t, affine, base + RA, RB, allow_freeze, et, st, ws);
+        while (a.running || b.running) {
+          if (a.running) a.running = a.w.advance(a.m, 0, true, a.pending);
+          if (b.running) b.running = b.w.advance(b.m, 0, true, b.pending);
+        }
+        stream_wait(n, s, n->stream2);
+        stream_wait(n, s, h->stream);
+        stream_wait(n, s, h->stream2);
+        launch_ck_merge(s, n->d_ck, n->d_ck + 1, n->ctr);
+        stream_wait(n, h->stream, s);  // h's next chunk reuses its arena after s
+        continue;
+      }
+      ChunkWalk a{Walker{n, s, t}};
+      start_chunk(n, a, t, affine, base, R, allow_freeze, et, st, ws);
+      a.w.walk(a.m, 0, true);
       stream_wait(n, s, n->stream2);  // the next chunk reuses the arena and row lists
-      w.pend.clear();
     }
   }
   if (W > 1 && n_live > 0) allgather_rows(n, n->live, n_live, 4, n->cand);
@@ -1421,13 +1508,33 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
     }
   };
   forward(0, targets[0]);
+  // PC_PROFILE: wall time and live rows per pass (host clock; the pass ends
+  // with the write-back, which the next pass's seed synchronises on)
+  std::vector<std::array<double, 3>> pass_t;
+  auto tp = std::chrono::steady_clock::now();
   for (size_t i = 0; i < targets.size(); ++i) {
     const int t = targets[i];
     const bool is_out = t == out;
     run_pass(n, t, !is_out, st);
     if (!is_out) forward(t, targets[i + 1]);
+    if (n->profile) {
+      ck(cudaStreamSynchronize(s), "sync");
+      const auto t1 = std::chrono::steady_clock::now();
+      pass_t.push_back({(double)t, (double)n->h_int[0],
+                        std::chrono::duration<double, std::milli>(t1 - tp).count()});
+      tp = t1;
+    }
   }
   if (label >= 0) run_margin(n, label, st, margins);
+  if (n->profile) {
+    const auto t1 = std::chrono::steady_clock::now();
+    pass_t.push_back({-1.0, (double)(n->n_out - 1), std::chrono::duration<double, std::milli>(t1 - tp).count()});
+    g_pass_json = "[";
+    for (size_t k = 0; k < pass_t.size(); ++k)
+      g_pass_json += (k ? ", [" : "[") + std::to_string((int)pass_t[k][0]) + ", " +
+                     std::to_string((int)pass_t[k][1]) + ", " + std::to_string(pass_t[k][2]) + "]";
+    g_pass_json += "]";
+  }
   Counters c{};
   ck(cudaMemcpyAsync(&c, n->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s), "d2h");
   ck(cudaStreamSynchronize(s), "sync");
@@ -1504,6 +1611,12 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     std::vector<double> m(std::max(1, n->n_out - 1), 0.0);
     n->ev_used = 0;
     n->sync_used = 0;
+    if (n->helper) {
+      n->helper->ev_used = 0;
+      n->helper->sync_used = 0;
+      n->helper->prof.clear();
+      n->helper->dense_ev.clear();
+    }
     g_gbc_window_madds = 0;
     g_alloc_ms = 0;
     g_allocs = 0;
@@ -1774,7 +1887,8 @@ int pc_last_profile(char* buf, int len) {
          std::to_string(g_gap_ms[c]) + "]";
   }
   j += ", \"gbc_window_madds\": [0, " + std::to_string(g_gbc_window_madds) + "]";
-  j += ", \"host_arena_alloc\": [" + std::to_string(g_allocs) + ", " + std::to_string(g_alloc_ms) + "]}";
+  j += ", \"host_arena_alloc\": [" + std::to_string(g_allocs) + ", " + std::to_string(g_alloc_ms) + "]";
+  j += ", \"passes\": " + g_pass_json + "}";
   if (buf && len > 0) {
     std::strncpy(buf, j.c_str(), len - 1);
     buf[len - 1] = 0;

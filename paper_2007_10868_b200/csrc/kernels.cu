@@ -1797,7 +1797,7 @@ void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const
 __global__ void __launch_bounds__(kScanThreads)
     k_offer(RowsDev rows, int R, const double* vals, const double* rvals, double* cand,
             char* frozen, int allow_freeze, int early_term, int* map, int* new_R,
-            int* new_row_q, Counters* ctr) {
+            int* new_row_q, Counters* ctr, unsigned long long* ck_count) {
   using Scan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
@@ -1841,7 +1841,8 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
   }
   if (froze) atomicAdd(&ctr->frozen, (unsigned long long)froze);
-  if (threadIdx.x == 0 && (s_live || !early_term)) atomicAdd(&ctr->checkpoints, 1ull);
+  if (threadIdx.x == 0 && (s_live || !early_term))
+    atomicAdd(ck_count ? ck_count : &ctr->checkpoints, 1ull);
   const int nR = s_base;
   for (int p = threadIdx.x; p < nR; p += blockDim.x) map[nR + p] = R + map[p];  // lower rows
   if (threadIdx.x == 0) *new_R = nR;
@@ -1849,9 +1850,9 @@ __global__ void __launch_bounds__(kScanThreads)
 
 void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals,
                   const double* rvals, double* cand, char* frozen, int allow_freeze,
-                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr) {
+                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr, unsigned long long* ck_count) {
   k_offer<<<1, kScanThreads, 0, s>>>(rows, R, vals, rvals, cand, frozen, allow_freeze, early_term,
-                                     map, new_R, new_row_q, ctr);
+                                     map, new_R, new_row_q, ctr, ck_count);
   ++g_launches;
 }
 
@@ -1890,6 +1891,19 @@ void launch_shard_unpack(cudaStream_t s, const int* live, int n_live, int world,
                          int width, const double* recv, double* dst) {
   k_shard_unpack<<<cdiv((long long)world * per * width, 256), 256, 0, s>>>(live, n_live, world, per,
                                                                           width, recv, dst);
+  ++g_launches;
+}
+
+// Two walk pipelines split a chunk: the reference walks the whole chunk while
+// any row is live, i.e. as many checkpoints as the longer half.
+__global__ void k_ck_merge(unsigned long long* a, unsigned long long* b, Counters* ctr) {
+  ctr->checkpoints += *a > *b ? *a : *b;
+  *a = 0;
+  *b = 0;
+}
+
+void launch_ck_merge(cudaStream_t s, unsigned long long* a, unsigned long long* b, Counters* ctr) {
+  k_ck_merge<<<1, 1, 0, s>>>(a, b, ctr);
   ++g_launches;
 }
 

@@ -306,7 +306,9 @@ void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const
 // lower physical rows) and the compacted query list.
 void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals,
                   const double* rvals, double* cand, char* frozen, int allow_freeze,
-                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr);
+                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr,
+                  unsigned long long* ck_count = nullptr);  // checkpoint tally (default ctr)
+void launch_ck_merge(cudaStream_t s, unsigned long long* a, unsigned long long* b, Counters* ctr);
 void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best, char* has);
 
 // Row sharding: pack this rank's slice of candidates (4 doubles per row, in

@@ -203,8 +203,9 @@ class Verifier:
     def last_profile() -> dict:
         """Per-kernel-class {class: [launches, ms]} of the last call (PC_PROFILE=1)."""
         import json
-        buf = ctypes.create_string_buffer(4096)
-        _lib.lib.pc_last_profile(buf, 4096)
+        n = _lib.lib.pc_last_profile(None, 0) + 1
+        buf = ctypes.create_string_buffer(n)
+        _lib.lib.pc_last_profile(buf, n)
         return json.loads(buf.value.decode())
 
     def last_timing(self):

@@ -29,10 +29,13 @@ for i, x in enumerate(X):
     t = v.last_timing()
     prof = v.last_profile()
     win = prof.pop("gbc_window_madds", [0, 0])[1]
+    passes = prof.pop("passes", [])
+    prof.pop("host_arena_alloc", None)
     tot = sum(ms for k, (_, ms) in prof.items() if not k.startswith("gap:"))
     print(json.dumps({"config": name, "image": i, "verified": verdict.verified, "wall_ms": round(wall, 2),
                       "device_ms": round(t["total_ms"], 2), "launches": t["launches"],
                       "stats": verdict.stats,
                       "gbc_nonzero_fraction": (verdict.stats["gbc_madds"] / win) if win else None,
+                      "passes": passes,
                       "classes": {k: [c, round(ms, 3), round(100 * ms / max(tot, 1e-9), 1)]
                                   for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]) if c or ms > 0.05}}))
