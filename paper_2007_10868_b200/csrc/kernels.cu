@@ -1623,8 +1623,110 @@ __global__ void __launch_bounds__(256)
   mag.flush(out.stat);
 }
 
+// Two adjacent input channels per thread (even cin, band path only): the
+// compacted coefficient (index + interval) is loaded once for two madds and the
+// weights as one 16-byte pair.
+__global__ void __launch_bounds__(256)
+    k_gbc_sparse2(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
+                  MatDev out) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  const int q = row_query(rows, i, upper);
+  int bw, bh, nbw, nbh;
+  frame_base(fi, q, bw, bh);
+  frame_base(fo, q, nbw, nbh);
+  const long long ocells = out.cells, opairs = ocells / 2;
+  const double* ilo = in.lo + phys_row(in, i) * in.cells;
+  const double* ihi = in.hi + phys_row(in, i) * in.cells;
+  const int cin = L.in_c, cout = L.out_c, cin2 = cin / 2;
+  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  const int* cnt = sp.cnt + (size_t)i * sp.ncell;
+  const size_t rbase = (size_t)i * sp.ncell * sp.C;
+  MagAcc mag;
+  for (long long o2 = blockIdx.x * blockDim.x + threadIdx.x; o2 < opairs;
+       o2 += (long long)gridDim.x * blockDim.x) {
+    const int cp = (int)(o2 % cin2);
+    const int x = (int)((o2 / cin2) % fo.S_w);
+    const int y = (int)(o2 / ((long long)cin2 * fo.S_w));
+    const int iy = nbh + y, ix = nbw + x, ci = 2 * cp;
+    Iv acc0, acc1;
+    if (!band) {
+      bool bad = false;
+      acc0 = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+      if (bad) acc0 = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+      bad = false;
+      acc1 = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ci + 1, bad);
+      if (bad) acc1 = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ci + 1, bad);
+    } else {
+      int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
+      int aw0 = floordiv(ix + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ix + L.pw, L.sw);
+      ah0 = max(ah0, bh);
+      ah1 = min(ah1, bh + fi.S_h - 1);
+      aw0 = max(aw0, bw);
+      aw1 = min(aw1, bw + fi.S_w - 1);
+      double lo0 = 0.0, hi0 = 0.0, lo1 = 0.0, hi1 = 0.0;
+      for (int ah = ah0; ah <= ah1; ++ah) {
+        const int fy = iy + L.ph - ah * L.sh;
+        for (int aw = aw0; aw <= aw1; ++aw) {
+          const int fx = ix + L.pw - aw * L.sw;
+          const int cell = (ah - bh) * fi.S_w + (aw - bw);
+          const int n = cnt[cell];
+          const size_t sb = rbase + (size_t)cell * sp.C;
+          const double2* wp =
+              reinterpret_cast<const double2*>(L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin) + cp;
+          constexpr int kB = 4;
+          int e = 0;
+          for (; e + kB <= n; e += kB) {
+            double cl[kB], ch[kB];
+            double2 w[kB];
+#pragma unroll
+            for (int k = 0; k < kB; ++k) {
+              const int d = sp.idx[sb + e + k];
+              cl[k] = sp.lo[sb + e + k];
+              ch[k] = sp.hi[sb + e + k];
+              w[k] = wp[(size_t)d * cin2];
+            }
+#pragma unroll
+            for (int k = 0; k < kB; ++k) {
+              madd_band(w[k].x, cl[k], ch[k], lo0, hi0);
+              madd_band(w[k].y, cl[k], ch[k], lo1, hi1);
+            }
+          }
+          for (; e < n; ++e) {
+            const double2 w = wp[(size_t)sp.idx[sb + e] * cin2];
+            madd_band(w.x, sp.lo[sb + e], sp.hi[sb + e], lo0, hi0);
+            madd_band(w.y, sp.lo[sb + e], sp.hi[sb + e], lo1, hi1);
+          }
+        }
+      }
+      acc0 = Iv{canon0(lo0), hi0};
+      acc1 = Iv{canon0(lo1), hi1};
+    }
+    const size_t ob = (size_t)i * ocells + 2 * o2;
+    out.lo[ob] = acc0.lo;
+    out.hi[ob] = acc0.hi;
+    out.lo[ob + 1] = acc1.lo;
+    out.hi[ob + 1] = acc1.hi;
+    mag.add(acc0.lo);
+    mag.add(acc0.hi);
+    mag.add(acc1.lo);
+    mag.add(acc1.hi);
+  }
+  mag.flush(out.stat);
+}
+
 void launch_gbc_sparse(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                        const FrameDev& fout, SparseDev sp, MatDev in, MatDev out) {
+  static const int pairs = env_int("PC_GBC_PAIRS", 1);
+  if (pairs && L.in_c % 2 == 0) {
+    unsigned gx = cdiv(out.cells / 2, 256);
+    if (gx > 1024) gx = 1024;
+    dim3 grid(gx, rows.n);
+    k_gbc_sparse2<<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out);
+    ++g_launches;
+    return;
+  }
   unsigned gx = cdiv(out.cells, 256);
   if (gx > 1024) gx = 1024;
   dim3 grid(gx, rows.n);
@@ -1934,7 +2036,7 @@ void init_kernel_attrs_kernels() {
   carve(k_fwd_dense); carve(k_fwd_conv); carve(k_fwd_relu); carve(k_fwd_join); carve(k_relax);
   carve(k_seed); carve(k_writeback); carve(k_init_affine); carve(k_init_identity);
   carve(k_init_margin); carve(k_chain_affine); carve(k_chain_relu); carve(k_concretize);
-  carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef); carve(k_gbc_sparse); carve(k_compact_cells);
+  carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef); carve(k_gbc_sparse); carve(k_gbc_sparse2); carve(k_compact_cells);
   carve(k_relu_coef); carve(k_merge); carve(k_offer); carve(k_shard_pack); carve(k_shard_unpack);
   carve(k_margin_offer); carve(k_margin_rows);
   carve(k_gbc_smem<1>); carve(k_gbc_smem<2>); carve(k_gbc_smem<4>); carve(k_gbc_smem<8>);
