@@ -51,8 +51,8 @@ def parse():
     ap.add_argument("--no-early-term", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch", type=int, default=32, help="images per step")
-    ap.add_argument("--concurrency", type=int, default=16, help="concurrent streams per GPU")
+    ap.add_argument("--batch", type=int, default=128, help="images per step")
+    ap.add_argument("--concurrency", type=int, default=4, help="worker contexts per GPU (each verifies batch/concurrency images per schedule)")
     return ap.parse_args()
 
 
@@ -321,8 +321,9 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "arch": arch, "eps": eps_s, "model_seed": mseed,
                    "input_seed": iseed, "early_term": et,
-                   "parallelism": f"replicas x{world} (image sharding); {per_step} images per step, "
-                                  f"{args.concurrency} concurrent streams per GPU",
+                   "parallelism": f"replicas x{world} (image sharding); {per_step} images per step over "
+                                  f"{args.concurrency} worker contexts per GPU, each verifying "
+                                  f"{-(-per_step // args.concurrency)} images per schedule (image-batched walks)",
                    "l2": "flushed between steps (256 MB write, outside the timed events)",
                    "verified": f"{dev_verified}/{imgs}"},
         "e2e": {"value": e2e_val, "unit": "ms/image", "h2d_bytes_per_step": per_step * 2 * 8 * n_in,

@@ -266,8 +266,11 @@ __global__ void __launch_bounds__(kCT)
   int i;
   if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
-  const int q = row_query(rows, i, upper);
-  if (frozen && frozen[q]) return;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  dev += img * rows.sst;
+  ctr += img;
   if (is_conv && threadIdx.x == 0)
     atomicAdd(&ctr->gbc_dense_equiv, (unsigned long long)L.out_w * L.out_h * L.out_c *
                                          ((unsigned long long)L.in_w * L.in_h * L.in_c));
@@ -297,9 +300,10 @@ __global__ void __launch_bounds__(kCT)
   int i;
   if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
-  const int q = row_query(rows, i, upper);
-  if (frozen && frozen[q]) return;
-  ReluGen g{f, 0, 0, upper, relax};
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  ReluGen g{f, 0, 0, upper, relax + 8 * img * rows.sst};
   frame_base(f, q, g.bw, g.bh);
   const size_t pr = phys_row(m, i);
   const double acc0 = (threadIdx.x < 4) ? m.K[4 * pr + threadIdx.x] : 0.0;
@@ -316,8 +320,14 @@ __global__ void __launch_bounds__(kCT)
   int i;
   if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
-  const int q = row_query(rows, i, upper);
-  if (frozen && frozen[q]) return;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  const long long so = img * rows.sst;
+  blo += so;
+  bhi += so;
+  rlo += so;
+  rhi += so;
   const size_t pr = phys_row(m, i);
   const double* K = m.K + 4 * pr;
   const double a0 = upper ? K[1] : K[0], a1 = upper ? K[3] : K[2];

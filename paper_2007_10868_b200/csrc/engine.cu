@@ -116,6 +116,7 @@ struct pc_net {
   std::mutex pool_mu;
   std::vector<Ctx*> pool;    // idle per-call contexts
   std::vector<Ctx*> all;
+  std::vector<Ctx*> bpool;  // idle image-batched contexts
   Ctx* primary = nullptr;
   // row sharding (pc_net_set_sharding)
   int shard_rank = 0, shard_world = 1;
@@ -187,6 +188,8 @@ struct Ctx {
   // analysis state aliased to this context's
   Ctx* helper = nullptr;
   bool is_helper = false;
+  int nimg = 1;  // images whose state this context holds (image-batched walks)
+  int* keys = nullptr;  // image-batched walks: the pass's live row keys
   double *sh_send = nullptr, *sh_recv = nullptr;  // sharding exchange buffers
   size_t sh_cap = 0;                              // doubles per rank
   int* h_int = nullptr;  // pinned
@@ -213,11 +216,14 @@ struct Ctx {
     return static_cast<T*>(p);
   }
 
-  void init() {
+  // nimg > 1: an image-batched context (state for nimg images, row buffers
+  // for nimg images' rows; see run_test_batched).
+  void init(int n_images = 1) {
+    nimg = n_images;
     ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking), "stream");
     const int nl = (int)L.size();
-    const size_t T = (size_t)total, M = (size_t)max_numel;
+    const size_t T = (size_t)total * nimg, M = (size_t)max_numel * nimg;
     blo = dalloc<double>(T);
     bhi = dalloc<double>(T);
     rlo = dalloc<double>(T);
@@ -230,20 +236,21 @@ struct Ctx {
     live = dalloc<int>(M);
     rowq[0] = dalloc<int>(M);
     rowq[1] = dalloc<int>(M);
+    keys = dalloc<int>(M);
     perm = dalloc<int>(2 * M);
-    d_int = dalloc<int>(8);
+    d_int = dalloc<int>(8 + nimg);
     vals = dalloc<double>(2 * M);
     rvals = dalloc<double>(2 * M);
     best = dalloc<double>(M);
     has = dalloc<char>(M);
-    ctr = dalloc<Counters>(1);
+    ctr = dalloc<Counters>(nimg);
     gen_n = dalloc<int>(T);
-    gen_pos = dalloc<int>((size_t)pofs[nl]);
-    gen_l = dalloc<int>(nl);
+    gen_pos = dalloc<int>((size_t)pofs[nl] * nimg);
+    gen_l = dalloc<int>((size_t)nl * nimg);
     ck(cudaMemset(gen_n, 0, T * sizeof(int)), "memset");
-    ck(cudaMemset(gen_pos, 0, (size_t)pofs[nl] * sizeof(int)), "memset");
-    ck(cudaMemset(gen_l, 0, nl * sizeof(int)), "memset");
-    ck(cudaMallocHost(&h_int, 64 + (size_t)n_out), "pinned");
+    ck(cudaMemset(gen_pos, 0, (size_t)pofs[nl] * nimg * sizeof(int)), "memset");
+    ck(cudaMemset(gen_l, 0, (size_t)nl * nimg * sizeof(int)), "memset");
+    ck(cudaMallocHost(&h_int, 64 + (size_t)n_out * nimg + 64 * (size_t)nimg), "pinned");
     ck(cudaMallocHost(&h_newR, sizeof(int) * kCkSlots), "pinned");
     for (int k = 0; k < kRing; ++k) {
       ring_map[k] = dalloc<int>(2 * M);
@@ -252,7 +259,7 @@ struct Ctx {
     d_ringR = dalloc<int>(kRing);
     d_ck = dalloc<unsigned long long>(2);
     ck(cudaMemset(d_ck, 0, 2 * sizeof(unsigned long long)), "memset");
-    d_label = dalloc<int>(1);
+    d_label = dalloc<int>(nimg);
     d_slots = dalloc<int>(kSlots);
     perm2 = dalloc<int>(2 * M);
     for (int k = 0; k < kCkSlots; ++k) ck(cudaEventCreateWithFlags(&ck_ev[k], cudaEventDisableTiming), "event");
@@ -304,7 +311,30 @@ Ctx* acquire(pc_net* n) {
 
 void release(pc_net* n, Ctx* c) {
   std::lock_guard<std::mutex> lk(n->pool_mu);
-  n->pool.push_back(c);
+  (c->nimg > 1 ? n->bpool : n->pool).push_back(c);
+}
+
+// An image-batched context holding state for at least B images.
+Ctx* acquire_batched(pc_net* n, int B) {
+  {
+    std::lock_guard<std::mutex> lk(n->pool_mu);
+    for (size_t k = 0; k < n->bpool.size(); ++k)
+      if (n->bpool[k]->nimg >= B) {
+        Ctx* c = n->bpool[k];
+        n->bpool.erase(n->bpool.begin() + k);
+        return c;
+      }
+  }
+  Ctx* c = new Ctx(n);
+  try {
+    c->init(B);
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  std::lock_guard<std::mutex> lk(n->pool_mu);
+  n->all.push_back(c);
+  return c;
 }
 
 struct CtxLease {
@@ -581,9 +611,16 @@ struct Walker {
   int nrows() const { return both ? 2 * R : R; }
   // rows frozen at an earlier checkpoint are skipped by the chain kernels
   const char* fz() const { return (allow_freeze && early_term && !margin) ? n->frozen : nullptr; }
+  // image-batched walks (run_test_batched): row keys img * kq + neuron
+  int kq = 0, nimg = 1;
+  long long sst = 0;
+
   RowsDev rows() const {
     RowsDev r{row_q, nrows(), both ? R : 0};
     r.dR = devr ? dR : nullptr;
+    r.kq = kq;
+    r.sst = sst;
+    r.nimg = nimg;
     return r;
   }
 
@@ -1568,6 +1605,144 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
   st->rows_terminated_early += (long long)(c.frozen + c.pad);
 }
 
+// ---------------------------------------------------------------------------
+// Image-batched verification (pc_net_test_batch): B images in one schedule.
+// Every pass seeds each image, concatenates the live rows of all images into
+// one key list (img * M + neuron) and walks them as one set of rows, so each
+// kernel launch carries B images' rows; the per-neuron state of image b sits
+// at offset b * total. Results per image are the single-image engine's.
+void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stats* stats) {
+  cudaStream_t s = n->stream;
+  const int nl = (int)n->L.size();
+  const int out = nl - 1;
+  const long long T = n->total, M = n->max_numel, P = n->pofs[nl];
+  const bool et = n->opt.early_term != 0;
+  ck(cudaMemsetAsync(n->ctr, 0, sizeof(Counters) * B, s), "memset");
+  const std::vector<int> targets = pass_targets(n);
+  auto forward = [&](int k0, int k1) {  // all B images per launch (blockIdx.z)
+    for (int k = k0 + 1; k <= k1; ++k) {
+      const HostLayer& l = n->L[k];
+      launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
+                           n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
+                           n->gen_pos, n->gen_l, n->gen, 1, B, T, P, nl);
+    }
+  };
+  long long rows_total = 0;
+  forward(0, targets[0]);
+  for (size_t ti = 0; ti < targets.size(); ++ti) {
+    const int t = targets[ti];
+    const bool allow_freeze = t != out;
+    const HostLayer& Q = n->L[t];
+    const int N = (int)Q.numel();
+    const long long o = n->off[t];
+    launch_seed(s, N, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o, allow_freeze ? 1 : 0,
+                et ? 1 : 0, n->cand, n->frozen, n->live, n->d_int + 8, &n->ctr[0].pad, B, T, M,
+                (int)(sizeof(Counters) / sizeof(unsigned long long)));
+    launch_gather_keys(s, n->live, n->d_int + 8, B, (int)M, n->keys, n->d_int);
+    ck(cudaMemcpyAsync(n->h_int, n->d_int, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+    const int n_live = n->h_int[0];
+    rows_total += N;
+    const bool affine = Q.kind == KIND_DENSE || Q.kind == KIND_CONV;
+    if (n_live > 0) {
+      const int* keys = n->keys;
+      const WalkSize ws = walk_size(n, t, affine, true);
+      long long chunk = n->opt.chunk_rows > 0
+                            ? n->opt.chunk_rows
+                            : std::max<long long>(1, budget_of(n) / (long long)ws.per_row);
+      chunk = std::min<long long>(chunk, n_live);
+      ensure_arena(n, ws.per_row * (size_t)chunk + 256 * ws.allocs + (1 << 20));
+      for (long long base = 0; base < n_live; base += chunk) {
+        const int R = (int)std::min<long long>(chunk, n_live - base);
+        n->arena_used = 0;
+        reset_stats(n, ws.stats);
+        Walker w{n, s, t};
+        w.s2 = n->stream2;
+        w.R = R;
+        w.both = true;
+        w.allow_freeze = allow_freeze;
+        w.early_term = et;
+        pc_stats dummy{};
+        w.st = &dummy;
+        w.kq = (int)M;
+        w.sst = T;
+        w.nimg = B;
+        ck(cudaMemcpyAsync(n->rowq[0], keys + base, sizeof(int) * R, cudaMemcpyDeviceToDevice, s), "d2d");
+        w.rq = 0;
+        w.row_q = n->rowq[0];
+        Frame f0 = initial_frame(n, t, affine);
+        Mat m = w.alloc(f0, true);
+        if (affine)
+          launch_init_affine(s, Q.d, w.rows(), fdev(n, f0, t), n->dev + o, md(m));
+        else
+          launch_init_identity(s, w.rows(), fdev(n, f0, t), md(m));
+        w.mark(m);
+        if (affine) w.checkpoint(m);
+        w.walk(m, 0, true);
+        stream_wait(n, s, n->stream2);
+      }
+    }
+    ++n->gen;
+    launch_writeback(s, N, Q.out_c, t, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
+                     Q.feeds_relu ? n->relax + 8 * o : nullptr, n->gen_n, n->gen_pos, n->gen_l,
+                     n->gen, o, n->pofs[t], B, T, P, nl, M);
+    if (t != out) forward(t, targets[ti + 1]);
+  }
+  // margin pass: rows img * M + class j (j != label), image-major
+  const int nr = n->n_out - 1;
+  long long margin_ck = 0;
+  if (nr > 0) {
+    std::vector<int> keys;
+    for (int b = 0; b < B; ++b)
+      for (int j = 0; j < n->n_out; ++j)
+        if (j != labels[b]) keys.push_back((int)(b * M + j));
+    const int R = (int)keys.size();
+    ck(cudaMemcpyAsync(n->rowq[0], keys.data(), sizeof(int) * R, cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemcpyAsync(n->d_label, labels, sizeof(int) * B, cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemsetAsync(n->has, 0, R, s), "memset");
+    const WalkSize ws = walk_size(n, out, false, false);
+    ensure_arena(n, ws.per_row * (size_t)R + 256 * ws.allocs + (1 << 20));
+    n->arena_used = 0;
+    reset_stats(n, ws.stats);
+    Walker w{n, s, out};
+    w.s2 = n->stream2;
+    w.R = R;
+    w.both = false;
+    w.margin = true;
+    pc_stats mst{};
+    w.st = &mst;
+    w.kq = (int)M;
+    w.sst = T;
+    w.nimg = B;
+    w.row_q = n->rowq[0];
+    Mat m = w.alloc(dense_frame(out), true);
+    launch_init_margin_keys(s, w.rows(), n->d_label, n->n_out, md(m));
+    w.mark(m);
+    w.walk(m, 0, true);
+    stream_wait(n, s, n->stream2);
+    ck(cudaMemcpyAsync(margins, n->best, sizeof(double) * R, cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaMemcpyAsync(n->h_int + 16, n->has, R, cudaMemcpyDeviceToHost, s), "d2h");
+    margin_ck = mst.checkpoints;
+    rows_total += nr;
+  }
+  std::vector<Counters> c(B);
+  ck(cudaMemcpyAsync(c.data(), n->ctr, sizeof(Counters) * B, cudaMemcpyDeviceToHost, s), "d2h");
+  ck(cudaStreamSynchronize(s), "sync");
+  const char* has = reinterpret_cast<const char*>(n->h_int + 16);
+  for (int r = 0; r < B * nr; ++r)
+    if (!has[r]) throw StatusError(PC_ERR_LOGIC, "margin pass produced no candidate");
+  for (int b = 0; b < B; ++b) {
+    pc_stats& st = stats[b];
+    st = pc_stats{};
+    st.rows_total = rows_total;
+    st.checkpoints = (long long)c[b].checkpoints + margin_ck;
+    st.gbc_dense_equiv = (long long)c[b].gbc_dense_equiv;
+    st.dense_madds = (long long)c[b].dense_madds;
+    st.gbc_madds = (long long)c[b].gbc_madds;
+    st.rows_terminated_early = (long long)(c[b].frozen + c[b].pad);
+  }
+}
+
 pc_status guard(const std::function<void()>& fn) {
   try {
     fn();
@@ -1938,9 +2113,20 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
     ck(cudaStreamCreateWithFlags(&master, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&start), "event");
     ck(cudaEventCreate(&end), "event");
+    // Image batching: each worker verifies B images per schedule (one
+    // kernel launch carries B images' rows). Needs every label (margin pass).
+    static const int batch_env = env_int("PC_IMG_BATCH", -1);
+    bool labeled = n_images >= 2 && net->opt.exec_mode != 2;
+    for (int i = 0; labeled && i < n_images; ++i) labeled = labels[i] >= 0 && labels[i] < net->n_out;
+    int B = 1;
+    if (labeled) {
+      B = batch_env >= 0 ? batch_env : (n_images + conc - 1) / conc;
+      if (net->total > (1ll << 20)) B = std::min(B, 4);  // large nets: per-image state is big
+      B = std::max(1, std::min(B, kMaxBatch));
+    }
     std::vector<Ctx*> ctxs(conc);
     for (int w = 0; w < conc; ++w) {
-      ctxs[w] = acquire(net);
+      ctxs[w] = B > 1 ? acquire_batched(net, B) : acquire(net);
       ctxs[w]->budget = budget;
     }
     ck(cudaEventRecord(start, master), "event");
@@ -1950,7 +2136,63 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
     std::mutex err_mu;
     std::string err;
     pc_status err_code = PC_OK;
+    auto work_batched = [&](int w) {
+      cudaSetDevice(net->device);
+      g_launches = 0;
+      Ctx* c = ctxs[w];
+      const long long T = c->total;
+      std::vector<double> mg((size_t)B * nm);
+      std::vector<pc_stats> sts(B);
+      for (;;) {
+        const int i = next.fetch_add(B);
+        if (i >= n_images) break;
+        const int nb = std::min(B, n_images - i);
+        const pc_status st = guard([&] {
+          cudaStream_t s = c->stream;
+          for (int b = 0; b < nb; ++b) {
+            const double* li = lo + (size_t)(i + b) * n0;
+            const double* ui = up + (size_t)(i + b) * n0;
+            const cudaMemcpyKind kind = device_inputs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+            if (!device_inputs)
+              for (long long k = 0; k < n0; ++k)
+                if (std::isnan(li[k]) || std::isnan(ui[k]))
+                  throw StatusError(PC_ERR_INVALID_ARGUMENT, "Interval: NaN endpoint");
+            ck(cudaMemcpyAsync(c->blo + b * T, li, sizeof(double) * n0, kind, s), "box");
+            ck(cudaMemcpyAsync(c->bhi + b * T, ui, sizeof(double) * n0, kind, s), "box");
+            ck(cudaMemcpyAsync(c->rlo + b * T, c->blo + b * T, sizeof(double) * n0, cudaMemcpyDeviceToDevice, s), "box");
+            ck(cudaMemcpyAsync(c->rhi + b * T, c->bhi + b * T, sizeof(double) * n0, cudaMemcpyDeviceToDevice, s), "box");
+          }
+          c->ev_used = 0;
+          c->sync_used = 0;
+          c->prof.clear();
+          c->dense_ev.clear();
+          run_test_batched(c, nb, labels + i, mg.data(), sts.data());
+          const int nr = net->n_out - 1;
+          for (int b = 0; b < nb; ++b) {
+            bool v = true;
+            for (int r = 0; r < nr; ++r) {
+              if (margins) margins[(size_t)(i + b) * nm + r] = mg[(size_t)b * nr + r];
+              if (!(mg[(size_t)b * nr + r] > 0.0)) v = false;
+            }
+            if (verified) verified[i + b] = v ? 1 : 0;
+            if (stats) stats[i + b] = sts[b];
+          }
+        });
+        if (st != PC_OK) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (err_code == PC_OK) {
+            err_code = st;
+            err = g_err;
+          }
+        }
+      }
+      launches += g_launches;
+    };
     auto work = [&](int w) {
+      if (B > 1) {
+        work_batched(w);
+        return;
+      }
       cudaSetDevice(net->device);
       g_launches = 0;
       for (;;) {

@@ -129,7 +129,19 @@ struct Dirty {
   int* gen_l;    // per layer
   int g;
   int force;
+  // image-batched launches: blockIdx.z = image; per-image strides of the
+  // neuron-indexed state (and gen_n), of gen_pos and of gen_l
+  long long zs = 0, zp = 0;
+  int zl = 0;
 };
+
+// Rebase one image's pointers (blockIdx.z) of a forward kernel.
+#define PC_FWD_IMAGE(...)                                      \
+  const long long pc_zo = (long long)blockIdx.z * dt.zs;       \
+  dt.gen_n += pc_zo;                                           \
+  dt.gen_pos += (long long)blockIdx.z * dt.zp;                 \
+  dt.gen_l += (long long)blockIdx.z * dt.zl;                   \
+  __VA_ARGS__
 
 __device__ __forceinline__ bool bits_differ(double a, double b) {
   return __double_as_longlong(a) != __double_as_longlong(b);
@@ -200,13 +212,20 @@ __device__ __forceinline__ void raw_term(double w, double a, double b, double& l
   }
 }
 
+// Dense layer. Block = 32 neurons x 2 tracks (warp 0: padded lo/hi/abs,
+// warp 1: raw lo/hi). Weight and input tiles stream through a cp.async double
+// buffer one tile ahead; within a tile the (checked) outward-rounded products
+// of a 16-input slice are formed first, off the accumulators' critical path,
+// then the serial chains run in ascending input order (eval.hpp:133-148).
 __global__ void __launch_bounds__(2 * kFDN)
     k_fwd_dense(LayerDev L, int layer, const double* xlo, const double* xhi, const double* xrlo,
                 const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi,
                 double* dev, double* relax, Dirty dt, long long gofs) {
+  PC_FWD_IMAGE(xlo += pc_zo; xhi += pc_zo; xrlo += pc_zo; xrhi += pc_zo; ylo += pc_zo; yhi += pc_zo;
+               yrlo += pc_zo; yrhi += pc_zo; dev += pc_zo; if (relax) relax += 8 * pc_zo;)
   if (!dt.force && dt.gen_l[L.pred0] != dt.g) return;  // no input changed this round
-  __shared__ double s_w[kFDT][kFDN];
-  __shared__ double s_x[5][kFDT];  // padded lo, hi, mag; raw lo, hi
+  __shared__ double s_w[2][kFDT][kFDN];
+  __shared__ double s_x[2][4][kFDT];  // padded lo, hi; raw lo, hi
   const int n_out = L.out_c;
   const int n_in = L.in_w * L.in_h * L.in_c;
   const int lane = threadIdx.x & 31, track = threadIdx.x >> 5;
@@ -216,29 +235,53 @@ __global__ void __launch_bounds__(2 * kFDN)
   double lo = bias, hi = bias, ab = fabs(bias);
   long long terms = 1;
   bool bad = false;
-  for (int t0 = 0; t0 < n_in; t0 += kFDT) {
+  auto stage = [&](int t0, int b) {
     const int tn = min(kFDT, n_in - t0);
-    __syncthreads();
     for (int e = threadIdx.x; e < kFDT * kFDN; e += 2 * kFDN) {
       const int tt = e / kFDN, jj = e % kFDN;
-      s_w[tt][jj] = (tt < tn && j0 + jj < n_out) ? L.WT[(size_t)(t0 + tt) * n_out + j0 + jj] : 0.0;
+      const bool ok = tt < tn && j0 + jj < n_out;
+      cp_async8(&s_w[b][tt][jj], L.WT + (ok ? (size_t)(t0 + tt) * n_out + j0 + jj : 0), ok);
     }
-    for (int e = threadIdx.x; e < tn; e += 2 * kFDN) {
-      const double a = xlo[t0 + e], b = xhi[t0 + e];
-      s_x[0][e] = a;
-      s_x[1][e] = b;
-      s_x[2][e] = smax(fabs(a), fabs(b));
-      s_x[3][e] = xrlo[t0 + e];
-      s_x[4][e] = xrhi[t0 + e];
+    for (int e = threadIdx.x; e < 4 * kFDT; e += 2 * kFDN) {
+      const int arr = e / kFDT, tt = e % kFDT;
+      const double* src = arr == 0 ? xlo : arr == 1 ? xhi : arr == 2 ? xrlo : xrhi;
+      const bool ok = tt < tn;
+      cp_async8(&s_x[b][arr][tt], src + (ok ? t0 + tt : 0), ok);
     }
-    __syncthreads();
-    if (track == 0) {
-#pragma unroll 4
-      for (int t = 0; t < tn; ++t)
-        pad_term<true>(s_w[t][lane], s_x[0][t], s_x[1][t], s_x[2][t], lo, hi, ab, terms, bad);
-    } else {
-#pragma unroll 4
-      for (int t = 0; t < tn; ++t) raw_term<true>(s_w[t][lane], s_x[3][t], s_x[4][t], lo, hi, bad);
+    cp_async_commit();
+  };
+  const int ntiles = (n_in + kFDT - 1) / kFDT;
+  stage(0, 0);
+  for (int ti = 0; ti < ntiles; ++ti) {
+    cp_async_wait_all();
+    __syncthreads();  // tile ti landed; tile ti-1 consumed
+    if (ti + 1 < ntiles) stage((ti + 1) * kFDT, (ti + 1) & 1);
+    const int b = ti & 1;
+    const int tn = min(kFDT, n_in - ti * kFDT);
+    constexpr int kS = 16;
+    for (int t1 = 0; t1 < tn; t1 += kS) {
+      double p0[kS], p1[kS], p2[kS];
+      bool nz[kS];
+#pragma unroll
+      for (int k = 0; k < kS; ++k) {
+        const int t = t1 + k;
+        const double w = t < tn ? s_w[b][t][lane] : 0.0;
+        nz[k] = w != 0.0;
+        terms += (track == 0) && nz[k];
+        const bool pos = w > 0.0;
+        const double a = s_x[b][track == 0 ? 0 : 2][t < tn ? t : 0];
+        const double c = s_x[b][track == 0 ? 1 : 3][t < tn ? t : 0];
+        p0[k] = f_mul_dn(w, pos ? a : c, bad);
+        p1[k] = f_mul_up(w, pos ? c : a, bad);
+        p2[k] = track == 0 ? f_mul_up(fabs(w), smax(fabs(a), fabs(c)), bad) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < kS; ++k) {
+        if (!nz[k]) continue;  // zero weights are skipped (eval.hpp:136)
+        lo = f_add_dn(lo, p0[k]);
+        hi = f_add_up(hi, p1[k]);
+        if (track == 0) ab = f_add_up(ab, p2[k]);
+      }
     }
   }
   if (act && bad) {  // out-of-band operand: redo this chain with the exact ops
@@ -312,6 +355,8 @@ __global__ void __launch_bounds__(128)
                const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi,
                double* dev, double* relax, Dirty dt, long long gofs, long long pofs_in,
                long long pofs_out) {
+  PC_FWD_IMAGE(xlo += pc_zo; xhi += pc_zo; xrlo += pc_zo; xrhi += pc_zo; ylo += pc_zo; yhi += pc_zo;
+               yrlo += pc_zo; yrhi += pc_zo; dev += pc_zo; if (relax) relax += 8 * pc_zo;)
   if (!dt.force && dt.gen_l[L.pred0] != dt.g) return;
   const long long numel = (long long)L.out_w * L.out_h * L.out_c;
   const long long jj = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -351,6 +396,8 @@ __global__ void k_fwd_relu(long long n, int C, int layer, const double* xlo, con
                            const double* xrlo, const double* xrhi, double* ylo, double* yhi,
                            double* yrlo, double* yrhi, Dirty dt, long long gofs_in, long long gofs,
                            long long pofs_out) {
+  PC_FWD_IMAGE(xlo += pc_zo; xhi += pc_zo; xrlo += pc_zo; xrhi += pc_zo; ylo += pc_zo; yhi += pc_zo;
+               yrlo += pc_zo; yrhi += pc_zo;)
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (!dt.force && dt.gen_n[gofs_in + i] != dt.g) return;
@@ -365,6 +412,9 @@ __global__ void k_fwd_join(long long n, int C, int layer, const double* alo, con
                            double* yhi, double* yrlo, double* yrhi, double* dev, double* relax,
                            Dirty dt, long long gofs_a, long long gofs_b, long long gofs,
                            long long pofs_out) {
+  PC_FWD_IMAGE(alo += pc_zo; ahi += pc_zo; arlo += pc_zo; arhi += pc_zo; blo += pc_zo; bhi += pc_zo;
+               brlo += pc_zo; brhi += pc_zo; ylo += pc_zo; yhi += pc_zo; yrlo += pc_zo; yrhi += pc_zo;
+               dev += pc_zo; if (relax) relax += 8 * pc_zo;)
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (!dt.force && dt.gen_n[gofs_a + i] != dt.g && dt.gen_n[gofs_b + i] != dt.g) return;
@@ -386,7 +436,7 @@ void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, con
                           const double* bhi, const double* rlo, const double* rhi,
                           const long long* offs, const long long* pofs, int k, int p0, int p1,
                           double* dev, double* relax, int* gen_n, int* gen_pos, int* gen_l, int g,
-                          int force) {
+                          int force, int nimg, long long zs, long long zp, int zl) {
   const long long o = offs[k], a = offs[p0];
   double* ylo = const_cast<double*>(blo) + o;
   double* yhi = const_cast<double*>(bhi) + o;
@@ -394,23 +444,26 @@ void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, con
   double* yrhi = const_cast<double*>(rhi) + o;
   double* rx = feeds_relu ? relax + 8 * o : nullptr;
   const long long n = (long long)L.out_w * L.out_h * L.out_c;
-  const Dirty dt{gen_n, gen_pos, gen_l, g, force};
+  Dirty dt{gen_n, gen_pos, gen_l, g, force};
+  dt.zs = zs;
+  dt.zp = zp;
+  dt.zl = zl;
   switch (L.kind) {
     case KIND_DENSE:
-      k_fwd_dense<<<cdiv(n, kFDN), 2 * kFDN, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo,
+      k_fwd_dense<<<dim3(cdiv(n, kFDN), 1, nimg), 2 * kFDN, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo,
                                                      yhi, yrlo, yrhi, dev + o, rx, dt, o);
       break;
     case KIND_CONV:
-      k_fwd_conv<<<cdiv(n, 64), 64, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi, yrlo,
+      k_fwd_conv<<<dim3(cdiv(n, 64), 1, nimg), 64, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi, yrlo,
                                             yrhi, dev + o, rx, dt, o, pofs[p0], pofs[k]);
       break;
     case KIND_RELU:
-      k_fwd_relu<<<cdiv(n, 256), 256, 0, s>>>(n, L.out_c, k, blo + a, bhi + a, rlo + a, rhi + a,
+      k_fwd_relu<<<dim3(cdiv(n, 256), 1, nimg), 256, 0, s>>>(n, L.out_c, k, blo + a, bhi + a, rlo + a, rhi + a,
                                               ylo, yhi, yrlo, yrhi, dt, a, o, pofs[k]);
       break;
     case KIND_JOIN: {
       const long long b = offs[p1];
-      k_fwd_join<<<cdiv(n, 256), 256, 0, s>>>(n, L.out_c, k, blo + a, bhi + a, rlo + a, rhi + a,
+      k_fwd_join<<<dim3(cdiv(n, 256), 1, nimg), 256, 0, s>>>(n, L.out_c, k, blo + a, bhi + a, rlo + a, rhi + a,
                                               blo + b, bhi + b, rlo + b, rhi + b, ylo, yhi, yrlo,
                                               yrhi, dev + o, rx, dt, a, b, o, pofs[k]);
       break;
@@ -438,7 +491,12 @@ constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads)
     k_seed(int n, const double* blo, const double* bhi, const double* rlo, const double* rhi,
            int allow_freeze, int early_term, double* cand, char* frozen, int* live, int* n_live,
-           unsigned long long* n_prefrozen) {
+           unsigned long long* n_prefrozen, long long sst, long long kq, int pstride) {
+  if (blockIdx.x) {  // image-batched: block b seeds image b
+    const long long b = blockIdx.x;
+    blo += b * sst; bhi += b * sst; rlo += b * sst; rhi += b * sst;
+    cand += 4 * b * kq; frozen += b * kq; live += b * kq; n_live += b; n_prefrozen += b * pstride;
+  }
   using Scan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
@@ -472,9 +530,10 @@ __global__ void __launch_bounds__(kScanThreads)
 
 void launch_seed(cudaStream_t s, int n, const double* blo, const double* bhi, const double* rlo,
                  const double* rhi, int allow_freeze, int early_term, double* cand, char* frozen,
-                 int* live, int* n_live, unsigned long long* n_prefrozen) {
-  k_seed<<<1, kScanThreads, 0, s>>>(n, blo, bhi, rlo, rhi, allow_freeze, early_term, cand, frozen,
-                                    live, n_live, n_prefrozen);
+                 int* live, int* n_live, unsigned long long* n_prefrozen, int nimg, long long sst,
+                 long long kq, int pstride) {
+  k_seed<<<nimg, kScanThreads, 0, s>>>(n, blo, bhi, rlo, rhi, allow_freeze, early_term, cand, frozen,
+                                       live, n_live, n_prefrozen, sst, kq, pstride);
   ++g_launches;
 }
 
@@ -483,7 +542,9 @@ void launch_seed(cudaStream_t s, int n, const double* blo, const double* bhi, co
 // neurons for the refresh round g.
 __global__ void k_writeback(int n, int C, int layer, const double* cand, double* blo, double* bhi,
                             double* rlo, double* rhi, double* relax, Dirty dt, long long gofs,
-                            long long pofs) {
+                            long long pofs, long long kq) {
+  PC_FWD_IMAGE(blo += pc_zo; bhi += pc_zo; rlo += pc_zo; rhi += pc_zo; if (relax) relax += 8 * pc_zo;
+               cand += 4 * (long long)blockIdx.z * kq;)
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const Iv b{cand[4 * q + 0], cand[4 * q + 1]};
@@ -499,10 +560,14 @@ __global__ void k_writeback(int n, int C, int layer, const double* cand, double*
 
 void launch_writeback(cudaStream_t s, int n, int C, int layer, const double* cand, double* blo,
                       double* bhi, double* rlo, double* rhi, double* relax, int* gen_n,
-                      int* gen_pos, int* gen_l, int g, long long gofs, long long pofs) {
-  const Dirty dt{gen_n, gen_pos, gen_l, g, 0};
-  k_writeback<<<cdiv(n, 256), 256, 0, s>>>(n, C, layer, cand, blo, bhi, rlo, rhi, relax, dt, gofs,
-                                           pofs);
+                      int* gen_pos, int* gen_l, int g, long long gofs, long long pofs, int nimg,
+                      long long zs, long long zp, int zl, long long kq) {
+  Dirty dt{gen_n, gen_pos, gen_l, g, 0};
+  dt.zs = zs;
+  dt.zp = zp;
+  dt.zl = zl;
+  k_writeback<<<dim3(cdiv(n, 256), 1, nimg), 256, 0, s>>>(n, C, layer, cand, blo, bhi, rlo, rhi, relax,
+                                                          dt, gofs, pofs, kq);
   ++g_launches;
 }
 
@@ -518,7 +583,9 @@ __global__ void k_init_affine(LayerDev Q, RowsDev rows, FrameDev f, const double
   int i;
   if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
-  const int q = row_query(rows, i, upper);
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  dev_q += img * rows.sst;
   const long long cells = out.cells;
   double* lo = out.lo + (size_t)i * cells;
   double* hi = out.hi + (size_t)i * cells;
@@ -745,8 +812,11 @@ __global__ void __launch_bounds__(32 * kChainWarps)
   int i;
   if (!rows_resolve(rows, blockIdx.x * kChainWarps + warp, i)) return;
   bool upper;
-  const int q = row_query(rows, i, upper);
-  if (frozen && frozen[q]) return;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  dev += img * rows.sst;
+  ctr += img;
   if (is_conv && lane == 0)
     atomicAdd(&ctr->gbc_dense_equiv, (unsigned long long)L.out_w * L.out_h * L.out_c *
                                          ((unsigned long long)L.in_w * L.in_h * L.in_c));
@@ -853,8 +923,10 @@ __global__ void __launch_bounds__(32 * kChainWarps)
   int i;
   if (!rows_resolve(rows, blockIdx.x * kChainWarps + warp, i)) return;
   bool upper;
-  const int q = row_query(rows, i, upper);
-  if (frozen && frozen[q]) return;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  relax += 8 * img * rows.sst;
   int bw, bh;
   frame_base(f, q, bw, bh);
   const long long cells = m.cells;
@@ -941,8 +1013,13 @@ __global__ void __launch_bounds__(32 * kChainWarps)
   int i;
   if (!rows_resolve(rows, blockIdx.x * kChainWarps + warp, i)) return;
   bool upper;
-  const int q = row_query(rows, i, upper);
-  if (frozen && frozen[q]) return;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  blo += img * rows.sst;
+  bhi += img * rows.sst;
+  rlo += img * rows.sst;
+  rhi += img * rows.sst;
   int bw, bh;
   frame_base(f, q, bw, bh);
   const long long cells = m.cells;
@@ -989,13 +1066,6 @@ void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, M
 // recomputed with the exact ops.
 constexpr int kDC = 128, kDK = 16;  // columns per block, frame cells per slab
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 8 : 0;  // src-size 0: zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 __device__ __forceinline__ void madd_fast(double w, double clo, double chi, double& lo, double& hi,
                                           bool& bad) {
@@ -1784,7 +1854,9 @@ __global__ void __launch_bounds__(256)
   int i;
   if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
-  const int q = row_query(rows, i, upper);
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  relax += 8 * img * rows.sst;
   int bw, bh;
   frame_base(f, q, bw, bh);
   const long long cells = in.cells;
@@ -1904,21 +1976,24 @@ __global__ void __launch_bounds__(kScanThreads)
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
   __shared__ int s_live;
+  __shared__ unsigned char s_live_img[kMaxBatch];  // image-batched walks: per image
   if (rows.dR) R = *rows.dR;  // device-driven walk: the live rows of this checkpoint
   if (threadIdx.x == 0) {
     s_base = 0;
     s_live = 0;
   }
+  if (threadIdx.x < kMaxBatch) s_live_img[threadIdx.x] = 0;
   int froze = 0;
   __syncthreads();
   for (int start = 0; start < R; start += kScanThreads) {
     const int r = start + threadIdx.x;
     int keep = 0, q = 0;
     if (r < R) {
-      q = rows.row_q[r];
+      q = rows.row_q[r];  // a key (img * kq + neuron) in batched walks: cand / frozen are keyed alike
       double* cd = cand + 4 * (size_t)q;
       if (!frozen[q]) {
         s_live = 1;  // the reference still has this row: the checkpoint runs
+        if (rows.kq) s_live_img[q / rows.kq] = 1;
         const double v = vals[r], rv = rvals[r];  // offer_hi
         if (v < cd[1]) cd[1] = v;
         if (rv < cd[3]) cd[3] = rv;
@@ -1927,7 +2002,10 @@ __global__ void __launch_bounds__(kScanThreads)
         if (rv2 > cd[2]) cd[2] = rv2;
         if (allow_freeze && (!(cd[2] < 0.0) || !(cd[3] > 0.0))) {
           frozen[q] = 1;
-          if (early_term) ++froze;
+          if (early_term) {
+            if (rows.kq) atomicAdd(&ctr[q / rows.kq].frozen, 1ull);
+            else ++froze;
+          }
         }
       }
       keep = !(early_term && frozen[q]);
@@ -1943,8 +2021,12 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
   }
   if (froze) atomicAdd(&ctr->frozen, (unsigned long long)froze);
-  if (threadIdx.x == 0 && (s_live || !early_term))
+  if (rows.kq) {
+    if (threadIdx.x < rows.nimg && (s_live_img[threadIdx.x] || !early_term))
+      atomicAdd(&ctr[threadIdx.x].checkpoints, 1ull);
+  } else if (threadIdx.x == 0 && (s_live || !early_term)) {
     atomicAdd(ck_count ? ck_count : &ctr->checkpoints, 1ull);
+  }
   const int nR = s_base;
   for (int p = threadIdx.x; p < nR; p += blockDim.x) map[nR + p] = R + map[p];  // lower rows
   if (threadIdx.x == 0) *new_R = nR;
@@ -2009,6 +2091,59 @@ void launch_ck_merge(cudaStream_t s, unsigned long long* a, unsigned long long* 
   ++g_launches;
 }
 
+// Image-batched seed: per-image live lists (live + img * kq, counts n_live[img])
+// concatenated into one key list (img * kq + neuron), image-major; total count.
+__global__ void k_gather_keys(const int* live, const int* n_live, int nimg, int kq, int* keys,
+                              int* total) {
+  __shared__ int s_off[kMaxBatch + 1];
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int b = 0; b < nimg; ++b) {
+      s_off[b] = a;
+      a += n_live[b];
+    }
+    s_off[nimg] = a;
+    *total = a;
+  }
+  __syncthreads();
+  for (int b = 0; b < nimg; ++b) {
+    const int cnt = s_off[b + 1] - s_off[b];
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x)
+      keys[s_off[b] + k] = b * kq + live[(size_t)b * kq + k];
+  }
+}
+
+void launch_gather_keys(cudaStream_t s, const int* live, const int* n_live, int nimg, int kq,
+                        int* keys, int* total) {
+  k_gather_keys<<<1, 256, 0, s>>>(live, n_live, nimg, kq, keys, total);
+  ++g_launches;
+}
+
+// Image-batched margin rows: row key img * kq + class j; +1 at labels[img].
+__global__ void k_init_margin_keys(RowsDev rows, const int* labels, int n_out, MatDev out) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
+  bool upper;
+  int img;
+  const int j = row_query(rows, i, upper, img);
+  const int label = labels[img];
+  MagAcc mag;
+  for (int c = threadIdx.x; c < n_out; c += blockDim.x) {
+    const double v = (c == label) ? 1.0 : (c == j ? -1.0 : 0.0);
+    out.lo[(size_t)i * n_out + c] = v;
+    out.hi[(size_t)i * n_out + c] = v;
+    mag.add(v);
+  }
+  mag.flush(out.stat);
+  if (threadIdx.x < 4) out.K[4 * (size_t)i + threadIdx.x] = 0.0;
+}
+
+void launch_init_margin_keys(cudaStream_t s, const RowsDev& rows, const int* labels, int n_out,
+                             MatDev out) {
+  k_init_margin_keys<<<rows.n, 128, 0, s>>>(rows, labels, n_out, out);
+  ++g_launches;
+}
+
 // run_margin_pass checkpoint (backsub.hpp:1082-1091): best = max.
 __global__ void k_margin_offer(int n, const double* vals, double* best, char* has) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2020,7 +2155,7 @@ __global__ void k_margin_offer(int n, const double* vals, double* best, char* ha
 }
 
 void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best, char* has) {
-  k_margin_offer<<<1, 128, 0, s>>>(n, vals, best, has);
+  k_margin_offer<<<cdiv(n, 128), 128, 0, s>>>(n, vals, best, has);
   ++g_launches;
 }
 
@@ -2038,7 +2173,7 @@ void init_kernel_attrs_kernels() {
   carve(k_init_margin); carve(k_chain_affine); carve(k_chain_relu); carve(k_concretize);
   carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef); carve(k_gbc_sparse); carve(k_gbc_sparse2); carve(k_compact_cells);
   carve(k_relu_coef); carve(k_merge); carve(k_offer); carve(k_shard_pack); carve(k_shard_unpack);
-  carve(k_margin_offer); carve(k_margin_rows);
+  carve(k_margin_offer); carve(k_margin_rows); carve(k_gather_keys); carve(k_init_margin_keys);
   carve(k_gbc_smem<1>); carve(k_gbc_smem<2>); carve(k_gbc_smem<4>); carve(k_gbc_smem<8>);
   cudaFuncSetAttribute(k_gbc_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbc_smem_bytes<1>());
   cudaFuncSetAttribute(k_gbc_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbc_smem_bytes<2>());

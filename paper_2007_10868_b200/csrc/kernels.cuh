@@ -162,6 +162,15 @@ __device__ __forceinline__ void madd_band_lat(double w, double cl, double ch, do
   hi = xh ? sh : th;
 }
 
+// cp.async (sm_80+): 8-byte global -> shared copies, zero-filled when !valid.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 // -0 -> +0 (RN: -0 + +0 = +0), everything else unchanged.
 __device__ __forceinline__ double canon0(double x) { return __dadd_rn(x, 0.0); }
 
@@ -177,7 +186,14 @@ struct RowsDev {
   // device memory (written by the pass seed and by each checkpoint's offers);
   // launches are sized for the bound above and surplus blocks exit.
   const int* dR = nullptr;
+  // Image-batched walks: row_q holds keys img * kq + q; per-neuron state
+  // arrays (bounds, deviations, relaxations) are strided by sst per image,
+  // candidate / freeze arrays by kq, counters by one Counters. kq = 0: one image.
+  int kq = 0;
+  long long sst = 0;
+  int nimg = 1;
 };
+constexpr int kMaxBatch = 64;  // images per batched walk
 
 // Resolve the block-row index b of a launch into logical row i of the rows
 // actually live (upper rows [0, R), lower rows [R, 2R)); false: no such row.
@@ -204,9 +220,15 @@ __device__ __forceinline__ bool rows_resolve(RowsDev& r, int b, int& i) {
   return b - Rmax < R;
 }
 
-__device__ __forceinline__ int row_query(const RowsDev& r, int i, bool& upper) {
+__device__ __forceinline__ int row_query(const RowsDev& r, int i, bool& upper, int& img) {
   upper = i < r.n_up;
-  return r.row_q[upper ? i : i - r.n_up];
+  const int key = r.row_q[upper ? i : i - r.n_up];
+  img = r.kq ? key / r.kq : 0;
+  return r.kq ? key - img * r.kq : key;
+}
+__device__ __forceinline__ int row_query(const RowsDev& r, int i, bool& upper) {
+  int img;
+  return row_query(r, i, upper, img);
 }
 
 struct Counters {  // device-side PassStats accumulators
@@ -225,15 +247,19 @@ void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, con
                           const double* bhi, const double* rlo, const double* rhi,
                           const long long* offs, const long long* pofs, int k, int pred0,
                           int pred1, double* dev, double* relax, int* gen_n, int* gen_pos,
-                          int* gen_l, int g, int force);
+                          int* gen_l, int g, int force, int nimg = 1, long long zs = 0,
+                          long long zp = 0, int zl = 0);  // nimg images (blockIdx.z), strided
 void launch_relax(cudaStream_t s, const double* blo, const double* bhi, long long n, double* relax);
 
 void launch_seed(cudaStream_t s, int n, const double* blo, const double* bhi, const double* rlo,
                  const double* rhi, int allow_freeze, int early_term, double* cand, char* frozen,
-                 int* live, int* n_live, unsigned long long* n_prefrozen);
+                 int* live, int* n_live, unsigned long long* n_prefrozen, int nimg = 1,
+                 long long sst = 0, long long kq = 0, int pstride = 0);
 void launch_writeback(cudaStream_t s, int n, int C, int layer, const double* cand, double* blo,
                       double* bhi, double* rlo, double* rhi, double* relax, int* gen_n,
-                      int* gen_pos, int* gen_l, int g, long long gofs, long long pofs);
+                      int* gen_pos, int* gen_l, int g, long long gofs, long long pofs,
+                      int nimg = 1, long long zs = 0, long long zp = 0, int zl = 0,
+                      long long kq = 0);
 
 void launch_init_affine(cudaStream_t s, const LayerDev& Q, const RowsDev& rows, const FrameDev& f,
                         const double* dev_q, MatDev out);
@@ -241,6 +267,10 @@ void launch_init_identity(cudaStream_t s, const RowsDev& rows, const FrameDev& f
 void launch_init_margin(cudaStream_t s, int label, const int* d_label, int n_out, int first,
                         int count, MatDev out);
 void launch_margin_rows(cudaStream_t s, const int* d_label, int n_out, int* row_q);
+void launch_gather_keys(cudaStream_t s, const int* live, const int* n_live, int nimg, int kq,
+                        int* keys, int* total);
+void launch_init_margin_keys(cudaStream_t s, const RowsDev& rows, const int* labels, int n_out,
+                             MatDev out);
 
 // Chains read the constants of m (through m.src) and write compact ones to Kout.
 // frozen (nullable): rows whose query neuron froze at an earlier checkpoint

@@ -134,16 +134,30 @@ def test_baseline_configs(pc, port, name, n_img):
         run_case(pc, port, net, x, float(eps_s), label=lab)
 
 
-def test_batch_matches_sequential(pc):
-    """pc_net_test_batch (concurrent contexts/streams) == one-at-a-time pc_net_test."""
-    net = pc.generate(11, EXTRA_ARCHS[3])
+@pytest.mark.parametrize("arch", [EXTRA_ARCHS[3], EXTRA_ARCHS[8], BACKSUB_ARCHS[1], EXTRA_ARCHS[9]])
+@pytest.mark.parametrize("concurrency", [1, 5, 12])
+def test_batch_matches_sequential(pc, arch, concurrency):
+    _batch_vs_sequential(pc, arch, concurrency, 12)
+
+
+@pytest.mark.parametrize("arch", [EXTRA_ARCHS[8], EXTRA_ARCHS[1]])
+def test_large_image_batch(pc, arch):
+    """One schedule over 40 images (> 128 margin rows, more rows than one block)."""
+    _batch_vs_sequential(pc, arch, 1, 40)
+
+
+def _batch_vs_sequential(pc, arch, concurrency, n_img):
+    """pc_net_test_batch == one-at-a-time pc_net_test, bit for bit (margins,
+    verdicts, PassStats). 12 images over `concurrency` workers: image-batched
+    schedules of 12 and 3 images per walk, and one image per walk."""
+    net = pc.generate(11, arch)
     v = pc.Verifier(net)
-    X = pc.random_inputs(12, 12, int(np.prod(net.input_shape)))
+    X = pc.random_inputs(12, n_img, int(np.prod(net.input_shape)))
     boxes = [pc.input_box(x, 0.05) for x in X]
     labels = np.array([max(v.candidate(x), 0) for x in X], dtype=np.int32)
     lo = np.stack([b.lo for b in boxes])
     hi = np.stack([b.hi for b in boxes])
-    ver, mar, st, ms = v.test_batch(lo, hi, labels, concurrency=5)
+    ver, mar, st, ms = v.test_batch(lo, hi, labels, concurrency=concurrency)
     assert ms > 0
     for i in range(len(X)):
         r = v.test(lo[i], hi[i], int(labels[i]))
