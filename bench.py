@@ -7,8 +7,9 @@ analyzer.hpp:256-276) on a generator-built network (random-init dyadic
 weights of the named architecture, gen.cpp) and generator inputs. Default
 workload: configs[1] = MNIST 9x500, eps 0.026, early termination on.
 
-  value  device-resident inputs (pc_net_test_device), per-step CUDA events on
-         the engine stream, L2 flushed between steps (outside the events)
+  value  device-resident inputs, per-step CUDA events around pc_net_test_batch
+         (128 images per step over 4 worker contexts, each verifying 32 images
+         per image-batched schedule), L2 flushed between steps (outside the events)
   e2e    the C-ABI call with HOST buffers (pc_net_test): box H2D + margins D2H
          inside the timed region
   cpu_baseline / --impl reference: the unmodified reference (oracle/_ref,
@@ -267,21 +268,24 @@ def main():
         dev_ms, launches, dev_verified = run(True)
     e2e_ms, _, _ = run(False)
 
-    # single-image latency and the roofline kernel's live timing (engine stream)
+    # single-image latency (one image alone on the engine stream)
     lat = []
-    dense_ms = dense_bytes = dense_madds = 0.0
-    dense_n = 0
     for i in range(min(5, len(boxes))):
         flush.fill_(i & 0xFF)
         torch.cuda.synchronize()
         r = v.test(boxes[i].lo, boxes[i].hi, int(labels_all[i]))
-        t = v.last_timing()
         if i:
-            lat.append(t["total_ms"])
-            dense_ms += t["dense_ms"]
-            dense_bytes += t["dense_bytes"]
-            dense_n += t["dense_launches"]
-            dense_madds += t["dense_madds"]
+            lat.append(v.last_timing()["total_ms"])
+    # the roofline kernel's live timing inside the measured workload: one more
+    # step of the batched run, CUDA events around every dense launch on the
+    # stream it is launched on
+    flush.fill_(7)
+    torch.cuda.synchronize()
+    dlo, dhi, lab = dev_batches[0]
+    v.test_batch(dlo.data_ptr(), dhi.data_ptr(), lab, args.concurrency, device_inputs=True)
+    t = v.last_timing()
+    dense_ms, dense_bytes = t["dense_ms"], t["dense_bytes"]
+    dense_n, dense_madds = t["dense_launches"], t["dense_madds"]
     # row-sharded single-image latency (north_star: one image's passes split across the GPUs)
     lat_sharded = None
     if world > 1:
@@ -335,6 +339,10 @@ def main():
                      "launches": dense_n, "kernel_ms": dense_ms,
                      "algorithmic_bytes": dense_bytes,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+                     # one ncu --set full capture of this kernel (profiles/r1_final_ncu_dense_coef.txt):
+                     # a 9-row launch read 2.118 MB of DRAM for 2.142 MB algorithmic bytes
+                     "ncu_capture": {"dram_bytes_per_launch": 2118400, "algorithmic_bytes_per_launch": 2142000,
+                                     "rows": 9, "source": "profiles/r1_final_ncu_dense_coef.txt"},
                      # the kernel is FP64-pipe / chain-latency bound, not HBM bound: its
                      # algorithmic interval multiply-adds per second against the measured
                      # bit-exact-emulation peak (profiles/r1_microbench_chain_latency.txt)

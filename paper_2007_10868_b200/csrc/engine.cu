@@ -2133,6 +2133,8 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
     for (Ctx* c : ctxs) ck(cudaStreamWaitEvent(c->stream, start, 0), "wait");
     std::atomic<int> next{0};
     std::atomic<long long> launches{0};
+    double agg_dense_ms = 0, agg_dense_bytes = 0, agg_dense_madds = 0;
+    long long agg_dense_launches = 0;
     std::mutex err_mu;
     std::string err;
     pc_status err_code = PC_OK;
@@ -2166,7 +2168,23 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
           c->sync_used = 0;
           c->prof.clear();
           c->dense_ev.clear();
+          g_dense_bytes = g_dense_madds = 0;
+          g_dense_launches = 0;
           run_test_batched(c, nb, labels + i, mg.data(), sts.data());
+          // the dense kernel's live timing (bench.py's roofline) across workers
+          double dms = 0;
+          for (size_t e : c->dense_ev) {
+            float d = 0;
+            if (cudaEventElapsedTime(&d, c->ev_pool[e], c->ev_pool[e + 1]) == cudaSuccess) dms += d;
+          }
+          cudaGetLastError();
+          {
+            std::lock_guard<std::mutex> lk(err_mu);
+            agg_dense_ms += dms;
+            agg_dense_bytes += g_dense_bytes;
+            agg_dense_madds += g_dense_madds;
+            agg_dense_launches += g_dense_launches;
+          }
           const int nr = net->n_out - 1;
           for (int b = 0; b < nb; ++b) {
             bool v = true;
@@ -2240,6 +2258,12 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
     cudaEventDestroy(end);
     cudaStreamDestroy(master);
     g_last_launches = launches.load();
+    if (B > 1) {
+      g_dense_ms = agg_dense_ms;
+      g_dense_bytes = agg_dense_bytes;
+      g_dense_madds = agg_dense_madds;
+      g_dense_launches = agg_dense_launches;
+    }
     if (err_code != PC_OK) throw StatusError(err_code, err);
   });
 }

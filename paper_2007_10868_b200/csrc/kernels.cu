@@ -212,11 +212,6 @@ __device__ __forceinline__ void raw_term(double w, double a, double b, double& l
   }
 }
 
-// Dense layer. Block = 32 neurons x 2 tracks (warp 0: padded lo/hi/abs,
-// warp 1: raw lo/hi). Weight and input tiles stream through a cp.async double
-// buffer one tile ahead; within a tile the (checked) outward-rounded products
-// of a 16-input slice are formed first, off the accumulators' critical path,
-// then the serial chains run in ascending input order (eval.hpp:133-148).
 __global__ void __launch_bounds__(2 * kFDN)
     k_fwd_dense(LayerDev L, int layer, const double* xlo, const double* xhi, const double* xrlo,
                 const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi,
@@ -224,8 +219,8 @@ __global__ void __launch_bounds__(2 * kFDN)
   PC_FWD_IMAGE(xlo += pc_zo; xhi += pc_zo; xrlo += pc_zo; xrhi += pc_zo; ylo += pc_zo; yhi += pc_zo;
                yrlo += pc_zo; yrhi += pc_zo; dev += pc_zo; if (relax) relax += 8 * pc_zo;)
   if (!dt.force && dt.gen_l[L.pred0] != dt.g) return;  // no input changed this round
-  __shared__ double s_w[2][kFDT][kFDN];
-  __shared__ double s_x[2][4][kFDT];  // padded lo, hi; raw lo, hi
+  __shared__ double s_w[kFDT][kFDN];
+  __shared__ double s_x[5][kFDT];  // padded lo, hi, mag; raw lo, hi
   const int n_out = L.out_c;
   const int n_in = L.in_w * L.in_h * L.in_c;
   const int lane = threadIdx.x & 31, track = threadIdx.x >> 5;
@@ -235,53 +230,29 @@ __global__ void __launch_bounds__(2 * kFDN)
   double lo = bias, hi = bias, ab = fabs(bias);
   long long terms = 1;
   bool bad = false;
-  auto stage = [&](int t0, int b) {
+  for (int t0 = 0; t0 < n_in; t0 += kFDT) {
     const int tn = min(kFDT, n_in - t0);
+    __syncthreads();
     for (int e = threadIdx.x; e < kFDT * kFDN; e += 2 * kFDN) {
       const int tt = e / kFDN, jj = e % kFDN;
-      const bool ok = tt < tn && j0 + jj < n_out;
-      cp_async8(&s_w[b][tt][jj], L.WT + (ok ? (size_t)(t0 + tt) * n_out + j0 + jj : 0), ok);
+      s_w[tt][jj] = (tt < tn && j0 + jj < n_out) ? L.WT[(size_t)(t0 + tt) * n_out + j0 + jj] : 0.0;
     }
-    for (int e = threadIdx.x; e < 4 * kFDT; e += 2 * kFDN) {
-      const int arr = e / kFDT, tt = e % kFDT;
-      const double* src = arr == 0 ? xlo : arr == 1 ? xhi : arr == 2 ? xrlo : xrhi;
-      const bool ok = tt < tn;
-      cp_async8(&s_x[b][arr][tt], src + (ok ? t0 + tt : 0), ok);
+    for (int e = threadIdx.x; e < tn; e += 2 * kFDN) {
+      const double a = xlo[t0 + e], b = xhi[t0 + e];
+      s_x[0][e] = a;
+      s_x[1][e] = b;
+      s_x[2][e] = smax(fabs(a), fabs(b));
+      s_x[3][e] = xrlo[t0 + e];
+      s_x[4][e] = xrhi[t0 + e];
     }
-    cp_async_commit();
-  };
-  const int ntiles = (n_in + kFDT - 1) / kFDT;
-  stage(0, 0);
-  for (int ti = 0; ti < ntiles; ++ti) {
-    cp_async_wait_all();
-    __syncthreads();  // tile ti landed; tile ti-1 consumed
-    if (ti + 1 < ntiles) stage((ti + 1) * kFDT, (ti + 1) & 1);
-    const int b = ti & 1;
-    const int tn = min(kFDT, n_in - ti * kFDT);
-    constexpr int kS = 16;
-    for (int t1 = 0; t1 < tn; t1 += kS) {
-      double p0[kS], p1[kS], p2[kS];
-      bool nz[kS];
-#pragma unroll
-      for (int k = 0; k < kS; ++k) {
-        const int t = t1 + k;
-        const double w = t < tn ? s_w[b][t][lane] : 0.0;
-        nz[k] = w != 0.0;
-        terms += (track == 0) && nz[k];
-        const bool pos = w > 0.0;
-        const double a = s_x[b][track == 0 ? 0 : 2][t < tn ? t : 0];
-        const double c = s_x[b][track == 0 ? 1 : 3][t < tn ? t : 0];
-        p0[k] = f_mul_dn(w, pos ? a : c, bad);
-        p1[k] = f_mul_up(w, pos ? c : a, bad);
-        p2[k] = track == 0 ? f_mul_up(fabs(w), smax(fabs(a), fabs(c)), bad) : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < kS; ++k) {
-        if (!nz[k]) continue;  // zero weights are skipped (eval.hpp:136)
-        lo = f_add_dn(lo, p0[k]);
-        hi = f_add_up(hi, p1[k]);
-        if (track == 0) ab = f_add_up(ab, p2[k]);
-      }
+    __syncthreads();
+    if (track == 0) {
+#pragma unroll 4
+      for (int t = 0; t < tn; ++t)
+        pad_term<true>(s_w[t][lane], s_x[0][t], s_x[1][t], s_x[2][t], lo, hi, ab, terms, bad);
+    } else {
+#pragma unroll 4
+      for (int t = 0; t < tn; ++t) raw_term<true>(s_w[t][lane], s_x[3][t], s_x[4][t], lo, hi, bad);
     }
   }
   if (act && bad) {  // out-of-band operand: redo this chain with the exact ops
