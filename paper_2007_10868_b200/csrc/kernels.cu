@@ -1667,7 +1667,8 @@ __global__ void __launch_bounds__(256)
 // Two adjacent input channels per thread (even cin, band path only): the
 // compacted coefficient (index + interval) is loaded once for two madds and the
 // weights as one 16-byte pair.
-__global__ void __launch_bounds__(256)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB)
     k_gbc_sparse2(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
                   MatDev out) {
   int i;
@@ -1760,11 +1761,15 @@ __global__ void __launch_bounds__(256)
 void launch_gbc_sparse(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                        const FrameDev& fout, SparseDev sp, MatDev in, MatDev out) {
   static const int pairs = env_int("PC_GBC_PAIRS", 1);
+  static const int minb = env_int("PC_GBC_MINB", 3);
   if (pairs && L.in_c % 2 == 0) {
     unsigned gx = cdiv(out.cells / 2, 256);
     if (gx > 1024) gx = 1024;
     dim3 grid(gx, rows.n);
-    k_gbc_sparse2<<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out);
+    if (minb >= 4) k_gbc_sparse2<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out);
+    else if (minb == 3) k_gbc_sparse2<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out);
+    else if (minb == 2) k_gbc_sparse2<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out);
+    else k_gbc_sparse2<1><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out);
     ++g_launches;
     return;
   }
@@ -2142,7 +2147,17 @@ void init_kernel_attrs_kernels() {
   carve(k_fwd_dense); carve(k_fwd_conv); carve(k_fwd_relu); carve(k_fwd_join); carve(k_relax);
   carve(k_seed); carve(k_writeback); carve(k_init_affine); carve(k_init_identity);
   carve(k_init_margin); carve(k_chain_affine); carve(k_chain_relu); carve(k_concretize);
-  carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef); carve(k_gbc_sparse); carve(k_gbc_sparse2); carve(k_compact_cells);
+  carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef); carve(k_compact_cells);
+  {
+    // the sparse conv kernels use no shared memory; PC_GBC_L1=1 gives them
+    // the largest L1 (weights are re-read by every position of a tap)
+    const int l1 = env_int("PC_GBC_L1", 1) ? 0 : 100;
+    cudaFuncSetAttribute(k_gbc_sparse, cudaFuncAttributePreferredSharedMemoryCarveout, l1);
+    cudaFuncSetAttribute(k_gbc_sparse2<1>, cudaFuncAttributePreferredSharedMemoryCarveout, l1);
+    cudaFuncSetAttribute(k_gbc_sparse2<2>, cudaFuncAttributePreferredSharedMemoryCarveout, l1);
+    cudaFuncSetAttribute(k_gbc_sparse2<3>, cudaFuncAttributePreferredSharedMemoryCarveout, l1);
+    cudaFuncSetAttribute(k_gbc_sparse2<4>, cudaFuncAttributePreferredSharedMemoryCarveout, l1);
+  }
   carve(k_relu_coef); carve(k_merge); carve(k_offer); carve(k_shard_pack); carve(k_shard_unpack);
   carve(k_margin_offer); carve(k_margin_rows); carve(k_gather_keys); carve(k_init_margin_keys);
   carve(k_gbc_smem<1>); carve(k_gbc_smem<2>); carve(k_gbc_smem<4>); carve(k_gbc_smem<8>);

@@ -163,3 +163,21 @@ def _batch_vs_sequential(pc, arch, concurrency, n_img):
         r = v.test(lo[i], hi[i], int(labels[i]))
         assert np.array_equal(r.margins.view(np.int64), mar[i].view(np.int64))
         assert bool(ver[i]) == r.verified and st[i] == r.stats
+
+
+def test_batch_device_inputs_match_host(pc):
+    """pc_net_test_batch with device-resident boxes == with host boxes (bench's value leg)."""
+    import torch
+    net = pc.generate(11, EXTRA_ARCHS[8])
+    v = pc.Verifier(net)
+    X = pc.random_inputs(13, 24, int(np.prod(net.input_shape)))
+    boxes = [pc.input_box(x, 0.05) for x in X]
+    labels = np.array([max(v.candidate(x), 0) for x in X], dtype=np.int32)
+    lo = np.stack([b.lo for b in boxes])
+    hi = np.stack([b.hi for b in boxes])
+    vh, mh, sh, _ = v.test_batch(lo, hi, labels, concurrency=3)
+    dlo, dhi = torch.from_numpy(lo).cuda(), torch.from_numpy(hi).cuda()
+    torch.cuda.synchronize()
+    vd, md_, sd, _ = v.test_batch(dlo.data_ptr(), dhi.data_ptr(), labels, 3, device_inputs=True)
+    assert np.array_equal(mh.view(np.int64), md_.view(np.int64))
+    assert np.array_equal(vh, vd) and sh == sd
