@@ -1089,20 +1089,35 @@ __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const doub
       lo[0] = xl ? sl : tl;  // a zero product (kk >= kn) adds an exact +-0: no-op
       hi[0] = xh ? sh : th;
     }
+  } else if constexpr (BAND) {
+    // Several rows per thread: skip a cell only when it is zero in every row
+    // (block-uniform; ReLU-dead cells are zero in all rows of an image), so
+    // the TM madds of a cell form one branch-free block of 2*TM independent
+    // chains. A zero cell inside a live group adds an exact +-0: a no-op up
+    // to the sign of a zero lower bound, which canon0 restores.
+#pragma unroll
+    for (int kk = 0; kk < kDK; ++kk) {
+      if (kk >= kn) break;
+      double cl[TM], ch[TM];
+      unsigned nz = 0u;
+#pragma unroll
+      for (int u = 0; u < TM; ++u) {
+        cl[u] = s_al[u][kk];
+        ch[u] = s_ah[u][kk];
+        nz |= ((unsigned)__double2hiint(cl[u]) << 1) | (unsigned)__double2loint(cl[u]) |
+              ((unsigned)__double2hiint(ch[u]) << 1) | (unsigned)__double2loint(ch[u]);
+      }
+      if (nz == 0u) continue;
+#pragma unroll
+      for (int u = 0; u < TM; ++u) madd_band(w[kk], cl[u], ch[u], lo[u], hi[u]);
+    }
   } else {
 #pragma unroll
   for (int kk = 0; kk < kDK; ++kk) {
     if (kk >= kn) break;
 #pragma unroll
     for (int u = 0; u < TM; ++u) {
-      if (BAND) {
-        if (bits_zero(s_al[u][kk]) && bits_zero(s_ah[u][kk])) continue;  // block-uniform skip
-        // one row per thread: the chain is latency bound, take the short form
-        if (TM == 1) madd_band_lat(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u]);
-        else madd_band(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u]);
-      } else {
-        madd_fast(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u], bad[u]);
-      }
+      madd_fast(w[kk], s_al[u][kk], s_ah[u][kk], lo[u], hi[u], bad[u]);
     }
   }
   }
@@ -1200,6 +1215,199 @@ __global__ void __launch_bounds__(kDC)
   mag.flush(out.stat);
 }
 
+// Many rows (image batches): TM rows x 128 columns per block, with the
+// layer's weight slab staged in shared memory next to the row slab (3-stage
+// cp.async ring, so no weight registers are held across slabs), and the
+// cells of a slab that are zero in every row of the block dropped before the
+// arithmetic: each warp ballots the slab's nonzero cells and walks them in
+// ascending order in groups of kDG, padding the last group with a zero cell
+// (an exact +-0 term). A group is one branch-free block of kDG x TM
+// independent madds, so the products of later cells overlap the accumulator
+// chains of earlier ones.
+constexpr int kDG = 4;
+constexpr int kDStages = 2;
+
+template <int TM>
+struct DenseSmem2 {
+  double2 c[kDStages][kDK + 1][TM];  // (lo, hi); cell kDK stays zero
+  double w[kDStages][kDK + 1][kDC];  // weight slab; cell kDK stays zero
+};
+
+template <int TM>
+__device__ __forceinline__ void dense2_stage(DenseSmem2<TM>& sm, int b, int k0, int n_k, int r0,
+                                             int nrows, const MatDev& in,
+                                             const double* __restrict__ W, int n_in, int col0,
+                                             int tx) {
+  for (int e = tx; e < TM * kDK; e += kDC) {
+    const int kk = e / TM, rr = e % TM;
+    const int r = r0 + rr, k = k0 + kk;
+    const bool ok = r < nrows && k < n_k;
+    const size_t o = ok ? phys_row(in, r) * (size_t)n_k + k : 0;
+    cp_async8(&sm.c[b][kk][rr].x, in.lo + o, ok);
+    cp_async8(&sm.c[b][kk][rr].y, in.hi + o, ok);
+  }
+  const int col = col0 + tx;
+#pragma unroll 4
+  for (int kk = 0; kk < kDK; ++kk) {
+    const int k = k0 + kk;
+    const bool ok = k < n_k && col < n_in;
+    cp_async8(&sm.w[b][kk][tx], ok ? W + (size_t)k * n_in + col : W, ok);
+  }
+}
+
+template <int TM>
+__global__ void __launch_bounds__(kDC, 6)
+    k_dense_coef2(const double* __restrict__ W, int n_k, int n_in, RowsDev rows, MatDev in,
+                  MatDev out, double wmin, double wmax) {
+  extern __shared__ __align__(16) unsigned char dense2_raw[];
+  DenseSmem2<TM>& sm = *reinterpret_cast<DenseSmem2<TM>*>(dense2_raw);
+  const int tx = threadIdx.x, lane = tx & 31;
+  const int col0 = blockIdx.x * kDC, col = col0 + tx;
+  const int r0 = blockIdx.y * TM;
+  int i0;
+  rows_resolve(rows, 0, i0);
+  const int nrows = rows.n;
+  if (r0 >= nrows) return;
+  const bool band = products_in_band(in.stat, wmin, wmax);
+  for (int b = 0; b < kDStages; ++b) {
+    if (tx < TM) sm.c[b][kDK][tx] = make_double2(0.0, 0.0);
+    sm.w[b][kDK][tx] = 0.0;
+  }
+  double lo[TM], hi[TM];
+  bool bad[TM];
+#pragma unroll
+  for (int u = 0; u < TM; ++u) {
+    lo[u] = hi[u] = 0.0;
+    bad[u] = false;
+  }
+  const int nslab = (n_k + kDK - 1) / kDK;
+#pragma unroll
+  for (int p = 0; p < kDStages - 1; ++p) {
+    if (p < nslab) dense2_stage<TM>(sm, p, p * kDK, n_k, r0, nrows, in, W, n_in, col0, tx);
+    cp_async_commit();
+  }
+  for (int sl = 0; sl < nslab; ++sl) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kDStages - 2));
+    __syncthreads();  // slab sl landed everywhere; slab sl-1's buffer is free
+    if (sl + kDStages - 1 < nslab)
+      dense2_stage<TM>(sm, (sl + kDStages - 1) % kDStages, (sl + kDStages - 1) * kDK, n_k, r0,
+                       nrows, in, W, n_in, col0, tx);
+    cp_async_commit();
+    const int b = sl % kDStages;
+    if (band) {
+      // lane kk < kDK: is cell kk nonzero in any row of the block?
+      unsigned nz = 0u;
+      if (lane < kDK) {
+#pragma unroll
+        for (int u = 0; u < TM; ++u) {
+          const double2 v = sm.c[b][lane][u];
+          nz |= ((unsigned)__double2hiint(v.x) << 1) | (unsigned)__double2loint(v.x) |
+                ((unsigned)__double2hiint(v.y) << 1) | (unsigned)__double2loint(v.y);
+        }
+      }
+      unsigned m = __ballot_sync(0xFFFFFFFFu, nz != 0u);
+      while (m) {
+        int ks[kDG];
+#pragma unroll
+        for (int g = 0; g < kDG; ++g) {
+          ks[g] = m ? __ffs(m) - 1 : kDK;
+          m &= m - 1;
+        }
+        double pl[kDG][TM], ph[kDG][TM];
+#pragma unroll
+        for (int g = 0; g < kDG; ++g) {
+          const double wk = sm.w[b][ks[g]][tx];
+#pragma unroll
+          for (int u = 0; u < TM; ++u) {
+            const double2 c = sm.c[b][ks[g]][u];
+            band_products(wk, c.x, c.y, pl[g][u], ph[g][u]);
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < kDG; ++g)
+#pragma unroll
+          for (int u = 0; u < TM; ++u) band_sums(pl[g][u], ph[g][u], lo[u], hi[u]);
+      }
+    } else {
+      const int kn = min(kDK, n_k - sl * kDK);
+      for (int kk = 0; kk < kn; ++kk) {
+        const double wk = sm.w[b][kk][tx];
+#pragma unroll
+        for (int u = 0; u < TM; ++u) {
+          const double2 v = sm.c[b][kk][u];
+          madd_fast(wk, v.x, v.y, lo[u], hi[u], bad[u]);
+        }
+      }
+    }
+  }
+  if (band) {
+#pragma unroll
+    for (int u = 0; u < TM; ++u) lo[u] = canon0(lo[u]);
+  }
+  if (col >= n_in) return;
+  MagAcc mag;
+#pragma unroll
+  for (int u = 0; u < TM; ++u) {
+    const int r = r0 + u;
+    if (r >= nrows) continue;
+    if (bad[u]) {
+      lo[u] = hi[u] = 0.0;
+      for (int k = 0; k < n_k; ++k)
+        madd_exact(W[(size_t)k * n_in + col], in.lo[phys_row(in, r) * n_k + k],
+                   in.hi[phys_row(in, r) * n_k + k], lo[u], hi[u]);
+    }
+    out.lo[(size_t)r * n_in + col] = lo[u];
+    out.hi[(size_t)r * n_in + col] = hi[u];
+    mag.add(lo[u]);
+    mag.add(hi[u]);
+  }
+  mag.flush(out.stat);
+}
+
+// Rows per thread (PC_DENSE_TM; default 4 above 64 rows). PC_DENSE_TM=-1
+// picks per launch by a wave model: a launch is one wave set of equal tiles
+// (every thread runs the whole n_k chain, so tiles cannot be split along k),
+// cost = waves x TM x per-row cost, waves = ceil(tiles / resident tiles) from
+// the occupancy queried at init. It wins for a lone stream and loses with
+// several worker contexts, whose launches fill each other's last waves.
+static int g_dense_tm = 4;
+static int g_dense_slots[9] = {0};  // resident blocks per GPU, per TM
+
+static int g_dense_v2 = 1;  // PC_DENSE_V2: staged-weight kernel for TM > 1
+
+template <int TM>
+static void dense_launch(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
+                         MatDev out, int n_k, int n_in) {
+  dim3 grid(cdiv(n_in, kDC), cdiv(rows.n, TM));
+  if constexpr (TM > 1) {
+    if (g_dense_v2) {
+      k_dense_coef2<TM><<<grid, kDC, sizeof(DenseSmem2<TM>), s>>>(L.W, n_k, n_in, rows, in, out,
+                                                                   L.wmin, L.wmax);
+      return;
+    }
+  }
+  k_dense_coef<TM><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax);
+}
+
+static int dense_tm(int nrows, int n_in) {
+  // Few rows: one row per thread maximises parallelism (the chain length
+  // n_k bounds latency).
+  if (nrows <= 64) return 1;
+  if (g_dense_tm) return g_dense_tm;
+  static const int cand[3] = {4, 3, 2};
+  static const double cost[9] = {0, 0, 1.08, 1.0, 1.0, 0, 0, 0, 1.0};  // per-row, relative
+  const long long cols = cdiv(n_in, kDC);
+  int best = 4;
+  double best_t = 1e300;
+  for (int TM : cand) {
+    const long long tiles = cols * cdiv(nrows, TM);
+    const long long slots = g_dense_slots[TM] > 0 ? g_dense_slots[TM] : 444;
+    const double t = (double)cdiv(tiles, slots) * TM * cost[TM];
+    if (t < best_t - 1e-9) best_t = t, best = TM;
+  }
+  return best;
+}
+
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
                        MatDev out, cudaEvent_t ev0, cudaEvent_t ev1) {
   const int nrows = rows.n;
@@ -1208,14 +1416,12 @@ void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, M
   if (ev0 || ev1) cudaStreamIsCapturing(s, &cap);
   const unsigned rf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0;
   if (ev0) cudaEventRecordWithFlags(ev0, s, rf);  // external: timeable inside graphs
-  // Few rows: one row per thread maximises parallelism (the chain length n_k
-  // bounds latency); many rows: 4 rows per thread for weight reuse.
-  if (nrows <= 64) {
-    dim3 grid(cdiv(n_in, kDC), nrows);
-    k_dense_coef<1><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax);
-  } else {
-    dim3 grid(cdiv(n_in, kDC), cdiv(nrows, 4));
-    k_dense_coef<4><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax);
+  switch (dense_tm(nrows, n_in)) {
+    case 1: dense_launch<1>(s, L, rows, in, out, n_k, n_in); break;
+    case 2: dense_launch<2>(s, L, rows, in, out, n_k, n_in); break;
+    case 3: dense_launch<3>(s, L, rows, in, out, n_k, n_in); break;
+    case 8: dense_launch<8>(s, L, rows, in, out, n_k, n_in); break;
+    default: dense_launch<4>(s, L, rows, in, out, n_k, n_in); break;
   }
   if (ev1) cudaEventRecordWithFlags(ev1, s, rf);
   ++g_launches;
@@ -2147,7 +2353,40 @@ void init_kernel_attrs_kernels() {
   carve(k_fwd_dense); carve(k_fwd_conv); carve(k_fwd_relu); carve(k_fwd_join); carve(k_relax);
   carve(k_seed); carve(k_writeback); carve(k_init_affine); carve(k_init_identity);
   carve(k_init_margin); carve(k_chain_affine); carve(k_chain_relu); carve(k_concretize);
-  carve(k_dense_coef<1>); carve(k_dense_coef<4>); carve(k_gbc_coef); carve(k_compact_cells);
+  carve(k_dense_coef<1>); carve(k_dense_coef<2>); carve(k_dense_coef<3>);
+  carve(k_dense_coef<4>); carve(k_dense_coef<8>); carve(k_gbc_coef); carve(k_compact_cells);
+  {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    auto slots = [&](auto k, int tm, size_t smem) {
+      int b = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kDC, smem);
+      g_dense_slots[tm] = b * sms;
+    };
+    g_dense_v2 = env_int("PC_DENSE_V2", 1);
+    auto big = [](auto k, size_t bytes) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      carve(k);
+    };
+    big(k_dense_coef2<2>, sizeof(DenseSmem2<2>)); big(k_dense_coef2<3>, sizeof(DenseSmem2<3>));
+    big(k_dense_coef2<4>, sizeof(DenseSmem2<4>)); big(k_dense_coef2<8>, sizeof(DenseSmem2<8>));
+    slots(k_dense_coef<1>, 1, 0);
+    if (g_dense_v2) {
+      slots(k_dense_coef2<2>, 2, sizeof(DenseSmem2<2>));
+      slots(k_dense_coef2<3>, 3, sizeof(DenseSmem2<3>));
+      slots(k_dense_coef2<4>, 4, sizeof(DenseSmem2<4>));
+      slots(k_dense_coef2<8>, 8, sizeof(DenseSmem2<8>));
+    } else {
+      slots(k_dense_coef<2>, 2, 0); slots(k_dense_coef<3>, 3, 0);
+      slots(k_dense_coef<4>, 4, 0); slots(k_dense_coef<8>, 8, 0);
+    }
+    // Default 4: with several worker contexts per GPU the launches of other
+    // streams fill a launch's last wave, so per-row efficiency wins over the
+    // single-launch wave model (PC_DENSE_TM=-1).
+    const int f = env_int("PC_DENSE_TM", 4);
+    g_dense_tm = (f == 1 || f == 2 || f == 3 || f == 4 || f == 8) ? f : 0;
+  }
   {
     // the sparse conv kernels use no shared memory; PC_GBC_L1=1 gives them
     // the largest L1 (weights are re-read by every position of a tap)

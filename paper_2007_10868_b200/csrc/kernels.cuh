@@ -145,6 +145,23 @@ __device__ __forceinline__ void madd_band(double w, double cl, double ch, double
   lo = __fma_rd(__dsub_rn(ul, dl), -0.5, sl);
   hi = __fma_ru(__dsub_rn(uh, dh), 0.5, sh);
 }
+// madd_band split into its accumulator-independent products and the two
+// accumulator steps, for kernels that schedule the products of several terms
+// ahead of the (latency-bound) sum chains.
+__device__ __forceinline__ void band_products(double w, double cl, double ch, double& pl,
+                                              double& ph) {
+  const bool neg = __double2hiint(w) < 0;
+  const double a = neg ? ch : cl, b = neg ? cl : ch;
+  const double pl0 = __dmul_rn(a, w), ph0 = __dmul_rn(b, w);
+  pl = __dadd_rd(pl0, -fabs(__fma_rn(a, w, -pl0)));
+  ph = __dadd_ru(ph0, fabs(__fma_rn(b, w, -ph0)));
+}
+__device__ __forceinline__ void band_sums(double pl, double ph, double& lo, double& hi) {
+  const double sl = __dadd_rn(lo, pl), dl = __dadd_rd(lo, pl), ul = __dadd_ru(lo, pl);
+  const double sh = __dadd_rn(hi, ph), dh = __dadd_rd(hi, ph), uh = __dadd_ru(hi, ph);
+  lo = __fma_rd(__dsub_rn(ul, dl), -0.5, sl);
+  hi = __fma_ru(__dsub_rn(uh, dh), 0.5, sh);
+}
 // Same result as madd_band with a shorter dependency chain through the
 // accumulators (2 FP64 latencies + a select instead of 3): for latency-bound
 // chains with little independent work per thread.
