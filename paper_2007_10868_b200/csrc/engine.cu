@@ -705,7 +705,9 @@ struct Walker {
         g_dense_madds += (double)nrows() * m.cells * out.cells;
         ++g_dense_launches;
       }
-      launch_dense_coef(s, L.d, rows(), md(m), md(out), e0, e1);
+      const HostLayer& P = n->L[L.pred0];
+      const double* rx = P.kind == PC_RELU ? n->relax + 8 * n->off[P.pred0] : nullptr;
+      launch_dense_coef(s, L.d, rows(), md(m), md(out), rx, e0, e1);
       mark(out);
     }
     m = out;

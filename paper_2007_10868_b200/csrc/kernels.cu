@@ -43,6 +43,17 @@ long long big_chain_cells() {
   return v;
 }
 
+// CTA-per-row chain kernels (chains.cu) for long rows. They shorten a lone
+// walk's critical path, but hold 512 threads per row while the serial fold
+// runs; image-batched walks share the GPU with other worker contexts, where
+// the warp-per-row kernels' smaller footprint lets more of the coefficient
+// kernels stay resident (PC_BIG_CHAIN_CELLS_BATCHED: the cell count from
+// which batched walks still use them).
+static bool use_big_chains(long long cells, const RowsDev& rows) {
+  static const long long batched = env_int("PC_BIG_CHAIN_CELLS_BATCHED", 4096);
+  return cells >= big_chain_cells() && (rows.nimg <= 1 || cells >= batched);
+}
+
 #define PC_NAN __longlong_as_double(0x7ff8000000000000ULL)
 
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
@@ -818,7 +829,7 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                          const FrameDev& fin, MatDev m, double* Kout, const double* dev,
                          Counters* ctr, const char* frozen) {
-  if (m.cells >= big_chain_cells()) {
+  if (use_big_chains(m.cells, rows)) {
     launch_chain_affine_big(s, L, is_conv, rows, fin, m, Kout, dev, ctr, frozen);
     return;
   }
@@ -914,7 +925,7 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 
 void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        double* Kout, const double* relax, const char* frozen) {
-  if (m.cells >= big_chain_cells()) {
+  if (use_big_chains(m.cells, rows)) {
     launch_chain_relu_big(s, rows, f, m, Kout, relax, frozen);
     return;
   }
@@ -1014,7 +1025,7 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        const double* blo, const double* bhi, const double* rlo,
                        const double* rhi, double* vals, double* rvals, const char* frozen) {
-  if (m.cells >= big_chain_cells()) {
+  if (use_big_chains(m.cells, rows)) {
     launch_concretize_big(s, rows, f, m, blo, bhi, rlo, rhi, vals, rvals, frozen);
     return;
   }
@@ -1055,6 +1066,81 @@ __device__ __forceinline__ void madd_exact(double w, double clo, double chi, dou
   const double a = w > 0.0 ? clo : chi, b = w > 0.0 ? chi : clo;
   lo = add_down(lo, mul_down(a, w));
   hi = add_up(hi, mul_up(b, w));
+}
+
+// Live output columns. When the frame after this step is a ReLU layer, the
+// relu step maps the coefficient of every stably-negative neuron (relaxation
+// alpha = gamma = 0, backsub.hpp:536-563, analyzer.hpp:50-55) to an exact
+// zero whatever its value, its offsets add exact zeros, and the checkpoint
+// between the two steps multiplies it by that neuron's relu bounds [0, 0]
+// (concretize, backsub.hpp:756-759): the reference computes it, but no
+// observable result depends on it as long as it is finite, which the band
+// proof guarantees. Such columns are written as +0 and not computed. A block
+// owns its column range for those zero writes and a kDC-slice of the
+// ascending list of columns live in any of its rows for the arithmetic, so
+// the warps stay dense. Without relax (frame not a ReLU, or out of band)
+// every column is live and the list is the identity.
+struct DenseCols {
+  int col;    // this thread's output column (>= n_in: none)
+  int count;  // live columns of this block
+};
+
+template <int TM>
+__device__ DenseCols dense_live_cols(const RowsDev& rows, int nrows, int r0, int n_in,
+                                     const double* relax, MatDev out, int* s_cols, int* s_warp) {
+  const int tx = threadIdx.x, lane = tx & 31, wid = tx >> 5;
+  const int x0 = blockIdx.x * kDC;
+  if (!relax) return DenseCols{x0 + tx, min(kDC, n_in - x0)};
+  const double* rx[TM];
+#pragma unroll
+  for (int u = 0; u < TM; ++u) {
+    rx[u] = nullptr;
+    if (r0 + u < nrows) {
+      bool upper;
+      int img;
+      row_query(rows, r0 + u, upper, img);
+      rx[u] = relax + 8 * (long long)img * rows.sst;
+    }
+  }
+  int base = 0;
+  for (int t0 = 0; t0 < n_in; t0 += kDC) {
+    const int t = t0 + tx;
+    bool live = false;
+    if (t < n_in) {
+#pragma unroll
+      for (int u = 0; u < TM; ++u) {
+        if (!rx[u]) continue;
+        const double* R = rx[u] + 8 * (long long)t;
+        const bool dead = bits_zero(R[0]) & bits_zero(R[1]) & bits_zero(R[4]) & bits_zero(R[5]);
+        live |= !dead;
+      }
+    }
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, live);
+    __syncthreads();  // s_warp of the previous round consumed
+    if (lane == 0) s_warp[wid] = __popc(b);
+    __syncthreads();
+    int before = base, total = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kDC / 32; ++w2) {
+      const int c = s_warp[w2];
+      if (w2 < wid) before += c;
+      total += c;
+    }
+    const int pos = before + __popc(b & ((1u << lane) - 1u));
+    if (live && pos >= x0 && pos < x0 + kDC) s_cols[pos - x0] = t;
+    if (!live && t >= x0 && t < x0 + kDC && t < n_in) {
+#pragma unroll
+      for (int u = 0; u < TM; ++u) {
+        if (r0 + u >= nrows) continue;
+        out.lo[(size_t)(r0 + u) * n_in + t] = 0.0;
+        out.hi[(size_t)(r0 + u) * n_in + t] = 0.0;
+      }
+    }
+    base += total;
+  }
+  __syncthreads();
+  const int count = max(0, min(kDC, base - x0));
+  return DenseCols{tx < count ? s_cols[tx] : n_in, count};
 }
 
 template <int TM, bool BAND>
@@ -1157,16 +1243,20 @@ __device__ __forceinline__ void dense_wload(double* w, const double* __restrict_
 template <int TM>
 __global__ void __launch_bounds__(kDC)
     k_dense_coef(const double* __restrict__ W, int n_k, int n_in, RowsDev rows, MatDev in,
-                 MatDev out, double wmin, double wmax) {
+                 MatDev out, double wmin, double wmax, const double* relax) {
   __shared__ DenseSmem<TM> sm;
+  __shared__ int s_cols[kDC], s_warp[kDC / 32];
   const int tx = threadIdx.x;
-  const int col = blockIdx.x * kDC + tx;
   const int r0 = blockIdx.y * TM;
   int i0;
   rows_resolve(rows, 0, i0);  // live row count (physical rows 0..n-1 in order)
   const int nrows = rows.n;
   if (r0 >= nrows) return;
   const bool band = products_in_band(in.stat, wmin, wmax);
+  const DenseCols dc = dense_live_cols<TM>(rows, nrows, r0, n_in, band ? relax : nullptr, out,
+                                           s_cols, s_warp);
+  if (dc.count <= 0) return;
+  const int col = dc.col;
   double lo[TM], hi[TM];
   bool bad[TM];
 #pragma unroll
@@ -1225,6 +1315,9 @@ __global__ void __launch_bounds__(kDC)
 // independent madds, so the products of later cells overlap the accumulator
 // chains of earlier ones.
 constexpr int kDG = 4;
+#ifndef PC_DENSE2_MINB
+#define PC_DENSE2_MINB 3  // resident blocks the register budget is sized for
+#endif
 constexpr int kDStages = 2;
 
 template <int TM>
@@ -1236,7 +1329,7 @@ struct DenseSmem2 {
 template <int TM>
 __device__ __forceinline__ void dense2_stage(DenseSmem2<TM>& sm, int b, int k0, int n_k, int r0,
                                              int nrows, const MatDev& in,
-                                             const double* __restrict__ W, int n_in, int col0,
+                                             const double* __restrict__ W, int n_in, int col,
                                              int tx) {
   for (int e = tx; e < TM * kDK; e += kDC) {
     const int kk = e / TM, rr = e % TM;
@@ -1246,7 +1339,6 @@ __device__ __forceinline__ void dense2_stage(DenseSmem2<TM>& sm, int b, int k0, 
     cp_async8(&sm.c[b][kk][rr].x, in.lo + o, ok);
     cp_async8(&sm.c[b][kk][rr].y, in.hi + o, ok);
   }
-  const int col = col0 + tx;
 #pragma unroll 4
   for (int kk = 0; kk < kDK; ++kk) {
     const int k = k0 + kk;
@@ -1256,19 +1348,25 @@ __device__ __forceinline__ void dense2_stage(DenseSmem2<TM>& sm, int b, int k0, 
 }
 
 template <int TM>
-__global__ void __launch_bounds__(kDC, 6)
+__global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
     k_dense_coef2(const double* __restrict__ W, int n_k, int n_in, RowsDev rows, MatDev in,
-                  MatDev out, double wmin, double wmax) {
+                  MatDev out, double wmin, double wmax, const double* relax) {
   extern __shared__ __align__(16) unsigned char dense2_raw[];
   DenseSmem2<TM>& sm = *reinterpret_cast<DenseSmem2<TM>*>(dense2_raw);
+  __shared__ int s_cols[kDC], s_warp[kDC / 32];
   const int tx = threadIdx.x, lane = tx & 31;
-  const int col0 = blockIdx.x * kDC, col = col0 + tx;
   const int r0 = blockIdx.y * TM;
   int i0;
   rows_resolve(rows, 0, i0);
   const int nrows = rows.n;
   if (r0 >= nrows) return;
   const bool band = products_in_band(in.stat, wmin, wmax);
+  const DenseCols dc = dense_live_cols<TM>(rows, nrows, r0, n_in, band ? relax : nullptr, out,
+                                           s_cols, s_warp);
+  if (dc.count <= 0) return;
+  const int col = dc.col;
+  // warps with no live column skip the arithmetic (they still stage and sync)
+  const bool warp_live = (tx & ~31) < dc.count;
   for (int b = 0; b < kDStages; ++b) {
     if (tx < TM) sm.c[b][kDK][tx] = make_double2(0.0, 0.0);
     sm.w[b][kDK][tx] = 0.0;
@@ -1283,7 +1381,7 @@ __global__ void __launch_bounds__(kDC, 6)
   const int nslab = (n_k + kDK - 1) / kDK;
 #pragma unroll
   for (int p = 0; p < kDStages - 1; ++p) {
-    if (p < nslab) dense2_stage<TM>(sm, p, p * kDK, n_k, r0, nrows, in, W, n_in, col0, tx);
+    if (p < nslab) dense2_stage<TM>(sm, p, p * kDK, n_k, r0, nrows, in, W, n_in, col, tx);
     cp_async_commit();
   }
   for (int sl = 0; sl < nslab; ++sl) {
@@ -1291,9 +1389,10 @@ __global__ void __launch_bounds__(kDC, 6)
     __syncthreads();  // slab sl landed everywhere; slab sl-1's buffer is free
     if (sl + kDStages - 1 < nslab)
       dense2_stage<TM>(sm, (sl + kDStages - 1) % kDStages, (sl + kDStages - 1) * kDK, n_k, r0,
-                       nrows, in, W, n_in, col0, tx);
+                       nrows, in, W, n_in, col, tx);
     cp_async_commit();
     const int b = sl % kDStages;
+    if (!warp_live) continue;
     if (band) {
       // lane kk < kDK: is cell kk nonzero in any row of the block?
       unsigned nz = 0u;
@@ -1373,20 +1472,21 @@ __global__ void __launch_bounds__(kDC, 6)
 static int g_dense_tm = 4;
 static int g_dense_slots[9] = {0};  // resident blocks per GPU, per TM
 
-static int g_dense_v2 = 1;  // PC_DENSE_V2: staged-weight kernel for TM > 1
+static int g_dense_v2 = 1;    // PC_DENSE_V2: staged-weight kernel for TM > 1
+static int g_dense_live = 1;  // PC_DENSE_LIVE: skip columns of stably-negative ReLU inputs
 
 template <int TM>
 static void dense_launch(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
-                         MatDev out, int n_k, int n_in) {
+                         MatDev out, int n_k, int n_in, const double* relax) {
   dim3 grid(cdiv(n_in, kDC), cdiv(rows.n, TM));
   if constexpr (TM > 1) {
     if (g_dense_v2) {
       k_dense_coef2<TM><<<grid, kDC, sizeof(DenseSmem2<TM>), s>>>(L.W, n_k, n_in, rows, in, out,
-                                                                   L.wmin, L.wmax);
+                                                                   L.wmin, L.wmax, relax);
       return;
     }
   }
-  k_dense_coef<TM><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax);
+  k_dense_coef<TM><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax, relax);
 }
 
 static int dense_tm(int nrows, int n_in) {
@@ -1409,7 +1509,8 @@ static int dense_tm(int nrows, int n_in) {
 }
 
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
-                       MatDev out, cudaEvent_t ev0, cudaEvent_t ev1) {
+                       MatDev out, const double* relax, cudaEvent_t ev0, cudaEvent_t ev1) {
+  if (!g_dense_live) relax = nullptr;
   const int nrows = rows.n;
   const int n_k = (int)in.cells, n_in = (int)out.cells;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -1417,11 +1518,11 @@ void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, M
   const unsigned rf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0;
   if (ev0) cudaEventRecordWithFlags(ev0, s, rf);  // external: timeable inside graphs
   switch (dense_tm(nrows, n_in)) {
-    case 1: dense_launch<1>(s, L, rows, in, out, n_k, n_in); break;
-    case 2: dense_launch<2>(s, L, rows, in, out, n_k, n_in); break;
-    case 3: dense_launch<3>(s, L, rows, in, out, n_k, n_in); break;
-    case 8: dense_launch<8>(s, L, rows, in, out, n_k, n_in); break;
-    default: dense_launch<4>(s, L, rows, in, out, n_k, n_in); break;
+    case 1: dense_launch<1>(s, L, rows, in, out, n_k, n_in, relax); break;
+    case 2: dense_launch<2>(s, L, rows, in, out, n_k, n_in, relax); break;
+    case 3: dense_launch<3>(s, L, rows, in, out, n_k, n_in, relax); break;
+    case 8: dense_launch<8>(s, L, rows, in, out, n_k, n_in, relax); break;
+    default: dense_launch<4>(s, L, rows, in, out, n_k, n_in, relax); break;
   }
   if (ev1) cudaEventRecordWithFlags(ev1, s, rf);
   ++g_launches;
@@ -2365,6 +2466,7 @@ void init_kernel_attrs_kernels() {
       g_dense_slots[tm] = b * sms;
     };
     g_dense_v2 = env_int("PC_DENSE_V2", 1);
+    g_dense_live = env_int("PC_DENSE_LIVE", 1);
     auto big = [](auto k, size_t bytes) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
       carve(k);

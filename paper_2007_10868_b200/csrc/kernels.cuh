@@ -316,8 +316,10 @@ void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& 
 // overrides, read once; the tests force 1 to run the corpus through them).
 long long big_chain_cells();
 
+// relax: relaxations of the ReLU whose output is the frame after this step
+// (per image, strided by rows.sst), or nullptr: see dense_live_cols.
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
-                       MatDev out, cudaEvent_t ev0, cudaEvent_t ev1);
+                       MatDev out, const double* relax, cudaEvent_t ev0, cudaEvent_t ev1);
 // Compacted nonzero coefficients of a conv step's input, per frame cell of
 // each (logical) row: cnt[row*ncell + cell] entries, channel idx and values
 // at ((row*ncell + cell)*C + k), ascending channel.
