@@ -182,7 +182,7 @@ __device__ __forceinline__ void store_bounds(double* ylo, double* yhi, double* y
 // Dense layer. Block = 32 neurons x 2 tracks (warp 0: padded lo/hi/abs,
 // warp 1: raw lo/hi); weights and inputs staged through shared memory in
 // ascending input tiles.
-constexpr int kFDN = 32, kFDT = 64;
+constexpr int kFDN = 32, kFDT = 64;  // kFDT == 2 * kFDN: one input per thread per tile
 
 template <bool FAST>
 __device__ __forceinline__ void pad_term(double w, double a, double b, double m, double& lo,
@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(2 * kFDN)
   if (!dt.force && dt.gen_l[L.pred0] != dt.g) return;  // no input changed this round
   __shared__ double s_w[kFDT][kFDN];
   __shared__ double s_x[5][kFDT];  // padded lo, hi, mag; raw lo, hi
+  __shared__ int s_live[kFDT], s_dead[kFDT], s_cnt[2][2];
   const int n_out = L.out_c;
   const int n_in = L.in_w * L.in_h * L.in_c;
   const int lane = threadIdx.x & 31, track = threadIdx.x >> 5;
@@ -241,6 +242,12 @@ __global__ void __launch_bounds__(2 * kFDN)
   double lo = bias, hi = bias, ab = fabs(bias);
   long long terms = 1;
   bool bad = false;
+  // Inputs whose padded and raw bounds are both [0, 0] (stably-negative
+  // ReLU outputs) add exact zeros: a no-op on the accumulators unless one is
+  // still -0, which only a -0 bias can start (RN sums of nonzero terms never
+  // return to -0). They only count as terms (w != 0); blocks with a -0 bias
+  // run every input.
+  const bool skip_dead = !__syncthreads_or(act && __double_as_longlong(bias) == (long long)0x8000000000000000ULL);
   for (int t0 = 0; t0 < n_in; t0 += kFDT) {
     const int tn = min(kFDT, n_in - t0);
     __syncthreads();
@@ -248,22 +255,46 @@ __global__ void __launch_bounds__(2 * kFDN)
       const int tt = e / kFDN, jj = e % kFDN;
       s_w[tt][jj] = (tt < tn && j0 + jj < n_out) ? L.WT[(size_t)(t0 + tt) * n_out + j0 + jj] : 0.0;
     }
-    for (int e = threadIdx.x; e < tn; e += 2 * kFDN) {
-      const double a = xlo[t0 + e], b = xhi[t0 + e];
-      s_x[0][e] = a;
-      s_x[1][e] = b;
-      s_x[2][e] = smax(fabs(a), fabs(b));
-      s_x[3][e] = xrlo[t0 + e];
-      s_x[4][e] = xrhi[t0 + e];
+    {  // one input per thread (kFDT == 2 * kFDN)
+      const int e = threadIdx.x;
+      bool live = false;
+      if (e < tn) {
+        const double a = xlo[t0 + e], b = xhi[t0 + e], ra = xrlo[t0 + e], rb = xrhi[t0 + e];
+        s_x[0][e] = a;
+        s_x[1][e] = b;
+        s_x[2][e] = smax(fabs(a), fabs(b));
+        s_x[3][e] = ra;
+        s_x[4][e] = rb;
+        live = !skip_dead || !(a == 0.0 && b == 0.0 && ra == 0.0 && rb == 0.0);
+      }
+      const unsigned bl = __ballot_sync(0xFFFFFFFFu, live);
+      const unsigned bd = __ballot_sync(0xFFFFFFFFu, e < tn && !live);
+      if (lane == 0) {
+        s_cnt[0][track] = __popc(bl);
+        s_cnt[1][track] = __popc(bd);
+      }
+      __syncthreads();
+      const unsigned below = (1u << lane) - 1u;
+      if (e < tn) {
+        if (live) s_live[(track ? s_cnt[0][0] : 0) + __popc(bl & below)] = e;
+        else s_dead[(track ? s_cnt[1][0] : 0) + __popc(bd & below)] = e;
+      }
     }
     __syncthreads();
+    const int n_live = s_cnt[0][0] + s_cnt[0][1], n_dead = s_cnt[1][0] + s_cnt[1][1];
     if (track == 0) {
+      for (int i = 0; i < n_dead; ++i) terms += s_w[s_dead[i]][lane] != 0.0;
 #pragma unroll 4
-      for (int t = 0; t < tn; ++t)
+      for (int i = 0; i < n_live; ++i) {
+        const int t = s_live[i];
         pad_term<true>(s_w[t][lane], s_x[0][t], s_x[1][t], s_x[2][t], lo, hi, ab, terms, bad);
+      }
     } else {
 #pragma unroll 4
-      for (int t = 0; t < tn; ++t) raw_term<true>(s_w[t][lane], s_x[3][t], s_x[4][t], lo, hi, bad);
+      for (int i = 0; i < n_live; ++i) {
+        const int t = s_live[i];
+        raw_term<true>(s_w[t][lane], s_x[3][t], s_x[4][t], lo, hi, bad);
+      }
     }
   }
   if (act && bad) {  // out-of-band operand: redo this chain with the exact ops
