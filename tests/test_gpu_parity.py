@@ -119,6 +119,34 @@ def test_gain_scaled_mlp(pc, port):
         run_case(pc, port, net, x, 0.012, label=0)
 
 
+@pytest.mark.parametrize("width", [20, 120])
+def test_signed_zero_parameters(pc, port, width):
+    """-0 biases (an accumulator that starts at -0 must see every exact-zero
+    term, as the reference adds them) and +-0 weights next to stably-negative
+    inputs: the skipped-term shortcuts of the dense kernels stay exact."""
+    net = pc.generate(21, f"input 4x4x1; dense {width}; relu; dense {width}; relu; dense {width}; relu; dense 10")
+    for k, L in enumerate(net.layers):
+        if L.kind == "dense":
+            L.bias = L.bias.copy()
+            L.bias[::3] = -0.0
+            L.weights = L.weights.copy()
+            L.weights[:, 1::5] = 0.0
+            L.weights[:, 3::7] = -0.0
+    X = pc.random_inputs(22, 2, 16)
+    for x in X:
+        run_case(pc, port, net, x, 0.05, label=0)
+    v = pc.Verifier(net)
+    X = pc.random_inputs(23, 9, 16)
+    boxes = [pc.input_box(x, 0.05) for x in X]
+    lo, hi = np.stack([b.lo for b in boxes]), np.stack([b.hi for b in boxes])
+    labels = np.zeros(len(X), dtype=np.int32)
+    ver, mar, st, _ = v.test_batch(lo, hi, labels, concurrency=1)
+    for i in range(len(X)):
+        r = v.test(lo[i], hi[i], 0)
+        assert np.array_equal(r.margins.view(np.int64), mar[i].view(np.int64))
+        assert bool(ver[i]) == r.verified and st[i] == r.stats
+
+
 @pytest.mark.parametrize("name,n_img", [("mnist_6x100", 3), ("mnist_9x500", 1), ("cifar_convbig", 1)])
 def test_baseline_configs(pc, port, name, n_img):
     """BASELINE.json configs: generator weights seed 7, inputs seed 8,
