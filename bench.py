@@ -8,9 +8,10 @@ weights of the named architecture, gen.cpp) and generator inputs. Default
 workload: configs[1] = MNIST 9x500, eps 0.026, early termination on.
 
   value  device-resident inputs, per-step CUDA events around pc_net_test_batch
-         (128 images per step over 4 worker contexts, each verifying 32 images
+         (512 images per step over 8 worker contexts, each verifying 64 images
          per image-batched schedule), L2 flushed between steps (outside the events)
-  e2e    the C-ABI call with HOST buffers (pc_net_test): box H2D + margins D2H
+  e2e    the same batched C-ABI call with HOST buffers (pc_net_test_batch): box H2D +
+         margins D2H
          inside the timed region
   cpu_baseline / --impl reference: the unmodified reference (oracle/_ref,
          compiled from /root/reference) on the host's cores; falls back to the
@@ -39,6 +40,7 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+FP64_MADD_PEAK = 9.5e11  # interval madds/s, measured band-madd peak (ILP8)
 METRIC = "ms/image to verify (1/2/4/8 B200) + certified count == CPU ref; HBM GB/s"
 
 
@@ -52,8 +54,8 @@ def parse():
     ap.add_argument("--no-early-term", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch", type=int, default=128, help="images per step")
-    ap.add_argument("--concurrency", type=int, default=4, help="worker contexts per GPU (each verifies batch/concurrency images per schedule)")
+    ap.add_argument("--batch", type=int, default=512, help="images per step")
+    ap.add_argument("--concurrency", type=int, default=8, help="worker contexts per GPU (each verifies batch/concurrency images per schedule)")
     return ap.parse_args()
 
 
@@ -344,11 +346,13 @@ def main():
                      "ncu_capture": {"dram_bytes_per_launch": 2118400, "algorithmic_bytes_per_launch": 2142000,
                                      "rows": 9, "source": "profiles/r1_final_ncu_dense_coef.txt"},
                      # the kernel is FP64-pipe / chain-latency bound, not HBM bound: its
-                     # algorithmic interval multiply-adds per second against the measured
-                     # bit-exact-emulation peak (profiles/r1_microbench_chain_latency.txt)
+                     # executed interval multiply-adds per second (device-counted) against the
+                     # measured band-madd peak (profiles/r1_microbench_fp64_ops.txt)
                      "fp64": {"achieved_madds_per_s": dense_madds / (dense_ms / 1000.0) if dense_ms else 0.0,
-                              "peak_madds_per_s": 6.9e11,
-                              "frac": (dense_madds / (dense_ms / 1000.0) / 6.9e11) if dense_ms else 0.0}},
+                              "peak_madds_per_s": FP64_MADD_PEAK,
+                              "peak_source": "scripts/micro/fp64_ops.cu (register-resident band madd, ILP8, "
+                                             "profiles/r1_microbench_fp64_ops.txt)",
+                              "frac": (dense_madds / (dense_ms / 1000.0) / FP64_MADD_PEAK) if dense_ms else 0.0}},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -167,8 +167,9 @@ long long pc_last_launch_count(void);
  * back-substitution kernel (the roofline kernel) with its algorithmic bytes. */
 void pc_last_timing(double* total_ms, double* dense_kernel_ms, double* dense_kernel_bytes,
                     long long* dense_kernel_launches);
-/* Algorithmic interval multiply-adds of those dense-kernel launches (rows x
- * frame cells x predecessor cells, summed). */
+/* Interval multiply-adds the dense-kernel launches of the last call executed
+ * (rows x live predecessor cells x nonzero frame cells walked, summed over
+ * launches; device-counted, all worker contexts of a batch). */
 double pc_last_dense_madds(void);
 
 /* Per-kernel-class device time of this thread's last pc_net_test* call as a

@@ -1860,8 +1860,10 @@ pc_status test_impl(pc_net* net, const double* lo, const double* up, bool device
   g_dense_launches = 0;
   return guard([&] {
     ck(cudaSetDevice(net->device), "cudaSetDevice");
+    dense_useful_madds(true);
     CtxLease lease(net);
     run_one(lease.c, lo, up, device_box, label, verified, margins, b_lo, b_hi, r_lo, r_hi, stats);
+    g_dense_madds = (double)dense_useful_madds(false);
   });
 }
 
@@ -2104,6 +2106,7 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
   }
   return guard([&] {
     ck(cudaSetDevice(net->device), "cudaSetDevice");
+    dense_useful_madds(true);
     const int conc = std::max(1, std::min(concurrency > 0 ? concurrency : 8, std::max(n_images, 1)));
     const long long n0 = net->L[0].numel();
     const int nm = std::max(1, net->n_out - 1);
@@ -2135,7 +2138,7 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
     for (Ctx* c : ctxs) ck(cudaStreamWaitEvent(c->stream, start, 0), "wait");
     std::atomic<int> next{0};
     std::atomic<long long> launches{0};
-    double agg_dense_ms = 0, agg_dense_bytes = 0, agg_dense_madds = 0;
+    double agg_dense_ms = 0, agg_dense_bytes = 0;
     long long agg_dense_launches = 0;
     std::mutex err_mu;
     std::string err;
@@ -2184,7 +2187,6 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
             std::lock_guard<std::mutex> lk(err_mu);
             agg_dense_ms += dms;
             agg_dense_bytes += g_dense_bytes;
-            agg_dense_madds += g_dense_madds;
             agg_dense_launches += g_dense_launches;
           }
           const int nr = net->n_out - 1;
@@ -2263,9 +2265,9 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
     if (B > 1) {
       g_dense_ms = agg_dense_ms;
       g_dense_bytes = agg_dense_bytes;
-      g_dense_madds = agg_dense_madds;
       g_dense_launches = agg_dense_launches;
     }
+    g_dense_madds = (double)dense_useful_madds(false);  // executed, all workers
     if (err_code != PC_OK) throw StatusError(err_code, err);
   });
 }

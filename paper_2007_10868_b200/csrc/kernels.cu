@@ -1079,6 +1079,19 @@ void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, M
 // recomputed with the exact ops.
 constexpr int kDC = 128, kDK = 16;  // columns per block, frame cells per slab
 
+// Executed interval madds of the dense kernels (rows x live columns x the
+// nonzero cells walked), for the roofline report (dense_useful_madds()).
+__device__ unsigned long long g_dense_useful;
+unsigned long long dense_useful_madds(bool reset) {
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, g_dense_useful, sizeof(v));
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_dense_useful, &z, sizeof(z));
+  }
+  return v;
+}
+
 
 __device__ __forceinline__ void madd_fast(double w, double clo, double chi, double& lo, double& hi,
                                           bool& bad) {
@@ -1177,7 +1190,7 @@ __device__ DenseCols dense_live_cols(const RowsDev& rows, int nrows, int r0, int
 template <int TM, bool BAND>
 __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const double (*s_ah)[kDK],
                                            const double* w, int kn, double* lo, double* hi,
-                                           bool* bad) {
+                                           bool* bad, int& cells) {
   if constexpr (BAND && TM == 1) {
     // One row per thread: the add chain is the critical path. Form the slab's
     // outward-rounded products first (independent of the accumulators), then
@@ -1198,6 +1211,7 @@ __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const doub
       // a zero row coefficient adds the zero interval (skipped by the
       // reference's iv_acc): block-uniform skip, shortens the chain
       if (bits_zero(s_al[0][kk]) && bits_zero(s_ah[0][kk])) continue;
+      ++cells;
       const double sl = __dadd_rn(lo[0], pl[kk]), sh = __dadd_rn(hi[0], ph[kk]);
       const bool xl = __dadd_rd(lo[0], pl[kk]) == __dadd_ru(lo[0], pl[kk]);
       const bool xh = __dadd_rd(hi[0], ph[kk]) == __dadd_ru(hi[0], ph[kk]);
@@ -1225,10 +1239,12 @@ __device__ __forceinline__ void dense_slab(const double (*s_al)[kDK], const doub
               ((unsigned)__double2hiint(ch[u]) << 1) | (unsigned)__double2loint(ch[u]);
       }
       if (nz == 0u) continue;
+      ++cells;
 #pragma unroll
       for (int u = 0; u < TM; ++u) madd_band(w[kk], cl[u], ch[u], lo[u], hi[u]);
     }
   } else {
+  cells += kn;
 #pragma unroll
   for (int kk = 0; kk < kDK; ++kk) {
     if (kk >= kn) break;
@@ -1296,6 +1312,7 @@ __global__ void __launch_bounds__(kDC)
     bad[u] = false;
   }
   const int nslab = (n_k + kDK - 1) / kDK;
+  int cells = 0;  // cells walked (block-uniform)
   double w[kDK], wn[kDK];
   dense_stage<TM>(sm, 0, 0, n_k, r0, nrows, in, tx);
   dense_wload(w, W, 0, n_k, n_in, col);
@@ -1307,8 +1324,8 @@ __global__ void __launch_bounds__(kDC)
       dense_wload(wn, W, (sl + 1) * kDK, n_k, n_in, col);
     }
     const int b = sl & 1, kn = min(kDK, n_k - sl * kDK);
-    if (band) dense_slab<TM, true>(sm.al[b], sm.ah[b], w, kn, lo, hi, bad);
-    else dense_slab<TM, false>(sm.al[b], sm.ah[b], w, kn, lo, hi, bad);
+    if (band) dense_slab<TM, true>(sm.al[b], sm.ah[b], w, kn, lo, hi, bad, cells);
+    else dense_slab<TM, false>(sm.al[b], sm.ah[b], w, kn, lo, hi, bad, cells);
 #pragma unroll
     for (int kk = 0; kk < kDK; ++kk) w[kk] = wn[kk];
   }
@@ -1316,6 +1333,8 @@ __global__ void __launch_bounds__(kDC)
 #pragma unroll
     for (int u = 0; u < TM; ++u) lo[u] = canon0(lo[u]);
   }
+  if (tx == 0)
+    atomicAdd(&g_dense_useful, (unsigned long long)cells * dc.count * min(TM, nrows - r0));
   if (col >= n_in) return;
   MagAcc mag;
 #pragma unroll
@@ -1410,6 +1429,7 @@ __global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
     bad[u] = false;
   }
   const int nslab = (n_k + kDK - 1) / kDK;
+  int cells = 0;  // cells walked (warp-uniform; warp 0 reports)
 #pragma unroll
   for (int p = 0; p < kDStages - 1; ++p) {
     if (p < nslab) dense2_stage<TM>(sm, p, p * kDK, n_k, r0, nrows, in, W, n_in, col, tx);
@@ -1436,6 +1456,7 @@ __global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
         }
       }
       unsigned m = __ballot_sync(0xFFFFFFFFu, nz != 0u);
+      cells += __popc(m);
       while (m) {
         int ks[kDG];
 #pragma unroll
@@ -1460,6 +1481,7 @@ __global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
       }
     } else {
       const int kn = min(kDK, n_k - sl * kDK);
+      cells += kn;
       for (int kk = 0; kk < kn; ++kk) {
         const double wk = sm.w[b][kk][tx];
 #pragma unroll
@@ -1474,6 +1496,8 @@ __global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
 #pragma unroll
     for (int u = 0; u < TM; ++u) lo[u] = canon0(lo[u]);
   }
+  if (tx == 0)
+    atomicAdd(&g_dense_useful, (unsigned long long)cells * dc.count * min(TM, nrows - r0));
   if (col >= n_in) return;
   MagAcc mag;
 #pragma unroll

@@ -210,7 +210,7 @@ struct RowsDev {
   long long sst = 0;
   int nimg = 1;
 };
-constexpr int kMaxBatch = 64;  // images per batched walk
+constexpr int kMaxBatch = 128;  // images per batched walk
 
 // Resolve the block-row index b of a launch into logical row i of the rows
 // actually live (upper rows [0, R), lower rows [R, 2R)); false: no such row.
@@ -318,6 +318,8 @@ long long big_chain_cells();
 
 // relax: relaxations of the ReLU whose output is the frame after this step
 // (per image, strided by rows.sst), or nullptr: see dense_live_cols.
+// Executed dense madds since the last reset (device counter; synchronous).
+unsigned long long dense_useful_madds(bool reset);
 void launch_dense_coef(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
                        MatDev out, const double* relax, cudaEvent_t ev0, cudaEvent_t ev1);
 // Compacted nonzero coefficients of a conv step's input, per frame cell of

@@ -28,13 +28,13 @@ __global__ void ops(double* out, double seed, int n) {
 
 template <int ILP>
 __global__ void madd(double* out, double seed, int n) {
-  double lo[ILP], hi[ILP], c[4];
+  double lo[ILP], hi[ILP], c[ILP + 1];
   for (int u = 0; u < ILP; ++u) lo[u] = hi[u] = 0.0;
-  for (int u = 0; u < 4; ++u) c[u] = seed * (threadIdx.x % 7 + u + 1);
+  for (int u = 0; u <= ILP; ++u) c[u] = seed * (threadIdx.x % 7 + u + 1) * (u & 1 ? -1 : 1);
   double w = seed * 0.3;
   for (int i = 0; i < n; ++i) {
 #pragma unroll
-    for (int u = 0; u < ILP; ++u) madd_band(w, c[u & 3], c[(u + 1) & 3], lo[u], hi[u]);
+    for (int u = 0; u < ILP; ++u) madd_band(w, fmin(c[u], c[u + 1]), fmax(c[u], c[u + 1]), lo[u], hi[u]);
     w = __dmul_rn(w, -1.0000000001);
   }
   double s = 0;
