@@ -1129,12 +1129,12 @@ struct DenseCols {
   int count;  // live columns of this block
 };
 
-template <int TM>
+template <int TM, int NC = kDC>
 __device__ DenseCols dense_live_cols(const RowsDev& rows, int nrows, int r0, int n_in,
                                      const double* relax, MatDev out, int* s_cols, int* s_warp) {
   const int tx = threadIdx.x, lane = tx & 31, wid = tx >> 5;
-  const int x0 = blockIdx.x * kDC;
-  if (!relax) return DenseCols{x0 + tx, min(kDC, n_in - x0)};
+  const int x0 = blockIdx.x * NC;
+  if (!relax) return DenseCols{x0 + tx, min(NC, n_in - x0)};
   const double* rx[TM];
 #pragma unroll
   for (int u = 0; u < TM; ++u) {
@@ -1147,7 +1147,7 @@ __device__ DenseCols dense_live_cols(const RowsDev& rows, int nrows, int r0, int
     }
   }
   int base = 0;
-  for (int t0 = 0; t0 < n_in; t0 += kDC) {
+  for (int t0 = 0; t0 < n_in; t0 += NC) {
     const int t = t0 + tx;
     bool live = false;
     if (t < n_in) {
@@ -1165,14 +1165,14 @@ __device__ DenseCols dense_live_cols(const RowsDev& rows, int nrows, int r0, int
     __syncthreads();
     int before = base, total = 0;
 #pragma unroll
-    for (int w2 = 0; w2 < kDC / 32; ++w2) {
+    for (int w2 = 0; w2 < NC / 32; ++w2) {
       const int c = s_warp[w2];
       if (w2 < wid) before += c;
       total += c;
     }
     const int pos = before + __popc(b & ((1u << lane) - 1u));
-    if (live && pos >= x0 && pos < x0 + kDC) s_cols[pos - x0] = t;
-    if (!live && t >= x0 && t < x0 + kDC && t < n_in) {
+    if (live && pos >= x0 && pos < x0 + NC) s_cols[pos - x0] = t;
+    if (!live && t >= x0 && t < x0 + NC && t < n_in) {
 #pragma unroll
       for (int u = 0; u < TM; ++u) {
         if (r0 + u >= nrows) continue;
@@ -1183,7 +1183,7 @@ __device__ DenseCols dense_live_cols(const RowsDev& rows, int nrows, int r0, int
     base += total;
   }
   __syncthreads();
-  const int count = max(0, min(kDC, base - x0));
+  const int count = max(0, min(NC, base - x0));
   return DenseCols{tx < count ? s_cols[tx] : n_in, count};
 }
 
@@ -1364,24 +1364,34 @@ __global__ void __launch_bounds__(kDC)
 // (an exact +-0 term). A group is one branch-free block of kDG x TM
 // independent madds, so the products of later cells overlap the accumulator
 // chains of earlier ones.
-constexpr int kDG = 4;
+#ifndef PC_DENSE2_DG
+#define PC_DENSE2_DG 4
+#endif
+#ifndef PC_DENSE2_DK
+#define PC_DENSE2_DK 32
+#endif
+#ifndef PC_DENSE2_STAGES
+#define PC_DENSE2_STAGES 2
+#endif
+constexpr int kDG = PC_DENSE2_DG;   // cells per branch-free group
+constexpr int kDK2 = PC_DENSE2_DK;  // cells per slab (<= 32: one ballot)
 #ifndef PC_DENSE2_MINB
 #define PC_DENSE2_MINB 3  // resident blocks the register budget is sized for
 #endif
-constexpr int kDStages = 2;
+constexpr int kDStages = PC_DENSE2_STAGES;
 
-template <int TM>
+template <int TM, int NC>
 struct DenseSmem2 {
-  double2 c[kDStages][kDK + 1][TM];  // (lo, hi); cell kDK stays zero
-  double w[kDStages][kDK + 1][kDC];  // weight slab; cell kDK stays zero
+  double2 c[kDStages][kDK2 + 1][TM];  // (lo, hi); cell kDK2 stays zero
+  double w[kDStages][kDK2 + 1][NC];  // weight slab; cell kDK2 stays zero
 };
 
-template <int TM>
-__device__ __forceinline__ void dense2_stage(DenseSmem2<TM>& sm, int b, int k0, int n_k, int r0,
+template <int TM, int NC>
+__device__ __forceinline__ void dense2_stage(DenseSmem2<TM, NC>& sm, int b, int k0, int n_k, int r0,
                                              int nrows, const MatDev& in,
                                              const double* __restrict__ W, int n_in, int col,
                                              int tx) {
-  for (int e = tx; e < TM * kDK; e += kDC) {
+  for (int e = tx; e < TM * kDK2; e += NC) {
     const int kk = e / TM, rr = e % TM;
     const int r = r0 + rr, k = k0 + kk;
     const bool ok = r < nrows && k < n_k;
@@ -1390,20 +1400,20 @@ __device__ __forceinline__ void dense2_stage(DenseSmem2<TM>& sm, int b, int k0, 
     cp_async8(&sm.c[b][kk][rr].y, in.hi + o, ok);
   }
 #pragma unroll 4
-  for (int kk = 0; kk < kDK; ++kk) {
+  for (int kk = 0; kk < kDK2; ++kk) {
     const int k = k0 + kk;
     const bool ok = k < n_k && col < n_in;
     cp_async8(&sm.w[b][kk][tx], ok ? W + (size_t)k * n_in + col : W, ok);
   }
 }
 
-template <int TM>
-__global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
+template <int TM, int NC>
+__global__ void __launch_bounds__(NC, PC_DENSE2_MINB * (kDC / NC))
     k_dense_coef2(const double* __restrict__ W, int n_k, int n_in, RowsDev rows, MatDev in,
                   MatDev out, double wmin, double wmax, const double* relax) {
   extern __shared__ __align__(16) unsigned char dense2_raw[];
-  DenseSmem2<TM>& sm = *reinterpret_cast<DenseSmem2<TM>*>(dense2_raw);
-  __shared__ int s_cols[kDC], s_warp[kDC / 32];
+  DenseSmem2<TM, NC>& sm = *reinterpret_cast<DenseSmem2<TM, NC>*>(dense2_raw);
+  __shared__ int s_cols[NC], s_warp[NC / 32];
   const int tx = threadIdx.x, lane = tx & 31;
   const int r0 = blockIdx.y * TM;
   int i0;
@@ -1411,15 +1421,15 @@ __global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
   const int nrows = rows.n;
   if (r0 >= nrows) return;
   const bool band = products_in_band(in.stat, wmin, wmax);
-  const DenseCols dc = dense_live_cols<TM>(rows, nrows, r0, n_in, band ? relax : nullptr, out,
+  const DenseCols dc = dense_live_cols<TM, NC>(rows, nrows, r0, n_in, band ? relax : nullptr, out,
                                            s_cols, s_warp);
   if (dc.count <= 0) return;
   const int col = dc.col;
   // warps with no live column skip the arithmetic (they still stage and sync)
   const bool warp_live = (tx & ~31) < dc.count;
   for (int b = 0; b < kDStages; ++b) {
-    if (tx < TM) sm.c[b][kDK][tx] = make_double2(0.0, 0.0);
-    sm.w[b][kDK][tx] = 0.0;
+    if (tx < TM) sm.c[b][kDK2][tx] = make_double2(0.0, 0.0);
+    sm.w[b][kDK2][tx] = 0.0;
   }
   double lo[TM], hi[TM];
   bool bad[TM];
@@ -1428,26 +1438,26 @@ __global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
     lo[u] = hi[u] = 0.0;
     bad[u] = false;
   }
-  const int nslab = (n_k + kDK - 1) / kDK;
+  const int nslab = (n_k + kDK2 - 1) / kDK2;
   int cells = 0;  // cells walked (warp-uniform; warp 0 reports)
 #pragma unroll
   for (int p = 0; p < kDStages - 1; ++p) {
-    if (p < nslab) dense2_stage<TM>(sm, p, p * kDK, n_k, r0, nrows, in, W, n_in, col, tx);
+    if (p < nslab) dense2_stage<TM, NC>(sm, p, p * kDK2, n_k, r0, nrows, in, W, n_in, col, tx);
     cp_async_commit();
   }
   for (int sl = 0; sl < nslab; ++sl) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(kDStages - 2));
     __syncthreads();  // slab sl landed everywhere; slab sl-1's buffer is free
     if (sl + kDStages - 1 < nslab)
-      dense2_stage<TM>(sm, (sl + kDStages - 1) % kDStages, (sl + kDStages - 1) * kDK, n_k, r0,
+      dense2_stage<TM, NC>(sm, (sl + kDStages - 1) % kDStages, (sl + kDStages - 1) * kDK2, n_k, r0,
                        nrows, in, W, n_in, col, tx);
     cp_async_commit();
     const int b = sl % kDStages;
     if (!warp_live) continue;
     if (band) {
-      // lane kk < kDK: is cell kk nonzero in any row of the block?
+      // lane kk < kDK2: is cell kk nonzero in any row of the block?
       unsigned nz = 0u;
-      if (lane < kDK) {
+      if (lane < kDK2) {
 #pragma unroll
         for (int u = 0; u < TM; ++u) {
           const double2 v = sm.c[b][lane][u];
@@ -1461,18 +1471,20 @@ __global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
         int ks[kDG];
 #pragma unroll
         for (int g = 0; g < kDG; ++g) {
-          ks[g] = m ? __ffs(m) - 1 : kDK;
+          ks[g] = m ? __ffs(m) - 1 : kDK2;
           m &= m - 1;
         }
         double pl[kDG][TM], ph[kDG][TM];
 #pragma unroll
         for (int g = 0; g < kDG; ++g) {
           const double wk = sm.w[b][ks[g]][tx];
+          // the factor of each bound is chosen by the weight's sign through
+          // the load address (lo, hi) -> (hi, lo) instead of by selects
+          const int sa = __double2hiint(wk) < 0;
+          const double* cg = &sm.c[b][ks[g]][0].x;
 #pragma unroll
-          for (int u = 0; u < TM; ++u) {
-            const double2 c = sm.c[b][ks[g]][u];
-            band_products(wk, c.x, c.y, pl[g][u], ph[g][u]);
-          }
+          for (int u = 0; u < TM; ++u)
+            band_products_ab(wk, cg[2 * u + sa], cg[2 * u + 1 - sa], pl[g][u], ph[g][u]);
         }
 #pragma unroll
         for (int g = 0; g < kDG; ++g)
@@ -1480,7 +1492,7 @@ __global__ void __launch_bounds__(kDC, PC_DENSE2_MINB)
           for (int u = 0; u < TM; ++u) band_sums(pl[g][u], ph[g][u], lo[u], hi[u]);
       }
     } else {
-      const int kn = min(kDK, n_k - sl * kDK);
+      const int kn = min(kDK2, n_k - sl * kDK2);
       cells += kn;
       for (int kk = 0; kk < kn; ++kk) {
         const double wk = sm.w[b][kk][tx];
@@ -1533,14 +1545,17 @@ static int g_dense_live = 1;  // PC_DENSE_LIVE: skip columns of stably-negative 
 template <int TM>
 static void dense_launch(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
                          MatDev out, int n_k, int n_in, const double* relax) {
-  dim3 grid(cdiv(n_in, kDC), cdiv(rows.n, TM));
   if constexpr (TM > 1) {
     if (g_dense_v2) {
-      k_dense_coef2<TM><<<grid, kDC, sizeof(DenseSmem2<TM>), s>>>(L.W, n_k, n_in, rows, in, out,
-                                                                   L.wmin, L.wmax, relax);
+      // TM = 8: half-width blocks, so the launch keeps as many blocks as TM = 4
+      constexpr int NC = TM >= 8 ? 64 : kDC;
+      dim3 grid(cdiv(n_in, NC), cdiv(rows.n, TM));
+      k_dense_coef2<TM, NC><<<grid, NC, sizeof(DenseSmem2<TM, NC>), s>>>(
+          L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax, relax);
       return;
     }
   }
+  dim3 grid(cdiv(n_in, kDC), cdiv(rows.n, TM));
   k_dense_coef<TM><<<grid, kDC, 0, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax, relax);
 }
 
@@ -2515,9 +2530,9 @@ void init_kernel_attrs_kernels() {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    auto slots = [&](auto k, int tm, size_t smem) {
+    auto slots = [&](auto k, int tm, size_t smem, int nc = kDC) {
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kDC, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, nc, smem);
       g_dense_slots[tm] = b * sms;
     };
     g_dense_v2 = env_int("PC_DENSE_V2", 1);
@@ -2526,14 +2541,16 @@ void init_kernel_attrs_kernels() {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
       carve(k);
     };
-    big(k_dense_coef2<2>, sizeof(DenseSmem2<2>)); big(k_dense_coef2<3>, sizeof(DenseSmem2<3>));
-    big(k_dense_coef2<4>, sizeof(DenseSmem2<4>)); big(k_dense_coef2<8>, sizeof(DenseSmem2<8>));
+    big(k_dense_coef2<2, kDC>, sizeof(DenseSmem2<2, kDC>));
+    big(k_dense_coef2<3, kDC>, sizeof(DenseSmem2<3, kDC>));
+    big(k_dense_coef2<4, kDC>, sizeof(DenseSmem2<4, kDC>));
+    big(k_dense_coef2<8, 64>, sizeof(DenseSmem2<8, 64>));
     slots(k_dense_coef<1>, 1, 0);
     if (g_dense_v2) {
-      slots(k_dense_coef2<2>, 2, sizeof(DenseSmem2<2>));
-      slots(k_dense_coef2<3>, 3, sizeof(DenseSmem2<3>));
-      slots(k_dense_coef2<4>, 4, sizeof(DenseSmem2<4>));
-      slots(k_dense_coef2<8>, 8, sizeof(DenseSmem2<8>));
+      slots(k_dense_coef2<2, kDC>, 2, sizeof(DenseSmem2<2, kDC>));
+      slots(k_dense_coef2<3, kDC>, 3, sizeof(DenseSmem2<3, kDC>));
+      slots(k_dense_coef2<4, kDC>, 4, sizeof(DenseSmem2<4, kDC>));
+      slots(k_dense_coef2<8, 64>, 8, sizeof(DenseSmem2<8, 64>), 64);
     } else {
       slots(k_dense_coef<2>, 2, 0); slots(k_dense_coef<3>, 3, 0);
       slots(k_dense_coef<4>, 4, 0); slots(k_dense_coef<8>, 8, 0);

@@ -156,6 +156,14 @@ __device__ __forceinline__ void band_products(double w, double cl, double ch, do
   pl = __dadd_rd(pl0, -fabs(__fma_rn(a, w, -pl0)));
   ph = __dadd_ru(ph0, fabs(__fma_rn(b, w, -ph0)));
 }
+// band_products with the factors already ordered by the weight's sign
+// (a multiplies into the lower bound, b into the upper).
+__device__ __forceinline__ void band_products_ab(double w, double a, double b, double& pl,
+                                                 double& ph) {
+  const double pl0 = __dmul_rn(a, w), ph0 = __dmul_rn(b, w);
+  pl = __dadd_rd(pl0, -fabs(__fma_rn(a, w, -pl0)));
+  ph = __dadd_ru(ph0, fabs(__fma_rn(b, w, -ph0)));
+}
 __device__ __forceinline__ void band_sums(double pl, double ph, double& lo, double& hi) {
   const double sl = __dadd_rn(lo, pl), dl = __dadd_rd(lo, pl), ul = __dadd_ru(lo, pl);
   const double sh = __dadd_rn(hi, ph), dh = __dadd_rd(hi, ph), uh = __dadd_ru(hi, ph);
