@@ -1370,6 +1370,9 @@ __global__ void __launch_bounds__(kDC)
 #ifndef PC_DENSE2_DK
 #define PC_DENSE2_DK 32
 #endif
+#ifndef PC_DENSE2_LATSUM
+#define PC_DENSE2_LATSUM 0
+#endif
 #ifndef PC_DENSE2_STAGES
 #define PC_DENSE2_STAGES 2
 #endif
@@ -1399,11 +1402,19 @@ __device__ __forceinline__ void dense2_stage(DenseSmem2<TM, NC>& sm, int b, int 
     cp_async8(&sm.c[b][kk][rr].x, in.lo + o, ok);
     cp_async8(&sm.c[b][kk][rr].y, in.hi + o, ok);
   }
-#pragma unroll 4
-  for (int kk = 0; kk < kDK2; ++kk) {
-    const int k = k0 + kk;
-    const bool ok = k < n_k && col < n_in;
-    cp_async8(&sm.w[b][kk][tx], ok ? W + (size_t)k * n_in + col : W, ok);
+  // weight slab: this thread's column of rows k0.., one pointer step per cell
+  const int kn = min(kDK2, n_k - k0);
+  const double* p = W + (size_t)k0 * n_in + (col < n_in ? col : 0);
+  const unsigned s0 = (unsigned)__cvta_generic_to_shared(&sm.w[b][0][tx]);
+  if (col < n_in && kn == kDK2) {
+#pragma unroll 8
+    for (int kk = 0; kk < kDK2; ++kk, p += n_in)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s0 + kk * NC * 8), "l"(p));
+  } else {
+    for (int kk = 0; kk < kDK2; ++kk, p += n_in) {
+      const bool ok = col < n_in && kk < kn;
+      cp_async8(&sm.w[b][kk][tx], ok ? p : W, ok);
+    }
   }
 }
 
@@ -1489,7 +1500,13 @@ __global__ void __launch_bounds__(NC, PC_DENSE2_MINB * (kDC / NC))
 #pragma unroll
         for (int g = 0; g < kDG; ++g)
 #pragma unroll
-          for (int u = 0; u < TM; ++u) band_sums(pl[g][u], ph[g][u], lo[u], hi[u]);
+          for (int u = 0; u < TM; ++u) {
+#if PC_DENSE2_LATSUM
+            band_sums_lat(pl[g][u], ph[g][u], lo[u], hi[u]);
+#else
+            band_sums(pl[g][u], ph[g][u], lo[u], hi[u]);
+#endif
+          }
       }
     } else {
       const int kn = min(kDK2, n_k - sl * kDK2);
