@@ -120,6 +120,23 @@ def test_gain_scaled_mlp(pc, port):
 
 
 @pytest.mark.parametrize("width", [20, 120])
+def test_out_of_band_magnitudes(pc, port, width):
+    """Layers scaled by 2^-560 / 2^+560: products leave [2^-499, 2^999], so the
+    forward and back-substitution kernels must take their checked paths (the
+    reference's 2^-500 residual floor, subnormal sums) and stay bit-exact."""
+    net = pc.generate(31, f"input 4x4x1; dense {width}; relu; dense {width}; relu; dense {width}; relu; dense 10")
+    scales = iter([1.0, 2.0 ** -560, 2.0 ** 560, 1.0])
+    for L in net.layers:
+        if L.kind == "dense":
+            f = next(scales)
+            L.weights = L.weights * f
+            L.bias = L.bias * f
+    X = pc.random_inputs(32, 2, 16)
+    for x in X:
+        run_case(pc, port, net, x, 0.05, label=0)
+
+
+@pytest.mark.parametrize("width", [20, 120])
 def test_signed_zero_parameters(pc, port, width):
     """-0 biases (an accumulator that starts at -0 must see every exact-zero
     term, as the reference adds them) and +-0 weights next to stably-negative
