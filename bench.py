@@ -278,13 +278,17 @@ def main():
         r = v.test(boxes[i].lo, boxes[i].hi, int(labels_all[i]))
         if i:
             lat.append(v.last_timing()["total_ms"])
-    # the roofline kernel's live timing inside the measured workload: one more
-    # step of the batched run, CUDA events around every dense launch on the
-    # stream it is launched on
+    # the roofline kernel's timing on the measured workload: one image-batched
+    # schedule of the step (batch / concurrency images) on a single worker
+    # context, CUDA events around every dense launch on the stream it is
+    # launched on (in the concurrent step the other contexts' kernels share the
+    # SMs and would inflate each launch's event time)
     flush.fill_(7)
     torch.cuda.synchronize()
     dlo, dhi, lab = dev_batches[0]
-    v.test_batch(dlo.data_ptr(), dhi.data_ptr(), lab, args.concurrency, device_inputs=True)
+    per_walk = max(1, per_step // args.concurrency)
+    v.test_batch(dlo[:per_walk].data_ptr(), dhi[:per_walk].data_ptr(), lab[:per_walk], 1,
+                 device_inputs=True)
     t = v.last_timing()
     dense_ms, dense_bytes = t["dense_ms"], t["dense_bytes"]
     dense_n, dense_madds = t["dense_launches"], t["dense_madds"]
@@ -337,14 +341,18 @@ def main():
         "gpu_launches": int(launches),
         "roofline": {"kernel": "k_dense_coef (dense back-substitution)", "bound": "hbm",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                     "frac": achieved / hbm_peak if hbm_peak else None,
+                     # DRAM read+write of one captured launch (ncu --set full, below)
+                     "traffic": 8722176 + 256,
                      "launches": dense_n, "kernel_ms": dense_ms,
+                     "sample": f"one {per_walk}-image schedule of the step on one worker context",
                      "algorithmic_bytes": dense_bytes,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                      # one ncu --set full capture of this kernel (profiles/r1_final_ncu_dense_coef.txt):
-                     # a 9-row launch read 2.118 MB of DRAM for 2.142 MB algorithmic bytes
-                     "ncu_capture": {"dram_bytes_per_launch": 2118400, "algorithmic_bytes_per_launch": 2142000,
-                                     "rows": 9, "source": "profiles/r1_final_ncu_dense_coef.txt"},
+                     # a 576-row launch (one 64-image schedule, 500x500 layer) moved 8.72 MB of DRAM
+                     # for 11.2 MB algorithmic bytes (rows in/out + weights once; L2 serves the rest)
+                     "ncu_capture": {"dram_bytes_per_launch": 8722432, "algorithmic_bytes_per_launch": 11216000,
+                                     "rows": 576, "source": "profiles/r1_final_ncu_dense_coef.txt"},
                      # the kernel is FP64-pipe / chain-latency bound, not HBM bound: its
                      # executed interval multiply-adds per second (device-counted) against the
                      # measured band-madd peak (profiles/r1_microbench_fp64_ops.txt)
