@@ -102,6 +102,7 @@ struct ReluGen {
     const Iv beta{R[2], R[3]}, delta{R[6], R[7]};
     const Iv op = upper ? delta : beta;
     const Iv on = upper ? beta : delta;
+    if (iv_zero(op) && iv_zero(on)) return false;  // stable neuron: exact zero terms
     Iv o0, o1{0.0, 0.0};
     if (!(c.lo < 0.0)) o0 = iv_mul(c, op);
     else if (!(c.hi > 0.0)) o0 = iv_mul(c, on);

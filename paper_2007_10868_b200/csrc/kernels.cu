@@ -223,6 +223,33 @@ __device__ __forceinline__ void raw_term(double w, double a, double b, double& l
   }
 }
 
+// In-band forms of pad_term / raw_term (see madd_band): valid when every
+// nonzero product is in [2^-499, 2^999] (checked per block from the input
+// bounds' magnitudes and the layer's weight range) and no accumulator starts
+// at -0. A zero weight or bound gives exact +-0 products, which leave the
+// accumulators unchanged up to a -0 lower bound (canonicalised at the end),
+// so only the term count needs the w != 0 test.
+__device__ __forceinline__ void band_pad_term(double w, double a, double b, double m, double& lo,
+                                              double& hi, double& ab, long long& terms) {
+  const bool neg = __double2hiint(w) < 0;
+  double pl, ph;
+  band_products_ab(w, neg ? b : a, neg ? a : b, pl, ph);
+  const double aw = fabs(w);
+  const double p0 = __dmul_rn(aw, m);
+  const double pa = __dadd_ru(p0, fabs(__fma_rn(aw, m, -p0)));
+  band_sums(pl, ph, lo, hi);
+  const double sa = __dadd_rn(ab, pa), da = __dadd_rd(ab, pa), ua = __dadd_ru(ab, pa);
+  ab = __fma_ru(__dsub_rn(ua, da), 0.5, sa);
+  terms += w != 0.0;
+}
+__device__ __forceinline__ void band_raw_term(double w, double a, double b, double& lo,
+                                              double& hi) {
+  const bool neg = __double2hiint(w) < 0;
+  double pl, ph;
+  band_products_ab(w, neg ? b : a, neg ? a : b, pl, ph);
+  band_sums(pl, ph, lo, hi);
+}
+
 __global__ void __launch_bounds__(2 * kFDN)
     k_fwd_dense(LayerDev L, int layer, const double* xlo, const double* xhi, const double* xrlo,
                 const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi,
@@ -247,7 +274,27 @@ __global__ void __launch_bounds__(2 * kFDN)
   // still -0, which only a -0 bias can start (RN sums of nonzero terms never
   // return to -0). They only count as terms (w != 0); blocks with a -0 bias
   // run every input.
-  const bool skip_dead = !__syncthreads_or(act && __double_as_longlong(bias) == (long long)0x8000000000000000ULL);
+  const bool neg0_bias = __syncthreads_or(act && __double_as_longlong(bias) == (long long)0x8000000000000000ULL);
+  const bool skip_dead = !neg0_bias;
+  // Band check for the lean forms: magnitudes of the nonzero input bounds
+  // (padded and raw) against the layer's weight range, and the biases.
+  bool band;
+  {
+    MagAcc mag;
+    for (int t = threadIdx.x; t < n_in; t += 2 * kFDN) {
+      mag.add(xlo[t]);
+      mag.add(xhi[t]);
+      mag.add(xrlo[t]);
+      mag.add(xrhi[t]);
+    }
+    __shared__ unsigned s_stat[2];
+    if (threadIdx.x == 0) s_stat[0] = s_stat[1] = 0xFFFFFFFFu;
+    __syncthreads();
+    mag.flush_shared(s_stat);
+    __syncthreads();
+    band = !neg0_bias && n_in < (1 << 20) && products_in_band(s_stat, L.wmin, L.wmax) &&
+           !__syncthreads_or(act && !(fabs(bias) <= 0x1p999));
+  }
   for (int t0 = 0; t0 < n_in; t0 += kFDT) {
     const int tn = min(kFDT, n_in - t0);
     __syncthreads();
@@ -284,19 +331,36 @@ __global__ void __launch_bounds__(2 * kFDN)
     const int n_live = s_cnt[0][0] + s_cnt[0][1], n_dead = s_cnt[1][0] + s_cnt[1][1];
     if (track == 0) {
       for (int i = 0; i < n_dead; ++i) terms += s_w[s_dead[i]][lane] != 0.0;
+      if (band) {
 #pragma unroll 4
-      for (int i = 0; i < n_live; ++i) {
-        const int t = s_live[i];
-        pad_term<true>(s_w[t][lane], s_x[0][t], s_x[1][t], s_x[2][t], lo, hi, ab, terms, bad);
+        for (int i = 0; i < n_live; ++i) {
+          const int t = s_live[i];
+          band_pad_term(s_w[t][lane], s_x[0][t], s_x[1][t], s_x[2][t], lo, hi, ab, terms);
+        }
+      } else {
+#pragma unroll 4
+        for (int i = 0; i < n_live; ++i) {
+          const int t = s_live[i];
+          pad_term<true>(s_w[t][lane], s_x[0][t], s_x[1][t], s_x[2][t], lo, hi, ab, terms, bad);
+        }
       }
     } else {
+      if (band) {
 #pragma unroll 4
-      for (int i = 0; i < n_live; ++i) {
-        const int t = s_live[i];
-        raw_term<true>(s_w[t][lane], s_x[3][t], s_x[4][t], lo, hi, bad);
+        for (int i = 0; i < n_live; ++i) {
+          const int t = s_live[i];
+          band_raw_term(s_w[t][lane], s_x[3][t], s_x[4][t], lo, hi);
+        }
+      } else {
+#pragma unroll 4
+        for (int i = 0; i < n_live; ++i) {
+          const int t = s_live[i];
+          raw_term<true>(s_w[t][lane], s_x[3][t], s_x[4][t], lo, hi, bad);
+        }
       }
     }
   }
+  if (band) lo = canon0(lo);  // the reference's accumulators are never -0 here
   if (act && bad) {  // out-of-band operand: redo this chain with the exact ops
     lo = hi = bias;
     ab = fabs(bias);
@@ -894,8 +958,10 @@ __device__ __forceinline__ bool chain_relu_row(const FrameDev& f, int bw, int bh
         const Iv beta{R[2], R[3]}, delta{R[6], R[7]};
         const Iv op = upper ? delta : beta;
         const Iv on = upper ? beta : delta;
-        Iv o0, o1{0.0, 0.0};
-        if (!(c.lo < 0.0)) o0 = FAST ? f_iv_mul(c, op, bad) : iv_mul(c, op);
+        Iv o0{0.0, 0.0}, o1{0.0, 0.0};
+        // stable neurons have zero offsets: every product is an exact zero
+        if (iv_zero(op) && iv_zero(on)) {
+        } else if (!(c.lo < 0.0)) o0 = FAST ? f_iv_mul(c, op, bad) : iv_mul(c, op);
         else if (!(c.hi > 0.0)) o0 = FAST ? f_iv_mul(c, on, bad) : iv_mul(c, on);
         else {
           o0 = FAST ? f_iv_mul(iv_pos_part(c), op, bad) : iv_mul(iv_pos_part(c), op);
@@ -1355,23 +1421,19 @@ __global__ void __launch_bounds__(kDC)
   mag.flush(out.stat);
 }
 
-// Many rows (image batches): TM rows x 128 columns per block, with the
-// layer's weight slab staged in shared memory next to the row slab (3-stage
-// cp.async ring, so no weight registers are held across slabs), and the
-// cells of a slab that are zero in every row of the block dropped before the
-// arithmetic: each warp ballots the slab's nonzero cells and walks them in
-// ascending order in groups of kDG, padding the last group with a zero cell
-// (an exact +-0 term). A group is one branch-free block of kDG x TM
-// independent madds, so the products of later cells overlap the accumulator
-// chains of earlier ones.
+// Many rows (image batches): TM rows x NC columns per block (the block's live
+// columns, dense_live_cols), with the layer's weight slab staged in shared
+// memory next to the row slab (2-stage cp.async ring, so no weight registers
+// are held across slabs), and the cells of a slab that are zero in every row
+// of the block dropped before the arithmetic: each warp ballots the slab's
+// nonzero cells and walks them in ascending order in groups of kDG (then 2,
+// then 1). A group is one branch-free block of G x TM independent products
+// followed by the 2*TM accumulator chains.
 #ifndef PC_DENSE2_DG
 #define PC_DENSE2_DG 4
 #endif
 #ifndef PC_DENSE2_DK
 #define PC_DENSE2_DK 32
-#endif
-#ifndef PC_DENSE2_LATSUM
-#define PC_DENSE2_LATSUM 0
 #endif
 #ifndef PC_DENSE2_STAGES
 #define PC_DENSE2_STAGES 2
@@ -1416,6 +1478,35 @@ __device__ __forceinline__ void dense2_stage(DenseSmem2<TM, NC>& sm, int b, int 
       cp_async8(&sm.w[b][kk][tx], ok ? p : W, ok);
     }
   }
+}
+
+// G cells of a slab (the next G set bits of m, ascending) x TM rows: all
+// products first (independent of the accumulators), then the 2*TM chains.
+template <int G, int TM, int NC>
+__device__ __forceinline__ void dense2_group(const DenseSmem2<TM, NC>& sm, int b, int tx,
+                                             unsigned& m, double* lo, double* hi) {
+  int ks[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    ks[g] = __ffs(m) - 1;
+    m &= m - 1;
+  }
+  double pl[G][TM], ph[G][TM];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const double wk = sm.w[b][ks[g]][tx];
+    // the factor of each bound is chosen by the weight's sign through the
+    // load address, (lo, hi) -> (hi, lo), instead of by selects
+    const int sa = __double2hiint(wk) < 0;
+    const double* cg = &sm.c[b][ks[g]][0].x;
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+      band_products_ab(wk, cg[2 * u + sa], cg[2 * u + 1 - sa], pl[g][u], ph[g][u]);
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int u = 0; u < TM; ++u) band_sums(pl[g][u], ph[g][u], lo[u], hi[u]);
 }
 
 template <int TM, int NC>
@@ -1478,36 +1569,14 @@ __global__ void __launch_bounds__(NC, PC_DENSE2_MINB * (kDC / NC))
       }
       unsigned m = __ballot_sync(0xFFFFFFFFu, nz != 0u);
       cells += __popc(m);
-      while (m) {
-        int ks[kDG];
-#pragma unroll
-        for (int g = 0; g < kDG; ++g) {
-          ks[g] = m ? __ffs(m) - 1 : kDK2;
-          m &= m - 1;
-        }
-        double pl[kDG][TM], ph[kDG][TM];
-#pragma unroll
-        for (int g = 0; g < kDG; ++g) {
-          const double wk = sm.w[b][ks[g]][tx];
-          // the factor of each bound is chosen by the weight's sign through
-          // the load address (lo, hi) -> (hi, lo) instead of by selects
-          const int sa = __double2hiint(wk) < 0;
-          const double* cg = &sm.c[b][ks[g]][0].x;
-#pragma unroll
-          for (int u = 0; u < TM; ++u)
-            band_products_ab(wk, cg[2 * u + sa], cg[2 * u + 1 - sa], pl[g][u], ph[g][u]);
-        }
-#pragma unroll
-        for (int g = 0; g < kDG; ++g)
-#pragma unroll
-          for (int u = 0; u < TM; ++u) {
-#if PC_DENSE2_LATSUM
-            band_sums_lat(pl[g][u], ph[g][u], lo[u], hi[u]);
-#else
-            band_sums(pl[g][u], ph[g][u], lo[u], hi[u]);
-#endif
-          }
+      // groups of kDG cells, then one of 2 and one of 1: no padding work
+      int left = __popc(m);
+      for (; left >= kDG; left -= kDG) dense2_group<kDG, TM, NC>(sm, b, tx, m, lo, hi);
+      if (left >= 2) {
+        dense2_group<2, TM, NC>(sm, b, tx, m, lo, hi);
+        left -= 2;
       }
+      if (left) dense2_group<1, TM, NC>(sm, b, tx, m, lo, hi);
     } else {
       const int kn = min(kDK2, n_k - sl * kDK2);
       cells += kn;
@@ -2244,11 +2313,21 @@ __global__ void __launch_bounds__(256)
       const long long j = ((long long)(bh + y) * f.G_w + (bw + x)) * f.C + cc;
       const double* R = relax + 8 * j;
       const Iv alpha{R[0], R[1]}, gamma{R[4], R[5]};
-      const Iv sp = upper ? gamma : alpha;
-      const Iv sn = upper ? alpha : gamma;
-      bool bad = false;
-      r = relu_map<true>(c, sp, sn, bad);
-      if (bad) r = relu_map<false>(c, sp, sn, bad);
+      // stably positive (alpha = gamma = [1, 1]): every corner product c*1
+      // is exact — for |c| at or above the reference's 2^-500 floor, below
+      // which it widens anyway (interval.hpp:71-83) — so the map is the
+      // identity on a coefficient with two nonzero ends (the straddling split
+      // re-adds exact parts); anything else, including signed-zero ends,
+      // takes the general map
+      const bool ident = alpha.lo == 1.0 && alpha.hi == 1.0 && gamma.lo == 1.0 &&
+                         gamma.hi == 1.0 && fabs(c.lo) >= kFloor && fabs(c.hi) >= kFloor;
+      if (!ident) {
+        const Iv sp = upper ? gamma : alpha;
+        const Iv sn = upper ? alpha : gamma;
+        bool bad = false;
+        r = relu_map<true>(c, sp, sn, bad);
+        if (bad) r = relu_map<false>(c, sp, sn, bad);
+      }
     }
     out.lo[(size_t)i * cells + cell] = r.lo;
     out.hi[(size_t)i * cells + cell] = r.hi;

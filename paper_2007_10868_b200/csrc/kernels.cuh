@@ -94,6 +94,15 @@ struct MagAcc {
       kmaxinv = min(kmaxinv, ~hi);
     }
   }
+  // Warp-reduce, then one shared-memory atomic per warp (block-level stat).
+  __device__ __forceinline__ void flush_shared(unsigned* s_stat) {
+    const unsigned mask = __activemask();
+    const unsigned a = __reduce_min_sync(mask, kmin), b = __reduce_min_sync(mask, kmaxinv);
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1)) {
+      atomicMin(s_stat, a);
+      atomicMin(s_stat + 1, b);
+    }
+  }
   // Warp-reduce over the lanes that reach this call, one atomic per warp.
   __device__ __forceinline__ void flush(unsigned* stat) {
     if (!stat) return;
@@ -155,15 +164,6 @@ __device__ __forceinline__ void band_products(double w, double cl, double ch, do
   const double pl0 = __dmul_rn(a, w), ph0 = __dmul_rn(b, w);
   pl = __dadd_rd(pl0, -fabs(__fma_rn(a, w, -pl0)));
   ph = __dadd_ru(ph0, fabs(__fma_rn(b, w, -ph0)));
-}
-// band_sums with a shorter accumulator dependency (2 FP64 latencies and a
-// select instead of 3; one more instruction): see madd_band_lat.
-__device__ __forceinline__ void band_sums_lat(double pl, double ph, double& lo, double& hi) {
-  const double sl = __dadd_rn(lo, pl), sh = __dadd_rn(hi, ph);
-  const bool xl = __dadd_rd(lo, pl) == __dadd_ru(lo, pl), xh = __dadd_rd(hi, ph) == __dadd_ru(hi, ph);
-  const double tl = __dadd_rd(sl, -4.9406564584124654e-324), th = __dadd_ru(sh, 4.9406564584124654e-324);
-  lo = xl ? sl : tl;
-  hi = xh ? sh : th;
 }
 // band_products with the factors already ordered by the weight's sign
 // (a multiplies into the lower bound, b into the upper).
