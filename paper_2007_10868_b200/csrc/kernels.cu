@@ -1620,6 +1620,195 @@ __global__ void __launch_bounds__(NC, PC_DENSE2_MINB * (kDC / NC))
   mag.flush(out.stat);
 }
 
+// v3 of the batched dense kernel: the union of the block rows' nonzero frame
+// cells is listed once (ascending; block scan) in a prologue, and the slabs
+// walk that list. Every staged weight row and every walked cell is then
+// useful (no per-slab ballot, no partial groups but the last), and full slabs
+// run with compile-time cell offsets. Frames longer than kDMaxList cells walk
+// every cell (zero cells add exact +-0).
+constexpr int kDMaxList = 2048;
+
+template <int TM, int NC>
+__device__ int dense3_cells(const RowsDev& rows, int nrows, int r0, int n_k, const MatDev& in,
+                            int* s_cells, int* s_warp) {
+  const int tx = threadIdx.x, lane = tx & 31, wid = tx >> 5;
+  size_t pr[TM];
+#pragma unroll
+  for (int u = 0; u < TM; ++u) pr[u] = r0 + u < nrows ? phys_row(in, r0 + u) * (size_t)n_k : 0;
+  int base = 0;
+  for (int k0 = 0; k0 < n_k; k0 += NC) {
+    const int k = k0 + tx;
+    bool nz = false;
+    if (k < n_k) {
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+        if (r0 + u < nrows) nz |= !(bits_zero(in.lo[pr[u] + k]) && bits_zero(in.hi[pr[u] + k]));
+    }
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, nz);
+    __syncthreads();  // s_warp of the previous round consumed
+    if (lane == 0) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    int before = base, total = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < NC / 32; ++w2) {
+      const int c = s_warp[w2];
+      if (w2 < wid) before += c;
+      total += c;
+    }
+    if (nz) s_cells[before + __popc(bal & ((1u << lane) - 1u))] = k;
+    base += total;
+  }
+  __syncthreads();
+  return base;
+}
+
+template <int TM, int NC>
+__device__ __forceinline__ void dense3_stage(DenseSmem2<TM, NC>& sm, int b, int j0, int nnz,
+                                             const int* s_cells, bool listed, int r0, int nrows,
+                                             int n_k, const MatDev& in,
+                                             const double* __restrict__ W, int n_in, int col,
+                                             int tx) {
+  for (int e = tx; e < TM * kDK2; e += NC) {
+    const int kk = e / TM, rr = e % TM, idx = j0 + kk;
+    const bool ok = idx < nnz && r0 + rr < nrows;
+    const int cell = ok ? (listed ? s_cells[idx] : idx) : 0;
+    const size_t o = ok ? phys_row(in, r0 + rr) * (size_t)n_k + cell : 0;
+    cp_async8(&sm.c[b][kk][rr].x, in.lo + o, ok);
+    cp_async8(&sm.c[b][kk][rr].y, in.hi + o, ok);
+  }
+  const unsigned s0 = (unsigned)__cvta_generic_to_shared(&sm.w[b][0][tx]);
+  const bool colok = col < n_in;
+#pragma unroll 4
+  for (int kk = 0; kk < kDK2; ++kk) {
+    const int idx = j0 + kk;
+    const bool ok = colok && idx < nnz;
+    const int row = ok ? (listed ? s_cells[idx] : idx) : 0;
+    const double* p = W + (size_t)row * n_in + (colok ? col : 0);
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %2, 0;\n"
+        "  @q cp.async.ca.shared.global [%0], [%1], 8;\n"
+        "  @!q st.shared.f64 [%0], 0d0000000000000000; }\n" ::"r"(s0 + kk * NC * 8),
+        "l"(p), "r"((int)ok));
+  }
+}
+
+// G consecutive staged cells k0.. x TM rows: products first, then the chains.
+template <int G, int TM, int NC>
+__device__ __forceinline__ void dense3_group(const DenseSmem2<TM, NC>& sm, int b, int k0, int tx,
+                                             double* lo, double* hi) {
+  double pl[G][TM], ph[G][TM];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const double wk = sm.w[b][k0 + g][tx];
+    const int sa = __double2hiint(wk) < 0;  // factor order by the weight's sign
+    const double* cg = &sm.c[b][k0 + g][0].x;
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+      band_products_ab(wk, cg[2 * u + sa], cg[2 * u + 1 - sa], pl[g][u], ph[g][u]);
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int u = 0; u < TM; ++u) band_sums(pl[g][u], ph[g][u], lo[u], hi[u]);
+}
+
+template <int TM, int NC>
+__global__ void __launch_bounds__(NC, PC_DENSE2_MINB * (kDC / NC))
+    k_dense_coef3(const double* __restrict__ W, int n_k, int n_in, RowsDev rows, MatDev in,
+                  MatDev out, double wmin, double wmax, const double* relax) {
+  extern __shared__ __align__(16) unsigned char dense3_raw[];
+  DenseSmem2<TM, NC>& sm = *reinterpret_cast<DenseSmem2<TM, NC>*>(dense3_raw);
+  int* s_cells = reinterpret_cast<int*>(dense3_raw + sizeof(DenseSmem2<TM, NC>));
+  __shared__ int s_cols[NC], s_warp[NC / 32];
+  const int tx = threadIdx.x;
+  const int r0 = blockIdx.y * TM;
+  int i0;
+  rows_resolve(rows, 0, i0);
+  const int nrows = rows.n;
+  if (r0 >= nrows) return;
+  const bool band = products_in_band(in.stat, wmin, wmax);
+  const DenseCols dc = dense_live_cols<TM, NC>(rows, nrows, r0, n_in, band ? relax : nullptr, out,
+                                               s_cols, s_warp);
+  if (dc.count <= 0) return;
+  const int col = dc.col;
+  const bool warp_live = (tx & ~31) < dc.count;
+  const bool listed = n_k <= kDMaxList;
+  const int nnz = listed ? dense3_cells<TM, NC>(rows, nrows, r0, n_k, in, s_cells, s_warp) : n_k;
+  double lo[TM], hi[TM];
+  bool bad[TM];
+#pragma unroll
+  for (int u = 0; u < TM; ++u) {
+    lo[u] = hi[u] = 0.0;
+    bad[u] = false;
+  }
+  const int nslab = (nnz + kDK2 - 1) / kDK2;
+#pragma unroll
+  for (int p = 0; p < kDStages - 1; ++p) {
+    if (p < nslab)
+      dense3_stage<TM, NC>(sm, p, p * kDK2, nnz, s_cells, listed, r0, nrows, n_k, in, W, n_in, col,
+                           tx);
+    cp_async_commit();
+  }
+  for (int sl = 0; sl < nslab; ++sl) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kDStages - 2));
+    __syncthreads();  // slab sl landed everywhere; slab sl-1's buffer is free
+    if (sl + kDStages - 1 < nslab)
+      dense3_stage<TM, NC>(sm, (sl + kDStages - 1) % kDStages, (sl + kDStages - 1) * kDK2, nnz,
+                           s_cells, listed, r0, nrows, n_k, in, W, n_in, col, tx);
+    cp_async_commit();
+    if (!warp_live) continue;
+    const int b = sl % kDStages;
+    const int n = min(kDK2, nnz - sl * kDK2);
+    if (band) {
+      if (n == kDK2) {
+#pragma unroll
+        for (int g = 0; g < kDK2; g += kDG) dense3_group<kDG, TM, NC>(sm, b, g, tx, lo, hi);
+      } else {
+        int k0 = 0;
+        for (; n - k0 >= kDG; k0 += kDG) dense3_group<kDG, TM, NC>(sm, b, k0, tx, lo, hi);
+        if (n - k0 >= 2) {
+          dense3_group<2, TM, NC>(sm, b, k0, tx, lo, hi);
+          k0 += 2;
+        }
+        if (n - k0) dense3_group<1, TM, NC>(sm, b, k0, tx, lo, hi);
+      }
+    } else {
+      for (int kk = 0; kk < n; ++kk) {
+        const double wk = sm.w[b][kk][tx];
+#pragma unroll
+        for (int u = 0; u < TM; ++u) {
+          const double2 v = sm.c[b][kk][u];
+          madd_fast(wk, v.x, v.y, lo[u], hi[u], bad[u]);
+        }
+      }
+    }
+  }
+  if (band) {
+#pragma unroll
+    for (int u = 0; u < TM; ++u) lo[u] = canon0(lo[u]);
+  }
+  if (tx == 0)
+    atomicAdd(&g_dense_useful, (unsigned long long)nnz * dc.count * min(TM, nrows - r0));
+  if (col >= n_in) return;
+  MagAcc mag;
+#pragma unroll
+  for (int u = 0; u < TM; ++u) {
+    const int r = r0 + u;
+    if (r >= nrows) continue;
+    if (bad[u]) {
+      lo[u] = hi[u] = 0.0;
+      for (int k = 0; k < n_k; ++k)
+        madd_exact(W[(size_t)k * n_in + col], in.lo[phys_row(in, r) * n_k + k],
+                   in.hi[phys_row(in, r) * n_k + k], lo[u], hi[u]);
+    }
+    out.lo[(size_t)r * n_in + col] = lo[u];
+    out.hi[(size_t)r * n_in + col] = hi[u];
+    mag.add(lo[u]);
+    mag.add(hi[u]);
+  }
+  mag.flush(out.stat);
+}
+
 // Rows per thread (PC_DENSE_TM; default 4 above 64 rows). PC_DENSE_TM=-1
 // picks per launch by a wave model: a launch is one wave set of equal tiles
 // (every thread runs the whole n_k chain, so tiles cannot be split along k),
@@ -1630,12 +1819,21 @@ static int g_dense_tm = 4;
 static int g_dense_slots[9] = {0};  // resident blocks per GPU, per TM
 
 static int g_dense_v2 = 1;    // PC_DENSE_V2: staged-weight kernel for TM > 1
+static int g_dense_v3 = 1;    // PC_DENSE_V3: listed-cell kernel (default)
 static int g_dense_live = 1;  // PC_DENSE_LIVE: skip columns of stably-negative ReLU inputs
 
 template <int TM>
 static void dense_launch(cudaStream_t s, const LayerDev& L, const RowsDev& rows, MatDev in,
                          MatDev out, int n_k, int n_in, const double* relax) {
   if constexpr (TM > 1) {
+    if (g_dense_v3) {
+      constexpr int NC = TM >= 8 ? 64 : kDC;
+      dim3 grid(cdiv(n_in, NC), cdiv(rows.n, TM));
+      const size_t sm = sizeof(DenseSmem2<TM, NC>) + 4 * (size_t)std::min(n_k, kDMaxList);
+      k_dense_coef3<TM, NC><<<grid, NC, sm, s>>>(L.W, n_k, n_in, rows, in, out, L.wmin, L.wmax,
+                                                  relax);
+      return;
+    }
     if (g_dense_v2) {
       // TM = 8: half-width blocks, so the launch keeps as many blocks as TM = 4
       constexpr int NC = TM >= 8 ? 64 : kDC;
@@ -2645,6 +2843,11 @@ void init_kernel_attrs_kernels() {
     big(k_dense_coef2<3, kDC>, sizeof(DenseSmem2<3, kDC>));
     big(k_dense_coef2<4, kDC>, sizeof(DenseSmem2<4, kDC>));
     big(k_dense_coef2<8, 64>, sizeof(DenseSmem2<8, 64>));
+    g_dense_v3 = env_int("PC_DENSE_V3", 1);
+    big(k_dense_coef3<2, kDC>, sizeof(DenseSmem2<2, kDC>) + 4 * kDMaxList);
+    big(k_dense_coef3<3, kDC>, sizeof(DenseSmem2<3, kDC>) + 4 * kDMaxList);
+    big(k_dense_coef3<4, kDC>, sizeof(DenseSmem2<4, kDC>) + 4 * kDMaxList);
+    big(k_dense_coef3<8, 64>, sizeof(DenseSmem2<8, 64>) + 4 * kDMaxList);
     slots(k_dense_coef<1>, 1, 0);
     if (g_dense_v2) {
       slots(k_dense_coef2<2, kDC>, 2, sizeof(DenseSmem2<2, kDC>));
