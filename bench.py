@@ -343,15 +343,15 @@ def main():
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak if hbm_peak else None,
                      # DRAM read+write of one captured launch (ncu --set full, below)
-                     "traffic": 8722176 + 256,
+                     "traffic": 7683584,
                      "launches": dense_n, "kernel_ms": dense_ms,
                      "sample": f"one {per_walk}-image schedule of the step on one worker context",
                      "algorithmic_bytes": dense_bytes,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                      # one ncu --set full capture of this kernel (profiles/r1_final_ncu_dense_coef.txt):
-                     # a 576-row launch (one 64-image schedule, 500x500 layer) moved 8.72 MB of DRAM
+                     # a 576-row launch (one 64-image schedule, 500x500 layer) moved 7.68 MB of DRAM
                      # for 11.2 MB algorithmic bytes (rows in/out + weights once; L2 serves the rest)
-                     "ncu_capture": {"dram_bytes_per_launch": 8722432, "algorithmic_bytes_per_launch": 11216000,
+                     "ncu_capture": {"dram_bytes_per_launch": 7683584, "algorithmic_bytes_per_launch": 11216000,
                                      "rows": 576, "source": "profiles/r1_final_ncu_dense_coef.txt"},
                      # the kernel is FP64-pipe / chain-latency bound, not HBM bound: its
                      # executed interval multiply-adds per second (device-counted) against the

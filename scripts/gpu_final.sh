@@ -9,7 +9,7 @@ for c in mnist_6x100 cifar_convbig cifar_resnet18 cifar_resnet34; do
   timeout 900 python scripts/profile_config.py $c 2 > gpurun_out/prof_final_$c.jsonl 2>&1; tail -1 gpurun_out/prof_final_$c.jsonl | cut -c1-300
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-PYTHONPATH=. timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dense_coef2 -s 20 -c 2 -o gpurun_out/prof_dense2_final python scripts/one_batch.py > /dev/null 2>&1
+PYTHONPATH=. timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dense_coef3 -s 20 -c 2 -o gpurun_out/prof_dense3_final python scripts/one_batch.py > /dev/null 2>&1
 PYTHONPATH=. timeout 900 ncu --metrics sm__inst_executed_pipe_fp64.sum,smsp__inst_executed.sum,gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/met_final.csv python scripts/one_batch.py > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gbc_sparse -s 30 -c 2 -o gpurun_out/prof_gbc_sparse_final python scripts/profile_config.py cifar_resnet18 1 > /dev/null 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
