@@ -2744,29 +2744,34 @@ void launch_ck_merge(cudaStream_t s, unsigned long long* a, unsigned long long* 
 
 // Image-batched seed: per-image live lists (live + img * kq, counts n_live[img])
 // concatenated into one key list (img * kq + neuron), image-major; total count.
-__global__ void k_gather_keys(const int* live, const int* n_live, int nimg, int kq, int* keys,
-                              int* total) {
+constexpr int kGatherThreads = 256;
+static_assert(kMaxBatch <= kGatherThreads, "one scan element per image");
+__global__ void __launch_bounds__(kGatherThreads)
+    k_gather_keys(const int* live, const int* n_live, int nimg, int kq, int* keys, int* total) {
+  using Scan = cub::BlockScan<int, kGatherThreads>;
+  __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_off[kMaxBatch + 1];
-  if (threadIdx.x == 0) {
-    int a = 0;
-    for (int b = 0; b < nimg; ++b) {
-      s_off[b] = a;
-      a += n_live[b];
-    }
-    s_off[nimg] = a;
-    *total = a;
+  const int t = threadIdx.x;
+  const int cnt = t < nimg ? n_live[t] : 0;
+  int off, all;
+  Scan(tmp).ExclusiveSum(cnt, off, all);  // image-major offsets
+  if (t < nimg) s_off[t] = off;
+  if (t == 0) {
+    s_off[nimg] = all;
+    *total = all;
   }
   __syncthreads();
-  for (int b = 0; b < nimg; ++b) {
-    const int cnt = s_off[b + 1] - s_off[b];
-    for (int k = threadIdx.x; k < cnt; k += blockDim.x)
-      keys[s_off[b] + k] = b * kq + live[(size_t)b * kq + k];
+  // one warp per image (strided), lanes over its keys
+  const int lane = t & 31, warp = t >> 5;
+  for (int b = warp; b < nimg; b += kGatherThreads / 32) {
+    const int o = s_off[b], n = s_off[b + 1] - o;
+    for (int k = lane; k < n; k += 32) keys[o + k] = b * kq + live[(size_t)b * kq + k];
   }
 }
 
 void launch_gather_keys(cudaStream_t s, const int* live, const int* n_live, int nimg, int kq,
                         int* keys, int* total) {
-  k_gather_keys<<<1, 256, 0, s>>>(live, n_live, nimg, kq, keys, total);
+  k_gather_keys<<<1, kGatherThreads, 0, s>>>(live, n_live, nimg, kq, keys, total);
   ++g_launches;
 }
 

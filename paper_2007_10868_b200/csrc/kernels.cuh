@@ -109,8 +109,11 @@ struct MagAcc {
     const unsigned mask = __activemask();
     const unsigned a = __reduce_min_sync(mask, kmin), b = __reduce_min_sync(mask, kmaxinv);
     if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1) && (a != 0xFFFFFFFFu || b != 0xFFFFFFFFu)) {
-      atomicMin(stat, a);
-      atomicMin(stat + 1, b);
+      // The stats only decrease, so a value already <= ours needs no atomic:
+      // after the first warps, most of a launch's thousands of warps skip
+      // them (same-address atomics serialise in L2).
+      if (a < *(volatile const unsigned*)stat) atomicMin(stat, a);
+      if (b < *(volatile const unsigned*)(stat + 1)) atomicMin(stat + 1, b);
     }
   }
 };
