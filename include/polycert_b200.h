@@ -117,6 +117,17 @@ pc_status pc_net_test(pc_net* net, const double* lo, const double* up, int label
                       double* margins, double* bounds_lo, double* bounds_hi, double* raw_lo,
                       double* raw_hi, pc_stats* stats);
 
+/* pc_net_test with per-call options: the AnalysisOptions of this one
+ * verify_robustness / analyze call (early_term, chunk_rows, memory_budget,
+ * exec_mode; `device` is ignored: the net's device is used). NULL: the net's
+ * options. Lets one pc_net (the device weights) serve calls with different
+ * options concurrently, as the reference's immutable Network does
+ * (analyzer.hpp:198-276, AnalysisOptions analyzer.hpp:164-169). */
+pc_status pc_net_test_ex(pc_net* net, const pc_options* call_opt, const double* lo,
+                         const double* up, int label, int* verified, double* margins,
+                         double* bounds_lo, double* bounds_hi, double* raw_lo, double* raw_hi,
+                         pc_stats* stats);
+
 /* Same with the input box already resident in device memory (d_lo, d_up are
  * CUDA device pointers on the net's device); outputs are host arrays. */
 pc_status pc_net_test_device(pc_net* net, const double* d_lo, const double* d_up, int label,

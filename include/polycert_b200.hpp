@@ -25,7 +25,10 @@
 #ifndef POLYCERT_B200_HPP
 #define POLYCERT_B200_HPP
 
+#include <cstdint>
+#include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -123,14 +126,37 @@ inline PassStats stats_of(const pc_stats& s) {
 
 struct Handle {
   pc_net* h = nullptr;
-  AnalysisOptions opt;
+  int device = -1;
+  uint64_t fingerprint = 0;  // layers + parameters the device copy was built from
   ~Handle() { if (h) pc_net_destroy(h); }
 };
 
+// Per-call options for pc_net_test_ex (the device is the handle's).
+inline pc_options call_options(const AnalysisOptions& opt) {
+  pc_options o;
+  pc_default_options(&o);
+  o.early_term = opt.early_term ? 1 : 0;
+  o.chunk_rows = opt.chunk_rows;
+  o.memory_budget = opt.memory_budget;
+  o.device = opt.device;
+  o.exec_mode = opt.exec_mode;
+  return o;
+}
+
+inline uint64_t mix(uint64_t h, uint64_t v) {
+  h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  return h * 0xFF51AFD7ED558CCDull;
+}
+
 }  // namespace detail
 
-// Network<WidenedFloat64> analogue. The device copy (pc_net) is created by
-// instantiate() / on first use and owned here; copies share it.
+// Network<WidenedFloat64> analogue. The device copy (pc_net: validated layers
+// and uploaded weights) is created once by instantiate() (or on first use) and
+// shared by copies; every call passes its own AnalysisOptions through
+// pc_net_test_ex, so concurrent calls with different options are safe, as on
+// the reference's immutable Network (analyzer.hpp:198-276). Each call holds a
+// reference to the handle for its whole duration. Editing layers or weights
+// after instantiate() is detected (content fingerprint) and re-uploads.
 class Network {
  public:
   Shape input_shape;
@@ -149,28 +175,57 @@ class Network {
       layers[k].out_shape = Shape{shapes[3 * k], shapes[3 * k + 1], shapes[3 * k + 2]};
   }
 
-  // The device handle for these options (re-created when the options change).
-  pc_net* handle(const AnalysisOptions& opt) const {
-    if (!dev_ || !(dev_->opt == opt)) {
+  // The device handle (created on first use, or again after the layers or
+  // the device changed). The returned reference keeps it alive for the call.
+  std::shared_ptr<detail::Handle> handle(const AnalysisOptions& opt) const {
+    const uint64_t fp = fingerprint();
+    std::lock_guard<std::mutex> lk(*mu_);
+    if (!dev_ || dev_->fingerprint != fp || dev_->device != opt.device) {
       std::vector<pc_layer_desc> d = descs();
-      pc_options o;
-      pc_default_options(&o);
-      o.early_term = opt.early_term ? 1 : 0;
-      o.chunk_rows = opt.chunk_rows;
-      o.memory_budget = opt.memory_budget;
-      o.device = opt.device;
-      o.exec_mode = opt.exec_mode;
+      const pc_options copt = detail::call_options(opt);
       auto h = std::make_shared<detail::Handle>();
-      h->opt = opt;
+      h->device = opt.device;
+      h->fingerprint = fp;
       detail::check(pc_net_create(d.data(), (int)d.size(), input_shape.w, input_shape.h,
-                                  input_shape.c, &o, &h->h));
+                                  input_shape.c, &copt, &h->h));
       dev_ = std::move(h);
     }
-    return dev_->h;
+    return dev_;
   }
 
  private:
   mutable std::shared_ptr<detail::Handle> dev_;
+  std::shared_ptr<std::mutex> mu_ = std::make_shared<std::mutex>();
+
+  uint64_t fingerprint() const {
+    uint64_t h = detail::mix(0, (uint64_t)input_shape.numel());
+    auto words = [&h](const std::vector<double>& v) {  // 4 independent lanes: ~1 word/cycle
+      uint64_t a[4] = {v.size(), 1, 2, 3};
+      size_t i = 0;
+      for (; i + 4 <= v.size(); i += 4)
+        for (int l = 0; l < 4; ++l) {
+          uint64_t b;
+          std::memcpy(&b, &v[i + l], 8);
+          a[l] = (a[l] ^ b) * 0x9E3779B97F4A7C15ull;
+        }
+      for (; i < v.size(); ++i) {
+        uint64_t b;
+        std::memcpy(&b, &v[i], 8);
+        a[0] = (a[0] ^ b) * 0x9E3779B97F4A7C15ull;
+      }
+      for (uint64_t x : a) h = detail::mix(h, x);
+    };
+    for (const Layer& l : layers) {
+      h = detail::mix(h, (uint64_t)l.kind);
+      for (int p : l.preds) h = detail::mix(h, (uint64_t)p);
+      for (int v : {l.n_out, l.fw, l.fh, l.cin, l.cout, l.sw, l.sh, l.pw, l.ph})
+        h = detail::mix(h, (uint64_t)(uint32_t)v);
+      words(l.weights);
+      words(l.bias);
+      words(l.filter);
+    }
+    return h;
+  }
 
   std::vector<pc_layer_desc> descs() const {
     std::vector<pc_layer_desc> d(layers.size());
@@ -224,15 +279,17 @@ inline void split(const InputBox& box, std::vector<double>& lo, std::vector<doub
 
 // analyze (analyzer.hpp:198-242): refined per-layer per-neuron bounds.
 inline AnalysisResult analyze(const Network& net, const InputBox& box, const AnalysisOptions& opt) {
-  pc_net* h = net.handle(opt);
+  const auto hold = net.handle(opt);
+  pc_net* h = hold->h;
+  const pc_options copt = detail::call_options(opt);
   std::vector<double> lo, hi;
   detail::split(box, lo, hi);
   const long long T = pc_net_total_neurons(h);
   std::vector<double> bl(T), bh(T), rl(T), rh(T);
   pc_stats st{};
   int verified = 0;
-  detail::check(pc_net_test(h, lo.data(), hi.data(), -1, &verified, nullptr, bl.data(), bh.data(),
-                            rl.data(), rh.data(), &st));
+  detail::check(pc_net_test_ex(h, &copt, lo.data(), hi.data(), -1, &verified, nullptr, bl.data(),
+                               bh.data(), rl.data(), rh.data(), &st));
   AnalysisResult r;
   r.stats = detail::stats_of(st);
   long long o = 0;
@@ -254,7 +311,9 @@ inline AnalysisResult analyze(const Network& net, const InputBox& box, const Ana
 // iff every margin lower bound is > 0.
 inline Verdict verify_robustness(const Network& net, const InputBox& box, int label,
                                  const AnalysisOptions& opt) {
-  pc_net* h = net.handle(opt);
+  const auto hold = net.handle(opt);
+  pc_net* h = hold->h;
+  const pc_options copt = detail::call_options(opt);
   const int n_out = pc_net_output_size(h);
   if (label < 0 || label >= n_out) throw std::invalid_argument("margin: label out of range");
   std::vector<double> lo, hi;
@@ -262,8 +321,8 @@ inline Verdict verify_robustness(const Network& net, const InputBox& box, int la
   std::vector<double> m(n_out > 1 ? n_out - 1 : 1);
   pc_stats st{};
   int verified = 0;
-  detail::check(pc_net_test(h, lo.data(), hi.data(), label, &verified, m.data(), nullptr, nullptr,
-                            nullptr, nullptr, &st));
+  detail::check(pc_net_test_ex(h, &copt, lo.data(), hi.data(), label, &verified, m.data(), nullptr,
+                               nullptr, nullptr, nullptr, &st));
   Verdict v;
   v.label = label;
   v.verified = verified != 0;

@@ -19,9 +19,10 @@ JSON="$(python3 -c 'import site,os;print(next(p for p in [os.path.join(s,"includ
 if [ -z "$JSON" ]; then echo "build_ref: nlohmann/json.hpp not found" >&2; exit 1; fi
 ln -sf "$JSON" "$OUT/vendor/json.hpp"
 GMP="$(ls /lib/x86_64-linux-gnu/libgmp.so.10 /usr/lib/x86_64-linux-gnu/libgmp.so.10 2>/dev/null | head -1)"
+# -O3 -DNDEBUG = the reference's CMake Release build (proj/CMakeLists.txt:8-10).
 # -ffp-contract=off: keep the reference's separate multiply/add roundings
 # (its CMake build uses no -march, so x86-64 has no FMA to contract into).
-CXXFLAGS="-std=c++20 -O2 -fPIC -ffp-contract=off -w -I$HERE/shim -I$OUT/vendor -I$REF/include"
+CXXFLAGS="-std=c++20 -O3 -DNDEBUG -fPIC -ffp-contract=off -w -I$HERE/shim -I$OUT/vendor -I$REF/include"
 g++ $CXXFLAGS -shared -o "$OUT/libpolycert_ref.so" \
   "$HERE/ref_driver.cpp" "$REF/src/decimal.cpp" "$REF/src/gen.cpp" "$REF/src/model_io.cpp" \
   "$GMP" -lpthread

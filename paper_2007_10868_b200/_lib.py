@@ -66,6 +66,7 @@ def _load():
         "pc_net_output_size": (i, [vp]),
         "pc_input_box": (i, [vp, i, d, i, vp, vp]),
         "pc_net_test": (i, [vp, vp, vp, i, vp, vp, vp, vp, vp, vp, vp]),
+        "pc_net_test_ex": (i, [vp, vp, vp, vp, i, vp, vp, vp, vp, vp, vp, vp]),
         "pc_net_test_device": (i, [vp, vp, vp, i, vp, vp, vp]),
         "pc_net_test_batch": (i, [vp, i, vp, vp, i, vp, i, vp, vp, vp, vp]),
         "pc_net_stream": (vp, [vp]),

@@ -37,18 +37,19 @@ def _run_flags(p):
 
 def _verify_or_bench(a, bench: bool) -> int:
     from . import AnalysisOptions, Verifier, input_box
-    from .model_io import _num, load_inputs, load_model
+    from .model_io import load_inputs, load_model, parse_decimal
     net = load_model(a.model)
     rows = load_inputs(a.inputs)
-    eps = _num(a.epsilon, 0)  # decimal string, one correct rounding (decimal.cpp:63-76)
+    eps = parse_decimal(a.epsilon)  # decimal string, one correct rounding (decimal.cpp:63-76)
     v = Verifier(net, AnalysisOptions(early_term=not a.no_early_term, chunk_rows=a.chunk_rows,
                                       memory_budget=a.memory_budget, device=a.device))
     n_in = v.net.numel(0)
     lines, failed = [], False
-    for i, x in enumerate(rows):
+    for i, cells in enumerate(rows):
         try:
-            if len(x) != n_in:
+            if len(cells) != n_in:
                 raise ValueError("input size mismatch")
+            x = [parse_decimal(t) for t in cells]  # scalar_from_decimal per cell (main.cpp:122-124)
             label = v.candidate(x)
             if label < 0:  # tied argmax: not a candidate (main.cpp:129-140)
                 lines.append(f"{i},0,0.000000" if bench else json.dumps(

@@ -142,7 +142,7 @@ struct Ctx {
   const std::vector<long long>& pofs;
   const long long total, max_numel;
   const int n_out;
-  const pc_options opt;
+  pc_options opt;  // the net's options, overridden per call (pc_net_test_ex)
   const int device;
   const bool timing, profile;
   long long budget = 0;  // workspace bytes for one pass (0: derive)
@@ -179,6 +179,7 @@ struct Ctx {
   int* perm2 = nullptr;
   cudaGraphExec_t graph = nullptr;
   int graph_label_mode = -1;       // label < 0 (analysis only) vs >= 0 when captured
+  int graph_et = -1;               // early_term the graph was captured with
   bool graph_failed = false;
   pc_stats graph_st{};             // host-side counts accumulated while capturing
   std::vector<size_t> graph_dense_ev;
@@ -1092,6 +1093,11 @@ long long budget_of(const Ctx* n) {
 
 inline long long slice_begin(long long n, int r, int w) { return n * r / w; }
 
+// Rows per polarity of one walker: row kernels put the 2R rows of a walk in
+// gridDim.y (<= 65535), so every chunk is capped here (results are
+// chunk-invariant, backsub.hpp:25-29).
+constexpr long long kMaxWalkRows = 32767;
+
 void ensure_shard_buffers(Ctx* n, size_t per_rank_doubles) {
   if (per_rank_doubles <= n->sh_cap) return;
   if (n->sh_send) cudaFree(n->sh_send);
@@ -1253,6 +1259,8 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
     // independent, backsub.hpp:31-34; results identical).
     static const int pipes = env_int("PC_PIPES", 2);
     const bool two = pipes >= 2 && !n->is_helper && chunk >= 16;
+    // rows of a walk ride in gridDim.y (both polarities: 2R <= 65535)
+    chunk = std::min<long long>(chunk, two ? 2ll * kMaxWalkRows : kMaxWalkRows);
     Ctx* h = two ? helper_of(n) : nullptr;
     const long long half = two ? (chunk + 1) / 2 : chunk;
     ensure_arena(n, ws.per_row * (size_t)half + 256 * ws.allocs + (1 << 20));
@@ -1470,6 +1478,7 @@ void capture_graph(Ctx* n, bool with_margin, size_t arena, size_t stat_count) {
   if (n->graph) cudaGraphExecDestroy(n->graph);
   n->graph = exec;
   n->graph_label_mode = with_margin ? 1 : 0;
+  n->graph_et = n->opt.early_term;
   n->graph_st = st;
   n->graph_dense_ev = n->dense_ev;
   n->graph_dense_bytes = g_dense_bytes;
@@ -1486,7 +1495,7 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
   size_t arena = 0, stat_count = 0;
   if (graph_eligible(n, &arena, &stat_count)) {
     const bool with_margin = label >= 0;
-    if (!n->graph || n->graph_label_mode != (with_margin ? 1 : 0)) {
+    if (!n->graph || n->graph_label_mode != (with_margin ? 1 : 0) || n->graph_et != n->opt.early_term) {
       try {
         capture_graph(n, with_margin, arena, stat_count);
       } catch (const StatusError&) {
@@ -1494,7 +1503,7 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
         n->graph_failed = true;  // fall back to the host-driven schedule
       }
     }
-    if (n->graph && n->graph_label_mode == (with_margin ? 1 : 0)) {
+    if (n->graph && n->graph_label_mode == (with_margin ? 1 : 0) && n->graph_et == n->opt.early_term) {
       n->h_int[2] = label;
       ck(cudaMemcpyAsync(n->d_label, n->h_int + 2, sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
       ck(cudaGraphLaunch(n->graph, s), "graph launch");
@@ -1652,7 +1661,7 @@ void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stat
       long long chunk = n->opt.chunk_rows > 0
                             ? n->opt.chunk_rows
                             : std::max<long long>(1, budget_of(n) / (long long)ws.per_row);
-      chunk = std::min<long long>(chunk, n_live);
+      chunk = std::min<long long>(std::min<long long>(chunk, n_live), kMaxWalkRows);
       ensure_arena(n, ws.per_row * (size_t)chunk + 256 * ws.allocs + (1 << 20));
       for (long long base = 0; base < n_live; base += chunk) {
         const int R = (int)std::min<long long>(chunk, n_live - base);
@@ -1804,6 +1813,7 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     if (b_hi) ck(cudaMemcpyAsync(b_hi, n->bhi, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
     if (r_lo) ck(cudaMemcpyAsync(r_lo, n->rlo, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
     if (r_hi) ck(cudaMemcpyAsync(r_hi, n->rhi, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaGetLastError(), "kernel");
     ck(cudaEventRecord(t1, s), "event");
     ck(cudaStreamSynchronize(s), "sync");
     ck(cudaGetLastError(), "kernel");
@@ -1848,9 +1858,20 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     g_last_launches = g_launches;
 }
 
-pc_status test_impl(pc_net* net, const double* lo, const double* up, bool device_box, int label,
-                    int* verified, double* margins, double* b_lo, double* b_hi, double* r_lo,
-                    double* r_hi, pc_stats* stats) {
+// Per-call options (AnalysisOptions of one verify_robustness / analyze call):
+// early_term, chunk_rows, memory_budget and exec_mode apply to this call only;
+// the device is the net's.
+void apply_call_options(Ctx* c, const pc_options* call) {
+  pc_options o = call ? *call : c->net->opt;
+  o.device = c->net->opt.device;
+  if (call && o.exec_mode == 0) o.exec_mode = c->net->opt.exec_mode;
+  c->opt = o;
+  if (c->helper) c->helper->opt = o;
+}
+
+pc_status test_impl(pc_net* net, const pc_options* call_opt, const double* lo, const double* up,
+                    bool device_box, int label, int* verified, double* margins, double* b_lo,
+                    double* b_hi, double* r_lo, double* r_hi, pc_stats* stats) {
   if (!net) {
     g_err = "null network";
     return PC_ERR_INVALID_ARGUMENT;
@@ -1862,6 +1883,7 @@ pc_status test_impl(pc_net* net, const double* lo, const double* up, bool device
     ck(cudaSetDevice(net->device), "cudaSetDevice");
     dense_useful_madds(true);
     CtxLease lease(net);
+    apply_call_options(lease.c, call_opt);
     run_one(lease.c, lo, up, device_box, label, verified, margins, b_lo, b_hi, r_lo, r_hi, stats);
     g_dense_madds = (double)dense_useful_madds(false);
   });
@@ -2090,7 +2112,15 @@ int pc_net_output_size(const pc_net* n) { return n ? n->n_out : -1; }
 pc_status pc_net_test(pc_net* n, const double* lo, const double* up, int label, int* verified,
                       double* margins, double* b_lo, double* b_hi, double* r_lo, double* r_hi,
                       pc_stats* stats) {
-  return test_impl(n, lo, up, false, label, verified, margins, b_lo, b_hi, r_lo, r_hi, stats);
+  return test_impl(n, nullptr, lo, up, false, label, verified, margins, b_lo, b_hi, r_lo, r_hi,
+                   stats);
+}
+
+pc_status pc_net_test_ex(pc_net* n, const pc_options* call_opt, const double* lo, const double* up,
+                         int label, int* verified, double* margins, double* b_lo, double* b_hi,
+                         double* r_lo, double* r_hi, pc_stats* stats) {
+  return test_impl(n, call_opt, lo, up, false, label, verified, margins, b_lo, b_hi, r_lo, r_hi,
+                   stats);
 }
 
 pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const double* up,
@@ -2132,6 +2162,7 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
     std::vector<Ctx*> ctxs(conc);
     for (int w = 0; w < conc; ++w) {
       ctxs[w] = B > 1 ? acquire_batched(net, B) : acquire(net);
+      apply_call_options(ctxs[w], nullptr);  // the net's options (a leased context keeps the last call's)
       ctxs[w]->budget = budget;
     }
     ck(cudaEventRecord(start, master), "event");
@@ -2176,13 +2207,14 @@ pc_status pc_net_test_batch(pc_net* net, int n_images, const double* lo, const d
           g_dense_bytes = g_dense_madds = 0;
           g_dense_launches = 0;
           run_test_batched(c, nb, labels + i, mg.data(), sts.data());
+          ck(cudaGetLastError(), "kernel");  // a failed launch voids the results
           // the dense kernel's live timing (bench.py's roofline) across workers
           double dms = 0;
           for (size_t e : c->dense_ev) {
             float d = 0;
             if (cudaEventElapsedTime(&d, c->ev_pool[e], c->ev_pool[e + 1]) == cudaSuccess) dms += d;
           }
-          cudaGetLastError();
+          (void)cudaGetLastError();  // timing is best effort: drop only its own errors
           {
             std::lock_guard<std::mutex> lk(err_mu);
             agg_dense_ms += dms;
@@ -2287,8 +2319,8 @@ pc_status pc_net_set_sharding(pc_net* net, int rank, int world, pc_allgather_fn 
 
 pc_status pc_net_test_device(pc_net* n, const double* d_lo, const double* d_up, int label,
                              int* verified, double* margins, pc_stats* stats) {
-  return test_impl(n, d_lo, d_up, true, label, verified, margins, nullptr, nullptr, nullptr,
-                   nullptr, stats);
+  return test_impl(n, nullptr, d_lo, d_up, true, label, verified, margins, nullptr, nullptr,
+                   nullptr, nullptr, stats);
 }
 
 }  // extern "C"

@@ -23,6 +23,13 @@ def _num(t, lid):
     return float(t)
 
 
+def parse_decimal(t: str) -> float:
+    """double_from_decimal (decimal.cpp:63-76): grammar check, one correct rounding."""
+    if not _DEC.match(t):
+        raise ValueError(f"bad decimal: {t}")
+    return float(t)
+
+
 def model_from_json_obj(j) -> Network:
     if j.get("format") != FORMAT:
         raise ValueError("model: missing or unsupported format tag")
@@ -80,19 +87,34 @@ def save_model(net: Network, path: str):
         f.write(json.dumps(model_to_json_obj(net), indent=1, sort_keys=True) + "\n")
 
 
-def load_inputs(path: str) -> np.ndarray:
-    """load_inputs (model_io.cpp:331-353)."""
+def load_inputs(path: str) -> list[list[str]]:
+    """load_inputs (model_io.cpp:331-353): rows of trimmed decimal strings.
+
+    Cells stay strings, as in the reference; they are parsed (and the row
+    length checked) per input inside the CLI's per-input try, so one bad row
+    becomes an {index, error} line instead of aborting the run
+    (tools/main.cpp:117-184). Split like std::getline(ss, cell, ','): a
+    trailing comma does not make an empty last cell.
+    """
     rows = []
-    with open(path) as f:
-        for n, line in enumerate(f, start=1):
-            line = line.rstrip("\n")
+    try:
+        f = open(path)
+    except OSError:
+        raise RuntimeError(f"cannot open inputs file: {path}")
+    with f:
+        for line in f:
+            line = line[:-1] if line.endswith("\n") else line
             if not line:
                 continue
-            cells = []
-            for cell in line.split(","):
+            parts = line.split(",")
+            if parts and parts[-1] == "":
+                parts.pop()  # getline yields no cell after a final delimiter
+            row = []
+            for cell in parts:
                 t = cell.strip(" \t\r")
                 if not t:
-                    raise ValueError(f"inputs {path}: empty cell on line {len(rows) + 1}")
-                cells.append(_num(t, 0))
-            rows.append(cells)
-    return np.array(rows, dtype=np.float64)
+                    raise RuntimeError(f"inputs {path}: empty cell on line {len(rows) + 1}")
+                row.append(t)
+            if row:
+                rows.append(row)
+    return rows

@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "polycert_b200.hpp"
 
@@ -132,6 +134,37 @@ int main() {
       for (const Interval& iv : layer) CHECK(iv.lo <= iv.hi);
     const Verdict v = verify_robustness(net, input_box({0.4, 0.6}, 0.05, true), 0, opt);
     CHECK(v.margins.size() == 1 && v.stats.rows_total > 0);
+  }
+  {  // one Network, concurrent calls with different options (the handle is
+     // bound once; options travel per call), then an edited copy re-uploads
+    Network net = instantiate(dense_net(Shape{1, 1, 2},
+                                        {{{{1, -1}, {0.5, 0.5}, {-1, 2}}, {0.1, -0.2, 0}},
+                                         {{{1, 1, -1}, {0.5, -1, 1}}, {0, 0}}},
+                                        true),
+                              opt);
+    const InputBox box = input_box({0.4, 0.6}, 0.05, true);
+    const Verdict want = verify_robustness(net, box, 0, opt);
+    std::vector<std::thread> th;
+    std::vector<int> ok(8, 0);
+    for (int t = 0; t < 8; ++t)
+      th.emplace_back([&, t] {
+        AnalysisOptions o;
+        o.early_term = (t & 1) != 0;
+        o.chunk_rows = (t & 2) ? 1 : 0;
+        for (int k = 0; k < 4; ++k) {
+          const Verdict v = verify_robustness(net, box, 0, o);
+          ok[t] += v.margins.size() == want.margins.size() &&
+                   std::memcmp(&v.margins[0].second, &want.margins[0].second, 8) == 0;
+        }
+      });
+    for (auto& x : th) x.join();
+    for (int t = 0; t < 8; ++t) CHECK(ok[t] == 4);
+    Network edited = net;
+    edited.layers[3].bias[0] += 1.0;  // out_0 - out_1 grows by exactly 1
+    const Verdict v2 = verify_robustness(edited, box, 0, opt);
+    CHECK(v2.margins[0].second > want.margins[0].second + 0.5);
+    const Verdict v3 = verify_robustness(net, box, 0, opt);  // the original is untouched
+    CHECK(std::memcmp(&v3.margins[0].second, &want.margins[0].second, 8) == 0);
   }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "facade ok", g_fail);
   return g_fail ? 1 : 0;

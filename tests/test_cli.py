@@ -59,3 +59,35 @@ def test_bench_matches_golden_csv():
         gi, _, gf = g.split(",")
         wi, _, wf = w.split(",")
         assert (gi, gf) == (wi, wf)
+
+
+def test_load_inputs_keeps_strings(tmp_path):
+    """model_io.cpp:331-353: cells stay strings, trimmed; a trailing comma
+    makes no empty cell (std::getline); an inner empty cell throws."""
+    from paper_2007_10868_b200.model_io import load_inputs, parse_decimal
+    p = tmp_path / "x.csv"
+    p.write_text("0.5, 0.25 ,\r\n\n1,x\n")
+    assert load_inputs(str(p)) == [["0.5", "0.25"], ["1", "x"]]
+    p.write_text("0.5,,1\n")
+    with pytest.raises(RuntimeError, match="empty cell on line 1"):
+        load_inputs(str(p))
+    assert parse_decimal("0.25") == 0.25
+    for bad in ("1.", ".5", "1e3", "x"):
+        with pytest.raises(ValueError, match="bad decimal: "):
+            parse_decimal(bad)
+
+
+@pytest.mark.gpu
+def test_bad_row_is_a_per_input_error(tmp_path):
+    """main.cpp:117-184: a malformed or short row yields {index, error}, the
+    other rows still verify, and the exit code is 1."""
+    rows = open(os.path.join(GOLDEN, "inputs.csv")).read().splitlines()
+    x = tmp_path / "x.csv"
+    x.write_text("\n".join([rows[0], "0.5,0.5", rows[1].replace(",", ",abc,", 1)]) + "\n")
+    r = cli("verify", "--model", os.path.join(GOLDEN, "model.json"), "--inputs", str(x),
+            "--epsilon", "0.03")
+    assert r.returncode == 1, r.stderr
+    got = [json.loads(l) for l in r.stdout.splitlines()]
+    assert got[0]["verdict"] == "verified"
+    assert got[1] == {"index": 1, "error": "input size mismatch"}
+    assert got[2]["index"] == 2 and "error" in got[2]
