@@ -1,30 +1,49 @@
 #!/usr/bin/env python
-"""Benchmark: ms/image to verify one image (BASELINE.json metric), GPU engine
-vs the reference's own CPU verifier.
+"""Benchmark: ms/image to verify one image (BASELINE.json metric) on 1/2/4/8
+B200, GPU engine vs the reference's own CPU verifier.
 
 A "step" verifies one image: analyze + margin pass (verify_robustness,
 analyzer.hpp:256-276) on a generator-built network (random-init dyadic
-weights of the named architecture, gen.cpp) and generator inputs. Default
-workload: configs[1] = MNIST 9x500, eps 0.026, early termination on.
+weights of the named architecture, gen.cpp) and generator inputs (seed 8,
+image s of the pool). Default workload: the paper's headline 34-layer
+residual net (BASELINE.json configs[4], `cifar_resnet34`, eps 2/255, early
+termination on).
 
-  value  device-resident inputs, per-step CUDA events around pc_net_test_batch
-         (512 images per step over 8 worker contexts, each verifying 64 images
-         per image-batched schedule), L2 flushed between steps (outside the events)
-  e2e    the same batched C-ABI call with HOST buffers (pc_net_test_batch): box H2D +
-         margins D2H
-         inside the timed region
-  cpu_baseline / --impl reference: the unmodified reference (oracle/_ref,
-         compiled from /root/reference) on the host's cores; falls back to the
-         plain-C restatement (oracle/, "port") if the reference lib is absent.
+  value  per-image latency (ms/image): the image's box already in HBM
+         (pc_net_test_device), CUDA events on the engine stream around the
+         whole verification; N > 1: the same image row-sharded over all ranks
+         (native NCCL all-gather), max over ranks. L2 flushed between steps.
+  e2e    the same through the reference-facing C-ABI call with HOST buffers
+         (pc_net_test: box H2D + margins D2H inside the timed region), host
+         clock around the synchronous call, max over ranks.
+  throughput_ms_per_image  replicas: images verified concurrently
+         (pc_net_test_batch) on every rank, whole-job ms/image.
+  parity  the timed images that have reference fixtures
+         (tests/golden/ref_<config>_img<i>.json, made by
+         scripts/ref_fixtures.py from the unmodified reference) are compared
+         bit for bit: verdict, margins, PassStats.
+  roofline  the conv back-substitution kernel (k_gbc_sparse2), the dominant
+         kernel of the residual configs: algorithmic FLOPs (4 per interval
+         multiply-add, the reference's gbc_madds) per second of its CUDA-event
+         time vs the FP64 FMA peak measured live (pc_fp64_peak); its HBM
+         fraction beside it.
+  cpu_baseline / --impl reference: the unmodified reference (oracle/_ref)
+         on the host's cores, one image with AnalysisOptions.workers = all
+         host threads (the reference's latency mode). When one image cannot
+         finish in the time allowed (the ResNets take hours), the line
+         reports the elapsed time as a lower bound (`value_is_lower_bound`).
 
-Multi-GPU (torchrun): replicas — rank r verifies images r, r+N, ...; no
-collective on the data path; time = max over ranks.
+`python bench.py --gpus N` (N > 1) relaunches itself under torch.distributed.run
+with N ranks; under torchrun the ranks come from the environment.
 """
 from __future__ import annotations
 
 import argparse
+import glob
+import importlib.util
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,43 +52,71 @@ import time
 
 import numpy as np
 
-# Many concurrent per-image streams: give each its own hardware work queue
-# (the default of 8 aliases streams onto shared queues, serialising them).
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FP64_MADD_PEAK = 9.5e11  # interval madds/s, measured band-madd peak (ILP8)
 METRIC = "ms/image to verify (1/2/4/8 B200) + certified count == CPU ref; HBM GB/s"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="mnist_9x500")
+    ap.add_argument("--config", default="cifar_resnet34")
     ap.add_argument("--no-early-term", action="store_true")
-    ap.add_argument("--cpu-sample-seconds", type=float, default=20.0)
+    ap.add_argument("--cpu-sample-seconds", type=float, default=30.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch", type=int, default=512, help="images per step")
-    ap.add_argument("--concurrency", type=int, default=8, help="worker contexts per GPU (each verifies batch/concurrency images per schedule)")
+    ap.add_argument("--throughput-images", type=int, default=16, help="images per replica batch")
+    ap.add_argument("--concurrency", type=int, default=4, help="worker contexts of the replica batch")
+    ap.add_argument("--pool", type=int, default=8, help="distinct images cycled through by the steps")
     return ap.parse_args()
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def load_configs():
+    """configs.py by file path: the reference arm never imports the product package."""
+    spec = importlib.util.spec_from_file_location(
+        "pc_configs", os.path.join(ROOT, "paper_2007_10868_b200", "configs.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
 
 
 def workload(name):
-    from paper_2007_10868_b200.configs import CONFIGS, INPUT_SEED, MODEL_SEED
-    arch, eps = CONFIGS[name]
-    return arch, eps, MODEL_SEED, INPUT_SEED
+    cfg = load_configs()
+    arch, eps = cfg.CONFIGS[name]
+    return arch, eps, cfg.MODEL_SEED, cfg.INPUT_SEED
+
+
+def config_dict(args, arch, eps_s, mseed, iseed, world):
+    return {"workload": args.config, "arch": arch, "eps": eps_s, "model_seed": mseed,
+            "input_seed": iseed, "images": f"pool of {args.pool} generator images, step s verifies image s mod {args.pool}",
+            "early_term": not args.no_early_term,
+            "parallelism": (f"row sharding x{world} (every pass's live rows split across ranks, "
+                            "candidate bounds all-gathered over NCCL)") if world > 1 else "1 GPU",
+            "l2": "flushed between steps (256 MB write, outside the timed region)"}
+
+
+def fixtures(config):
+    out = {}
+    for p in glob.glob(os.path.join(ROOT, "tests", "golden", f"ref_{config}_img*.json")):
+        fx = json.load(open(p))
+        if fx.get("early_term", True):
+            out[int(fx["image"])] = fx
+    return out
+
+
+def offline_reference_seconds(config):
+    """Full-image reference times recorded when the fixtures were made (this
+    repo's container CPU, not the bench host)."""
+    fx = fixtures(config)
+    return {i: {"seconds": f["ref_seconds"], "workers": f["workers"]} for i, f in sorted(fx.items())}
 
 
 class ClockSampler:
@@ -120,47 +167,50 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-_REF_CACHE = {}
+# ---------------------------------------------------------------------------
+# The reference (CPU): oracle/_ref, the unmodified reference verifier.
+
+_REF_CHILD = r"""
+import json, sys, time
+sys.path.insert(0, sys.argv[1])
+from oracle.pyoracle import Ref
+arch, eps_s, mseed, iseed, image, workers, et = json.loads(sys.argv[2])
+ref = Ref()
+h = ref.generate(mseed, arch)
+dim = 1
+for v in ref.layers(h)[0].out_shape: dim *= v
+x = ref.random_inputs(iseed, image + 1, dim)[image]
+lab = ref.candidate(h, x)
+print(json.dumps({"phase": "ready", "label": lab}), flush=True)
+r = ref.verify(h, x, ref.double_from_decimal(eps_s), True, max(lab, 0), et, 0, 0, workers, False)
+print(json.dumps({"phase": "done", "seconds": r["seconds"], "verified": r["verified"],
+                  "margins": [m.hex() for m in r["margins"]], "stats": r["stats"]}), flush=True)
+"""
 
 
-def cpu_reference(arch, eps_s, mseed, iseed, n_images, threads, early_term):
-    """The reference's CPU verifier on `threads` host cores (oracle/_ref), else
-    the plain-C restatement. Returns (ms_per_image, kind, verdicts, seconds)."""
-    from oracle.pyoracle import Ref
-    if Ref.available():
-        key = (arch, mseed)
-        if key not in _REF_CACHE:
-            ref = Ref()
-            h = ref.generate(mseed, arch)
-            _REF_CACHE[key] = (ref, h, int(np.prod(ref.layers(h)[0].out_shape)))
-        ref, h, dim = _REF_CACHE[key]
-        X = ref.random_inputs(iseed, n_images, dim)
-        eps = ref.double_from_decimal(eps_s)
-        verdicts, wall, per = ref.verify_batch(h, X, eps, True, threads, early_term)
-        return 1000.0 * wall / n_images, "reference", verdicts, wall, per
-    # plain-C restatement, one image at a time per thread
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle.pyoracle import Port
-    import paper_2007_10868_b200 as pc
-    port = Port()
-    net = pc.generate(mseed, arch)
-    X = pc.random_inputs(iseed, n_images, int(np.prod(net.input_shape)))
-    eps = float(eps_s)
-    v = pc.Verifier(net)
-    labels = [v.candidate(x) for x in X]
-
-    def one(i):
-        lo, hi = port.input_box(X[i], eps)
-        t0 = time.perf_counter()
-        r = port.analyze(net.layers, lo, hi, label=max(labels[i], 0), early_term=early_term)
-        return (1 if r["verified"] else 0), time.perf_counter() - t0
-
+def reference_image(arch, eps_s, mseed, iseed, image, workers, et, limit_s):
+    """verify_robustness of one image by the unmodified reference in a child
+    process with `workers` threads (AnalysisOptions.workers, the reference's
+    intra-call row parallelism). Returns (seconds, finished, result). The
+    network build / model generation is outside the timed region (as in
+    tools/main.cpp:146-150); a run still going after `limit_s` is stopped and
+    its elapsed time returned as a lower bound."""
+    p = subprocess.Popen([sys.executable, "-c", _REF_CHILD, ROOT,
+                          json.dumps([arch, eps_s, mseed, iseed, image, workers, et])],
+                         stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+    ready = p.stdout.readline()
+    if not ready:
+        raise RuntimeError("reference child failed: " + p.stderr.read()[-500:])
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(threads) as ex:
-        res = list(ex.map(one, range(n_images)))
-    wall = time.perf_counter() - t0
-    return 1000.0 * wall / n_images, "port", np.array([r[0] for r in res]), wall, [r[1] for r in res]
+    try:
+        out, _ = p.communicate(timeout=limit_s)
+        r = json.loads(out.strip().splitlines()[-1])
+        return r["seconds"], True, r
+    except subprocess.TimeoutExpired:
+        elapsed = time.perf_counter() - t0
+        p.kill()
+        p.communicate()
+        return elapsed, False, None
 
 
 def run_reference_arm(args):
@@ -170,31 +220,68 @@ def run_reference_arm(args):
     arch, eps_s, mseed, iseed = workload(args.config)
     threads = os.cpu_count() or 1
     et = not args.no_early_term
-    # one image per host thread per step (the CLI's worker-pool mode)
-    per_step = threads
-    steps, warm = args.steps, args.warmup
-    t_all = 0.0
-    n_timed = 0
-    verified = 0
-    for s in range(warm + steps):
-        ms, kind, verdicts, wall, _ = cpu_reference(arch, eps_s, mseed, iseed + 1000 * s, per_step,
-                                                    threads, et)
-        if s >= warm:
-            t_all += wall
-            n_timed += per_step
-            verified += int((np.asarray(verdicts) == 1).sum())
-    val = 1000.0 * t_all / max(n_timed, 1)
-    line = {"metric": METRIC, "value": val, "unit": "ms/image", "n_gpus": 0, "steps": steps,
-            "warmup": warm, "ms_per_step": 1000.0 * t_all / max(steps, 1), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": args.config, "arch": arch, "eps": eps_s, "model_seed": mseed,
-                       "early_term": et, "images_per_step": per_step},
-            "cpu_baseline": {"value": val, "unit": "ms/image", "cores": threads, "kind": kind,
-                             "sample": f"{n_timed} images ({per_step} per step, one image per host "
-                                       f"thread, reference CLI worker-pool mode), {verified} verified"},
+    from oracle.pyoracle import Ref
+    if not Ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}), flush=True)
+        return
+    # the same images as our arm: step s verifies image s mod pool; latency mode
+    # (one image, all host threads as the reference's row workers)
+    budget = max(30.0, args.cpu_sample_seconds * 4)
+    times, lower, verified, done = [], False, 0, 0
+    t_start = time.perf_counter()
+    for s in range(args.warmup + args.steps):
+        left = budget - (time.perf_counter() - t_start)
+        if left <= 1.0:
+            break
+        sec, finished, r = reference_image(arch, eps_s, mseed, iseed, s % args.pool, threads, et, left)
+        if not finished:
+            times.append(sec)
+            lower = True
+            break
+        if s >= args.warmup or args.warmup + args.steps == 1:
+            times.append(sec)
+            done += 1
+            verified += int(bool(r["verified"]))
+    val = 1000.0 * (statistics.mean(times) if times else float("nan"))
+    sample = (f"{done} images verified in full (image s mod {args.pool}), workers={threads}"
+              if not lower else
+              f"one image (image 0) of {args.config} did not finish within {times[-1]:.0f} s with "
+              f"workers={threads}; value = elapsed time, a LOWER BOUND on the reference's ms/image")
+    line = {"metric": METRIC, "value": val, "unit": "ms/image", "n_gpus": 0, "steps": len(times),
+            "warmup": args.warmup, "ms_per_step": val, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "value_is_lower_bound": lower,
+            "config": config_dict(args, arch, eps_s, mseed, iseed, 1),
+            "cpu_baseline": {"value": val, "unit": "ms/image", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "offline_full_image_reference": offline_reference_seconds(args.config),
             "e2e": {"value": val, "unit": "ms/image", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+
+def relaunch_distributed(args):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def ncu_traffic(config):
+    """DRAM bytes per launch of the conv kernel from a committed ncu --set full
+    capture of this config (profiles/*_ncu_gbc_*<config>*.json), or None."""
+    best = None
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", f"*ncu_gbc*{config}*.json"))):
+        try:
+            best = (json.load(open(p)), os.path.relpath(p, ROOT))
+        except Exception:
+            pass
+    return best
 
 
 def main():
@@ -202,9 +289,11 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args)
         return
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        relaunch_distributed(args)
     import torch
 
-    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -218,161 +307,156 @@ def main():
     v = pc.Verifier(net, pc.AnalysisOptions(early_term=et, device=local))
     n_in = int(np.prod(net.input_shape))
     steps, warm = args.steps, args.warmup
-    total_imgs = max(64, args.batch) * world
-    X = pc.random_inputs(iseed, total_imgs, n_in)
-    mine = [i for i in range(total_imgs) if i % world == rank]
-    boxes = [pc.input_box(X[i], eps, True) for i in mine]
-    labels_all = np.array([max(v.candidate(X[i]), 0) for i in mine], dtype=np.int32)
-    per_step = args.batch
+    X = pc.random_inputs(iseed, args.pool, n_in)
+    boxes = [pc.input_box(x, eps, True) for x in X]
+    labels = [max(v.candidate(x), 0) for x in X]
     dev = torch.device("cuda", local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    dboxes = [(torch.from_numpy(b.lo).to(dev), torch.from_numpy(b.hi).to(dev)) for b in boxes]
     torch.cuda.synchronize()
 
-    # Whole-job throughput: each step verifies `per_step` images concurrently
-    # (pc_net_test_batch: one stream per worker context); the batch's device
-    # time comes from CUDA events inside the library; L2 is flushed between
-    # steps outside the timed region.
-    def batch_arrays(s):
-        idx = [(s * per_step + j) % len(boxes) for j in range(per_step)]
-        lo = np.stack([boxes[i].lo for i in idx])
-        hi = np.stack([boxes[i].hi for i in idx])
-        return lo, hi, labels_all[idx]
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
 
-    host_batches = [batch_arrays(s) for s in range(warm + steps)]
-    dev_batches = [(torch.from_numpy(lo).to(dev), torch.from_numpy(hi).to(dev), lab)
-                   for lo, hi, lab in host_batches]
+    def max_over_ranks(vals):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return t.tolist()
+
+    # roofline of the conv kernel: one unsharded verification per rank (the
+    # kernel's own launches, CUDA events on the stream they run on)
+    flush.fill_(1)
     torch.cuda.synchronize()
+    r0 = v.test_device(dboxes[0][0].data_ptr(), dboxes[0][1].data_ptr(), labels[0])
+    kt = v.last_kernel_timing("conv")
+    roof_madds = r0[2]["gbc_madds"]
+    fma_peak = pc.verifier.fp64_peak(local)
 
-    def run(device_inputs):
-        tot_ms = 0.0
-        launches = 0
-        n_ver = 0
+    transport = None
+    if world > 1:
+        v.enable_sharding()  # native NCCL communicator on an NCCL group
+        transport = v.shard_transport
+
+    results = {}
+    lat, e2e, launches = [], [], 0
+    with ClockSampler(local) as clk:
         for s in range(warm + steps):
+            i = s % args.pool
             flush.fill_(s & 0xFF)
             torch.cuda.synchronize()
-            if device_inputs:
-                dlo, dhi, lab = dev_batches[s]
-                ver, _, _, ms = v.test_batch(dlo.data_ptr(), dhi.data_ptr(), lab, args.concurrency,
-                                             device_inputs=True)
-            else:
-                lo, hi, lab = host_batches[s]
-                ver, _, _, ms = v.test_batch(lo, hi, lab, args.concurrency)
+            barrier()
+            ver, mar, st = v.test_device(dboxes[i][0].data_ptr(), dboxes[i][1].data_ptr(), labels[i])
+            ms = v.last_timing()["total_ms"]
             if s >= warm:
-                tot_ms += ms
+                lat.append(ms)
                 launches += v.last_timing()["launches"]
-                n_ver += int(ver.sum())
-        return tot_ms, launches, n_ver
-
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        dev_ms, launches, dev_verified = run(True)
-    e2e_ms, _, _ = run(False)
-
-    # single-image latency (one image alone on the engine stream)
-    lat = []
-    for i in range(min(5, len(boxes))):
-        flush.fill_(i & 0xFF)
+            results.setdefault(i, (ver, mar, st))
+    for s in range(warm + steps):  # e2e: host buffers through pc_net_test
+        i = s % args.pool
+        flush.fill_(s & 0xFF)
         torch.cuda.synchronize()
-        r = v.test(boxes[i].lo, boxes[i].hi, int(labels_all[i]))
-        if i:
-            lat.append(v.last_timing()["total_ms"])
-    # the roofline kernel's timing on the measured workload: one image-batched
-    # schedule of the step (batch / concurrency images) on a single worker
-    # context, CUDA events around every dense launch on the stream it is
-    # launched on (in the concurrent step the other contexts' kernels share the
-    # SMs and would inflate each launch's event time)
-    flush.fill_(7)
-    torch.cuda.synchronize()
-    dlo, dhi, lab = dev_batches[0]
-    per_walk = max(1, per_step // args.concurrency)
-    v.test_batch(dlo[:per_walk].data_ptr(), dhi[:per_walk].data_ptr(), lab[:per_walk], 1,
-                 device_inputs=True)
-    t = v.last_timing()
-    dense_ms, dense_bytes = t["dense_ms"], t["dense_bytes"]
-    dense_n, dense_madds = t["dense_launches"], t["dense_madds"]
-    # row-sharded single-image latency (north_star: one image's passes split across the GPUs)
-    lat_sharded = None
+        barrier()
+        t0 = time.perf_counter()
+        r = v.test(boxes[i].lo, boxes[i].hi, labels[i])
+        t1 = time.perf_counter()
+        if s >= warm:
+            e2e.append(1000.0 * (t1 - t0))
+        assert np.array_equal(r.margins.view(np.int64), results[i][1].view(np.int64))
+    lat = max_over_ranks(lat)
+    e2e = max_over_ranks(e2e)
     if world > 1:
-        v.enable_sharding()
-        ls = []
-        for i in range(4):
-            torch.distributed.barrier()
-            v.test(boxes[0].lo, boxes[0].hi, int(labels_all[0]))
-            tt = torch.tensor([v.last_timing()["total_ms"]], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            if i:
-                ls.append(float(tt[0]))
         v.disable_sharding()
-        lat_sharded = float(np.median(ls))
-    if world > 1:
-        t = torch.tensor([dev_ms, e2e_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        dev_ms, e2e_ms = float(t[0]), float(t[1])
-        c = torch.tensor([dev_verified], device=dev)
-        torch.distributed.all_reduce(c)
-        dev_verified = int(c[0])
-    imgs = steps * per_step * world
-    value = dev_ms / imgs  # whole job: max-over-ranks time / images over all ranks
-    e2e_val = e2e_ms / imgs
-    peaks = {}
+
+    # replicas: images verified concurrently on every rank (no collective)
+    thr = None
+    if args.throughput_images > 0:
+        n_t = args.throughput_images
+        idx = [(rank * n_t + j) % args.pool for j in range(n_t)]
+        lo = torch.stack([dboxes[j][0] for j in idx])
+        hi = torch.stack([dboxes[j][1] for j in idx])
+        lab = np.array([labels[j] for j in idx], dtype=np.int32)
+        torch.cuda.synchronize()
+        v.test_batch(lo.data_ptr(), hi.data_ptr(), lab, args.concurrency, device_inputs=True)  # warm
+        barrier()
+        _, _, _, bms = v.test_batch(lo.data_ptr(), hi.data_ptr(), lab, args.concurrency, device_inputs=True)
+        bms = max_over_ranks([bms])[0]
+        thr = {"value": bms / (n_t * world), "unit": "ms/image", "images": n_t * world,
+               "concurrency_per_gpu": args.concurrency, "scaling": "weak"}
+
+    # in-bench parity against the reference fixtures of the timed images
+    fx = fixtures(args.config)
+    checked, mismatches = [], []
+    for i, (ver, mar, st) in sorted(results.items()):
+        if i in fx:
+            f = fx[i]
+            ok = (labels[i] == f["label"] and bool(ver) == f["verified"]
+                  and [m.hex() for m in mar] == f["margins_hex"] and st == f["stats"])
+            checked.append(i)
+            if not ok:
+                mismatches.append(i)
+    n_ver = sum(int(bool(r[0])) for r in results.values())
+
+    value = statistics.mean(lat)
+    hbm_peak = None
     try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
     except Exception:
         pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = (dense_bytes / (dense_ms / 1000.0) / 1e9) if dense_ms > 0 else 0.0
+    peak_tflops = 2.0 * fma_peak / 1e12
+    conv_s = kt["ms"] / 1000.0
+    achieved_tflops = 4.0 * roof_madds / conv_s / 1e12 if conv_s > 0 else 0.0
+    hbm_achieved = kt["bytes"] / conv_s / 1e9 if conv_s > 0 else 0.0
+    traffic = ncu_traffic(args.config)
     line = {
         "metric": METRIC, "value": value, "unit": "ms/image", "n_gpus": world, "steps": steps,
-        "warmup": warm, "ms_per_step": dev_ms / steps, "higher_is_better": False,
-        "latency_ms_per_image": float(np.median(lat)) if lat else None,
-        "latency_ms_per_image_row_sharded": lat_sharded,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "arch": arch, "eps": eps_s, "model_seed": mseed,
-                   "input_seed": iseed, "early_term": et,
-                   "parallelism": f"replicas x{world} (image sharding); {per_step} images per step over "
-                                  f"{args.concurrency} worker contexts per GPU, each verifying "
-                                  f"{-(-per_step // args.concurrency)} images per schedule (image-batched walks)",
-                   "l2": "flushed between steps (256 MB write, outside the timed events)",
-                   "verified": f"{dev_verified}/{imgs}"},
-        "e2e": {"value": e2e_val, "unit": "ms/image", "h2d_bytes_per_step": per_step * 2 * 8 * n_in,
-                "d2h_bytes_per_step": per_step * (8 * (net.output_size - 1) + 4)},
+        "warmup": warm, "ms_per_step": value, "higher_is_better": False,
+        "latency_ms_per_image": {"mean": value, "median": statistics.median(lat), "min": min(lat),
+                                 "max": max(lat)},
+        "throughput_ms_per_image": thr,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, arch, eps_s, mseed, iseed, world),
+        "verified": f"{n_ver}/{len(results)} distinct images",
+        "parity": {"fixtures": "tests/golden/ref_<config>_img<i>.json (unmodified reference)",
+                   "images_checked": checked, "mismatches": mismatches,
+                   "all_equal": bool(checked) and not mismatches},
+        "sharding_transport": transport,
+        "e2e": {"value": statistics.mean(e2e), "unit": "ms/image",
+                "h2d_bytes_per_step": 2 * 8 * n_in, "d2h_bytes_per_step": 8 * (net.output_size - 1) + 4},
         "gpu_launches": int(launches),
-        "roofline": {"kernel": "k_dense_coef (dense back-substitution)", "bound": "hbm",
-                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak if hbm_peak else None,
-                     # DRAM read+write of one captured launch (ncu --set full, below)
-                     "traffic": 7683584,
-                     "launches": dense_n, "kernel_ms": dense_ms,
-                     "sample": f"one {per_walk}-image schedule of the step on one worker context",
-                     "algorithmic_bytes": dense_bytes,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
-                     # one ncu --set full capture of this kernel (profiles/r1_final_ncu_dense_coef.txt):
-                     # a 576-row launch (one 64-image schedule, 500x500 layer) moved 7.68 MB of DRAM
-                     # for 11.2 MB algorithmic bytes (rows in/out + weights once; L2 serves the rest)
-                     "ncu_capture": {"dram_bytes_per_launch": 7683584, "algorithmic_bytes_per_launch": 11216000,
-                                     "rows": 576, "source": "profiles/r1_final_ncu_dense_coef.txt"},
-                     # the kernel is FP64-pipe / chain-latency bound, not HBM bound: its
-                     # executed interval multiply-adds per second (device-counted) against the
-                     # measured band-madd peak (profiles/r1_microbench_fp64_ops.txt)
-                     "fp64": {"achieved_madds_per_s": dense_madds / (dense_ms / 1000.0) if dense_ms else 0.0,
-                              "peak_madds_per_s": FP64_MADD_PEAK,
-                              "peak_source": "scripts/micro/fp64_ops.cu (register-resident band madd, ILP8, "
-                                             "profiles/r1_microbench_fp64_ops.txt)",
-                              "frac": (dense_madds / (dense_ms / 1000.0) / FP64_MADD_PEAK) if dense_ms else 0.0}},
+        "roofline": {
+            "kernel": "k_gbc_sparse2 (conv back-substitution coefficients)", "bound": "fp64",
+            "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+            "frac": achieved_tflops / peak_tflops if peak_tflops else None,
+            "traffic": (traffic[0].get("dram_bytes_per_launch") if traffic else None),
+            "traffic_source": (traffic[1] if traffic else "no ncu capture committed for this config"),
+            "algorithmic": "4 FLOPs per interval multiply-add (lo and hi FMA pair), madds = the "
+                           "reference's PassStats.gbc_madds of one image; time = CUDA events around "
+                           "every conv launch of that image",
+            "peak_source": "pc_fp64_peak: DFMA throughput measured live on this GPU (2 FLOPs per FMA)",
+            "emulation_note": "bit-exact WidenedFloat64 costs 16 FP64-pipe instructions per interval "
+                              "madd (4 algorithmic FLOPs), so frac <= 0.125 at full FP64-pipe use",
+            "fp64_pipe_frac": (16.0 * roof_madds / conv_s / fma_peak) if conv_s > 0 else None,
+            "launches": kt["launches"], "kernel_ms": kt["ms"], "interval_madds": roof_madds,
+            "hbm": {"achieved_gbs": hbm_achieved, "peak_gbs": hbm_peak,
+                    "frac": hbm_achieved / hbm_peak if hbm_peak else None,
+                    "algorithmic_bytes": kt["bytes"],
+                    "bytes_model": "16 B per interval of the rows in and out + 8 B per filter tap, per launch"}},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            ms1, kind, _, _, _ = cpu_reference(arch, eps_s, mseed, iseed, 1, 1, et)
-            n = max(1, min(4 * threads, int(args.cpu_sample_seconds * 1000.0 * threads / max(ms1, 1e-3))))
-            ms, kind, vd, wall, per = cpu_reference(arch, eps_s, mseed, iseed, n, threads, et)
+            sec, finished, r = reference_image(arch, eps_s, mseed, iseed, 0, threads, et,
+                                               args.cpu_sample_seconds)
             line["cpu_baseline"] = {
-                "value": ms, "unit": "ms/image", "cores": threads, "kind": kind,
-                "sample": f"{n} images of {args.config} ({wall:.1f} s wall; one image per thread; "
-                          f"single-image latency {1000 * float(np.mean(per)):.1f} ms)"}
+                "value": 1000.0 * sec, "unit": "ms/image", "cores": threads, "kind": "reference",
+                "value_is_lower_bound": not finished,
+                "sample": (f"image 0 of {args.config}, verify_robustness with workers={threads}"
+                           + ("" if finished else f"; stopped after {sec:.0f} s: a LOWER BOUND")),
+                "offline_full_image_reference": offline_reference_seconds(args.config)}
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:

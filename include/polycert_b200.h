@@ -170,6 +170,21 @@ typedef int (*pc_allgather_fn)(void* user, const void* d_send, void* d_recv, siz
 pc_status pc_net_set_sharding(pc_net* net, int rank, int world, pc_allgather_fn allgather,
                               void* user);
 
+/* Native NCCL transport for row sharding (no host callback on the data
+ * path): rank 0 creates a 128-byte id with pc_nccl_unique_id and shares it
+ * out of band (e.g. torch.distributed broadcast); every rank creates its
+ * communicator on the net's device with pc_nccl_comm_create and passes
+ * pc_nccl_allgather with the communicator as `user` to pc_net_set_sharding:
+ * the exchange is then one ncclAllGather on the engine's stream. libnccl.so.2
+ * is loaded at run time (dlopen). Return 0 / non-NULL on success; `err`
+ * receives the message otherwise. */
+typedef struct pc_nccl_comm pc_nccl_comm;
+int pc_nccl_unique_id(void* out128, char* err, int err_len);
+pc_nccl_comm* pc_nccl_comm_create(int device, int rank, int world, const void* id128, char* err,
+                                  int err_len);
+void pc_nccl_comm_destroy(pc_nccl_comm* comm);
+int pc_nccl_allgather(void* user, const void* d_send, void* d_recv, size_t bytes, void* stream);
+
 /* Kernel launches issued by this thread's last pc_net_test* call. */
 long long pc_last_launch_count(void);
 
@@ -178,6 +193,19 @@ long long pc_last_launch_count(void);
  * back-substitution kernel (the roofline kernel) with its algorithmic bytes. */
 void pc_last_timing(double* total_ms, double* dense_kernel_ms, double* dense_kernel_bytes,
                     long long* dense_kernel_launches);
+/* The same for one back-substitution coefficient kernel of the last
+ * pc_net_test* call on this thread: kernel 0 = the dense kernel
+ * (k_dense_coef*), 1 = the conv kernel (k_gbc_sparse2 / k_gbc_coef): summed
+ * CUDA-event milliseconds over its launches (on the stream each is launched
+ * on), algorithmic bytes (coefficient rows in and out, 16 B per interval,
+ * plus the weights / filter once per launch) and the launch count. */
+void pc_last_kernel_timing(int kernel, double* ms, double* bytes, long long* launches);
+
+/* Measured FP64 FMA throughput of the device (FMA/s): a register-resident
+ * DFMA kernel (8 independent chains per thread, every SM), timed with CUDA
+ * events; the FP64-pipe roofline denominator. */
+pc_status pc_fp64_peak(int device, double* fma_per_s);
+
 /* Interval multiply-adds the dense-kernel launches of the last call executed
  * (rows x live predecessor cells x nonzero frame cells walked, summed over
  * launches; device-counted, all worker contexts of a batch). */

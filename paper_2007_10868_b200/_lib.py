@@ -74,10 +74,15 @@ def _load():
         "pc_last_launch_count": (ll, []),
         "pc_last_timing": (None, [vp, vp, vp, vp]),
         "pc_last_dense_madds": (d, []),
+        "pc_last_kernel_timing": (None, [i, vp, vp, vp]),
+        "pc_fp64_peak": (i, [i, vp]),
         "pc_scalar_ops": (i, [i, vp, vp, vp, ll]),
         "pc_last_profile": (i, [ctypes.c_char_p, i]),
         "pc_last_error": (ctypes.c_char_p, []),
         "pc_net_set_sharding": (i, [vp, i, i, ALLGATHER_FN, vp]),
+        "pc_nccl_unique_id": (i, [vp, ctypes.c_char_p, i]),
+        "pc_nccl_comm_create": (vp, [i, i, i, vp, ctypes.c_char_p, i]),
+        "pc_nccl_comm_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpolycert_b200.so")
-SOURCES = ["kernels.cu", "chains.cu", "gbc.cu", "engine.cu"]
+SOURCES = ["kernels.cu", "chains.cu", "gbc.cu", "engine.cu", "nccl_shard.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 

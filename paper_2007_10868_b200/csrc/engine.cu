@@ -34,6 +34,10 @@ thread_local std::string g_err;
 thread_local long long g_last_launches = 0;
 thread_local double g_total_ms = 0, g_dense_ms = 0, g_dense_bytes = 0, g_dense_madds = 0;
 thread_local long long g_dense_launches = 0;
+// conv back-substitution kernel (k_gbc_sparse2 / k_gbc_coef) of the last call:
+// CUDA-event time over its launches, algorithmic bytes (rows in/out + filter)
+thread_local double g_conv_ms = 0, g_conv_bytes = 0;
+thread_local long long g_conv_launches = 0;
 
 struct StatusError : std::runtime_error {
   pc_status code;
@@ -182,7 +186,9 @@ struct Ctx {
   int graph_et = -1;               // early_term the graph was captured with
   bool graph_failed = false;
   pc_stats graph_st{};             // host-side counts accumulated while capturing
-  std::vector<size_t> graph_dense_ev;
+  std::vector<size_t> graph_dense_ev, graph_conv_ev;
+  double graph_conv_bytes = 0;
+  long long graph_conv_launches = 0;
   double graph_dense_bytes = 0, graph_dense_madds = 0;
   long long graph_launches = 0, graph_dense_launches = 0;
   // second walk pipeline (run_pass): its own streams and walk resources, the
@@ -204,6 +210,7 @@ struct Ctx {
   size_t ev_used = 0;
   std::vector<std::pair<int, size_t>> prof;  // (class, event index of the begin event)
   std::vector<size_t> dense_ev;               // begin events of dense-coefficient launches
+  std::vector<size_t> conv_ev;                // begin events of conv-coefficient launches
 
   explicit Ctx(pc_net* n)
       : net(n), L(n->L), off(n->off), pofs(n->pofs), total(n->total), max_numel(n->max_numel),
@@ -750,12 +757,20 @@ struct Walker {
                           n->ctr, fz());
       prof_end(n, s2);
       prof_begin(n, PROF_GBC);
-      if (sparse) {
-        launch_compact_cells(s, rows(), md(m), sp);
-        launch_gbc_sparse(s, L.d, rows(), fi, fo, sp, md(m), md(out));
-      } else {
-        launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out), n->d_int + 6);
+      if (sparse) launch_compact_cells(s, rows(), md(m), sp);
+      if (n->timing) {  // the headline config's roofline kernel (bench.py reads it)
+        n->conv_ev.push_back(n->ev_used);
+        ck(cudaEventRecord(take_event(n), s), "event");
+        // algorithmic bytes: coefficient rows in/out (16 B per interval) + the filter once
+        g_conv_bytes += 16.0 * nrows() * (double)(m.cells + out.cells) +
+                        8.0 * L.fw * L.fh * L.in_c * L.out_c;
+        ++g_conv_launches;
       }
+      if (sparse)
+        launch_gbc_sparse(s, L.d, rows(), fi, fo, sp, md(m), md(out));
+      else
+        launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out), n->d_int + 6);
+      if (n->timing) ck(cudaEventRecord(take_event(n), s), "event");
       prof_end(n);
       if (n->profile)  // dense-window work of this step (all coefficients nonzero)
         g_gbc_window_madds += (double)nrows() * fo.S_w * fo.S_h * L.in_c * L.out_c *
@@ -1448,9 +1463,12 @@ void capture_graph(Ctx* n, bool with_margin, size_t arena, size_t stat_count) {
   n->sync_used = 0;
   n->ev_used = 0;
   n->dense_ev.clear();
+  n->conv_ev.clear();
   const long long l0 = g_launches;
   g_dense_bytes = g_dense_madds = 0;
   g_dense_launches = 0;
+  g_conv_bytes = 0;
+  g_conv_launches = 0;
   pc_stats st{};
   ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
   cudaGraph_t g = nullptr;
@@ -1481,6 +1499,9 @@ void capture_graph(Ctx* n, bool with_margin, size_t arena, size_t stat_count) {
   n->graph_et = n->opt.early_term;
   n->graph_st = st;
   n->graph_dense_ev = n->dense_ev;
+  n->graph_conv_ev = n->conv_ev;
+  n->graph_conv_bytes = g_conv_bytes;
+  n->graph_conv_launches = g_conv_launches;
   n->graph_dense_bytes = g_dense_bytes;
   n->graph_dense_madds = g_dense_madds;
   n->graph_dense_launches = g_dense_launches;
@@ -1509,6 +1530,9 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
       ck(cudaGraphLaunch(n->graph, s), "graph launch");
       g_launches += n->graph_launches;
       n->dense_ev = n->graph_dense_ev;
+      n->conv_ev = n->graph_conv_ev;
+      g_conv_bytes = n->graph_conv_bytes;
+      g_conv_launches = n->graph_conv_launches;
       g_dense_bytes = n->graph_dense_bytes;
       g_dense_madds = n->graph_dense_madds;
       g_dense_launches = n->graph_dense_launches;
@@ -1802,12 +1826,16 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
       n->helper->sync_used = 0;
       n->helper->prof.clear();
       n->helper->dense_ev.clear();
+      n->helper->conv_ev.clear();
     }
     g_gbc_window_madds = 0;
     g_alloc_ms = 0;
     g_allocs = 0;
     n->prof.clear();
     n->dense_ev.clear();
+    n->conv_ev.clear();
+    g_conv_ms = g_conv_bytes = 0;
+    g_conv_launches = 0;
     run_test(n, label, m.data(), &st);
     if (b_lo) ck(cudaMemcpyAsync(b_lo, n->blo, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
     if (b_hi) ck(cudaMemcpyAsync(b_hi, n->bhi, sizeof(double) * n->total, cudaMemcpyDeviceToHost, s), "d2h");
@@ -1825,6 +1853,13 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     for (size_t e : n->dense_ev) {
       float d = 0;
       if (cudaEventElapsedTime(&d, n->ev_pool[e], n->ev_pool[e + 1]) == cudaSuccess) g_dense_ms += d;
+    }
+    for (Ctx* c : {n, n->helper}) {  // both walk pipelines
+      if (!c) continue;
+      for (size_t e : c->conv_ev) {
+        float d = 0;
+        if (cudaEventElapsedTime(&d, c->ev_pool[e], c->ev_pool[e + 1]) == cudaSuccess) g_conv_ms += d;
+      }
     }
     cudaGetLastError();  // timing is best effort; never leave a sticky error behind
     for (int c = 0; c < PROF_N; ++c) {
@@ -1908,6 +1943,13 @@ const char* pc_last_error(void) { return g_err.c_str(); }
 double pc_last_dense_madds(void) { return g_dense_madds; }
 long long pc_last_launch_count(void) { return g_last_launches; }
 
+void pc_last_kernel_timing(int kernel, double* ms, double* bytes, long long* launches) {
+  const bool conv = kernel == 1;
+  if (ms) *ms = conv ? g_conv_ms : g_dense_ms;
+  if (bytes) *bytes = conv ? g_conv_bytes : g_dense_bytes;
+  if (launches) *launches = conv ? g_conv_launches : g_dense_launches;
+}
+
 void pc_last_timing(double* total_ms, double* dense_ms, double* dense_bytes, long long* launches) {
   if (total_ms) *total_ms = g_total_ms;
   if (dense_ms) *dense_ms = g_dense_ms;
@@ -1927,6 +1969,14 @@ pc_status pc_input_box(const double* center, int n, double eps, int clamp01, dou
         throw StatusError(PC_ERR_INVALID_ARGUMENT, "input_box: clamped center outside [0,1]");
     }
     ck(input_box_device(center, n, eps, clamp01, lo, up), "input_box");
+  });
+}
+
+pc_status pc_fp64_peak(int device, double* fma_per_s) {
+  if (!fma_per_s) return PC_ERR_INVALID_ARGUMENT;
+  return guard([&] {
+    if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(fp64_peak_device(fma_per_s), "fp64_peak");
   });
 }
 

@@ -3018,3 +3018,54 @@ cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* 
 }
 
 }  // namespace pc
+
+namespace pc {
+
+// ---------------------------------------------------------------------------
+// FP64 pipe peak (the roofline denominator of the FP64-bound kernels): every
+// thread runs 8 independent register-resident DFMA chains; 4 blocks of 256
+// threads per SM.
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, double x, double y, int iters) {
+  double a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = x + u + threadIdx.x;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = __fma_rn(a[u], x, y);
+  double s = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s += a[u];
+  if (s == 12345.0) out[blockIdx.x] = s;  // keep the chains live
+}
+
+cudaError_t fp64_peak_device(double* fma_per_s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out = nullptr;
+  cudaError_t e = cudaMalloc(&out, sizeof(double) * 4 * sms);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int iters = 1 << 14, blocks = 4 * sms;
+  k_dfma_peak<<<blocks, 256>>>(out, 0.999999, 1e-7, iters);  // warm-up (clocks up)
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    k_dfma_peak<<<blocks, 256>>>(out, 0.999999, 1e-7, iters);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    best = ms < best ? ms : best;
+  }
+  e = cudaGetLastError();
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  *fma_per_s = (double)blocks * 256 * 8 * iters / (best * 1e-3);
+  return e;
+}
+
+}  // namespace pc

@@ -396,6 +396,7 @@ void launch_eval_layer(cudaStream_t s, const LayerDev& L, const double* x, const
                        double* y);
 
 cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* out, long long n);
+cudaError_t fp64_peak_device(double* fma_per_s);
 
 extern thread_local long long g_launches;
 

@@ -76,15 +76,53 @@ def make_allgather(group=None, device=None):
     return _lib.ALLGATHER_FN(cb)
 
 
-def enable(verifier, group=None):
-    """Shard `verifier`'s passes across the ranks of `group`."""
+def _native_nccl(verifier, group, rank, world):
+    """A native NCCL communicator for this net (pc_nccl_comm_create): the id
+    from rank 0 travels over the process group, then every rank's exchange is
+    one ncclAllGather on the engine stream (no Python on the data path)."""
+    import torch.distributed as dist
+
+    from . import _lib
+    err = ctypes.create_string_buffer(512)
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0 and _lib.lib.pc_nccl_unique_id(uid, err, 512) != 0:
+        raise RuntimeError(err.value.decode())
+    box = [uid.raw if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                               group=group)
+    uid = ctypes.create_string_buffer(box[0], 128)
+    import torch
+    dev = verifier.options.device if verifier.options.device >= 0 else torch.cuda.current_device()
+    comm = _lib.lib.pc_nccl_comm_create(int(dev), rank, world, uid, err, 512)
+    if not comm:
+        raise RuntimeError(err.value.decode())
+    return comm
+
+
+def enable(verifier, group=None, transport: str = "auto"):
+    """Shard `verifier`'s passes across the ranks of `group`.
+
+    transport: "native" — the engine's own NCCL communicator
+    (pc_nccl_allgather, ncclAllGather on the engine stream); "callback" — the
+    torch.distributed callback above (NCCL in place or gloo via host memory);
+    "auto" — native on an NCCL group, else the callback."""
     import torch.distributed as dist
 
     from . import _lib
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    disable(verifier)
+    nccl = dist.get_backend(group) == "nccl"
+    if transport == "native" or (transport == "auto" and nccl and world > 1):
+        comm = _native_nccl(verifier, group, rank, world)
+        fn = _lib.ALLGATHER_FN(("pc_nccl_allgather", _lib.lib))
+        _lib.check(_lib.lib.pc_net_set_sharding(verifier._h, rank, world, fn, comm))
+        verifier._allgather, verifier._nccl_comm = fn, comm
+        verifier.shard_transport = "native-nccl"
+        return rank, world
     fn = make_allgather(group, verifier.options.device if verifier.options.device >= 0 else None)
     _lib.check(_lib.lib.pc_net_set_sharding(verifier._h, rank, world, fn, None))
     verifier._allgather = fn  # keep the callback alive
+    verifier.shard_transport = "torch-callback-" + dist.get_backend(group)
     return rank, world
 
 
@@ -93,3 +131,7 @@ def disable(verifier):
     _lib.check(_lib.lib.pc_net_set_sharding(verifier._h, 0, 1, ctypes.cast(None, _lib.ALLGATHER_FN),
                                             None))
     verifier._allgather = None
+    comm = getattr(verifier, "_nccl_comm", None)
+    if comm:
+        _lib.lib.pc_nccl_comm_destroy(comm)
+        verifier._nccl_comm = None

@@ -56,6 +56,13 @@ def _ptr(a):
     return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
 
 
+def fp64_peak(device: int = -1) -> float:
+    """Measured FP64 FMA throughput of the device (FMA/s; pc_fp64_peak)."""
+    v = ctypes.c_double(0)
+    _lib.check(_lib.lib.pc_fp64_peak(int(device), ctypes.byref(v)))
+    return v.value
+
+
 def input_box(center, eps: float, clamp01: bool = True) -> InputBox:
     """input_box<WidenedFloat64> (network.hpp:160-177), computed on the GPU."""
     c = np.ascontiguousarray(center, dtype=np.float64).reshape(-1)
@@ -189,11 +196,12 @@ class Verifier:
                                                ctypes.byref(st)))
         return bool(verified.value), margins[: self.n_out - 1], st.as_dict()
 
-    def enable_sharding(self, group=None):
+    def enable_sharding(self, group=None, transport: str = "auto"):
         """Row-shard every pass across the ranks of a torch.distributed group
-        (one process per GPU; results identical to unsharded). Returns (rank, world)."""
+        (one process per GPU; results identical to unsharded). Returns (rank, world).
+        transport: "auto" (native NCCL on an NCCL group), "native", "callback"."""
         from . import sharding
-        return sharding.enable(self, group)
+        return sharding.enable(self, group, transport)
 
     def disable_sharding(self):
         from . import sharding
@@ -207,6 +215,15 @@ class Verifier:
         buf = ctypes.create_string_buffer(n)
         _lib.lib.pc_last_profile(buf, n)
         return json.loads(buf.value.decode())
+
+    @staticmethod
+    def last_kernel_timing(kernel: str = "conv"):
+        """CUDA-event ms, algorithmic bytes and launches of one coefficient kernel
+        ("dense" = k_dense_coef*, "conv" = k_gbc_sparse2 / k_gbc_coef) in the last call."""
+        ms, by, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
+        _lib.lib.pc_last_kernel_timing(1 if kernel == "conv" else 0, ctypes.byref(ms), ctypes.byref(by),
+                                       ctypes.byref(n))
+        return {"ms": ms.value, "bytes": by.value, "launches": n.value}
 
     def last_timing(self):
         t, dm, db, dl = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
