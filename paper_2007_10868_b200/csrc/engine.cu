@@ -124,6 +124,10 @@ struct pc_net {
   Ctx* primary = nullptr;
   // row sharding (pc_net_set_sharding)
   int shard_rank = 0, shard_world = 1;
+  // conv steps onto a ReLU frame compute its live cells only (k_gbc_live);
+  // off when a bias is -0 (an accumulator could then start at -0, and the
+  // +0 terms of dead cells would matter) or PC_LIVE_CELLS=0
+  bool live_cells = true;
   pc_allgather_fn allgather = nullptr;
   void* allgather_user = nullptr;
 
@@ -176,7 +180,9 @@ struct Ctx {
   int* ring_map[kRing] = {};
   int* ring_q[kRing] = {};
   int* d_ringR = nullptr;
-  unsigned long long* d_ck = nullptr;  // the two pipelines' checkpoint tallies
+  double* ckat = nullptr;  // per live row: the checkpoint that froze it (k_ck_count)
+  int* lv_cnt = nullptr;             // live channels per grid position of each ReLU layer
+  unsigned short* lv_idx = nullptr;  // (k_live_build; read by the conv kernel k_gbc_live)
   int* d_label = nullptr;
   int* d_slots = nullptr;
   static constexpr int kSlots = 8192;
@@ -265,8 +271,9 @@ struct Ctx {
       ring_q[k] = dalloc<int>(M);
     }
     d_ringR = dalloc<int>(kRing);
-    d_ck = dalloc<unsigned long long>(2);
-    ck(cudaMemset(d_ck, 0, 2 * sizeof(unsigned long long)), "memset");
+    ckat = dalloc<double>(M);
+    lv_cnt = dalloc<int>((size_t)pofs[nl] * nimg);
+    lv_idx = dalloc<unsigned short>(T);
     d_label = dalloc<int>(nimg);
     d_slots = dalloc<int>(kSlots);
     perm2 = dalloc<int>(2 * M);
@@ -614,7 +621,7 @@ struct Walker {
   std::vector<Pending> pend;
   int gen = 0;
   int cur_slot = -1;  // ring slot holding the current row list (-1: the chunk's own list)
-  unsigned long long* ck_count = nullptr;  // per-walker checkpoint tally (two pipelines)
+  int ck_index = 0;  // checkpoints issued by this walk (1-based index of the last)
 
   int nrows() const { return both ? 2 * R : R; }
   // rows frozen at an earlier checkpoint are skipped by the chain kernels
@@ -766,7 +773,11 @@ struct Walker {
                         8.0 * L.fw * L.fh * L.in_c * L.out_c;
         ++g_conv_launches;
       }
-      if (sparse)
+      if (sparse && n->net->live_cells && n->L[L.pred0].kind == KIND_RELU) {
+        const int nl = (int)n->L.size();
+        const LiveDev lv{n->lv_cnt + n->pofs[L.pred0], n->lv_idx + n->off[L.pred0], n->pofs[nl], n->total};
+        launch_gbc_live(s, L.d, rows(), fi, fo, sp, md(m), md(out), lv);
+      } else if (sparse)
         launch_gbc_sparse(s, L.d, rows(), fi, fo, sp, md(m), md(out));
       else
         launch_gbc_coef(s, L.d, rows(), fi, fo, md(m), md(out), n->d_int + 6);
@@ -844,7 +855,7 @@ struct Walker {
   // margin pass's (:1082-1091). Runs on s2 after m's coefficients.
   void checkpoint(Mat& m) {
     if (dry) return;
-    if (margin) st->checkpoints++;  // pass checkpoints are counted on the device (k_offer)
+    if (!margin) ++ck_index;  // PassStats.checkpoints: walk_checkpoints / k_ck_count
     const int fl = m.f.layer;
     const long long o = n->off[fl];
     need(m);
@@ -869,7 +880,7 @@ struct Walker {
       int* nR = n->d_slots + slot_next++;
       prof_begin(n, PROF_OFFER, s2);
       launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
-                   early_term ? 1 : 0, map, nR, new_q, n->ctr);
+                   early_term ? 1 : 0, map, nR, new_q, n->ctr, n->ckat, ck_index);
       prof_end(n, s2);
       if (allow_freeze && early_term) {
         m.src = map;
@@ -885,7 +896,7 @@ struct Walker {
     if (!(allow_freeze && early_term)) {
       prof_begin(n, PROF_OFFER, s2);
       launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, allow_freeze ? 1 : 0,
-                   early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr, ck_count);
+                   early_term ? 1 : 0, n->perm, n->d_int + 1, new_q, n->ctr, n->ckat, ck_index);
       prof_end(n, s2);
       return;
     }
@@ -896,7 +907,7 @@ struct Walker {
     }
     prof_begin(n, PROF_OFFER, s2);
     launch_offer(s2, rows(), R, n->vals, n->rvals, n->cand, n->frozen, 1, 1, n->ring_map[slot],
-                 n->d_ringR + slot, n->ring_q[slot], n->ctr, ck_count);
+                 n->d_ringR + slot, n->ring_q[slot], n->ctr, n->ckat, ck_index);
     prof_end(n, s2);
     const int ckx = ck_next;
     ck_next = (ck_next + 1) % Ctx::kCkSlots;
@@ -1043,6 +1054,105 @@ Frame initial_frame(const Ctx* n, int t, bool affine) {
   return f;
 }
 
+// Checkpoints of a full walk of pass t (no row leaving early): the affine
+// init, every dense / conv / join step, and a final one when the walk reaches
+// the input through a relu (walk_back, backsub.hpp:854-893; :1056).
+int walk_checkpoints(const Ctx* n, const Frame& f0, bool affine) {
+  int cnt = affine ? 1 : 0, layer = f0.layer;
+  bool pending = false;
+  while (layer != 0) {
+    const HostLayer& L = n->L[layer];
+    if (L.kind == KIND_RELU) {
+      pending = true;
+      layer = L.pred0;
+      continue;
+    }
+    ++cnt;
+    pending = false;
+    layer = L.kind == KIND_JOIN ? L.head : L.pred0;
+  }
+  return cnt + (pending ? 1 : 0);
+}
+
+// The reference's rows_per_chunk (backsub.hpp:969-987) over its own geometry
+// dry run (peak_row_cells / sim_walk, :895-967: unclamped cuboid widths, the
+// additive join-union rule). The GPU sizes its own chunks from the clamped
+// frames (walk_size); this only reproduces the reference's chunking for
+// PassStats.checkpoints, which counts per chunk. memory_budget: the call's
+// (the reference default, 1 GiB, when 0).
+struct SimSt {
+  bool dense;
+  long long ww, wh;
+};
+long long sim_cells(const Ctx* n, int layer, const SimSt& st) {
+  const HostLayer& L = n->L[layer];
+  return st.dense ? L.numel() : st.ww * st.wh * L.out_c;
+}
+std::pair<SimSt, long long> sim_walk(const Ctx* n, int layer, SimSt st, int stop) {
+  long long peak = sim_cells(n, layer, st);
+  while (layer != stop) {
+    const HostLayer& L = n->L[layer];
+    if (layer == 0) return {st, peak};
+    switch (L.kind) {
+      case KIND_DENSE:
+        st = {true, 0, 0};
+        layer = L.pred0;
+        break;
+      case KIND_CONV:
+        if (!st.dense) {  // grow_width on int, after the reference's 2^20 clamp
+          st.ww = (long long)(((int)std::min<long long>(st.ww, 1 << 20) - 1) * L.sw + L.fw);
+          st.wh = (long long)(((int)std::min<long long>(st.wh, 1 << 20) - 1) * L.sh + L.fh);
+        }
+        layer = L.pred0;
+        break;
+      case KIND_RELU:
+        layer = L.pred0;
+        break;
+      case KIND_JOIN: {
+        const auto a = sim_walk(n, L.pred0, st, L.head);
+        const auto b = sim_walk(n, L.pred1, st, L.head);
+        peak = std::max(peak, a.second + b.second);
+        layer = L.head;
+        if (a.first.dense || b.first.dense) st = {true, 0, 0};
+        else st = {false, a.first.ww + b.first.ww, a.first.wh + b.first.wh};
+        break;
+      }
+      default:
+        return {st, peak};
+    }
+    peak = std::max(peak, sim_cells(n, layer, st));
+  }
+  return {st, peak};
+}
+long long ref_rows_per_chunk(const Ctx* n, int t) {
+  if (n->opt.chunk_rows > 0) return n->opt.chunk_rows;
+  const HostLayer& Q = n->L[t];
+  SimSt st{true, 0, 0};
+  int start = t;
+  if (Q.kind == KIND_CONV) {
+    st = {false, Q.fw, Q.fh};
+    start = Q.pred0;
+  } else if (Q.kind == KIND_DENSE) {
+    start = Q.pred0;
+  } else if (Q.out_w > 1 || Q.out_h > 1) {
+    st = {false, 1, 1};
+  }
+  const long long cells = std::max<long long>(sim_walk(n, start, st, 0).second, 1);
+  const long long per_row = cells * 16 * 4 + 1024;
+  const long long mb = n->opt.memory_budget > 0 ? n->opt.memory_budget : (1ll << 30);
+  return std::max<long long>(1, std::max(mb, per_row) / per_row);
+}
+
+// After a pass's walks: PassStats.checkpoints under the reference's chunking
+// (keys = the pass's live rows, count at n_keys on the device).
+void count_checkpoints(Ctx* n, int t, bool affine, bool allow_freeze, const int* keys,
+                       const int* n_keys, int kq, int nimg) {
+  const int T = walk_checkpoints(n, initial_frame(n, t, affine), affine);
+  const bool all_full = !(allow_freeze && n->opt.early_term);
+  launch_ck_count(n->stream, keys, n_keys, kq, nimg, ref_rows_per_chunk(n, t), T, all_full ? 1 : 0,
+                  n->ckat, n->ctr);
+}
+
 // Workspace of pass t: bytes per query row (both polarities; the arena is a
 // bump allocator reset per chunk, so this is the walk's total) and the number
 // of allocations (each may round up by < 256 B).
@@ -1159,6 +1269,9 @@ Ctx* helper_of(Ctx* n) {
   h->is_helper = true;
   h->blo = n->blo; h->bhi = n->bhi; h->rlo = n->rlo; h->rhi = n->rhi;
   h->dev = n->dev; h->relax = n->relax; h->cand = n->cand; h->frozen = n->frozen;
+  h->ckat = n->ckat;
+  h->lv_cnt = n->lv_cnt;
+  h->lv_idx = n->lv_idx;
   h->live = n->live; h->ctr = n->ctr;
   h->gen_n = n->gen_n; h->gen_pos = n->gen_pos; h->gen_l = n->gen_l;
   h->budget = n->budget;
@@ -1210,6 +1323,7 @@ void run_pass_graph(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   const bool et = n->opt.early_term != 0;
   launch_seed(s, N, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o, allow_freeze ? 1 : 0, et ? 1 : 0,
               n->cand, n->frozen, n->live, n->d_int, &n->ctr->pad);
+  launch_ck_fill(s, n->live, n->d_int, N, n->ckat);
   st->rows_total += N;
   const bool affine = Q.kind == KIND_DENSE || Q.kind == KIND_CONV;
   const WalkSize ws = walk_size(n, t, affine, true);
@@ -1236,6 +1350,7 @@ void run_pass_graph(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   if (affine) w.checkpoint(m);
   w.walk(m, 0, true);
   stream_wait(n, s, n->stream2);
+  count_checkpoints(n, t, affine, allow_freeze, n->live, n->d_int, 0, 1);
   ++n->gen;
   launch_writeback(s, N, Q.out_c, t, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
                    Q.feeds_relu ? n->relax + 8 * o : nullptr, n->gen_n, n->gen_pos, n->gen_l,
@@ -1252,6 +1367,7 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   launch_seed(s, N, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o, allow_freeze ? 1 : 0, et ? 1 : 0,
               n->cand, n->frozen, n->live, n->d_int, &n->ctr->pad);
   prof_end(n);
+  launch_ck_fill(s, n->live, n->d_int, N, n->ckat);
   ck(cudaMemcpyAsync(n->h_int, n->d_int, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
   ck(cudaStreamSynchronize(s), "sync");
   const int n_live = n->h_int[0];
@@ -1286,8 +1402,6 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
         const int RA = R / 2, RB = R - RA;
         stream_wait(n, h->stream, s);  // the seed and live list are on s
         ChunkWalk a{Walker{n, s, t}}, b{Walker{h, h->stream, t}};
-        a.w.ck_count = n->d_ck;
-        b.w.ck_count = n->d_ck + 1;
         start_chunk(n, a, t, affine, base, RA, allow_freeze, et, st, ws);
         start_chunk(h, b, t, affine, base + RA, RB, allow_freeze, et, st, ws);
         while (a.running || b.running) {
@@ -1297,7 +1411,6 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
         stream_wait(n, s, n->stream2);
         stream_wait(n, s, h->stream);
         stream_wait(n, s, h->stream2);
-        launch_ck_merge(s, n->d_ck, n->d_ck + 1, n->ctr);
         stream_wait(n, h->stream, s);  // h's next chunk reuses its arena after s
         continue;
       }
@@ -1307,7 +1420,11 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
       stream_wait(n, s, n->stream2);  // the next chunk reuses the arena and row lists
     }
   }
-  if (W > 1 && n_live > 0) allgather_rows(n, n->live, n_live, 4, n->cand);
+  if (W > 1 && n_live > 0) {
+    allgather_rows(n, n->live, n_live, 4, n->cand);
+    allgather_rows(n, n->live, n_live, 1, n->ckat);
+  }
+  count_checkpoints(n, t, affine, allow_freeze, n->live, n->d_int, 0, 1);
   ++n->gen;  // refresh round: the write-back marks what this pass changed
   prof_begin(n, PROF_WRITEBACK);
   launch_writeback(s, N, Q.out_c, t, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
@@ -1324,6 +1441,7 @@ void run_margin_graph(Ctx* n, pc_stats* st) {
   const int nr = n->n_out - 1;
   st->rows_total += nr;
   if (nr <= 0) return;
+  st->checkpoints += walk_checkpoints(n, dense_frame(out), false);  // one chunk, never frozen
   launch_margin_rows(s, n->d_label, n->n_out, n->rowq[0]);
   ck(cudaMemsetAsync(n->has, 0, nr, s), "memset");
   const WalkSize ws = walk_size(n, out, false, false);
@@ -1350,6 +1468,7 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
   const int nr = n->n_out - 1;
   st->rows_total += nr;
   if (nr <= 0) return;
+  st->checkpoints += walk_checkpoints(n, dense_frame(out), false);  // one chunk, never frozen
   std::vector<int> cls;
   for (int j = 0; j < n->n_out; ++j)
     if (j != label) cls.push_back(j);
@@ -1432,13 +1551,30 @@ bool graph_eligible(Ctx* n, size_t* arena_bytes, size_t* stat_count) {
   return n->opt.exec_mode == 2;
 }
 
-void forward_layers(Ctx* n, int k0, int k1) {  // layers (k0, k1]
+// Forward refresh of layers (k0, k1] (all nimg images of a batched context
+// per launch). A ReLU layer's bounds are final once refreshed here (no later
+// pass changes a layer below its target), so its live-channel table for the
+// conv kernels (k_live_build) is rebuilt right after.
+void forward_layers(Ctx* n, int k0, int k1, int nimg = 1) {
+  const int nl = (int)n->L.size();
+  const long long T = n->total, P = n->pofs[nl];
   for (int k = k0 + 1; k <= k1; ++k) {
     const HostLayer& l = n->L[k];
     prof_begin(n, PROF_FWD);
-    launch_forward_layer(n->stream, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
-                         n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
-                         n->gen_pos, n->gen_l, n->gen, 1);
+    if (nimg > 1)
+      launch_forward_layer(n->stream, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
+                           n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
+                           n->gen_pos, n->gen_l, n->gen, 1, nimg, T, P, nl);
+    else
+      launch_forward_layer(n->stream, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
+                           n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
+                           n->gen_pos, n->gen_l, n->gen, 1);
+    if (l.kind == KIND_RELU && n->net->live_cells) {
+      const long long o = n->off[k];
+      launch_live_build(n->stream, l.out_w * l.out_h, l.out_c, n->relax + 8 * n->off[l.pred0], n->blo + o,
+                        n->bhi + o, n->rlo + o, n->rhi + o, n->lv_cnt + n->pofs[k], n->lv_idx + o, nimg,
+                        T, P);
+    }
     prof_end(n);
   }
 }
@@ -1569,16 +1705,7 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
   // predecessor values. So computing layer k once, right after the last pass
   // before it (and the forward pass for k <= first target), yields the
   // reference's state bit-for-bit with each layer evaluated once per image.
-  auto forward = [&](int k0, int k1) {  // layers (k0, k1]
-    for (int k = k0 + 1; k <= k1; ++k) {
-      const HostLayer& l = n->L[k];
-      prof_begin(n, PROF_FWD);
-      launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
-                           n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
-                           n->gen_pos, n->gen_l, n->gen, 1);
-      prof_end(n);
-    }
-  };
+  auto forward = [&](int k0, int k1) { forward_layers(n, k0, k1); };  // layers (k0, k1]
   forward(0, targets[0]);
   // PC_PROFILE: wall time and live rows per pass (host clock; the pass ends
   // with the write-back, which the next pass's seed synchronises on)
@@ -1614,9 +1741,9 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
   if (W > 1) {
     // per-rank work counters (walk freezes, madds, checkpoints, dense-equivalent
     // GBC work) add up; pre-freezes and rows_total are identical on every rank
-    unsigned long long h[8] = {c.dense_madds, c.gbc_madds, c.frozen, 0,
-                               (unsigned long long)st->checkpoints + c.checkpoints,
-                               c.gbc_dense_equiv, 0, 0};
+    // (checkpoints are counted from the gathered per-row freeze checkpoints,
+    // identical on every rank)
+    unsigned long long h[8] = {c.dense_madds, c.gbc_madds, c.frozen, 0, 0, c.gbc_dense_equiv, 0, 0};
     ensure_shard_buffers(n, 8);
     ck(cudaMemcpyAsync(n->sh_send, h, sizeof(h), cudaMemcpyHostToDevice, s), "h2d");
     exchange(n, sizeof(h));
@@ -1629,8 +1756,6 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
     c.dense_madds = sum[0];
     c.gbc_madds = sum[1];
     c.frozen = sum[2];
-    st->checkpoints = (long long)sum[4];
-    c.checkpoints = 0;
     c.gbc_dense_equiv = sum[5];
   }
   st->checkpoints += (long long)c.checkpoints;
@@ -1654,14 +1779,7 @@ void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stat
   const bool et = n->opt.early_term != 0;
   ck(cudaMemsetAsync(n->ctr, 0, sizeof(Counters) * B, s), "memset");
   const std::vector<int> targets = pass_targets(n);
-  auto forward = [&](int k0, int k1) {  // all B images per launch (blockIdx.z)
-    for (int k = k0 + 1; k <= k1; ++k) {
-      const HostLayer& l = n->L[k];
-      launch_forward_layer(s, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
-                           n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
-                           n->gen_pos, n->gen_l, n->gen, 1, B, T, P, nl);
-    }
-  };
+  auto forward = [&](int k0, int k1) { forward_layers(n, k0, k1, B); };  // all B images per launch
   long long rows_total = 0;
   forward(0, targets[0]);
   for (size_t ti = 0; ti < targets.size(); ++ti) {
@@ -1674,6 +1792,7 @@ void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stat
                 et ? 1 : 0, n->cand, n->frozen, n->live, n->d_int + 8, &n->ctr[0].pad, B, T, M,
                 (int)(sizeof(Counters) / sizeof(unsigned long long)));
     launch_gather_keys(s, n->live, n->d_int + 8, B, (int)M, n->keys, n->d_int);
+    launch_ck_fill(s, n->keys, n->d_int, (int)(M * B), n->ckat);
     ck(cudaMemcpyAsync(n->h_int, n->d_int, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
     ck(cudaStreamSynchronize(s), "sync");
     const int n_live = n->h_int[0];
@@ -1716,6 +1835,7 @@ void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stat
         w.walk(m, 0, true);
         stream_wait(n, s, n->stream2);
       }
+      count_checkpoints(n, t, affine, allow_freeze, n->keys, n->d_int, (int)M, B);
     }
     ++n->gen;
     launch_writeback(s, N, Q.out_c, t, n->cand, n->blo + o, n->bhi + o, n->rlo + o, n->rhi + o,
@@ -1757,7 +1877,7 @@ void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stat
     stream_wait(n, s, n->stream2);
     ck(cudaMemcpyAsync(margins, n->best, sizeof(double) * R, cudaMemcpyDeviceToHost, s), "d2h");
     ck(cudaMemcpyAsync(n->h_int + 16, n->has, R, cudaMemcpyDeviceToHost, s), "d2h");
-    margin_ck = mst.checkpoints;
+    margin_ck = walk_checkpoints(n, dense_frame(out), false);
     rows_total += nr;
   }
   std::vector<Counters> c(B);
@@ -2025,6 +2145,10 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
     n->pofs.assign(nl + 1, 0);
     for (int k = 0; k < nl; ++k) n->pofs[k + 1] = n->pofs[k] + (long long)n->L[k].out_w * n->L[k].out_h;
     n->n_out = (int)n->L.back().numel();
+    n->live_cells = env_int("PC_LIVE_CELLS", 1) != 0;
+    for (const HostLayer& l : n->L)
+      for (double b : l.bias)
+        if (std::signbit(b) && b == 0.0) n->live_cells = false;
     for (int k = 0; k < nl; ++k) {
       HostLayer& l = n->L[k];
       LayerDev& d = l.d;

@@ -2423,6 +2423,217 @@ __global__ void __launch_bounds__(256, MINB)
   mag.flush(out.stat);
 }
 
+// ---------------------------------------------------------------------------
+// Live output cells of a conv step whose frame lands on a ReLU layer P.
+//
+// The relu step that follows maps the coefficient of every stably-negative
+// neuron of P (relaxation all zero, analyzer.hpp:50-55) to an exact zero
+// whatever its value and adds no offset for it (backsub.hpp:536-563); the
+// checkpoint in between multiplies it by P's padded and raw bounds, both
+// [0, 0] for such a neuron, i.e. adds +0 terms (concretize, :756-759), which
+// change nothing unless the accumulator is -0 (never, unless a bias is -0:
+// the engine then keeps every cell live). In a residual join the branch
+// result is added to the other branch before that checkpoint and relu step,
+// so the sum at such a cell is just as irrelevant. So these cells (about 60 %
+// of the coefficients on the ResNets) are written as +0 and not computed; no
+// observable value — bounds, margins, PassStats — depends on them.
+//
+// k_live_build lists, once per image when P's bounds are final (right after
+// its forward refresh), the live channels of every grid position of P:
+// cnt[pos], idx[pos * C + k] ascending. Dead = relaxation all zero and P's
+// padded and raw bounds exactly zero in value.
+__global__ void __launch_bounds__(256)
+    k_live_build(int npos, int C, const double* relax, const double* blo, const double* bhi,
+                 const double* rlo, const double* rhi, int* cnt, unsigned short* idx,
+                 long long sst, long long pst) {
+  const int img = blockIdx.z;
+  relax += 8 * img * sst;
+  blo += img * sst; bhi += img * sst; rlo += img * sst; rhi += img * sst;
+  idx += img * sst;
+  cnt += img * pst;
+  const int lane = threadIdx.x & 31;
+  for (int pos = blockIdx.x * 8 + (threadIdx.x >> 5); pos < npos; pos += gridDim.x * 8) {
+    int base = 0;
+    for (int c0 = 0; c0 < C; c0 += 32) {
+      const int c = c0 + lane;
+      bool live = false;
+      if (c < C) {
+        const long long j = (long long)pos * C + c;
+        const double* R = relax + 8 * j;
+        bool zr = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) zr &= R[k] == 0.0;
+        live = !(zr && blo[j] == 0.0 && bhi[j] == 0.0 && rlo[j] == 0.0 && rhi[j] == 0.0);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, live);
+      if (live) idx[(long long)pos * C + base + __popc(m & ((1u << lane) - 1u))] = (unsigned short)c;
+      base += __popc(m);
+    }
+    if (lane == 0) cnt[pos] = base;
+  }
+}
+
+void launch_live_build(cudaStream_t s, int npos, int C, const double* relax, const double* blo,
+                       const double* bhi, const double* rlo, const double* rhi, int* cnt,
+                       unsigned short* idx, int nimg, long long sst, long long pst) {
+  unsigned gx = cdiv(npos, 8);
+  if (gx > 1024) gx = 1024;
+  k_live_build<<<dim3(gx, 1, nimg), 256, 0, s>>>(npos, C, relax, blo, bhi, rlo, rhi, cnt, idx, sst, pst);
+  ++g_launches;
+}
+
+// Conv coefficients over the live cells only: one warp per output position of
+// the row's window, lanes over that position's live channels (two per lane
+// when more than 32 are live, sharing each compacted coefficient load), the
+// same gather as k_gbc_sparse2 in the reference's (ch, cw, d) order.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_gbc_live(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
+               MatDev out, LiveDev lv) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  int bw, bh, nbw, nbh;
+  frame_base(fi, q, bw, bh);
+  frame_base(fo, q, nbw, nbh);
+  const int* lcnt = lv.cnt + (long long)img * lv.pst;
+  const unsigned short* lidx = lv.idx + (long long)img * lv.sst;
+  const long long ocells = out.cells;
+  const double* ilo = in.lo + phys_row(in, i) * in.cells;
+  const double* ihi = in.hi + phys_row(in, i) * in.cells;
+  double* olo = out.lo + (size_t)i * ocells;
+  double* ohi = out.hi + (size_t)i * ocells;
+  const int cin = L.in_c, cout = L.out_c;
+  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  const int* cnt = sp.cnt + (size_t)i * sp.ncell;
+  const size_t rbase = (size_t)i * sp.ncell * sp.C;
+  const int lane = threadIdx.x & 31;
+  const int npos = fo.S_w * fo.S_h;
+  MagAcc mag;
+  for (int pos = blockIdx.x * 8 + (threadIdx.x >> 5); pos < npos; pos += gridDim.x * 8) {
+    const int y = pos / fo.S_w, x = pos - y * fo.S_w;
+    const int iy = nbh + y, ix = nbw + x;
+    const int gp = iy * fo.G_w + ix;
+    const int nl = lcnt[gp];
+    const unsigned short* li = lidx + (size_t)gp * cin;
+    double* plo = olo + (size_t)pos * cin;
+    double* phi = ohi + (size_t)pos * cin;
+    for (int c = lane; c < cin; c += 32) {  // dead cells: +0 (live ones overwritten below)
+      plo[c] = 0.0;
+      phi[c] = 0.0;
+    }
+    __syncwarp();
+    if (nl == 0) continue;
+    int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
+    int aw0 = floordiv(ix + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ix + L.pw, L.sw);
+    ah0 = max(ah0, bh);
+    ah1 = min(ah1, bh + fi.S_h - 1);
+    aw0 = max(aw0, bw);
+    aw1 = min(aw1, bw + fi.S_w - 1);
+    for (int k0 = 0; k0 < nl; k0 += 64) {
+      const int ka = k0 + lane, kb = k0 + 32 + lane;
+      const bool va = ka < nl, vb = kb < nl;
+      const bool two = k0 + 32 < nl;  // warp-uniform
+      const int ca = li[va ? ka : 0];
+      const int cb = vb ? li[kb] : ca;
+      Iv acc0{0.0, 0.0}, acc1{0.0, 0.0};
+      if (!band) {
+        bool bad = false;
+        acc0 = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ca, bad);
+        if (bad) acc0 = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ca, bad);
+        if (two) {
+          bad = false;
+          acc1 = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, cb, bad);
+          if (bad) acc1 = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, cb, bad);
+        }
+      } else {
+        double lo0 = 0.0, hi0 = 0.0, lo1 = 0.0, hi1 = 0.0;
+        for (int ah = ah0; ah <= ah1; ++ah) {
+          const int fy = iy + L.ph - ah * L.sh;
+          for (int aw = aw0; aw <= aw1; ++aw) {
+            const int fx = ix + L.pw - aw * L.sw;
+            const int cell = (ah - bh) * fi.S_w + (aw - bw);
+            const int n = cnt[cell];
+            const size_t sb = rbase + (size_t)cell * sp.C;
+            const double* wa = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ca;
+            const double* wb = wa + (cb - ca);
+            constexpr int kB = 4;
+            int e = 0;
+            if (two) {
+              for (; e + kB <= n; e += kB) {
+                double cl[kB], ch[kB], w0[kB], w1[kB];
+#pragma unroll
+                for (int k = 0; k < kB; ++k) {
+                  const size_t d = sp.idx[sb + e + k];
+                  cl[k] = sp.lo[sb + e + k];
+                  ch[k] = sp.hi[sb + e + k];
+                  w0[k] = wa[d * cin];
+                  w1[k] = wb[d * cin];
+                }
+#pragma unroll
+                for (int k = 0; k < kB; ++k) {
+                  madd_band(w0[k], cl[k], ch[k], lo0, hi0);
+                  madd_band(w1[k], cl[k], ch[k], lo1, hi1);
+                }
+              }
+              for (; e < n; ++e) {
+                const size_t d = sp.idx[sb + e];
+                const double cl = sp.lo[sb + e], ch = sp.hi[sb + e];
+                madd_band(wa[d * cin], cl, ch, lo0, hi0);
+                madd_band(wb[d * cin], cl, ch, lo1, hi1);
+              }
+            } else {
+              for (; e + kB <= n; e += kB) {
+                double cl[kB], ch[kB], w0[kB];
+#pragma unroll
+                for (int k = 0; k < kB; ++k) {
+                  const size_t d = sp.idx[sb + e + k];
+                  cl[k] = sp.lo[sb + e + k];
+                  ch[k] = sp.hi[sb + e + k];
+                  w0[k] = wa[d * cin];
+                }
+#pragma unroll
+                for (int k = 0; k < kB; ++k) madd_band(w0[k], cl[k], ch[k], lo0, hi0);
+              }
+              for (; e < n; ++e)
+                madd_band(wa[(size_t)sp.idx[sb + e] * cin], sp.lo[sb + e], sp.hi[sb + e], lo0, hi0);
+            }
+          }
+        }
+        acc0 = Iv{canon0(lo0), hi0};
+        acc1 = Iv{canon0(lo1), hi1};
+      }
+      if (va) {
+        plo[ca] = acc0.lo;
+        phi[ca] = acc0.hi;
+        mag.add(acc0.lo);
+        mag.add(acc0.hi);
+      }
+      if (vb) {
+        plo[cb] = acc1.lo;
+        phi[cb] = acc1.hi;
+        mag.add(acc1.lo);
+        mag.add(acc1.hi);
+      }
+    }
+  }
+  mag.flush(out.stat);
+}
+
+void launch_gbc_live(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv) {
+  static const int minb = env_int("PC_GBC_LIVE_MINB", 2);
+  unsigned gx = cdiv(fout.S_w * fout.S_h, 8);
+  if (gx > 1024) gx = 1024;
+  dim3 grid(gx, rows.n);
+  if (minb >= 3) k_gbc_live<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv);
+  else if (minb == 2) k_gbc_live<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv);
+  else k_gbc_live<1><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv);
+  ++g_launches;
+}
+
 void launch_gbc_sparse(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                        const FrameDev& fout, SparseDev sp, MatDev in, MatDev out) {
   static const int pairs = env_int("PC_GBC_PAIRS", 1);
@@ -2622,18 +2833,12 @@ void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const
 __global__ void __launch_bounds__(kScanThreads)
     k_offer(RowsDev rows, int R, const double* vals, const double* rvals, double* cand,
             char* frozen, int allow_freeze, int early_term, int* map, int* new_R,
-            int* new_row_q, Counters* ctr, unsigned long long* ck_count) {
+            int* new_row_q, Counters* ctr, double* ckat, int ck_index) {
   using Scan = cub::BlockScan<int, kScanThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
-  __shared__ int s_live;
-  __shared__ unsigned char s_live_img[kMaxBatch];  // image-batched walks: per image
   if (rows.dR) R = *rows.dR;  // device-driven walk: the live rows of this checkpoint
-  if (threadIdx.x == 0) {
-    s_base = 0;
-    s_live = 0;
-  }
-  if (threadIdx.x < kMaxBatch) s_live_img[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_base = 0;
   int froze = 0;
   __syncthreads();
   for (int start = 0; start < R; start += kScanThreads) {
@@ -2643,8 +2848,6 @@ __global__ void __launch_bounds__(kScanThreads)
       q = rows.row_q[r];  // a key (img * kq + neuron) in batched walks: cand / frozen are keyed alike
       double* cd = cand + 4 * (size_t)q;
       if (!frozen[q]) {
-        s_live = 1;  // the reference still has this row: the checkpoint runs
-        if (rows.kq) s_live_img[q / rows.kq] = 1;
         const double v = vals[r], rv = rvals[r];  // offer_hi
         if (v < cd[1]) cd[1] = v;
         if (rv < cd[3]) cd[3] = rv;
@@ -2654,6 +2857,7 @@ __global__ void __launch_bounds__(kScanThreads)
         if (allow_freeze && (!(cd[2] < 0.0) || !(cd[3] > 0.0))) {
           frozen[q] = 1;
           if (early_term) {
+            ckat[q] = ck_index;  // the checkpoint that retires this row (k_ck_count)
             if (rows.kq) atomicAdd(&ctr[q / rows.kq].frozen, 1ull);
             else ++froze;
           }
@@ -2672,12 +2876,6 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
   }
   if (froze) atomicAdd(&ctr->frozen, (unsigned long long)froze);
-  if (rows.kq) {
-    if (threadIdx.x < rows.nimg && (s_live_img[threadIdx.x] || !early_term))
-      atomicAdd(&ctr[threadIdx.x].checkpoints, 1ull);
-  } else if (threadIdx.x == 0 && (s_live || !early_term)) {
-    atomicAdd(ck_count ? ck_count : &ctr->checkpoints, 1ull);
-  }
   const int nR = s_base;
   for (int p = threadIdx.x; p < nR; p += blockDim.x) map[nR + p] = R + map[p];  // lower rows
   if (threadIdx.x == 0) *new_R = nR;
@@ -2685,9 +2883,10 @@ __global__ void __launch_bounds__(kScanThreads)
 
 void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals,
                   const double* rvals, double* cand, char* frozen, int allow_freeze,
-                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr, unsigned long long* ck_count) {
+                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr, double* ckat,
+                  int ck_index) {
   k_offer<<<1, kScanThreads, 0, s>>>(rows, R, vals, rvals, cand, frozen, allow_freeze, early_term,
-                                     map, new_R, new_row_q, ctr, ck_count);
+                                     map, new_R, new_row_q, ctr, ckat, ck_index);
   ++g_launches;
 }
 
@@ -2729,16 +2928,66 @@ void launch_shard_unpack(cudaStream_t s, const int* live, int n_live, int world,
   ++g_launches;
 }
 
-// Two walk pipelines split a chunk: the reference walks the whole chunk while
-// any row is live, i.e. as many checkpoints as the longer half.
-__global__ void k_ck_merge(unsigned long long* a, unsigned long long* b, Counters* ctr) {
-  ctr->checkpoints += *a > *b ? *a : *b;
-  *a = 0;
-  *b = 0;
+// PassStats.checkpoints as the reference counts it (backsub.hpp:1018-1063):
+// the live rows of a pass are walked in chunks of `chunk` rows (its
+// rows_per_chunk, from the memory budget; engine.cu ref_rows_per_chunk), and a
+// chunk's walk runs checkpoints until its last row froze and was compacted
+// (walk_back's rows() == 0 exit, :859) or the walk ends (T checkpoints). A
+// row's freeze checkpoint (1-based, ckat; 0 = never froze) is chunk-invariant,
+// so each chunk contributes the max over its rows. keys: the pass's live rows
+// in the reference's order (image-major keys img * kq + neuron when batched;
+// one block per image). all_full: no row ever leaves its walk early (early
+// termination off, or the output pass).
+__global__ void k_ck_fill(const int* keys, const int* n_keys, double* ckat) {
+  const int n = *n_keys;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    ckat[keys[i]] = 0.0;
 }
 
-void launch_ck_merge(cudaStream_t s, unsigned long long* a, unsigned long long* b, Counters* ctr) {
-  k_ck_merge<<<1, 1, 0, s>>>(a, b, ctr);
+__device__ __forceinline__ int lower_bound_key(const int* keys, int n, long long v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (keys[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_ck_count(const int* keys, const int* n_keys, int kq, long long chunk, int T,
+                           int all_full, const double* ckat, Counters* ctr) {
+  const int n = *n_keys;
+  const int b = blockIdx.x;
+  const int lo = kq ? lower_bound_key(keys, n, (long long)b * kq) : 0;
+  const int hi = kq ? lower_bound_key(keys, n, (long long)(b + 1) * kq) : n;
+  const long long nchunks = hi > lo ? (hi - lo + chunk - 1) / chunk : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  unsigned long long sum = 0;
+  for (long long c = warp; c < nchunks; c += nwarps) {
+    int mx = 0;
+    if (all_full) {
+      mx = T;
+    } else {
+      const long long e = min((long long)hi, lo + (c + 1) * chunk);
+      for (long long i = lo + c * chunk + lane; i < e; i += 32) {
+        const int v = (int)ckat[keys[i]];
+        mx = max(mx, v == 0 ? T : v);
+      }
+      for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) sum += (unsigned long long)mx;
+  }
+  if (lane == 0 && sum) atomicAdd(&ctr[b].checkpoints, sum);
+}
+
+void launch_ck_fill(cudaStream_t s, const int* keys, const int* n_keys, int cap, double* ckat) {
+  k_ck_fill<<<cdiv(cap > 0 ? cap : 1, 256) > 1024 ? 1024 : cdiv(cap > 0 ? cap : 1, 256), 256, 0, s>>>(keys, n_keys, ckat);
+  ++g_launches;
+}
+
+void launch_ck_count(cudaStream_t s, const int* keys, const int* n_keys, int kq, int nimg,
+                     long long chunk, int T, int all_full, const double* ckat, Counters* ctr) {
+  k_ck_count<<<nimg, 256, 0, s>>>(keys, n_keys, kq, chunk, T, all_full, ckat, ctr);
   ++g_launches;
 }
 

@@ -353,6 +353,20 @@ struct SparseDev {
   int ncell, C;
 };
 void launch_compact_cells(cudaStream_t s, const RowsDev& rows, MatDev m, SparseDev sp);
+// Live channels per grid position of a ReLU layer (k_live_build, kernels.cu):
+// cnt at the layer's position offset, idx at its neuron offset; strided per
+// image by pst / sst.
+struct LiveDev {
+  const int* cnt;
+  const unsigned short* idx;
+  long long pst, sst;
+};
+void launch_live_build(cudaStream_t s, int npos, int C, const double* relax, const double* blo,
+                       const double* bhi, const double* rlo, const double* rhi, int* cnt,
+                       unsigned short* idx, int nimg, long long sst, long long pst);
+// Conv coefficients of the live cells of a ReLU frame (dead ones written +0).
+void launch_gbc_live(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv);
 // Conv coefficients from the compacted input (band path; falls back to the
 // checked gather on `in` when the launch's operands are not proven in band).
 void launch_gbc_sparse(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
@@ -377,9 +391,12 @@ void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const
 // lower physical rows) and the compacted query list.
 void launch_offer(cudaStream_t s, const RowsDev& rows, int R, const double* vals,
                   const double* rvals, double* cand, char* frozen, int allow_freeze,
-                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr,
-                  unsigned long long* ck_count = nullptr);  // checkpoint tally (default ctr)
-void launch_ck_merge(cudaStream_t s, unsigned long long* a, unsigned long long* b, Counters* ctr);
+                  int early_term, int* map, int* new_R, int* new_row_q, Counters* ctr, double* ckat,
+                  int ck_index);  // ckat[q] = ck_index when row q freezes
+// PassStats.checkpoints of a pass under the reference's chunking (kernels.cu).
+void launch_ck_fill(cudaStream_t s, const int* keys, const int* n_keys, int cap, double* ckat);
+void launch_ck_count(cudaStream_t s, const int* keys, const int* n_keys, int kq, int nimg,
+                     long long chunk, int T, int all_full, const double* ckat, Counters* ctr);
 void launch_margin_offer(cudaStream_t s, int n, const double* vals, double* best, char* has);
 
 // Row sharding: pack this rank's slice of candidates (4 doubles per row, in
