@@ -195,11 +195,22 @@ void pc_last_timing(double* total_ms, double* dense_kernel_ms, double* dense_ker
                     long long* dense_kernel_launches);
 /* The same for one back-substitution coefficient kernel of the last
  * pc_net_test* call on this thread: kernel 0 = the dense kernel
- * (k_dense_coef*), 1 = the conv kernel (k_gbc_sparse2 / k_gbc_coef): summed
+ * (k_dense_coef*), 1 = the conv kernel (k_gbc_live / k_gbc_sparse2 / k_gbc_coef): summed
  * CUDA-event milliseconds over its launches (on the stream each is launched
  * on), algorithmic bytes (coefficient rows in and out, 16 B per interval,
  * plus the weights / filter once per launch) and the launch count. */
 void pc_last_kernel_timing(int kernel, double* ms, double* bytes, long long* launches);
+
+/* Interval multiply-adds the live-cell conv kernel (k_gbc_live) executed in
+ * the last pc_net_test* call on this thread (device-counted; the reference's
+ * PassStats.gbc_madds also counts the cells whose value no result reads). */
+double pc_last_conv_executed_madds(void);
+
+/* Timing mode: serial != 0 runs every walk on one stream and one pipeline,
+ * so the per-launch CUDA events of pc_last_kernel_timing time each kernel
+ * alone (roofline measurement); results are identical. Not thread-safe
+ * against concurrent pc_net_test* calls on the net. */
+pc_status pc_net_set_serial(pc_net* net, int serial);
 
 /* Measured FP64 FMA throughput of the device (FMA/s): a register-resident
  * DFMA kernel (8 independent chains per thread, every SM), timed with CUDA
@@ -223,6 +234,14 @@ int pc_last_profile(char* buf, int len);
  * (down/up) and 13/14 band sum (down/up) used by the conv/dense kernels when
  * their operands are proven in band. HOST arrays. */
 pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, long long n);
+
+/* Chain-fold self test (device): out[c] = acc0[c] folded with terms[c*len ..
+ * c*len+len) in order by add_up (up[c] & 1) or add_down (interval.hpp:59-68),
+ * NaN terms skipped — the row-constant / concretisation chains of
+ * backsub.hpp:365-389, 740-760, evaluated by the warp-scan fold the chain
+ * kernels use (csrc/scanfold.cuh; up[c] & 2: its 32-link variant). HOST arrays. */
+pc_status pc_chain_fold(int n_chains, int len, const double* acc0, const double* terms, const int* up,
+                        double* out);
 
 const char* pc_last_error(void);
 

@@ -1143,6 +1143,20 @@ int port_analyze(const int* info, int n_layers, const double* const* weights, co
 
 /* Scalar ops exported for the numeric-core parity tests (op: 0 add_down,
  * 1 add_up, 2 mul_down, 3 mul_up, 4 div_down, 5 div_up, 6 ulp_above(a)). */
+/* Serial chains (test infrastructure): acc0[c] += terms[c*len + j] for j
+ * ascending with add_up / add_down, NaN terms skipped (backsub.hpp:740-760). */
+void port_chain_fold(int n_chains, int len, const double* acc0, const double* terms, const int* up,
+                     double* out) {
+  for (int c = 0; c < n_chains; ++c) {
+    double acc = acc0[c];
+    for (int j = 0; j < len; ++j) {
+      const double t = terms[(long long)c * len + j];
+      if (t == t) acc = up[c] ? add_up(acc, t) : add_down(acc, t);
+    }
+    out[c] = acc;
+  }
+}
+
 void port_scalar_ops(int op, const double* a, const double* b, double* out, long long n) {
   for (long long i = 0; i < n; ++i) {
     switch (op) {

@@ -61,6 +61,14 @@ class Port:
         self.lib.port_scalar_ops(ci(op), _p(a), _p(b), _p(out), ll(len(a)))
         return out
 
+    def chain_fold(self, acc0, terms, up):
+        acc0 = np.ascontiguousarray(acc0, dtype=np.float64)
+        terms = np.ascontiguousarray(terms, dtype=np.float64)
+        upa = np.ascontiguousarray(up, dtype=np.int32)
+        out = np.empty_like(acc0)
+        self.lib.port_chain_fold(ci(terms.shape[0]), ci(terms.shape[1]), _p(acc0), _p(terms), _p(upa), _p(out))
+        return out
+
     def analyze(self, layers, box_lo, box_hi, label=-1, early_term=True, chunk_rows=0,
                 memory_budget=0):
         """layers: list of objects with kind, preds, out_shape, fw.., weights, bias."""
@@ -207,6 +215,22 @@ class Ref:
                                    "gbc_dense_equiv", "dense_madds", "checkpoints"],
                                   stats.tolist())),
                 "b_lo": bl, "b_hi": bh, "r_lo": rl, "r_hi": rh, "seconds": sec.value}
+
+    def rational_contains(self, h, center, eps_num, eps_den, clamp01, label, b_lo, b_hi, margins):
+        """Exact-rational soundness check (oracle.hpp / the ExactRational engine,
+        analyzer.hpp:198-276 over mpq): the number of given widened bounds and
+        margins that fail to contain the exact ones, and the exact verdict."""
+        c = np.ascontiguousarray(center, dtype=np.float64)
+        bl = np.ascontiguousarray(b_lo, dtype=np.float64)
+        bh = np.ascontiguousarray(b_hi, dtype=np.float64)
+        m = np.ascontiguousarray(margins if margins is not None else np.zeros(1), dtype=np.float64)
+        ver = ci(0)
+        bad = self.lib.ref_rational_contains(h, _p(c), ctypes.c_long(eps_num), ctypes.c_long(eps_den),
+                                             ci(int(clamp01)), ci(label), _p(bl), _p(bh), _p(m),
+                                             ctypes.byref(ver))
+        if bad < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return bad, bool(ver.value)
 
     def verify_batch(self, h, centers, eps, clamp01=True, threads=1, early_term=True):
         X = np.ascontiguousarray(centers, dtype=np.float64)

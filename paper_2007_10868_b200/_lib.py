@@ -75,8 +75,11 @@ def _load():
         "pc_last_timing": (None, [vp, vp, vp, vp]),
         "pc_last_dense_madds": (d, []),
         "pc_last_kernel_timing": (None, [i, vp, vp, vp]),
+        "pc_last_conv_executed_madds": (ctypes.c_double, []),
+        "pc_net_set_serial": (i, [vp, i]),
         "pc_fp64_peak": (i, [i, vp]),
         "pc_scalar_ops": (i, [i, vp, vp, vp, ll]),
+        "pc_chain_fold": (i, [i, i, vp, vp, vp, vp]),
         "pc_last_profile": (i, [ctypes.c_char_p, i]),
         "pc_last_error": (ctypes.c_char_p, []),
         "pc_net_set_sharding": (i, [vp, i, i, ALLGATHER_FN, vp]),

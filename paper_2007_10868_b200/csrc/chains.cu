@@ -3,38 +3,60 @@
 // The reference accumulates each row constant and each concretisation as an
 // ascending serial chain of directed-rounded adds (backsub.hpp:365-389,
 // 454-489, 536-563, 740-760): term j is added only for nonzero coefficient
-// cells, and the chain itself cannot be split or reassociated. Only the adds
-// are serial; the terms are independent. So one CTA per row splits the work:
+// cells, and the chain cannot be split or reassociated in floating point.
+// One CTA per row splits the work:
 //
-//   warps 1..15 (producers)  compute the terms of a 960-cell tile in parallel
-//                            and write the cells that contribute (in ascending
-//                            order, by a block scan) into a shared-memory
-//                            buffer — skipped cells cost nothing downstream;
-//   warp 0 (consumer)        folds the previous tile's compacted terms, one
-//                            lane per chain, in order.
+//   producer warps  compute the terms of a tile of cells in parallel and
+//                   write the cells that contribute (in ascending order, by a
+//                   block scan) into a shared-memory buffer — skipped cells
+//                   cost nothing downstream;
+//   consumer warps  one per chain (k.lo, k.hi, kraw.lo, kraw.hi, dev; or the
+//                   padded / raw concretisation) fold the previous tile's
+//                   compacted terms in order with the warp-scan fold of
+//                   scanfold.cuh: 32 links per step as an exact integer
+//                   prefix sum inside the accumulator's binade, the scalar
+//                   op for the rare link that leaves it.
 //
 // Tiles are double-buffered, so term generation runs one tile ahead of the
-// fold and the kernel's duration is the fold's: one chain step (≈2 dependent
-// FP64 adds) per CONTRIBUTING cell instead of per cell. Results are identical
-// to the warp-per-row kernels in kernels.cu (same terms, same order, same
-// add_up/add_down), which remain in use for short rows.
+// fold. Results are identical to the reference's chains (same terms, same
+// order, same add_up / add_down), tested against serial folds on adversarial
+// chains (tests/test_gpu_numeric.py) and on whole networks.
 #include "kernels.cuh"
 #include "numeric.cuh"
+#include "scanfold.cuh"
 
 namespace pc {
 
 #define PC_NAN __longlong_as_double(0x7ff8000000000000ULL)
 
-constexpr int kCT = 512;             // threads per CTA
-constexpr int kProd = kCT - 32;      // producer threads
-constexpr int kCPT = 2;              // cells per producer thread per tile
-constexpr int kTile = kProd * kCPT;  // cells per tile
+constexpr int kCT = 512;  // threads per CTA
+constexpr int kCPT = 2;   // cells per producer thread per tile
 
-__device__ __forceinline__ void cell_pos(const FrameDev& f, long long cell, int bw, int bh, int& d,
+// Warp roles per generator: G::NF consumer warps (one per chain), the rest
+// producers.
+template <class G>
+struct Roles {
+  static constexpr int kProd = kCT - 32 * G::NF;  // producer threads
+  static constexpr int kTile = kProd * kCPT;       // cells per tile
+};
+
+// Frame cell -> (channel, absolute grid column, row). 32-bit (a row holds
+// fewer than 2^31 cells); the channel split is a shift for the power-of-two
+// channel counts of the residual nets.
+__device__ __forceinline__ void cell_pos(const FrameDev& f, long long cell64, int bw, int bh, int& d,
                                          int& aw, int& ah) {
-  d = (int)(cell % f.C);
-  aw = bw + (int)((cell / f.C) % f.S_w);
-  ah = bh + (int)(cell / ((long long)f.C * f.S_w));
+  const unsigned cell = (unsigned)cell64, C = (unsigned)f.C;
+  unsigned pos;
+  if ((C & (C - 1)) == 0) {
+    d = (int)(cell & (C - 1));
+    pos = cell >> (__ffs(C) - 1);
+  } else {
+    pos = cell / C;
+    d = (int)(cell - pos * C);
+  }
+  const unsigned y = pos / (unsigned)f.S_w;
+  aw = bw + (int)(pos - y * (unsigned)f.S_w);
+  ah = bh + (int)y;
 }
 
 // ---------------------------------------------------------------------------
@@ -153,71 +175,63 @@ struct ConcGen {
   static constexpr int TPE = 1;
 };
 
+// Consumer warp w folds chain w: the terms of array G::arr(w, k) (k < TPE:
+// entry e contributes its TPE terms in order), direction G::up(w) (the row's
+// polarity for concretisations).
 template <class G>
-__device__ __forceinline__ bool lane_up(const G& g, int lane) {
-  return G::up(lane);
+__device__ __forceinline__ bool chain_up(const G& g, int w) {
+  return G::up(w);
 }
 template <>
-__device__ __forceinline__ bool lane_up<ConcGen>(const ConcGen& g, int) {
+__device__ __forceinline__ bool chain_up<ConcGen>(const ConcGen& g, int) {
   return g.upper;
 }
 
-// Shared layout: buf[2][NA][kTile] doubles, then counters.
 struct ChainShared {
   int cnt[2];
-  int bad[2];
-  int wsum[kProd / 32];
+  int wsum[kCT / 32];
+  double acc[8];  // each chain's result (consumer warp w -> acc[w])
 };
 
+// Shared layout: buf[2][NA][kTile] doubles. acc: the chain's start value in
+// consumer warp w (all lanes); returns its result there (sh.acc[w] too).
 template <class G>
 __device__ __forceinline__ double fold_row(G& g, const double* lo, const double* hi,
                                            long long cells, double acc, double* buf,
                                            ChainShared& sh) {
+  constexpr int kProd = Roles<G>::kProd, kTile = Roles<G>::kTile;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntiles = (int)((cells + kTile - 1) / kTile);
-  const bool up = lane_up(g, lane);
-  const bool folder = warp == 0 && lane < G::NF;
+  const bool consumer = warp < G::NF;
+  const bool up = consumer && chain_up(g, warp);
   for (int it = 0; it <= ntiles; ++it) {
-    if (warp == 0) {
-      if (it > 0 && folder) {
+    if (consumer) {
+      if (it > 0) {
         const int b = (it - 1) & 1;
         const int n = sh.cnt[b];
         const double* B = buf + (size_t)b * G::NA * kTile;
-        if (!sh.bad[b] && !start_bad(acc)) {
-#pragma unroll 4
-          for (int e = 0; e < n; ++e) {
-#pragma unroll
-            for (int k = 0; k < G::TPE; ++k) {
-              const double t = B[G::arr(lane, k) * kTile + e];
-              const double s = f_add_dir(acc, t, up);
-              acc = (t == t) ? s : acc;
-            }
-          }
+        if (G::TPE == 1) {
+          const double* T = B + G::arr(warp, 0) * kTile;
+          acc = scan_fold4(acc, n, up, [&](int j) { return T[j]; });
         } else {
-          for (int e = 0; e < n; ++e)
-            for (int k = 0; k < G::TPE; ++k) {
-              const double t = B[G::arr(lane, k) * kTile + e];
-              if (t == t) acc = add_dir(acc, t, up);
-            }
+          const double* T0 = B + G::arr(warp, 0) * kTile;
+          const double* T1 = B + G::arr(warp, 1) * kTile;
+          acc = scan_fold4(acc, G::TPE * n, up, [&](int j) { return (j & 1) ? T1[j >> 1] : T0[j >> 1]; });
         }
       }
     } else if (it < ntiles) {
-      const int p = tid - 32;
+      const int p = tid - 32 * G::NF;
       const int b = it & 1;
       double* B = buf + (size_t)b * G::NA * kTile;
       double t[kCPT][G::NA];
       bool v[kCPT];
-      int nv = 0, bad = 0;
+      int nv = 0;
       const long long c0 = (long long)it * kTile + (long long)p * kCPT;
 #pragma unroll
       for (int k = 0; k < kCPT; ++k) {
         v[k] = false;
         if (c0 + k < cells) v[k] = g.gen(lo, hi, c0 + k, t[k]);
-        if (v[k]) {
-          ++nv;
-#pragma unroll
-          for (int a = 0; a < G::NA; ++a) bad |= (t[k][a] == t[k][a]) && start_bad(t[k][a]);
-        }
+        if (v[k]) ++nv;
       }
       // exclusive scan of nv over the producer threads (ascending cells)
       int inc = nv;
@@ -226,9 +240,8 @@ __device__ __forceinline__ double fold_row(G& g, const double* lo, const double*
         const int y = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += y;
       }
-      const int pw = warp - 1;
+      const int pw = warp - G::NF;
       if (lane == 31) sh.wsum[pw] = inc;
-      const int anybad = __any_sync(0xffffffffu, bad);
       asm volatile("bar.sync 1, %0;" ::"r"(kProd));
       int base = 0, tot = 0;
 #pragma unroll
@@ -245,15 +258,13 @@ __device__ __forceinline__ double fold_row(G& g, const double* lo, const double*
           for (int a = 0; a < G::NA; ++a) B[a * kTile + pos] = t[k][a];
           ++pos;
         }
-      if (p == 0) {
-        sh.cnt[b] = tot;
-        sh.bad[b] = 0;
-      }
+      if (p == 0) sh.cnt[b] = tot;
       asm volatile("bar.sync 1, %0;" ::"r"(kProd));
-      if (anybad && lane == 0) sh.bad[b] = 1;
     }
     __syncthreads();
   }
+  if (consumer && lane == 0) sh.acc[warp] = acc;
+  __syncthreads();
   return acc;
 }
 
@@ -278,15 +289,15 @@ __global__ void __launch_bounds__(kCT)
   AffineGen g{L, is_conv, f, 0, 0, dev};
   if (is_conv) frame_base(f, q, g.bw, g.bh);
   const size_t pr = phys_row(m, i);
-  const int lane = threadIdx.x & 31;
-  const double acc0 = (threadIdx.x < 4) ? m.K[4 * pr + lane] : 0.0;
-  const double acc = fold_row(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, acc0, buf, sh);
-  if (threadIdx.x < 32) {
-    const double dtot = __shfl_sync(0xffffffffu, acc, 4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double acc0 = warp < 4 ? m.K[4 * pr + warp] : 0.0;  // warp 4: dev, from 0
+  fold_row(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, acc0, buf, sh);
+  if (threadIdx.x < 4) {
+    const double dtot = sh.acc[4], a = sh.acc[threadIdx.x];
     double* K = Kout + 4 * (size_t)i;
-    if (lane == 0) K[0] = dtot != 0.0 ? add_down(acc, -dtot) : acc;  // widen_constant :175-179
-    if (lane == 1) K[1] = dtot != 0.0 ? add_up(acc, dtot) : acc;
-    if (lane == 2 || lane == 3) K[lane] = acc;
+    if (threadIdx.x == 0) K[0] = dtot != 0.0 ? add_down(a, -dtot) : a;  // widen_constant :175-179
+    else if (threadIdx.x == 1) K[1] = dtot != 0.0 ? add_up(a, dtot) : a;
+    else K[threadIdx.x] = a;
   }
   unsigned long long md = g.madds;
   for (int o = 16; o > 0; o >>= 1) md += __shfl_down_sync(0xffffffffu, md, o);
@@ -307,9 +318,10 @@ __global__ void __launch_bounds__(kCT)
   ReluGen g{f, 0, 0, upper, relax + 8 * img * rows.sst};
   frame_base(f, q, g.bw, g.bh);
   const size_t pr = phys_row(m, i);
-  const double acc0 = (threadIdx.x < 4) ? m.K[4 * pr + threadIdx.x] : 0.0;
-  const double acc = fold_row(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, acc0, buf, sh);
-  if (threadIdx.x < 4) Kout[4 * (size_t)i + threadIdx.x] = acc;
+  const int warp = threadIdx.x >> 5;
+  const double acc0 = warp < 4 ? m.K[4 * pr + warp] : 0.0;
+  fold_row(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, acc0, buf, sh);
+  if (threadIdx.x < 4) Kout[4 * (size_t)i + threadIdx.x] = sh.acc[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(kCT)
@@ -336,15 +348,16 @@ __global__ void __launch_bounds__(kCT)
                     (__double_as_longlong(a1) == (long long)0x8000000000000000ULL);
   ConcGen g{f, 0, 0, upper, !neg0, blo, bhi, rlo, rhi};
   frame_base(f, q, g.bw, g.bh);
-  const double acc0 = threadIdx.x == 0 ? a0 : (threadIdx.x == 1 ? a1 : 0.0);
-  const double acc = fold_row(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, acc0, buf, sh);
-  if (threadIdx.x == 0) vals[i] = acc;
-  if (threadIdx.x == 1) rvals[i] = acc;
+  const int warp = threadIdx.x >> 5;
+  const double acc0 = warp == 0 ? a0 : (warp == 1 ? a1 : 0.0);
+  fold_row(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, acc0, buf, sh);
+  if (threadIdx.x == 0) vals[i] = sh.acc[0];
+  if (threadIdx.x == 1) rvals[i] = sh.acc[1];
 }
 
 template <class G>
 constexpr size_t chain_smem() {
-  return (size_t)2 * G::NA * kTile * sizeof(double);
+  return (size_t)2 * G::NA * Roles<G>::kTile * sizeof(double);
 }
 
 static void set_attrs() {

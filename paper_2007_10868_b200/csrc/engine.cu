@@ -38,6 +38,7 @@ thread_local long long g_dense_launches = 0;
 // CUDA-event time over its launches, algorithmic bytes (rows in/out + filter)
 thread_local double g_conv_ms = 0, g_conv_bytes = 0;
 thread_local long long g_conv_launches = 0;
+thread_local double g_conv_exec = 0;  // interval madds executed by the live-cell conv kernel
 
 struct StatusError : std::runtime_error {
   pc_status code;
@@ -128,6 +129,9 @@ struct pc_net {
   // off when a bias is -0 (an accumulator could then start at -0, and the
   // +0 terms of dead cells would matter) or PC_LIVE_CELLS=0
   bool live_cells = true;
+  // pc_net_set_serial: walks on one stream and one pipeline, so per-launch
+  // CUDA events time each kernel alone (roofline measurement)
+  bool serial = false;
   pc_allgather_fn allgather = nullptr;
   void* allgather_user = nullptr;
 
@@ -183,6 +187,8 @@ struct Ctx {
   double* ckat = nullptr;  // per live row: the checkpoint that froze it (k_ck_count)
   int* lv_cnt = nullptr;             // live channels per grid position of each ReLU layer
   unsigned short* lv_idx = nullptr;  // (k_live_build; read by the conv kernel k_gbc_live)
+  int* un_idx = nullptr;  // per ReLU layer: ascending neurons with a nonzero relaxation offset
+  int* un_cnt = nullptr;  // their count per (image, layer) (k_offset_list)
   int* d_label = nullptr;
   int* d_slots = nullptr;
   static constexpr int kSlots = 8192;
@@ -274,6 +280,8 @@ struct Ctx {
     ckat = dalloc<double>(M);
     lv_cnt = dalloc<int>((size_t)pofs[nl] * nimg);
     lv_idx = dalloc<unsigned short>(T);
+    un_idx = dalloc<int>(T);
+    un_cnt = dalloc<int>((size_t)nl * nimg);
     d_label = dalloc<int>(nimg);
     d_slots = dalloc<int>(kSlots);
     perm2 = dalloc<int>(2 * M);
@@ -776,7 +784,7 @@ struct Walker {
       if (sparse && n->net->live_cells && n->L[L.pred0].kind == KIND_RELU) {
         const int nl = (int)n->L.size();
         const LiveDev lv{n->lv_cnt + n->pofs[L.pred0], n->lv_idx + n->off[L.pred0], n->pofs[nl], n->total};
-        launch_gbc_live(s, L.d, rows(), fi, fo, sp, md(m), md(out), lv);
+        launch_gbc_live(s, L.d, rows(), fi, fo, sp, md(m), md(out), lv, n->ctr);
       } else if (sparse)
         launch_gbc_sparse(s, L.d, rows(), fi, fo, sp, md(m), md(out));
       else
@@ -802,7 +810,12 @@ struct Walker {
       const double* rx = n->relax + 8 * n->off[L.pred0];
       need(m);
       prof_begin(n, PROF_CHAIN_RELU, s2);
-      launch_chain_relu(s2, rows(), f, md(m), out.K, rx, fz());
+      static const int relu_list = env_int("PC_RELU_LIST", 1);
+      if (relu_list)
+        launch_chain_relu_list(s2, rows(), f, md(m), out.K, rx, n->un_idx + n->off[L.pred0],
+                               n->un_cnt + L.pred0, (int)n->L.size(), fz());
+      else
+        launch_chain_relu(s2, rows(), f, md(m), out.K, rx, fz());
       prof_end(n, s2);
       prof_begin(n, PROF_RELU);
       launch_relu_coef(s, rows(), f, md(m), md(out), rx);
@@ -1272,6 +1285,8 @@ Ctx* helper_of(Ctx* n) {
   h->ckat = n->ckat;
   h->lv_cnt = n->lv_cnt;
   h->lv_idx = n->lv_idx;
+  h->un_idx = n->un_idx;
+  h->un_cnt = n->un_cnt;
   h->live = n->live; h->ctr = n->ctr;
   h->gen_n = n->gen_n; h->gen_pos = n->gen_pos; h->gen_l = n->gen_l;
   h->budget = n->budget;
@@ -1294,7 +1309,7 @@ void start_chunk(Ctx* c, ChunkWalk& cw, int t, bool affine, long long base, int 
   c->arena_used = 0;
   reset_stats(c, ws.stats);
   Walker& w = cw.w;
-  w.s2 = c->stream2;
+  w.s2 = c->net->serial ? c->stream : c->stream2;
   w.R = R;
   w.both = true;
   w.allow_freeze = allow_freeze;
@@ -1330,7 +1345,7 @@ void run_pass_graph(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
   n->arena_used = 0;
   reset_stats(n, ws.stats);
   Walker w{n, s, t};
-  w.s2 = n->stream2;
+  w.s2 = n->net->serial ? n->stream : n->stream2;
   w.devr = true;
   w.dR = n->d_int;  // the seed's live count
   w.R = N;
@@ -1389,7 +1404,7 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
     // / concretisation chains and checkpoint round trips (rows are
     // independent, backsub.hpp:31-34; results identical).
     static const int pipes = env_int("PC_PIPES", 2);
-    const bool two = pipes >= 2 && !n->is_helper && chunk >= 16;
+    const bool two = pipes >= 2 && !n->is_helper && chunk >= 16 && !n->net->serial;
     // rows of a walk ride in gridDim.y (both polarities: 2R <= 65535)
     chunk = std::min<long long>(chunk, two ? 2ll * kMaxWalkRows : kMaxWalkRows);
     Ctx* h = two ? helper_of(n) : nullptr;
@@ -1448,7 +1463,7 @@ void run_margin_graph(Ctx* n, pc_stats* st) {
   n->arena_used = 0;
   reset_stats(n, ws.stats);
   Walker w{n, s, out};
-  w.s2 = n->stream2;
+  w.s2 = n->net->serial ? n->stream : n->stream2;
   w.R = nr;
   w.both = false;
   w.margin = true;
@@ -1485,7 +1500,7 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
     n->arena_used = 0;
     reset_stats(n, ws.stats);
     Walker w{n, s, out};
-    w.s2 = n->stream2;
+    w.s2 = n->net->serial ? n->stream : n->stream2;
     w.R = R;
     w.both = false;
     w.margin = true;
@@ -1569,6 +1584,9 @@ void forward_layers(Ctx* n, int k0, int k1, int nimg = 1) {
       launch_forward_layer(n->stream, l.d, l.feeds_relu, n->blo, n->bhi, n->rlo, n->rhi, n->off.data(),
                            n->pofs.data(), k, l.pred0, l.pred1, n->dev, n->relax, n->gen_n,
                            n->gen_pos, n->gen_l, n->gen, 1);
+    if (l.kind == KIND_RELU)
+      launch_offset_list(n->stream, (int)l.numel(), n->relax + 8 * n->off[l.pred0], n->un_idx + n->off[l.pred0],
+                         n->un_cnt + l.pred0, nimg, T, nl);
     if (l.kind == KIND_RELU && n->net->live_cells) {
       const long long o = n->off[k];
       launch_live_build(n->stream, l.out_w * l.out_h, l.out_c, n->relax + 8 * n->off[l.pred0], n->blo + o,
@@ -1688,6 +1706,7 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
       st->gbc_dense_equiv += (long long)c.gbc_dense_equiv;
       st->dense_madds += (long long)c.dense_madds;
       st->gbc_madds += (long long)c.gbc_madds;
+      g_conv_exec = (double)c.conv_exec;
       st->rows_terminated_early += (long long)(c.frozen + c.pad);
       return;
     }
@@ -1762,6 +1781,7 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
   st->gbc_dense_equiv += (long long)c.gbc_dense_equiv;
   st->dense_madds += (long long)c.dense_madds;
   st->gbc_madds += (long long)c.gbc_madds;
+  g_conv_exec = (double)c.conv_exec;
   st->rows_terminated_early += (long long)(c.frozen + c.pad);
 }
 
@@ -1811,7 +1831,7 @@ void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stat
         n->arena_used = 0;
         reset_stats(n, ws.stats);
         Walker w{n, s, t};
-        w.s2 = n->stream2;
+        w.s2 = n->net->serial ? n->stream : n->stream2;
         w.R = R;
         w.both = true;
         w.allow_freeze = allow_freeze;
@@ -1860,7 +1880,7 @@ void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stat
     n->arena_used = 0;
     reset_stats(n, ws.stats);
     Walker w{n, s, out};
-    w.s2 = n->stream2;
+    w.s2 = n->net->serial ? n->stream : n->stream2;
     w.R = R;
     w.both = false;
     w.margin = true;
@@ -2063,6 +2083,14 @@ const char* pc_last_error(void) { return g_err.c_str(); }
 double pc_last_dense_madds(void) { return g_dense_madds; }
 long long pc_last_launch_count(void) { return g_last_launches; }
 
+double pc_last_conv_executed_madds(void) { return g_conv_exec; }
+
+pc_status pc_net_set_serial(pc_net* net, int serial) {
+  if (!net) return PC_ERR_INVALID_ARGUMENT;
+  net->serial = serial != 0;
+  return PC_OK;
+}
+
 void pc_last_kernel_timing(int kernel, double* ms, double* bytes, long long* launches) {
   const bool conv = kernel == 1;
   if (ms) *ms = conv ? g_conv_ms : g_dense_ms;
@@ -2102,6 +2130,13 @@ pc_status pc_fp64_peak(int device, double* fma_per_s) {
 
 pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, long long n) {
   return guard([&] { ck(scalar_ops_device(op, a, b, out, n), "scalar_ops"); });
+}
+
+pc_status pc_chain_fold(int n_chains, int len, const double* acc0, const double* terms, const int* up,
+                        double* out) {
+  if (n_chains < 0 || len < 0 || (n_chains && (!acc0 || !up || !out || (len && !terms))))
+    return PC_ERR_INVALID_ARGUMENT;
+  return guard([&] { ck(chain_fold_device(n_chains, len, acc0, terms, up, out), "chain_fold"); });
 }
 
 pc_status pc_validate(const pc_layer_desc* layers, int n_layers, int in_w, int in_h, int in_c,

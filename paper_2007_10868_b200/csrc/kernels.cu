@@ -13,6 +13,7 @@
 
 #include "kernels.cuh"
 #include "numeric.cuh"
+#include "scanfold.cuh"
 
 namespace pc {
 
@@ -1028,6 +1029,129 @@ void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, M
   }
   k_chain_relu<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, Kout, relax,
                                                                       frozen);
+  ++g_launches;
+}
+
+// ---------------------------------------------------------------------------
+// relu_step constants from the layer's offset list. Only neurons with a
+// nonzero relaxation offset (beta or delta; the unstable ones,
+// analyzer.hpp:56-66) add terms (backsub.hpp:536-563: stable neurons' offset
+// products are exact zeros, skipped by iv_acc), so the chain visits the
+// ascending list of those neurons (k_offset_list, built once per image when
+// the layer's bounds are final) instead of scanning the row: same terms, same
+// order. Warp per row; lanes 0..3 fold k.lo, k.hi, kraw.lo, kraw.hi.
+__global__ void __launch_bounds__(1024)
+    k_offset_list(int n, const double* relax, int* list, int* count, long long sst, int cstride) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_base;
+  const int img = blockIdx.z;
+  relax += 8 * img * sst;
+  list += img * sst;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int start = 0; start < n; start += 1024) {
+    const int j = start + threadIdx.x;
+    int has = 0;
+    if (j < n) {
+      const double* R = relax + 8 * (long long)j;
+      has = !(bits_zero(R[2]) & bits_zero(R[3]) & bits_zero(R[6]) & bits_zero(R[7]));
+    }
+    int pos, total;
+    Scan(tmp).ExclusiveSum(has, pos, total);
+    if (has) list[s_base + pos] = j;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) count[img * cstride] = s_base;
+}
+
+void launch_offset_list(cudaStream_t s, int n, const double* relax, int* list, int* count,
+                        int nimg, long long sst, int cstride) {
+  k_offset_list<<<dim3(1, 1, nimg), 1024, 0, s>>>(n, relax, list, count, sst, cstride);
+  ++g_launches;
+}
+
+__global__ void __launch_bounds__(32 * kChainWarps)
+    k_chain_relu_list(RowsDev rows, FrameDev f, MatDev m, double* Kout, const double* relax,
+                      const int* list, const int* count, int cstride, const char* frozen) {
+  __shared__ double s_t[kChainWarps][2][2][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * kChainWarps + warp, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  relax += 8 * img * rows.sst;
+  list += img * rows.sst;
+  const int n = count[img * cstride];
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const size_t pr = phys_row(m, i);
+  const double* lo = m.lo + pr * m.cells;
+  const double* hi = m.hi + pr * m.cells;
+  double acc = lane < 4 ? m.K[4 * pr + lane] : 0.0;
+  const bool up = lane & 1;
+  const int arr = lane & 1;
+  const int GC = f.G_w * f.C;
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int e = e0 + lane;
+    double t0l = PC_NAN, t0h = PC_NAN, t1l = PC_NAN, t1h = PC_NAN;
+    if (e < n) {
+      const int j = list[e];
+      const int ah = j / GC, rem = j - ah * GC;
+      const int aw = rem / f.C, d = rem - aw * f.C;
+      const int x = aw - bw, y = ah - bh;
+      if (x >= 0 && x < f.S_w && y >= 0 && y < f.S_h) {
+        const long long cell = ((long long)y * f.S_w + x) * f.C + d;
+        const Iv c{lo[cell], hi[cell]};
+        if (!iv_zero(c)) {
+          const double* R = relax + 8 * (long long)j;
+          const Iv beta{R[2], R[3]}, delta{R[6], R[7]};
+          const Iv op = upper ? delta : beta;
+          const Iv on = upper ? beta : delta;
+          Iv o0{0.0, 0.0}, o1{0.0, 0.0};
+          if (!(c.lo < 0.0)) o0 = iv_mul(c, op);
+          else if (!(c.hi > 0.0)) o0 = iv_mul(c, on);
+          else {
+            o0 = iv_mul(iv_pos_part(c), op);
+            o1 = iv_mul(iv_neg_part(c), on);
+          }
+          if (!iv_zero(o0)) { t0l = o0.lo; t0h = o0.hi; }
+          if (!iv_zero(o1)) { t1l = o1.lo; t1h = o1.hi; }
+        }
+      }
+    }
+    const bool v = (t0l == t0l) | (t0h == t0h) | (t1l == t1l) | (t1h == t1h);
+    const unsigned mask = __ballot_sync(0xffffffffu, v);
+    if (v) {
+      const int p = __popc(mask & ((1u << lane) - 1u));
+      s_t[warp][0][0][p] = t0l;
+      s_t[warp][0][1][p] = t0h;
+      s_t[warp][1][0][p] = t1l;
+      s_t[warp][1][1][p] = t1h;
+    }
+    __syncwarp();
+    if (lane < 4) {
+      const int k = __popc(mask);
+      for (int u = 0; u < k; ++u) {
+        const double a = s_t[warp][0][arr][u], b = s_t[warp][1][arr][u];
+        if (a == a) acc = up ? add_up(acc, a) : add_down(acc, a);
+        if (b == b) acc = up ? add_up(acc, b) : add_down(acc, b);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane < 4) Kout[4 * (size_t)i + lane] = acc;
+}
+
+void launch_chain_relu_list(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                            double* Kout, const double* relax, const int* list, const int* count,
+                            int cstride, const char* frozen) {
+  k_chain_relu_list<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, Kout, relax, list,
+                                                                           count, cstride, frozen);
   ++g_launches;
 }
 
@@ -2489,7 +2613,7 @@ void launch_live_build(cudaStream_t s, int npos, int C, const double* relax, con
 template <int MINB>
 __global__ void __launch_bounds__(256, MINB)
     k_gbc_live(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
-               MatDev out, LiveDev lv) {
+               MatDev out, LiveDev lv, Counters* ctr) {
   int i;
   if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
@@ -2512,6 +2636,7 @@ __global__ void __launch_bounds__(256, MINB)
   const int lane = threadIdx.x & 31;
   const int npos = fo.S_w * fo.S_h;
   MagAcc mag;
+  unsigned long long exec = 0;  // madds of the live cells (lane 0's tally)
   for (int pos = blockIdx.x * 8 + (threadIdx.x >> 5); pos < npos; pos += gridDim.x * 8) {
     const int y = pos / fo.S_w, x = pos - y * fo.S_w;
     const int iy = nbh + y, ix = nbw + x;
@@ -2532,6 +2657,12 @@ __global__ void __launch_bounds__(256, MINB)
     ah1 = min(ah1, bh + fi.S_h - 1);
     aw0 = max(aw0, bw);
     aw1 = min(aw1, bw + fi.S_w - 1);
+    if (ctr && lane == 0) {
+      int terms = 0;
+      for (int ah = ah0; ah <= ah1; ++ah)
+        for (int aw = aw0; aw <= aw1; ++aw) terms += cnt[(ah - bh) * fi.S_w + (aw - bw)];
+      exec += (unsigned long long)terms * nl;
+    }
     for (int k0 = 0; k0 < nl; k0 += 64) {
       const int ka = k0 + lane, kb = k0 + 32 + lane;
       const bool va = ka < nl, vb = kb < nl;
@@ -2620,17 +2751,18 @@ __global__ void __launch_bounds__(256, MINB)
     }
   }
   mag.flush(out.stat);
+  if (ctr && lane == 0 && exec) atomicAdd(&ctr[img].conv_exec, exec);
 }
 
 void launch_gbc_live(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
-                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv) {
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv, Counters* ctr) {
   static const int minb = env_int("PC_GBC_LIVE_MINB", 2);
   unsigned gx = cdiv(fout.S_w * fout.S_h, 8);
   if (gx > 1024) gx = 1024;
   dim3 grid(gx, rows.n);
-  if (minb >= 3) k_gbc_live<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv);
-  else if (minb == 2) k_gbc_live<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv);
-  else k_gbc_live<1><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv);
+  if (minb >= 3) k_gbc_live<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv, ctr);
+  else if (minb == 2) k_gbc_live<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv, ctr);
+  else k_gbc_live<1><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, lv, ctr);
   ++g_launches;
 }
 
@@ -3262,6 +3394,44 @@ cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* 
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaMemcpy(out, d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
+
+// Chain-fold self test: chain c folds terms[c * len .. +len) into acc0[c]
+// with add_up (up[c]) or add_down, by the warp scan of scanfold.cuh (the
+// chain kernels' fold). One warp per chain.
+__global__ void k_chain_fold(int n_chains, int len, const double* acc0, const double* terms,
+                             const int* up, double* out) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n_chains) return;
+  const double* t = terms + (size_t)c * len;
+  const bool dir = up[c] & 1;  // bit 1 set: the 32-link fold (scan_fold) instead of scan_fold4
+  const double r = (up[c] & 2) ? scan_fold(acc0[c], len, dir, [&](int j) { return t[j]; })
+                               : scan_fold4(acc0[c], len, dir, [&](int j) { return t[j]; });
+  if ((threadIdx.x & 31) == 0) out[c] = r;
+}
+
+cudaError_t chain_fold_device(int n_chains, int len, const double* acc0, const double* terms,
+                              const int* up, double* out) {
+  const size_t nt = (size_t)n_chains * len;
+  char* d = nullptr;
+  const size_t bytes = 8 * (2 * (size_t)n_chains + nt) + 4 * (size_t)n_chains + 64;
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e != cudaSuccess) return e;
+  double* da = reinterpret_cast<double*>(d);
+  double* dt = da + n_chains;
+  double* dout = dt + nt;
+  int* du = reinterpret_cast<int*>(dout + n_chains);
+  e = cudaMemcpy(da, acc0, 8 * (size_t)n_chains, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && nt) e = cudaMemcpy(dt, terms, 8 * nt, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(du, up, 4 * (size_t)n_chains, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && n_chains > 0) {
+    k_chain_fold<<<cdiv(n_chains, 4), 128>>>(n_chains, len, da, dt, du, dout);
+    ++g_launches;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, 8 * (size_t)n_chains, cudaMemcpyDeviceToHost);
   cudaFree(d);
   return e;
 }

@@ -275,6 +275,7 @@ struct Counters {  // device-side PassStats accumulators
   unsigned long long pad;
   unsigned long long gbc_dense_equiv;
   unsigned long long checkpoints;  // non-margin checkpoints the reference would run
+  unsigned long long conv_exec;    // interval madds executed by k_gbc_live (live cells only)
 };
 
 // ----- launchers (kernels.cu) -----
@@ -364,9 +365,16 @@ struct LiveDev {
 void launch_live_build(cudaStream_t s, int npos, int C, const double* relax, const double* blo,
                        const double* bhi, const double* rlo, const double* rhi, int* cnt,
                        unsigned short* idx, int nimg, long long sst, long long pst);
+// Ascending list of the neurons of a ReLU layer with a nonzero relaxation
+// offset (k_offset_list) and the relu_step constant chains over it.
+void launch_offset_list(cudaStream_t s, int n, const double* relax, int* list, int* count,
+                        int nimg, long long sst, int cstride);
+void launch_chain_relu_list(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                            double* Kout, const double* relax, const int* list, const int* count,
+                            int cstride, const char* frozen);
 // Conv coefficients of the live cells of a ReLU frame (dead ones written +0).
 void launch_gbc_live(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
-                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv);
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv, Counters* ctr);
 // Conv coefficients from the compacted input (band path; falls back to the
 // checked gather on `in` when the launch's operands are not proven in band).
 void launch_gbc_sparse(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
@@ -414,6 +422,8 @@ void launch_eval_layer(cudaStream_t s, const LayerDev& L, const double* x, const
 
 cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* out, long long n);
 cudaError_t fp64_peak_device(double* fma_per_s);
+cudaError_t chain_fold_device(int n_chains, int len, const double* acc0, const double* terms,
+                              const int* up, double* out);
 
 extern thread_local long long g_launches;
 

@@ -223,7 +223,13 @@ class Verifier:
         ms, by, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
         _lib.lib.pc_last_kernel_timing(1 if kernel == "conv" else 0, ctypes.byref(ms), ctypes.byref(by),
                                        ctypes.byref(n))
-        return {"ms": ms.value, "bytes": by.value, "launches": n.value}
+        return {"ms": ms.value, "bytes": by.value, "launches": n.value,
+                "executed_madds": float(_lib.lib.pc_last_conv_executed_madds()) if kernel == "conv" else None}
+
+    def set_serial(self, serial: bool = True):
+        """One stream, one pipeline per walk, so per-launch CUDA events time
+        each kernel alone (roofline measurement); results are identical."""
+        _lib.check(_lib.lib.pc_net_set_serial(self._h, int(bool(serial))))
 
     def last_timing(self):
         t, dm, db, dl = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()

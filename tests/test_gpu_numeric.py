@@ -93,3 +93,87 @@ def test_band_forms(port):
         assert np.array_equal(g, r), (op, np.flatnonzero(g != r)[:4])
         nz = r != 0
         assert same_bits(g[nz], r[nz]), op
+
+
+def gpu_chain_fold(acc0, terms, up):
+    from paper_2007_10868_b200 import _lib
+    acc0 = np.ascontiguousarray(acc0, dtype=np.float64)
+    terms = np.ascontiguousarray(terms, dtype=np.float64)
+    upa = np.ascontiguousarray(up, dtype=np.int32)
+    out = np.empty_like(acc0)
+    vp = ctypes.c_void_p
+    _lib.check(_lib.lib.pc_chain_fold(terms.shape[0], terms.shape[1], acc0.ctypes.data_as(vp),
+                                      terms.ctypes.data_as(vp), upa.ctypes.data_as(vp),
+                                      out.ctypes.data_as(vp)))
+    return out
+
+
+def chain_cases(rng, n_chains, length):
+    """Adversarial chains for the scan fold (scanfold.cuh): every regime that
+    must leave the integer scan (ties, binade and sign changes, zero and
+    subnormal accumulators, huge / infinite / tiny terms) next to the common
+    one (many small inexact terms on a large accumulator)."""
+    T = np.empty((n_chains, length))
+    A = np.empty(n_chains)
+    for c in range(n_chains):
+        kind = c % 12
+        if kind == 0:    # the common regime: random terms, |acc| >> |t|
+            T[c] = rng.standard_normal(length) * 1e-3
+            A[c] = rng.standard_normal() * 10
+        elif kind == 1:  # dyadic terms: exact adds and exact half-ulp ties
+            A[c] = 1.0 + rng.integers(0, 2 ** 20) * 2.0 ** -52
+            T[c] = rng.integers(-4, 5, length) * 2.0 ** -53
+        elif kind == 2:  # random walk through zero: sign and binade changes
+            A[c] = 0.0
+            T[c] = rng.standard_normal(length)
+        elif kind == 3:  # accumulator near a power of two
+            A[c] = 2.0 ** rng.integers(-20, 20)
+            T[c] = rng.standard_normal(length) * 2.0 ** -45 * A[c]
+        elif kind == 4:  # tiny terms, sometimes below the accumulator's ulp
+            A[c] = rng.standard_normal()
+            T[c] = rng.standard_normal(length) * 10.0 ** rng.integers(-40, -10, length)
+        elif kind == 5:  # huge terms, infinities, zeros, NaN (no term)
+            A[c] = rng.standard_normal() * 1e3
+            T[c] = rng.standard_normal(length)
+            m = rng.integers(0, 50, length)
+            T[c][m == 0] = 1e300
+            T[c][m == 1] = -1e300
+            T[c][m == 2] = 0.0
+            T[c][m == 3] = -0.0
+            T[c][m == 4] = np.nan
+            T[c][m == 5] = np.inf if c % 24 == 5 else T[c][m == 5]
+        elif kind == 6:  # subnormal region
+            A[c] = 5e-324 * rng.integers(1, 1000)
+            T[c] = rng.standard_normal(length) * 1e-310
+        elif kind == 7:  # signed zero starts, then exact cancellations
+            A[c] = -0.0
+            x = rng.integers(-8, 9, length) / 8.0
+            T[c] = np.where(np.arange(length) % 2, -np.roll(x, 1), x)
+        elif kind == 8:  # terms comparable to the accumulator (every link changes binade often)
+            A[c] = rng.standard_normal()
+            T[c] = rng.standard_normal(length) * np.abs(A[c])
+        elif kind == 9:  # row-constant shape: bias products c*b, b = k/64
+            A[c] = rng.integers(-32, 33) / 64.0
+            T[c] = rng.standard_normal(length) * 1e-2 * rng.integers(-32, 33, length) / 64.0
+        elif kind == 10:  # large magnitudes near the scan's exponent limits
+            A[c] = 2.0 ** rng.integers(800, 1000) * rng.standard_normal()
+            T[c] = rng.standard_normal(length) * 2.0 ** rng.integers(700, 1010)
+        else:            # very small magnitudes near the limits
+            A[c] = 2.0 ** rng.integers(-1000, -800) * rng.standard_normal()
+            T[c] = rng.standard_normal(length) * 2.0 ** rng.integers(-1070, -820)
+    return A, T
+
+
+@pytest.mark.parametrize("length", [1, 31, 33, 1000, 5000])
+def test_chain_fold_matches_serial(port, length):
+    """The warp-scan fold == the reference's serial add_up / add_down chain,
+    bit for bit, on both directions."""
+    rng = np.random.default_rng(length)
+    A, T = chain_cases(rng, 96, length)
+    for upv in (0, 1, 2, 3):  # bit 0: add_up; bit 1: the 32-link scan variant
+        up = np.full(len(A), upv, dtype=np.int32)
+        up[::3] ^= 1
+        g = gpu_chain_fold(A, T, up)
+        r = port.chain_fold(A, T, up & 1)
+        bad = ~((g.view(np.int64) == r.view(np.int64)) | (np.isnan(g) & np.isnan(r)))
+        assert not bad.any(), (np.nonzero(bad)[0][:8] % 12, g[bad][:4], r[bad][:4])
