@@ -187,6 +187,8 @@ struct Ctx {
   double* ckat = nullptr;  // per live row: the checkpoint that froze it (k_ck_count)
   int* lv_cnt = nullptr;             // live channels per grid position of each ReLU layer
   unsigned short* lv_idx = nullptr;  // (k_live_build; read by the conv kernel k_gbc_live)
+  int* lv_pref = nullptr;             // flat live-cell list per ReLU layer (k_live_flat):
+  unsigned short *lv_fpos = nullptr, *lv_fch = nullptr;  // prefix per position, position, channel
   int* un_idx = nullptr;  // per ReLU layer: ascending neurons with a nonzero relaxation offset
   int* un_cnt = nullptr;  // their count per (image, layer) (k_offset_list)
   int* d_label = nullptr;
@@ -281,6 +283,9 @@ struct Ctx {
     lv_cnt = dalloc<int>((size_t)pofs[nl] * nimg);
     lv_idx = dalloc<unsigned short>(T);
     un_idx = dalloc<int>(T);
+    lv_pref = dalloc<int>(((size_t)pofs[nl] + nl) * nimg);
+    lv_fpos = dalloc<unsigned short>(T);
+    lv_fch = dalloc<unsigned short>(T);
     un_cnt = dalloc<int>((size_t)nl * nimg);
     d_label = dalloc<int>(nimg);
     d_slots = dalloc<int>(kSlots);
@@ -781,10 +786,18 @@ struct Walker {
                         8.0 * L.fw * L.fh * L.in_c * L.out_c;
         ++g_conv_launches;
       }
-      if (sparse && n->net->live_cells && n->L[L.pred0].kind == KIND_RELU) {
+      static const int live_min_cin = env_int("PC_LIVE_MIN_CIN", 0);
+      if (sparse && n->net->live_cells && n->L[L.pred0].kind == KIND_RELU && L.in_c >= live_min_cin) {
         const int nl = (int)n->L.size();
-        const LiveDev lv{n->lv_cnt + n->pofs[L.pred0], n->lv_idx + n->off[L.pred0], n->pofs[nl], n->total};
-        launch_gbc_live(s, L.d, rows(), fi, fo, sp, md(m), md(out), lv, n->ctr);
+        static const int flat = env_int("PC_GBC_FLAT", 1);
+        if (flat && fo.S_h <= 64 && (long long)fo.G_w * fo.G_h < 65536) {
+          const FlatDev fl{n->lv_pref + n->pofs[L.pred0] + L.pred0, n->lv_fpos + n->off[L.pred0],
+                           n->lv_fch + n->off[L.pred0], n->pofs[nl] + nl, n->total};
+          launch_gbc_flat(s, L.d, rows(), fi, fo, sp, md(m), md(out), fl, n->ctr);
+        } else {
+          const LiveDev lv{n->lv_cnt + n->pofs[L.pred0], n->lv_idx + n->off[L.pred0], n->pofs[nl], n->total};
+          launch_gbc_live(s, L.d, rows(), fi, fo, sp, md(m), md(out), lv, n->ctr);
+        }
       } else if (sparse)
         launch_gbc_sparse(s, L.d, rows(), fi, fo, sp, md(m), md(out));
       else
@@ -1286,6 +1299,9 @@ Ctx* helper_of(Ctx* n) {
   h->lv_cnt = n->lv_cnt;
   h->lv_idx = n->lv_idx;
   h->un_idx = n->un_idx;
+  h->lv_pref = n->lv_pref;
+  h->lv_fpos = n->lv_fpos;
+  h->lv_fch = n->lv_fch;
   h->un_cnt = n->un_cnt;
   h->live = n->live; h->ctr = n->ctr;
   h->gen_n = n->gen_n; h->gen_pos = n->gen_pos; h->gen_l = n->gen_l;
@@ -1592,6 +1608,8 @@ void forward_layers(Ctx* n, int k0, int k1, int nimg = 1) {
       launch_live_build(n->stream, l.out_w * l.out_h, l.out_c, n->relax + 8 * n->off[l.pred0], n->blo + o,
                         n->bhi + o, n->rlo + o, n->rhi + o, n->lv_cnt + n->pofs[k], n->lv_idx + o, nimg,
                         T, P);
+      launch_live_flat(n->stream, l.out_w * l.out_h, l.out_c, n->lv_cnt + n->pofs[k], n->lv_idx + o,
+                       n->lv_pref + n->pofs[k] + k, n->lv_fpos + o, n->lv_fch + o, nimg, T, P, P + nl);
     }
     prof_end(n);
   }

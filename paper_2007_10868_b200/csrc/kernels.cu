@@ -2075,6 +2075,17 @@ __device__ __forceinline__ Iv gbc_gather(const LayerDev& L, const FrameDev& fi, 
   return Iv{lo, hi};
 }
 
+// The checked gather out of line (keeps the band loop's register budget).
+static __device__ __noinline__ Iv gbc_gather_checked(const LayerDev& L, const FrameDev& fi, int bw, int bh,
+                                                     const double* ilo, const double* ihi, int iy, int ix,
+                                                     int ci) {
+  bool bad = false;
+  Iv acc = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+  if (bad) acc = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+  return acc;
+}
+
+
 __global__ void __launch_bounds__(256)
     k_gbc_coef(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, MatDev in, MatDev out) {
   int i;
@@ -2406,9 +2417,7 @@ __global__ void __launch_bounds__(256)
     const int iy = nbh + y, ix = nbw + x;
     Iv acc;
     if (!band) {
-      bool bad = false;
-      acc = gbc_gather<1>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
-      if (bad) acc = gbc_gather<0>(L, fi, bw, bh, ilo, ihi, iy, ix, ci, bad);
+      acc = gbc_gather_checked(L, fi, bw, bh, ilo, ihi, iy, ix, ci);
     } else {
       int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
       int aw0 = floordiv(ix + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ix + L.pw, L.sw);
@@ -2752,6 +2761,171 @@ __global__ void __launch_bounds__(256, MINB)
   }
   mag.flush(out.stat);
   if (ctr && lane == 0 && exec) atomicAdd(&ctr[img].conv_exec, exec);
+}
+
+// ---------------------------------------------------------------------------
+// The live cells of a ReLU layer as one flat ascending list (position-major,
+// channel ascending): pref[pos] = live cells before grid position pos,
+// fpos / fch = position and channel of each. Built from k_live_build's
+// per-position lists once per image (k_live_flat: one block scan).
+__global__ void __launch_bounds__(1024)
+    k_live_flat(int npos, int C, const int* cnt, const unsigned short* idx, int* pref,
+                unsigned short* fpos, unsigned short* fch, long long sst, long long pst, long long fst) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_base;
+  const int img = blockIdx.z;
+  cnt += img * pst;
+  idx += img * sst;
+  pref += img * fst;
+  fpos += img * sst;
+  fch += img * sst;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int start = 0; start < npos; start += 1024) {
+    const int p = start + threadIdx.x;
+    const int c = p < npos ? cnt[p] : 0;
+    int off, total;
+    Scan(tmp).ExclusiveSum(c, off, total);
+    off += s_base;
+    if (p < npos) {
+      pref[p] = off;
+      for (int k = 0; k < c; ++k) {
+        fpos[off + k] = (unsigned short)p;
+        fch[off + k] = idx[(long long)p * C + k];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) pref[npos] = s_base;
+}
+
+void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const unsigned short* idx,
+                      int* pref, unsigned short* fpos, unsigned short* fch, int nimg, long long sst,
+                      long long pst, long long fst) {
+  k_live_flat<<<dim3(1, 1, nimg), 1024, 0, s>>>(npos, C, cnt, idx, pref, fpos, fch, sst, pst, fst);
+  ++g_launches;
+}
+
+// Conv coefficients over the flat list of live cells: one output (a live
+// cell of the row's window) per thread, the gather of k_gbc_sparse2 in the
+// reference's (ch, cw, d) order. Threads of a warp take consecutive live
+// cells (one or two grid positions), so coefficient loads are broadcasts and
+// no lane computes a dead cell. The output rows are zeroed beforehand (dead
+// cells). A block takes kFlatOPB consecutive live cells of its row's window:
+// the window's grid rows are consecutive runs of the flat list.
+constexpr int kFlatOPB = 512;
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_gbc_flat(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
+               MatDev out, FlatDev fl, Counters* ctr) {
+  __shared__ int s_seg[65];  // live cells before each window row (S_h <= 64)
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  int bw, bh, nbw, nbh;
+  frame_base(fi, q, bw, bh);
+  frame_base(fo, q, nbw, nbh);
+  const int* pref = fl.pref + (long long)img * fl.fst;
+  const unsigned short* fpos = fl.fpos + (long long)img * fl.sst;
+  const unsigned short* fch = fl.fch + (long long)img * fl.sst;
+  if (threadIdx.x <= fo.S_h) {
+    int c = 0;
+    for (int y = 0; y < (int)threadIdx.x; ++y) {
+      const int g0 = (nbh + y) * fo.G_w + nbw;
+      c += pref[g0 + fo.S_w] - pref[g0];
+    }
+    s_seg[threadIdx.x] = c;
+  }
+  __syncthreads();
+  const int total = s_seg[fo.S_h];
+  const int t0 = blockIdx.x * kFlatOPB;
+  if (t0 >= total) return;
+  const int t1 = min(total, t0 + kFlatOPB);
+  const long long ocells = out.cells;
+  const double* ilo = in.lo + phys_row(in, i) * in.cells;
+  const double* ihi = in.hi + phys_row(in, i) * in.cells;
+  double* olo = out.lo + (size_t)i * ocells;
+  double* ohi = out.hi + (size_t)i * ocells;
+  const int cin = L.in_c, cout = L.out_c;
+  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  const int* cnt = sp.cnt + (size_t)i * sp.ncell;
+  const size_t rbase = (size_t)i * sp.ncell * sp.C;
+  MagAcc mag;
+  unsigned long long exec = 0;
+  int y = 0;
+  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    while (t >= s_seg[y + 1]) ++y;
+    const int e = pref[(nbh + y) * fo.G_w + nbw] + (t - s_seg[y]);
+    const int gp = fpos[e], ci = fch[e];
+    const int iy = nbh + y, ix = gp - iy * fo.G_w;
+    Iv acc;
+    if (!band) {
+      acc = gbc_gather_checked(L, fi, bw, bh, ilo, ihi, iy, ix, ci);
+    } else {
+      int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
+      int aw0 = floordiv(ix + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ix + L.pw, L.sw);
+      ah0 = max(ah0, bh);
+      ah1 = min(ah1, bh + fi.S_h - 1);
+      aw0 = max(aw0, bw);
+      aw1 = min(aw1, bw + fi.S_w - 1);
+      double lo = 0.0, hi = 0.0;
+      for (int ah = ah0; ah <= ah1; ++ah) {
+        const int fy = iy + L.ph - ah * L.sh;
+        for (int aw = aw0; aw <= aw1; ++aw) {
+          const int fx = ix + L.pw - aw * L.sw;
+          const int cell = (ah - bh) * fi.S_w + (aw - bw);
+          const int n = cnt[cell];
+          exec += n;
+          const size_t sb = rbase + (size_t)cell * sp.C;
+          const double* wp = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ci;
+          constexpr int kB = 4;
+          int k = 0;
+          for (; k + kB <= n; k += kB) {
+            double cl[kB], ch[kB], w[kB];
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+              cl[u] = sp.lo[sb + k + u];
+              ch[u] = sp.hi[sb + k + u];
+              w[u] = wp[(size_t)sp.idx[sb + k + u] * cin];
+            }
+#pragma unroll
+            for (int u = 0; u < kB; ++u) madd_band(w[u], cl[u], ch[u], lo, hi);
+          }
+          for (; k < n; ++k) madd_band(wp[(size_t)sp.idx[sb + k] * cin], sp.lo[sb + k], sp.hi[sb + k], lo, hi);
+        }
+      }
+      acc = Iv{canon0(lo), hi};
+    }
+    const size_t o = ((size_t)y * fo.S_w + (ix - nbw)) * cin + ci;
+    olo[o] = acc.lo;
+    ohi[o] = acc.hi;
+    mag.add(acc.lo);
+    mag.add(acc.hi);
+  }
+  mag.flush(out.stat);
+  if (ctr) {
+    for (int o = 16; o > 0; o >>= 1) exec += __shfl_down_sync(__activemask(), exec, o);
+    if ((threadIdx.x & 31) == 0 && exec) atomicAdd(&ctr[img].conv_exec, exec);
+  }
+}
+
+void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr) {
+  static const int minb = env_int("PC_GBC_FLAT_MINB", 3);
+  // dead cells: +0 (the live ones are overwritten)
+  cudaMemsetAsync(out.lo, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
+  cudaMemsetAsync(out.hi, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
+  const long long cells = (long long)fout.S_w * fout.S_h * L.in_c;
+  dim3 grid(cdiv(cells, kFlatOPB), rows.n);
+  if (minb >= 4) k_gbc_flat<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  else if (minb == 3) k_gbc_flat<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  else k_gbc_flat<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  ++g_launches;
 }
 
 void launch_gbc_live(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,

@@ -372,6 +372,19 @@ void launch_offset_list(cudaStream_t s, int n, const double* relax, int* list, i
 void launch_chain_relu_list(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                             double* Kout, const double* relax, const int* list, const int* count,
                             int cstride, const char* frozen);
+// The live cells of a ReLU layer as one flat list (k_live_flat): pref per
+// grid position (npos + 1 entries), position / channel per live cell.
+struct FlatDev {
+  const int* pref;
+  const unsigned short* fpos;
+  const unsigned short* fch;
+  long long fst, sst;  // per-image strides of pref and of fpos / fch
+};
+void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const unsigned short* idx,
+                      int* pref, unsigned short* fpos, unsigned short* fch, int nimg, long long sst,
+                      long long pst, long long fst);
+void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr);
 // Conv coefficients of the live cells of a ReLU frame (dead ones written +0).
 void launch_gbc_live(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv, Counters* ctr);

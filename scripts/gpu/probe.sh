@@ -1,7 +1,7 @@
-# quick conv / latency probes. usage (via gpurun): bash scripts/gpu/probe.sh TAG
-TAG=${1:-probe}
+# quick conv / latency probes. usage (via gpurun): bash scripts/gpu/probe.sh TAG "ENV1" "ENV2" ...
+TAG=${1:-probe}; shift
 mkdir -p gpurun_out
-for env in "" "PC_LIVE_CELLS=0" "PC_LAZY_COMPACT=1" "PC_PIPES=1"; do
+for env in "$@"; do
   echo "== $env"
-  env $env timeout 600 python scripts/conv_probe.py cifar_resnet34 2>&1 | tee -a gpurun_out/probe_$TAG.txt | cut -c1-400
+  env PROBE_SERIAL_ONLY=1 $env timeout 600 python scripts/conv_probe.py cifar_resnet34 2>&1 | tee -a gpurun_out/probe_$TAG.txt | tail -1 | cut -c1-300
 done

@@ -17,6 +17,8 @@ et = not (len(sys.argv) > 3 and sys.argv[3] == "noet")
 arch, eps_s = CONFIGS[name]
 net = pc.generate(MODEL_SEED, arch)
 v = pc.Verifier(net, pc.AnalysisOptions(early_term=et))
+if os.environ.get("PROFILE_SERIAL"):  # one stream, one pipeline: class times are exclusive
+    v.set_serial(True)
 X = pc.random_inputs(INPUT_SEED, n_img + 1, int(np.prod(net.input_shape)))
 for i, x in enumerate(X):
     lab = v.candidate(x)
