@@ -22,11 +22,13 @@ termination on).
          (tests/golden/ref_<config>_img<i>.json, made by
          scripts/ref_fixtures.py from the unmodified reference) are compared
          bit for bit: verdict, margins, PassStats.
-  roofline  the conv back-substitution kernel (k_gbc_sparse2), the dominant
-         kernel of the residual configs: algorithmic FLOPs (4 per interval
-         multiply-add, the reference's gbc_madds) per second of its CUDA-event
-         time vs the FP64 FMA peak measured live (pc_fp64_peak); its HBM
-         fraction beside it.
+  roofline  the conv back-substitution kernel (k_gbc_flat), the dominant
+         kernel of the residual configs: FLOPs (4 per interval multiply-add it
+         executes, device-counted) per second of its CUDA-event time with the
+         walks serialised (each launch alone on the GPU) vs the FP64 FMA peak
+         measured live (pc_fp64_peak); its HBM fraction and the reference-
+         equivalent rate (the reference's gbc_madds, which also counts cells
+         no result reads) beside it.
   cpu_baseline / --impl reference: the unmodified reference (oracle/_ref)
          on the host's cores, one image with AnalysisOptions.workers = all
          host threads (the reference's latency mode). When one image cannot
@@ -326,13 +328,18 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return t.tolist()
 
-    # roofline of the conv kernel: one unsharded verification per rank (the
-    # kernel's own launches, CUDA events on the stream they run on)
+    # roofline of the conv kernel: one unsharded verification per rank with the
+    # walks serialised (one stream, one pipeline), so the CUDA events around
+    # each conv launch time that kernel alone; the kernel counts the interval
+    # multiply-adds it executes (live cells only)
     flush.fill_(1)
     torch.cuda.synchronize()
+    v.set_serial(True)
     r0 = v.test_device(dboxes[0][0].data_ptr(), dboxes[0][1].data_ptr(), labels[0])
     kt = v.last_kernel_timing("conv")
-    roof_madds = r0[2]["gbc_madds"]
+    v.set_serial(False)
+    ref_madds = r0[2]["gbc_madds"]
+    roof_madds = kt["executed_madds"] or ref_madds
     fma_peak = pc.verifier.fp64_peak(local)
 
     transport = None
@@ -427,14 +434,18 @@ def main():
                 "h2d_bytes_per_step": 2 * 8 * n_in, "d2h_bytes_per_step": 8 * (net.output_size - 1) + 4},
         "gpu_launches": int(launches),
         "roofline": {
-            "kernel": "k_gbc_sparse2 (conv back-substitution coefficients)", "bound": "fp64",
+            "kernel": "k_gbc_flat (conv back-substitution coefficients, live cells)", "bound": "fp64",
             "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": achieved_tflops / peak_tflops if peak_tflops else None,
             "traffic": (traffic[0].get("dram_bytes_per_launch") if traffic else None),
+            "traffic_launch": (traffic[0] if traffic else None),
             "traffic_source": (traffic[1] if traffic else "no ncu capture committed for this config"),
-            "algorithmic": "4 FLOPs per interval multiply-add (lo and hi FMA pair), madds = the "
-                           "reference's PassStats.gbc_madds of one image; time = CUDA events around "
-                           "every conv launch of that image",
+            "algorithmic": "4 FLOPs per interval multiply-add (lo and hi FMA pair); madds = the ones the "
+                           "kernel executes (device-counted: live cells x nonzero terms); time = CUDA events "
+                           "around every conv launch of one image with the walks serialised (each launch "
+                           "alone on the GPU)",
+            "reference_equivalent_tflops": 4.0 * ref_madds / conv_s / 1e12 if conv_s > 0 else None,
+            "reference_madds": ref_madds,
             "peak_source": "pc_fp64_peak: DFMA throughput measured live on this GPU (2 FLOPs per FMA)",
             "emulation_note": "bit-exact WidenedFloat64 costs 16 FP64-pipe instructions per interval "
                               "madd (4 algorithmic FLOPs), so frac <= 0.125 at full FP64-pipe use",

@@ -80,6 +80,7 @@ def _load():
         "pc_fp64_peak": (i, [i, vp]),
         "pc_scalar_ops": (i, [i, vp, vp, vp, ll]),
         "pc_chain_fold": (i, [i, i, vp, vp, vp, vp]),
+        "pc_scan_stats": (i, [i, vp]),
         "pc_last_profile": (i, [ctypes.c_char_p, i]),
         "pc_last_error": (ctypes.c_char_p, []),
         "pc_net_set_sharding": (i, [vp, i, i, ALLGATHER_FN, vp]),

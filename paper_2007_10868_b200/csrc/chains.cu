@@ -73,30 +73,36 @@ struct AffineGen {
   int bw, bh;
   const double* dev;
   unsigned long long madds = 0;
-  __device__ bool gen(const double* lo, const double* hi, long long cell, double* t) {
-    const Iv c{lo[cell], hi[cell]};
-    if (iv_zero(c)) return false;
-    double b;
+  // index-only operands of a cell, loaded a tile ahead of its coefficient
+  struct Pre {
+    double b, dj;
+    unsigned taps;
+  };
+  __device__ void pre(long long cell, Pre& p) const {
     long long jd;
     if (is_conv) {
       int d, aw, ah;
       cell_pos(f, cell, bw, bh, d, aw, ah);
-      b = L.bias[d];
+      p.b = L.bias[d];
       jd = ((long long)ah * f.G_w + aw) * f.C + d;
       const int y0 = ah * L.sh - L.ph, x0 = aw * L.sw - L.pw;
       const int ny = min(L.fh, L.in_h - y0) - max(0, -y0);
       const int nx = min(L.fw, L.in_w - x0) - max(0, -x0);
-      if (ny > 0 && nx > 0) madds += (unsigned long long)L.in_c * ny * nx;
+      p.taps = (ny > 0 && nx > 0) ? (unsigned)(L.in_c * ny * nx) : 0u;
     } else {
-      b = L.bias[cell];
+      p.b = L.bias[cell];
       jd = cell;
-      madds += (unsigned long long)L.in_w * L.in_h * L.in_c;
+      p.taps = (unsigned)(L.in_w * L.in_h * L.in_c);
     }
-    const Iv bt = iv_mul_scalar(c, b);
+    p.dj = dev[jd];
+  }
+  __device__ bool gen(Iv c, const Pre& p, double* t) {
+    if (iv_zero(c)) return false;
+    madds += p.taps;
+    const Iv bt = iv_mul_scalar(c, p.b);
     t[0] = iv_zero(bt) ? PC_NAN : bt.lo;
     t[1] = iv_zero(bt) ? PC_NAN : bt.hi;
-    const double dj = dev[jd];
-    t[2] = dj != 0.0 ? mul_up(iv_mag(c), dj) : PC_NAN;
+    t[2] = p.dj != 0.0 ? mul_up(iv_mag(c), p.dj) : PC_NAN;
     return true;
   }
   // fold lanes: k.lo, k.hi, kraw.lo, kraw.hi, dev
@@ -115,13 +121,19 @@ struct ReluGen {
   bool upper;
   const double* relax;
   unsigned long long madds = 0;
-  __device__ bool gen(const double* lo, const double* hi, long long cell, double* t) {
-    const Iv c{lo[cell], hi[cell]};
-    if (iv_zero(c)) return false;
+  struct Pre {
+    Iv beta, delta;
+  };
+  __device__ void pre(long long cell, Pre& p) const {
     int d, aw, ah;
     cell_pos(f, cell, bw, bh, d, aw, ah);
     const double* R = relax + 8 * (((long long)ah * f.G_w + aw) * f.C + d);
-    const Iv beta{R[2], R[3]}, delta{R[6], R[7]};
+    p.beta = Iv{R[2], R[3]};
+    p.delta = Iv{R[6], R[7]};
+  }
+  __device__ bool gen(Iv c, const Pre& p, double* t) {
+    if (iv_zero(c)) return false;
+    const Iv beta = p.beta, delta = p.delta;
     const Iv op = upper ? delta : beta;
     const Iv on = upper ? beta : delta;
     if (iv_zero(op) && iv_zero(on)) return false;  // stable neuron: exact zero terms
@@ -155,15 +167,20 @@ struct ConcGen {
   bool upper, skip0;
   const double *blo, *bhi, *rlo, *rhi;
   unsigned long long madds = 0;
-  __device__ bool gen(const double* lo, const double* hi, long long cell, double* t) {
-    const Iv c{lo[cell], hi[cell]};
-    if (iv_zero(c)) return false;
+  struct Pre {
+    Iv B, Br;
+  };
+  __device__ void pre(long long cell, Pre& p) const {
     int d, aw, ah;
     cell_pos(f, cell, bw, bh, d, aw, ah);
     const long long j = ((long long)ah * f.G_w + aw) * f.C + d;
-    const Iv B{blo[j], bhi[j]}, Br{rlo[j], rhi[j]};
-    const double tp = upper ? corner_hi(c, B) : corner_lo(c, B);
-    const double tr = upper ? corner_hi(c, Br) : corner_lo(c, Br);
+    p.B = Iv{blo[j], bhi[j]};
+    p.Br = Iv{rlo[j], rhi[j]};
+  }
+  __device__ bool gen(Iv c, const Pre& p, double* t) {
+    if (iv_zero(c)) return false;
+    const double tp = upper ? corner_hi(c, p.B) : corner_lo(c, p.B);
+    const double tr = upper ? corner_hi(c, p.Br) : corner_lo(c, p.Br);
     const bool zp = skip0 && __double_as_longlong(tp) == 0, zr = skip0 && __double_as_longlong(tr) == 0;
     t[0] = zp ? PC_NAN : tp;
     t[1] = zr ? PC_NAN : tr;
@@ -187,7 +204,38 @@ __device__ __forceinline__ bool chain_up<ConcGen>(const ConcGen& g, int) {
   return g.upper;
 }
 
+// 1-D bulk copies (TMA, cp.async.bulk) global -> shared, completing on an
+// mbarrier with a transaction count.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra "
+      "WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+constexpr int kStages = 4;  // coefficient tiles in flight (TMA ring)
+
 struct ChainShared {
+  unsigned long long bar[kStages];  // coefficient tile staged (TMA) per ring slot
   int cnt[2];
   int wsum[kCT / 32];
   double acc[8];  // each chain's result (consumer warp w -> acc[w])
@@ -204,6 +252,37 @@ __device__ __forceinline__ double fold_row(G& g, const double* lo, const double*
   const int ntiles = (int)((cells + kTile - 1) / kTile);
   const bool consumer = warp < G::NF;
   const bool up = consumer && chain_up(g, warp);
+  // The row's coefficients stream through shared memory by TMA bulk copies
+  // (a kStages ring, issued kStages tiles ahead of the producers), when the
+  // row is 16-byte aligned; the index-only operands of the next tile (bounds,
+  // deviations, biases) are loaded into registers one tile ahead.
+  double* cbuf = buf + 2 * G::NA * kTile;  // [kStages][lo, hi][kTile]
+  const bool tma = ((reinterpret_cast<unsigned long long>(lo) | reinterpret_cast<unsigned long long>(hi)) & 15) == 0;
+  const int p0 = 32 * G::NF;  // first producer thread
+  auto issue = [&](int it) {  // by thread p0
+    const int b = it % kStages;
+    const long long c0 = (long long)it * kTile;
+    const long long n = cells - c0 < kTile ? cells - c0 : kTile;
+    const unsigned bytes = (unsigned)(((n * 8) + 15) & ~15LL);  // the arena rounds rows' ends to 256 B
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
+    mbar_expect_tx(&sh.bar[b], 2 * bytes);
+    bulk_g2s(cbuf + (size_t)b * 2 * kTile, lo + c0, bytes, &sh.bar[b]);
+    bulk_g2s(cbuf + (size_t)b * 2 * kTile + kTile, hi + c0, bytes, &sh.bar[b]);
+  };
+  if (tma && tid == p0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(&sh.bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tma && tid == p0)
+    for (int k = 0; k < kStages && k < ntiles; ++k) issue(k);
+  typename G::Pre pre[kCPT];
+  if (!consumer) {
+    const long long c0 = (long long)(tid - p0) * kCPT;
+#pragma unroll
+    for (int k = 0; k < kCPT; ++k)
+      if (c0 + k < cells) g.pre(c0 + k, pre[k]);
+  }
   for (int it = 0; it <= ntiles; ++it) {
     if (consumer) {
       if (it > 0) {
@@ -220,19 +299,34 @@ __device__ __forceinline__ double fold_row(G& g, const double* lo, const double*
         }
       }
     } else if (it < ntiles) {
-      const int p = tid - 32 * G::NF;
-      const int b = it & 1;
+      const int p = tid - p0;
+      const int b = it & 1, cb = it % kStages;
       double* B = buf + (size_t)b * G::NA * kTile;
+      const double* C = cbuf + (size_t)cb * 2 * kTile;
+      const long long c0 = (long long)it * kTile + (long long)p * kCPT;
+      Iv cv[kCPT];
+      if (tma) {
+        mbar_wait(&sh.bar[cb], (unsigned)((it / kStages) & 1));
+#pragma unroll
+        for (int k = 0; k < kCPT; ++k) cv[k] = Iv{C[p * kCPT + k], C[kTile + p * kCPT + k]};
+      } else {
+#pragma unroll
+        for (int k = 0; k < kCPT; ++k)
+          cv[k] = c0 + k < cells ? Iv{lo[c0 + k], hi[c0 + k]} : Iv{0.0, 0.0};
+      }
       double t[kCPT][G::NA];
       bool v[kCPT];
       int nv = 0;
-      const long long c0 = (long long)it * kTile + (long long)p * kCPT;
 #pragma unroll
       for (int k = 0; k < kCPT; ++k) {
-        v[k] = false;
-        if (c0 + k < cells) v[k] = g.gen(lo, hi, c0 + k, t[k]);
+        v[k] = c0 + k < cells && g.gen(cv[k], pre[k], t[k]);
         if (v[k]) ++nv;
       }
+      // next tile's index-only operands, in flight during the scan and barriers
+      const long long c1 = c0 + kTile;
+#pragma unroll
+      for (int k = 0; k < kCPT; ++k)
+        if (c1 + k < cells) g.pre(c1 + k, pre[k]);
       // exclusive scan of nv over the producer threads (ascending cells)
       int inc = nv;
 #pragma unroll
@@ -260,6 +354,8 @@ __device__ __forceinline__ double fold_row(G& g, const double* lo, const double*
         }
       if (p == 0) sh.cnt[b] = tot;
       asm volatile("bar.sync 1, %0;" ::"r"(kProd));
+      // every producer has read coefficient buffer cb: refill it kStages tiles ahead
+      if (tma && tid == p0 && it + kStages < ntiles) issue(it + kStages);
     }
     __syncthreads();
   }
@@ -270,7 +366,7 @@ __device__ __forceinline__ double fold_row(G& g, const double* lo, const double*
 
 // ----- kernels: one CTA per row -----
 
-__global__ void __launch_bounds__(kCT)
+__global__ void __launch_bounds__(kCT, 2)
     k_chain_affine_big(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, double* Kout,
                        const double* dev, Counters* ctr, const char* frozen) {
   extern __shared__ double buf[];
@@ -304,7 +400,7 @@ __global__ void __launch_bounds__(kCT)
   if (lane == 0 && md) atomicAdd(is_conv ? &ctr->gbc_madds : &ctr->dense_madds, md);
 }
 
-__global__ void __launch_bounds__(kCT)
+__global__ void __launch_bounds__(kCT, 2)
     k_chain_relu_big(RowsDev rows, FrameDev f, MatDev m, double* Kout, const double* relax,
                      const char* frozen) {
   extern __shared__ double buf[];
@@ -324,7 +420,7 @@ __global__ void __launch_bounds__(kCT)
   if (threadIdx.x < 4) Kout[4 * (size_t)i + threadIdx.x] = sh.acc[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(kCT)
+__global__ void __launch_bounds__(kCT, 2)
     k_concretize_big(RowsDev rows, FrameDev f, MatDev m, const double* blo, const double* bhi,
                      const double* rlo, const double* rhi, double* vals, double* rvals,
                      const char* frozen) {
@@ -355,9 +451,162 @@ __global__ void __launch_bounds__(kCT)
   if (threadIdx.x == 1) rvals[i] = sh.acc[1];
 }
 
+// ---------------------------------------------------------------------------
+// CTA-per-chain kernels: every chain of a row is folded by its own CTA with
+// the block-wide scan fold (4 * kSF links per step); terms are computed on the
+// fly by all threads. Used for the conv steps' constant chains (from the
+// compacted nonzero coefficients k_compact_cells already wrote: no second
+// pass over the dense row) and for the checkpoints' concretisations, so a
+// pass with few rows still spreads over many SMs and a row's chain costs
+// microseconds.
+constexpr int kSF = 512;
+
+// gbc_step constants (backsub.hpp:449-489) of one row, one chain per CTA
+// (blockIdx.y: 0 k.lo, 1 k.hi, 2 kraw.lo, 3 kraw.hi, 4 dev); terms in the
+// compacted layout [cell][slot < cnt] = ascending (cell, d). Results go to
+// tmp[5 * i + chain]; k_affine_finish widens and stores K.
+__global__ void __launch_bounds__(kSF)
+    k_chain_affine_scan(LayerDev L, RowsDev rows, FrameDev f, MatDev m, SparseDev sp,
+                        const double* dev, double* tmp, Counters* ctr, const char* frozen) {
+  __shared__ long long sm[2 * kSF / 32 + 4];
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  dev += img * rows.sst;
+  ctr += img;
+  const int chain = blockIdx.y;
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const int C = sp.C;
+  const int* cnt = sp.cnt + (size_t)i * sp.ncell;
+  const size_t rb = (size_t)i * sp.ncell * C;
+  const size_t pr = phys_row(m, i);
+  if (chain == 0) {  // PassStats: madds of the in-grid taps per nonzero coefficient, dense-equivalent work
+    unsigned long long md = 0;
+    for (int cell = threadIdx.x; cell < sp.ncell; cell += kSF) {
+      const int n = cnt[cell];
+      if (!n) continue;
+      const int y = cell / f.S_w, x = cell - y * f.S_w;
+      const int y0 = (bh + y) * L.sh - L.ph, x0 = (bw + x) * L.sw - L.pw;
+      const int ny = min(L.fh, L.in_h - y0) - max(0, -y0);
+      const int nx = min(L.fw, L.in_w - x0) - max(0, -x0);
+      if (ny > 0 && nx > 0) md += (unsigned long long)n * L.in_c * ny * nx;
+    }
+    for (int o = 16; o > 0; o >>= 1) md += __shfl_down_sync(0xffffffffu, md, o);
+    if ((threadIdx.x & 31) == 0 && md) atomicAdd(&ctr->gbc_madds, md);
+    if (threadIdx.x == 0)
+      atomicAdd(&ctr->gbc_dense_equiv, (unsigned long long)L.out_w * L.out_h * L.out_c *
+                                           ((unsigned long long)L.in_w * L.in_h * L.in_c));
+  }
+  const bool up = chain == 1 || chain == 3 || chain == 4;
+  const double acc0 = chain < 4 ? m.K[4 * pr + chain] : 0.0;
+  const int cs = (C & (C - 1)) == 0 ? __ffs(C) - 1 : -1;
+  auto term = [&](int j) -> double {
+    const int cell = cs >= 0 ? (j >> cs) : j / C;
+    const int k = j - cell * C;
+    if (k >= cnt[cell]) return PC_NAN;
+    const size_t e = rb + (size_t)j;
+    const Iv c{sp.lo[e], sp.hi[e]};
+    const int d = sp.idx[e];
+    if (chain < 4) {
+      const Iv bt = iv_mul_scalar(c, L.bias[d]);
+      if (iv_zero(bt)) return PC_NAN;
+      return (chain & 1) ? bt.hi : bt.lo;
+    }
+    const int y = cell / f.S_w, x = cell - y * f.S_w;
+    const double dj = dev[((long long)(bh + y) * f.G_w + (bw + x)) * f.C + d];
+    return dj != 0.0 ? mul_up(iv_mag(c), dj) : PC_NAN;
+  };
+  const double acc = block_scan_fold<kSF>(acc0, sp.ncell * C, up, term, sm);
+  if (threadIdx.x == 0) tmp[5 * (size_t)i + chain] = acc;
+}
+
+// widen_constant (backsub.hpp:175-179) with the dev total, store K.
+__global__ void k_affine_finish(RowsDev rows, const double* tmp, double* Kout, const char* frozen) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * blockDim.x + threadIdx.x, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  const double* t = tmp + 5 * (size_t)i;
+  const double dtot = t[4];
+  double* K = Kout + 4 * (size_t)i;
+  K[0] = dtot != 0.0 ? add_down(t[0], -dtot) : t[0];
+  K[1] = dtot != 0.0 ? add_up(t[1], dtot) : t[1];
+  K[2] = t[2];
+  K[3] = t[3];
+}
+
+// concretize (backsub.hpp:725-764) of one row and one track per CTA
+// (blockIdx.y: 0 padded vs bounds, 1 raw vs raw bounds).
+__global__ void __launch_bounds__(kSF)
+    k_concretize_scan(RowsDev rows, FrameDev f, MatDev m, const double* blo, const double* bhi,
+                      const double* rlo, const double* rhi, double* vals, double* rvals,
+                      const char* frozen) {
+  __shared__ long long sm[2 * kSF / 32 + 4];
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  const int track = blockIdx.y;
+  const long long so = img * rows.sst;
+  const double* BL = (track ? rlo : blo) + so;
+  const double* BH = (track ? rhi : bhi) + so;
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const size_t pr = phys_row(m, i);
+  const double* lo = m.lo + pr * m.cells;
+  const double* hi = m.hi + pr * m.cells;
+  const double* K = m.K + 4 * pr;
+  const double a0 = track ? (upper ? K[3] : K[2]) : (upper ? K[1] : K[0]);
+  const bool skip0 = __double_as_longlong(a0) != (long long)0x8000000000000000ULL;
+  const unsigned C = (unsigned)f.C;
+  const int cs = (C & (C - 1)) == 0 ? __ffs(C) - 1 : -1;
+  auto term = [&](int cell) -> double {
+    const Iv c{lo[cell], hi[cell]};
+    if (iv_zero(c)) return PC_NAN;
+    unsigned pos, d;
+    if (cs >= 0) {
+      pos = (unsigned)cell >> cs;
+      d = (unsigned)cell & (C - 1);
+    } else {
+      pos = (unsigned)cell / C;
+      d = (unsigned)cell - pos * C;
+    }
+    const unsigned y = pos / (unsigned)f.S_w;
+    const long long j = ((long long)(bh + (int)y) * f.G_w + (bw + (int)(pos - y * f.S_w))) * f.C + d;
+    const Iv B{BL[j], BH[j]};
+    const double t = upper ? corner_hi(c, B) : corner_lo(c, B);
+    return (skip0 && __double_as_longlong(t) == 0) ? PC_NAN : t;
+  };
+  const double acc = block_scan_fold<kSF>(a0, (int)m.cells, upper, term, sm);
+  if (threadIdx.x == 0) (track ? rvals : vals)[i] = acc;
+}
+
+void launch_chain_affine_scan(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                              MatDev m, SparseDev sp, double* tmp, double* Kout, const double* dev,
+                              Counters* ctr, const char* frozen) {
+  k_chain_affine_scan<<<dim3(rows.n, 5), kSF, 0, s>>>(L, rows, fin, m, sp, dev, tmp, ctr, frozen);
+  k_affine_finish<<<(rows.n + 127) / 128, 128, 0, s>>>(rows, tmp, Kout, frozen);
+  g_launches += 2;
+}
+
+void launch_concretize_scan(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                            const double* blo, const double* bhi, const double* rlo, const double* rhi,
+                            double* vals, double* rvals, const char* frozen) {
+  k_concretize_scan<<<dim3(rows.n, 2), kSF, 0, s>>>(rows, f, m, blo, bhi, rlo, rhi, vals, rvals, frozen);
+  ++g_launches;
+}
+
 template <class G>
 constexpr size_t chain_smem() {
-  return (size_t)2 * G::NA * Roles<G>::kTile * sizeof(double);
+  return (size_t)(2 * G::NA + 2 * kStages) * Roles<G>::kTile * sizeof(double);  // terms + coefficient ring
 }
 
 static void set_attrs() {
@@ -373,6 +622,15 @@ static void set_attrs() {
 }
 
 void init_kernel_attrs_chains() { set_attrs(); }
+
+cudaError_t scan_stats_device_chains(int on, unsigned long long* out4) {
+  cudaError_t e = cudaSuccess;
+  if (out4) e = cudaMemcpyFromSymbol(out4, g_scan_stats, sizeof(unsigned long long) * 6);
+  const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_scan_stats, z, sizeof(z));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_scan_stats_on, &on, sizeof(int));
+  return e;
+}
 
 void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                              const FrameDev& fin, MatDev m, double* Kout, const double* dev,

@@ -769,15 +769,30 @@ struct Walker {
       sp.lo = arena_take(slots * sizeof(double));
       sp.hi = arena_take(slots * sizeof(double));
     }
+    // constant chains from the compacted coefficients (CTA per chain)
+    static const int chain_scan = env_int("PC_CHAIN_SCAN", 0);
+    const bool scan = sparse && chain_scan && m.cells >= 256;
+    double* tmp = scan ? arena_take((size_t)alloc_rows() * 5 * sizeof(double)) : nullptr;
     if (!dry) {
       const FrameDev fi = fdev(n, m.f, q), fo = fdev(n, nf, q);
-      need(m);
-      prof_begin(n, PROF_CHAIN_AFFINE, s2);
-      launch_chain_affine(s2, L.d, true, rows(), fi, md(m), out.K, n->dev + n->off[m.f.layer],
-                          n->ctr, fz());
-      prof_end(n, s2);
-      prof_begin(n, PROF_GBC);
+      if (!scan) {
+        need(m);
+        prof_begin(n, PROF_CHAIN_AFFINE, s2);
+        launch_chain_affine(s2, L.d, true, rows(), fi, md(m), out.K, n->dev + n->off[m.f.layer],
+                            n->ctr, fz());
+        prof_end(n, s2);
+      }
       if (sparse) launch_compact_cells(s, rows(), md(m), sp);
+      if (scan) {
+        cudaEvent_t e = sync_event(n);
+        ck(cudaEventRecord(e, s), "event");
+        ck(cudaStreamWaitEvent(s2, e, 0), "wait");
+        prof_begin(n, PROF_CHAIN_AFFINE, s2);
+        launch_chain_affine_scan(s2, L.d, rows(), fi, md(m), sp, tmp, out.K, n->dev + n->off[m.f.layer],
+                                 n->ctr, fz());
+        prof_end(n, s2);
+      }
+      prof_begin(n, PROF_GBC);
       if (n->timing) {  // the headline config's roofline kernel (bench.py reads it)
         n->conv_ev.push_back(n->ev_used);
         ck(cudaEventRecord(take_event(n), s), "event");
@@ -894,8 +909,13 @@ struct Walker {
       return;
     }
     prof_begin(n, PROF_CONC, s2);
-    launch_concretize(s2, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
-                      n->rhi + o, n->vals, n->rvals, fz());
+    static const int conc_scan = env_int("PC_CHAIN_SCAN", 0);
+    if (conc_scan && m.cells >= 1024)
+      launch_concretize_scan(s2, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
+                             n->rhi + o, n->vals, n->rvals, fz());
+    else
+      launch_concretize(s2, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
+                        n->rhi + o, n->vals, n->rvals, fz());
     prof_end(n, s2);
     int* new_q = n->rowq[rq ^ 1];
     if (devr) {
@@ -1012,6 +1032,27 @@ struct Walker {
       return;
     }
     resolve(m, R <= lag_rows ? 1 : 0);
+  }
+
+  // True when the next advance() would not block the host: the eager
+  // schedule resolves every pending checkpoint before a step, so it is ready
+  // once the newest one has completed (offers complete in stream order).
+  bool ready() const {
+    static const int lazy = env_int("PC_LAZY_COMPACT", 0);
+    static const int lag_rows = env_int("PC_LAG_ROWS", 0);
+    if (dry || devr || !(allow_freeze && early_term) || lazy || pend.empty()) return true;
+    const size_t keep = R <= lag_rows ? 1 : 0;
+    if (pend.size() <= keep) return true;
+    const cudaError_t e = cudaEventQuery(n->ck_ev[pend[pend.size() - 1 - keep].ck]);
+    if (e == cudaErrorNotReady) return false;
+    ck(e, "event query");
+    return true;
+  }
+  // Block until ready() (the checkpoint the next step waits for).
+  void wait_ready() const {
+    static const int lag_rows = env_int("PC_LAG_ROWS", 0);
+    const size_t keep = R <= lag_rows ? 1 : 0;
+    if (pend.size() > keep) ck(cudaEventSynchronize(n->ck_ev[pend[pend.size() - 1 - keep].ck]), "sync");
   }
 
   // walk_back (backsub.hpp:854-893)
@@ -1435,9 +1476,19 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
         ChunkWalk a{Walker{n, s, t}}, b{Walker{h, h->stream, t}};
         start_chunk(n, a, t, affine, base, RA, allow_freeze, et, st, ws);
         start_chunk(h, b, t, affine, base + RA, RB, allow_freeze, et, st, ws);
+        // advance whichever walk's last checkpoint has resolved, so the host
+        // never blocks on one pipeline while the other could launch work
         while (a.running || b.running) {
-          if (a.running) a.running = a.w.advance(a.m, 0, true, a.pending);
-          if (b.running) b.running = b.w.advance(b.m, 0, true, b.pending);
+          bool moved = false;
+          if (a.running && a.w.ready()) {
+            a.running = a.w.advance(a.m, 0, true, a.pending);
+            moved = true;
+          }
+          if (b.running && b.w.ready()) {
+            b.running = b.w.advance(b.m, 0, true, b.pending);
+            moved = true;
+          }
+          if (!moved) (a.running ? a : b).w.wait_ready();
         }
         stream_wait(n, s, n->stream2);
         stream_wait(n, s, h->stream);
@@ -2148,6 +2199,16 @@ pc_status pc_fp64_peak(int device, double* fma_per_s) {
 
 pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, long long n) {
   return guard([&] { ck(scalar_ops_device(op, a, b, out, n), "scalar_ops"); });
+}
+
+pc_status pc_scan_stats(int on, unsigned long long* out4) {
+  return guard([&] {
+    unsigned long long a[6] = {0, 0, 0, 0, 0, 0}, b[6] = {0, 0, 0, 0, 0, 0};
+    ck(scan_stats_device(on, a), "scan_stats");
+    ck(scan_stats_device_chains(on, b), "scan_stats");
+    if (out4)
+      for (int k = 0; k < 6; ++k) out4[k] = a[k] + b[k];
+  });
 }
 
 pc_status pc_chain_fold(int n_chains, int len, const double* acc0, const double* terms, const int* up,

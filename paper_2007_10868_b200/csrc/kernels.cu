@@ -3586,6 +3586,24 @@ __global__ void k_chain_fold(int n_chains, int len, const double* acc0, const do
   if ((threadIdx.x & 31) == 0) out[c] = r;
 }
 
+__global__ void __launch_bounds__(512) k_chain_fold_block(int len, const double* acc0, const double* terms,
+                                                          const int* up, double* out) {
+  __shared__ long long sm[2 * 512 / 32 + 4];
+  const int c = blockIdx.x;
+  const double* t = terms + (size_t)c * len;
+  const double r = block_scan_fold<512>(acc0[c], len, (up[c] & 1) != 0, [&](int j) { return t[j]; }, sm);
+  if (threadIdx.x == 0) out[c] = r;
+}
+
+cudaError_t scan_stats_device(int on, unsigned long long* out4) {
+  cudaError_t e = cudaSuccess;
+  if (out4) e = cudaMemcpyFromSymbol(out4, g_scan_stats, sizeof(unsigned long long) * 6);
+  const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_scan_stats, z, sizeof(z));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_scan_stats_on, &on, sizeof(int));
+  return e;
+}
+
 cudaError_t chain_fold_device(int n_chains, int len, const double* acc0, const double* terms,
                               const int* up, double* out) {
   const size_t nt = (size_t)n_chains * len;
@@ -3601,7 +3619,10 @@ cudaError_t chain_fold_device(int n_chains, int len, const double* acc0, const d
   if (e == cudaSuccess && nt) e = cudaMemcpy(dt, terms, 8 * nt, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(du, up, 4 * (size_t)n_chains, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && n_chains > 0) {
-    k_chain_fold<<<cdiv(n_chains, 4), 128>>>(n_chains, len, da, dt, du, dout);
+    int u0 = 0;
+    cudaMemcpy(&u0, du, sizeof(int), cudaMemcpyDeviceToHost);
+    if (u0 & 4) k_chain_fold_block<<<n_chains, 512>>>(len, da, dt, du, dout);  // CTA-wide fold
+    else k_chain_fold<<<cdiv(n_chains, 4), 128>>>(n_chains, len, da, dt, du, dout);
     ++g_launches;
     e = cudaGetLastError();
   }

@@ -385,6 +385,15 @@ void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const uns
                       long long pst, long long fst);
 void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr);
+// CTA-per-chain scan-fold kernels (chains.cu): the conv steps' constant
+// chains from the compacted coefficients (tmp: 5 doubles per row), the
+// checkpoints' concretisations.
+void launch_chain_affine_scan(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                              MatDev m, SparseDev sp, double* tmp, double* Kout, const double* dev,
+                              Counters* ctr, const char* frozen);
+void launch_concretize_scan(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
+                            const double* blo, const double* bhi, const double* rlo, const double* rhi,
+                            double* vals, double* rvals, const char* frozen);
 // Conv coefficients of the live cells of a ReLU frame (dead ones written +0).
 void launch_gbc_live(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv, Counters* ctr);
@@ -435,6 +444,8 @@ void launch_eval_layer(cudaStream_t s, const LayerDev& L, const double* x, const
 
 cudaError_t scalar_ops_device(int op, const double* a, const double* b, double* out, long long n);
 cudaError_t fp64_peak_device(double* fma_per_s);
+cudaError_t scan_stats_device(int on, unsigned long long* out4);         // kernels.cu's folds
+cudaError_t scan_stats_device_chains(int on, unsigned long long* out4);  // chains.cu's folds
 cudaError_t chain_fold_device(int n_chains, int len, const double* acc0, const double* terms,
                               const int* up, double* out);
 

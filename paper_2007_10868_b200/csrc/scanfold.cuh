@@ -34,6 +34,18 @@
 
 namespace pc {
 
+#define PC_SCAN_NAN __longlong_as_double(0x7ff8000000000000ULL)
+
+// Diagnostics (pc_scan_stats): [0] scan steps, [1] links committed by scans,
+// [2] scalar links after a failed step, [3] frame-less scalar links.
+// One copy per translation unit (no relocatable device code); each .cu that
+// folds exposes its own accessor (scan_stats_device*).
+static __device__ unsigned long long g_scan_stats[6];
+static __device__ int g_scan_stats_on;
+__device__ __forceinline__ void scan_stat(int k, unsigned long long v) {
+  if (g_scan_stats_on) atomicAdd(&g_scan_stats[k], v);
+}
+
 constexpr long long kScanLo = (1LL << 52) + 2;  // |M| range of a scanned partial result
 constexpr long long kScanHi = (1LL << 53) - 3;
 
@@ -67,12 +79,14 @@ __device__ __forceinline__ long long scan_delta(double t, double inv, bool up, b
   if (ay < 0.25) return up ? 1 : -1;  // 0 < |y| < 1/4: f in (0, 1/4) or (3/4, 1)
   if (!(ay < 0x1p60)) {
     ok = false;
+    scan_stat(5, 1);
     return 0;
   }
   const double T = floor(y);
   const double f = y - T;  // a rounded f can only land on 1/2, which falls back
   if (f == 0.5) {
     ok = false;
+    scan_stat(4, 1);
     return 0;
   }
   long long d = __double2ll_rz(T);
@@ -91,9 +105,19 @@ __device__ __forceinline__ double scan_fold(double acc, int n, bool up, const Te
     double inv;
     long long M;
     if (!scan_frame(acc, ex, inv, M)) {
-      const double t = term(base);
-      if (t == t) acc = up ? add_up(acc, t) : add_down(acc, t);
-      ++base;
+      // no binade frame (zero / subnormal / extreme acc): skip to the next
+      // term (NaN = none) in one step and apply it as the scalar op
+      const int cnt = min(32, n - base);
+      const double tl = lane < cnt ? term(base + lane) : PC_SCAN_NAN;
+      const unsigned has = __ballot_sync(0xffffffffu, tl == tl);
+      if (!has) {
+        base += cnt;
+        continue;
+      }
+      const int k = __ffs(has) - 1;
+      const double t = __shfl_sync(0xffffffffu, tl, k);
+      acc = up ? add_up(acc, t) : add_down(acc, t);
+      base += k + 1;
       continue;
     }
     const int cnt = min(32, n - base);
@@ -122,9 +146,54 @@ __device__ __forceinline__ double scan_fold(double acc, int n, bool up, const Te
   return acc;
 }
 
+// Tie-aware increments: a link whose term sits exactly half way between two
+// grid points (f = 1/2) rounds to the even neighbour, so its increment
+// depends on the parity p of the incoming partial result: the link maps p to
+// (d0, d1)[p]. A run of links composes as such a pair — A then B maps p to
+// A(p) + B(p ^ (A(p) & 1)) — and the composition is associative, so the warp
+// prefix-sums pairs instead of integers and ties stay inside the scan.
+__device__ __forceinline__ void scan_delta2(double t, double inv, bool up, bool& ok, long long& d0,
+                                            long long& d1) {
+  d0 = d1 = 0;
+  if (!(t == t) || t == 0.0) return;
+  const double y = t * inv;
+  const double ay = fabs(y);
+  if (ay < 0.25) {
+    d0 = d1 = up ? 1 : -1;
+    return;
+  }
+  if (!(ay < 0x1p60)) {
+    ok = false;
+    scan_stat(5, 1);
+    return;
+  }
+  const double T = floor(y);
+  const double f = y - T;
+  const long long Ti = __double2ll_rz(T);
+  if (f == 0.5) {  // RN(m + T + 1/2) = the even one of m + T, m + T + 1
+    const long long q = Ti & 1, base = Ti + (up ? 1 : -1);
+    d0 = base + q;
+    d1 = base + (1 - q);
+    scan_stat(4, 1);
+    return;
+  }
+  long long d = Ti;
+  if (f != 0.0) d += up ? (f < 0.5 ? 1 : 2) : (f < 0.5 ? -1 : 0);
+  d0 = d1 = d;
+}
+
+// a then b, as parity-indexed pairs
+__device__ __forceinline__ void scan_compose2(long long a0, long long a1, long long b0, long long b1,
+                                              long long& c0, long long& c1) {
+  const long long x0 = a0 + ((a0 & 1) ? b1 : b0);
+  const long long x1 = a1 + ((a1 & 1) ? b0 : b1);
+  c0 = x0;
+  c1 = x1;
+}
+
 // The same fold, 4 links per lane (128 per warp step): lane l takes links
-// 4l .. 4l+3 of the group, prefix-sums them locally and the lane totals across
-// the warp, so a step costs one warp scan for 128 links.
+// 4l .. 4l+3 of the group, composes them locally and scans the lane pairs
+// across the warp, so a step costs one warp scan for 128 links.
 template <class TermFn>
 __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const TermFn& term) {
   const int lane = threadIdx.x & 31;
@@ -133,38 +202,53 @@ __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const T
     int ex;
     double inv;
     long long M;
-    if (!scan_frame(acc, ex, inv, M)) {
-      const double t = term(base);
-      if (t == t) acc = up ? add_up(acc, t) : add_down(acc, t);
-      ++base;
+    if (!scan_frame(acc, ex, inv, M)) {  // skip to the next term, apply it as the scalar op
+      const int cnt = min(32, n - base);
+      const double tl = lane < cnt ? term(base + lane) : PC_SCAN_NAN;
+      const unsigned has = __ballot_sync(0xffffffffu, tl == tl);
+      if (!has) {
+        base += cnt;
+        continue;
+      }
+      const int k = __ffs(has) - 1;
+      const double t = __shfl_sync(0xffffffffu, tl, k);
+      acc = up ? add_up(acc, t) : add_down(acc, t);
+      base += k + 1;
+      if (lane == 0) scan_stat(3, 1);
       continue;
     }
     const int cnt = min(128, n - base);
     const int j0 = 4 * lane;
-    long long part[4];
-    int first = 4;  // first link of this lane that leaves the scan (4: none)
-    long long run = 0;
+    long long p0[4], p1[4];  // lane-local inclusive pairs
+    int first = 4;           // first link of this lane that leaves the scan (4: none)
+    long long r0 = 0, r1 = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       bool ok = true;
-      long long d = 0;
-      if (j0 + k < cnt) d = scan_delta(term(base + j0 + k), inv, up, ok);
-      run += d;
-      part[k] = run;
+      long long d0 = 0, d1 = 0;
+      if (j0 + k < cnt) scan_delta2(term(base + j0 + k), inv, up, ok, d0, d1);
+      scan_compose2(r0, r1, d0, d1, r0, r1);
+      p0[k] = r0;
+      p1[k] = r1;
       if (!ok && j0 + k < cnt && first == 4) first = k;
     }
-    long long incl = run;
+    long long i0 = r0, i1 = r1;  // inclusive over lanes
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const long long v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+      const long long u0 = __shfl_up_sync(0xffffffffu, i0, o), u1 = __shfl_up_sync(0xffffffffu, i1, o);
+      if (lane >= o) scan_compose2(u0, u1, i0, i1, i0, i1);
     }
-    const long long excl = incl - run;
+    long long e0 = __shfl_up_sync(0xffffffffu, i0, 1), e1 = __shfl_up_sync(0xffffffffu, i1, 1);
+    if (lane == 0) e0 = e1 = 0;
+    const int pin = (int)(M & 1);
+    const long long P = pin ? e1 : e0;            // increments before this lane
+    const int pl = (int)((M + P) & 1);            // parity entering this lane
+    long long mk[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const long long m = M + excl + part[k];
-      const long long am = m < 0 ? -m : m;
-      if (k < first && j0 + k < cnt && !(((m < 0) == (M < 0)) && am >= kScanLo && am <= kScanHi)) first = k;
+      mk[k] = M + P + (pl ? p1[k] : p0[k]);
+      const long long am = mk[k] < 0 ? -mk[k] : mk[k];
+      if (k < first && j0 + k < cnt && !(((mk[k] < 0) == (M < 0)) && am >= kScanLo && am <= kScanHi)) first = k;
     }
     const unsigned bad = __ballot_sync(0xffffffffu, first < 4);
     int k = cnt;  // links committed by the scan
@@ -172,9 +256,14 @@ __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const T
       const int bl = __ffs(bad) - 1;
       k = 4 * bl + __shfl_sync(0xffffffffu, first, bl);
     }
+    if (lane == 0) {
+      scan_stat(0, 1);
+      scan_stat(1, k);
+      if (bad) scan_stat(2, 1);
+    }
     if (k > 0) {
       const int src = (k - 1) >> 2, slot = (k - 1) & 3;
-      const long long mine = M + excl + (slot == 0 ? part[0] : slot == 1 ? part[1] : slot == 2 ? part[2] : part[3]);
+      const long long mine = slot == 0 ? mk[0] : slot == 1 ? mk[1] : slot == 2 ? mk[2] : mk[3];
       acc = scan_compose(__shfl_sync(0xffffffffu, mine, src), ex);
     }
     base += k;
@@ -183,6 +272,123 @@ __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const T
       if (t == t) acc = up ? add_up(acc, t) : add_down(acc, t);
       ++base;
     }
+  }
+  return acc;
+}
+
+// The same fold by a whole CTA of NT threads, 4 links per thread (4*NT per
+// step): lane-local pairs, a warp scan of the pairs, warp 0 composing the
+// warp totals, and a block-wide minimum of the first link that leaves the
+// scan's domain. All NT threads call it with the same acc; returns it in
+// every thread. sm: at least 2*NT/32 + 4 long longs of shared memory.
+template <int NT, class TermFn>
+__device__ __forceinline__ double block_scan_fold(double acc, int n, bool up, const TermFn& term,
+                                                  long long* sm) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long* s_w0 = sm;                              // [NW] warp totals -> exclusive prefixes
+  long long* s_w1 = sm + NW;
+  int* s_first = reinterpret_cast<int*>(sm + 2 * NW);  // first failing link of the step
+  long long* s_m = sm + 2 * NW + 1;                  // committed partial result
+  double* s_t = reinterpret_cast<double*>(sm + 2 * NW + 2);
+  int base = 0;
+  while (base < n) {
+    int ex;
+    double inv;
+    long long M;
+    if (!scan_frame(acc, ex, inv, M)) {  // skip to the next term, apply it as the scalar op
+      const int cnt = min(NT, n - base);
+      const double tl = tid < cnt ? term(base + tid) : PC_SCAN_NAN;
+      if (tid == 0) *s_first = NT;
+      __syncthreads();
+      if (tl == tl) atomicMin(s_first, tid);
+      __syncthreads();
+      const int k = *s_first;
+      if (k == tid) *s_t = tl;
+      __syncthreads();
+      if (k < NT) {
+        const double t = *s_t;
+        acc = up ? add_up(acc, t) : add_down(acc, t);
+        base += k + 1;
+        if (tid == 0) scan_stat(3, 1);
+      } else {
+        base += cnt;
+      }
+      __syncthreads();
+      continue;
+    }
+    const int cnt = min(4 * NT, n - base);
+    const int j0 = 4 * tid;
+    long long p0[4], p1[4];
+    int first = 4 * NT;
+    long long r0 = 0, r1 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bool ok = true;
+      long long d0 = 0, d1 = 0;
+      if (j0 + k < cnt) scan_delta2(term(base + j0 + k), inv, up, ok, d0, d1);
+      scan_compose2(r0, r1, d0, d1, r0, r1);
+      p0[k] = r0;
+      p1[k] = r1;
+      if (!ok && j0 + k < cnt && first == 4 * NT) first = j0 + k;
+    }
+    long long i0 = r0, i1 = r1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u0 = __shfl_up_sync(0xffffffffu, i0, o), u1 = __shfl_up_sync(0xffffffffu, i1, o);
+      if (lane >= o) scan_compose2(u0, u1, i0, i1, i0, i1);
+    }
+    long long e0 = __shfl_up_sync(0xffffffffu, i0, 1), e1 = __shfl_up_sync(0xffffffffu, i1, 1);
+    if (lane == 0) e0 = e1 = 0;
+    if (tid == 0) *s_first = 4 * NT;
+    if (lane == 31) {
+      s_w0[warp] = i0;
+      s_w1[warp] = i1;
+    }
+    __syncthreads();
+    if (tid == 0) {  // exclusive prefixes of the warp totals (NW compositions)
+      long long a0 = 0, a1 = 0;
+      for (int w = 0; w < NW; ++w) {
+        const long long b0 = s_w0[w], b1 = s_w1[w];
+        s_w0[w] = a0;
+        s_w1[w] = a1;
+        scan_compose2(a0, a1, b0, b1, a0, a1);
+      }
+    }
+    __syncthreads();
+    long long x0, x1;  // increments before this thread: warp prefix, then lane prefix
+    scan_compose2(s_w0[warp], s_w1[warp], e0, e1, x0, x1);
+    const long long P = (M & 1) ? x1 : x0;
+    const int pl = (int)((M + P) & 1);
+    long long mk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mk[k] = M + P + (pl ? p1[k] : p0[k]);
+      const long long am = mk[k] < 0 ? -mk[k] : mk[k];
+      if (j0 + k < first && j0 + k < cnt && !(((mk[k] < 0) == (M < 0)) && am >= kScanLo && am <= kScanHi))
+        first = j0 + k;
+    }
+    if (first < 4 * NT) atomicMin(s_first, first);
+    __syncthreads();
+    const int k = min(*s_first, cnt);  // links committed by the scan
+    if (tid == 0) {
+      scan_stat(0, 1);
+      scan_stat(1, k);
+      if (k < cnt) scan_stat(2, 1);
+    }
+    if (k > 0 && (k - 1) >> 2 == tid) {
+      const int slot = (k - 1) & 3;
+      *s_m = slot == 0 ? mk[0] : slot == 1 ? mk[1] : slot == 2 ? mk[2] : mk[3];
+    }
+    __syncthreads();
+    if (k > 0) acc = scan_compose(*s_m, ex);
+    base += k;
+    if (k < cnt) {  // the link that left the scan's domain, as the scalar op (every thread alike)
+      const double t = term(base);
+      if (t == t) acc = up ? add_up(acc, t) : add_down(acc, t);
+      ++base;
+    }
+    __syncthreads();  // shared scratch reused by the next step
   }
   return acc;
 }

@@ -170,7 +170,7 @@ def test_chain_fold_matches_serial(port, length):
     bit for bit, on both directions."""
     rng = np.random.default_rng(length)
     A, T = chain_cases(rng, 96, length)
-    for upv in (0, 1, 2, 3):  # bit 0: add_up; bit 1: the 32-link scan variant
+    for upv in (0, 1, 2, 3, 4, 5):  # bit 0: add_up; bit 1: the 32-link warp scan; bit 2: the CTA scan
         up = np.full(len(A), upv, dtype=np.int32)
         up[::3] ^= 1
         g = gpu_chain_fold(A, T, up)
