@@ -239,8 +239,9 @@ pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, l
  * c*len+len) in order by add_up (up[c] & 1) or add_down (interval.hpp:59-68),
  * NaN terms skipped — the row-constant / concretisation chains of
  * backsub.hpp:365-389, 740-760, evaluated by the warp-scan fold the chain
- * kernels use (csrc/scanfold.cuh; up[c] & 2: its 32-link variant; up[0] & 4: the
- * CTA-wide fold for every chain). HOST arrays. */
+ * kernels use (csrc/scanfold.cuh; up[c] & 2: its 32-link variant; & 8: its
+ * prefetching variant over a term array; up[0] & 4: the CTA-wide fold for every
+ * chain). HOST arrays. */
 /* Chain-fold diagnostics of the current device: out4 (optional, 6 entries)
  * receives the counters since the last call — scan steps, links committed by
  * scans, scalar links after a failed step, frame-less scalar links, rounding

@@ -21,6 +21,11 @@
 // fold. Results are identical to the reference's chains (same terms, same
 // order, same add_up / add_down), tested against serial folds on adversarial
 // chains (tests/test_gpu_numeric.py) and on whole networks.
+#include <cub/block/block_scan.cuh>
+
+#include <mutex>
+#include <unordered_map>
+
 #include "kernels.cuh"
 #include "numeric.cuh"
 #include "scanfold.cuh"
@@ -604,6 +609,196 @@ void launch_concretize_scan(cudaStream_t s, const RowsDev& rows, const FrameDev&
   ++g_launches;
 }
 
+// ---------------------------------------------------------------------------
+// Split chains: a term kernel spreads a row's cells over many CTAs (each
+// computes and compacts the terms of one 1024-cell tile into a per-stream
+// scratch buffer), then a fold kernel runs one warp per chain over the
+// compacted tiles in order. The fold warps hold few resources, so the conv
+// kernels stay resident beside them; the term kernel is short and wide.
+constexpr int kTT = 256;           // term-kernel threads
+constexpr int kTCP = 4;            // cells per thread
+constexpr int kTTile = kTT * kTCP;  // cells per tile
+
+struct StreamScratch {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+static std::mutex g_scr_mu;
+static std::unordered_map<cudaStream_t, StreamScratch> g_scr;
+// Grow-only scratch per stream (its kernels run in order, so consecutive
+// chains on one stream reuse it).
+static void* stream_scratch(cudaStream_t s, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_scr_mu);
+  StreamScratch& e = g_scr[s];
+  if (bytes > e.cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return nullptr;  // no allocation inside a graph capture: the caller takes the in-CTA fold
+    }
+    if (e.p) {
+      cudaStreamSynchronize(s);
+      cudaFree(e.p);
+    }
+    e.p = nullptr;
+    e.cap = 0;
+    const size_t want = bytes + bytes / 4;
+    if (cudaMalloc(&e.p, want) != cudaSuccess) return nullptr;
+    e.cap = want;
+  }
+  return e.p;
+}
+
+template <class G>
+__device__ __forceinline__ void tile_terms(G& g, const double* lo, const double* hi, long long cells,
+                                           double* tb, long long tstride, int* tcnt) {
+  using Scan = cub::BlockScan<int, kTT>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int tile = blockIdx.x;
+  const long long c0 = (long long)tile * kTTile + (long long)threadIdx.x * kTCP;
+  typename G::Pre pre[kTCP];
+  Iv cv[kTCP];
+#pragma unroll
+  for (int k = 0; k < kTCP; ++k)
+    if (c0 + k < cells) {
+      g.pre(c0 + k, pre[k]);
+      cv[k] = Iv{lo[c0 + k], hi[c0 + k]};
+    }
+  double t[kTCP][G::NA];
+  bool v[kTCP];
+  int nv = 0;
+#pragma unroll
+  for (int k = 0; k < kTCP; ++k) {
+    v[k] = c0 + k < cells && g.gen(cv[k], pre[k], t[k]);
+    nv += v[k];
+  }
+  int pos, tot;
+  Scan(tmp).ExclusiveSum(nv, pos, tot);
+  double* T = tb + (long long)tile * kTTile;
+#pragma unroll
+  for (int k = 0; k < kTCP; ++k)
+    if (v[k]) {
+#pragma unroll
+      for (int a = 0; a < G::NA; ++a) T[a * tstride + pos] = t[k][a];
+      ++pos;
+    }
+  if (threadIdx.x == 0) tcnt[tile] = tot;
+}
+
+__global__ void __launch_bounds__(kTT)
+    k_affine_terms(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, const double* dev,
+                   double* tbuf, int* tcnt, long long tstride, int ntiles, Counters* ctr, const char* frozen) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  ctr += img;
+  AffineGen g{L, is_conv, f, 0, 0, dev + img * rows.sst};
+  if (is_conv) frame_base(f, q, g.bw, g.bh);
+  const size_t pr = phys_row(m, i);
+  tile_terms(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, tbuf + (size_t)i * 3 * tstride, tstride,
+             tcnt + (size_t)i * ntiles);
+  unsigned long long md = g.madds;
+  for (int o = 16; o > 0; o >>= 1) md += __shfl_down_sync(0xffffffffu, md, o);
+  if ((threadIdx.x & 31) == 0 && md) atomicAdd(is_conv ? &ctr->gbc_madds : &ctr->dense_madds, md);
+  if (is_conv && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(&ctr->gbc_dense_equiv, (unsigned long long)L.out_w * L.out_h * L.out_c *
+                                         ((unsigned long long)L.in_w * L.in_h * L.in_c));
+}
+
+__global__ void __launch_bounds__(160)
+    k_affine_fold(RowsDev rows, MatDev m, double* Kout, const double* tbuf, const int* tcnt,
+                  long long tstride, int ntiles, const char* frozen) {
+  __shared__ double s_acc[5];
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  const int warp = threadIdx.x >> 5;  // chain: k.lo, k.hi, kraw.lo, kraw.hi, dev
+  const size_t pr = phys_row(m, i);
+  double acc = warp < 4 ? m.K[4 * pr + warp] : 0.0;
+  const bool up = AffineGen::up(warp);
+  const double* T = tbuf + (size_t)i * 3 * tstride + AffineGen::arr(warp, 0) * tstride;
+  const int* cnt = tcnt + (size_t)i * ntiles;
+  for (int t = 0; t < ntiles; ++t) {
+    acc = scan_fold4_pf(acc, cnt[t], up, T + (long long)t * kTTile);
+  }
+  if ((threadIdx.x & 31) == 0) s_acc[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const double dtot = s_acc[4], a = s_acc[threadIdx.x];
+    double* K = Kout + 4 * (size_t)i;
+    if (threadIdx.x == 0) K[0] = dtot != 0.0 ? add_down(a, -dtot) : a;  // widen_constant :175-179
+    else if (threadIdx.x == 1) K[1] = dtot != 0.0 ? add_up(a, dtot) : a;
+    else K[threadIdx.x] = a;
+  }
+}
+
+__global__ void __launch_bounds__(kTT)
+    k_conc_terms(RowsDev rows, FrameDev f, MatDev m, const double* blo, const double* bhi,
+                 const double* rlo, const double* rhi, double* tbuf, int* tcnt, long long tstride,
+                 int ntiles, const char* frozen) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  const long long so = img * rows.sst;
+  const size_t pr = phys_row(m, i);
+  const double* K = m.K + 4 * pr;
+  const double a0 = upper ? K[1] : K[0], a1 = upper ? K[3] : K[2];
+  const bool neg0 = (__double_as_longlong(a0) == (long long)0x8000000000000000ULL) ||
+                    (__double_as_longlong(a1) == (long long)0x8000000000000000ULL);
+  ConcGen g{f, 0, 0, upper, !neg0, blo + so, bhi + so, rlo + so, rhi + so};
+  frame_base(f, q, g.bw, g.bh);
+  tile_terms(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, tbuf + (size_t)i * 2 * tstride, tstride,
+             tcnt + (size_t)i * ntiles);
+}
+
+__global__ void __launch_bounds__(64)
+    k_conc_fold(RowsDev rows, MatDev m, double* vals, double* rvals, const double* tbuf, const int* tcnt,
+                long long tstride, int ntiles, const char* frozen) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  const int warp = threadIdx.x >> 5;  // 0: padded track, 1: raw track
+  const size_t pr = phys_row(m, i);
+  const double* K = m.K + 4 * pr;
+  double acc = warp == 0 ? (upper ? K[1] : K[0]) : (upper ? K[3] : K[2]);
+  const double* T = tbuf + (size_t)i * 2 * tstride + warp * tstride;
+  const int* cnt = tcnt + (size_t)i * ntiles;
+  for (int t = 0; t < ntiles; ++t) {
+    acc = scan_fold4_pf(acc, cnt[t], upper, T + (long long)t * kTTile);
+  }
+  if ((threadIdx.x & 31) == 0) (warp ? rvals : vals)[i] = acc;
+}
+
+static bool split_chains(cudaStream_t s, long long cells, int nrows, int na, double** tb, int** tc,
+                         long long* tstride, int* ntiles) {
+  static const int on = [] {
+    const char* e = getenv("PC_SPLIT_CHAINS");
+    return e && *e ? atoi(e) : 1;
+  }();
+  if (!on) return false;
+  *ntiles = (int)((cells + kTTile - 1) / kTTile);
+  *tstride = (long long)*ntiles * kTTile;
+  const size_t tb_bytes = (size_t)nrows * na * (size_t)*tstride * sizeof(double);
+  const size_t tc_bytes = (size_t)nrows * *ntiles * sizeof(int);
+  char* p = static_cast<char*>(stream_scratch(s, tb_bytes + tc_bytes + 256));
+  if (!p) return false;
+  *tb = reinterpret_cast<double*>(p);
+  *tc = reinterpret_cast<int*>(p + ((tb_bytes + 255) & ~(size_t)255));
+  return true;
+}
+
 template <class G>
 constexpr size_t chain_smem() {
   return (size_t)(2 * G::NA + 2 * kStages) * Roles<G>::kTile * sizeof(double);  // terms + coefficient ring
@@ -635,6 +830,17 @@ cudaError_t scan_stats_device_chains(int on, unsigned long long* out4) {
 void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                              const FrameDev& fin, MatDev m, double* Kout, const double* dev,
                              Counters* ctr, const char* frozen) {
+  double* tb;
+  int* tc;
+  long long ts;
+  int nt;
+  if (split_chains(s, m.cells, rows.n, 3, &tb, &tc, &ts, &nt)) {
+    k_affine_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(L, is_conv ? 1 : 0, rows, fin, m, dev, tb, tc, ts, nt, ctr,
+                                                   frozen);
+    k_affine_fold<<<rows.n, 160, 0, s>>>(rows, m, Kout, tb, tc, ts, nt, frozen);
+    g_launches += 2;
+    return;
+  }
   k_chain_affine_big<<<rows.n, kCT, chain_smem<AffineGen>(), s>>>(L, is_conv ? 1 : 0, rows, fin, m,
                                                                    Kout, dev, ctr, frozen);
   ++g_launches;
@@ -649,6 +855,16 @@ void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& 
 void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            const double* blo, const double* bhi, const double* rlo,
                            const double* rhi, double* vals, double* rvals, const char* frozen) {
+  double* tb;
+  int* tc;
+  long long ts;
+  int nt;
+  if (split_chains(s, m.cells, rows.n, 2, &tb, &tc, &ts, &nt)) {
+    k_conc_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(rows, f, m, blo, bhi, rlo, rhi, tb, tc, ts, nt, frozen);
+    k_conc_fold<<<rows.n, 64, 0, s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen);
+    g_launches += 2;
+    return;
+  }
   k_concretize_big<<<rows.n, kCT, chain_smem<ConcGen>(), s>>>(rows, f, m, blo, bhi, rlo, rhi, vals,
                                                                rvals, frozen);
   ++g_launches;

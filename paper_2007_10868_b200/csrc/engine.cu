@@ -189,6 +189,7 @@ struct Ctx {
   unsigned short* lv_idx = nullptr;  // (k_live_build; read by the conv kernel k_gbc_live)
   int* lv_pref = nullptr;             // flat live-cell list per ReLU layer (k_live_flat):
   unsigned short *lv_fpos = nullptr, *lv_fch = nullptr;  // prefix per position, position, channel
+  unsigned* lv_chm = nullptr;  // per ReLU layer: channels live at any position (16 words)
   int* un_idx = nullptr;  // per ReLU layer: ascending neurons with a nonzero relaxation offset
   int* un_cnt = nullptr;  // their count per (image, layer) (k_offset_list)
   int* d_label = nullptr;
@@ -283,6 +284,7 @@ struct Ctx {
     lv_cnt = dalloc<int>((size_t)pofs[nl] * nimg);
     lv_idx = dalloc<unsigned short>(T);
     un_idx = dalloc<int>(T);
+    lv_chm = dalloc<unsigned>((size_t)nl * 16 * nimg);
     lv_pref = dalloc<int>(((size_t)pofs[nl] + nl) * nimg);
     lv_fpos = dalloc<unsigned short>(T);
     lv_fch = dalloc<unsigned short>(T);
@@ -768,6 +770,7 @@ struct Walker {
       sp.idx = reinterpret_cast<unsigned short*>(arena_take(slots * sizeof(unsigned short)));
       sp.lo = arena_take(slots * sizeof(double));
       sp.hi = arena_take(slots * sizeof(double));
+      sp.dmask = reinterpret_cast<unsigned*>(arena_take(rows_n * 16 * sizeof(unsigned)));
     }
     // constant chains from the compacted coefficients (CTA per chain)
     static const int chain_scan = env_int("PC_CHAIN_SCAN", 0);
@@ -782,7 +785,10 @@ struct Walker {
                             n->ctr, fz());
         prof_end(n, s2);
       }
-      if (sparse) launch_compact_cells(s, rows(), md(m), sp);
+      if (sparse) {
+        ck(cudaMemsetAsync(sp.dmask, 0, (size_t)nrows() * 16 * sizeof(unsigned), s), "memset");
+        launch_compact_cells(s, rows(), md(m), sp);
+      }
       if (scan) {
         cudaEvent_t e = sync_event(n);
         ck(cudaEventRecord(e, s), "event");
@@ -805,7 +811,11 @@ struct Walker {
       if (sparse && n->net->live_cells && n->L[L.pred0].kind == KIND_RELU && L.in_c >= live_min_cin) {
         const int nl = (int)n->L.size();
         static const int flat = env_int("PC_GBC_FLAT", 1);
-        if (flat && fo.S_h <= 64 && (long long)fo.G_w * fo.G_h < 65536) {
+        static const int tile = env_int("PC_GBC_TILE", 0);
+        if (tile && L.in_c <= 512 && L.out_c <= 512) {
+          launch_gbc_tile(s, L.d, rows(), fi, fo, sp, md(m), md(out), n->lv_chm + (size_t)L.pred0 * 16,
+                          (long long)nl * 16, n->ctr);
+        } else if (flat && fo.S_h <= 64 && (long long)fo.G_w * fo.G_h < 65536) {
           const FlatDev fl{n->lv_pref + n->pofs[L.pred0] + L.pred0, n->lv_fpos + n->off[L.pred0],
                            n->lv_fch + n->off[L.pred0], n->pofs[nl] + nl, n->total};
           launch_gbc_flat(s, L.d, rows(), fi, fo, sp, md(m), md(out), fl, n->ctr);
@@ -1340,6 +1350,7 @@ Ctx* helper_of(Ctx* n) {
   h->lv_cnt = n->lv_cnt;
   h->lv_idx = n->lv_idx;
   h->un_idx = n->un_idx;
+  h->lv_chm = n->lv_chm;
   h->lv_pref = n->lv_pref;
   h->lv_fpos = n->lv_fpos;
   h->lv_fch = n->lv_fch;
@@ -1658,7 +1669,7 @@ void forward_layers(Ctx* n, int k0, int k1, int nimg = 1) {
       const long long o = n->off[k];
       launch_live_build(n->stream, l.out_w * l.out_h, l.out_c, n->relax + 8 * n->off[l.pred0], n->blo + o,
                         n->bhi + o, n->rlo + o, n->rhi + o, n->lv_cnt + n->pofs[k], n->lv_idx + o, nimg,
-                        T, P);
+                        T, P, n->lv_chm + (size_t)k * 16, nl * 16);
       launch_live_flat(n->stream, l.out_w * l.out_h, l.out_c, n->lv_cnt + n->pofs[k], n->lv_idx + o,
                        n->lv_pref + n->pofs[k] + k, n->lv_fpos + o, n->lv_fch + o, nimg, T, P, P + nl);
     }
@@ -1752,8 +1763,10 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
       ck(cudaMemcpyAsync(n->d_label, n->h_int + 2, sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
       ck(cudaGraphLaunch(n->graph, s), "graph launch");
       g_launches += n->graph_launches;
-      n->dense_ev = n->graph_dense_ev;
-      n->conv_ev = n->graph_conv_ev;
+      // events recorded inside the capture are graph nodes: no per-kernel
+      // elapsed times in this schedule (pc_last_kernel_timing reads 0)
+      n->dense_ev.clear();
+      n->conv_ev.clear();
       g_conv_bytes = n->graph_conv_bytes;
       g_conv_launches = n->graph_conv_launches;
       g_dense_bytes = n->graph_dense_bytes;

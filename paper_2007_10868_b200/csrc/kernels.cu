@@ -2353,10 +2353,13 @@ void launch_gbc_smem(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
 
 __global__ void __launch_bounds__(256)
     k_compact_cells(RowsDev rows, MatDev m, SparseDev sp) {
+  __shared__ unsigned s_mask[16];  // nonzero channels of this block's cells (sp.dmask)
   int i;
   if (!rows_resolve(rows, blockIdx.y, i)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = sp.C;
+  if (threadIdx.x < 16) s_mask[threadIdx.x] = 0;
+  __syncthreads();
   const double* lo = m.lo + phys_row(m, i) * m.cells;
   const double* hi = m.hi + phys_row(m, i) * m.cells;
   for (int cell = blockIdx.x * 8 + warp; cell < sp.ncell; cell += gridDim.x * 8) {
@@ -2377,10 +2380,14 @@ __global__ void __launch_bounds__(256)
         sp.lo[slot + k] = a;
         sp.hi[slot + k] = b;
       }
+      if (sp.dmask && lane == 0 && mask && c0 < 512) atomicOr(&s_mask[c0 >> 5], mask);
       base += __popc(mask);
     }
     if (lane == 0) sp.cnt[(size_t)i * sp.ncell + cell] = base;
   }
+  __syncthreads();
+  if (sp.dmask && threadIdx.x < 16 && s_mask[threadIdx.x])
+    atomicOr(&sp.dmask[(size_t)i * 16 + threadIdx.x], s_mask[threadIdx.x]);
 }
 
 void launch_compact_cells(cudaStream_t s, const RowsDev& rows, MatDev m, SparseDev sp) {
@@ -2578,8 +2585,9 @@ __global__ void __launch_bounds__(256, MINB)
 __global__ void __launch_bounds__(256)
     k_live_build(int npos, int C, const double* relax, const double* blo, const double* bhi,
                  const double* rlo, const double* rhi, int* cnt, unsigned short* idx,
-                 long long sst, long long pst) {
+                 long long sst, long long pst, unsigned* chmask, int mstride) {
   const int img = blockIdx.z;
+  if (chmask) chmask += (long long)img * mstride;
   relax += 8 * img * sst;
   blo += img * sst; bhi += img * sst; rlo += img * sst; rhi += img * sst;
   idx += img * sst;
@@ -2600,6 +2608,7 @@ __global__ void __launch_bounds__(256)
       }
       const unsigned m = __ballot_sync(0xffffffffu, live);
       if (live) idx[(long long)pos * C + base + __popc(m & ((1u << lane) - 1u))] = (unsigned short)c;
+      if (chmask && lane == 0 && m && c0 < 512) atomicOr(&chmask[c0 >> 5], m);  // live at any position
       base += __popc(m);
     }
     if (lane == 0) cnt[pos] = base;
@@ -2608,10 +2617,14 @@ __global__ void __launch_bounds__(256)
 
 void launch_live_build(cudaStream_t s, int npos, int C, const double* relax, const double* blo,
                        const double* bhi, const double* rlo, const double* rhi, int* cnt,
-                       unsigned short* idx, int nimg, long long sst, long long pst) {
+                       unsigned short* idx, int nimg, long long sst, long long pst, unsigned* chmask,
+                       int mstride) {
   unsigned gx = cdiv(npos, 8);
   if (gx > 1024) gx = 1024;
-  k_live_build<<<dim3(gx, 1, nimg), 256, 0, s>>>(npos, C, relax, blo, bhi, rlo, rhi, cnt, idx, sst, pst);
+  if (chmask)
+    for (int b = 0; b < nimg; ++b) cudaMemsetAsync(chmask + (size_t)b * mstride, 0, 16 * sizeof(unsigned), s);
+  k_live_build<<<dim3(gx, 1, nimg), 256, 0, s>>>(npos, C, relax, blo, bhi, rlo, rhi, cnt, idx, sst, pst, chmask,
+                                                 mstride);
   ++g_launches;
 }
 
@@ -2914,6 +2927,159 @@ __global__ void __launch_bounds__(256, MINB)
   }
 }
 
+// k_gbc_flat with two consecutive live cells per thread: they are (almost
+// always) two channels of one grid position, so they share every compacted
+// coefficient load and give the thread two independent interval chains.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_gbc_flat2(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
+                MatDev out, FlatDev fl, Counters* ctr) {
+  __shared__ int s_seg[65];
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  int bw, bh, nbw, nbh;
+  frame_base(fi, q, bw, bh);
+  frame_base(fo, q, nbw, nbh);
+  const int* pref = fl.pref + (long long)img * fl.fst;
+  const unsigned short* fpos = fl.fpos + (long long)img * fl.sst;
+  const unsigned short* fch = fl.fch + (long long)img * fl.sst;
+  if (threadIdx.x <= fo.S_h) {
+    int c = 0;
+    for (int y = 0; y < (int)threadIdx.x; ++y) {
+      const int g0 = (nbh + y) * fo.G_w + nbw;
+      c += pref[g0 + fo.S_w] - pref[g0];
+    }
+    s_seg[threadIdx.x] = c;
+  }
+  __syncthreads();
+  const int total = s_seg[fo.S_h];
+  const int t0b = blockIdx.x * kFlatOPB;
+  if (t0b >= total) return;
+  const int t1b = min(total, t0b + kFlatOPB);
+  const long long ocells = out.cells;
+  const double* ilo = in.lo + phys_row(in, i) * in.cells;
+  const double* ihi = in.hi + phys_row(in, i) * in.cells;
+  double* olo = out.lo + (size_t)i * ocells;
+  double* ohi = out.hi + (size_t)i * ocells;
+  const int cin = L.in_c, cout = L.out_c;
+  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  const int* cnt = sp.cnt + (size_t)i * sp.ncell;
+  const size_t rbase = (size_t)i * sp.ncell * sp.C;
+  MagAcc mag;
+  unsigned long long exec = 0;
+  auto locate = [&](int t, int& y, int& ix, int& ci) {
+    while (t >= s_seg[y + 1]) ++y;
+    const int e = pref[(nbh + y) * fo.G_w + nbw] + (t - s_seg[y]);
+    const int gp = fpos[e];
+    ci = fch[e];
+    ix = gp - (nbh + y) * fo.G_w;
+  };
+  auto put = [&](int y, int ix, int ci, Iv acc) {
+    const size_t o = ((size_t)y * fo.S_w + (ix - nbw)) * cin + ci;
+    olo[o] = acc.lo;
+    ohi[o] = acc.hi;
+    mag.add(acc.lo);
+    mag.add(acc.hi);
+  };
+  int ya = 0;
+  for (int t = t0b + 2 * threadIdx.x; t < t1b; t += 2 * blockDim.x) {
+    int ixa, ca, yb, ixb = -1, cb = -1;
+    locate(t, ya, ixa, ca);
+    const bool has_b = t + 1 < t1b;
+    yb = ya;
+    if (has_b) locate(t + 1, yb, ixb, cb);
+    const bool pair = has_b && yb == ya && ixb == ixa;
+    const int iy = nbh + ya;
+    if (!band || !pair) {  // checked path, or two positions: one output at a time
+      for (int u = 0; u < (has_b ? 2 : 1); ++u) {
+        const int yy = u ? yb : ya, xx = u ? ixb : ixa, cc = u ? cb : ca;
+        Iv acc;
+        if (!band) {
+          acc = gbc_gather_checked(L, fi, bw, bh, ilo, ihi, nbh + yy, xx, cc);
+        } else {
+          const int py = nbh + yy;
+          int ah0 = floordiv(py + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(py + L.ph, L.sh);
+          int aw0 = floordiv(xx + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(xx + L.pw, L.sw);
+          ah0 = max(ah0, bh);
+          ah1 = min(ah1, bh + fi.S_h - 1);
+          aw0 = max(aw0, bw);
+          aw1 = min(aw1, bw + fi.S_w - 1);
+          double lo = 0.0, hi = 0.0;
+          for (int ah = ah0; ah <= ah1; ++ah) {
+            const int fy = py + L.ph - ah * L.sh;
+            for (int aw = aw0; aw <= aw1; ++aw) {
+              const int fx = xx + L.pw - aw * L.sw;
+              const int cell = (ah - bh) * fi.S_w + (aw - bw);
+              const int n = cnt[cell];
+              exec += n;
+              const size_t sb = rbase + (size_t)cell * sp.C;
+              const double* wp = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + cc;
+              for (int k = 0; k < n; ++k)
+                madd_band(wp[(size_t)sp.idx[sb + k] * cin], sp.lo[sb + k], sp.hi[sb + k], lo, hi);
+            }
+          }
+          acc = Iv{canon0(lo), hi};
+        }
+        put(yy, xx, cc, acc);
+      }
+      continue;
+    }
+    int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
+    int aw0 = floordiv(ixa + L.pw - L.fw, L.sw) + 1, aw1 = floordiv(ixa + L.pw, L.sw);
+    ah0 = max(ah0, bh);
+    ah1 = min(ah1, bh + fi.S_h - 1);
+    aw0 = max(aw0, bw);
+    aw1 = min(aw1, bw + fi.S_w - 1);
+    double lo0 = 0.0, hi0 = 0.0, lo1 = 0.0, hi1 = 0.0;
+    for (int ah = ah0; ah <= ah1; ++ah) {
+      const int fy = iy + L.ph - ah * L.sh;
+      for (int aw = aw0; aw <= aw1; ++aw) {
+        const int fx = ixa + L.pw - aw * L.sw;
+        const int cell = (ah - bh) * fi.S_w + (aw - bw);
+        const int n = cnt[cell];
+        exec += 2 * n;
+        const size_t sb = rbase + (size_t)cell * sp.C;
+        const double* wa = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ca;
+        const double* wb = wa + (cb - ca);
+        constexpr int kB = 4;
+        int k = 0;
+        for (; k + kB <= n; k += kB) {
+          double cl[kB], ch[kB], w0[kB], w1[kB];
+#pragma unroll
+          for (int u = 0; u < kB; ++u) {
+            const size_t d = sp.idx[sb + k + u];
+            cl[u] = sp.lo[sb + k + u];
+            ch[u] = sp.hi[sb + k + u];
+            w0[u] = wa[d * cin];
+            w1[u] = wb[d * cin];
+          }
+#pragma unroll
+          for (int u = 0; u < kB; ++u) {
+            madd_band(w0[u], cl[u], ch[u], lo0, hi0);
+            madd_band(w1[u], cl[u], ch[u], lo1, hi1);
+          }
+        }
+        for (; k < n; ++k) {
+          const size_t d = sp.idx[sb + k];
+          const double cl = sp.lo[sb + k], ch = sp.hi[sb + k];
+          madd_band(wa[d * cin], cl, ch, lo0, hi0);
+          madd_band(wb[d * cin], cl, ch, lo1, hi1);
+        }
+      }
+    }
+    put(ya, ixa, ca, Iv{canon0(lo0), hi0});
+    put(yb, ixb, cb, Iv{canon0(lo1), hi1});
+  }
+  mag.flush(out.stat);
+  if (ctr) {
+    for (int o = 16; o > 0; o >>= 1) exec += __shfl_down_sync(__activemask(), exec, o);
+    if ((threadIdx.x & 31) == 0 && exec) atomicAdd(&ctr[img].conv_exec, exec);
+  }
+}
+
 void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr) {
   static const int minb = env_int("PC_GBC_FLAT_MINB", 3);
@@ -2922,9 +3088,216 @@ void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
   cudaMemsetAsync(out.hi, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
   const long long cells = (long long)fout.S_w * fout.S_h * L.in_c;
   dim3 grid(cdiv(cells, kFlatOPB), rows.n);
-  if (minb >= 4) k_gbc_flat<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  static const int pairs = env_int("PC_GBC_FLAT_PAIRS", 1);
+  static const int minb2 = env_int("PC_GBC_FLAT2_MINB", 2);
+  if (pairs) {
+    if (minb2 >= 3) k_gbc_flat2<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    else k_gbc_flat2<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  } else if (minb >= 4) k_gbc_flat<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
   else if (minb == 3) k_gbc_flat<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
   else k_gbc_flat<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  ++g_launches;
+}
+
+// ---------------------------------------------------------------------------
+// Dense-tile conv over compacted channel sets. On the residual nets the zero
+// pattern of a conv step is (nearly) channel-uniform: a ReLU layer's dead
+// neurons are whole channels at almost every position (scripts/live_stats.py),
+// so the input coefficients are nonzero on a channel set D (the row's union,
+// sp.dmask) and the live outputs on a channel set CI (the layer's union,
+// k_live_build's chmask). The step is then a dense product over D x CI per
+// filter tap, done as a shared-memory tiled loop: a CTA owns 32 output
+// positions (one stride-parity class) x 64 channels of CI; per (tap, 16-wide
+// chunk of D) it stages the 32 positions' covering coefficients and the
+// 16 x 64 weights by cp.async (double buffered) and every thread runs 8
+// interval chains (1 position x 8 channels: the coefficient is reused 8 times,
+// the weights are warp broadcasts). Taps run in descending (fy, fx) and D
+// ascending, i.e. covering cells ascending then d ascending: the reference's
+// (ch, cw, d) order for every output (backsub.hpp:449-489). Terms outside
+// the sets are exact zeros (zero coefficient, or a cell no result reads) and a
+// zero term leaves the accumulators unchanged, so results are the flat
+// kernel's bit for bit.
+constexpr int kTP = 32, kTCH = 64, kTD = 16;
+struct TileSmem {
+  double c[2][kTD][kTP][2];   // coefficients (lo, hi) per d-slot, position
+  double w[2][kTD][kTCH];     // weights per d-slot, channel
+  unsigned short dl[512], cl[512];
+  int nd, nc;
+};
+
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+__global__ void __launch_bounds__(256, 2)
+    k_gbc_tile(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in, MatDev out,
+               const unsigned* chmask, long long mstride, Counters* ctr) {
+  extern __shared__ __align__(16) unsigned char tsm_raw[];
+  TileSmem& S = *reinterpret_cast<TileSmem*>(tsm_raw);
+  int i;
+  if (!rows_resolve(rows, blockIdx.z, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  int bw, bh, nbw, nbh;
+  frame_base(fi, q, bw, bh);
+  frame_base(fo, q, nbw, nbh);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cin = L.in_c, cout = L.out_c;
+  // channel lists: D from the row's nonzero-channel mask, CI from the layer's
+  if (tid == 0) {
+    const unsigned* dm = sp.dmask + (size_t)i * 16;
+    const unsigned* cm = chmask + (long long)img * mstride;
+    int nd = 0, nc = 0;
+    for (int w = 0; w < 16 && 32 * w < cout; ++w)
+      for (unsigned b = dm[w]; b; b &= b - 1) S.dl[nd++] = (unsigned short)(32 * w + __ffs(b) - 1);
+    for (int w = 0; w < 16 && 32 * w < cin; ++w)
+      for (unsigned b = cm[w]; b; b &= b - 1) S.cl[nc++] = (unsigned short)(32 * w + __ffs(b) - 1);
+    S.nd = nd;
+    S.nc = nc;
+  }
+  __syncthreads();
+  const int nd = S.nd, nc = S.nc;
+  const int ch0 = blockIdx.y * kTCH;
+  if (ch0 >= nc) return;
+  // stride-parity class and tile of positions
+  const int sh = L.sh, sw = L.sw;
+  int cls = 0, tile = blockIdx.x, ncy = 0, ncx = 0, y0 = 0, x0 = 0;
+  for (;; ++cls) {
+    if (cls >= sh * sw) return;
+    const int cy = cls / sw, cx = cls - cy * sw;
+    y0 = ((cy - nbh) % sh + sh) % sh;  // first window row with (nbh + y) % sh == cy
+    x0 = ((cx - nbw) % sw + sw) % sw;
+    ncy = y0 < fo.S_h ? (fo.S_h - y0 + sh - 1) / sh : 0;
+    ncx = x0 < fo.S_w ? (fo.S_w - x0 + sw - 1) / sw : 0;
+    const int nt = (ncy * ncx + kTP - 1) / kTP;
+    if (tile < nt) break;
+    tile -= nt;
+  }
+  const int cy = cls / sw, cx = cls - cy * sw;
+  const int npos = ncy * ncx;
+  // this thread's output: position lane of the tile, channels ch0 + 8*warp .. +8
+  const int li = tile * kTP + lane;
+  const bool pvalid = li < npos;
+  const int y = y0 + sh * (pvalid ? li / ncx : 0), x = x0 + sw * (pvalid ? li % ncx : 0);
+  const int iy = nbh + y, ix = nbw + x;
+  const int cg = ch0 + 8 * warp;  // first channel slot of this warp
+  const bool wvalid = cg < nc;
+  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  const double* ilo = in.lo + phys_row(in, i) * in.cells;
+  const double* ihi = in.hi + phys_row(in, i) * in.cells;
+  double* olo = out.lo + (size_t)i * out.cells;
+  double* ohi = out.hi + (size_t)i * out.cells;
+  if (!band) {  // operands not proven in band: the checked gather per output
+    if (pvalid && wvalid)
+      for (int k = 0; k < 8 && cg + k < nc; ++k) {
+        const int ci = S.cl[cg + k];
+        const Iv a = gbc_gather_checked(L, fi, bw, bh, ilo, ihi, iy, ix, ci);
+        const size_t o = ((size_t)y * fo.S_w + x) * cin + ci;
+        olo[o] = a.lo;
+        ohi[o] = a.hi;
+      }
+    return;
+  }
+  // taps of this parity class, descending: fy = fy_hi, fy_hi - sh, ... (same for x)
+  const int fyp = ((cy + L.ph) % sh + sh) % sh, fxp = ((cx + L.pw) % sw + sw) % sw;
+  const int nfy = fyp < L.fh ? (L.fh - fyp + sh - 1) / sh : 0;
+  const int nfx = fxp < L.fw ? (L.fw - fxp + sw - 1) / sw : 0;
+  const int ntap = nfy * nfx, nch = (nd + kTD - 1) / kTD, nit = ntap * nch;
+  auto stage = [&](int it, int buf) {
+    const int tp = it / nch, dc = (it - tp * nch) * kTD;
+    const int fy = fyp + sh * (nfy - 1 - tp / nfx), fx = fxp + sw * (nfx - 1 - tp % nfx);
+    // coefficients: 16 d-slots x 32 positions x (lo, hi) = 1024 8-byte copies, 4 per thread
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + 256 * r;              // (d-slot, position, half)
+      const int half = e & 1, p = (e >> 1) & 31, ds = e >> 6;
+      const int lp = tile * kTP + p;
+      bool ok = lp < npos && dc + ds < nd;
+      const double* src = ilo;
+      if (ok) {
+        const int py = nbh + y0 + sh * (lp / ncx), px = nbw + x0 + sw * (lp % ncx);
+        const int ah = (py + L.ph - fy) / sh, aw = (px + L.pw - fx) / sw;  // exact: parity class
+        ok = ah >= bh && ah < bh + fi.S_h && aw >= bw && aw < bw + fi.S_w;
+        if (ok) src = (half ? ihi : ilo) + ((size_t)(ah - bh) * fi.S_w + (aw - bw)) * cout + S.dl[dc + ds];
+      }
+      cp_async8(&S.c[buf][ds][p][half], src, ok);
+    }
+    // weights: 16 d-slots x 64 channels, 4 per thread
+    const double* wt = L.FT + (size_t)(fy * L.fw + fx) * cout * cin;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + 256 * r;
+      const int c = e & 63, ds = e >> 6;
+      const bool ok = dc + ds < nd && ch0 + c < nc;
+      const double* src = ok ? wt + (size_t)S.dl[dc + ds] * cin + S.cl[ch0 + c] : wt;
+      cp_async8(&S.w[buf][ds][c], src, ok);
+    }
+    cp_async_commit();
+  };
+  double lo[8], hi[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) lo[k] = hi[k] = 0.0;
+  if (nit > 0) stage(0, 0);
+  for (int it = 0; it < nit; ++it) {
+    const int buf = it & 1;
+    if (it + 1 < nit) {
+      stage(it + 1, buf ^ 1);
+      cp_async_wait1();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    if (wvalid) {
+#pragma unroll 4
+      for (int ds = 0; ds < kTD; ++ds) {
+        const double2 cv = *reinterpret_cast<const double2*>(&S.c[buf][ds][lane][0]);
+        const double4* wp = reinterpret_cast<const double4*>(&S.w[buf][ds][8 * warp]);
+        const double4 w0 = wp[0], w1 = wp[1];
+        madd_band(w0.x, cv.x, cv.y, lo[0], hi[0]);
+        madd_band(w0.y, cv.x, cv.y, lo[1], hi[1]);
+        madd_band(w0.z, cv.x, cv.y, lo[2], hi[2]);
+        madd_band(w0.w, cv.x, cv.y, lo[3], hi[3]);
+        madd_band(w1.x, cv.x, cv.y, lo[4], hi[4]);
+        madd_band(w1.y, cv.x, cv.y, lo[5], hi[5]);
+        madd_band(w1.z, cv.x, cv.y, lo[6], hi[6]);
+        madd_band(w1.w, cv.x, cv.y, lo[7], hi[7]);
+      }
+    }
+    __syncthreads();  // buffer `buf` is restaged two iterations on
+  }
+  MagAcc mag;
+  if (pvalid && wvalid) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (cg + k >= nc) break;
+      const int ci = S.cl[cg + k];
+      const size_t o = ((size_t)y * fo.S_w + x) * cin + ci;
+      const double a = canon0(lo[k]);
+      olo[o] = a;
+      ohi[o] = hi[k];
+      mag.add(a);
+      mag.add(hi[k]);
+    }
+  }
+  mag.flush(out.stat);
+  if (ctr && tid == 0)  // interval madds issued (zero terms included): positions x channels x taps x |D|
+    atomicAdd(&ctr[img].conv_exec,
+              (unsigned long long)min(kTP, npos - tile * kTP) * min(kTCH, nc - ch0) * ntap * nd);
+}
+
+void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, const unsigned* chmask,
+                     long long mstride, Counters* ctr) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gbc_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TileSmem));
+    attr = true;
+  }
+  cudaMemsetAsync(out.lo, 0, sizeof(double) * (size_t)rows.n * out.cells, s);  // channels outside CI
+  cudaMemsetAsync(out.hi, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
+  const int npos = fout.S_w * fout.S_h;
+  const unsigned gx = cdiv(npos, kTP) + L.sh * L.sw;  // parity classes round up separately
+  dim3 grid(gx, cdiv(L.in_c, kTCH), rows.n);
+  k_gbc_tile<<<grid, 256, sizeof(TileSmem), s>>>(L, rows, fin, fout, sp, in, out, chmask, mstride, ctr);
   ++g_launches;
 }
 
@@ -3581,8 +3954,9 @@ __global__ void k_chain_fold(int n_chains, int len, const double* acc0, const do
   if (c >= n_chains) return;
   const double* t = terms + (size_t)c * len;
   const bool dir = up[c] & 1;  // bit 1 set: the 32-link fold (scan_fold) instead of scan_fold4
-  const double r = (up[c] & 2) ? scan_fold(acc0[c], len, dir, [&](int j) { return t[j]; })
-                               : scan_fold4(acc0[c], len, dir, [&](int j) { return t[j]; });
+  const double r = (up[c] & 2)   ? scan_fold(acc0[c], len, dir, [&](int j) { return t[j]; })
+                   : (up[c] & 8) ? scan_fold4_pf(acc0[c], len, dir, t)
+                                 : scan_fold4(acc0[c], len, dir, [&](int j) { return t[j]; });
   if ((threadIdx.x & 31) == 0) out[c] = r;
 }
 

@@ -352,6 +352,7 @@ struct SparseDev {
   double* lo;
   double* hi;
   int ncell, C;
+  unsigned* dmask = nullptr;  // optional: per row, the channels nonzero in any cell (16 words)
 };
 void launch_compact_cells(cudaStream_t s, const RowsDev& rows, MatDev m, SparseDev sp);
 // Live channels per grid position of a ReLU layer (k_live_build, kernels.cu):
@@ -364,7 +365,8 @@ struct LiveDev {
 };
 void launch_live_build(cudaStream_t s, int npos, int C, const double* relax, const double* blo,
                        const double* bhi, const double* rlo, const double* rhi, int* cnt,
-                       unsigned short* idx, int nimg, long long sst, long long pst);
+                       unsigned short* idx, int nimg, long long sst, long long pst,
+                       unsigned* chmask = nullptr, int mstride = 0);  // chmask: live-anywhere channels
 // Ascending list of the neurons of a ReLU layer with a nonzero relaxation
 // offset (k_offset_list) and the relu_step constant chains over it.
 void launch_offset_list(cudaStream_t s, int n, const double* relax, int* list, int* count,
@@ -394,6 +396,11 @@ void launch_chain_affine_scan(cudaStream_t s, const LayerDev& L, const RowsDev& 
 void launch_concretize_scan(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                             const double* blo, const double* bhi, const double* rlo, const double* rhi,
                             double* vals, double* rvals, const char* frozen);
+// Dense-tile conv over the row's nonzero input channels x the layer's
+// live-anywhere output channels (needs sp.dmask; chmask per image, 16 words).
+void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, const unsigned* chmask,
+                     long long mstride, Counters* ctr);
 // Conv coefficients of the live cells of a ReLU frame (dead ones written +0).
 void launch_gbc_live(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, LiveDev lv, Counters* ctr);

@@ -276,6 +276,106 @@ __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const T
   return acc;
 }
 
+// scan_fold4 over a contiguous term array in global memory, with the next
+// group's terms loaded while the current group is scanned (the loads of a
+// group depend only on where it starts, which a failed link rarely moves).
+__device__ __forceinline__ double scan_fold4_pf(double acc, int n, bool up, const double* T) {
+  const int lane = threadIdx.x & 31;
+  auto load = [&](int b, double* v) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = b + 4 * lane + k;
+      v[k] = j < n ? __ldg(T + j) : PC_SCAN_NAN;
+    }
+  };
+  double cur[4], nxt[4];
+  int base = 0;
+  load(0, cur);
+  while (base < n) {
+    int ex;
+    double inv;
+    long long M;
+    if (!scan_frame(acc, ex, inv, M)) {  // next term (NaN = none) as the scalar op
+      const int lane_first = (cur[0] == cur[0]) ? 0 : (cur[1] == cur[1]) ? 1 : (cur[2] == cur[2]) ? 2 : (cur[3] == cur[3]) ? 3 : 4;
+      const unsigned has = __ballot_sync(0xffffffffu, lane_first < 4);
+      if (!has) {
+        base += 128;
+        load(base, cur);
+        continue;
+      }
+      const int bl = __ffs(has) - 1;
+      const int k = 4 * bl + __shfl_sync(0xffffffffu, lane_first, bl);
+      const double t = __shfl_sync(0xffffffffu, (k & 3) == 0 ? cur[0] : (k & 3) == 1 ? cur[1] : (k & 3) == 2 ? cur[2] : cur[3], bl);
+      acc = up ? add_up(acc, t) : add_down(acc, t);
+      base += k + 1;
+      if (lane == 0) scan_stat(3, 1);
+      load(base, cur);
+      continue;
+    }
+    load(base + 128, nxt);
+    const int cnt = min(128, n - base);
+    const int j0 = 4 * lane;
+    long long p0[4], p1[4];
+    int first = 4;
+    long long r0 = 0, r1 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bool ok = true;
+      long long d0 = 0, d1 = 0;
+      if (j0 + k < cnt) scan_delta2(cur[k], inv, up, ok, d0, d1);
+      scan_compose2(r0, r1, d0, d1, r0, r1);
+      p0[k] = r0;
+      p1[k] = r1;
+      if (!ok && j0 + k < cnt && first == 4) first = k;
+    }
+    long long i0 = r0, i1 = r1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u0 = __shfl_up_sync(0xffffffffu, i0, o), u1 = __shfl_up_sync(0xffffffffu, i1, o);
+      if (lane >= o) scan_compose2(u0, u1, i0, i1, i0, i1);
+    }
+    long long e0 = __shfl_up_sync(0xffffffffu, i0, 1), e1 = __shfl_up_sync(0xffffffffu, i1, 1);
+    if (lane == 0) e0 = e1 = 0;
+    const long long P = (M & 1) ? e1 : e0;
+    const int pl = (int)((M + P) & 1);
+    long long mk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mk[k] = M + P + (pl ? p1[k] : p0[k]);
+      const long long am = mk[k] < 0 ? -mk[k] : mk[k];
+      if (k < first && j0 + k < cnt && !(((mk[k] < 0) == (M < 0)) && am >= kScanLo && am <= kScanHi)) first = k;
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, first < 4);
+    int k = cnt;
+    if (bad) {
+      const int bl = __ffs(bad) - 1;
+      k = 4 * bl + __shfl_sync(0xffffffffu, first, bl);
+    }
+    if (lane == 0) {
+      scan_stat(0, 1);
+      scan_stat(1, k);
+      if (bad) scan_stat(2, 1);
+    }
+    if (k > 0) {
+      const int src = (k - 1) >> 2, slot = (k - 1) & 3;
+      const long long mine = slot == 0 ? mk[0] : slot == 1 ? mk[1] : slot == 2 ? mk[2] : mk[3];
+      acc = scan_compose(__shfl_sync(0xffffffffu, mine, src), ex);
+    }
+    if (!bad) {
+      base += cnt;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+    } else {
+      base += k;
+      const double t = __ldg(T + base);  // the link that left the scan's domain, as the scalar op
+      if (t == t) acc = up ? add_up(acc, t) : add_down(acc, t);
+      ++base;
+      load(base, cur);
+    }
+  }
+  return acc;
+}
+
 // The same fold by a whole CTA of NT threads, 4 links per thread (4*NT per
 // step): lane-local pairs, a warp scan of the pairs, warp 0 composing the
 // warp totals, and a block-wide minimum of the first link that leaves the

@@ -170,10 +170,10 @@ def test_chain_fold_matches_serial(port, length):
     bit for bit, on both directions."""
     rng = np.random.default_rng(length)
     A, T = chain_cases(rng, 96, length)
-    for upv in (0, 1, 2, 3, 4, 5):  # bit 0: add_up; bit 1: the 32-link warp scan; bit 2: the CTA scan
+    for upv in (0, 1, 2, 3, 4, 5, 8, 9):  # bit 0: add_up; 1: 32-link warp scan; 2: CTA scan; 3: prefetching warp scan
         up = np.full(len(A), upv, dtype=np.int32)
         up[::3] ^= 1
         g = gpu_chain_fold(A, T, up)
-        r = port.chain_fold(A, T, up & 1)
+        r = port.chain_fold(A, T, up & 1)  # noqa: the device variant is chosen by the other bits
         bad = ~((g.view(np.int64) == r.view(np.int64)) | (np.isnan(g) & np.isnan(r)))
         assert not bad.any(), (np.nonzero(bad)[0][:8] % 12, g[bad][:4], r[bad][:4])
