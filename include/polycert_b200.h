@@ -241,12 +241,13 @@ pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, l
  * backsub.hpp:365-389, 740-760, evaluated by the warp-scan fold the chain
  * kernels use (csrc/scanfold.cuh; up[c] & 2: its 32-link variant; & 8: its
  * prefetching variant over a term array; up[0] & 4: the CTA-wide fold for every
- * chain). HOST arrays. */
-/* Chain-fold diagnostics of the current device: out4 (optional, 6 entries)
+ * chain, & 16 with it: the CTA-wide fold with local retry). HOST arrays. */
+/* Chain-fold diagnostics of the current device: out4 (optional, 8 entries)
  * receives the counters since the last call — scan steps, links committed by
  * scans, scalar links after a failed step, frame-less scalar links, rounding
- * ties met, out-of-range terms met — which are then reset; on != 0 enables
- * counting (off by default). */
+ * ties met, out-of-range terms met, failed links that grew past / shrank or
+ * flipped out of the accumulator's binade (prefetching fold) — which are then
+ * reset; on != 0 enables counting (off by default). */
 pc_status pc_scan_stats(int on, unsigned long long* out4);
 
 pc_status pc_chain_fold(int n_chains, int len, const double* acc0, const double* terms, const int* up,

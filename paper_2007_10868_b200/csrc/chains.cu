@@ -708,6 +708,40 @@ __global__ void __launch_bounds__(kTT)
                                          ((unsigned long long)L.in_w * L.in_h * L.in_c));
 }
 
+// Fold one chain over the row's compacted tiles with the warp scan, each tile
+// staged into the warp's shared-memory buffer by cp.async one tile ahead
+// (16-byte copies; the scratch tiles are 16-byte aligned, kTTile doubles
+// apart), so every scan step reads shared memory.
+__device__ __forceinline__ double fold_tiles(double acc, bool up, const double* T, const int* cnt,
+                                             int ntiles, double* buf /* [2][kTTile] */) {
+  const int lane = threadIdx.x & 31;
+  auto stage = [&](int t, int b) {
+    const int n = cnt[t];
+    const double* src = T + (long long)t * kTTile;
+    double* dst = buf + b * kTTile;
+    for (int e = 2 * lane; e < n; e += 64) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + e);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + e));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  if (ntiles > 0) stage(0, 0);
+  for (int t = 0; t < ntiles; ++t) {
+    const int b = t & 1;
+    if (t + 1 < ntiles) {
+      stage(t + 1, b ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncwarp();
+    const double* B = buf + b * kTTile;
+    acc = scan_fold4(acc, cnt[t], up, [&](int j) { return B[j]; });
+    __syncwarp();  // buffer b is restaged by the next iteration's stage(t + 2)
+  }
+  return acc;
+}
+
 __global__ void __launch_bounds__(160)
     k_affine_fold(RowsDev rows, MatDev m, double* Kout, const double* tbuf, const int* tcnt,
                   long long tstride, int ntiles, const char* frozen) {
@@ -724,9 +758,8 @@ __global__ void __launch_bounds__(160)
   const bool up = AffineGen::up(warp);
   const double* T = tbuf + (size_t)i * 3 * tstride + AffineGen::arr(warp, 0) * tstride;
   const int* cnt = tcnt + (size_t)i * ntiles;
-  for (int t = 0; t < ntiles; ++t) {
-    acc = scan_fold4_pf(acc, cnt[t], up, T + (long long)t * kTTile);
-  }
+  extern __shared__ __align__(16) double fbuf[];
+  acc = fold_tiles(acc, up, T, cnt, ntiles, fbuf + (size_t)warp * 2 * kTTile);
   if ((threadIdx.x & 31) == 0) s_acc[warp] = acc;
   __syncthreads();
   if (threadIdx.x < 4) {
@@ -775,10 +808,91 @@ __global__ void __launch_bounds__(64)
   double acc = warp == 0 ? (upper ? K[1] : K[0]) : (upper ? K[3] : K[2]);
   const double* T = tbuf + (size_t)i * 2 * tstride + warp * tstride;
   const int* cnt = tcnt + (size_t)i * ntiles;
-  for (int t = 0; t < ntiles; ++t) {
-    acc = scan_fold4_pf(acc, cnt[t], upper, T + (long long)t * kTTile);
-  }
+  extern __shared__ __align__(16) double fbuf[];
+  acc = fold_tiles(acc, upper, T, cnt, ntiles, fbuf + (size_t)warp * 2 * kTTile);
   if ((threadIdx.x & 31) == 0) (warp ? rvals : vals)[i] = acc;
+}
+
+// Few-row passes: one CTA per chain with the block fold (local retry), terms
+// read from the compacted tiles through a tile prefix in shared memory.
+constexpr int kFB = 512;
+constexpr int kMaxFoldTiles = 128;
+
+template <class F>
+__device__ __forceinline__ double fold_tiles_block(double acc, bool up, const double* T, const int* cnt,
+                                                   int ntiles, F&& /*unused*/) {
+  __shared__ int s_pref[kMaxFoldTiles + 1];
+  __shared__ long long sm[2 * kFB / 32 + 8];
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      s_pref[t] = c;
+      c += cnt[t];
+    }
+    s_pref[ntiles] = c;
+  }
+  __syncthreads();
+  const int n = s_pref[ntiles];
+  auto term = [&](int j) -> double {
+    int a = 0, b = ntiles;  // largest t with s_pref[t] <= j
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (s_pref[mid] <= j) a = mid;
+      else b = mid;
+    }
+    return T[(long long)a * kTTile + (j - s_pref[a])];
+  };
+  return block_scan_fold_rt<kFB>(acc, n, up, term, sm);
+}
+
+__global__ void __launch_bounds__(kFB)
+    k_affine_fold_block(RowsDev rows, MatDev m, double* tmp, const double* tbuf, const int* tcnt,
+                        long long tstride, int ntiles, const char* frozen) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  const int chain = blockIdx.y;
+  const size_t pr = phys_row(m, i);
+  const double acc0 = chain < 4 ? m.K[4 * pr + chain] : 0.0;
+  const double* T = tbuf + (size_t)i * 3 * tstride + AffineGen::arr(chain, 0) * tstride;
+  const double acc = fold_tiles_block(acc0, AffineGen::up(chain), T, tcnt + (size_t)i * ntiles, ntiles, 0);
+  if (threadIdx.x == 0) tmp[5 * (size_t)i + chain] = acc;
+}
+
+__global__ void __launch_bounds__(kFB)
+    k_conc_fold_block(RowsDev rows, MatDev m, double* vals, double* rvals, const double* tbuf,
+                      const int* tcnt, long long tstride, int ntiles, const char* frozen) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.x, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  const int track = blockIdx.y;
+  const size_t pr = phys_row(m, i);
+  const double* K = m.K + 4 * pr;
+  const double acc0 = track == 0 ? (upper ? K[1] : K[0]) : (upper ? K[3] : K[2]);
+  const double* T = tbuf + (size_t)i * 2 * tstride + track * tstride;
+  const double acc = fold_tiles_block(acc0, upper, T, tcnt + (size_t)i * ntiles, ntiles, 0);
+  if (threadIdx.x == 0) (track ? rvals : vals)[i] = acc;
+}
+
+static int block_fold_rows() {
+  static const int v = [] {
+    const char* e = getenv("PC_BLOCK_FOLD_ROWS");
+    return e && *e ? atoi(e) : 16;
+  }();
+  return v;
+}
+
+static void set_attrs_split() {
+  cudaFuncSetAttribute(k_affine_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(5 * 2 * kTTile * sizeof(double)));
+  cudaFuncSetAttribute(k_conc_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(2 * 2 * kTTile * sizeof(double)));
 }
 
 static bool split_chains(cudaStream_t s, long long cells, int nrows, int na, double** tb, int** tc,
@@ -792,7 +906,7 @@ static bool split_chains(cudaStream_t s, long long cells, int nrows, int na, dou
   *tstride = (long long)*ntiles * kTTile;
   const size_t tb_bytes = (size_t)nrows * na * (size_t)*tstride * sizeof(double);
   const size_t tc_bytes = (size_t)nrows * *ntiles * sizeof(int);
-  char* p = static_cast<char*>(stream_scratch(s, tb_bytes + tc_bytes + 256));
+  char* p = static_cast<char*>(stream_scratch(s, tb_bytes + tc_bytes + 512 + (size_t)nrows * 5 * sizeof(double)));
   if (!p) return false;
   *tb = reinterpret_cast<double*>(p);
   *tc = reinterpret_cast<int*>(p + ((tb_bytes + 255) & ~(size_t)255));
@@ -804,7 +918,9 @@ constexpr size_t chain_smem() {
   return (size_t)(2 * G::NA + 2 * kStages) * Roles<G>::kTile * sizeof(double);  // terms + coefficient ring
 }
 
+static void set_attrs_split();
 static void set_attrs() {
+  set_attrs_split();
   cudaFuncSetAttribute(k_chain_affine_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_chain_relu_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_concretize_big, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -820,8 +936,8 @@ void init_kernel_attrs_chains() { set_attrs(); }
 
 cudaError_t scan_stats_device_chains(int on, unsigned long long* out4) {
   cudaError_t e = cudaSuccess;
-  if (out4) e = cudaMemcpyFromSymbol(out4, g_scan_stats, sizeof(unsigned long long) * 6);
-  const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+  if (out4) e = cudaMemcpyFromSymbol(out4, g_scan_stats, sizeof(unsigned long long) * 8);
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_scan_stats, z, sizeof(z));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_scan_stats_on, &on, sizeof(int));
   return e;
@@ -837,7 +953,14 @@ void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, co
   if (split_chains(s, m.cells, rows.n, 3, &tb, &tc, &ts, &nt)) {
     k_affine_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(L, is_conv ? 1 : 0, rows, fin, m, dev, tb, tc, ts, nt, ctr,
                                                    frozen);
-    k_affine_fold<<<rows.n, 160, 0, s>>>(rows, m, Kout, tb, tc, ts, nt, frozen);
+    if (rows.n <= block_fold_rows() && nt <= kMaxFoldTiles && !rows.dR) {
+      double* tmp = reinterpret_cast<double*>(reinterpret_cast<char*>(tc) + (((size_t)rows.n * nt * sizeof(int) + 255) & ~(size_t)255));
+      k_affine_fold_block<<<dim3(rows.n, 5), kFB, 0, s>>>(rows, m, tmp, tb, tc, ts, nt, frozen);
+      k_affine_finish<<<(rows.n + 127) / 128, 128, 0, s>>>(rows, tmp, Kout, frozen);
+      g_launches += 3;
+      return;
+    }
+    k_affine_fold<<<rows.n, 160, 5 * 2 * kTTile * sizeof(double), s>>>(rows, m, Kout, tb, tc, ts, nt, frozen);
     g_launches += 2;
     return;
   }
@@ -861,7 +984,10 @@ void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& 
   int nt;
   if (split_chains(s, m.cells, rows.n, 2, &tb, &tc, &ts, &nt)) {
     k_conc_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(rows, f, m, blo, bhi, rlo, rhi, tb, tc, ts, nt, frozen);
-    k_conc_fold<<<rows.n, 64, 0, s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen);
+    if (rows.n <= block_fold_rows() && nt <= kMaxFoldTiles && !rows.dR)
+      k_conc_fold_block<<<dim3(rows.n, 2), kFB, 0, s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen);
+    else
+      k_conc_fold<<<rows.n, 64, 2 * 2 * kTTile * sizeof(double), s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen);
     g_launches += 2;
     return;
   }

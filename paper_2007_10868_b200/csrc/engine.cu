@@ -1024,8 +1024,10 @@ struct Walker {
   //            checkpoint once it froze >= 1/8 of the rows.
   void maybe_compact(Mat& m) {
     if (dry || devr || !(allow_freeze && early_term)) return;
-    static const int lazy = env_int("PC_LAZY_COMPACT", 0);
+    static const int lazy_all = env_int("PC_LAZY_COMPACT", 0);
+    static const int lazy_rows = env_int("PC_LAZY_ROWS", 0);
     static const int lag_rows = env_int("PC_LAG_ROWS", 0);
+    const bool lazy = lazy_all || R <= lazy_rows;
     if (lazy) {
       while (!pend.empty()) {
         const cudaError_t e = cudaEventQuery(n->ck_ev[pend.front().ck]);
@@ -1049,8 +1051,9 @@ struct Walker {
   // once the newest one has completed (offers complete in stream order).
   bool ready() const {
     static const int lazy = env_int("PC_LAZY_COMPACT", 0);
+    static const int lazy_rows = env_int("PC_LAZY_ROWS", 0);
     static const int lag_rows = env_int("PC_LAG_ROWS", 0);
-    if (dry || devr || !(allow_freeze && early_term) || lazy || pend.empty()) return true;
+    if (dry || devr || !(allow_freeze && early_term) || lazy || R <= lazy_rows || pend.empty()) return true;
     const size_t keep = R <= lag_rows ? 1 : 0;
     if (pend.size() <= keep) return true;
     const cudaError_t e = cudaEventQuery(n->ck_ev[pend[pend.size() - 1 - keep].ck]);
@@ -2216,11 +2219,11 @@ pc_status pc_scalar_ops(int op, const double* a, const double* b, double* out, l
 
 pc_status pc_scan_stats(int on, unsigned long long* out4) {
   return guard([&] {
-    unsigned long long a[6] = {0, 0, 0, 0, 0, 0}, b[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long a[8] = {0, 0, 0, 0, 0, 0, 0, 0}, b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     ck(scan_stats_device(on, a), "scan_stats");
     ck(scan_stats_device_chains(on, b), "scan_stats");
     if (out4)
-      for (int k = 0; k < 6; ++k) out4[k] = a[k] + b[k];
+      for (int k = 0; k < 8; ++k) out4[k] = a[k] + b[k];
   });
 }
 

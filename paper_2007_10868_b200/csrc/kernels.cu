@@ -3088,7 +3088,7 @@ void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
   cudaMemsetAsync(out.hi, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
   const long long cells = (long long)fout.S_w * fout.S_h * L.in_c;
   dim3 grid(cdiv(cells, kFlatOPB), rows.n);
-  static const int pairs = env_int("PC_GBC_FLAT_PAIRS", 1);
+  static const int pairs = env_int("PC_GBC_FLAT_PAIRS", 0);
   static const int minb2 = env_int("PC_GBC_FLAT2_MINB", 2);
   if (pairs) {
     if (minb2 >= 3) k_gbc_flat2<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
@@ -3962,17 +3962,18 @@ __global__ void k_chain_fold(int n_chains, int len, const double* acc0, const do
 
 __global__ void __launch_bounds__(512) k_chain_fold_block(int len, const double* acc0, const double* terms,
                                                           const int* up, double* out) {
-  __shared__ long long sm[2 * 512 / 32 + 4];
+  __shared__ long long sm[2 * 512 / 32 + 8];
   const int c = blockIdx.x;
   const double* t = terms + (size_t)c * len;
-  const double r = block_scan_fold<512>(acc0[c], len, (up[c] & 1) != 0, [&](int j) { return t[j]; }, sm);
+  const double r = (up[c] & 16) ? block_scan_fold_rt<512>(acc0[c], len, (up[c] & 1) != 0, [&](int j) { return t[j]; }, sm)
+                                : block_scan_fold<512>(acc0[c], len, (up[c] & 1) != 0, [&](int j) { return t[j]; }, sm);
   if (threadIdx.x == 0) out[c] = r;
 }
 
 cudaError_t scan_stats_device(int on, unsigned long long* out4) {
   cudaError_t e = cudaSuccess;
-  if (out4) e = cudaMemcpyFromSymbol(out4, g_scan_stats, sizeof(unsigned long long) * 6);
-  const unsigned long long z[6] = {0, 0, 0, 0, 0, 0};
+  if (out4) e = cudaMemcpyFromSymbol(out4, g_scan_stats, sizeof(unsigned long long) * 8);
+  const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_scan_stats, z, sizeof(z));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_scan_stats_on, &on, sizeof(int));
   return e;

@@ -40,7 +40,7 @@ namespace pc {
 // [2] scalar links after a failed step, [3] frame-less scalar links.
 // One copy per translation unit (no relocatable device code); each .cu that
 // folds exposes its own accessor (scan_stats_device*).
-static __device__ unsigned long long g_scan_stats[6];
+static __device__ unsigned long long g_scan_stats[8];
 static __device__ int g_scan_stats_on;
 __device__ __forceinline__ void scan_stat(int k, unsigned long long v) {
   if (g_scan_stats_on) atomicAdd(&g_scan_stats[k], v);
@@ -350,6 +350,13 @@ __device__ __forceinline__ double scan_fold4_pf(double acc, int n, bool up, cons
     if (bad) {
       const int bl = __ffs(bad) - 1;
       k = 4 * bl + __shfl_sync(0xffffffffu, first, bl);
+      if (g_scan_stats_on && lane == bl) {  // why the link left the scan: 6 grew past the binade, 7 shrank / flipped
+        const int f = k & 3;
+        const long long mf = f == 0 ? mk[0] : f == 1 ? mk[1] : f == 2 ? mk[2] : mk[3];
+        const long long am = mf < 0 ? -mf : mf;
+        if (am > kScanHi && ((mf < 0) == (M < 0))) scan_stat(6, 1);
+        else if (am < kScanLo || ((mf < 0) != (M < 0))) scan_stat(7, 1);
+      }
     }
     if (lane == 0) {
       scan_stat(0, 1);
@@ -489,6 +496,141 @@ __device__ __forceinline__ double block_scan_fold(double acc, int n, bool up, co
       ++base;
     }
     __syncthreads();  // shared scratch reused by the next step
+  }
+  return acc;
+}
+
+// CTA-wide fold with local retry: a window of 4*NT links is loaded into
+// registers once; the block scans it, and after a link that leaves the scan's
+// domain (applied as the scalar op) it rescans only the rest of the window in
+// the new frame, without reloading or recomputing terms. For long chains of
+// few rows, where one warp's step latency would be the critical path.
+// sm: at least 2*NT/32 + 8 long longs of shared memory.
+template <int NT, class TermFn>
+__device__ __forceinline__ double block_scan_fold_rt(double acc, int n, bool up, const TermFn& term,
+                                                     long long* sm) {
+  constexpr int NW = NT / 32, WIN = 4 * NT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long* s_w0 = sm;
+  long long* s_w1 = sm + NW;
+  int* s_first = reinterpret_cast<int*>(sm + 2 * NW);
+  long long* s_m = sm + 2 * NW + 1;
+  double* s_t = reinterpret_cast<double*>(sm + 2 * NW + 2);
+  for (int wb = 0; wb < n; wb += WIN) {
+    const int cnt = min(WIN, n - wb);
+    const int j0 = 4 * tid;
+    double tv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tv[k] = j0 + k < cnt ? term(wb + j0 + k) : PC_SCAN_NAN;
+    int lo = 0;  // first link of the window not yet folded
+    while (lo < cnt) {
+      int ex;
+      double inv;
+      long long M;
+      if (!scan_frame(acc, ex, inv, M)) {  // next term as the scalar op
+        int mine = WIN;
+#pragma unroll
+        for (int k = 3; k >= 0; --k)
+          if (j0 + k >= lo && j0 + k < cnt && tv[k] == tv[k]) mine = j0 + k;
+        if (tid == 0) *s_first = WIN;
+        __syncthreads();
+        if (mine < WIN) atomicMin(s_first, mine);
+        __syncthreads();
+        const int f = *s_first;
+        if (f < WIN && f >> 2 == tid) *s_t = (f & 3) == 0 ? tv[0] : (f & 3) == 1 ? tv[1] : (f & 3) == 2 ? tv[2] : tv[3];
+        __syncthreads();
+        if (f < WIN) {
+          const double t = *s_t;
+          acc = up ? add_up(acc, t) : add_down(acc, t);
+          lo = f + 1;
+          if (tid == 0) scan_stat(3, 1);
+        } else {
+          lo = cnt;
+        }
+        __syncthreads();
+        continue;
+      }
+      long long p0[4], p1[4];
+      int first = WIN;
+      long long r0 = 0, r1 = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bool ok = true;
+        long long d0 = 0, d1 = 0;
+        const int j = j0 + k;
+        if (j >= lo && j < cnt) scan_delta2(tv[k], inv, up, ok, d0, d1);
+        scan_compose2(r0, r1, d0, d1, r0, r1);
+        p0[k] = r0;
+        p1[k] = r1;
+        if (!ok && j >= lo && j < cnt && first == WIN) first = j;
+      }
+      long long i0 = r0, i1 = r1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long u0 = __shfl_up_sync(0xffffffffu, i0, o), u1 = __shfl_up_sync(0xffffffffu, i1, o);
+        if (lane >= o) scan_compose2(u0, u1, i0, i1, i0, i1);
+      }
+      long long e0 = __shfl_up_sync(0xffffffffu, i0, 1), e1 = __shfl_up_sync(0xffffffffu, i1, 1);
+      if (lane == 0) e0 = e1 = 0;
+      if (tid == 0) *s_first = WIN;
+      if (lane == 31) {
+        s_w0[warp] = i0;
+        s_w1[warp] = i1;
+      }
+      __syncthreads();
+      if (warp == 0) {  // exclusive prefixes of the warp totals, by one warp
+        long long a0 = lane < NW ? s_w0[lane] : 0, a1 = lane < NW ? s_w1[lane] : 0;
+        long long q0 = a0, q1 = a1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long u0 = __shfl_up_sync(0xffffffffu, q0, o), u1 = __shfl_up_sync(0xffffffffu, q1, o);
+          if (lane >= o) scan_compose2(u0, u1, q0, q1, q0, q1);
+        }
+        long long x0 = __shfl_up_sync(0xffffffffu, q0, 1), x1 = __shfl_up_sync(0xffffffffu, q1, 1);
+        if (lane == 0) x0 = x1 = 0;
+        if (lane < NW) {
+          s_w0[lane] = x0;
+          s_w1[lane] = x1;
+        }
+      }
+      __syncthreads();
+      long long x0, x1;
+      scan_compose2(s_w0[warp], s_w1[warp], e0, e1, x0, x1);
+      const long long P = (M & 1) ? x1 : x0;
+      const int pl = (int)((M + P) & 1);
+      long long mk[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mk[k] = M + P + (pl ? p1[k] : p0[k]);
+        const long long am = mk[k] < 0 ? -mk[k] : mk[k];
+        const int j = j0 + k;
+        if (j < first && j >= lo && j < cnt && !(((mk[k] < 0) == (M < 0)) && am >= kScanLo && am <= kScanHi))
+          first = j;
+      }
+      if (first < WIN) atomicMin(s_first, first);
+      __syncthreads();
+      const int f = min(*s_first, cnt);  // links lo .. f-1 committed by the scan
+      if (tid == 0) {
+        scan_stat(0, 1);
+        scan_stat(1, f - lo);
+        if (f < cnt) scan_stat(2, 1);
+      }
+      if (f > lo && (f - 1) >> 2 == tid) {
+        const int slot = (f - 1) & 3;
+        *s_m = slot == 0 ? mk[0] : slot == 1 ? mk[1] : slot == 2 ? mk[2] : mk[3];
+      }
+      if (f < cnt && f >> 2 == tid) *s_t = (f & 3) == 0 ? tv[0] : (f & 3) == 1 ? tv[1] : (f & 3) == 2 ? tv[2] : tv[3];
+      __syncthreads();
+      if (f > lo) acc = scan_compose(*s_m, ex);
+      if (f < cnt) {  // the link that left the scan's domain, as the scalar op
+        const double t = *s_t;
+        if (t == t) acc = up ? add_up(acc, t) : add_down(acc, t);
+        lo = f + 1;
+      } else {
+        lo = cnt;
+      }
+      __syncthreads();
+    }
   }
   return acc;
 }

@@ -19,11 +19,12 @@ x = pc.random_inputs(INPUT_SEED, 1, int(np.prod(net.input_shape)))[0]
 box = pc.input_box(x, float(eps_s))
 lab = max(v.candidate(x), 0)
 v.verify_robustness(box, lab)
-out = (ctypes.c_ulonglong * 6)()
+out = (ctypes.c_ulonglong * 8)()
 _lib.check(_lib.lib.pc_scan_stats(1, out))
 v.verify_robustness(box, lab)
 _lib.check(_lib.lib.pc_scan_stats(0, out))
-steps, links, fails, frameless, ties, huge = list(out)
+steps, links, fails, frameless, ties, huge, grew, shrank = list(out)
 print({"config": name, "scan_steps": steps, "scanned_links": links, "fallbacks_after_scan": fails,
-       "frameless_scalar": frameless, "ties": ties, "huge_terms": huge, "links_per_step": links / max(steps, 1),
+       "frameless_scalar": frameless, "ties": ties, "huge_terms": huge, "fail_grew": grew,
+       "fail_shrank_or_flipped": shrank, "links_per_step": links / max(steps, 1),
        "fallback_per_link": fails / max(links, 1)})

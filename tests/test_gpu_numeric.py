@@ -170,7 +170,7 @@ def test_chain_fold_matches_serial(port, length):
     bit for bit, on both directions."""
     rng = np.random.default_rng(length)
     A, T = chain_cases(rng, 96, length)
-    for upv in (0, 1, 2, 3, 4, 5, 8, 9):  # bit 0: add_up; 1: 32-link warp scan; 2: CTA scan; 3: prefetching warp scan
+    for upv in (0, 1, 2, 3, 4, 5, 8, 9, 20, 21):  # bit 0: add_up; 1: 32-link warp scan; 2: CTA scan; 3: prefetching warp scan; 4 (with 2): CTA scan with local retry
         up = np.full(len(A), upv, dtype=np.int32)
         up[::3] ^= 1
         g = gpu_chain_fold(A, T, up)
