@@ -73,6 +73,7 @@ def parse():
     ap.add_argument("--throughput-images", type=int, default=16, help="images per replica batch")
     ap.add_argument("--concurrency", type=int, default=4, help="worker contexts of the replica batch")
     ap.add_argument("--pool", type=int, default=8, help="distinct images cycled through by the steps")
+    ap.add_argument("--fast-steps", type=int, default=4, help="steps of the fast numeric mode (0: skip)")
     return ap.parse_args()
 
 
@@ -393,6 +394,35 @@ def main():
         thr = {"value": bms / (n_t * world), "unit": "ms/image", "images": n_t * world,
                "concurrency_per_gpu": args.concurrency, "scaling": "weak"}
 
+    # the fast numeric mode (native directed rounding, sound, not bit-identical;
+    # SURVEY.md §8f.3): latency on the same images, verdicts and margins
+    # against the reference fixtures reported separately
+    fast = None
+    if world == 1 and args.fast_steps > 0:
+        vf = pc.Verifier(net, pc.AnalysisOptions(early_term=et, device=local, numeric_mode=1))
+        fl, fres = [], {}
+        for s in range(warm + args.fast_steps):
+            i = s % args.pool
+            flush.fill_(s & 0xFF)
+            torch.cuda.synchronize()
+            ver, mar, st = vf.test_device(dboxes[i][0].data_ptr(), dboxes[i][1].data_ptr(), labels[i])
+            if s >= warm:
+                fl.append(vf.last_timing()["total_ms"])
+            fres.setdefault(i, (ver, mar))
+        fxs = fixtures(args.config)
+        cmp = {}
+        for i, (ver, mar) in sorted(fres.items()):
+            if i in fxs:
+                ref_m = np.array([float.fromhex(h) for h in fxs[i]["margins_hex"]])
+                cmp[i] = {"verdict_equal": bool(ver) == fxs[i]["verified"],
+                          "max_rel_margin_diff": float(np.max(np.abs(mar - ref_m) / np.maximum(1.0, np.abs(ref_m))))}
+        fast = {"mode": "numeric_mode=1: RD/RU FMAs in the conv coefficients, RD/RU chains and concretisations "
+                        "(sound, not bit-identical to the reference)",
+                "latency_ms_per_image": statistics.mean(fl) if fl else None, "steps": len(fl),
+                "verified": f"{sum(int(bool(r[0])) for r in fres.values())}/{len(fres)} distinct images",
+                "vs_reference_fixtures": cmp}
+        vf.close()
+
     # in-bench parity against the reference fixtures of the timed images
     fx = fixtures(args.config)
     checked, mismatches = [], []
@@ -430,6 +460,7 @@ def main():
                    "images_checked": checked, "mismatches": mismatches,
                    "all_equal": bool(checked) and not mismatches},
         "sharding_transport": transport,
+        "fast_mode": fast,
         "e2e": {"value": statistics.mean(e2e), "unit": "ms/image",
                 "h2d_bytes_per_step": 2 * 8 * n_in, "d2h_bytes_per_step": 8 * (net.output_size - 1) + 4},
         "gpu_launches": int(launches),

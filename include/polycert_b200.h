@@ -73,6 +73,10 @@ typedef struct {
   long long memory_budget; /* bytes; 0: engine default */
   int device;              /* CUDA ordinal; -1: current */
   int exec_mode;           /* 0 auto, 1 host-driven schedule, 2 device-driven (CUDA graph) */
+  int numeric_mode;        /* 0 the reference's WidenedFloat64, bit for bit (default);
+                              1 fast: native directed rounding (RD / RU FMAs and adds) in
+                              the conv coefficients, the constant chains and the
+                              concretisations — sound (outward), not bit-identical */
 } pc_options;
 
 /* PassStats (backsub.hpp:119-136). */

@@ -73,9 +73,11 @@ struct AnalysisOptions {  // analyzer.hpp:164-169
   int workers = 1;              // accepted for source compatibility; the GPU grid is the parallelism
   int device = -1;              // CUDA ordinal; -1: current
   int exec_mode = 0;            // 0 auto, 1 host-driven schedule, 2 device-driven (CUDA graph)
+  int numeric_mode = 0;         // 0 WidenedFloat64 bit for bit; 1 fast native directed rounding (sound)
   bool operator==(const AnalysisOptions& o) const {
     return early_term == o.early_term && chunk_rows == o.chunk_rows &&
-           memory_budget == o.memory_budget && device == o.device && exec_mode == o.exec_mode;
+           memory_budget == o.memory_budget && device == o.device && exec_mode == o.exec_mode &&
+           numeric_mode == o.numeric_mode;
   }
 };
 
@@ -140,6 +142,7 @@ inline pc_options call_options(const AnalysisOptions& opt) {
   o.memory_budget = opt.memory_budget;
   o.device = opt.device;
   o.exec_mode = opt.exec_mode;
+  o.numeric_mode = opt.numeric_mode;
   return o;
 }
 

@@ -31,7 +31,7 @@ class PcLayerDesc(ctypes.Structure):
 class PcOptions(ctypes.Structure):
     _fields_ = [("early_term", ctypes.c_int), ("chunk_rows", ctypes.c_longlong),
                 ("memory_budget", ctypes.c_longlong), ("device", ctypes.c_int),
-                ("exec_mode", ctypes.c_int)]
+                ("exec_mode", ctypes.c_int), ("numeric_mode", ctypes.c_int)]
 
 
 class PcStats(ctypes.Structure):

@@ -101,9 +101,21 @@ struct AffineGen {
     }
     p.dj = dev[jd];
   }
+  bool fast = false;  // fast numeric mode: directed-rounding products
   __device__ bool gen(Iv c, const Pre& p, double* t) {
     if (iv_zero(c)) return false;
     madds += p.taps;
+    if (fast) {
+      const double b = p.b;
+      if (b == 0.0) {
+        t[0] = t[1] = PC_NAN;
+      } else {
+        t[0] = __dmul_rd(b > 0.0 ? c.lo : c.hi, b);
+        t[1] = __dmul_ru(b > 0.0 ? c.hi : c.lo, b);
+      }
+      t[2] = p.dj != 0.0 ? __dmul_ru(iv_mag(c), p.dj) : PC_NAN;
+      return true;
+    }
     const Iv bt = iv_mul_scalar(c, p.b);
     t[0] = iv_zero(bt) ? PC_NAN : bt.lo;
     t[1] = iv_zero(bt) ? PC_NAN : bt.hi;
@@ -182,10 +194,16 @@ struct ConcGen {
     p.B = Iv{blo[j], bhi[j]};
     p.Br = Iv{rlo[j], rhi[j]};
   }
+  bool fast = false;  // fast numeric mode: directed-rounding corner products
+  __device__ static double fcorner(Iv c, Iv B, bool up) {
+    if (up)
+      return fmax(fmax(__dmul_ru(c.lo, B.lo), __dmul_ru(c.lo, B.hi)), fmax(__dmul_ru(c.hi, B.lo), __dmul_ru(c.hi, B.hi)));
+    return fmin(fmin(__dmul_rd(c.lo, B.lo), __dmul_rd(c.lo, B.hi)), fmin(__dmul_rd(c.hi, B.lo), __dmul_rd(c.hi, B.hi)));
+  }
   __device__ bool gen(Iv c, const Pre& p, double* t) {
     if (iv_zero(c)) return false;
-    const double tp = upper ? corner_hi(c, p.B) : corner_lo(c, p.B);
-    const double tr = upper ? corner_hi(c, p.Br) : corner_lo(c, p.Br);
+    const double tp = fast ? fcorner(c, p.B, upper) : upper ? corner_hi(c, p.B) : corner_lo(c, p.B);
+    const double tr = fast ? fcorner(c, p.Br, upper) : upper ? corner_hi(c, p.Br) : corner_lo(c, p.Br);
     const bool zp = skip0 && __double_as_longlong(tp) == 0, zr = skip0 && __double_as_longlong(tr) == 0;
     t[0] = zp ? PC_NAN : tp;
     t[1] = zr ? PC_NAN : tr;
@@ -687,7 +705,8 @@ __device__ __forceinline__ void tile_terms(G& g, const double* lo, const double*
 
 __global__ void __launch_bounds__(kTT)
     k_affine_terms(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, const double* dev,
-                   double* tbuf, int* tcnt, long long tstride, int ntiles, Counters* ctr, const char* frozen) {
+                   double* tbuf, int* tcnt, long long tstride, int ntiles, Counters* ctr, const char* frozen,
+                   int fast) {
   int i;
   if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
@@ -696,6 +715,7 @@ __global__ void __launch_bounds__(kTT)
   if (frozen && frozen[(size_t)img * rows.kq + q]) return;
   ctr += img;
   AffineGen g{L, is_conv, f, 0, 0, dev + img * rows.sst};
+  g.fast = fast != 0;
   if (is_conv) frame_base(f, q, g.bw, g.bh);
   const size_t pr = phys_row(m, i);
   tile_terms(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, tbuf + (size_t)i * 3 * tstride, tstride,
@@ -712,6 +732,7 @@ __global__ void __launch_bounds__(kTT)
 // staged into the warp's shared-memory buffer by cp.async one tile ahead
 // (16-byte copies; the scratch tiles are 16-byte aligned, kTTile doubles
 // apart), so every scan step reads shared memory.
+template <bool FAST>
 __device__ __forceinline__ double fold_tiles(double acc, bool up, const double* T, const int* cnt,
                                              int ntiles, double* buf /* [2][kTTile] */) {
   const int lane = threadIdx.x & 31;
@@ -736,7 +757,7 @@ __device__ __forceinline__ double fold_tiles(double acc, bool up, const double* 
     }
     __syncwarp();
     const double* B = buf + b * kTTile;
-    acc = scan_fold4(acc, cnt[t], up, [&](int j) { return B[j]; });
+    acc = scan_fold4m<FAST>(acc, cnt[t], up, [&](int j) { return B[j]; });
     __syncwarp();  // buffer b is restaged by the next iteration's stage(t + 2)
   }
   return acc;
@@ -744,7 +765,7 @@ __device__ __forceinline__ double fold_tiles(double acc, bool up, const double* 
 
 __global__ void __launch_bounds__(160)
     k_affine_fold(RowsDev rows, MatDev m, double* Kout, const double* tbuf, const int* tcnt,
-                  long long tstride, int ntiles, const char* frozen) {
+                  long long tstride, int ntiles, const char* frozen, int fast) {
   __shared__ double s_acc[5];
   int i;
   if (!rows_resolve(rows, blockIdx.x, i)) return;
@@ -759,7 +780,8 @@ __global__ void __launch_bounds__(160)
   const double* T = tbuf + (size_t)i * 3 * tstride + AffineGen::arr(warp, 0) * tstride;
   const int* cnt = tcnt + (size_t)i * ntiles;
   extern __shared__ __align__(16) double fbuf[];
-  acc = fold_tiles(acc, up, T, cnt, ntiles, fbuf + (size_t)warp * 2 * kTTile);
+  acc = fast ? fold_tiles<true>(acc, up, T, cnt, ntiles, fbuf + (size_t)warp * 2 * kTTile)
+             : fold_tiles<false>(acc, up, T, cnt, ntiles, fbuf + (size_t)warp * 2 * kTTile);
   if ((threadIdx.x & 31) == 0) s_acc[warp] = acc;
   __syncthreads();
   if (threadIdx.x < 4) {
@@ -774,7 +796,7 @@ __global__ void __launch_bounds__(160)
 __global__ void __launch_bounds__(kTT)
     k_conc_terms(RowsDev rows, FrameDev f, MatDev m, const double* blo, const double* bhi,
                  const double* rlo, const double* rhi, double* tbuf, int* tcnt, long long tstride,
-                 int ntiles, const char* frozen) {
+                 int ntiles, const char* frozen, int fast) {
   int i;
   if (!rows_resolve(rows, blockIdx.y, i)) return;
   bool upper;
@@ -788,6 +810,7 @@ __global__ void __launch_bounds__(kTT)
   const bool neg0 = (__double_as_longlong(a0) == (long long)0x8000000000000000ULL) ||
                     (__double_as_longlong(a1) == (long long)0x8000000000000000ULL);
   ConcGen g{f, 0, 0, upper, !neg0, blo + so, bhi + so, rlo + so, rhi + so};
+  g.fast = fast != 0;
   frame_base(f, q, g.bw, g.bh);
   tile_terms(g, m.lo + pr * m.cells, m.hi + pr * m.cells, m.cells, tbuf + (size_t)i * 2 * tstride, tstride,
              tcnt + (size_t)i * ntiles);
@@ -795,7 +818,7 @@ __global__ void __launch_bounds__(kTT)
 
 __global__ void __launch_bounds__(64)
     k_conc_fold(RowsDev rows, MatDev m, double* vals, double* rvals, const double* tbuf, const int* tcnt,
-                long long tstride, int ntiles, const char* frozen) {
+                long long tstride, int ntiles, const char* frozen, int fast) {
   int i;
   if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
@@ -809,7 +832,8 @@ __global__ void __launch_bounds__(64)
   const double* T = tbuf + (size_t)i * 2 * tstride + warp * tstride;
   const int* cnt = tcnt + (size_t)i * ntiles;
   extern __shared__ __align__(16) double fbuf[];
-  acc = fold_tiles(acc, upper, T, cnt, ntiles, fbuf + (size_t)warp * 2 * kTTile);
+  acc = fast ? fold_tiles<true>(acc, upper, T, cnt, ntiles, fbuf + (size_t)warp * 2 * kTTile)
+             : fold_tiles<false>(acc, upper, T, cnt, ntiles, fbuf + (size_t)warp * 2 * kTTile);
   if ((threadIdx.x & 31) == 0) (warp ? rvals : vals)[i] = acc;
 }
 
@@ -818,9 +842,9 @@ __global__ void __launch_bounds__(64)
 constexpr int kFB = 512;
 constexpr int kMaxFoldTiles = 128;
 
-template <class F>
+template <bool FAST>
 __device__ __forceinline__ double fold_tiles_block(double acc, bool up, const double* T, const int* cnt,
-                                                   int ntiles, F&& /*unused*/) {
+                                                   int ntiles) {
   __shared__ int s_pref[kMaxFoldTiles + 1];
   __shared__ long long sm[2 * kFB / 32 + 8];
   if (threadIdx.x == 0) {
@@ -842,12 +866,12 @@ __device__ __forceinline__ double fold_tiles_block(double acc, bool up, const do
     }
     return T[(long long)a * kTTile + (j - s_pref[a])];
   };
-  return block_scan_fold_rt<kFB>(acc, n, up, term, sm);
+  return block_scan_fold_rtm<kFB, FAST>(acc, n, up, term, sm);
 }
 
 __global__ void __launch_bounds__(kFB)
     k_affine_fold_block(RowsDev rows, MatDev m, double* tmp, const double* tbuf, const int* tcnt,
-                        long long tstride, int ntiles, const char* frozen) {
+                        long long tstride, int ntiles, const char* frozen, int fast) {
   int i;
   if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
@@ -858,13 +882,14 @@ __global__ void __launch_bounds__(kFB)
   const size_t pr = phys_row(m, i);
   const double acc0 = chain < 4 ? m.K[4 * pr + chain] : 0.0;
   const double* T = tbuf + (size_t)i * 3 * tstride + AffineGen::arr(chain, 0) * tstride;
-  const double acc = fold_tiles_block(acc0, AffineGen::up(chain), T, tcnt + (size_t)i * ntiles, ntiles, 0);
+  const double acc = fast ? fold_tiles_block<true>(acc0, AffineGen::up(chain), T, tcnt + (size_t)i * ntiles, ntiles)
+                          : fold_tiles_block<false>(acc0, AffineGen::up(chain), T, tcnt + (size_t)i * ntiles, ntiles);
   if (threadIdx.x == 0) tmp[5 * (size_t)i + chain] = acc;
 }
 
 __global__ void __launch_bounds__(kFB)
     k_conc_fold_block(RowsDev rows, MatDev m, double* vals, double* rvals, const double* tbuf,
-                      const int* tcnt, long long tstride, int ntiles, const char* frozen) {
+                      const int* tcnt, long long tstride, int ntiles, const char* frozen, int fast) {
   int i;
   if (!rows_resolve(rows, blockIdx.x, i)) return;
   bool upper;
@@ -876,7 +901,8 @@ __global__ void __launch_bounds__(kFB)
   const double* K = m.K + 4 * pr;
   const double acc0 = track == 0 ? (upper ? K[1] : K[0]) : (upper ? K[3] : K[2]);
   const double* T = tbuf + (size_t)i * 2 * tstride + track * tstride;
-  const double acc = fold_tiles_block(acc0, upper, T, tcnt + (size_t)i * ntiles, ntiles, 0);
+  const double acc = fast ? fold_tiles_block<true>(acc0, upper, T, tcnt + (size_t)i * ntiles, ntiles)
+                          : fold_tiles_block<false>(acc0, upper, T, tcnt + (size_t)i * ntiles, ntiles);
   if (threadIdx.x == 0) (track ? rvals : vals)[i] = acc;
 }
 
@@ -945,22 +971,23 @@ cudaError_t scan_stats_device_chains(int on, unsigned long long* out4) {
 
 void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                              const FrameDev& fin, MatDev m, double* Kout, const double* dev,
-                             Counters* ctr, const char* frozen) {
+                             Counters* ctr, const char* frozen, bool fast) {
   double* tb;
   int* tc;
   long long ts;
   int nt;
   if (split_chains(s, m.cells, rows.n, 3, &tb, &tc, &ts, &nt)) {
     k_affine_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(L, is_conv ? 1 : 0, rows, fin, m, dev, tb, tc, ts, nt, ctr,
-                                                   frozen);
+                                                   frozen, fast ? 1 : 0);
     if (rows.n <= block_fold_rows() && nt <= kMaxFoldTiles && !rows.dR) {
       double* tmp = reinterpret_cast<double*>(reinterpret_cast<char*>(tc) + (((size_t)rows.n * nt * sizeof(int) + 255) & ~(size_t)255));
-      k_affine_fold_block<<<dim3(rows.n, 5), kFB, 0, s>>>(rows, m, tmp, tb, tc, ts, nt, frozen);
+      k_affine_fold_block<<<dim3(rows.n, 5), kFB, 0, s>>>(rows, m, tmp, tb, tc, ts, nt, frozen, fast ? 1 : 0);
       k_affine_finish<<<(rows.n + 127) / 128, 128, 0, s>>>(rows, tmp, Kout, frozen);
       g_launches += 3;
       return;
     }
-    k_affine_fold<<<rows.n, 160, 5 * 2 * kTTile * sizeof(double), s>>>(rows, m, Kout, tb, tc, ts, nt, frozen);
+    k_affine_fold<<<rows.n, 160, 5 * 2 * kTTile * sizeof(double), s>>>(rows, m, Kout, tb, tc, ts, nt, frozen,
+                                                                       fast ? 1 : 0);
     g_launches += 2;
     return;
   }
@@ -977,17 +1004,19 @@ void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& 
 
 void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            const double* blo, const double* bhi, const double* rlo,
-                           const double* rhi, double* vals, double* rvals, const char* frozen) {
+                           const double* rhi, double* vals, double* rvals, const char* frozen, bool fast) {
   double* tb;
   int* tc;
   long long ts;
   int nt;
   if (split_chains(s, m.cells, rows.n, 2, &tb, &tc, &ts, &nt)) {
-    k_conc_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(rows, f, m, blo, bhi, rlo, rhi, tb, tc, ts, nt, frozen);
+    k_conc_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(rows, f, m, blo, bhi, rlo, rhi, tb, tc, ts, nt, frozen,
+                                                 fast ? 1 : 0);
     if (rows.n <= block_fold_rows() && nt <= kMaxFoldTiles && !rows.dR)
-      k_conc_fold_block<<<dim3(rows.n, 2), kFB, 0, s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen);
+      k_conc_fold_block<<<dim3(rows.n, 2), kFB, 0, s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen, fast ? 1 : 0);
     else
-      k_conc_fold<<<rows.n, 64, 2 * 2 * kTTile * sizeof(double), s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen);
+      k_conc_fold<<<rows.n, 64, 2 * 2 * kTTile * sizeof(double), s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen,
+                                                                      fast ? 1 : 0);
     g_launches += 2;
     return;
   }

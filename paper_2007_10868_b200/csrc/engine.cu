@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/polycert_b200.h"
+#include <nvtx3/nvToolsExt.h>
 #include "kernels.cuh"
 
 using namespace pc;
@@ -39,6 +40,18 @@ thread_local long long g_dense_launches = 0;
 thread_local double g_conv_ms = 0, g_conv_bytes = 0;
 thread_local long long g_conv_launches = 0;
 thread_local double g_conv_exec = 0;  // interval madds executed by the live-cell conv kernel
+
+// NVTX ranges (header-only nvtx3): visible in Nsight Systems / ncu --nvtx;
+// no cost without a tool attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* what, int k) {
+    char buf[48];
+    snprintf(buf, sizeof(buf), "%s %d", what, k);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct StatusError : std::runtime_error {
   pc_status code;
@@ -639,6 +652,8 @@ struct Walker {
   int ck_index = 0;  // checkpoints issued by this walk (1-based index of the last)
 
   int nrows() const { return both ? 2 * R : R; }
+  // fast numeric mode (pc_options.numeric_mode = 1)
+  bool fast() const { return n->opt.numeric_mode == 1; }
   // rows frozen at an earlier checkpoint are skipped by the chain kernels
   const char* fz() const { return (allow_freeze && early_term && !margin) ? n->frozen : nullptr; }
   // image-batched walks (run_test_batched): row keys img * kq + neuron
@@ -723,7 +738,7 @@ struct Walker {
       need(m);
       prof_begin(n, PROF_CHAIN_AFFINE, s2);
       launch_chain_affine(s2, L.d, false, rows(), fdev(n, m.f, q), md(m), out.K,
-                          n->dev + n->off[m.f.layer], n->ctr, fz());
+                          n->dev + n->off[m.f.layer], n->ctr, fz(), fast());
       prof_end(n, s2);
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (n->timing) {  // the roofline kernel is always timed (bench.py reads it)
@@ -782,7 +797,7 @@ struct Walker {
         need(m);
         prof_begin(n, PROF_CHAIN_AFFINE, s2);
         launch_chain_affine(s2, L.d, true, rows(), fi, md(m), out.K, n->dev + n->off[m.f.layer],
-                            n->ctr, fz());
+                            n->ctr, fz(), fast());
         prof_end(n, s2);
       }
       if (sparse) {
@@ -818,7 +833,7 @@ struct Walker {
         } else if (flat && fo.S_h <= 64 && (long long)fo.G_w * fo.G_h < 65536) {
           const FlatDev fl{n->lv_pref + n->pofs[L.pred0] + L.pred0, n->lv_fpos + n->off[L.pred0],
                            n->lv_fch + n->off[L.pred0], n->pofs[nl] + nl, n->total};
-          launch_gbc_flat(s, L.d, rows(), fi, fo, sp, md(m), md(out), fl, n->ctr);
+          launch_gbc_flat(s, L.d, rows(), fi, fo, sp, md(m), md(out), fl, n->ctr, fast());
         } else {
           const LiveDev lv{n->lv_cnt + n->pofs[L.pred0], n->lv_idx + n->off[L.pred0], n->pofs[nl], n->total};
           launch_gbc_live(s, L.d, rows(), fi, fo, sp, md(m), md(out), lv, n->ctr);
@@ -913,7 +928,7 @@ struct Walker {
     if (margin) {
       prof_begin(n, PROF_CONC, s2);
       launch_concretize(s2, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->blo + o,
-                        n->bhi + o, n->vals, n->rvals, nullptr);
+                        n->bhi + o, n->vals, n->rvals, nullptr, fast());
       prof_end(n, s2);
       launch_margin_offer(s2, R, n->vals, n->best, n->has);
       return;
@@ -925,7 +940,7 @@ struct Walker {
                              n->rhi + o, n->vals, n->rvals, fz());
     else
       launch_concretize(s2, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
-                        n->rhi + o, n->vals, n->rvals, fz());
+                        n->rhi + o, n->vals, n->rvals, fz(), fast());
     prof_end(n, s2);
     int* new_q = n->rowq[rq ^ 1];
     if (devr) {
@@ -1444,6 +1459,7 @@ void run_pass_graph(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
 }
 
 void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
+  NvtxRange nv("pass", t);
   cudaStream_t s = n->stream;
   const HostLayer& Q = n->L[t];
   const int N = (int)Q.numel();
@@ -1559,6 +1575,7 @@ void run_margin_graph(Ctx* n, pc_stats* st) {
 
 // run_margin_pass (backsub.hpp:1070-1096)
 void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
+  NvtxRange nv("margin pass");
   cudaStream_t s = n->stream;
   const int out = (int)n->L.size() - 1;
   const int nr = n->n_out - 1;
@@ -1624,7 +1641,9 @@ std::vector<int> pass_targets(const Ctx* n) {
 // The device-driven schedule needs every pass in one chunk sized for all of
 // the layer's neurons (the live count is only known on the device).
 bool graph_eligible(Ctx* n, size_t* arena_bytes, size_t* stat_count) {
-  if (n->net->shard_world > 1 || n->profile || n->opt.exec_mode != 2 || n->graph_failed) return false;
+  if (n->net->shard_world > 1 || n->profile || n->opt.exec_mode != 2 || n->graph_failed ||
+      n->opt.numeric_mode != 0)
+    return false;
   if (n->opt.chunk_rows > 0) return false;  // an explicit chunking request keeps the host schedule
   size_t arena = 0, stats = 0;
   for (int t : pass_targets(n)) {
@@ -1652,6 +1671,7 @@ bool graph_eligible(Ctx* n, size_t* arena_bytes, size_t* stat_count) {
 // pass changes a layer below its target), so its live-channel table for the
 // conv kernels (k_live_build) is rebuilt right after.
 void forward_layers(Ctx* n, int k0, int k1, int nimg = 1) {
+  NvtxRange nv("forward refresh", k1);
   const int nl = (int)n->L.size();
   const long long T = n->total, P = n->pofs[nl];
   for (int k = k0 + 1; k <= k1; ++k) {
@@ -1747,6 +1767,7 @@ void capture_graph(Ctx* n, bool with_margin, size_t arena, size_t stat_count) {
 
 // analyze + run_margin_pass (analyzer.hpp:198-276)
 void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
+  NvtxRange nv("verify_robustness");
   cudaStream_t s = n->stream;
   const int nl = (int)n->L.size();
   const int out = nl - 1;
@@ -1877,6 +1898,7 @@ void run_test(Ctx* n, int label, double* margins, pc_stats* st) {
 // kernel launch carries B images' rows; the per-neuron state of image b sits
 // at offset b * total. Results per image are the single-image engine's.
 void run_test_batched(Ctx* n, int B, const int* labels, double* margins, pc_stats* stats) {
+  NvtxRange nv("verify_robustness batch", B);
   cudaStream_t s = n->stream;
   const int nl = (int)n->L.size();
   const int out = nl - 1;
@@ -2162,6 +2184,7 @@ void pc_default_options(pc_options* opt) {
   opt->memory_budget = 0;
   opt->device = -1;
   opt->exec_mode = 0;
+  opt->numeric_mode = 0;
 }
 
 const char* pc_last_error(void) { return g_err.c_str(); }
@@ -2257,6 +2280,7 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
     if (opt) n->opt = *opt;
     else pc_default_options(&n->opt);
     if (n->opt.exec_mode == 0) n->opt.exec_mode = env_int("PC_EXEC_MODE", 0);  // tests / experiments
+    if (n->opt.numeric_mode == 0) n->opt.numeric_mode = env_int("PC_NUMERIC_MODE", 0);
     validate(layers, n_layers, in_w, in_h, in_c, n->L);
     int devc = 0;
     ck(cudaGetDeviceCount(&devc), "cudaGetDeviceCount");

@@ -924,9 +924,9 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                          const FrameDev& fin, MatDev m, double* Kout, const double* dev,
-                         Counters* ctr, const char* frozen) {
+                         Counters* ctr, const char* frozen, bool fast) {
   if (use_big_chains(m.cells, rows)) {
-    launch_chain_affine_big(s, L, is_conv, rows, fin, m, Kout, dev, ctr, frozen);
+    launch_chain_affine_big(s, L, is_conv, rows, fin, m, Kout, dev, ctr, frozen, fast);
     return;
   }
   k_chain_affine<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(L, is_conv ? 1 : 0, rows,
@@ -1245,9 +1245,9 @@ __global__ void __launch_bounds__(32 * kChainWarps)
 
 void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        const double* blo, const double* bhi, const double* rlo,
-                       const double* rhi, double* vals, double* rvals, const char* frozen) {
+                       const double* rhi, double* vals, double* rvals, const char* frozen, bool fast) {
   if (use_big_chains(m.cells, rows)) {
-    launch_concretize_big(s, rows, f, m, blo, bhi, rlo, rhi, vals, rvals, frozen);
+    launch_concretize_big(s, rows, f, m, blo, bhi, rlo, rhi, vals, rvals, frozen, fast);
     return;
   }
   k_concretize<<<cdiv(rows.n, kChainWarps), 32 * kChainWarps, 0, s>>>(rows, f, m, blo, bhi, rlo,
@@ -2830,7 +2830,7 @@ void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const uns
 // cells). A block takes kFlatOPB consecutive live cells of its row's window:
 // the window's grid rows are consecutive runs of the flat list.
 constexpr int kFlatOPB = 512;
-template <int MINB>
+template <int MINB, bool FAST = false>
 __global__ void __launch_bounds__(256, MINB)
     k_gbc_flat(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
                MatDev out, FlatDev fl, Counters* ctr) {
@@ -2865,7 +2865,7 @@ __global__ void __launch_bounds__(256, MINB)
   double* olo = out.lo + (size_t)i * ocells;
   double* ohi = out.hi + (size_t)i * ocells;
   const int cin = L.in_c, cout = L.out_c;
-  const bool band = products_in_band(in.stat, L.wmin, L.wmax);
+  const bool band = FAST || products_in_band(in.stat, L.wmin, L.wmax);
   const int* cnt = sp.cnt + (size_t)i * sp.ncell;
   const size_t rbase = (size_t)i * sp.ncell * sp.C;
   MagAcc mag;
@@ -2907,9 +2907,15 @@ __global__ void __launch_bounds__(256, MINB)
               w[u] = wp[(size_t)sp.idx[sb + k + u] * cin];
             }
 #pragma unroll
-            for (int u = 0; u < kB; ++u) madd_band(w[u], cl[u], ch[u], lo, hi);
+            for (int u = 0; u < kB; ++u) {
+              if (FAST) madd_dir(w[u], cl[u], ch[u], lo, hi);
+              else madd_band(w[u], cl[u], ch[u], lo, hi);
+            }
           }
-          for (; k < n; ++k) madd_band(wp[(size_t)sp.idx[sb + k] * cin], sp.lo[sb + k], sp.hi[sb + k], lo, hi);
+          for (; k < n; ++k) {
+            if (FAST) madd_dir(wp[(size_t)sp.idx[sb + k] * cin], sp.lo[sb + k], sp.hi[sb + k], lo, hi);
+            else madd_band(wp[(size_t)sp.idx[sb + k] * cin], sp.lo[sb + k], sp.hi[sb + k], lo, hi);
+          }
         }
       }
       acc = Iv{canon0(lo), hi};
@@ -3081,7 +3087,8 @@ __global__ void __launch_bounds__(256, MINB)
 }
 
 void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
-                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr) {
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr,
+                     bool fast) {
   static const int minb = env_int("PC_GBC_FLAT_MINB", 3);
   // dead cells: +0 (the live ones are overwritten)
   cudaMemsetAsync(out.lo, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
@@ -3093,7 +3100,8 @@ void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
   if (pairs) {
     if (minb2 >= 3) k_gbc_flat2<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
     else k_gbc_flat2<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
-  } else if (minb >= 4) k_gbc_flat<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  } else if (fast) k_gbc_flat<3, true><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  else if (minb >= 4) k_gbc_flat<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
   else if (minb == 3) k_gbc_flat<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
   else k_gbc_flat<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
   ++g_launches;

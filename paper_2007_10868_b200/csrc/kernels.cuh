@@ -157,6 +157,15 @@ __device__ __forceinline__ void madd_band(double w, double cl, double ch, double
   lo = __fma_rd(__dsub_rn(ul, dl), -0.5, sl);
   hi = __fma_ru(__dsub_rn(uh, dh), 0.5, sh);
 }
+// Fast numeric mode (pc_options.numeric_mode = 1): the interval
+// multiply-add as two directed-rounding FMAs, RD for the lower end and RU for
+// the upper — each the correctly rounded exact result, so sound (outward) but
+// not the reference's RN-then-step bits. Zero terms add exactly nothing.
+__device__ __forceinline__ void madd_dir(double w, double cl, double ch, double& lo, double& hi) {
+  const bool neg = __double2hiint(w) < 0;
+  lo = __fma_rd(neg ? ch : cl, w, lo);
+  hi = __fma_ru(neg ? cl : ch, w, hi);
+}
 // madd_band split into its accumulator-independent products and the two
 // accumulator steps, for kernels that schedule the products of several terms
 // ahead of the (latency-bound) sum chains.
@@ -314,25 +323,29 @@ void launch_init_margin_keys(cudaStream_t s, const RowsDev& rows, const int* lab
 // frozen (nullable): rows whose query neuron froze at an earlier checkpoint
 // are skipped — the reference has compacted them away by then (early
 // termination, backsub.hpp:1040-1054); their results are never read.
+// fast: the fast numeric mode (directed-rounding terms and folds) where the
+// long-row kernels run; every other path stays exact (also sound).
 void launch_chain_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                          const FrameDev& fin, MatDev m, double* Kout, const double* dev,
-                         Counters* ctr, const char* frozen);
+                         Counters* ctr, const char* frozen, bool fast = false);
 void launch_chain_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        double* Kout, const double* relax, const char* frozen);
 void launch_concretize(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                        const double* blo, const double* bhi, const double* rlo,
-                       const double* rhi, double* vals, double* rvals, const char* frozen);
+                       const double* rhi, double* vals, double* rvals, const char* frozen,
+                       bool fast = false);
 
 // Long-row variants (chains.cu): one CTA per row, producer warps compact the
 // contributing terms, one consumer warp folds them in order.
 void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                              const FrameDev& fin, MatDev m, double* Kout, const double* dev,
-                             Counters* ctr, const char* frozen);
+                             Counters* ctr, const char* frozen, bool fast = false);
 void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            double* Kout, const double* relax, const char* frozen);
 void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            const double* blo, const double* bhi, const double* rlo,
-                           const double* rhi, double* vals, double* rvals, const char* frozen);
+                           const double* rhi, double* vals, double* rvals, const char* frozen,
+                           bool fast = false);
 // Rows at least this long use the CTA-per-row chains (env PC_BIG_CHAIN_CELLS
 // overrides, read once; the tests force 1 to run the corpus through them).
 long long big_chain_cells();
@@ -386,7 +399,8 @@ void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const uns
                       int* pref, unsigned short* fpos, unsigned short* fch, int nimg, long long sst,
                       long long pst, long long fst);
 void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
-                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr);
+                     const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr,
+                     bool fast = false);
 // CTA-per-chain scan-fold kernels (chains.cu): the conv steps' constant
 // chains from the compacted coefficients (tmp: 5 doubles per row), the
 // checkpoints' concretisations.

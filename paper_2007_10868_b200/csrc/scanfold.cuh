@@ -152,6 +152,9 @@ __device__ __forceinline__ double scan_fold(double acc, int n, bool up, const Te
 // (d0, d1)[p]. A run of links composes as such a pair — A then B maps p to
 // A(p) + B(p ^ (A(p) & 1)) — and the composition is associative, so the warp
 // prefix-sums pairs instead of integers and ties stay inside the scan.
+// FAST: plain directed rounding (fast numeric mode): RD(M + T + f) = M + T,
+// RU = M + T + [f > 0]; no ties.
+template <bool FAST = false>
 __device__ __forceinline__ void scan_delta2(double t, double inv, bool up, bool& ok, long long& d0,
                                             long long& d1) {
   d0 = d1 = 0;
@@ -159,7 +162,8 @@ __device__ __forceinline__ void scan_delta2(double t, double inv, bool up, bool&
   const double y = t * inv;
   const double ay = fabs(y);
   if (ay < 0.25) {
-    d0 = d1 = up ? 1 : -1;
+    if (FAST) d0 = d1 = up ? (t > 0.0 ? 1 : 0) : (t < 0.0 ? -1 : 0);
+    else d0 = d1 = up ? 1 : -1;
     return;
   }
   if (!(ay < 0x1p60)) {
@@ -170,6 +174,10 @@ __device__ __forceinline__ void scan_delta2(double t, double inv, bool up, bool&
   const double T = floor(y);
   const double f = y - T;
   const long long Ti = __double2ll_rz(T);
+  if (FAST) {
+    d0 = d1 = Ti + ((up && f != 0.0) ? 1 : 0);
+    return;
+  }
   if (f == 0.5) {  // RN(m + T + 1/2) = the even one of m + T, m + T + 1
     const long long q = Ti & 1, base = Ti + (up ? 1 : -1);
     d0 = base + q;
@@ -180,6 +188,13 @@ __device__ __forceinline__ void scan_delta2(double t, double inv, bool up, bool&
   long long d = Ti;
   if (f != 0.0) d += up ? (f < 0.5 ? 1 : 2) : (f < 0.5 ? -1 : 0);
   d0 = d1 = d;
+}
+
+// One link as the scalar op of the mode.
+template <bool FAST>
+__device__ __forceinline__ double link_op(double acc, double t, bool up) {
+  if (FAST) return up ? __dadd_ru(acc, t) : __dadd_rd(acc, t);
+  return up ? add_up(acc, t) : add_down(acc, t);
 }
 
 // a then b, as parity-indexed pairs
@@ -194,7 +209,7 @@ __device__ __forceinline__ void scan_compose2(long long a0, long long a1, long l
 // The same fold, 4 links per lane (128 per warp step): lane l takes links
 // 4l .. 4l+3 of the group, composes them locally and scans the lane pairs
 // across the warp, so a step costs one warp scan for 128 links.
-template <class TermFn>
+template <class TermFn, bool FAST = false>
 __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const TermFn& term) {
   const int lane = threadIdx.x & 31;
   int base = 0;
@@ -212,7 +227,7 @@ __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const T
       }
       const int k = __ffs(has) - 1;
       const double t = __shfl_sync(0xffffffffu, tl, k);
-      acc = up ? add_up(acc, t) : add_down(acc, t);
+      acc = link_op<FAST>(acc, t, up);
       base += k + 1;
       if (lane == 0) scan_stat(3, 1);
       continue;
@@ -226,7 +241,7 @@ __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const T
     for (int k = 0; k < 4; ++k) {
       bool ok = true;
       long long d0 = 0, d1 = 0;
-      if (j0 + k < cnt) scan_delta2(term(base + j0 + k), inv, up, ok, d0, d1);
+      if (j0 + k < cnt) scan_delta2<FAST>(term(base + j0 + k), inv, up, ok, d0, d1);
       scan_compose2(r0, r1, d0, d1, r0, r1);
       p0[k] = r0;
       p1[k] = r1;
@@ -269,11 +284,16 @@ __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const T
     base += k;
     if (bad) {  // the link that left the scan's domain, as the scalar op
       const double t = term(base);
-      if (t == t) acc = up ? add_up(acc, t) : add_down(acc, t);
+      if (t == t) acc = link_op<FAST>(acc, t, up);
       ++base;
     }
   }
   return acc;
+}
+
+template <bool FAST, class TermFn>
+__device__ __forceinline__ double scan_fold4m(double acc, int n, bool up, const TermFn& term) {
+  return scan_fold4<TermFn, FAST>(acc, n, up, term);
 }
 
 // scan_fold4 over a contiguous term array in global memory, with the next
@@ -506,7 +526,7 @@ __device__ __forceinline__ double block_scan_fold(double acc, int n, bool up, co
 // the new frame, without reloading or recomputing terms. For long chains of
 // few rows, where one warp's step latency would be the critical path.
 // sm: at least 2*NT/32 + 8 long longs of shared memory.
-template <int NT, class TermFn>
+template <int NT, class TermFn, bool FAST = false>
 __device__ __forceinline__ double block_scan_fold_rt(double acc, int n, bool up, const TermFn& term,
                                                      long long* sm) {
   constexpr int NW = NT / 32, WIN = 4 * NT;
@@ -541,7 +561,7 @@ __device__ __forceinline__ double block_scan_fold_rt(double acc, int n, bool up,
         __syncthreads();
         if (f < WIN) {
           const double t = *s_t;
-          acc = up ? add_up(acc, t) : add_down(acc, t);
+          acc = link_op<FAST>(acc, t, up);
           lo = f + 1;
           if (tid == 0) scan_stat(3, 1);
         } else {
@@ -558,7 +578,7 @@ __device__ __forceinline__ double block_scan_fold_rt(double acc, int n, bool up,
         bool ok = true;
         long long d0 = 0, d1 = 0;
         const int j = j0 + k;
-        if (j >= lo && j < cnt) scan_delta2(tv[k], inv, up, ok, d0, d1);
+        if (j >= lo && j < cnt) scan_delta2<FAST>(tv[k], inv, up, ok, d0, d1);
         scan_compose2(r0, r1, d0, d1, r0, r1);
         p0[k] = r0;
         p1[k] = r1;
@@ -624,7 +644,7 @@ __device__ __forceinline__ double block_scan_fold_rt(double acc, int n, bool up,
       if (f > lo) acc = scan_compose(*s_m, ex);
       if (f < cnt) {  // the link that left the scan's domain, as the scalar op
         const double t = *s_t;
-        if (t == t) acc = up ? add_up(acc, t) : add_down(acc, t);
+        if (t == t) acc = link_op<FAST>(acc, t, up);
         lo = f + 1;
       } else {
         lo = cnt;
@@ -633,6 +653,12 @@ __device__ __forceinline__ double block_scan_fold_rt(double acc, int n, bool up,
     }
   }
   return acc;
+}
+
+template <int NT, bool FAST, class TermFn>
+__device__ __forceinline__ double block_scan_fold_rtm(double acc, int n, bool up, const TermFn& term,
+                                                      long long* sm) {
+  return block_scan_fold_rt<NT, TermFn, FAST>(acc, n, up, term, sm);
 }
 
 }  // namespace pc

@@ -27,6 +27,7 @@ class AnalysisOptions:  # analyzer.hpp:164-169
     memory_budget: int = 0  # 0: engine default (16 GiB of device workspace)
     device: int = -1
     exec_mode: int = 0  # 0 auto, 1 host-driven schedule, 2 device-driven (CUDA graph)
+    numeric_mode: int = 0  # 0 WidenedFloat64 bit for bit; 1 fast native directed rounding (sound)
 
 
 @dataclass
@@ -87,6 +88,7 @@ class Verifier:
         o.memory_budget = int(self.options.memory_budget)
         o.device = int(self.options.device)
         o.exec_mode = int(self.options.exec_mode)
+        o.numeric_mode = int(self.options.numeric_mode)
         descs = net.descs()
         h = ctypes.c_void_p()
         w, hh, c = net.input_shape
