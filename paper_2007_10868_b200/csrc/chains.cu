@@ -972,6 +972,7 @@ cudaError_t scan_stats_device_chains(int on, unsigned long long* out4) {
 void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows,
                              const FrameDev& fin, MatDev m, double* Kout, const double* dev,
                              Counters* ctr, const char* frozen, bool fast) {
+  if (debug_skip("folds")) return;
   double* tb;
   int* tc;
   long long ts;
@@ -1005,6 +1006,7 @@ void launch_chain_relu_big(cudaStream_t s, const RowsDev& rows, const FrameDev& 
 void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                            const double* blo, const double* bhi, const double* rlo,
                            const double* rhi, double* vals, double* rvals, const char* frozen, bool fast) {
+  if (debug_skip("folds")) return;
   double* tb;
   int* tc;
   long long ts;

@@ -236,7 +236,12 @@ struct Ctx {
   size_t sync_used = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  std::vector<std::pair<int, size_t>> prof;  // (class, event index of the begin event)
+  struct ProfEv {
+    int cls;
+    cudaStream_t st;
+    size_t b, e;  // begin / end event indices (e == SIZE_MAX while open)
+  };
+  std::vector<ProfEv> prof;  // PC_PROFILE: one entry per profiled launch group
   std::vector<size_t> dense_ev;               // begin events of dense-coefficient launches
   std::vector<size_t> conv_ev;                // begin events of conv-coefficient launches
 
@@ -401,7 +406,8 @@ thread_local double g_prof_ms[PROF_N];
 thread_local long long g_prof_n[PROF_N];
 thread_local double g_gap_ms[PROF_N];
 thread_local double g_gbc_window_madds = 0;
-thread_local std::string g_pass_json = "[]";  // PC_PROFILE: [[target, live rows, ms], ...], -1 = margin  // PC_PROFILE: madds of the conv steps if no coefficient were zero  // device idle (or unprofiled work) before each class
+thread_local std::string g_pass_json = "[]";
+thread_local std::string g_timeline_json = "[]";  // PC_PROFILE: [class, stream, start ms, end ms] per launch group  // PC_PROFILE: [[target, live rows, ms], ...], -1 = margin  // PC_PROFILE: madds of the conv steps if no coefficient were zero  // device idle (or unprofiled work) before each class
 
 cudaEvent_t take_event(Ctx* n) {
   while (n->ev_pool.size() <= n->ev_used) {
@@ -414,12 +420,19 @@ cudaEvent_t take_event(Ctx* n) {
 
 void prof_begin(Ctx* n, int cls, cudaStream_t st = nullptr) {
   if (!n->profile) return;
-  n->prof.emplace_back(cls, n->ev_used);
-  ck(cudaEventRecord(take_event(n), st ? st : n->stream), "event");
+  st = st ? st : n->stream;
+  n->prof.push_back(Ctx::ProfEv{cls, st, n->ev_used, SIZE_MAX});
+  ck(cudaEventRecord(take_event(n), st), "event");
 }
 void prof_end(Ctx* n, cudaStream_t st = nullptr) {
   if (!n->profile) return;
-  ck(cudaEventRecord(take_event(n), st ? st : n->stream), "event");
+  st = st ? st : n->stream;
+  for (size_t k = n->prof.size(); k-- > 0;)  // the open entry of this stream
+    if (n->prof[k].st == st && n->prof[k].e == SIZE_MAX) {
+      n->prof[k].e = n->ev_used;
+      break;
+    }
+  ck(cudaEventRecord(take_event(n), st), "event");
 }
 
 // Ordering between the coefficient stream and the constants stream.
@@ -2095,8 +2108,6 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     float ms = 0;
     cudaEventElapsedTime(&ms, t0, t1);
     g_total_ms = ms;
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
     for (size_t e : n->dense_ev) {
       float d = 0;
       if (cudaEventElapsedTime(&d, n->ev_pool[e], n->ev_pool[e + 1]) == cudaSuccess) g_dense_ms += d;
@@ -2114,18 +2125,25 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
       g_prof_n[c] = 0;
       g_gap_ms[c] = 0;
     }
+    g_timeline_json = "[";
     for (size_t k = 0; k < n->prof.size(); ++k) {
       const auto& pe = n->prof[k];
-      float d = 0;
-      cudaEventElapsedTime(&d, n->ev_pool[pe.second], n->ev_pool[pe.second + 1]);
-      g_prof_ms[pe.first] += d;
-      g_prof_n[pe.first] += 1;
-      if (k) {
-        float gap = 0;
-        cudaEventElapsedTime(&gap, n->ev_pool[n->prof[k - 1].second + 1], n->ev_pool[pe.second]);
-        g_gap_ms[pe.first] += gap;
-      }
+      if (pe.e == SIZE_MAX) continue;
+      float d = 0, t_b = 0, t_e = 0;
+      cudaEventElapsedTime(&d, n->ev_pool[pe.b], n->ev_pool[pe.e]);
+      g_prof_ms[pe.cls] += d;
+      g_prof_n[pe.cls] += 1;
+      // timeline: [class, stream (0 coefficients, 1 constants), start ms, end ms] from t0
+      cudaEventElapsedTime(&t_b, t0, n->ev_pool[pe.b]);
+      cudaEventElapsedTime(&t_e, t0, n->ev_pool[pe.e]);
+      char buf[96];
+      snprintf(buf, sizeof(buf), "%s[%d, %d, %.4f, %.4f]", g_timeline_json.size() > 1 ? ", " : "", pe.cls,
+               pe.st == n->stream ? 0 : 1, t_b, t_e);
+      g_timeline_json += buf;
     }
+    g_timeline_json += "]";
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
     if (label >= 0) {
       bool v = true;
       for (int r = 0; r < n->n_out - 1; ++r) {
@@ -2417,7 +2435,8 @@ int pc_last_profile(char* buf, int len) {
   }
   j += ", \"gbc_window_madds\": [0, " + std::to_string(g_gbc_window_madds) + "]";
   j += ", \"host_arena_alloc\": [" + std::to_string(g_allocs) + ", " + std::to_string(g_alloc_ms) + "]";
-  j += ", \"passes\": " + g_pass_json + "}";
+  j += ", \"passes\": " + g_pass_json;
+  j += ", \"timeline\": " + g_timeline_json + "}";
   if (buf && len > 0) {
     std::strncpy(buf, j.c_str(), len - 1);
     buf[len - 1] = 0;

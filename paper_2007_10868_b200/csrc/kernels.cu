@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "kernels.cuh"
 #include "numeric.cuh"
@@ -58,6 +59,14 @@ static bool use_big_chains(long long cells, const RowsDev& rows) {
 #define PC_NAN __longlong_as_double(0x7ff8000000000000ULL)
 
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+bool debug_skip(const char* what) {
+  static const std::string v = [] {
+    const char* e = getenv("PC_DEBUG_SKIP");
+    return std::string(e ? e : "");
+  }();
+  return !v.empty() && v.find(what) != std::string::npos;
+}
 
 // ===========================================================================
 // Forward interval propagation: affine_bound / compute_layer_bounds
@@ -515,6 +524,7 @@ void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, con
                           const long long* offs, const long long* pofs, int k, int p0, int p1,
                           double* dev, double* relax, int* gen_n, int* gen_pos, int* gen_l, int g,
                           int force, int nimg, long long zs, long long zp, int zl) {
+  if (debug_skip("forward")) return;
   const long long o = offs[k], a = offs[p0];
   double* ylo = const_cast<double*>(blo) + o;
   double* yhi = const_cast<double*>(bhi) + o;
@@ -2830,7 +2840,7 @@ void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const uns
 // cells). A block takes kFlatOPB consecutive live cells of its row's window:
 // the window's grid rows are consecutive runs of the flat list.
 constexpr int kFlatOPB = 512;
-template <int MINB, bool FAST = false>
+template <int MINB, bool FAST = false, int KB = 4, bool CHECKED = false>
 __global__ void __launch_bounds__(256, MINB)
     k_gbc_flat(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
                MatDev out, FlatDev fl, Counters* ctr) {
@@ -2866,6 +2876,10 @@ __global__ void __launch_bounds__(256, MINB)
   double* ohi = out.hi + (size_t)i * ocells;
   const int cin = L.in_c, cout = L.out_c;
   const bool band = FAST || products_in_band(in.stat, L.wmin, L.wmax);
+  // Two instantiations per launch: the band one (no call in its loop, so a
+  // lean register budget) returns when the operands are not proven in band,
+  // the CHECKED one only works in that (rare) case.
+  if (band == CHECKED) return;
   const int* cnt = sp.cnt + (size_t)i * sp.ncell;
   const size_t rbase = (size_t)i * sp.ncell * sp.C;
   MagAcc mag;
@@ -2877,7 +2891,7 @@ __global__ void __launch_bounds__(256, MINB)
     const int gp = fpos[e], ci = fch[e];
     const int iy = nbh + y, ix = gp - iy * fo.G_w;
     Iv acc;
-    if (!band) {
+    if (CHECKED) {
       acc = gbc_gather_checked(L, fi, bw, bh, ilo, ihi, iy, ix, ci);
     } else {
       int ah0 = floordiv(iy + L.ph - L.fh, L.sh) + 1, ah1 = floordiv(iy + L.ph, L.sh);
@@ -2896,7 +2910,7 @@ __global__ void __launch_bounds__(256, MINB)
           exec += n;
           const size_t sb = rbase + (size_t)cell * sp.C;
           const double* wp = L.FT + ((size_t)(fy * L.fw + fx) * cout) * cin + ci;
-          constexpr int kB = 4;
+          constexpr int kB = KB;
           int k = 0;
           for (; k + kB <= n; k += kB) {
             double cl[kB], ch[kB], w[kB];
@@ -3089,6 +3103,7 @@ __global__ void __launch_bounds__(256, MINB)
 void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr,
                      bool fast) {
+  if (debug_skip("conv")) return;
   static const int minb = env_int("PC_GBC_FLAT_MINB", 3);
   // dead cells: +0 (the live ones are overwritten)
   cudaMemsetAsync(out.lo, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
@@ -3096,14 +3111,23 @@ void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
   const long long cells = (long long)fout.S_w * fout.S_h * L.in_c;
   dim3 grid(cdiv(cells, kFlatOPB), rows.n);
   static const int pairs = env_int("PC_GBC_FLAT_PAIRS", 0);
+  static const int kb = env_int("PC_GBC_FLAT_KB", 4);
   static const int minb2 = env_int("PC_GBC_FLAT2_MINB", 2);
   if (pairs) {
     if (minb2 >= 3) k_gbc_flat2<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
     else k_gbc_flat2<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
-  } else if (fast) k_gbc_flat<3, true><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
-  else if (minb >= 4) k_gbc_flat<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
-  else if (minb == 3) k_gbc_flat<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
-  else k_gbc_flat<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  } else if (fast) {
+    k_gbc_flat<3, true><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+  } else {
+    if (kb == 2 && minb >= 4) k_gbc_flat<4, false, 2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    else if (kb == 2) k_gbc_flat<3, false, 2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    else if (kb == 8) k_gbc_flat<2, false, 8><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    else if (minb >= 4) k_gbc_flat<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    else if (minb == 3) k_gbc_flat<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    else k_gbc_flat<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    k_gbc_flat<2, false, 4, true><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    ++g_launches;
+  }
   ++g_launches;
 }
 
@@ -3439,6 +3463,7 @@ __global__ void __launch_bounds__(256)
 
 void launch_relu_coef(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev in,
                       MatDev out, const double* relax) {
+  if (debug_skip("relu")) return;
   unsigned gx = cdiv(in.cells, 256);
   if (gx > 1024) gx = 1024;
   dim3 grid(gx, rows.n);
@@ -3505,6 +3530,7 @@ __global__ void __launch_bounds__(256)
 
 void launch_merge(cudaStream_t s, const RowsDev& rows, const FrameDev& fa, const FrameDev& fb,
                   const FrameDev& fu, int dense_path, MatDev a, MatDev b, MatDev out, int part) {
+  if (debug_skip("merge")) return;
   unsigned gx = (part & 1) ? cdiv(out.cells, 256) : 1;
   if (gx > 1024) gx = 1024;
   dim3 grid(gx, rows.n);

@@ -287,6 +287,12 @@ struct Counters {  // device-side PassStats accumulators
   unsigned long long conv_exec;    // interval madds executed by k_gbc_live (live cells only)
 };
 
+// Timing ablation (PC_DEBUG_SKIP=conv,folds,relu,merge,forward): the named
+// kernels are not launched. Results are WRONG; only for attributing the
+// critical path (with early termination off the work does not depend on
+// the values). Never set in tests or the bench.
+bool debug_skip(const char* what);
+
 // ----- launchers (kernels.cu) -----
 // Forward bounds of layer k (padded + raw + dev + relaxation), skipping
 // neurons whose inputs did not change in refresh round g (force: all).

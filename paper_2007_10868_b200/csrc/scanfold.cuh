@@ -234,34 +234,74 @@ __device__ __forceinline__ double scan_fold4(double acc, int n, bool up, const T
     }
     const int cnt = min(128, n - base);
     const int j0 = 4 * lane;
-    long long p0[4], p1[4];  // lane-local inclusive pairs
-    int first = 4;           // first link of this lane that leaves the scan (4: none)
-    long long r0 = 0, r1 = 0;
+    // A run of links as (v, e): increment v for an incoming partial result of
+    // even parity, v + e for odd (the parity pair (v, v + e), scan_compose2);
+    // e is 0 except after ties and stays small. a then b:
+    //   v = a.v + b.v + [a.v odd] * b.e,   e = a.e odd ? a.e : a.e + (a.v odd ? -b.e : b.e)
+    long long pv[4];  // lane-local inclusive runs
+    int pe[4];
+    int first = 4;    // first link of this lane that leaves the scan (4: none)
+    long long rv = 0;
+    int re = 0;
+    bool small = true;  // every increment below 2^23: the warp scan runs in 32 bits
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       bool ok = true;
       long long d0 = 0, d1 = 0;
       if (j0 + k < cnt) scan_delta2<FAST>(term(base + j0 + k), inv, up, ok, d0, d1);
-      scan_compose2(r0, r1, d0, d1, r0, r1);
-      p0[k] = r0;
-      p1[k] = r1;
+      small &= (d0 < (1LL << 23)) & (d0 > -(1LL << 23));
+      const int de = (int)(d1 - d0);
+      const bool odd = rv & 1;
+      rv += d0 + (odd ? de : 0);
+      re = (re & 1) ? re : re + (odd ? -de : de);
+      pv[k] = rv;
+      pe[k] = re;
       if (!ok && j0 + k < cnt && first == 4) first = k;
     }
-    long long i0 = r0, i1 = r1;  // inclusive over lanes
+    long long xv;  // increments before this lane (even incoming parity), and their e
+    int xe;
+    if (__all_sync(0xffffffffu, small)) {
+      int iv = (int)rv, ie = re;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long u0 = __shfl_up_sync(0xffffffffu, i0, o), u1 = __shfl_up_sync(0xffffffffu, i1, o);
-      if (lane >= o) scan_compose2(u0, u1, i0, i1, i0, i1);
+      for (int o = 1; o < 32; o <<= 1) {
+        const int uv = __shfl_up_sync(0xffffffffu, iv, o), ue = __shfl_up_sync(0xffffffffu, ie, o);
+        if (lane >= o) {
+          const bool odd = uv & 1;
+          const int nv = uv + iv + (odd ? ie : 0);
+          ie = (ue & 1) ? ue : ue + (odd ? -ie : ie);
+          iv = nv;
+        }
+      }
+      int ev = __shfl_up_sync(0xffffffffu, iv, 1), ee = __shfl_up_sync(0xffffffffu, ie, 1);
+      if (lane == 0) ev = ee = 0;
+      xv = ev;
+      xe = ee;
+    } else {
+      long long iv = rv;
+      int ie = re;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long uv = __shfl_up_sync(0xffffffffu, iv, o);
+        const int ue = __shfl_up_sync(0xffffffffu, ie, o);
+        if (lane >= o) {
+          const bool odd = uv & 1;
+          const long long nv = uv + iv + (odd ? ie : 0);
+          ie = (ue & 1) ? ue : ue + (odd ? -ie : ie);
+          iv = nv;
+        }
+      }
+      long long ev = __shfl_up_sync(0xffffffffu, iv, 1);
+      int ee = __shfl_up_sync(0xffffffffu, ie, 1);
+      if (lane == 0) ev = ee = 0;
+      xv = ev;
+      xe = ee;
     }
-    long long e0 = __shfl_up_sync(0xffffffffu, i0, 1), e1 = __shfl_up_sync(0xffffffffu, i1, 1);
-    if (lane == 0) e0 = e1 = 0;
-    const int pin = (int)(M & 1);
-    const long long P = pin ? e1 : e0;            // increments before this lane
-    const int pl = (int)((M + P) & 1);            // parity entering this lane
+    const long long P = xv + ((M & 1) ? xe : 0);  // increments before this lane, from M's parity
+    const bool pl = (M + P) & 1;                   // parity entering this lane
     long long mk[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      mk[k] = M + P + (pl ? p1[k] : p0[k]);
+      mk[k] = M + P + pv[k] + (pl ? pe[k] : 0);
       const long long am = mk[k] < 0 ? -mk[k] : mk[k];
       if (k < first && j0 + k < cnt && !(((mk[k] < 0) == (M < 0)) && am >= kScanLo && am <= kScanHi)) first = k;
     }

@@ -1,0 +1,69 @@
+"""Where the time of one verification goes, from the PC_PROFILE timeline
+(one walk pipeline, its two streams): busy time of each kernel class, of the
+coefficient stream (s) and the constants stream (s2), their overlap and the
+time neither runs (host round trips, launch gaps).
+usage: PC_PIPES=1 python scripts/timeline.py CONFIG"""
+import json
+import os
+import sys
+
+os.environ["PC_PROFILE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2007_10868_b200 as pc  # noqa: E402
+from paper_2007_10868_b200.configs import CONFIGS, INPUT_SEED, MODEL_SEED  # noqa: E402
+
+NAMES = None
+
+
+def union(iv):
+    iv = sorted(iv)
+    tot, cur = 0.0, None
+    for a, b in iv:
+        if cur is None or a > cur[1]:
+            if cur:
+                tot += cur[1] - cur[0]
+            cur = [a, b]
+        else:
+            cur[1] = max(cur[1], b)
+    if cur:
+        tot += cur[1] - cur[0]
+    return tot
+
+
+def intersect(a_iv, b_iv, grid=0.005):
+    # busy-both time on a fine grid (ms)
+    end = max([b for _, b in a_iv + b_iv] + [0])
+    n = int(end / grid) + 2
+    A = np.zeros(n, bool)
+    B = np.zeros(n, bool)
+    for s, e in a_iv:
+        A[int(s / grid):int(e / grid) + 1] = True
+    for s, e in b_iv:
+        B[int(s / grid):int(e / grid) + 1] = True
+    return float((A & B).sum() * grid), float((~A & ~B).sum() * grid)
+
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cifar_resnet34"
+arch, eps_s = CONFIGS[name]
+net = pc.generate(MODEL_SEED, arch)
+v = pc.Verifier(net)
+X = pc.random_inputs(INPUT_SEED, 2, int(np.prod(net.input_shape)))
+for i, x in enumerate(X):
+    v.verify_robustness(pc.input_box(x, float(eps_s)), max(v.candidate(x), 0))
+prof = v.last_profile()
+t = v.last_timing()
+tl = prof["timeline"]
+classes = [k for k in prof if not k.startswith("gap:") and k not in ("timeline", "passes", "gbc_window_madds", "host_arena_alloc")]
+s0 = [(a, b) for c, st, a, b in tl if st == 0]
+s1 = [(a, b) for c, st, a, b in tl if st == 1]
+both, idle = intersect(s0, s1)
+out = {"config": name, "total_ms": t["total_ms"], "s_busy_ms": union(s0), "s2_busy_ms": union(s1),
+       "both_busy_ms": both, "neither_busy_ms": idle,
+       "class_busy_ms": {}}
+for ci, cname in enumerate(classes):
+    iv = [(a, b) for c, st, a, b in tl if c == ci]
+    if iv:
+        out["class_busy_ms"][cname] = round(union(iv), 2)
+print(json.dumps(out))

@@ -25,7 +25,7 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 # long-row chains run (smaller layers take the exact kernels, also sound)
 FAST_ARCHS = [
     "input 6x6x2; conv 3x3x32 s1 p1; relu; conv 3x3x32 s1 p1; relu; dense 4",
-    "input 8x8x1; conv 3x3x32 s1 p1; relu; block(conv 3x3x32 s1 p1; relu; conv 3x3x32 s1 p1 | skip); relu; dense 3",
+    "input 6x6x1; conv 3x3x32 s1 p1; relu; block(conv 3x3x32 s1 p1; relu; conv 3x3x32 s1 p1 | skip); relu; dense 3",
     "input 8x8x1; conv 3x3x32 s1 p1; relu; block(conv 4x4x32 s2 p1; relu; conv 3x3x32 s1 p1 | conv 2x2x32 s2 p0); relu; dense 3",
 ]
 
@@ -46,7 +46,7 @@ def test_fast_mode_contains_exact_rational(pc, ref, arch):
     net = pc.generate(31, arch)
     h = _ref_model(ref, net)
     v = pc.Verifier(net, pc.AnalysisOptions(numeric_mode=1, early_term=False))
-    X = pc.random_inputs(32, 2, int(np.prod(net.input_shape)))
+    X = pc.random_inputs(32, 1, int(np.prod(net.input_shape)))  # exact rationals: ~5-30 s per box
     for num, den in [(1, 64), (1, 16)]:
         for x in X:
             lab = max(v.candidate(x), 0)
