@@ -914,6 +914,149 @@ static int block_fold_rows() {
   return v;
 }
 
+// ---------------------------------------------------------------------------
+// Predicted compaction. Early termination drops a row once a checkpoint's
+// exact raw concretisation freezes it, and the next step waits for that
+// decision. The decision only needs the sign of the raw value, and the
+// reference's chain lies provably close to a plain parallel sum: with
+// B = |K| + sum |t_j| over the n terms, every add_up / add_down link moves
+// the partial result by its exact sum plus at most 2 ulp outward, so the
+// chain value v satisfies
+//   add_up:   K + sum t <= v <= K + sum t + 3 n 2^-52 B
+//   add_down: K + sum t - 3 n 2^-52 B <= v <= K + sum t
+// and a round-to-nearest parallel sum S is within 1.01 n 2^-53 B of
+// K + sum t. So with E = 4 (n + 2) 2^-52 B (rounded up), S + E <= 0 proves
+// the row's raw upper value is <= 0 and S - E >= 0 its raw lower value >= 0
+// (per link at most 2.5 ulp of the exact partial sum: RN's half ulp plus one
+// step, which can be twice as wide across a binade boundary; ulps never drop
+// below 2^-1074, so E also carries that absolute floor per link):
+// the row certainly freezes at this checkpoint (backsub.hpp:814-817). Such
+// rows are dropped before the next step without waiting for the exact folds;
+// rows not proven (vanishingly rare) simply stay in the walk until the exact
+// offers freeze them, which costs work but never changes a result. The exact
+// concretisations and offers (candidates, freeze flags, counters) still run,
+// on a third stream, off the critical path.
+constexpr int kPT = 256;
+constexpr int kPredScan = 1024;  // threads of the predicted-offer scan
+__global__ void __launch_bounds__(kPT)
+    k_pred_terms(RowsDev rows, FrameDev f, MatDev m, const double* rlo, const double* rhi, double* part,
+                 int ntiles, const char* frozen) {
+  __shared__ double s_red[3][kPT / 32];
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  double S = 0.0, A = 0.0, N = 0.0;
+  if (!(frozen && frozen[(size_t)img * rows.kq + q])) {
+    const long long so = img * rows.sst;
+    int bw, bh;
+    frame_base(f, q, bw, bh);
+    const size_t pr = phys_row(m, i);
+    const double* lo = m.lo + pr * m.cells;
+    const double* hi = m.hi + pr * m.cells;
+    const long long c0 = (long long)blockIdx.x * (kPT * 4);
+    for (int k = 0; k < 4; ++k) {
+      const long long cell = c0 + (long long)k * kPT + threadIdx.x;
+      if (cell >= m.cells) break;
+      const Iv c{lo[cell], hi[cell]};
+      if (iv_zero(c)) continue;
+      int d, aw, ah;
+      cell_pos(f, cell, bw, bh, d, aw, ah);
+      const long long j = ((long long)ah * f.G_w + aw) * f.C + d;
+      const Iv Br{rlo[so + j], rhi[so + j]};
+      const double t = upper ? corner_hi(c, Br) : corner_lo(c, Br);
+      S += t;
+      A += fabs(t);
+      N += 1.0;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    S += __shfl_down_sync(0xffffffffu, S, o);
+    A += __shfl_down_sync(0xffffffffu, A, o);
+    N += __shfl_down_sync(0xffffffffu, N, o);
+  }
+  if (lane == 0) {
+    s_red[0][warp] = S;
+    s_red[1][warp] = A;
+    s_red[2][warp] = N;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0, a = 0.0, nn = 0.0;
+    for (int w = 0; w < kPT / 32; ++w) {
+      s += s_red[0][w];
+      a += s_red[1][w];
+      nn += s_red[2][w];
+    }
+    double* P = part + ((size_t)i * ntiles + blockIdx.x) * 3;
+    P[0] = s;
+    P[1] = a;
+    P[2] = nn;
+  }
+}
+
+// The predicted offers: certain freezes dropped, the survivors' row map,
+// query list and count written like k_offer's (stable order).
+__global__ void __launch_bounds__(kPredScan)
+    k_pred_offer(RowsDev rows, int R, MatDev m, const double* part, int ntiles, const char* frozen,
+                 int* map, int* new_R, int* new_row_q) {
+  using Scan = cub::BlockScan<int, kPredScan>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  auto certain = [&](int row, bool upper) {
+    const double* K = m.K + 4 * phys_row(m, row);
+    const double k0 = upper ? K[3] : K[2];  // kraw.hi / kraw.lo
+    double S = k0, A = fabs(k0), N = 0.0;
+    for (int t = 0; t < ntiles; ++t) {
+      const double* P = part + ((size_t)row * ntiles + t) * 3;
+      S += P[0];
+      A += P[1];
+      N += P[2];
+    }
+    if (!(fabs(S) < 1e300) || !(A < 1e300)) return false;
+    const double B = __dmul_ru(A, 1.0 + 0x1p-30);
+    // 2.5 ulp per outward link + the parallel sum's error, relative to B,
+    // plus an absolute ulp floor per link for the subnormal range
+    const double E = __dmul_ru(4.0 * (N + 2.0), __dadd_ru(__dmul_ru(0x1p-52, B), 0x1p-1074));
+    return upper ? (__dadd_ru(S, E) <= 0.0) : (__dadd_rd(S, -E) >= 0.0);
+  };
+  for (int start = 0; start < R; start += kPredScan) {
+    const int r = start + threadIdx.x;
+    int keep = 0, q = 0;
+    if (r < R) {
+      q = rows.row_q[r];
+      const bool gone = (frozen && frozen[q]) || certain(r, true) || certain(R + r, false);
+      keep = !gone;
+    }
+    int pos, total;
+    Scan(tmp).ExclusiveSum(keep, pos, total);
+    if (keep) {
+      map[s_base + pos] = r;
+      new_row_q[s_base + pos] = q;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += total;
+    __syncthreads();
+  }
+  const int nR = s_base;
+  for (int p = threadIdx.x; p < nR; p += blockDim.x) map[nR + p] = R + map[p];  // lower rows
+  if (threadIdx.x == 0) *new_R = nR;
+}
+
+void launch_pred_offer(cudaStream_t s, const RowsDev& rows, int R, const FrameDev& f, MatDev m,
+                       const double* rlo, const double* rhi, const char* frozen, int* map, int* new_R,
+                       int* new_row_q) {
+  const int ntiles = (int)((m.cells + kPT * 4 - 1) / (kPT * 4));
+  double* part = static_cast<double*>(stream_scratch(s, (size_t)rows.n * ntiles * 3 * sizeof(double)));
+  k_pred_terms<<<dim3(ntiles, rows.n), kPT, 0, s>>>(rows, f, m, rlo, rhi, part, ntiles, frozen);
+  k_pred_offer<<<1, kPredScan, 0, s>>>(rows, R, m, part, ntiles, frozen, map, new_R, new_row_q);
+  g_launches += 2;
+}
+
 static void set_attrs_split() {
   cudaFuncSetAttribute(k_affine_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(5 * 2 * kTTile * sizeof(double)));

@@ -173,6 +173,8 @@ struct Ctx {
   long long budget = 0;  // workspace bytes for one pass (0: derive)
   cudaStream_t stream = nullptr;   // coefficient stream (and everything outside a walk)
   cudaStream_t stream2 = nullptr;  // constants / concretisation / offers of a walk
+  cudaStream_t stream3 = nullptr;  // exact concretisations + offers behind predicted compaction
+  int *xmap = nullptr, *xq = nullptr;  // the exact offers' (unused) compaction outputs there
   std::vector<void*> owned;
   int* gen_n = nullptr;
   int* gen_pos = nullptr;
@@ -193,10 +195,11 @@ struct Ctx {
   // device-driven walks (graph mode): label, per-checkpoint live-row counts,
   // a second row-map buffer, and the captured whole-analysis graph
   // compaction ring of the host-driven schedule (Walker::checkpoint)
-  static constexpr int kRing = 4;
+  static constexpr int kRing = 8;
   int* ring_map[kRing] = {};
   int* ring_q[kRing] = {};
   int* d_ringR = nullptr;
+  cudaEvent_t ring_ev[kRing] = {};  // s3 work that last read a ring slot's rows / map
   double* ckat = nullptr;  // per live row: the checkpoint that froze it (k_ck_count)
   int* lv_cnt = nullptr;             // live channels per grid position of each ReLU layer
   unsigned short* lv_idx = nullptr;  // (k_live_build; read by the conv kernel k_gbc_live)
@@ -263,6 +266,7 @@ struct Ctx {
     nimg = n_images;
     ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&stream3, cudaStreamNonBlocking), "stream");
     const int nl = (int)L.size();
     const size_t T = (size_t)total * nimg, M = (size_t)max_numel * nimg;
     blo = dalloc<double>(T);
@@ -299,6 +303,8 @@ struct Ctx {
     }
     d_ringR = dalloc<int>(kRing);
     ckat = dalloc<double>(M);
+    xmap = dalloc<int>(2 * M);
+    xq = dalloc<int>(M);
     lv_cnt = dalloc<int>((size_t)pofs[nl] * nimg);
     lv_idx = dalloc<unsigned short>(T);
     un_idx = dalloc<int>(T);
@@ -311,12 +317,14 @@ struct Ctx {
     d_slots = dalloc<int>(kSlots);
     perm2 = dalloc<int>(2 * M);
     for (int k = 0; k < kCkSlots; ++k) ck(cudaEventCreateWithFlags(&ck_ev[k], cudaEventDisableTiming), "event");
+    for (int k = 0; k < kRing; ++k) ck(cudaEventCreateWithFlags(&ring_ev[k], cudaEventDisableTiming), "event");
   }
 
   ~Ctx() {
     delete helper;
     if (stream) cudaStreamSynchronize(stream);
     if (stream2) cudaStreamSynchronize(stream2);
+    if (stream3) cudaStreamSynchronize(stream3);
     for (void* p : owned) cudaFree(p);
     if (arena) cudaFree(arena);
     if (stats) cudaFree(stats);
@@ -327,10 +335,13 @@ struct Ctx {
     if (h_newR) cudaFreeHost(h_newR);
     for (cudaEvent_t e : ck_ev)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ring_ev)
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : sync_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (stream2) cudaStreamDestroy(stream2);
+    if (stream3) cudaStreamDestroy(stream3);
   }
 };
 
@@ -645,6 +656,7 @@ struct Walker {
   bool allow_freeze = false, early_term = true, margin = false;
   pc_stats* st = nullptr;
   cudaStream_t s2 = nullptr;
+  cudaStream_t s3 = nullptr;  // set: predicted compaction, exact checkpoint work on s3
   // device-driven walk (graph mode): R is the launch bound; the live count is
   // read by the kernels from dR, which each checkpoint's offers advance
   bool devr = false;
@@ -730,7 +742,8 @@ struct Walker {
       arena_take((size_t)alloc_rows() * 4 * sizeof(double));
       return nullptr;
     }
-    return m.src ? arena_take((size_t)nrows() * 4 * sizeof(double)) : m.K;
+    // never in place when checkpoints lag on s3: they still read m.K
+    return (m.src || s3) ? arena_take((size_t)nrows() * 4 * sizeof(double)) : m.K;
   }
 
   // m's coefficients are complete (recorded on s after their producer).
@@ -944,6 +957,40 @@ struct Walker {
                         n->bhi + o, n->vals, n->rvals, nullptr, fast());
       prof_end(n, s2);
       launch_margin_offer(s2, R, n->vals, n->best, n->has);
+      return;
+    }
+    // Predicted compaction (launch_pred_offer): the survivors of this
+    // checkpoint come from a parallel sum with a proven error bound, on s2
+    // right behind the constants; the exact concretisations and offers run on
+    // s3, off the path the next step waits for.
+    static const int predict = env_int("PC_PREDICT", 1);
+    const bool pred = predict && s3 && s3 != s2 && !devr && allow_freeze && early_term;
+    if (pred) {
+      int slot = free_slot();
+      if (slot < 0) {
+        resolve(m, 0);
+        slot = free_slot();
+      }
+      // the exact work on s3 may still read this slot's rows / map from an
+      // earlier generation
+      ck(cudaStreamWaitEvent(s2, n->ring_ev[slot], 0), "wait");
+      prof_begin(n, PROF_OFFER, s2);
+      launch_pred_offer(s2, rows(), R, fdev(n, m.f, q), md(m), n->rlo + o, n->rhi + o, n->frozen,
+                        n->ring_map[slot], n->d_ringR + slot, n->ring_q[slot]);
+      prof_end(n, s2);
+      const int ckx = ck_next;
+      ck_next = (ck_next + 1) % Ctx::kCkSlots;
+      ck(cudaMemcpyAsync(n->h_newR + ckx, n->d_ringR + slot, sizeof(int), cudaMemcpyDeviceToHost, s2), "d2h");
+      ck(cudaEventRecord(n->ck_ev[ckx], s2), "event");
+      pend.push_back(Pending{ckx, slot, gen});
+      stream_wait(n, s3, s2);  // M and K of this checkpoint
+      prof_begin(n, PROF_CONC, s3);
+      launch_concretize(s3, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
+                        n->rhi + o, n->vals, n->rvals, fz(), fast());
+      prof_end(n, s3);
+      launch_offer(s3, rows(), R, n->vals, n->rvals, n->cand, n->frozen, 1, 1, n->xmap, n->d_int + 3, n->xq,
+                   n->ctr, n->ckat, ck_index);
+      if (cur_slot >= 0) ck(cudaEventRecord(n->ring_ev[cur_slot], s3), "event");  // s3 read that slot
       return;
     }
     prof_begin(n, PROF_CONC, s2);
@@ -1409,6 +1456,7 @@ void start_chunk(Ctx* c, ChunkWalk& cw, int t, bool affine, long long base, int 
   reset_stats(c, ws.stats);
   Walker& w = cw.w;
   w.s2 = c->net->serial ? c->stream : c->stream2;
+  w.s3 = c->net->serial ? c->stream : c->stream3;
   w.R = R;
   w.both = true;
   w.allow_freeze = allow_freeze;
@@ -1534,8 +1582,10 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
           if (!moved) (a.running ? a : b).w.wait_ready();
         }
         stream_wait(n, s, n->stream2);
+        stream_wait(n, s, n->stream3);
         stream_wait(n, s, h->stream);
         stream_wait(n, s, h->stream2);
+        stream_wait(n, s, h->stream3);
         stream_wait(n, h->stream, s);  // h's next chunk reuses its arena after s
         continue;
       }
@@ -1543,6 +1593,7 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
       start_chunk(n, a, t, affine, base, R, allow_freeze, et, st, ws);
       a.w.walk(a.m, 0, true);
       stream_wait(n, s, n->stream2);  // the next chunk reuses the arena and row lists
+      stream_wait(n, s, n->stream3);
     }
   }
   if (W > 1 && n_live > 0) {

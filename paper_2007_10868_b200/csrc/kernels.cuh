@@ -416,6 +416,13 @@ void launch_chain_affine_scan(cudaStream_t s, const LayerDev& L, const RowsDev& 
 void launch_concretize_scan(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m,
                             const double* blo, const double* bhi, const double* rlo, const double* rhi,
                             double* vals, double* rvals, const char* frozen);
+// Predicted compaction (chains.cu): rows whose raw concretisation provably
+// freezes them at this checkpoint (parallel sum + rigorous bound on the
+// reference chain's distance from it) are dropped; map / new_R / new_row_q
+// like launch_offer's.
+void launch_pred_offer(cudaStream_t s, const RowsDev& rows, int R, const FrameDev& f, MatDev m,
+                       const double* rlo, const double* rhi, const char* frozen, int* map, int* new_R,
+                       int* new_row_q);
 // Dense-tile conv over the row's nonzero input channels x the layer's
 // live-anywhere output channels (needs sp.dmask; chmask per image, 16 words).
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,

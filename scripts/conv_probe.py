@@ -17,7 +17,8 @@ arch, eps_s = CONFIGS[name]
 net = pc.generate(MODEL_SEED, arch)
 v = pc.Verifier(net)
 X = pc.random_inputs(INPUT_SEED, 2, int(np.prod(net.input_shape)))
-for serial in ((True,) if os.environ.get("PROBE_SERIAL_ONLY") else (False, True)):
+modes = (True,) if os.environ.get("PROBE_SERIAL_ONLY") else (False,) if os.environ.get("PROBE_CONC_ONLY") else (False, True)
+for serial in modes:
     v.set_serial(serial)
     for i, x in enumerate(X):
         box = pc.input_box(x, float(eps_s))

@@ -32,6 +32,7 @@ for i, x in enumerate(X):
     prof = v.last_profile()
     win = prof.pop("gbc_window_madds", [0, 0])[1]
     passes = prof.pop("passes", [])
+    prof.pop("timeline", None)
     prof.pop("host_arena_alloc", None)
     tot = sum(ms for k, (_, ms) in prof.items() if not k.startswith("gap:"))
     print(json.dumps({"config": name, "image": i, "verified": verdict.verified, "wall_ms": round(wall, 2),
