@@ -1007,7 +1007,9 @@ __global__ void __launch_bounds__(kPredScan)
   __shared__ int s_base;
   if (threadIdx.x == 0) s_base = 0;
   __syncthreads();
-  auto certain = [&](int row, bool upper) {
+  // +1: the raw value is proven to freeze the row (upper <= 0 / lower >= 0),
+  // -1: proven not to, 0: undecided
+  auto decide = [&](int row, bool upper) {
     const double* K = m.K + 4 * phys_row(m, row);
     const double k0 = upper ? K[3] : K[2];  // kraw.hi / kraw.lo
     double S = k0, A = fabs(k0), N = 0.0;
@@ -1017,19 +1019,28 @@ __global__ void __launch_bounds__(kPredScan)
       A += P[1];
       N += P[2];
     }
-    if (!(fabs(S) < 1e300) || !(A < 1e300)) return false;
+    if (!(fabs(S) < 1e300) || !(A < 1e300)) return 0;
     const double B = __dmul_ru(A, 1.0 + 0x1p-30);
     // 2.5 ulp per outward link + the parallel sum's error, relative to B,
     // plus an absolute ulp floor per link for the subnormal range
     const double E = __dmul_ru(4.0 * (N + 2.0), __dadd_ru(__dmul_ru(0x1p-52, B), 0x1p-1074));
-    return upper ? (__dadd_ru(S, E) <= 0.0) : (__dadd_rd(S, -E) >= 0.0);
+    const double up = __dadd_ru(S, E), dn = __dadd_rd(S, -E);
+    if (upper) return up <= 0.0 ? 1 : dn > 0.0 ? -1 : 0;
+    return dn >= 0.0 ? 1 : up < 0.0 ? -1 : 0;
   };
+  int undecided = 0;
   for (int start = 0; start < R; start += kPredScan) {
     const int r = start + threadIdx.x;
     int keep = 0, q = 0;
     if (r < R) {
       q = rows.row_q[r];
-      const bool gone = (frozen && frozen[q]) || certain(r, true) || certain(R + r, false);
+      bool gone = frozen && frozen[q];
+      if (!gone) {
+        const int a = decide(r, true);
+        const int b = a == 1 ? 1 : decide(R + r, false);
+        gone = a == 1 || b == 1;
+        undecided |= !gone && (a == 0 || b == 0);
+      }
       keep = !gone;
     }
     int pos, total;
@@ -1044,7 +1055,10 @@ __global__ void __launch_bounds__(kPredScan)
   }
   const int nR = s_base;
   for (int p = threadIdx.x; p < nR; p += blockDim.x) map[nR + p] = R + map[p];  // lower rows
-  if (threadIdx.x == 0) *new_R = nR;
+  // an undecided row may still freeze in the exact offers: -(nR + 1) tells
+  // the host to order the next step's counters behind them
+  undecided = __syncthreads_or(undecided);
+  if (threadIdx.x == 0) *new_R = undecided ? -(nR + 1) : nR;
 }
 
 void launch_pred_offer(cudaStream_t s, const RowsDev& rows, int R, const FrameDev& f, MatDev m,
@@ -1070,7 +1084,12 @@ static bool split_chains(cudaStream_t s, long long cells, int nrows, int na, dou
     const char* e = getenv("PC_SPLIT_CHAINS");
     return e && *e ? atoi(e) : 1;
   }();
-  if (!on) return false;
+  // rows shorter than a few tiles fold faster in one CTA-per-row kernel
+  static const long long min_cells = [] {
+    const char* e = getenv("PC_SPLIT_MIN_CELLS");
+    return e && *e ? atoll(e) : 1024ll;
+  }();
+  if (!on || cells < min_cells) return false;
   *ntiles = (int)((cells + kTTile - 1) / kTTile);
   *tstride = (long long)*ntiles * kTTile;
   const size_t tb_bytes = (size_t)nrows * na * (size_t)*tstride * sizeof(double);

@@ -964,7 +964,13 @@ struct Walker {
     // right behind the constants; the exact concretisations and offers run on
     // s3, off the path the next step waits for.
     static const int predict = env_int("PC_PREDICT", 1);
-    const bool pred = predict && s3 && s3 != s2 && !devr && allow_freeze && early_term;
+    // (eager schedule only: lazy / lagged walks leave frozen rows in place,
+    // whose counters must then see the exact freezes in stream order)
+    static const int lazy_all = env_int("PC_LAZY_COMPACT", 0);
+    static const int lazy_rows = env_int("PC_LAZY_ROWS", 0);
+    static const int lag_rows = env_int("PC_LAG_ROWS", 0);
+    const bool pred = predict && s3 && s3 != s2 && !devr && allow_freeze && early_term && !lazy_all &&
+                      R > lazy_rows && R > lag_rows;
     if (pred) {
       int slot = free_slot();
       if (slot < 0) {
@@ -1070,8 +1076,15 @@ struct Walker {
     }
   }
   void apply(Mat& m, const Pending& p) {
+    int newR = n->h_newR[p.ck];
+    if (newR < 0) {
+      // a predicted offer left rows undecided: the exact offers (s3) may
+      // still freeze them, and the next step's counting kernels (s2) must
+      // see those freezes, as after the reference's compaction
+      newR = -newR - 1;
+      stream_wait(n, s2, s3);
+    }
     if (p.gen != gen) return;
-    const int newR = n->h_newR[p.ck];
     if (newR >= R) return;
     m.src = n->ring_map[p.slot];
     row_q = n->ring_q[p.slot];
@@ -1752,7 +1765,9 @@ void forward_layers(Ctx* n, int k0, int k1, int nimg = 1) {
     if (l.kind == KIND_RELU)
       launch_offset_list(n->stream, (int)l.numel(), n->relax + 8 * n->off[l.pred0], n->un_idx + n->off[l.pred0],
                          n->un_cnt + l.pred0, nimg, T, nl);
-    if (l.kind == KIND_RELU && n->net->live_cells) {
+    bool feeds_conv = false;  // the live tables serve the conv steps onto this frame (gbc_step)
+    for (const HostLayer& c : n->L) feeds_conv |= c.kind == KIND_CONV && c.pred0 == k;
+    if (l.kind == KIND_RELU && n->net->live_cells && feeds_conv) {
       const long long o = n->off[k];
       launch_live_build(n->stream, l.out_w * l.out_h, l.out_c, n->relax + 8 * n->off[l.pred0], n->blo + o,
                         n->bhi + o, n->rlo + o, n->rhi + o, n->lv_cnt + n->pofs[k], n->lv_idx + o, nimg,
