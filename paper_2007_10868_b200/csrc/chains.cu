@@ -1000,8 +1000,8 @@ __global__ void __launch_bounds__(kPT)
 // The predicted offers: certain freezes dropped, the survivors' row map,
 // query list and count written like k_offer's (stable order).
 __global__ void __launch_bounds__(kPredScan)
-    k_pred_offer(RowsDev rows, int R, MatDev m, const double* part, int ntiles, const char* frozen,
-                 int* map, int* new_R, int* new_row_q) {
+    k_pred_offer(RowsDev rows, int R, MatDev m, const double* P, const double* part, int ntiles,
+                 const char* frozen, int* map, int* new_R, int* new_row_q) {
   using Scan = cub::BlockScan<int, kPredScan>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
@@ -1010,9 +1010,15 @@ __global__ void __launch_bounds__(kPredScan)
   // +1: the raw value is proven to freeze the row (upper <= 0 / lower >= 0),
   // -1: proven not to, 0: undecided
   auto decide = [&](int row, bool upper) {
-    const double* K = m.K + 4 * phys_row(m, row);
-    const double k0 = upper ? K[3] : K[2];  // kraw.hi / kraw.lo
-    double S = k0, A = fabs(k0), N = 0.0;
+    double k0, pe = 0.0;
+    if (P) {  // predicted raw constant and its error radius (k_pk_*)
+      k0 = P[2 * phys_row(m, row)];
+      pe = P[2 * phys_row(m, row) + 1];
+    } else {
+      const double* K = m.K + 4 * phys_row(m, row);
+      k0 = upper ? K[3] : K[2];  // kraw.hi / kraw.lo
+    }
+    double S = k0, A = __dadd_ru(fabs(k0), pe), N = 0.0;
     for (int t = 0; t < ntiles; ++t) {
       const double* P = part + ((size_t)row * ntiles + t) * 3;
       S += P[0];
@@ -1023,7 +1029,8 @@ __global__ void __launch_bounds__(kPredScan)
     const double B = __dmul_ru(A, 1.0 + 0x1p-30);
     // 2.5 ulp per outward link + the parallel sum's error, relative to B,
     // plus an absolute ulp floor per link for the subnormal range
-    const double E = __dmul_ru(4.0 * (N + 2.0), __dadd_ru(__dmul_ru(0x1p-52, B), 0x1p-1074));
+    const double E = __dadd_ru(pe, __dmul_ru(4.0 * (N + 2.0), __dadd_ru(__dmul_ru(0x1p-52, B), 0x1p-1074)));
+    if (!(E < 1e300)) return 0;
     const double up = __dadd_ru(S, E), dn = __dadd_rd(S, -E);
     if (upper) return up <= 0.0 ? 1 : dn > 0.0 ? -1 : 0;
     return dn >= 0.0 ? 1 : up < 0.0 ? -1 : 0;
@@ -1062,13 +1069,239 @@ __global__ void __launch_bounds__(kPredScan)
 }
 
 void launch_pred_offer(cudaStream_t s, const RowsDev& rows, int R, const FrameDev& f, MatDev m,
-                       const double* rlo, const double* rhi, const char* frozen, int* map, int* new_R,
-                       int* new_row_q) {
+                       const double* P, const double* rlo, const double* rhi, const char* frozen, int* map,
+                       int* new_R, int* new_row_q) {
   const int ntiles = (int)((m.cells + kPT * 4 - 1) / (kPT * 4));
   double* part = static_cast<double*>(stream_scratch(s, (size_t)rows.n * ntiles * 3 * sizeof(double)));
   k_pred_terms<<<dim3(ntiles, rows.n), kPT, 0, s>>>(rows, f, m, rlo, rhi, part, ntiles, frozen);
-  k_pred_offer<<<1, kPredScan, 0, s>>>(rows, R, m, part, ntiles, frozen, map, new_R, new_row_q);
+  k_pred_offer<<<1, kPredScan, 0, s>>>(rows, R, m, P, part, ntiles, frozen, map, new_R, new_row_q);
   g_launches += 2;
+}
+
+// ---------------------------------------------------------------------------
+// Predicted raw constants. The predicted offers need each row's raw constant
+// (kraw.hi of an upper row, kraw.lo of a lower one), which the serial chain
+// folds produce last. To keep the coefficient stream from waiting on them,
+// a prediction stream carries P = (S, E) per row through the walk: a
+// parallel sum S of the same terms the chain adds and a radius E with
+// |exact chain value - S| <= E. Each step with n terms t_j (the affine
+// step's bias products, the relu step's offset products, a join's branch
+// constant) widens it, with B = |S_in| + E_in + sum |t_j| bounding every
+// partial result of the chain, by the bound of k_pred_offer:
+//   E_out = E_in + 4 (n + 2) (2^-52 B + 2^-1074).
+// Rows are never skipped here (a row frozen by the exact offers may still
+// sit in the map; its prediction stays valid).
+__device__ __forceinline__ void pk_widen(const double* Pin, double S, double A, double N, double* Pout) {
+  const double ps = Pin ? Pin[0] : 0.0, pe = Pin ? Pin[1] : 0.0;
+  const double s = ps + S;
+  const double B = __dmul_ru(__dadd_ru(__dadd_ru(fabs(ps), pe), A), 1.0 + 0x1p-30);
+  const double e = __dadd_ru(pe, __dmul_ru(4.0 * (N + 2.0), __dadd_ru(__dmul_ru(0x1p-52, B), 0x1p-1074)));
+  const bool ok = fabs(s) < 1e300 && e < 1e300 && N < 0x1p22;
+  Pout[0] = ok ? s : 0.0;
+  Pout[1] = ok ? e : INFINITY;
+}
+
+template <int NT>
+__device__ __forceinline__ void block_sum3(double& S, double& A, double& N, double (*red)[NT / 32]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    S += __shfl_down_sync(0xffffffffu, S, o);
+    A += __shfl_down_sync(0xffffffffu, A, o);
+    N += __shfl_down_sync(0xffffffffu, N, o);
+  }
+  if (lane == 0) {
+    red[0][warp] = S;
+    red[1][warp] = A;
+    red[2][warp] = N;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S = A = N = 0.0;
+    for (int w = 0; w < NT / 32; ++w) {
+      S += red[0][w];
+      A += red[1][w];
+      N += red[2][w];
+    }
+  }
+}
+
+// affine step (dense_step / gbc_step constants, backsub.hpp:375-392, 469-486):
+// raw track terms iv_mul_scalar(c, bias).hi (upper rows) / .lo (lower rows)
+__global__ void __launch_bounds__(kPT)
+    k_pk_affine_terms(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, double* part, int ntiles) {
+  __shared__ double s_red[3][kPT / 32];
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const size_t pr = phys_row(m, i);
+  const double* lo = m.lo + pr * m.cells;
+  const double* hi = m.hi + pr * m.cells;
+  double S = 0.0, A = 0.0, N = 0.0;
+  const long long c0 = (long long)blockIdx.x * (kPT * 4);
+  for (int k = 0; k < 4; ++k) {
+    const long long cell = c0 + (long long)k * kPT + threadIdx.x;
+    if (cell >= m.cells) break;
+    const Iv c{lo[cell], hi[cell]};
+    if (iv_zero(c)) continue;
+    double b;
+    if (is_conv) {
+      int d, aw, ah;
+      cell_pos(f, cell, bw, bh, d, aw, ah);
+      b = L.bias[d];
+    } else {
+      b = L.bias[cell];
+    }
+    const Iv bt = iv_mul_scalar(c, b);
+    if (iv_zero(bt)) continue;
+    const double t = upper ? bt.hi : bt.lo;
+    S += t;
+    A += fabs(t);
+    N += 1.0;
+  }
+  block_sum3<kPT>(S, A, N, s_red);
+  if (threadIdx.x == 0) {
+    double* Pp = part + ((size_t)i * ntiles + blockIdx.x) * 3;
+    Pp[0] = S;
+    Pp[1] = A;
+    Pp[2] = N;
+  }
+}
+
+__global__ void k_pk_affine_fin(RowsDev rows, MatDev m, const double* Pin, const double* part, int ntiles,
+                                double* Pout) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows.n) return;
+  double S = 0.0, A = 0.0, N = 0.0;
+  for (int t = 0; t < ntiles; ++t) {
+    const double* Pp = part + ((size_t)i * ntiles + t) * 3;
+    S += Pp[0];
+    A += Pp[1];
+    N += Pp[2];
+  }
+  pk_widen(Pin + 2 * phys_row(m, i), S, A, N, Pout + 2 * (size_t)i);
+}
+
+void launch_pk_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows, const FrameDev& f,
+                      MatDev m, const double* Pin, double* Pout) {
+  const int ntiles = (int)((m.cells + kPT * 4 - 1) / (kPT * 4));
+  double* part = static_cast<double*>(stream_scratch(s, (size_t)rows.n * ntiles * 3 * sizeof(double)));
+  k_pk_affine_terms<<<dim3(ntiles, rows.n), kPT, 0, s>>>(L, is_conv ? 1 : 0, rows, f, m, part, ntiles);
+  k_pk_affine_fin<<<(rows.n + 127) / 128, 128, 0, s>>>(rows, m, Pin, part, ntiles, Pout);
+  g_launches += 2;
+}
+
+// relu step (backsub.hpp:536-563) over the layer's offset list, like
+// k_chain_relu_list: raw track terms o0 then o1 (.hi upper / .lo lower)
+constexpr int kPkWarps = 4;
+__global__ void __launch_bounds__(32 * kPkWarps)
+    k_pk_relu(RowsDev rows, FrameDev f, MatDev m, const double* Pin, double* Pout, const double* relax,
+              const int* list, const int* count, int cstride) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * kPkWarps + warp, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  relax += 8 * img * rows.sst;
+  list += img * rows.sst;
+  const int n = count[img * cstride];
+  int bw, bh;
+  frame_base(f, q, bw, bh);
+  const size_t pr = phys_row(m, i);
+  const double* lo = m.lo + pr * m.cells;
+  const double* hi = m.hi + pr * m.cells;
+  const int GC = f.G_w * f.C;
+  double S = 0.0, A = 0.0, N = 0.0;
+  for (int e = lane; e < n; e += 32) {
+    const int j = list[e];
+    const int ah = j / GC, rem = j - ah * GC;
+    const int aw = rem / f.C, d = rem - aw * f.C;
+    const int x = aw - bw, y = ah - bh;
+    if (x < 0 || x >= f.S_w || y < 0 || y >= f.S_h) continue;
+    const long long cell = ((long long)y * f.S_w + x) * f.C + d;
+    const Iv c{lo[cell], hi[cell]};
+    if (iv_zero(c)) continue;
+    const double* R = relax + 8 * (long long)j;
+    const Iv beta{R[2], R[3]}, delta{R[6], R[7]};
+    const Iv op = upper ? delta : beta;
+    const Iv on = upper ? beta : delta;
+    Iv o0{0.0, 0.0}, o1{0.0, 0.0};
+    if (!(c.lo < 0.0)) o0 = iv_mul(c, op);
+    else if (!(c.hi > 0.0)) o0 = iv_mul(c, on);
+    else {
+      o0 = iv_mul(iv_pos_part(c), op);
+      o1 = iv_mul(iv_neg_part(c), on);
+    }
+    if (!iv_zero(o0)) {
+      const double t = upper ? o0.hi : o0.lo;
+      S += t;
+      A += fabs(t);
+      N += 1.0;
+    }
+    if (!iv_zero(o1)) {
+      const double t = upper ? o1.hi : o1.lo;
+      S += t;
+      A += fabs(t);
+      N += 1.0;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    S += __shfl_down_sync(0xffffffffu, S, o);
+    A += __shfl_down_sync(0xffffffffu, A, o);
+    N += __shfl_down_sync(0xffffffffu, N, o);
+  }
+  if (lane == 0) pk_widen(Pin + 2 * pr, S, A, N, Pout + 2 * (size_t)i);
+}
+
+void launch_pk_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m, const double* Pin,
+                    double* Pout, const double* relax, const int* list, const int* count, int cstride) {
+  k_pk_relu<<<(rows.n + kPkWarps - 1) / kPkWarps, 32 * kPkWarps, 0, s>>>(rows, f, m, Pin, Pout, relax, list,
+                                                                       count, cstride);
+  ++g_launches;
+}
+
+// join (align_add, backsub.hpp:610-688): one link, branch a's constant plus b's
+__global__ void k_pk_merge(RowsDev rows, MatDev a, const double* Pa, MatDev b, const double* Pb, double* Pout) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows.n) return;
+  const double* pb = Pb + 2 * phys_row(b, i);
+  double* po = Pout + 2 * (size_t)i;
+  pk_widen(Pa + 2 * phys_row(a, i), pb[0], __dadd_ru(fabs(pb[0]), pb[1]), 1.0, po);
+  po[1] = __dadd_ru(po[1], pb[1]);
+  if (!(po[1] < 1e300)) {
+    po[0] = 0.0;
+    po[1] = INFINITY;
+  }
+}
+
+void launch_pk_merge(cudaStream_t s, const RowsDev& rows, MatDev a, const double* Pa, MatDev b, const double* Pb,
+                     double* Pout) {
+  k_pk_merge<<<(rows.n + 127) / 128, 128, 0, s>>>(rows, a, Pa, b, Pb, Pout);
+  ++g_launches;
+}
+
+// a walk's first rows: the exact constants, radius 0
+__global__ void k_pk_init(RowsDev rows, MatDev m, double* Pout) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows.n) return;
+  bool upper;
+  int img;
+  row_query(rows, i, upper, img);
+  const double* K = m.K + 4 * phys_row(m, i);
+  const double k = upper ? K[3] : K[2];
+  double* po = Pout + 2 * (size_t)phys_row(m, i);
+  const bool ok = fabs(k) < 1e300;
+  po[0] = ok ? k : 0.0;
+  po[1] = ok ? 0.0 : INFINITY;
+}
+
+void launch_pk_init(cudaStream_t s, const RowsDev& rows, MatDev m, double* P) {
+  k_pk_init<<<(rows.n + 127) / 128, 128, 0, s>>>(rows, m, P);
+  ++g_launches;
 }
 
 static void set_attrs_split() {

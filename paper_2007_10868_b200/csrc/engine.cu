@@ -102,6 +102,7 @@ struct Mat {
   double* lo = nullptr;
   double* hi = nullptr;
   double* K = nullptr;
+  double* P = nullptr;  // predicted raw constants (S, E) per physical row (Walker::pk)
   long long cells = 0;
   Frame f;
   const int* src = nullptr;  // row map after a compaction (see MatDev::src)
@@ -174,6 +175,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;   // coefficient stream (and everything outside a walk)
   cudaStream_t stream2 = nullptr;  // constants / concretisation / offers of a walk
   cudaStream_t stream3 = nullptr;  // exact concretisations + offers behind predicted compaction
+  cudaStream_t stream4 = nullptr;  // predicted raw constants + predicted offers
   int *xmap = nullptr, *xq = nullptr;  // the exact offers' (unused) compaction outputs there
   std::vector<void*> owned;
   int* gen_n = nullptr;
@@ -267,6 +269,7 @@ struct Ctx {
     ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&stream3, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&stream4, cudaStreamNonBlocking), "stream");
     const int nl = (int)L.size();
     const size_t T = (size_t)total * nimg, M = (size_t)max_numel * nimg;
     blo = dalloc<double>(T);
@@ -325,6 +328,7 @@ struct Ctx {
     if (stream) cudaStreamSynchronize(stream);
     if (stream2) cudaStreamSynchronize(stream2);
     if (stream3) cudaStreamSynchronize(stream3);
+    if (stream4) cudaStreamSynchronize(stream4);
     for (void* p : owned) cudaFree(p);
     if (arena) cudaFree(arena);
     if (stats) cudaFree(stats);
@@ -342,6 +346,7 @@ struct Ctx {
     if (stream) cudaStreamDestroy(stream);
     if (stream2) cudaStreamDestroy(stream2);
     if (stream3) cudaStreamDestroy(stream3);
+    if (stream4) cudaStreamDestroy(stream4);
   }
 };
 
@@ -409,10 +414,10 @@ namespace {
 
 enum ProfClass { PROF_FWD, PROF_SEED, PROF_INIT, PROF_CHAIN_AFFINE, PROF_DENSE, PROF_GBC,
                  PROF_CHAIN_RELU, PROF_RELU, PROF_MERGE, PROF_CONC, PROF_OFFER, PROF_WRITEBACK,
-                 PROF_N };
+                 PROF_PREDICT, PROF_N };
 const char* kProfNames[PROF_N] = {"forward", "seed", "init", "chain_affine", "dense_coef",
                                   "gbc_coef", "chain_relu", "relu_coef", "merge", "concretize",
-                                  "offer", "writeback"};
+                                  "offer", "writeback", "predict"};
 thread_local double g_prof_ms[PROF_N];
 thread_local long long g_prof_n[PROF_N];
 thread_local double g_gap_ms[PROF_N];
@@ -657,6 +662,7 @@ struct Walker {
   pc_stats* st = nullptr;
   cudaStream_t s2 = nullptr;
   cudaStream_t s3 = nullptr;  // set: predicted compaction, exact checkpoint work on s3
+  cudaStream_t s4 = nullptr;  // predicted raw constants and offers (pk())
   // device-driven walk (graph mode): R is the launch bound; the live count is
   // read by the kernels from dR, which each checkpoint's offers advance
   bool devr = false;
@@ -756,10 +762,43 @@ struct Walker {
     if (m.ready) ck(cudaStreamWaitEvent(s2, m.ready, 0), "wait");
   }
 
+  // Predicted compaction (checkpoint): PC_PREDICT=1 carries predicted raw
+  // constants on s4 (launch_pk_*), so the predicted offers never wait for
+  // the serial constant folds; PC_PREDICT=2 predicts from the exact
+  // constants on s2. Eager schedule only: lazy / lagged walks leave frozen
+  // rows in place, whose counters must then see the exact freezes in
+  // stream order.
+  int predict_mode() const {
+    static const int predict = env_int("PC_PREDICT", 1);
+    static const int lazy_all = env_int("PC_LAZY_COMPACT", 0);
+    static const int lazy_rows = env_int("PC_LAZY_ROWS", 0);
+    static const int lag_rows = env_int("PC_LAG_ROWS", 0);
+    if (dry || !predict || !s3 || s3 == s2 || devr || margin || !allow_freeze || !early_term || lazy_all ||
+        lazy_rows || lag_rows)
+      return 0;
+    return predict == 1 && s4 && s4 != s2 ? 1 : 2;
+  }
+  bool pk() const { return predict_mode() == 1; }
+  // P of a step's output (taken in the dry run too, so the arena fits it)
+  double* p_take() {
+    if (dry) return arena_take((size_t)alloc_rows() * 2 * sizeof(double));
+    return pk() ? arena_take((size_t)nrows() * 2 * sizeof(double)) : nullptr;
+  }
+  void need4(const Mat& m) {
+    if (m.ready) ck(cudaStreamWaitEvent(s4, m.ready, 0), "wait");
+  }
+
   void dense_step(Mat& m) {  // backsub.hpp:343-399
     const HostLayer& L = n->L[m.f.layer];
     Mat out = alloc(dense_frame(L.pred0), false);
     out.K = k_out(m);
+    out.P = p_take();
+    if (!dry && pk()) {
+      need4(m);
+      prof_begin(n, PROF_PREDICT, s4);
+      launch_pk_affine(s4, L.d, false, rows(), fdev(n, m.f, q), md(m), m.P, out.P);
+      prof_end(n, s4);
+    }
     if (!dry) {
       need(m);
       prof_begin(n, PROF_CHAIN_AFFINE, s2);
@@ -799,6 +838,13 @@ struct Walker {
     }
     Mat out = alloc(nf, false);
     out.K = k_out(m);
+    out.P = p_take();
+    if (!dry && pk()) {
+      need4(m);
+      prof_begin(n, PROF_PREDICT, s4);
+      launch_pk_affine(s4, L.d, true, rows(), fdev(n, m.f, q), md(m), m.P, out.P);
+      prof_end(n, s4);
+    }
     // compacted nonzero input coefficients for the sparse conv kernel
     const bool sparse = gbc_sparse_wanted(L.d);
     SparseDev sp{};
@@ -884,6 +930,14 @@ struct Walker {
     nf.layer = L.pred0;
     Mat out = alloc(nf, false);
     out.K = k_out(m);
+    out.P = p_take();
+    if (!dry && pk()) {
+      need4(m);
+      prof_begin(n, PROF_PREDICT, s4);
+      launch_pk_relu(s4, rows(), fdev(n, m.f, q), md(m), m.P, out.P, n->relax + 8 * n->off[L.pred0],
+                     n->un_idx + n->off[L.pred0], n->un_cnt + L.pred0, (int)n->L.size());
+      prof_end(n, s4);
+    }
     if (!dry) {
       const FrameDev f = fdev(n, m.f, q);
       const double* rx = n->relax + 8 * n->off[L.pred0];
@@ -912,6 +966,8 @@ struct Walker {
     // branch b starts from zero constants, laid out like m's rows
     b.K = arena_take((size_t)(dry ? alloc_rows() : m.phys) * 4 * sizeof(double));
     if (!dry) ck(cudaMemsetAsync(b.K, 0, (size_t)m.phys * 4 * sizeof(double), s2), "memset");
+    b.P = (dry || pk()) ? arena_take((size_t)(dry ? alloc_rows() : m.phys) * 2 * sizeof(double)) : nullptr;
+    if (!dry && pk()) ck(cudaMemsetAsync(b.P, 0, (size_t)m.phys * 2 * sizeof(double), s4), "memset");
     walk(a, L.head, false);
     walk(b, L.head, false);
     // align_add (backsub.hpp:610-688): union frame
@@ -932,6 +988,8 @@ struct Walker {
       u.Wh = std::max(a.f.Ah + a.f.Wh, b.f.Ah + b.f.Wh) - u.Ah;
     }
     Mat out = alloc(u, true);
+    out.P = p_take();
+    if (!dry && pk()) launch_pk_merge(s4, rows(), md(a), a.P, md(b), b.P, out.P);
     if (!dry) {
       const FrameDev fa = fdev(n, a.f, q), fb = fdev(n, b.f, q), fu = fdev(n, u, q);
       prof_begin(n, PROF_MERGE);
@@ -960,34 +1018,30 @@ struct Walker {
       return;
     }
     // Predicted compaction (launch_pred_offer): the survivors of this
-    // checkpoint come from a parallel sum with a proven error bound, on s2
-    // right behind the constants; the exact concretisations and offers run on
-    // s3, off the path the next step waits for.
-    static const int predict = env_int("PC_PREDICT", 1);
-    // (eager schedule only: lazy / lagged walks leave frozen rows in place,
-    // whose counters must then see the exact freezes in stream order)
-    static const int lazy_all = env_int("PC_LAZY_COMPACT", 0);
-    static const int lazy_rows = env_int("PC_LAZY_ROWS", 0);
-    static const int lag_rows = env_int("PC_LAG_ROWS", 0);
-    const bool pred = predict && s3 && s3 != s2 && !devr && allow_freeze && early_term && !lazy_all &&
-                      R > lazy_rows && R > lag_rows;
-    if (pred) {
+    // checkpoint come from a parallel sum with a proven error bound, on s4
+    // from the predicted raw constants (or on s2 right behind the exact
+    // ones); the exact concretisations and offers run on s3, off the path the
+    // next step waits for.
+    const int pmode = predict_mode();
+    if (pmode) {
       int slot = free_slot();
       if (slot < 0) {
         resolve(m, 0);
         slot = free_slot();
       }
+      cudaStream_t sp = pmode == 1 ? s4 : s2;
       // the exact work on s3 may still read this slot's rows / map from an
       // earlier generation
-      ck(cudaStreamWaitEvent(s2, n->ring_ev[slot], 0), "wait");
-      prof_begin(n, PROF_OFFER, s2);
-      launch_pred_offer(s2, rows(), R, fdev(n, m.f, q), md(m), n->rlo + o, n->rhi + o, n->frozen,
-                        n->ring_map[slot], n->d_ringR + slot, n->ring_q[slot]);
-      prof_end(n, s2);
+      ck(cudaStreamWaitEvent(sp, n->ring_ev[slot], 0), "wait");
+      if (pmode == 1) need4(m);
+      prof_begin(n, PROF_OFFER, sp);
+      launch_pred_offer(sp, rows(), R, fdev(n, m.f, q), md(m), pmode == 1 ? m.P : nullptr, n->rlo + o,
+                        n->rhi + o, n->frozen, n->ring_map[slot], n->d_ringR + slot, n->ring_q[slot]);
+      prof_end(n, sp);
       const int ckx = ck_next;
       ck_next = (ck_next + 1) % Ctx::kCkSlots;
-      ck(cudaMemcpyAsync(n->h_newR + ckx, n->d_ringR + slot, sizeof(int), cudaMemcpyDeviceToHost, s2), "d2h");
-      ck(cudaEventRecord(n->ck_ev[ckx], s2), "event");
+      ck(cudaMemcpyAsync(n->h_newR + ckx, n->d_ringR + slot, sizeof(int), cudaMemcpyDeviceToHost, sp), "d2h");
+      ck(cudaEventRecord(n->ck_ev[ckx], sp), "event");
       pend.push_back(Pending{ckx, slot, gen});
       stream_wait(n, s3, s2);  // M and K of this checkpoint
       prof_begin(n, PROF_CONC, s3);
@@ -1053,12 +1107,20 @@ struct Walker {
     pend.push_back(Pending{ckx, slot, gen});
   }
 
-  int free_slot() const {
-    for (int k = 0; k < Ctx::kRing; ++k) {
+  // Round robin: a reused slot was last read kRing checkpoints ago, so the
+  // wait on its ring event (the exact offers behind the serial folds) has
+  // long completed.
+  int slot_rr = 0;
+  int free_slot() {
+    for (int u = 0; u < Ctx::kRing; ++u) {
+      const int k = (slot_rr + u) % Ctx::kRing;
       if (k == cur_slot) continue;
       bool used = false;
       for (const Pending& p : pend) used |= p.slot == k;
-      if (!used) return k;
+      if (!used) {
+        slot_rr = (k + 1) % Ctx::kRing;
+        return k;
+      }
     }
     return -1;
   }
@@ -1335,6 +1397,7 @@ WalkSize walk_size(Ctx* n, int t, bool affine, bool both) {
   pc_stats dummy{};
   w.st = &dummy;
   Mat m = w.alloc(initial_frame(n, t, affine), true);
+  m.P = w.p_take();
   w.walk(m, 0, false);
   return WalkSize{w.dry_peak, w.dry_allocs, w.dry_stats};
 }
@@ -1470,6 +1533,7 @@ void start_chunk(Ctx* c, ChunkWalk& cw, int t, bool affine, long long base, int 
   Walker& w = cw.w;
   w.s2 = c->net->serial ? c->stream : c->stream2;
   w.s3 = c->net->serial ? c->stream : c->stream3;
+  w.s4 = c->net->serial ? c->stream : c->stream4;
   w.R = R;
   w.both = true;
   w.allow_freeze = allow_freeze;
@@ -1485,6 +1549,11 @@ void start_chunk(Ctx* c, ChunkWalk& cw, int t, bool affine, long long base, int 
   else
     launch_init_identity(s, w.rows(), fdev(c, f0, t), md(cw.m));
   w.mark(cw.m);
+  cw.m.P = w.p_take();
+  if (w.pk()) {
+    w.need4(cw.m);
+    launch_pk_init(w.s4, w.rows(), md(cw.m), cw.m.P);
+  }
   if (affine) w.checkpoint(cw.m);  // the init itself is an affine step (:1056)
 }
 
@@ -1596,9 +1665,11 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
         }
         stream_wait(n, s, n->stream2);
         stream_wait(n, s, n->stream3);
+        stream_wait(n, s, n->stream4);
         stream_wait(n, s, h->stream);
         stream_wait(n, s, h->stream2);
         stream_wait(n, s, h->stream3);
+        stream_wait(n, s, h->stream4);
         stream_wait(n, h->stream, s);  // h's next chunk reuses its arena after s
         continue;
       }
@@ -1607,6 +1678,7 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
       a.w.walk(a.m, 0, true);
       stream_wait(n, s, n->stream2);  // the next chunk reuses the arena and row lists
       stream_wait(n, s, n->stream3);
+      stream_wait(n, s, n->stream4);
     }
   }
   if (W > 1 && n_live > 0) {
@@ -2199,12 +2271,13 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
       cudaEventElapsedTime(&d, n->ev_pool[pe.b], n->ev_pool[pe.e]);
       g_prof_ms[pe.cls] += d;
       g_prof_n[pe.cls] += 1;
-      // timeline: [class, stream (0 coefficients, 1 constants), start ms, end ms] from t0
+      // timeline: [class, stream (0 coefficients, 1 constants, 2 exact checkpoints,
+      // 3 predictions), start ms, end ms] from t0
       cudaEventElapsedTime(&t_b, t0, n->ev_pool[pe.b]);
       cudaEventElapsedTime(&t_e, t0, n->ev_pool[pe.e]);
       char buf[96];
       snprintf(buf, sizeof(buf), "%s[%d, %d, %.4f, %.4f]", g_timeline_json.size() > 1 ? ", " : "", pe.cls,
-               pe.st == n->stream ? 0 : 1, t_b, t_e);
+               pe.st == n->stream ? 0 : pe.st == n->stream2 ? 1 : pe.st == n->stream3 ? 2 : 3, t_b, t_e);
       g_timeline_json += buf;
     }
     g_timeline_json += "]";

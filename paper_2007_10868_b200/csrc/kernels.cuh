@@ -420,9 +420,19 @@ void launch_concretize_scan(cudaStream_t s, const RowsDev& rows, const FrameDev&
 // freezes them at this checkpoint (parallel sum + rigorous bound on the
 // reference chain's distance from it) are dropped; map / new_R / new_row_q
 // like launch_offer's.
+// P (nullable): the predicted raw constants (S, E) per physical row, else m.K.
 void launch_pred_offer(cudaStream_t s, const RowsDev& rows, int R, const FrameDev& f, MatDev m,
-                       const double* rlo, const double* rhi, const char* frozen, int* map, int* new_R,
-                       int* new_row_q);
+                       const double* P, const double* rlo, const double* rhi, const char* frozen, int* map,
+                       int* new_R, int* new_row_q);
+// Predicted raw constants (chains.cu): (S, E) per row, |chain value - S| <= E;
+// Pin read through the input matrix's row map, Pout compact.
+void launch_pk_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows, const FrameDev& f,
+                      MatDev m, const double* Pin, double* Pout);
+void launch_pk_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatDev m, const double* Pin,
+                    double* Pout, const double* relax, const int* list, const int* count, int cstride);
+void launch_pk_merge(cudaStream_t s, const RowsDev& rows, MatDev a, const double* Pa, MatDev b, const double* Pb,
+                     double* Pout);
+void launch_pk_init(cudaStream_t s, const RowsDev& rows, MatDev m, double* P);
 // Dense-tile conv over the row's nonzero input channels x the layer's
 // live-anywhere output channels (needs sp.dmask; chmask per image, 16 words).
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,

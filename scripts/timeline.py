@@ -1,6 +1,7 @@
 """Where the time of one verification goes, from the PC_PROFILE timeline
 (one walk pipeline, its two streams): busy time of each kernel class, of the
-coefficient stream (s) and the constants stream (s2), their overlap and the
+coefficient stream (s), the constants stream (s2), the exact checkpoint
+stream (s3) and the prediction stream (s4), the overlap of s and s2 and the
 time neither runs (host round trips, launch gaps).
 usage: PC_PIPES=1 python scripts/timeline.py CONFIG"""
 import json
@@ -58,9 +59,12 @@ tl = prof["timeline"]
 classes = [k for k in prof if not k.startswith("gap:") and k not in ("timeline", "passes", "gbc_window_madds", "host_arena_alloc")]
 s0 = [(a, b) for c, st, a, b in tl if st == 0]
 s1 = [(a, b) for c, st, a, b in tl if st == 1]
+s3 = [(a, b) for c, st, a, b in tl if st == 2]
+s4 = [(a, b) for c, st, a, b in tl if st == 3]
 both, idle = intersect(s0, s1)
 out = {"config": name, "total_ms": t["total_ms"], "s_busy_ms": union(s0), "s2_busy_ms": union(s1),
-       "both_busy_ms": both, "neither_busy_ms": idle,
+       "s3_busy_ms": union(s3), "s4_busy_ms": union(s4),
+       "both_busy_ms": both, "neither_busy_ms": idle, "s_idle_ms": t["total_ms"] - union(s0),
        "class_busy_ms": {}}
 for ci, cname in enumerate(classes):
     iv = [(a, b) for c, st, a, b in tl if c == ci]
