@@ -998,57 +998,86 @@ __global__ void __launch_bounds__(kPT)
 }
 
 // The predicted offers: certain freezes dropped, the survivors' row map,
-// query list and count written like k_offer's (stable order).
+// query list and count written like k_offer's (stable order). Phase 1: a
+// warp per row pair (upper r, lower R + r) sums the partials and decides;
+// phase 2: block scan over the decisions (dynamic shared memory: one flag
+// per row of the launch bound).
+__device__ __forceinline__ int pred_decide(double S, double A, double N, double k0, double pe, bool upper) {
+  S += k0;
+  A = __dadd_ru(A, __dadd_ru(fabs(k0), pe));
+  if (!(fabs(S) < 1e300) || !(A < 1e300)) return 0;
+  const double B = __dmul_ru(A, 1.0 + 0x1p-30);
+  // 2.5 ulp per outward link + the parallel sum's error, relative to B,
+  // plus an absolute ulp floor per link for the subnormal range
+  const double E = __dadd_ru(pe, __dmul_ru(4.0 * (N + 2.0), __dadd_ru(__dmul_ru(0x1p-52, B), 0x1p-1074)));
+  if (!(E < 1e300)) return 0;
+  const double up = __dadd_ru(S, E), dn = __dadd_rd(S, -E);
+  // +1: the raw value is proven to freeze the row (upper <= 0 / lower >= 0),
+  // -1: proven not to, 0: undecided
+  if (upper) return up <= 0.0 ? 1 : dn > 0.0 ? -1 : 0;
+  return dn >= 0.0 ? 1 : up < 0.0 ? -1 : 0;
+}
+
 __global__ void __launch_bounds__(kPredScan)
     k_pred_offer(RowsDev rows, int R, MatDev m, const double* P, const double* part, int ntiles,
                  const char* frozen, int* map, int* new_R, int* new_row_q) {
   using Scan = cub::BlockScan<int, kPredScan>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_base;
+  extern __shared__ unsigned char s_keep[];
+  if (rows.dR) R = *rows.dR;  // device-applied compaction: the live rows of this checkpoint
   if (threadIdx.x == 0) s_base = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = warp; r < R; r += kPredScan / 32) {
+    const int q = rows.row_q[r];
+    if (frozen && frozen[q]) {
+      if (lane == 0) s_keep[r] = 0;
+      continue;
+    }
+    double S0 = 0.0, A0 = 0.0, N0 = 0.0, S1 = 0.0, A1 = 0.0, N1 = 0.0;
+    for (int t = lane; t < ntiles; t += 32) {
+      const double* p0 = part + ((size_t)r * ntiles + t) * 3;
+      const double* p1 = part + ((size_t)(R + r) * ntiles + t) * 3;
+      S0 += p0[0];
+      A0 += p0[1];
+      N0 += p0[2];
+      S1 += p1[0];
+      A1 += p1[1];
+      N1 += p1[2];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      S0 += __shfl_down_sync(0xffffffffu, S0, o);
+      A0 += __shfl_down_sync(0xffffffffu, A0, o);
+      N0 += __shfl_down_sync(0xffffffffu, N0, o);
+      S1 += __shfl_down_sync(0xffffffffu, S1, o);
+      A1 += __shfl_down_sync(0xffffffffu, A1, o);
+      N1 += __shfl_down_sync(0xffffffffu, N1, o);
+    }
+    if (lane == 0) {
+      double k0, e0 = 0.0, k1, e1 = 0.0;
+      if (P) {  // predicted raw constants and their error radii (k_pk_*)
+        k0 = P[2 * phys_row(m, r)];
+        e0 = P[2 * phys_row(m, r) + 1];
+        k1 = P[2 * phys_row(m, R + r)];
+        e1 = P[2 * phys_row(m, R + r) + 1];
+      } else {
+        k0 = m.K[4 * phys_row(m, r) + 3];  // kraw.hi
+        k1 = m.K[4 * phys_row(m, R + r) + 2];  // kraw.lo
+      }
+      // undecided rows stay; should the exact offers freeze them, their
+      // later work is not counted (launch_count_affine reads the exact
+      // freezes in stream order) and their results are ignored
+      const bool gone = pred_decide(S0, A0, N0, k0, e0, true) == 1 || pred_decide(S1, A1, N1, k1, e1, false) == 1;
+      s_keep[r] = gone ? 0 : 1;
+    }
+  }
   __syncthreads();
-  // +1: the raw value is proven to freeze the row (upper <= 0 / lower >= 0),
-  // -1: proven not to, 0: undecided
-  auto decide = [&](int row, bool upper) {
-    double k0, pe = 0.0;
-    if (P) {  // predicted raw constant and its error radius (k_pk_*)
-      k0 = P[2 * phys_row(m, row)];
-      pe = P[2 * phys_row(m, row) + 1];
-    } else {
-      const double* K = m.K + 4 * phys_row(m, row);
-      k0 = upper ? K[3] : K[2];  // kraw.hi / kraw.lo
-    }
-    double S = k0, A = __dadd_ru(fabs(k0), pe), N = 0.0;
-    for (int t = 0; t < ntiles; ++t) {
-      const double* P = part + ((size_t)row * ntiles + t) * 3;
-      S += P[0];
-      A += P[1];
-      N += P[2];
-    }
-    if (!(fabs(S) < 1e300) || !(A < 1e300)) return 0;
-    const double B = __dmul_ru(A, 1.0 + 0x1p-30);
-    // 2.5 ulp per outward link + the parallel sum's error, relative to B,
-    // plus an absolute ulp floor per link for the subnormal range
-    const double E = __dadd_ru(pe, __dmul_ru(4.0 * (N + 2.0), __dadd_ru(__dmul_ru(0x1p-52, B), 0x1p-1074)));
-    if (!(E < 1e300)) return 0;
-    const double up = __dadd_ru(S, E), dn = __dadd_rd(S, -E);
-    if (upper) return up <= 0.0 ? 1 : dn > 0.0 ? -1 : 0;
-    return dn >= 0.0 ? 1 : up < 0.0 ? -1 : 0;
-  };
-  int undecided = 0;
   for (int start = 0; start < R; start += kPredScan) {
     const int r = start + threadIdx.x;
     int keep = 0, q = 0;
     if (r < R) {
       q = rows.row_q[r];
-      bool gone = frozen && frozen[q];
-      if (!gone) {
-        const int a = decide(r, true);
-        const int b = a == 1 ? 1 : decide(R + r, false);
-        gone = a == 1 || b == 1;
-        undecided |= !gone && (a == 0 || b == 0);
-      }
-      keep = !gone;
+      keep = s_keep[r];
     }
     int pos, total;
     Scan(tmp).ExclusiveSum(keep, pos, total);
@@ -1062,10 +1091,7 @@ __global__ void __launch_bounds__(kPredScan)
   }
   const int nR = s_base;
   for (int p = threadIdx.x; p < nR; p += blockDim.x) map[nR + p] = R + map[p];  // lower rows
-  // an undecided row may still freeze in the exact offers: -(nR + 1) tells
-  // the host to order the next step's counters behind them
-  undecided = __syncthreads_or(undecided);
-  if (threadIdx.x == 0) *new_R = undecided ? -(nR + 1) : nR;
+  if (threadIdx.x == 0) *new_R = nR;
 }
 
 void launch_pred_offer(cudaStream_t s, const RowsDev& rows, int R, const FrameDev& f, MatDev m,
@@ -1074,8 +1100,17 @@ void launch_pred_offer(cudaStream_t s, const RowsDev& rows, int R, const FrameDe
   const int ntiles = (int)((m.cells + kPT * 4 - 1) / (kPT * 4));
   double* part = static_cast<double*>(stream_scratch(s, (size_t)rows.n * ntiles * 3 * sizeof(double)));
   k_pred_terms<<<dim3(ntiles, rows.n), kPT, 0, s>>>(rows, f, m, rlo, rhi, part, ntiles, frozen);
-  k_pred_offer<<<1, kPredScan, 0, s>>>(rows, R, m, P, part, ntiles, frozen, map, new_R, new_row_q);
+  k_pred_offer<<<1, kPredScan, rows.n_up + 16, s>>>(rows, R, m, P, part, ntiles, frozen, map, new_R, new_row_q);
   g_launches += 2;
+}
+
+// The predicted offers from partial sums a conv kernel already produced
+// (k_gbc_flat with FlatDev::part: nparts per row).
+void launch_pred_offer_parts(cudaStream_t s, const RowsDev& rows, int R, MatDev m, const double* P,
+                             const double* part, int nparts, const char* frozen, int* map, int* new_R,
+                             int* new_row_q) {
+  k_pred_offer<<<1, kPredScan, rows.n_up + 16, s>>>(rows, R, m, P, part, nparts, frozen, map, new_R, new_row_q);
+  ++g_launches;
 }
 
 // ---------------------------------------------------------------------------
@@ -1173,8 +1208,8 @@ __global__ void __launch_bounds__(kPT)
 
 __global__ void k_pk_affine_fin(RowsDev rows, MatDev m, const double* Pin, const double* part, int ntiles,
                                 double* Pout) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows.n) return;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * blockDim.x + threadIdx.x, i)) return;
   double S = 0.0, A = 0.0, N = 0.0;
   for (int t = 0; t < ntiles; ++t) {
     const double* Pp = part + ((size_t)i * ntiles + t) * 3;
@@ -1266,8 +1301,8 @@ void launch_pk_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatD
 
 // join (align_add, backsub.hpp:610-688): one link, branch a's constant plus b's
 __global__ void k_pk_merge(RowsDev rows, MatDev a, const double* Pa, MatDev b, const double* Pb, double* Pout) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows.n) return;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * blockDim.x + threadIdx.x, i)) return;
   const double* pb = Pb + 2 * phys_row(b, i);
   double* po = Pout + 2 * (size_t)i;
   pk_widen(Pa + 2 * phys_row(a, i), pb[0], __dadd_ru(fabs(pb[0]), pb[1]), 1.0, po);
@@ -1286,8 +1321,8 @@ void launch_pk_merge(cudaStream_t s, const RowsDev& rows, MatDev a, const double
 
 // a walk's first rows: the exact constants, radius 0
 __global__ void k_pk_init(RowsDev rows, MatDev m, double* Pout) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows.n) return;
+  int i;
+  if (!rows_resolve(rows, blockIdx.x * blockDim.x + threadIdx.x, i)) return;
   bool upper;
   int img;
   row_query(rows, i, upper, img);
@@ -1301,6 +1336,58 @@ __global__ void k_pk_init(RowsDev rows, MatDev m, double* Pout) {
 
 void launch_pk_init(cudaStream_t s, const RowsDev& rows, MatDev m, double* P) {
   k_pk_init<<<(rows.n + 127) / 128, 128, 0, s>>>(rows, m, P);
+  ++g_launches;
+}
+
+// PassStats work of an affine step (dense_madds / gbc_madds: the in-grid
+// taps of every nonzero coefficient, backsub.hpp:386,483; gbc_dense_equiv)
+// for the rows the reference still walks. With predicted compaction the
+// chain kernels on s2 cannot know whether the exact offers (s3) froze a
+// row the prediction kept, so the counting runs here, on s3, in stream
+// order behind those offers.
+__global__ void __launch_bounds__(kPT)
+    k_count_affine(LayerDev L, int is_conv, RowsDev rows, FrameDev f, MatDev m, const char* frozen,
+                   Counters* ctr) {
+  int i;
+  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  bool upper;
+  int img;
+  const int q = row_query(rows, i, upper, img);
+  if (frozen && frozen[(size_t)img * rows.kq + q]) return;
+  ctr += img;
+  int bw = 0, bh = 0;
+  if (is_conv) frame_base(f, q, bw, bh);
+  const size_t pr = phys_row(m, i);
+  const double* lo = m.lo + pr * m.cells;
+  const double* hi = m.hi + pr * m.cells;
+  unsigned long long md = 0;
+  const long long c0 = (long long)blockIdx.x * (kPT * 4);
+  for (int k = 0; k < 4; ++k) {
+    const long long cell = c0 + (long long)k * kPT + threadIdx.x;
+    if (cell >= m.cells) break;
+    if (iv_zero(Iv{lo[cell], hi[cell]})) continue;
+    if (is_conv) {
+      int d, aw, ah;
+      cell_pos(f, cell, bw, bh, d, aw, ah);
+      const int y0 = ah * L.sh - L.ph, x0 = aw * L.sw - L.pw;
+      const int ny = min(L.fh, L.in_h - y0) - max(0, -y0);
+      const int nx = min(L.fw, L.in_w - x0) - max(0, -x0);
+      if (ny > 0 && nx > 0) md += (unsigned long long)L.in_c * ny * nx;
+    } else {
+      md += (unsigned long long)L.in_w * L.in_h * L.in_c;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) md += __shfl_down_sync(0xffffffffu, md, o);
+  if ((threadIdx.x & 31) == 0 && md) atomicAdd(is_conv ? &ctr->gbc_madds : &ctr->dense_madds, md);
+  if (is_conv && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(&ctr->gbc_dense_equiv, (unsigned long long)L.out_w * L.out_h * L.out_c *
+                                         ((unsigned long long)L.in_w * L.in_h * L.in_c));
+}
+
+void launch_count_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows, const FrameDev& f,
+                         MatDev m, const char* frozen, Counters* ctr) {
+  const int ntiles = (int)((m.cells + kPT * 4 - 1) / (kPT * 4));
+  k_count_affine<<<dim3(ntiles, rows.n), kPT, 0, s>>>(L, is_conv ? 1 : 0, rows, f, m, frozen, ctr);
   ++g_launches;
 }
 

@@ -103,6 +103,9 @@ struct Mat {
   double* hi = nullptr;
   double* K = nullptr;
   double* P = nullptr;  // predicted raw constants (S, E) per physical row (Walker::pk)
+  cudaEvent_t pk_ready = nullptr;  // recorded on s4 after P
+  double* part = nullptr;  // predicted-offer partials fused into the producing conv kernel
+  int nparts = 0;
   long long cells = 0;
   Frame f;
   const int* src = nullptr;  // row map after a compaction (see MatDev::src)
@@ -190,6 +193,7 @@ struct Ctx {
   double *vals = nullptr, *rvals = nullptr, *best = nullptr;
   char* has = nullptr;
   Counters* ctr = nullptr;
+  Counters* ctr_sink = nullptr;  // the chain kernels' counting when it runs on s3 (launch_count_affine)
   char* arena = nullptr;
   size_t arena_cap = 0, arena_used = 0;
   unsigned* stats = nullptr;  // MagStat pool: 2 words per bound matrix of a walk
@@ -292,6 +296,7 @@ struct Ctx {
     best = dalloc<double>(M);
     has = dalloc<char>(M);
     ctr = dalloc<Counters>(nimg);
+    ctr_sink = dalloc<Counters>(nimg);
     gen_n = dalloc<int>(T);
     gen_pos = dalloc<int>((size_t)pofs[nl] * nimg);
     gen_l = dalloc<int>((size_t)nl * nimg);
@@ -668,6 +673,11 @@ struct Walker {
   bool devr = false;
   const int* dR = nullptr;
   int slot_next = 0, pq = 0;
+  // device-applied predicted compaction (pred_device()): the live row count
+  // of the current row list on the device; R is then only a bound, lowered
+  // as the checkpoints' counts reach the host (learn)
+  const int* hdR = nullptr;
+  std::vector<int> learn;
   // lazy compaction state: checkpoints launched since the last compaction
   int ck_next = 0;             // next pinned slot
   // Compaction ring: each checkpoint's offers write their row map, query list
@@ -693,7 +703,7 @@ struct Walker {
 
   RowsDev rows() const {
     RowsDev r{row_q, nrows(), both ? R : 0};
-    r.dR = devr ? dR : nullptr;
+    r.dR = devr ? dR : hdR;
     r.kq = kq;
     r.sst = sst;
     r.nimg = nimg;
@@ -779,6 +789,38 @@ struct Walker {
     return predict == 1 && s4 && s4 != s2 ? 1 : 2;
   }
   bool pk() const { return predict_mode() == 1; }
+  // PC_PRED_DEVICE=1: the predicted compaction takes effect on the device
+  // (the next step's streams wait for the predicted offers, the kernels read
+  // the row count from the ring slot); the host never blocks on a checkpoint
+  // and learns the counts one checkpoint late
+  bool pred_device() const {
+    static const int on = env_int("PC_PRED_DEVICE", 1);
+    return on && pk();
+  }
+  // PassStats work counters of the chain kernels: counted on s3 instead
+  // (launch_count_affine) when compaction is predicted
+  Counters* cctr() const { return predict_mode() ? n->ctr_sink : n->ctr; }
+  void count_affine(const LayerDev& L, bool is_conv, const Mat& m) {
+    if (dry || !predict_mode()) return;
+    if (m.ready) ck(cudaStreamWaitEvent(s3, m.ready, 0), "wait");
+    launch_count_affine(s3, L, is_conv, rows(), fdev(n, m.f, q), md(m), fz(), n->ctr);
+  }
+  // lower R to the counts of completed checkpoints; block while more than
+  // `keep` are unknown
+  void learn_R(size_t keep) {
+    while (!learn.empty()) {
+      const int ckx = learn.front();
+      if (learn.size() > keep) {
+        ck(cudaEventSynchronize(n->ck_ev[ckx]), "sync");
+      } else {
+        const cudaError_t e = cudaEventQuery(n->ck_ev[ckx]);
+        if (e == cudaErrorNotReady) break;
+        ck(e, "event query");
+      }
+      R = std::min(R, n->h_newR[ckx]);
+      learn.erase(learn.begin());
+    }
+  }
   // P of a step's output (taken in the dry run too, so the arena fits it)
   double* p_take() {
     if (dry) return arena_take((size_t)alloc_rows() * 2 * sizeof(double));
@@ -786,6 +828,11 @@ struct Walker {
   }
   void need4(const Mat& m) {
     if (m.ready) ck(cudaStreamWaitEvent(s4, m.ready, 0), "wait");
+  }
+  cudaEvent_t pk_event() {
+    cudaEvent_t e = sync_event(n);
+    ck(cudaEventRecord(e, s4), "event");
+    return e;
   }
 
   void dense_step(Mat& m) {  // backsub.hpp:343-399
@@ -798,12 +845,14 @@ struct Walker {
       prof_begin(n, PROF_PREDICT, s4);
       launch_pk_affine(s4, L.d, false, rows(), fdev(n, m.f, q), md(m), m.P, out.P);
       prof_end(n, s4);
+      out.pk_ready = pk_event();
     }
+    count_affine(L.d, false, m);
     if (!dry) {
       need(m);
       prof_begin(n, PROF_CHAIN_AFFINE, s2);
       launch_chain_affine(s2, L.d, false, rows(), fdev(n, m.f, q), md(m), out.K,
-                          n->dev + n->off[m.f.layer], n->ctr, fz(), fast());
+                          n->dev + n->off[m.f.layer], cctr(), fz(), fast());
       prof_end(n, s2);
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (n->timing) {  // the roofline kernel is always timed (bench.py reads it)
@@ -844,7 +893,9 @@ struct Walker {
       prof_begin(n, PROF_PREDICT, s4);
       launch_pk_affine(s4, L.d, true, rows(), fdev(n, m.f, q), md(m), m.P, out.P);
       prof_end(n, s4);
+      out.pk_ready = pk_event();
     }
+    count_affine(L.d, true, m);
     // compacted nonzero input coefficients for the sparse conv kernel
     const bool sparse = gbc_sparse_wanted(L.d);
     SparseDev sp{};
@@ -863,13 +914,21 @@ struct Walker {
     static const int chain_scan = env_int("PC_CHAIN_SCAN", 0);
     const bool scan = sparse && chain_scan && m.cells >= 256;
     double* tmp = scan ? arena_take((size_t)alloc_rows() * 5 * sizeof(double)) : nullptr;
+    // predicted compaction: partials of the raw concretisation from the conv
+    // kernel (k_gbc_flat), so the predicted offer does not re-read the matrix
+    static const int fuse_env = env_int("PC_PRED_FUSED", 1);
+    double* fused_part = nullptr;
+    if (fuse_env && n->L[L.pred0].kind == KIND_RELU && (dry || pk())) {
+      const int nparts = gbc_flat_blocks(fdev(n, nf, q), L.d);
+      fused_part = arena_take((size_t)alloc_rows() * nparts * 3 * sizeof(double));
+    }
     if (!dry) {
       const FrameDev fi = fdev(n, m.f, q), fo = fdev(n, nf, q);
       if (!scan) {
         need(m);
         prof_begin(n, PROF_CHAIN_AFFINE, s2);
         launch_chain_affine(s2, L.d, true, rows(), fi, md(m), out.K, n->dev + n->off[m.f.layer],
-                            n->ctr, fz(), fast());
+                            cctr(), fz(), fast());
         prof_end(n, s2);
       }
       if (sparse) {
@@ -882,7 +941,7 @@ struct Walker {
         ck(cudaStreamWaitEvent(s2, e, 0), "wait");
         prof_begin(n, PROF_CHAIN_AFFINE, s2);
         launch_chain_affine_scan(s2, L.d, rows(), fi, md(m), sp, tmp, out.K, n->dev + n->off[m.f.layer],
-                                 n->ctr, fz());
+                                 cctr(), fz());
         prof_end(n, s2);
       }
       prof_begin(n, PROF_GBC);
@@ -903,8 +962,15 @@ struct Walker {
           launch_gbc_tile(s, L.d, rows(), fi, fo, sp, md(m), md(out), n->lv_chm + (size_t)L.pred0 * 16,
                           (long long)nl * 16, n->ctr);
         } else if (flat && fo.S_h <= 64 && (long long)fo.G_w * fo.G_h < 65536) {
-          const FlatDev fl{n->lv_pref + n->pofs[L.pred0] + L.pred0, n->lv_fpos + n->off[L.pred0],
-                           n->lv_fch + n->off[L.pred0], n->pofs[nl] + nl, n->total};
+          FlatDev fl{n->lv_pref + n->pofs[L.pred0] + L.pred0, n->lv_fpos + n->off[L.pred0],
+                     n->lv_fch + n->off[L.pred0], n->pofs[nl] + nl, n->total};
+          if (fused_part) {  // the predicted offer's partial sums in the conv epilogue
+            fl.prlo = n->rlo + n->off[L.pred0];
+            fl.prhi = n->rhi + n->off[L.pred0];
+            fl.part = fused_part;
+            out.part = fused_part;
+            out.nparts = gbc_flat_blocks(fo, L.d);
+          }
           launch_gbc_flat(s, L.d, rows(), fi, fo, sp, md(m), md(out), fl, n->ctr, fast());
         } else {
           const LiveDev lv{n->lv_cnt + n->pofs[L.pred0], n->lv_idx + n->off[L.pred0], n->pofs[nl], n->total};
@@ -989,7 +1055,10 @@ struct Walker {
     }
     Mat out = alloc(u, true);
     out.P = p_take();
-    if (!dry && pk()) launch_pk_merge(s4, rows(), md(a), a.P, md(b), b.P, out.P);
+    if (!dry && pk()) {
+      launch_pk_merge(s4, rows(), md(a), a.P, md(b), b.P, out.P);
+      out.pk_ready = pk_event();
+    }
     if (!dry) {
       const FrameDev fa = fdev(n, a.f, q), fb = fdev(n, b.f, q), fu = fdev(n, u, q);
       prof_begin(n, PROF_MERGE);
@@ -1029,20 +1098,32 @@ struct Walker {
         resolve(m, 0);
         slot = free_slot();
       }
-      cudaStream_t sp = pmode == 1 ? s4 : s2;
+      // fused partials: the offer runs on the coefficient stream right
+      // behind the conv kernel (and the predicted constants)
+      const bool fused = pmode == 1 && m.part;
+      cudaStream_t sp = fused ? s : pmode == 1 ? s4 : s2;
       // the exact work on s3 may still read this slot's rows / map from an
       // earlier generation
       ck(cudaStreamWaitEvent(sp, n->ring_ev[slot], 0), "wait");
-      if (pmode == 1) need4(m);
+      if (fused) {
+        if (m.pk_ready) ck(cudaStreamWaitEvent(s, m.pk_ready, 0), "wait");
+      } else if (pmode == 1) {
+        need4(m);
+      }
       prof_begin(n, PROF_OFFER, sp);
-      launch_pred_offer(sp, rows(), R, fdev(n, m.f, q), md(m), pmode == 1 ? m.P : nullptr, n->rlo + o,
-                        n->rhi + o, n->frozen, n->ring_map[slot], n->d_ringR + slot, n->ring_q[slot]);
+      if (fused)
+        launch_pred_offer_parts(sp, rows(), R, md(m), m.P, m.part, m.nparts, n->frozen, n->ring_map[slot],
+                                n->d_ringR + slot, n->ring_q[slot]);
+      else
+        launch_pred_offer(sp, rows(), R, fdev(n, m.f, q), md(m), pmode == 1 ? m.P : nullptr, n->rlo + o,
+                          n->rhi + o, n->frozen, n->ring_map[slot], n->d_ringR + slot, n->ring_q[slot]);
       prof_end(n, sp);
       const int ckx = ck_next;
       ck_next = (ck_next + 1) % Ctx::kCkSlots;
       ck(cudaMemcpyAsync(n->h_newR + ckx, n->d_ringR + slot, sizeof(int), cudaMemcpyDeviceToHost, sp), "d2h");
       ck(cudaEventRecord(n->ck_ev[ckx], sp), "event");
-      pend.push_back(Pending{ckx, slot, gen});
+      const bool on_device = pred_device();
+      if (!on_device) pend.push_back(Pending{ckx, slot, gen});
       stream_wait(n, s3, s2);  // M and K of this checkpoint
       prof_begin(n, PROF_CONC, s3);
       launch_concretize(s3, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->rlo + o,
@@ -1051,6 +1132,20 @@ struct Walker {
       launch_offer(s3, rows(), R, n->vals, n->rvals, n->cand, n->frozen, 1, 1, n->xmap, n->d_int + 3, n->xq,
                    n->ctr, n->ckat, ck_index);
       if (cur_slot >= 0) ck(cudaEventRecord(n->ring_ev[cur_slot], s3), "event");  // s3 read that slot
+      if (on_device) {
+        // the compaction takes effect now: every stream's next work reads
+        // the slot's rows, map and count (the work above read the old ones)
+        cudaEvent_t e = sync_event(n);
+        ck(cudaEventRecord(e, sp), "event");
+        for (cudaStream_t w : {s, s2, s3, s4})
+          if (w != sp) ck(cudaStreamWaitEvent(w, e, 0), "wait");
+        m.src = n->ring_map[slot];
+        row_q = n->ring_q[slot];
+        hdR = n->d_ringR + slot;
+        cur_slot = slot;
+        ++gen;
+        learn.push_back(ckx);
+      }
       return;
     }
     prof_begin(n, PROF_CONC, s2);
@@ -1138,14 +1233,7 @@ struct Walker {
     }
   }
   void apply(Mat& m, const Pending& p) {
-    int newR = n->h_newR[p.ck];
-    if (newR < 0) {
-      // a predicted offer left rows undecided: the exact offers (s3) may
-      // still freeze them, and the next step's counting kernels (s2) must
-      // see those freezes, as after the reference's compaction
-      newR = -newR - 1;
-      stream_wait(n, s2, s3);
-    }
+    const int newR = n->h_newR[p.ck];
     if (p.gen != gen) return;
     if (newR >= R) return;
     m.src = n->ring_map[p.slot];
@@ -1174,6 +1262,10 @@ struct Walker {
   //            checkpoint once it froze >= 1/8 of the rows.
   void maybe_compact(Mat& m) {
     if (dry || devr || !(allow_freeze && early_term)) return;
+    if (pred_device()) {  // compaction already applied on the device
+      learn_R(1);
+      return;
+    }
     static const int lazy_all = env_int("PC_LAZY_COMPACT", 0);
     static const int lazy_rows = env_int("PC_LAZY_ROWS", 0);
     static const int lag_rows = env_int("PC_LAG_ROWS", 0);
@@ -1203,6 +1295,8 @@ struct Walker {
     static const int lazy = env_int("PC_LAZY_COMPACT", 0);
     static const int lazy_rows = env_int("PC_LAZY_ROWS", 0);
     static const int lag_rows = env_int("PC_LAG_ROWS", 0);
+    if (pred_device())
+      return learn.size() <= 1 || cudaEventQuery(n->ck_ev[learn[learn.size() - 2]]) != cudaErrorNotReady;
     if (dry || devr || !(allow_freeze && early_term) || lazy || R <= lazy_rows || pend.empty()) return true;
     const size_t keep = R <= lag_rows ? 1 : 0;
     if (pend.size() <= keep) return true;
@@ -1213,6 +1307,10 @@ struct Walker {
   }
   // Block until ready() (the checkpoint the next step waits for).
   void wait_ready() const {
+    if (pred_device()) {
+      if (learn.size() > 1) ck(cudaEventSynchronize(n->ck_ev[learn[learn.size() - 2]]), "sync");
+      return;
+    }
     static const int lag_rows = env_int("PC_LAG_ROWS", 0);
     const size_t keep = R <= lag_rows ? 1 : 0;
     if (pend.size() > keep) ck(cudaEventSynchronize(n->ck_ev[pend[pend.size() - 1 - keep].ck]), "sync");

@@ -2867,7 +2867,12 @@ __global__ void __launch_bounds__(256, MINB)
   __syncthreads();
   const int total = s_seg[fo.S_h];
   const int t0 = blockIdx.x * kFlatOPB;
-  if (t0 >= total) return;
+  const bool band = FAST || products_in_band(in.stat, L.wmin, L.wmax);
+  double* part = fl.part ? fl.part + ((size_t)i * gridDim.x + blockIdx.x) * 3 : nullptr;
+  if (t0 >= total) {
+    if (part && band != CHECKED && threadIdx.x < 3) part[threadIdx.x] = 0.0;
+    return;
+  }
   const int t1 = min(total, t0 + kFlatOPB);
   const long long ocells = out.cells;
   const double* ilo = in.lo + phys_row(in, i) * in.cells;
@@ -2875,11 +2880,12 @@ __global__ void __launch_bounds__(256, MINB)
   double* olo = out.lo + (size_t)i * ocells;
   double* ohi = out.hi + (size_t)i * ocells;
   const int cin = L.in_c, cout = L.out_c;
-  const bool band = FAST || products_in_band(in.stat, L.wmin, L.wmax);
   // Two instantiations per launch: the band one (no call in its loop, so a
   // lean register budget) returns when the operands are not proven in band,
   // the CHECKED one only works in that (rare) case.
   if (band == CHECKED) return;
+  double pS = 0.0, pA = 0.0, pN = 0.0;  // predicted compaction partials (FlatDev::part)
+  const long long pso = (long long)img * rows.sst;
   const int* cnt = sp.cnt + (size_t)i * sp.ncell;
   const size_t rbase = (size_t)i * sp.ncell * sp.C;
   MagAcc mag;
@@ -2939,11 +2945,38 @@ __global__ void __launch_bounds__(256, MINB)
     ohi[o] = acc.hi;
     mag.add(acc.lo);
     mag.add(acc.hi);
+    if (part && !iv_zero(acc)) {  // the raw concretisation's corner term (k_pred_terms)
+      const long long j = ((long long)iy * fo.G_w + ix) * fo.C + ci;
+      const Iv Br{fl.prlo[pso + j], fl.prhi[pso + j]};
+      const double tt = upper ? corner_hi(acc, Br) : corner_lo(acc, Br);
+      pS += tt;
+      pA += fabs(tt);
+      pN += 1.0;
+    }
   }
   mag.flush(out.stat);
   if (ctr) {
     for (int o = 16; o > 0; o >>= 1) exec += __shfl_down_sync(__activemask(), exec, o);
     if ((threadIdx.x & 31) == 0 && exec) atomicAdd(&ctr[img].conv_exec, exec);
+  }
+  if (part) {
+    __shared__ double s_pr[3][8];
+    for (int o = 16; o > 0; o >>= 1) {
+      pS += __shfl_down_sync(0xffffffffu, pS, o);
+      pA += __shfl_down_sync(0xffffffffu, pA, o);
+      pN += __shfl_down_sync(0xffffffffu, pN, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_pr[0][threadIdx.x >> 5] = pS;
+      s_pr[1][threadIdx.x >> 5] = pA;
+      s_pr[2][threadIdx.x >> 5] = pN;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      double v = 0.0;
+      for (int w = 0; w < 8; ++w) v += s_pr[threadIdx.x][w];
+      part[threadIdx.x] = v;
+    }
   }
 }
 
@@ -3098,6 +3131,10 @@ __global__ void __launch_bounds__(256, MINB)
     for (int o = 16; o > 0; o >>= 1) exec += __shfl_down_sync(__activemask(), exec, o);
     if ((threadIdx.x & 31) == 0 && exec) atomicAdd(&ctr[img].conv_exec, exec);
   }
+}
+
+int gbc_flat_blocks(const FrameDev& fout, const LayerDev& L) {
+  return (int)cdiv((long long)fout.S_w * fout.S_h * L.in_c, kFlatOPB);
 }
 
 void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,

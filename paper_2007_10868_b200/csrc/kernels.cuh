@@ -400,10 +400,17 @@ struct FlatDev {
   const unsigned short* fpos;
   const unsigned short* fch;
   long long fst, sst;  // per-image strides of pref and of fpos / fch
+  // predicted compaction (optional): the output frame layer's raw bounds;
+  // each block writes the (sum, sum of magnitudes, count) of its outputs'
+  // raw concretisation corner terms to part[(row * gridDim.x + block) * 3]
+  const double* prlo = nullptr;
+  const double* prhi = nullptr;
+  double* part = nullptr;
 };
 void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const unsigned short* idx,
                       int* pref, unsigned short* fpos, unsigned short* fch, int nimg, long long sst,
                       long long pst, long long fst);
+int gbc_flat_blocks(const FrameDev& fout, const LayerDev& L);  // blocks per row of k_gbc_flat
 void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
                      const FrameDev& fout, SparseDev sp, MatDev in, MatDev out, FlatDev fl, Counters* ctr,
                      bool fast = false);
@@ -424,6 +431,9 @@ void launch_concretize_scan(cudaStream_t s, const RowsDev& rows, const FrameDev&
 void launch_pred_offer(cudaStream_t s, const RowsDev& rows, int R, const FrameDev& f, MatDev m,
                        const double* P, const double* rlo, const double* rhi, const char* frozen, int* map,
                        int* new_R, int* new_row_q);
+void launch_pred_offer_parts(cudaStream_t s, const RowsDev& rows, int R, MatDev m, const double* P,
+                             const double* part, int nparts, const char* frozen, int* map, int* new_R,
+                             int* new_row_q);
 // Predicted raw constants (chains.cu): (S, E) per row, |chain value - S| <= E;
 // Pin read through the input matrix's row map, Pout compact.
 void launch_pk_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows, const FrameDev& f,
@@ -433,6 +443,10 @@ void launch_pk_relu(cudaStream_t s, const RowsDev& rows, const FrameDev& f, MatD
 void launch_pk_merge(cudaStream_t s, const RowsDev& rows, MatDev a, const double* Pa, MatDev b, const double* Pb,
                      double* Pout);
 void launch_pk_init(cudaStream_t s, const RowsDev& rows, MatDev m, double* P);
+// PassStats dense_madds / gbc_madds / gbc_dense_equiv of an affine step for
+// the rows not frozen (the chain kernels' counting, run behind the exact offers)
+void launch_count_affine(cudaStream_t s, const LayerDev& L, bool is_conv, const RowsDev& rows, const FrameDev& f,
+                         MatDev m, const char* frozen, Counters* ctr);
 // Dense-tile conv over the row's nonzero input channels x the layer's
 // live-anywhere output channels (needs sp.dmask; chmask per image, 16 words).
 void launch_gbc_tile(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,

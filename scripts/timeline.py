@@ -70,4 +70,14 @@ for ci, cname in enumerate(classes):
     iv = [(a, b) for c, st, a, b in tl if c == ci]
     if iv:
         out["class_busy_ms"][cname] = round(union(iv), 2)
+# per pass: the seed launch opens each pass (on s)
+seed_cls = classes.index("seed") if "seed" in classes else -1
+starts = sorted(a for c, st, a, b in tl if c == seed_cls)
+per = []
+for k, t0 in enumerate(starts):
+    t1 = starts[k + 1] if k + 1 < len(starts) else max(b for _, _, _, b in tl)
+    seg = [(c, st, max(a, t0), min(b, t1)) for c, st, a, b in tl if b > t0 and a < t1]
+    busy = [round(union([(a, b) for c, st, a, b in seg if st == j]), 2) for j in range(4)]
+    per.append({"ms": round(t1 - t0, 2), "s": busy[0], "s2": busy[1], "s3": busy[2], "s4": busy[3]})
+out["passes"] = per
 print(json.dumps(out))
