@@ -2853,6 +2853,11 @@ __global__ void __launch_bounds__(256, MINB)
   int bw, bh, nbw, nbh;
   frame_base(fi, q, bw, bh);
   frame_base(fo, q, nbw, nbh);
+  // Two instantiations per launch: the band one (no call in its loop, so a
+  // lean register budget) returns when the operands are not proven in band,
+  // the CHECKED one only works in that (rare) case.
+  const bool band = FAST || products_in_band(in.stat, L.wmin, L.wmax);
+  if (band == CHECKED) return;
   const int* pref = fl.pref + (long long)img * fl.fst;
   const unsigned short* fpos = fl.fpos + (long long)img * fl.sst;
   const unsigned short* fch = fl.fch + (long long)img * fl.sst;
@@ -2867,10 +2872,9 @@ __global__ void __launch_bounds__(256, MINB)
   __syncthreads();
   const int total = s_seg[fo.S_h];
   const int t0 = blockIdx.x * kFlatOPB;
-  const bool band = FAST || products_in_band(in.stat, L.wmin, L.wmax);
   double* part = fl.part ? fl.part + ((size_t)i * gridDim.x + blockIdx.x) * 3 : nullptr;
   if (t0 >= total) {
-    if (part && band != CHECKED && threadIdx.x < 3) part[threadIdx.x] = 0.0;
+    if (part && threadIdx.x < 3) part[threadIdx.x] = 0.0;
     return;
   }
   const int t1 = min(total, t0 + kFlatOPB);
@@ -2880,10 +2884,6 @@ __global__ void __launch_bounds__(256, MINB)
   double* olo = out.lo + (size_t)i * ocells;
   double* ohi = out.hi + (size_t)i * ocells;
   const int cin = L.in_c, cout = L.out_c;
-  // Two instantiations per launch: the band one (no call in its loop, so a
-  // lean register budget) returns when the operands are not proven in band,
-  // the CHECKED one only works in that (rare) case.
-  if (band == CHECKED) return;
   double pS = 0.0, pA = 0.0, pN = 0.0;  // predicted compaction partials (FlatDev::part)
   const long long pso = (long long)img * rows.sst;
   const int* cnt = sp.cnt + (size_t)i * sp.ncell;
