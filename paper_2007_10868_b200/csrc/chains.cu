@@ -999,7 +999,7 @@ __global__ void __launch_bounds__(kPT)
 
 // The predicted offers: certain freezes dropped, the survivors' row map,
 // query list and count written like k_offer's (stable order). Phase 1: a
-// warp per row pair (upper r, lower R + r) sums the partials and decides;
+// thread per row pair (upper r, lower R + r) sums the partials and decides;
 // phase 2: block scan over the decisions (dynamic shared memory: one flag
 // per row of the launch bound).
 __device__ __forceinline__ int pred_decide(double S, double A, double N, double k0, double pe, bool upper) {
@@ -1027,49 +1027,40 @@ __global__ void __launch_bounds__(kPredScan)
   extern __shared__ unsigned char s_keep[];
   if (rows.dR) R = *rows.dR;  // device-applied compaction: the live rows of this checkpoint
   if (threadIdx.x == 0) s_base = 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int r = warp; r < R; r += kPredScan / 32) {
+  // a thread per row pair: the loads of a row are independent (row list,
+  // freeze flag, partials, predicted constants), so each thread's latency is
+  // about one memory round trip
+  for (int r = threadIdx.x; r < R; r += kPredScan) {
     const int q = rows.row_q[r];
-    if (frozen && frozen[q]) {
-      if (lane == 0) s_keep[r] = 0;
-      continue;
+    const size_t p0 = phys_row(m, r), p1 = phys_row(m, R + r);
+    double k0, e0 = 0.0, k1, e1 = 0.0;
+    if (P) {  // predicted raw constants and their error radii (k_pk_*)
+      k0 = P[2 * p0];
+      e0 = P[2 * p0 + 1];
+      k1 = P[2 * p1];
+      e1 = P[2 * p1 + 1];
+    } else {
+      k0 = m.K[4 * p0 + 3];  // kraw.hi
+      k1 = m.K[4 * p1 + 2];  // kraw.lo
     }
     double S0 = 0.0, A0 = 0.0, N0 = 0.0, S1 = 0.0, A1 = 0.0, N1 = 0.0;
-    for (int t = lane; t < ntiles; t += 32) {
-      const double* p0 = part + ((size_t)r * ntiles + t) * 3;
-      const double* p1 = part + ((size_t)(R + r) * ntiles + t) * 3;
-      S0 += p0[0];
-      A0 += p0[1];
-      N0 += p0[2];
-      S1 += p1[0];
-      A1 += p1[1];
-      N1 += p1[2];
+    const double* q0 = part + (size_t)r * ntiles * 3;
+    const double* q1 = part + (size_t)(R + r) * ntiles * 3;
+#pragma unroll 4
+    for (int t = 0; t < ntiles; ++t) {
+      S0 += q0[3 * t];
+      A0 += q0[3 * t + 1];
+      N0 += q0[3 * t + 2];
+      S1 += q1[3 * t];
+      A1 += q1[3 * t + 1];
+      N1 += q1[3 * t + 2];
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      S0 += __shfl_down_sync(0xffffffffu, S0, o);
-      A0 += __shfl_down_sync(0xffffffffu, A0, o);
-      N0 += __shfl_down_sync(0xffffffffu, N0, o);
-      S1 += __shfl_down_sync(0xffffffffu, S1, o);
-      A1 += __shfl_down_sync(0xffffffffu, A1, o);
-      N1 += __shfl_down_sync(0xffffffffu, N1, o);
-    }
-    if (lane == 0) {
-      double k0, e0 = 0.0, k1, e1 = 0.0;
-      if (P) {  // predicted raw constants and their error radii (k_pk_*)
-        k0 = P[2 * phys_row(m, r)];
-        e0 = P[2 * phys_row(m, r) + 1];
-        k1 = P[2 * phys_row(m, R + r)];
-        e1 = P[2 * phys_row(m, R + r) + 1];
-      } else {
-        k0 = m.K[4 * phys_row(m, r) + 3];  // kraw.hi
-        k1 = m.K[4 * phys_row(m, R + r) + 2];  // kraw.lo
-      }
-      // undecided rows stay; should the exact offers freeze them, their
-      // later work is not counted (launch_count_affine reads the exact
-      // freezes in stream order) and their results are ignored
-      const bool gone = pred_decide(S0, A0, N0, k0, e0, true) == 1 || pred_decide(S1, A1, N1, k1, e1, false) == 1;
-      s_keep[r] = gone ? 0 : 1;
-    }
+    // undecided rows stay; should the exact offers freeze them, their later
+    // work is not counted (launch_count_affine reads the exact freezes in
+    // stream order) and their results are ignored
+    const bool gone = (frozen && frozen[q]) || pred_decide(S0, A0, N0, k0, e0, true) == 1 ||
+                      pred_decide(S1, A1, N1, k1, e1, false) == 1;
+    s_keep[r] = gone ? 0 : 1;
   }
   __syncthreads();
   for (int start = 0; start < R; start += kPredScan) {
