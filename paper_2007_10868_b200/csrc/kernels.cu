@@ -479,6 +479,126 @@ __global__ void __launch_bounds__(128)
   if (relax) store_relax(relax, jj, y);
 }
 
+// Conv layer forward with the taps staged through shared memory. A block is
+// 64 output channels of one position (out_c % 64 == 0), so its threads walk
+// the same receptive field in the same order (fy, fx, ci; out-of-grid taps
+// skipped, eval.hpp:150-200): chunks of kFC taps, their inputs (4 tracks) and
+// weight rows (64 channels) are copied by cp.async into a double buffer while
+// the previous chunk is folded. The chain per output is the reference's, so
+// results equal k_fwd_conv's; the few-warps-per-SM launches of the deep
+// layers then wait on shared memory instead of an L2 round trip per tap.
+constexpr int kFC = 32;
+template <bool FAST>
+__device__ __forceinline__ bool fwd_conv_staged(const LayerDev& L, int h, int w, int d0, const double* xl,
+                                                const double* xh, const double* xrl, const double* xrh,
+                                                double (*sw)[kFC][64], double (*sx)[4][kFC], double& lo,
+                                                double& hi, double& ab, double& rlo, double& rhi,
+                                                long long& terms, long long& dterms) {
+  const int tid = threadIdx.x, d = d0 + tid;
+  const int cin = L.in_c, cout = L.out_c;
+  const int y0 = h * L.sh - L.ph, x0 = w * L.sw - L.pw;
+  const int fy0 = max(0, -y0), fy1 = min(L.fh, L.in_h - y0);  // valid taps [fy0, fy1)
+  const int fx0 = max(0, -x0), fx1 = min(L.fw, L.in_w - x0);
+  const int ny = max(0, fy1 - fy0), nx = max(0, fx1 - fx0);
+  const long long T = (long long)ny * nx * cin;
+  const double bias = L.bias[d];
+  lo = hi = rlo = rhi = bias;
+  ab = fabs(bias);
+  terms = 1;
+  dterms = 1 + T;
+  bool bad = false;
+  const int nch = (int)((T + kFC - 1) / kFC);
+  // incremental tap cursor of the copies (fy, fx, ci), advanced in issue order
+  int cfy = fy0, cfx = fx0, cci = 0;
+  auto issue = [&](int c, int buf) {
+    const long long g0 = (long long)c * kFC;
+    int fy = cfy, fx = cfx, ci = cci;
+    for (int t = 0; t < kFC; ++t) {
+      const bool v = g0 + t < T;
+      const double* src = L.F + ((size_t)(fy * L.fw + fx) * cin + ci) * cout + d;
+      cp_async8(&sw[buf][t][tid], v ? src : L.F, v);
+      if (tid == t) {
+        const size_t xb = ((size_t)(y0 + fy) * L.in_w + (x0 + fx)) * cin + ci;
+        cp_async8(&sx[buf][0][t], v ? xl + xb : xl, v);
+        cp_async8(&sx[buf][1][t], v ? xh + xb : xh, v);
+        cp_async8(&sx[buf][2][t], v ? xrl + xb : xrl, v);
+        cp_async8(&sx[buf][3][t], v ? xrh + xb : xrh, v);
+      }
+      if (v && ++ci == cin) {
+        ci = 0;
+        if (++fx == fx1) {
+          fx = fx0;
+          ++fy;
+        }
+      }
+    }
+    cfy = fy;
+    cfx = fx;
+    cci = ci;
+    cp_async_commit();
+  };
+  if (nch > 0) issue(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      issue(c + 1, (c + 1) & 1);
+      cp_async_wait_one();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    const int b = c & 1;
+    const long long rem = T - (long long)c * kFC;
+    const int n = rem < kFC ? (int)rem : kFC;
+    for (int t = 0; t < n; ++t)
+      affine_term<FAST>(sw[b][t][tid], sx[b][0][t], sx[b][1][t], sx[b][2][t], sx[b][3][t], lo, hi, ab, rlo, rhi,
+                        terms, bad);
+    __syncthreads();
+  }
+  return bad;
+}
+
+__global__ void __launch_bounds__(64)
+    k_fwd_conv_staged(LayerDev L, int layer, const double* xlo, const double* xhi, const double* xrlo,
+                      const double* xrhi, double* ylo, double* yhi, double* yrlo, double* yrhi, double* dev,
+                      double* relax, Dirty dt, long long gofs, long long pofs_in, long long pofs_out) {
+  __shared__ __align__(16) double sw[2][kFC][64];
+  __shared__ __align__(16) double sx[2][4][kFC];
+  PC_FWD_IMAGE(xlo += pc_zo; xhi += pc_zo; xrlo += pc_zo; xrhi += pc_zo; ylo += pc_zo; yhi += pc_zo;
+               yrlo += pc_zo; yrhi += pc_zo; dev += pc_zo; if (relax) relax += 8 * pc_zo;)
+  if (!dt.force && dt.gen_l[L.pred0] != dt.g) return;
+  const int pos = blockIdx.x;
+  const int h = pos / L.out_w, w = pos - h * L.out_w;
+  const int d0 = blockIdx.y * 64;
+  if (!dt.force) {  // any input position of the receptive field changed this round? (block-uniform)
+    bool any = false;
+    for (int fy = 0; fy < L.fh && !any; ++fy) {
+      const int iy = h * L.sh - L.ph + fy;
+      if (iy < 0 || iy >= L.in_h) continue;
+      for (int fx = 0; fx < L.fw; ++fx) {
+        const int ix = w * L.sw - L.pw + fx;
+        if (ix < 0 || ix >= L.in_w) continue;
+        if (dt.gen_pos[pofs_in + (long long)iy * L.in_w + ix] == dt.g) {
+          any = true;
+          break;
+        }
+      }
+    }
+    if (!any) return;
+  }
+  double lo, hi, ab, rlo, rhi;
+  long long terms, dterms;
+  const bool bad = fwd_conv_staged<true>(L, h, w, d0, xlo, xhi, xrlo, xrhi, sw, sx, lo, hi, ab, rlo, rhi, terms,
+                                         dterms);
+  if (__syncthreads_or(bad))  // operands outside the proven band: the literal restatement
+    fwd_conv_staged<false>(L, h, w, d0, xlo, xhi, xrlo, xrhi, sw, sx, lo, hi, ab, rlo, rhi, terms, dterms);
+  const long long jj = (long long)pos * L.out_c + d0 + threadIdx.x;
+  const double slack = __dmul_rn(__dmul_rn(2.0, (double)(terms + 1)), ulp_above(ab));
+  const Iv y{add_down(lo, -slack), add_up(hi, slack)};
+  store_bounds(ylo, yhi, yrlo, yrhi, jj, y, rlo, rhi, dt, gofs, pofs_out + pos, layer);
+  dev[jj] = __dmul_rn(__dmul_rn(2.0, (double)(dterms + 1)), ulp_above(ab));  // analyzer.hpp:140
+  if (relax) store_relax(relax, jj, y);
+}
+
 __global__ void k_fwd_relu(long long n, int C, int layer, const double* xlo, const double* xhi,
                            const double* xrlo, const double* xrhi, double* ylo, double* yhi,
                            double* yrlo, double* yrhi, Dirty dt, long long gofs_in, long long gofs,
@@ -541,10 +661,16 @@ void launch_forward_layer(cudaStream_t s, const LayerDev& L, int feeds_relu, con
       k_fwd_dense<<<dim3(cdiv(n, kFDN), 1, nimg), 2 * kFDN, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo,
                                                      yhi, yrlo, yrhi, dev + o, rx, dt, o);
       break;
-    case KIND_CONV:
-      k_fwd_conv<<<dim3(cdiv(n, 64), 1, nimg), 64, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi, yrlo,
-                                            yrhi, dev + o, rx, dt, o, pofs[p0], pofs[k]);
+    case KIND_CONV: {
+      static const int staged = env_int("PC_FWD_STAGED", 1);
+      if (staged && L.out_c % 64 == 0)
+        k_fwd_conv_staged<<<dim3(L.out_w * L.out_h, L.out_c / 64, nimg), 64, 0, s>>>(
+            L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi, yrlo, yrhi, dev + o, rx, dt, o, pofs[p0], pofs[k]);
+      else
+        k_fwd_conv<<<dim3(cdiv(n, 64), 1, nimg), 64, 0, s>>>(L, k, blo + a, bhi + a, rlo + a, rhi + a, ylo, yhi,
+                                                            yrlo, yrhi, dev + o, rx, dt, o, pofs[p0], pofs[k]);
       break;
+    }
     case KIND_RELU:
       k_fwd_relu<<<dim3(cdiv(n, 256), 1, nimg), 256, 0, s>>>(n, L.out_c, k, blo + a, bhi + a, rlo + a, rhi + a,
                                               ylo, yhi, yrlo, yrhi, dt, a, o, pofs[k]);

@@ -216,6 +216,7 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
 // -0 -> +0 (RN: -0 + +0 = +0), everything else unchanged.
 __device__ __forceinline__ double canon0(double x) { return __dadd_rn(x, 0.0); }
