@@ -678,6 +678,9 @@ struct Walker {
   // as the checkpoints' counts reach the host (learn)
   const int* hdR = nullptr;
   std::vector<int> learn;
+  // margin walks split over two contexts: where this walker's margin offers go
+  double* mbest = nullptr;
+  char* mhas = nullptr;
   // lazy compaction state: checkpoints launched since the last compaction
   int ck_next = 0;             // next pinned slot
   // Compaction ring: each checkpoint's offers write their row map, query list
@@ -1083,7 +1086,7 @@ struct Walker {
       launch_concretize(s2, rows(), fdev(n, m.f, q), md(m), n->blo + o, n->bhi + o, n->blo + o,
                         n->bhi + o, n->vals, n->rvals, nullptr, fast());
       prof_end(n, s2);
-      launch_margin_offer(s2, R, n->vals, n->best, n->has);
+      launch_margin_offer(s2, R, n->vals, mbest ? mbest : n->best, mhas ? mhas : n->has);
       return;
     }
     // Predicted compaction (launch_pred_offer): the survivors of this
@@ -1837,7 +1840,52 @@ void run_margin(Ctx* n, int label, pc_stats* st, double* margins_host) {
   const int mb = (int)slice_begin(nr, n->net->shard_rank, W);
   const int me = (int)slice_begin(nr, n->net->shard_rank + 1, W);
   const int R = me - mb;
-  if (R > 0) {
+  // two walk pipelines as in run_pass: the margin rows split between this
+  // context and its helper, advanced step by step in turn, so one half's
+  // conv substitutions overlap the other half's constant folds
+  static const int pipes = env_int("PC_PIPES", 2);
+  static const int margin_min = env_int("PC_MARGIN_PIPE_MIN", 4);
+  if (R > 0 && pipes >= 2 && R >= margin_min && !n->is_helper && !n->net->serial) {
+    Ctx* h = helper_of(n);
+    const int RA = R / 2, RB = R - RA;
+    ck(cudaMemcpyAsync(n->rowq[0], cls.data() + mb, sizeof(int) * RA, cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemcpyAsync(h->rowq[0], cls.data() + mb + RA, sizeof(int) * RB, cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemsetAsync(n->has, 0, R, s), "memset");
+    const WalkSize ws = walk_size(n, out, false, false);
+    ensure_arena(n, ws.per_row * (size_t)RB + 256 * ws.allocs + (1 << 20));
+    ensure_arena(h, ws.per_row * (size_t)RB + 256 * ws.allocs + (1 << 20));
+    stream_wait(n, h->stream, s);  // row lists, has[], the refreshed bounds
+    Ctx* cx[2] = {n, h};
+    const int r0[2] = {0, RA}, rn[2] = {RA, RB};
+    ChunkWalk a{Walker{n, s, out}}, b{Walker{h, h->stream, out}};
+    ChunkWalk* cw[2] = {&a, &b};
+    for (int k = 0; k < 2; ++k) {
+      Ctx* c = cx[k];
+      c->arena_used = 0;
+      reset_stats(c, ws.stats);
+      Walker& w = cw[k]->w;
+      w.s2 = c->stream2;
+      w.R = rn[k];
+      w.both = false;
+      w.margin = true;
+      w.st = st;
+      w.row_q = c->rowq[0];
+      w.mbest = n->best + r0[k];
+      w.mhas = n->has + r0[k];
+      cw[k]->m = w.alloc(dense_frame(out), true);
+      launch_init_margin(w.s, label, nullptr, n->n_out, mb + r0[k], rn[k], md(cw[k]->m));
+      w.mark(cw[k]->m);
+    }
+    while (a.running || b.running) {
+      if (a.running) a.running = a.w.advance(a.m, 0, true, a.pending);
+      if (b.running) b.running = b.w.advance(b.m, 0, true, b.pending);
+    }
+    stream_wait(n, s, n->stream2);
+    stream_wait(n, s, h->stream);
+    stream_wait(n, s, h->stream2);
+    stream_wait(n, h->stream, s);  // h's next walk reuses its arena after s
+    ck(cudaMemcpyAsync(n->h_int + 4, n->has, R, cudaMemcpyDeviceToHost, s), "d2h");
+  } else if (R > 0) {
     ck(cudaMemcpyAsync(n->rowq[0], cls.data() + mb, sizeof(int) * R, cudaMemcpyHostToDevice, s), "h2d");
     ck(cudaMemsetAsync(n->has, 0, R, s), "memset");
     const WalkSize ws = walk_size(n, out, false, false);
