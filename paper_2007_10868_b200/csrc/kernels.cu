@@ -2963,9 +2963,12 @@ void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const uns
 // reference's (ch, cw, d) order. Threads of a warp take consecutive live
 // cells (one or two grid positions), so coefficient loads are broadcasts and
 // no lane computes a dead cell. The output rows are zeroed beforehand (dead
-// cells). A block takes kFlatOPB consecutive live cells of its row's window:
+// cells). A block takes FlatDev::opb consecutive live cells of its row's window:
 // the window's grid rows are consecutive runs of the flat list.
-constexpr int kFlatOPB = 512;
+static int flat_opb() {  // live cells per block (PC_GBC_FLAT_OPB)
+  static const int v = env_int("PC_GBC_FLAT_OPB", 512);
+  return v;
+}
 template <int MINB, bool FAST = false, int KB = 4, bool CHECKED = false>
 __global__ void __launch_bounds__(256, MINB)
     k_gbc_flat(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
@@ -2997,13 +3000,13 @@ __global__ void __launch_bounds__(256, MINB)
   }
   __syncthreads();
   const int total = s_seg[fo.S_h];
-  const int t0 = blockIdx.x * kFlatOPB;
+  const int t0 = blockIdx.x * fl.opb;
   double* part = fl.part ? fl.part + ((size_t)i * gridDim.x + blockIdx.x) * 3 : nullptr;
   if (t0 >= total) {
     if (part && threadIdx.x < 3) part[threadIdx.x] = 0.0;
     return;
   }
-  const int t1 = min(total, t0 + kFlatOPB);
+  const int t1 = min(total, t0 + fl.opb);
   const long long ocells = out.cells;
   const double* ilo = in.lo + phys_row(in, i) * in.cells;
   const double* ihi = in.hi + phys_row(in, i) * in.cells;
@@ -3135,9 +3138,9 @@ __global__ void __launch_bounds__(256, MINB)
   }
   __syncthreads();
   const int total = s_seg[fo.S_h];
-  const int t0b = blockIdx.x * kFlatOPB;
+  const int t0b = blockIdx.x * fl.opb;
   if (t0b >= total) return;
-  const int t1b = min(total, t0b + kFlatOPB);
+  const int t1b = min(total, t0b + fl.opb);
   const long long ocells = out.cells;
   const double* ilo = in.lo + phys_row(in, i) * in.cells;
   const double* ihi = in.hi + phys_row(in, i) * in.cells;
@@ -3260,7 +3263,7 @@ __global__ void __launch_bounds__(256, MINB)
 }
 
 int gbc_flat_blocks(const FrameDev& fout, const LayerDev& L) {
-  return (int)cdiv((long long)fout.S_w * fout.S_h * L.in_c, kFlatOPB);
+  return (int)cdiv((long long)fout.S_w * fout.S_h * L.in_c, flat_opb());
 }
 
 void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, const FrameDev& fin,
@@ -3272,7 +3275,8 @@ void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
   cudaMemsetAsync(out.lo, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
   cudaMemsetAsync(out.hi, 0, sizeof(double) * (size_t)rows.n * out.cells, s);
   const long long cells = (long long)fout.S_w * fout.S_h * L.in_c;
-  dim3 grid(cdiv(cells, kFlatOPB), rows.n);
+  fl.opb = flat_opb();
+  dim3 grid(cdiv(cells, fl.opb), rows.n);
   static const int pairs = env_int("PC_GBC_FLAT_PAIRS", 0);
   static const int kb = env_int("PC_GBC_FLAT_KB", 4);
   static const int minb2 = env_int("PC_GBC_FLAT2_MINB", 2);

@@ -407,6 +407,7 @@ struct FlatDev {
   const double* prlo = nullptr;
   const double* prhi = nullptr;
   double* part = nullptr;
+  int opb = 512;  // live cells per block (set by launch_gbc_flat)
 };
 void launch_live_flat(cudaStream_t s, int npos, int C, const int* cnt, const unsigned short* idx,
                       int* pref, unsigned short* fpos, unsigned short* fch, int nimg, long long sst,
