@@ -1735,7 +1735,8 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
     // / concretisation chains and checkpoint round trips (rows are
     // independent, backsub.hpp:31-34; results identical).
     static const int pipes = env_int("PC_PIPES", 2);
-    const bool two = pipes >= 2 && !n->is_helper && chunk >= 16 && !n->net->serial;
+    static const int pipe_min = env_int("PC_PIPE_MIN_ROWS", 4);
+    const bool two = pipes >= 2 && !n->is_helper && chunk >= pipe_min && !n->net->serial;
     // rows of a walk ride in gridDim.y (both polarities: 2R <= 65535)
     chunk = std::min<long long>(chunk, two ? 2ll * kMaxWalkRows : kMaxWalkRows);
     Ctx* h = two ? helper_of(n) : nullptr;
@@ -1744,7 +1745,7 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
     if (h) ensure_arena(h, ws.per_row * (size_t)half + 256 * ws.allocs + (1 << 20));
     for (long long base = lb; base < le; base += chunk) {
       const int R = (int)std::min<long long>(chunk, le - base);
-      if (h && R >= 16) {
+      if (h && R >= pipe_min) {
         const int RA = R / 2, RB = R - RA;
         stream_wait(n, h->stream, s);  // the seed and live list are on s
         ChunkWalk a{Walker{n, s, t}}, b{Walker{h, h->stream, t}};
