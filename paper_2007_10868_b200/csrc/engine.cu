@@ -1736,43 +1736,53 @@ void run_pass(Ctx* n, int t, bool allow_freeze, pc_stats* st) {
     // independent, backsub.hpp:31-34; results identical).
     static const int pipes = env_int("PC_PIPES", 2);
     static const int pipe_min = env_int("PC_PIPE_MIN_ROWS", 4);
-    const bool two = pipes >= 2 && !n->is_helper && chunk >= pipe_min && !n->net->serial;
+    const int K = (pipes >= 2 && !n->is_helper && chunk >= pipe_min && !n->net->serial)
+                      ? (int)std::min<long long>(std::min(pipes, 4), chunk)
+                      : 1;
     // rows of a walk ride in gridDim.y (both polarities: 2R <= 65535)
-    chunk = std::min<long long>(chunk, two ? 2ll * kMaxWalkRows : kMaxWalkRows);
-    Ctx* h = two ? helper_of(n) : nullptr;
-    const long long half = two ? (chunk + 1) / 2 : chunk;
-    ensure_arena(n, ws.per_row * (size_t)half + 256 * ws.allocs + (1 << 20));
-    if (h) ensure_arena(h, ws.per_row * (size_t)half + 256 * ws.allocs + (1 << 20));
+    chunk = std::min<long long>(chunk, (long long)K * kMaxWalkRows);
+    std::vector<Ctx*> cx{n};  // the pipelines' contexts: n and its helper chain
+    while ((int)cx.size() < K) cx.push_back(helper_of(cx.back()));
+    const long long part = (chunk + K - 1) / K;
+    for (Ctx* c : cx) ensure_arena(c, ws.per_row * (size_t)part + 256 * ws.allocs + (1 << 20));
     for (long long base = lb; base < le; base += chunk) {
       const int R = (int)std::min<long long>(chunk, le - base);
-      if (h && R >= pipe_min) {
-        const int RA = R / 2, RB = R - RA;
-        stream_wait(n, h->stream, s);  // the seed and live list are on s
-        ChunkWalk a{Walker{n, s, t}}, b{Walker{h, h->stream, t}};
-        start_chunk(n, a, t, affine, base, RA, allow_freeze, et, st, ws);
-        start_chunk(h, b, t, affine, base + RA, RB, allow_freeze, et, st, ws);
-        // advance whichever walk's last checkpoint has resolved, so the host
-        // never blocks on one pipeline while the other could launch work
-        while (a.running || b.running) {
-          bool moved = false;
-          if (a.running && a.w.ready()) {
-            a.running = a.w.advance(a.m, 0, true, a.pending);
-            moved = true;
-          }
-          if (b.running && b.w.ready()) {
-            b.running = b.w.advance(b.m, 0, true, b.pending);
-            moved = true;
-          }
-          if (!moved) (a.running ? a : b).w.wait_ready();
+      if (K > 1 && R >= pipe_min && R >= K) {
+        std::vector<ChunkWalk> cw;
+        cw.reserve(K);
+        long long b0 = base;
+        for (int k = 0; k < K; ++k) {
+          const int Rk = R / K + (k >= K - R % K ? 1 : 0);
+          Ctx* c = cx[k];
+          if (k) stream_wait(n, c->stream, s);  // the seed and live list are on s
+          cw.push_back(ChunkWalk{Walker{c, c->stream, t}});
+          start_chunk(c, cw.back(), t, affine, b0, Rk, allow_freeze, et, st, ws);
+          b0 += Rk;
         }
-        stream_wait(n, s, n->stream2);
-        stream_wait(n, s, n->stream3);
-        stream_wait(n, s, n->stream4);
-        stream_wait(n, s, h->stream);
-        stream_wait(n, s, h->stream2);
-        stream_wait(n, s, h->stream3);
-        stream_wait(n, s, h->stream4);
-        stream_wait(n, h->stream, s);  // h's next chunk reuses its arena after s
+        // advance whichever walk's last checkpoint has resolved, so the host
+        // never blocks on one pipeline while another could launch work
+        for (;;) {
+          bool moved = false, any = false;
+          for (ChunkWalk& w : cw) {
+            if (!w.running) continue;
+            any = true;
+            if (w.w.ready()) {
+              w.running = w.w.advance(w.m, 0, true, w.pending);
+              moved = true;
+            }
+          }
+          if (!any) break;
+          if (!moved)
+            for (ChunkWalk& w : cw)
+              if (w.running) {
+                w.w.wait_ready();
+                break;
+              }
+        }
+        for (Ctx* c : cx)
+          for (cudaStream_t q : {c->stream, c->stream2, c->stream3, c->stream4})
+            if (q != s) stream_wait(n, s, q);
+        for (size_t k = 1; k < cx.size(); ++k) stream_wait(n, cx[k]->stream, s);  // arenas reused after s
         continue;
       }
       ChunkWalk a{Walker{n, s, t}};
@@ -2366,12 +2376,12 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
     std::vector<double> m(std::max(1, n->n_out - 1), 0.0);
     n->ev_used = 0;
     n->sync_used = 0;
-    if (n->helper) {
-      n->helper->ev_used = 0;
-      n->helper->sync_used = 0;
-      n->helper->prof.clear();
-      n->helper->dense_ev.clear();
-      n->helper->conv_ev.clear();
+    for (Ctx* h = n->helper; h; h = h->helper) {
+      h->ev_used = 0;
+      h->sync_used = 0;
+      h->prof.clear();
+      h->dense_ev.clear();
+      h->conv_ev.clear();
     }
     g_gbc_window_madds = 0;
     g_alloc_ms = 0;
@@ -2397,8 +2407,7 @@ void run_one(Ctx* n, const double* lo, const double* up, bool device_box, int la
       float d = 0;
       if (cudaEventElapsedTime(&d, n->ev_pool[e], n->ev_pool[e + 1]) == cudaSuccess) g_dense_ms += d;
     }
-    for (Ctx* c : {n, n->helper}) {  // both walk pipelines
-      if (!c) continue;
+    for (Ctx* c = n; c; c = c->helper) {  // every walk pipeline
       for (size_t e : c->conv_ev) {
         float d = 0;
         if (cudaEventElapsedTime(&d, c->ev_pool[e], c->ev_pool[e + 1]) == cudaSuccess) g_conv_ms += d;
@@ -2452,7 +2461,7 @@ void apply_call_options(Ctx* c, const pc_options* call) {
   o.device = c->net->opt.device;
   if (call && o.exec_mode == 0) o.exec_mode = c->net->opt.exec_mode;
   c->opt = o;
-  if (c->helper) c->helper->opt = o;
+  for (Ctx* h = c->helper; h; h = h->helper) h->opt = o;
 }
 
 pc_status test_impl(pc_net* net, const pc_options* call_opt, const double* lo, const double* up,
