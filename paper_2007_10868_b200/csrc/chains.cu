@@ -1453,7 +1453,7 @@ void launch_chain_affine_big(cudaStream_t s, const LayerDev& L, bool is_conv, co
   if (split_chains(s, m.cells, rows.n, 3, &tb, &tc, &ts, &nt)) {
     k_affine_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(L, is_conv ? 1 : 0, rows, fin, m, dev, tb, tc, ts, nt, ctr,
                                                    frozen, fast ? 1 : 0);
-    if (rows.n <= block_fold_rows() && nt <= kMaxFoldTiles && !rows.dR) {
+    if (rows.n <= block_fold_rows() && nt <= kMaxFoldTiles) {
       double* tmp = reinterpret_cast<double*>(reinterpret_cast<char*>(tc) + (((size_t)rows.n * nt * sizeof(int) + 255) & ~(size_t)255));
       k_affine_fold_block<<<dim3(rows.n, 5), kFB, 0, s>>>(rows, m, tmp, tb, tc, ts, nt, frozen, fast ? 1 : 0);
       k_affine_finish<<<(rows.n + 127) / 128, 128, 0, s>>>(rows, tmp, Kout, frozen);
@@ -1487,7 +1487,7 @@ void launch_concretize_big(cudaStream_t s, const RowsDev& rows, const FrameDev& 
   if (split_chains(s, m.cells, rows.n, 2, &tb, &tc, &ts, &nt)) {
     k_conc_terms<<<dim3(nt, rows.n), kTT, 0, s>>>(rows, f, m, blo, bhi, rlo, rhi, tb, tc, ts, nt, frozen,
                                                  fast ? 1 : 0);
-    if (rows.n <= block_fold_rows() && nt <= kMaxFoldTiles && !rows.dR)
+    if (rows.n <= block_fold_rows() && nt <= kMaxFoldTiles)
       k_conc_fold_block<<<dim3(rows.n, 2), kFB, 0, s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen, fast ? 1 : 0);
     else
       k_conc_fold<<<rows.n, 64, 2 * 2 * kTTile * sizeof(double), s>>>(rows, m, vals, rvals, tb, tc, ts, nt, frozen,
