@@ -2633,6 +2633,10 @@ pc_status pc_net_create(const pc_layer_desc* layers, int n_layers, int in_w, int
             if (!any || a > d.wmax) d.wmax = a;
             any = true;
           }
+        // test switch: no product is proven in band, every coefficient kernel
+        // takes its checked (literal restatement) path
+        static const int force_checked = env_int("PC_FORCE_CHECKED", 0);
+        if (force_checked) d.wmin = 0.0;
         double* b = n->dalloc<double>(l.bias.size());
         ck(cudaMemcpy(b, l.bias.data(), l.bias.size() * 8, cudaMemcpyHostToDevice), "h2d");
         d.bias = b;

@@ -2971,22 +2971,27 @@ static int flat_opb() {  // live cells per block (PC_GBC_FLAT_OPB)
 }
 template <int MINB, bool FAST = false, int KB = 4, bool CHECKED = false>
 __global__ void __launch_bounds__(256, MINB)
-    k_gbc_flat(LayerDev L, RowsDev rows, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
+    k_gbc_flat(LayerDev L, RowsDev rows_in, FrameDev fi, FrameDev fo, SparseDev sp, MatDev in,
                MatDev out, FlatDev fl, Counters* ctr) {
   __shared__ int s_seg[65];  // live cells before each window row (S_h <= 64)
+  // Two instantiations per launch: the band one (no call in its loop, so a
+  // lean register budget) returns when the operands are not proven in band,
+  // the CHECKED one only works in that (rare) case. The CHECKED one is
+  // launched one block row only (gridDim.y == 1) and loops over the rows,
+  // so its blocks that return cost little.
+  const bool band = FAST || products_in_band(in.stat, L.wmin, L.wmax);
+  if (band == CHECKED) return;
+  const int nblk = CHECKED ? rows_in.n : 1;
+  for (int rb = CHECKED ? 0 : (int)blockIdx.y; rb < (CHECKED ? nblk : (int)blockIdx.y + 1); ++rb) {
+  RowsDev rows = rows_in;
   int i;
-  if (!rows_resolve(rows, blockIdx.y, i)) return;
+  if (!rows_resolve(rows, rb, i)) continue;
   bool upper;
   int img;
   const int q = row_query(rows, i, upper, img);
   int bw, bh, nbw, nbh;
   frame_base(fi, q, bw, bh);
   frame_base(fo, q, nbw, nbh);
-  // Two instantiations per launch: the band one (no call in its loop, so a
-  // lean register budget) returns when the operands are not proven in band,
-  // the CHECKED one only works in that (rare) case.
-  const bool band = FAST || products_in_band(in.stat, L.wmin, L.wmax);
-  if (band == CHECKED) return;
   const int* pref = fl.pref + (long long)img * fl.fst;
   const unsigned short* fpos = fl.fpos + (long long)img * fl.sst;
   const unsigned short* fch = fl.fch + (long long)img * fl.sst;
@@ -3004,7 +3009,8 @@ __global__ void __launch_bounds__(256, MINB)
   double* part = fl.part ? fl.part + ((size_t)i * gridDim.x + blockIdx.x) * 3 : nullptr;
   if (t0 >= total) {
     if (part && threadIdx.x < 3) part[threadIdx.x] = 0.0;
-    return;
+    __syncthreads();  // s_seg is rewritten by the next row
+    continue;
   }
   const int t1 = min(total, t0 + fl.opb);
   const long long ocells = out.cells;
@@ -3106,6 +3112,8 @@ __global__ void __launch_bounds__(256, MINB)
       for (int w = 0; w < 8; ++w) v += s_pr[threadIdx.x][w];
       part[threadIdx.x] = v;
     }
+  }
+  __syncthreads();  // s_seg / s_pr are rewritten by the next row
   }
 }
 
@@ -3292,7 +3300,7 @@ void launch_gbc_flat(cudaStream_t s, const LayerDev& L, const RowsDev& rows, con
     else if (minb >= 4) k_gbc_flat<4><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
     else if (minb == 3) k_gbc_flat<3><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
     else k_gbc_flat<2><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
-    k_gbc_flat<2, false, 4, true><<<grid, 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
+    k_gbc_flat<2, false, 4, true><<<dim3(grid.x, 1), 256, 0, s>>>(L, rows, fin, fout, sp, in, out, fl, ctr);
     ++g_launches;
   }
   ++g_launches;

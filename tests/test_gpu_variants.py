@@ -22,7 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
                                  {"PC_DENSE_TM": "-1"}, {"PC_LIVE_CELLS": "0"}, {"PC_GBC_TILE": "1"},
                                  {"PC_SPLIT_CHAINS": "0"}, {"PC_CHAIN_SCAN": "1"}, {"PC_GBC_FLAT": "0"},
                                  {"PC_RELU_LIST": "0"}, {"PC_PREDICT": "0"}, {"PC_NUMERIC_MODE": "0", "PC_PIPES": "1"},
-                                     {"PC_PREDICT": "2"}, {"PC_PRED_DEVICE": "0"}, {"PC_PRED_FUSED": "0"}, {"PC_FWD_STAGED": "0"}, {"PC_MARGIN_PIPE_MIN": "1000000"}, {"PC_PIPES": "3"}],
+                                     {"PC_PREDICT": "2"}, {"PC_PRED_DEVICE": "0"}, {"PC_PRED_FUSED": "0"}, {"PC_FWD_STAGED": "0"}, {"PC_MARGIN_PIPE_MIN": "1000000"}, {"PC_PIPES": "3"}, {"PC_FORCE_CHECKED": "1"}],
                          ids=["host_schedule", "graph_schedule", "big_chains", "gbc_tiled", "gbc_legacy",
                               "gbc_smem", "gbc_smem_everywhere", "lazy_compaction", "eager_compaction",
                               "lagged_compaction", "one_pipeline", "dense_all_columns_v1", "dense_ballot_v2", "dense_tm8",
@@ -30,7 +30,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
                               "chains_cta_scan", "conv_live_warp", "relu_chain_scan", "exact_compaction",
                               "one_pipeline_predicted", "predicted_from_exact_constants",
                                   "predicted_compaction_on_host", "predicted_offer_unfused",
-                                  "forward_conv_unstaged", "margin_one_pipeline", "three_pipelines"])
+                                  "forward_conv_unstaged", "margin_one_pipeline", "three_pipelines", "checked_products_everywhere"])
 def test_parity_corpus_under_variant(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(HERE, "test_gpu_parity.py"), "-x", "-q",
