@@ -40,7 +40,7 @@ int env_int(const char* name, int dflt) {
 long long big_chain_cells() {
   static const long long v = [] {
     const char* e = getenv("PC_BIG_CHAIN_CELLS");
-    return e && *e ? atoll(e) : 256ll;
+    return e && *e ? atoll(e) : 2048ll;
   }();
   return v;
 }
